@@ -1,0 +1,345 @@
+"""CPU oracle for the cutting-plane order-statistic path — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package.  The product path (paper_1104_2732_b200, libcpsel.so)
+never imports, links or executes anything here, and this package imports nothing
+from the product path.  It shares no code with the CUDA kernels; the only common
+dependency is the seeded input generator in datagen/ (which holds no method
+arithmetic).
+
+Plain, slow, obviously correct: numpy for whole-array steps (a library sort /
+partition is used only as the "sort" step the paper itself names), Python
+integers for counts, np.longdouble (80-bit on x86) for sums, fractions.Fraction
+for exact subgradients.  Every function cites the PAPER.md line it follows
+(P:Lnnn = /root/reference/PAPER.md line nnn).  Readings where the paper is silent
+or inconsistent are numbered R1..R20 and listed in DESIGN.md §3.
+
+Pins (tests/test_oracle_pins.py) tie every function to something other than
+itself: brute-force rank definition on tiny inputs, exact-rational finite
+differences, the paper's closed forms, SPEC worked examples under
+tests/golden/, the Appendix-A identity in exact rationals, and the paper's
+algorithmic claims.
+parity unpinned: none of the functions below (the iteration-count claims are
+only bounds, see DESIGN.md §3 "pins").
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+import numpy as np
+
+LD = np.longdouble
+
+
+# ============================================================================ helpers
+def _as_array(x) -> np.ndarray:
+    x = np.asarray(x)
+    if x.dtype not in (np.float32, np.float64):
+        x = x.astype(np.float64)
+    return x
+
+
+def _f64(v):
+    """Comparison value as a *strong* float64 scalar: numpy then promotes a float32 array to
+    float64 before comparing (a bare Python float would be rounded to float32 under NEP 50)."""
+    return np.float64(v)
+
+
+def canonical(v):
+    """-0.0 -> +0.0 (reading R13: ±0 compare equal; the returned bits are canonical)."""
+    return v + type(v)(0) if v == 0 else v
+
+
+def check_input(x, k: int) -> int:
+    """Validation of the selection problem (SPEC S:L61-62 rank range, S:L85 NaN rejected).
+
+    Returns n.  Raises ValueError on n==0, k out of [1,n] or a non-finite element (R12).
+    """
+    x = _as_array(x)
+    n = x.size
+    if n == 0:
+        raise ValueError("empty sample")
+    if not (1 <= k <= n):
+        raise ValueError(f"rank k={k} out of [1,{n}]")
+    if not np.all(np.isfinite(x)):
+        raise ValueError("non-finite element")
+    return n
+
+
+def median_rank(n: int) -> int:
+    """Med(x) = x_([(n+1)/2]), [t] the integer part — the lower median (R3)."""
+    return (n + 1) // 2
+
+
+# ============================================================================ plain definition
+def order_statistic(x, k: int):
+    """x_(k): the k-th smallest element (P:L19 abstract).
+
+    Plain definition: sort (here: numpy's partition, a library selection primitive)
+    and take position k-1.  Returned in the input dtype, canonical zero (R13).
+    """
+    x = _as_array(x)
+    check_input(x, k)
+    return canonical(np.partition(x, k - 1)[k - 1])
+
+
+def order_statistic_sorted(x, k: int):
+    """Second, independent path: full sort then index (P:L37 'sort the elements ... and select')."""
+    x = _as_array(x)
+    check_input(x, k)
+    return canonical(np.sort(x, kind="stable")[k - 1])
+
+
+def median(x):
+    """Med(x)."""
+    x = _as_array(x)
+    return order_statistic(x, median_rank(x.size))
+
+
+def rank_counts(x, v):
+    """(#{x_i < v}, #{x_i = v}) with IEEE comparisons (P:L130 'count' terms)."""
+    x = _as_array(x)
+    v = _f64(v)
+    return int(np.count_nonzero(x < v)), int(np.count_nonzero(x == v))
+
+
+# ============================================================================ objectives (Eq. 1, Eq. 2)
+def f_median(x, y) -> LD:
+    """Eq. (1) objective f(y) = sum_i |x_i - y|, long-double sum."""
+    xl = _as_array(x).astype(LD)
+    return LD(np.sum(np.abs(xl - LD(y))))
+
+
+def u_paper(t, n: int, kp: int):
+    """Eq. (2) penalty exactly as printed:
+    u(t) = (n-kp+1/2) t for t >= 0, -(kp-1/2) t for t < 0.
+    """
+    t = np.asarray(t, dtype=LD)
+    return np.where(t >= 0, (LD(n) - LD(kp) + LD(0.5)) * t, -(LD(kp) - LD(0.5)) * t)
+
+
+def paper_k(n: int, k: int) -> int:
+    """Eq. (2)'s k selects the k-th LARGEST element (reading R2);
+    the API's k-th smallest is Eq. (2) with paper-k = n-k+1."""
+    return n - k + 1
+
+
+def f_os(x, y, k: int) -> LD:
+    """F_k(y) = sum_i u(x_i - y) (Eq. 2) for the k-th smallest (R2)."""
+    x = _as_array(x)
+    n = x.size
+    t = x.astype(LD) - LD(y)
+    return LD(np.sum(u_paper(t, n, paper_k(n, k))))
+
+
+# ============================================================================ subdifferentials
+def g_paper(x, y):
+    """The set-valued g of P:L130 *as printed*:
+    g(y) = count(x_i>y) + count(x_i<y)(-1) + count(x_i=y)[-1,1]   (Minkowski sum).
+    Returned as the exact interval (lo, hi).  Reading R1: this is -df; see subdiff_median.
+    """
+    x = _as_array(x)
+    c_lt, c_eq = rank_counts(x, y)
+    c_gt = x.size - c_lt - c_eq
+    return (c_gt - c_lt - c_eq, c_gt - c_lt + c_eq)
+
+
+def subdiff_median(x, y):
+    """Clarke subdifferential of Eq. (1) (with d|t| of P:L122-127):
+    each |x_i - y| contributes -1 (x_i>y), +1 (x_i<y), [-1,1] (x_i=y); Minkowski sum.
+    Exact integer interval (lo, hi)."""
+    x = _as_array(x)
+    c_lt, c_eq = rank_counts(x, y)
+    c_gt = x.size - c_lt - c_eq
+    return (c_lt - c_gt - c_eq, c_lt - c_gt + c_eq)
+
+
+def subdiff_os(x, y, k: int):
+    """Subdifferential of F_k(y) = sum_i u(x_i - y) (Eq. 2), term by term as in P:L128-132:
+    d/dy u(x_i - y) = -u'(x_i - y); u' = (n-kp+1/2) on t>0, -(kp-1/2) on t<0,
+    [-(kp-1/2), n-kp+1/2] at t=0.  Exact Fractions (lo, hi)."""
+    x = _as_array(x)
+    n = x.size
+    kp = paper_k(n, k)
+    wpos = Fraction(2 * (n - kp) + 1, 2)   # slope of u for t >= 0
+    wneg = Fraction(2 * kp - 1, 2)         # -slope of u for t < 0
+    c_lt, c_eq = rank_counts(x, y)
+    c_gt = n - c_lt - c_eq
+    # x_i > y : t>0, d/dy = -wpos ; x_i < y : t<0, d/dy = +wneg ; x_i = y : [-wpos, +wneg]
+    lo = c_lt * wneg - c_gt * wpos - c_eq * wpos
+    hi = c_lt * wneg - c_gt * wpos + c_eq * wneg
+    return lo, hi
+
+
+# ============================================================================ reductions used by Algorithm 1
+def init_record(x):
+    """The single init reduction of P:L155/P:L194: y_L = x_(1), y_R = x_(n), sum x_i
+    (+ the multiplicities of min and max, reading R5)."""
+    x = _as_array(x)
+    mn, mx = x.min(), x.max()
+    return {
+        "min": canonical(mn), "cnt_min": int(np.count_nonzero(x == mn)),
+        "max": canonical(mx), "cnt_max": int(np.count_nonzero(x == mx)),
+        "sum": LD(np.sum(x.astype(LD))),
+    }
+
+
+def pass_stats(x, t, y_lo, y_hi):
+    """Everything one objective pass at t can report (Fig. 1):
+      c_lt = #{x<t}, c_eq = #{x=t}                           (subgradient counts)
+      P = sum (x-t)^+, N = sum (t-x)^+                         (F's two halves, direct)
+      L_lo = sum_{y_lo<x<t} (t-x), L_hi = sum_{t<x<y_hi} (x-t) (bracket-local sums)
+      pred = max{x : y_lo<x<t} (-inf if none), succ = min{x : t<x<y_hi} (+inf if none)
+      (P:L192 footnote 'largest x_i <= y~', restricted to the bracket)
+    Sums in long double."""
+    x = _as_array(x)
+    xl = x.astype(LD)
+    t_ = LD(t)
+    t, y_lo, y_hi = _f64(t), _f64(y_lo), _f64(y_hi)
+    lt, gt, eq = x < t, x > t, x == t
+    lo_in = lt & (x > y_lo)
+    hi_in = gt & (x < y_hi)
+    return {
+        "c_lt": int(np.count_nonzero(lt)), "c_eq": int(np.count_nonzero(eq)),
+        "P": LD(np.sum(xl[gt] - t_)), "N": LD(np.sum(t_ - xl[lt])),
+        "L_lo": LD(np.sum(t_ - xl[lo_in])), "L_hi": LD(np.sum(xl[hi_in] - t_)),
+        "c_lo": int(np.count_nonzero(lo_in)), "c_hi": int(np.count_nonzero(hi_in)),
+        "pred": float(x[lo_in].max()) if lo_in.any() else -math.inf,
+        "succ": float(x[hi_in].min()) if hi_in.any() else math.inf,
+    }
+
+
+def F_from_PN(n: int, k: int, P, N) -> LD:
+    """F_k = (k-1/2) P + (n-k+1/2) N (Eq. 2 with paper-k = n-k+1, R2)."""
+    return (LD(k) - LD(0.5)) * LD(P) + (LD(n) - LD(k) + LD(0.5)) * LD(N)
+
+
+# ============================================================================ Algorithm 1 (literal)
+def hybrid_finish(x, k: int, y_L, y_R):
+    """Second stage of the hybrid method (Fig. 1 SortZ P:L284-294):
+    z = {x_i : y_L < x_i < y_R} (copy_if), sort z, return z_(k-m) with
+    m = #{x_i <= y_L} (reading R3: 1-based rank k-m, i.e. 0-based index k-m-1)."""
+    x = _as_array(x)
+    y_L, y_R = _f64(y_L), _f64(y_R)
+    m = int(np.count_nonzero(x <= y_L))
+    z = np.sort(x[(x > y_L) & (x < y_R)])
+    if not (1 <= k - m <= z.size):
+        raise AssertionError("bracket does not contain the k-th order statistic")
+    return canonical(z[k - m - 1]), int(z.size)
+
+
+def cutting_plane(x, k: int, maxit: int = 64, z_cap: int = 0, tol_f: float | None = None):
+    """Kelley's cutting plane method, Algorithm 1, for F_k (Eq. 2), followed by
+    the hybrid finish.  Straightforward double precision:
+
+    step 0: one reduction -> y_L=x_(1), y_R=x_(n), sum x; then the closed
+        forms F(y_L) = (k-1/2)(sum x - n y_L), F(y_R) = (n-k+1/2)(n y_R - sum x)
+        (Eq. 1's f(y_L)=sum x - n y_L, f(y_R)=n y_R - sum x, weighted per Eq. 2) and
+        g_L = right end of dF(y_L), g_R = left end of dF(y_R) (R4 tightest cuts, R5 multiplicity).
+        If k <= cnt_min -> x_(1); if k > n-cnt_max -> x_(n).
+    step 1.1: t = (fR - fL + y_L gL - y_R gR)/(gL - gR) in double; if rounding puts t
+        outside ]y_L, y_R[ the midpoint is used and counted as a fallback.
+    step 1.2: ft = F(t) by a direct long-double reduction, gt = dF(t) (exact interval).
+    step 1.3: stop if 0 in dF(t) (t is then x_(k)); or if the bracket interior
+        #{y_L<x<y_R} <= z_cap (R7/R8: the count replaces tolerance_f); or, when tol_f is
+        given, the paper's own y_R - y_L <= tolerance_f.
+    step 1.4 (sign fixed per R1): dF(t) < 0 -> y_L <- t (gL = right end),
+        else y_R <- t (gR = left end).
+    step 2 / hybrid: the exact finish by copy_if + sort.
+
+    Returns dict(value, iterations, reductions, fallbacks, trace, y_L, y_R, z_count, exit).
+    trace rows: (t, F(t), c_lt, c_eq, interior count after the update).
+    """
+    x = _as_array(x)
+    n = check_input(x, k)
+    rec = init_record(x)
+    reductions = 1
+    yL, yR = float(rec["min"]), float(rec["max"])
+    base = {"iterations": 0, "reductions": reductions, "fallbacks": 0, "trace": [],
+            "y_L": yL, "y_R": yR, "z_count": 0}
+    if k <= rec["cnt_min"]:
+        return dict(base, value=rec["min"], exit="init_min")
+    if k > n - rec["cnt_max"]:
+        return dict(base, value=rec["max"], exit="init_max")
+    S = rec["sum"]
+    fL = float((LD(k) - LD(0.5)) * (S - LD(n) * LD(yL)))
+    fR = float((LD(n) - LD(k) + LD(0.5)) * (LD(n) * LD(yR) - S))
+    gL = float(Fraction(n * (2 * rec["cnt_min"] - 2 * k + 1), 2))            # dF+(y_L)
+    gR = float(Fraction(n * (2 * (n - rec["cnt_max"]) - 2 * k + 1), 2))      # dF-(y_R)
+    c_le_L = rec["cnt_min"]            # #{x <= y_L}
+    c_lt_R = n - rec["cnt_max"]        # #{x <  y_R}
+    trace, fallbacks, exit_reason, value = [], 0, "maxit", None
+    it = 0
+    for it in range(1, maxit + 1):
+        t = (fR - fL + yL * gL - yR * gR) / (gL - gR)                       # step 1.1
+        if not (yL < t < yR):
+            t = 0.5 * (yL + yR)
+            fallbacks += 1
+        ft = float(f_os(x, t, k))                                             # step 1.2
+        lo, hi = subdiff_os(x, t, k)
+        reductions += 1
+        c_lt, c_eq = rank_counts(x, t)
+        if lo <= 0 <= hi:                                                     # step 1.3
+            trace.append((t, ft, c_lt, c_eq, 0))
+            value, exit_reason = canonical(x.dtype.type(t)), "hit"
+            break
+        if hi < 0:                                                            # step 1.4
+            yL, fL, gL, c_le_L = t, ft, float(hi), c_lt + c_eq
+        else:
+            yR, fR, gR, c_lt_R = t, ft, float(lo), c_lt
+        interior = c_lt_R - c_le_L
+        trace.append((t, ft, c_lt, c_eq, interior))
+        if interior <= z_cap:
+            exit_reason = "z_cap"
+            break
+        if tol_f is not None and yR - yL <= tol_f:
+            exit_reason = "tol_f"
+            break
+    z_count = 0
+    if value is None:                                                         # step 2 + hybrid
+        value, z_count = hybrid_finish(x, k, yL, yR)
+    return {"value": value, "iterations": it, "reductions": reductions, "fallbacks": fallbacks,
+            "trace": trace, "y_L": yL, "y_R": yR, "z_count": z_count, "exit": exit_reason}
+
+
+def eval_at(x, k: int, t, y_lo, y_hi):
+    """Replay hook: one pass at t (pass_stats) plus F_k(t) and dF_k(t) — compared against the
+    GPU's cpsel_eval / trace at identical t."""
+    s = pass_stats(x, t, y_lo, y_hi)
+    n = _as_array(x).size
+    s["F"] = F_from_PN(n, k, s["P"], s["N"])
+    s["subdiff"] = subdiff_os(x, t, k)
+    return s
+
+
+# ============================================================================ robust regression (§6)
+def lms_residuals_sq(X, y, thetas):
+    """r_i(theta) = f_theta(x_i) - y_i (model P:L440) and r_i^2, in float64.
+    X: n x p, y: n, thetas: C x p (theta_j as rows).  Returns S (n x C) float64."""
+    X64 = np.asarray(X, dtype=np.float64)
+    y64 = np.asarray(y, dtype=np.float64)
+    T64 = np.asarray(thetas, dtype=np.float64)
+    R = X64 @ T64.T - y64[:, None]
+    return R * R
+
+
+def lms_objective(X, y, thetas):
+    """LMS objective F(theta_j) = Med(r_i(theta_j)^2) per candidate (reading R19: median of
+    the squared residuals, lower median P:L32).  float64 result per column."""
+    S = lms_residuals_sq(X, y, thetas)
+    n = S.shape[0]
+    k = median_rank(n)
+    return np.array([np.partition(S[:, j], k - 1)[k - 1] for j in range(S.shape[1])])
+
+
+def lts_objective(rsq, h: int):
+    """LTS objective via the rho reformulation, reading R20:
+    m = (r^2)_(h); b_L = #{r^2 < m}; b = #{r^2 = m}; a = h - b_L;
+    F = sum_{r^2<m} r^2 + (a/b) sum_{r^2=m} r^2   (= sum of the h smallest squares)."""
+    r = np.asarray(rsq, dtype=np.float64)
+    m = np.partition(r, h - 1)[h - 1]
+    bL = int(np.count_nonzero(r < m))
+    b = int(np.count_nonzero(r == m))
+    a = h - bL
+    return float(np.sum(r[r < m].astype(LD)) + LD(a) / LD(b) * np.sum(r[r == m].astype(LD)))
