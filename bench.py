@@ -1,0 +1,303 @@
+#!/usr/bin/env python
+"""Benchmark: exact median (k-th order statistic) of n = 2^30 float32 per GPU by the cutting-plane
+path (BASELINE.json metric: "elements/s and HBM-roofline fraction for k-th select at n=2^30,
+1/2/4/8 B200").
+
+One step = one median selection over each of the four resident synthetic arrays (uniform, normal,
+Cauchy, many-duplicate; BASELINE.json configs[1] distributions at the metric size), i.e.
+4 x 2^30 elements per GPU per step.  At N>1 each rank holds its own 2^30-element shard of every
+array and the step is one sharded selection over N x 2^30 elements (weak scaling; one NCCL
+all-gather of the 96-byte pass tuple per iteration, an all-gather-v of the bracket at the end).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream bracketed by a barrier
+and torch.cuda.synchronize(), max over ranks; inputs (4 GiB each) are larger than L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "elements/s and HBM-roofline fraction for k-th select at n=2^30, 1/2/4/8 B200"
+UNIT = "elements/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cpsel", choices=["cpsel", "reference"])
+    ap.add_argument("--log2n", type=int, default=30)
+    ap.add_argument("--dists", default="uniform,normal,cauchy,dup256")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--z-cap", type=int, default=0)
+    return ap.parse_args()
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+        time.sleep(0.25)
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                parts = [s.strip() for s in line.split(",")]
+                if len(parts) >= 8:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(a, rank: int, world: int):
+    """--impl reference: the oracle (sort-based selection, numpy partition) timed as it stands on the
+    host cores, each step a bounded sample (2^24 elements of each distribution) of the workload."""
+    if rank != 0:
+        return
+    import numpy as np
+
+    import datagen
+    import oracle
+    dists = a.dists.split(",")
+    m = 1 << 24
+    xs = [datagen.make(d, m, "f32") for d in dists]
+    k = oracle.median_rank(m)
+    for _ in range(a.warmup):
+        for x in xs:
+            oracle.order_statistic(x, k)
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        for x in xs:
+            oracle.order_statistic(x, k)
+    dt = time.perf_counter() - t0
+    value = a.steps * len(xs) * m / dt
+    sample = f"oracle.order_statistic (np.partition, 1 thread) median of 2^24-element samples of {dists} per step"
+    n = 1 << a.log2n
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": 1e3 * dt / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"median of n=2^{a.log2n} float32 x {dists}", "n": n, "k": "median (n+1)//2"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------------------ our arm
+def main():
+    a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        return run_reference(a, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import datagen
+    import paper_1104_2732_b200 as cp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cp.load()
+    dists = a.dists.split(",")
+    n = 1 << a.log2n
+    xs = [datagen.make(d, n, "f32", seed=datagen.SEED + 7919 * rank, device=dev) for d in dists]
+    torch.cuda.synchronize()
+    n_global = n * world
+    k = (n_global + 1) // 2
+    cp.set_config(local, z_cap=a.z_cap)
+    if world > 1:
+        obj = [cp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        cp.comm_init(obj[0], rank, world, local)
+
+    def select(x):
+        if world > 1:
+            return cp.select_kth_sharded(x, k, return_info=True)
+        return cp.select_kth(x, k, return_info=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    for _ in range(a.warmup):
+        for x in xs:
+            select(x)
+    cp.set_config(local, z_cap=a.z_cap, record_timing=1)
+    stream = torch.cuda.current_stream(dev)
+    clocks = Clocks(local)
+    infos = []
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        for x in xs:
+            infos.append(select(x)[1])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1) / a.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = len(xs) * n_global / (ms / 1e3)
+
+    # dominant kernel: the cutting-plane pass (algorithmic bytes = one read of the shard)
+    pass_ms = [i["kernel_ms_passes"] / max(i["cp_iters"], 1) for i in infos if i["cp_iters"]]
+    init_ms = [i["kernel_ms_init"] for i in infos]
+    sel_ms = [i["kernel_ms_select"] for i in infos]
+    iters = [i["cp_iters"] for i in infos]
+    bytes_per_pass = n * 4
+    avg_pass_ms = statistics.fmean(pass_ms) if pass_ms else float("nan")
+    peak, peak_src = peaks()
+    achieved = bytes_per_pass / (avg_pass_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_pass_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    step_kernel_ms = sum(i["kernel_ms_init"] + i["kernel_ms_passes"] + i["kernel_ms_select"] for i in infos) / a.steps
+    launches = sum(i["launches"] for i in infos)
+    cp.set_config(local, z_cap=a.z_cap, record_timing=0)
+
+    # end to end through the C ABI with HOST buffers (H2D inside the timed region)
+    e2e = None
+    if not a.no_e2e and a.e2e_steps > 0:
+        pinned = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        tot_s, tot_el, d2h = 0.0, 0, 0
+        for s in range(a.e2e_steps):
+            for x in xs:
+                pinned.copy_(x)                         # untimed: stage this step's input on the host
+                torch.cuda.synchronize()
+                barrier()
+                t0 = time.perf_counter()
+                if world > 1:
+                    xd = pinned.to(dev, non_blocking=True)
+                    _, info = cp.select_kth_sharded(xd, k, return_info=True)
+                    torch.cuda.synchronize()
+                else:
+                    _, info = cp.select_kth_host(pinned, k, device=local, return_info=True)
+                dt = time.perf_counter() - t0
+                if world > 1:
+                    tt = torch.tensor([dt], device=dev)
+                    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                    dt = float(tt.item())
+                tot_s += dt
+                tot_el += n_global
+                d2h += 4 + 96 * info["passes"]
+        del pinned
+        e2e = {"value": tot_el / tot_s, "unit": UNIT, "h2d_bytes_per_step": len(xs) * n * 4,
+               "d2h_bytes_per_step": d2h // a.e2e_steps,
+               "note": "select_kth_host: pinned host array -> device staging copy inside the timed call"}
+
+    # CPU baseline: the oracle as it stands, on a bounded host sample (rank 0, N=1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        import oracle
+        m = 1 << 24
+        samples = [x[:m].cpu().numpy() for x in xs]
+        km = oracle.median_rank(m)
+        done, t0 = 0, time.perf_counter()
+        while time.perf_counter() - t0 < a.cpu_seconds:
+            for smp in samples:
+                oracle.order_statistic(smp, km)
+                done += m
+        dt = time.perf_counter() - t0
+        cpu = {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle.order_statistic (np.partition, single thread) median of the first 2^24 "
+                         f"elements of each of {dists}, repeated for {a.cpu_seconds:.0f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"median of n=2^{a.log2n} float32 per GPU x {dists} (4 selections per step)",
+                       "n_per_gpu": n, "n_global": n_global, "k": "lower median (n+1)//2",
+                       "parallelism": "single GPU" if world == 1 else f"sharded x{world} (NCCL tuple all-gather)",
+                       "l2": "inputs larger than L2 (4 GiB per array vs 126 MB L2); no flush needed",
+                       "z_cap": a.z_cap or "auto"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "pass_kernel<float,hot> (a2)", "bytes_per_launch": bytes_per_pass,
+                         "avg_launch_ms": avg_pass_ms, "peak_source": peak_src},
+            "cp_iters": {"mean": statistics.fmean(iters), "min": min(iters), "max": max(iters)},
+            "kernel_ms_per_step": {"init": sum(init_ms) / a.steps, "passes": sum(i["kernel_ms_passes"] for i in infos) / a.steps,
+                                   "select": sum(sel_ms) / a.steps, "all": step_kernel_ms},
+            "gpu_launches": launches,
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

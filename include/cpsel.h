@@ -1,0 +1,201 @@
+/*
+ * cpsel.h — C ABI of libcpsel.so: exact k-th order statistics (median) of large device
+ * arrays by Kelley's cutting-plane method (Beliakov, arXiv:1104.2732), B200 / sm_100a.
+ *
+ * Citations: P:Lnnn = line nnn of the paper's text (/root/reference/PAPER.md, not shipped);
+ * "R<n>" = numbered reading of the paper in DESIGN.md §3.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns cpsel_status; nothing aborts or throws.  On error the ctx keeps a
+ *    message readable with cpsel_last_error().  Validation happens before any launch.
+ *  - Ranks k are 1-based and select the k-th SMALLEST element (R2 maps Eq. 2).
+ *  - The median is the lower median k = floor((n+1)/2) (R3).
+ *  - d_* pointers are device pointers on the ctx's device, h_* pointers are host pointers.
+ *    Input arrays are read-only for the duration of the call (the caller owns them and must
+ *    not modify them concurrently).  The ctx owns all scratch; it grows lazily, is cached
+ *    across calls and is freed by cpsel_destroy.  No allocation happens inside the
+ *    iteration loop.
+ *  - Work is enqueued on the ctx stream.  Calls are host-blocking (the cutting-plane driver
+ *    needs each pass's tuple on the host, P:L426 'partial sums ... added on the CPU').
+ *  - A ctx is not thread-safe; distinct ctxs may be used from distinct threads.
+ *  - Non-finite inputs (NaN, +-Inf) are rejected with CPSEL_ENONFINITE (R12).
+ *  - Returned values are elements of the input, bit-exact, with -0.0 canonicalised to +0.0 (R13).
+ */
+#ifndef CPSEL_H
+#define CPSEL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CPSEL_OK = 0,
+  CPSEL_EINVAL = 1,     /* null pointer, n == 0, bad dtype, misaligned element pointer, bad config */
+  CPSEL_ERANK = 2,      /* k < 1 or k > n */
+  CPSEL_ENONFINITE = 3, /* the input holds NaN or +-Inf */
+  CPSEL_ECUDA = 4,      /* a CUDA runtime error (message in cpsel_last_error) */
+  CPSEL_ENCCL = 5,      /* an NCCL error, or NCCL not loadable / comm not initialised */
+  CPSEL_ENOMEM = 6,     /* device or pinned allocation failed */
+  CPSEL_EINTERNAL = 7   /* a safeguard tripped (iteration cap); never expected */
+} cpsel_status;
+
+typedef enum { CPSEL_F32 = 0, CPSEL_F64 = 1 } cpsel_dtype;
+
+typedef struct cpsel_ctx cpsel_ctx;
+
+/* Tunables.  cpsel_config_default() fills the defaults noted here. */
+typedef struct {
+  uint64_t z_cap;            /* compaction threshold on the bracket interior count m:
+                                the pass whose current interior m <= z_cap also copies the
+                                interior into z (P:L196 copy_if, R8).  0 = auto. */
+  uint64_t direct_threshold; /* n <= this: skip the cutting plane, select on x directly
+                                (P:L311 'radix sort ... most efficient up to 2^21').  Default 2^17 */
+  uint32_t max_iters;        /* safety cap on cutting-plane passes (P:L169 maxit).  Default 200 */
+  int32_t force_cp;          /* 1: always run cutting-plane passes (parity runs), ignore direct_threshold */
+  int32_t record_trace;      /* 1: keep the per-iteration trace (cpsel_get_trace).  Default 1 */
+  int32_t record_timing;     /* 1: time every kernel with CUDA events on the ctx stream (info / trace
+                                kernel_ms fields).  Default 0 */
+} cpsel_config;
+
+/* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
+typedef struct {
+  uint32_t passes;         /* full passes over x (init + cutting-plane), P:L194 'maxit+1 reductions' */
+  uint32_t cp_iters;       /* cutting-plane iterations (Algorithm 1 step 1) */
+  uint32_t fallback_steps; /* safeguard steps (ordered-key bisection), R7 */
+  uint32_t exit_reason;    /* 0 init_min, 1 init_max, 2 hit, 3 pred, 4 succ, 5 compact+select, 6 direct select */
+  uint64_t z_count;        /* elements in the final selection set (0 if none) */
+  uint64_t bytes_moved;    /* algorithmic HBM bytes of all passes (reads of x + writes/reads of z) */
+  double ms_total;         /* host wall time of the call */
+  uint32_t launches;       /* kernels this call launched */
+  uint32_t reserved;
+  double kernel_ms_init;   /* record_timing: CUDA-event time of the init kernel */
+  double kernel_ms_passes; /* record_timing: sum over the cutting-plane pass kernels */
+  double kernel_ms_select; /* record_timing: the small-set selection kernels */
+} cpsel_info;
+
+/* One objective pass at t (Fig. 1 'Objective'), see cpsel_eval. */
+typedef struct {
+  uint64_t c_lt, c_eq;   /* #{x < t}, #{x == t}: dF(t) = [n(c_lt-k+1/2), n(c_lt+c_eq-k+1/2)] */
+  uint64_t c_lo, c_hi;   /* #{y_lo < x < t}, #{t < x < y_hi} */
+  double L_lo, L_hi;     /* sum_{y_lo<x<t} (t-x),  sum_{t<x<y_hi} (x-t)   (fp64 accumulation) */
+  double P, N;           /* sum (x-t)^+, sum (t-x)^+ over all x (direct, as Fig. 1 does) */
+  double pred, succ;     /* max{x: y_lo<x<t} (-inf if none), min{x: t<x<y_hi} (+inf if none) */
+} cpsel_pass_stats;
+
+/* The init reduction (x_(1), x_(n) and sum x in ONE pass; R5 multiplicities). */
+typedef struct {
+  double vmin, vmax;      /* exact */
+  uint64_t cnt_min, cnt_max, nonfinite;
+  double x0;              /* the shift x[0] */
+  double S;               /* sum_i (x_i - x0), fp64 */
+} cpsel_init_stats;
+
+/* One row per cutting-plane pass (R7 trace). */
+typedef struct {
+  double t;               /* query point (an element of the dtype) */
+  double F;               /* F_k(t) = (k-1/2) P(t) + (n-k+1/2) N(t)  (Eq. 2, R2) via App. A identities */
+  uint64_t c_lt, c_eq;    /* exact counts at t */
+  uint64_t interior;      /* bracket interior count after the update */
+  uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard */
+  uint32_t compacted;     /* 1 if this pass also wrote z */
+  double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
+} cpsel_trace_row;
+
+/* ---- context ------------------------------------------------------------------------- */
+/* device: CUDA ordinal; cuda_stream: a cudaStream_t on that device, or NULL for a private
+ * non-blocking stream.  *out receives the new ctx. */
+cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out);
+void cpsel_destroy(cpsel_ctx* ctx);
+const char* cpsel_last_error(const cpsel_ctx* ctx);
+const char* cpsel_status_string(cpsel_status s);
+void cpsel_config_default(cpsel_config* cfg);
+cpsel_status cpsel_set_config(cpsel_ctx* ctx, const cpsel_config* cfg);
+cpsel_status cpsel_get_config(const cpsel_ctx* ctx, cpsel_config* cfg);
+/* Re-target the ctx stream (e.g. torch's current stream) without recreating scratch. */
+cpsel_status cpsel_set_stream(cpsel_ctx* ctx, void* cuda_stream);
+
+/* ---- selection (north_star: select_kth(x, n, k), median(x, n)) -------------------------- */
+/* d_x: device array of n elements of dtype (element-aligned, any 16-byte phase).
+ * k in [1, n].  *h_out receives one element (4 or 8 bytes).  info may be NULL. */
+cpsel_status cpsel_select_kth(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype,
+                              uint64_t k, void* h_out, cpsel_info* info);
+/* k = floor((n+1)/2). */
+cpsel_status cpsel_median(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype,
+                          void* h_out, cpsel_info* info);
+/* Same as cpsel_select_kth for a HOST array h_x (pinned memory recommended): the H2D copy
+ * into ctx-owned device staging is part of the call (end-to-end path). */
+cpsel_status cpsel_select_kth_host(cpsel_ctx* ctx, const void* h_x, uint64_t n, cpsel_dtype dtype,
+                                   uint64_t k, void* h_out, cpsel_info* info);
+
+/* ---- LMS (north_star: lms_objective(X, y, thetas)) -------------------------- */
+/* d_X: float32 n x p row-major; d_y: float32[n]; d_thetas: float32 p x C column-major
+ * (theta_j = d_thetas[j*p .. j*p+p)).  d_out: float32[C] (device) receives, per candidate,
+ * Med_i (x_i . theta_j - y_i)^2 (R19: median of squared residuals, lower median).
+ * p <= 16.  Host-blocking; d_out is complete on return. */
+cpsel_status cpsel_lms_objective(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n,
+                                 uint32_t p, const float* d_thetas, uint32_t C, float* d_out,
+                                 cpsel_info* info);
+/* The residual stage alone: d_S (float32, n x C column-major, column j at d_S + j*n) receives
+ * (x_i . theta_j - y_i)^2 computed on the tensor cores (tcgen05, 3xTF32 split). */
+cpsel_status cpsel_lms_residuals(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n,
+                                 uint32_t p, const float* d_thetas, uint32_t C, float* d_S);
+/* Batched selection: for each column j of d_S (n x C column-major) the k-th smallest
+ * -> d_out[j] (float32, device). */
+cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t n, uint32_t C,
+                                      uint64_t k, float* d_out, cpsel_info* info);
+
+/* ---- parity hooks ------------------------------------------------------------------------ */
+/* One pass at t with bracket (y_lo, y_hi).  t, y_lo, y_hi must be representable in dtype
+ * (else CPSEL_EINVAL).  Computes every field of cpsel_pass_stats in a single read of x. */
+cpsel_status cpsel_eval(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, double t,
+                        double y_lo, double y_hi, cpsel_pass_stats* out);
+/* The init reduction alone (step a1). */
+cpsel_status cpsel_init(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype,
+                        cpsel_init_stats* out);
+/* The small-set exact selection alone (step a5): r-th smallest (1-based) of d_z[0..m). */
+cpsel_status cpsel_small_select(cpsel_ctx* ctx, const void* d_z, uint64_t m, cpsel_dtype dtype,
+                                uint64_t r, void* h_out);
+/* Copy up to max_rows rows of the last call's trace into rows; *n_rows = rows available. */
+cpsel_status cpsel_get_trace(const cpsel_ctx* ctx, cpsel_trace_row* rows, uint32_t max_rows,
+                             uint32_t* n_rows);
+
+/* ---- multi-GPU (one process per GPU) -------------------------------------- */
+/* Writes a fresh 128-byte ncclUniqueId into id_out (call on rank 0, broadcast it yourself,
+ * e.g. torch.distributed.broadcast_object_list).  NCCL is resolved at run time from the
+ * libnccl.so.2 already loaded in the process (torch's), else from the system. */
+cpsel_status cpsel_nccl_unique_id(void* id_out128);
+/* Collective: every rank calls with the same id, its rank and the world size. */
+cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int world);
+/* Collective: x is the concatenation over ranks (in rank order) of the shards d_shard
+ * (n_local elements each, may differ per rank, may be 0).  k is the global rank.  Every
+ * rank receives the same *h_out.  Per iteration one 64-byte-per-rank NCCL all-gather of
+ * the pass tuples; at the end an NCCL all-gather-v of the bracket contents (north_star). */
+cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint64_t n_local,
+                                      cpsel_dtype dtype, uint64_t k, void* h_out, cpsel_info* info);
+
+/* ---- host-only driver (no GPU needed) ------------------------------------------------------ */
+/* The same cutting-plane driver, with the three device steps supplied as callbacks.  Used by
+ * the CPU tests (world-size-2 gloo tests of the sharded combine) to exercise the exact host
+ * logic the GPU path runs.  Each callback returns 0 on success. */
+typedef struct {
+  void* user;
+  /* init reduction over the whole (possibly sharded) array: fill *out. */
+  int (*init)(void* user, cpsel_init_stats* out);
+  /* one pass at t over bracket (y_lo, y_hi); fill c_lt, c_eq, L_lo, L_hi, pred, succ of *out.
+     If compact != 0 the callee must also retain {y_lo < x < t} and {t < x < y_hi}. */
+  int (*pass)(void* user, double t, double y_lo, double y_hi, int compact, cpsel_pass_stats* out);
+  /* exact selection of the r-th smallest (1-based) of the retained half (side 0: (y_lo,t),
+     side 1: (t,y_hi)) of the last compacting pass, or of all of x if side == 2. */
+  int (*select)(void* user, int side, uint64_t r, double* value_out);
+} cpsel_host_backend;
+cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dtype dtype,
+                              uint64_t k, const cpsel_config* cfg, double* value_out,
+                              cpsel_info* info, cpsel_trace_row* trace, uint32_t max_rows,
+                              uint32_t* n_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CPSEL_H */

@@ -1,0 +1,459 @@
+"""Python binding of libcpsel.so — exact k-th order statistics by Kelley's cutting-plane method
+(Beliakov, arXiv:1104.2732) on B200.
+
+Argument marshalling only: every step of the path (init reduction, cutting-plane passes,
+compaction, radix select, LMS residuals, NCCL exchange) runs inside libcpsel.so (C ABI in
+include/cpsel.h).  PyTorch supplies device memory, the current CUDA stream and process groups.
+There is no CPU fallback: if the shared library is missing or CUDA is unavailable the calls
+raise.  Names follow the C ABI: select_kth, median, lms_objective, eval, ...
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+__all__ = [
+    "select_kth", "median", "select_kth_host", "lms_objective", "lms_residuals", "select_kth_batched",
+    "eval", "init_stats", "small_select", "get_trace", "set_config", "get_config", "nccl_unique_id",
+    "comm_init", "select_kth_sharded", "drive_host", "library_path", "load", "CpselError",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libcpsel.so")
+
+F32, F64 = 0, 1
+OK, EINVAL, ERANK, ENONFINITE, ECUDA, ENCCL, ENOMEM, EINTERNAL = range(8)
+EXIT_REASONS = ["init_min", "init_max", "hit", "pred", "succ", "compact_select", "direct_select"]
+
+
+class CpselError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"cpsel status {status}: {msg}")
+        self.status = status
+
+
+class Config(C.Structure):
+    _fields_ = [("z_cap", C.c_uint64), ("direct_threshold", C.c_uint64), ("max_iters", C.c_uint32),
+                ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("passes", C.c_uint32), ("cp_iters", C.c_uint32), ("fallback_steps", C.c_uint32),
+                ("exit_reason", C.c_uint32), ("z_count", C.c_uint64), ("bytes_moved", C.c_uint64),
+                ("ms_total", C.c_double), ("launches", C.c_uint32), ("reserved", C.c_uint32),
+                ("kernel_ms_init", C.c_double), ("kernel_ms_passes", C.c_double), ("kernel_ms_select", C.c_double)]
+
+    def as_dict(self):
+        d = {f: getattr(self, f) for f, _ in self._fields_}
+        d["exit"] = EXIT_REASONS[self.exit_reason] if self.exit_reason < len(EXIT_REASONS) else "?"
+        return d
+
+
+class PassStats(C.Structure):
+    _fields_ = [("c_lt", C.c_uint64), ("c_eq", C.c_uint64), ("c_lo", C.c_uint64), ("c_hi", C.c_uint64),
+                ("L_lo", C.c_double), ("L_hi", C.c_double), ("P", C.c_double), ("N", C.c_double),
+                ("pred", C.c_double), ("succ", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class InitStats(C.Structure):
+    _fields_ = [("vmin", C.c_double), ("vmax", C.c_double), ("cnt_min", C.c_uint64), ("cnt_max", C.c_uint64),
+                ("nonfinite", C.c_uint64), ("x0", C.c_double), ("S", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+class TraceRow(C.Structure):
+    _fields_ = [("t", C.c_double), ("F", C.c_double), ("c_lt", C.c_uint64), ("c_eq", C.c_uint64),
+                ("interior", C.c_uint64), ("kind", C.c_uint32), ("compacted", C.c_uint32),
+                ("kernel_ms", C.c_double)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_INIT_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(InitStats))
+_PASS_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int, C.POINTER(PassStats))
+_SEL_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.POINTER(C.c_double))
+
+
+class HostBackend(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("init", _INIT_CB), ("pass_", _PASS_CB), ("select", _SEL_CB)]
+
+
+# every symbol the header declares (tests check the library exports exactly these)
+SYMBOLS = [
+    "cpsel_create", "cpsel_destroy", "cpsel_last_error", "cpsel_status_string", "cpsel_config_default",
+    "cpsel_set_config", "cpsel_get_config", "cpsel_set_stream", "cpsel_select_kth", "cpsel_median",
+    "cpsel_select_kth_host", "cpsel_lms_objective", "cpsel_lms_residuals", "cpsel_select_kth_batched",
+    "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_nccl_unique_id",
+    "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host",
+]
+
+_lib = None
+_lock = threading.Lock()
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libcpsel.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_1104_2732_b200.build`")
+        lib = C.CDLL(_LIB_PATH)
+        P, U64, U32, I, D = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_double
+        sig = {
+            "cpsel_create": (I, [I, P, C.POINTER(P)]),
+            "cpsel_destroy": (None, [P]),
+            "cpsel_last_error": (C.c_char_p, [P]),
+            "cpsel_status_string": (C.c_char_p, [I]),
+            "cpsel_config_default": (None, [C.POINTER(Config)]),
+            "cpsel_set_config": (I, [P, C.POINTER(Config)]),
+            "cpsel_get_config": (I, [P, C.POINTER(Config)]),
+            "cpsel_set_stream": (I, [P, P]),
+            "cpsel_select_kth": (I, [P, P, U64, I, U64, P, C.POINTER(Info)]),
+            "cpsel_median": (I, [P, P, U64, I, P, C.POINTER(Info)]),
+            "cpsel_select_kth_host": (I, [P, P, U64, I, U64, P, C.POINTER(Info)]),
+            "cpsel_lms_objective": (I, [P, P, P, U64, U32, P, U32, P, C.POINTER(Info)]),
+            "cpsel_lms_residuals": (I, [P, P, P, U64, U32, P, U32, P]),
+            "cpsel_select_kth_batched": (I, [P, P, U64, U32, U64, P, C.POINTER(Info)]),
+            "cpsel_eval": (I, [P, P, U64, I, D, D, D, C.POINTER(PassStats)]),
+            "cpsel_init": (I, [P, P, U64, I, C.POINTER(InitStats)]),
+            "cpsel_small_select": (I, [P, P, U64, I, U64, P]),
+            "cpsel_get_trace": (I, [P, C.POINTER(TraceRow), U32, C.POINTER(U32)]),
+            "cpsel_nccl_unique_id": (I, [P]),
+            "cpsel_comm_init": (I, [P, P, I, I]),
+            "cpsel_select_kth_sharded": (I, [P, P, U64, I, U64, P, C.POINTER(Info)]),
+            "cpsel_drive_host": (I, [C.POINTER(HostBackend), U64, I, U64, C.POINTER(Config), C.POINTER(D),
+                                     C.POINTER(Info), C.POINTER(TraceRow), U32, C.POINTER(U32)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+    return _lib
+
+
+# ------------------------------------------------------------------------------------------ ctx
+class _Ctx:
+    def __init__(self, device: int):
+        lib = load()
+        self.device = device
+        self.handle = C.c_void_p()
+        st = lib.cpsel_create(device, None, C.byref(self.handle))
+        if st != OK:
+            raise CpselError(st, "cpsel_create failed (see stderr)")
+        self._stream = None
+
+    def bind_stream(self, stream_ptr: int):
+        if stream_ptr != self._stream:
+            _check(self, load().cpsel_set_stream(self.handle, C.c_void_p(stream_ptr)))
+            self._stream = stream_ptr
+
+    def __del__(self):
+        try:
+            if self.handle and _lib is not None:
+                _lib.cpsel_destroy(self.handle)
+        except Exception:
+            pass
+
+
+_ctxs: dict[int, _Ctx] = {}
+
+
+def _ctx_for(t) -> _Ctx:
+    import torch
+    if not (hasattr(t, "is_cuda") and t.is_cuda):
+        raise ValueError("expected a CUDA tensor (no CPU fallback)")
+    dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
+    c = _ctxs.get(dev)
+    if c is None:
+        c = _ctxs[dev] = _Ctx(dev)
+    c.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+    return c
+
+
+def _ctx_device(dev: int) -> _Ctx:
+    import torch
+    c = _ctxs.get(dev)
+    if c is None:
+        c = _ctxs[dev] = _Ctx(dev)
+    c.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+    return c
+
+
+def _check(ctx: _Ctx, st: int):
+    if st == OK:
+        return
+    msg = load().cpsel_last_error(ctx.handle).decode(errors="replace")
+    if st in (EINVAL, ERANK, ENONFINITE):
+        raise ValueError(f"cpsel status {st}: {msg}")
+    raise CpselError(st, msg)
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.float32:
+        return F32
+    if t.dtype == torch.float64:
+        return F64
+    raise ValueError(f"unsupported dtype {t.dtype} (float32 / float64)")
+
+
+def _flat(t):
+    if t.dim() != 1:
+        t = t.reshape(-1)
+    if not t.is_contiguous():
+        raise ValueError("tensor must be contiguous")
+    return t
+
+
+def _out_value(buf, dt: int) -> float:
+    return float(C.cast(buf, C.POINTER(C.c_float if dt == F32 else C.c_double))[0])
+
+
+# ------------------------------------------------------------------------------------------ API
+def select_kth(x, k: int, return_info: bool = False):
+    """k-th smallest element (1-based) of the CUDA tensor x (float32/float64)."""
+    x = _flat(x)
+    ctx = _ctx_for(x)
+    dt = _dtype_code(x)
+    out = C.create_string_buffer(8)
+    info = Info()
+    _check(ctx, load().cpsel_select_kth(ctx.handle, C.c_void_p(x.data_ptr()), x.numel(), dt, int(k), out,
+                                       C.byref(info)))
+    v = _out_value(out, dt)
+    return (v, info.as_dict()) if return_info else v
+
+
+def median(x, return_info: bool = False):
+    """Lower median x_((n+1)//2)."""
+    x = _flat(x)
+    return select_kth(x, (x.numel() + 1) // 2, return_info)
+
+
+def select_kth_host(x, k: int, device: int = 0, return_info: bool = False):
+    """k-th smallest of a HOST tensor (pinned recommended); the H2D copy is inside the call."""
+    import torch
+    if x.is_cuda:
+        raise ValueError("select_kth_host expects a CPU tensor")
+    x = _flat(x)
+    ctx = _ctx_device(device)
+    dt = _dtype_code(x)
+    out = C.create_string_buffer(8)
+    info = Info()
+    _check(ctx, load().cpsel_select_kth_host(ctx.handle, C.c_void_p(x.data_ptr()), x.numel(), dt, int(k), out,
+                                            C.byref(info)))
+    v = _out_value(out, dt)
+    return (v, info.as_dict()) if return_info else v
+
+
+def eval(x, t: float, y_lo: float, y_hi: float) -> dict:  # noqa: A001  (C ABI name)
+    """One cutting-plane pass at t over bracket (y_lo, y_hi): counts, local sums, P, N, pred, succ."""
+    x = _flat(x)
+    ctx = _ctx_for(x)
+    s = PassStats()
+    _check(ctx, load().cpsel_eval(ctx.handle, C.c_void_p(x.data_ptr()), x.numel(), _dtype_code(x), float(t),
+                                  float(y_lo), float(y_hi), C.byref(s)))
+    return s.as_dict()
+
+
+def init_stats(x) -> dict:
+    x = _flat(x)
+    ctx = _ctx_for(x)
+    s = InitStats()
+    _check(ctx, load().cpsel_init(ctx.handle, C.c_void_p(x.data_ptr()), x.numel(), _dtype_code(x), C.byref(s)))
+    return s.as_dict()
+
+
+def small_select(z, r: int) -> float:
+    z = _flat(z)
+    ctx = _ctx_for(z)
+    dt = _dtype_code(z)
+    out = C.create_string_buffer(8)
+    _check(ctx, load().cpsel_small_select(ctx.handle, C.c_void_p(z.data_ptr()), z.numel(), dt, int(r), out))
+    return _out_value(out, dt)
+
+
+def get_trace(device: int = 0) -> list:
+    c = _ctxs.get(device)
+    if c is None:
+        return []
+    n = C.c_uint32()
+    load().cpsel_get_trace(c.handle, None, 0, C.byref(n))
+    rows = (TraceRow * max(n.value, 1))()
+    load().cpsel_get_trace(c.handle, rows, n.value, C.byref(n))
+    return [rows[i].as_dict() for i in range(n.value)]
+
+
+def set_config(device: int = 0, **kw) -> None:
+    c = _ctx_device(device)
+    cfg = Config()
+    _check(c, load().cpsel_get_config(c.handle, C.byref(cfg)))
+    for k, v in kw.items():
+        if not hasattr(cfg, k):
+            raise ValueError(f"unknown config field {k}")
+        setattr(cfg, k, int(v))
+    _check(c, load().cpsel_set_config(c.handle, C.byref(cfg)))
+
+
+def get_config(device: int = 0) -> dict:
+    c = _ctx_device(device)
+    cfg = Config()
+    _check(c, load().cpsel_get_config(c.handle, C.byref(cfg)))
+    return {f: getattr(cfg, f) for f, _ in cfg._fields_}
+
+
+def default_config() -> dict:
+    cfg = Config()
+    load().cpsel_config_default(C.byref(cfg))
+    return {f: getattr(cfg, f) for f, _ in cfg._fields_}
+
+
+# ------------------------------------------------------------------------------------------ LMS
+def _check_lms(X, y, thetas):
+    import torch
+    for t in (X, y, thetas):
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("X, y, thetas must be contiguous float32 CUDA tensors")
+    n, p = X.shape
+    if y.numel() != n:
+        raise ValueError("y must have n elements")
+    if thetas.dim() != 2 or thetas.shape[1] != p:
+        raise ValueError("thetas must be (C, p): row j is theta_j (= p x C column-major)")
+    return n, p, thetas.shape[0]
+
+
+def lms_objective(X, y, thetas, return_info: bool = False):
+    """Med_i (x_i . theta_j - y_i)^2 for every candidate theta_j (rows of thetas)."""
+    import torch
+    n, p, Cn = _check_lms(X, y, thetas)
+    ctx = _ctx_for(X)
+    out = torch.empty(Cn, device=X.device, dtype=torch.float32)
+    info = Info()
+    _check(ctx, load().cpsel_lms_objective(ctx.handle, C.c_void_p(X.data_ptr()), C.c_void_p(y.data_ptr()), n, p,
+                                           C.c_void_p(thetas.data_ptr()), Cn, C.c_void_p(out.data_ptr()),
+                                           C.byref(info)))
+    return (out, info.as_dict()) if return_info else out
+
+
+def lms_residuals(X, y, thetas, out=None):
+    """S[j, i] = (x_i . theta_j - y_i)^2 as a (C, n) tensor (= n x C column-major)."""
+    import torch
+    n, p, Cn = _check_lms(X, y, thetas)
+    ctx = _ctx_for(X)
+    if out is None:
+        out = torch.empty((Cn, n), device=X.device, dtype=torch.float32)
+    _check(ctx, load().cpsel_lms_residuals(ctx.handle, C.c_void_p(X.data_ptr()), C.c_void_p(y.data_ptr()), n, p,
+                                           C.c_void_p(thetas.data_ptr()), Cn, C.c_void_p(out.data_ptr())))
+    return out
+
+
+def select_kth_batched(S, k: int, return_info: bool = False):
+    """Row-wise k-th smallest of a (C, n) float32 CUDA tensor (columns of an n x C column-major S)."""
+    import torch
+    if S.dtype != torch.float32 or not S.is_cuda or not S.is_contiguous() or S.dim() != 2:
+        raise ValueError("S must be a contiguous (C, n) float32 CUDA tensor")
+    ctx = _ctx_for(S)
+    Cn, n = S.shape
+    out = torch.empty(Cn, device=S.device, dtype=torch.float32)
+    info = Info()
+    _check(ctx, load().cpsel_select_kth_batched(ctx.handle, C.c_void_p(S.data_ptr()), n, Cn, int(k),
+                                                C.c_void_p(out.data_ptr()), C.byref(info)))
+    return (out, info.as_dict()) if return_info else out
+
+
+# ------------------------------------------------------------------------------------------ multi-GPU
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = load().cpsel_nccl_unique_id(buf)
+    if st != OK:
+        raise CpselError(st, "ncclGetUniqueId failed / NCCL not loadable")
+    return buf.raw
+
+
+def comm_init(uid: bytes, rank: int, world: int, device: int) -> None:
+    c = _ctx_device(device)
+    buf = C.create_string_buffer(uid, 128)
+    _check(c, load().cpsel_comm_init(c.handle, buf, int(rank), int(world)))
+
+
+def select_kth_sharded(shard, k: int, return_info: bool = False):
+    """Collective: k-th smallest of the concatenation (rank order) of every rank's shard."""
+    shard = _flat(shard)
+    ctx = _ctx_for(shard)
+    dt = _dtype_code(shard)
+    out = C.create_string_buffer(8)
+    info = Info()
+    ptr = C.c_void_p(shard.data_ptr()) if shard.numel() else C.c_void_p(0)
+    _check(ctx, load().cpsel_select_kth_sharded(ctx.handle, ptr, shard.numel(), dt, int(k), out, C.byref(info)))
+    v = _out_value(out, dt)
+    return (v, info.as_dict()) if return_info else v
+
+
+# ------------------------------------------------------------------------------------------ host driver
+def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, select_fn, config: dict | None = None):
+    """Run libcpsel's cutting-plane driver with Python callbacks for the three data steps
+    (init_fn() -> dict of InitStats fields; pass_fn(t, y_lo, y_hi, compact) -> dict of PassStats
+    fields; select_fn(side, r) -> float).  No GPU involved: used to test the host logic."""
+    lib = load()
+    errors = []
+
+    def _init(_u, out):
+        try:
+            d = init_fn()
+            for f, _ in InitStats._fields_:
+                setattr(out.contents, f, d[f])
+            return 0
+        except Exception as e:  # pragma: no cover - surfaced below
+            errors.append(e)
+            return 1
+
+    def _pass(_u, t, lo, hi, compact, out):
+        try:
+            d = pass_fn(t, lo, hi, bool(compact))
+            for f, _ in PassStats._fields_:
+                setattr(out.contents, f, d.get(f, 0))
+            return 0
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            return 1
+
+    def _sel(_u, side, r, out):
+        try:
+            out[0] = float(select_fn(side, r))
+            return 0
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            return 1
+
+    cbs = (_INIT_CB(_init), _PASS_CB(_pass), _SEL_CB(_sel))
+    be = HostBackend(None, *cbs)
+    cfg = Config()
+    lib.cpsel_config_default(C.byref(cfg))
+    for key, v in (config or {}).items():
+        setattr(cfg, key, int(v))
+    val = C.c_double()
+    info = Info()
+    rows = (TraceRow * 512)()
+    nrows = C.c_uint32()
+    st = lib.cpsel_drive_host(C.byref(be), int(n), F32 if dtype == "f32" else F64, int(k), C.byref(cfg),
+                              C.byref(val), C.byref(info), rows, 512, C.byref(nrows))
+    if errors:
+        raise errors[0]
+    if st != OK:
+        raise CpselError(st, lib.cpsel_status_string(st).decode())
+    return val.value, info.as_dict(), [rows[i].as_dict() for i in range(min(nrows.value, 512))]

@@ -1,0 +1,972 @@
+// Host side of libcpsel.so: the cutting-plane driver (Algorithm 1, with the hybrid
+// finish of P:L196), its three back ends (one GPU, G GPUs over NCCL, host callbacks) and the
+// C ABI declared in include/cpsel.h.
+//
+// The driver is a pure host state machine; every step over the data is a kernel launch
+// (cpsel_kernels.cu) whose 96-byte result tuple comes back to the host once per pass
+// (P:L426 'partial sums ... added together on the CPU').  Readings R1-R20: DESIGN.md §3.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/cpsel.h"
+#include "cpsel_kernels.h"
+#include "cpsel_lms.h"
+#include "cpsel_nccl.h"
+
+using namespace cpsel;
+
+// ============================================================================================
+// context
+struct cpsel_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  LaunchShape shape{};
+  cpsel_config cfg{};
+  std::string err;
+  // device scratch
+  void* d_partials = nullptr;
+  unsigned int* d_ticket = nullptr;
+  unsigned long long* d_cursors = nullptr;
+  DevPass* d_pass = nullptr;
+  DevInit* d_init = nullptr;
+  RadixState* d_radix = nullptr;
+  unsigned int* d_hist = nullptr;
+  DevPass* d_gather = nullptr;       // G x DevPass (sharded)
+  DevInit* d_gather_init = nullptr;  // G x DevInit (sharded)
+  void* d_z = nullptr;               // compaction target
+  size_t z_bytes = 0;
+  void* d_zall = nullptr;            // all-gathered bracket contents (sharded)
+  size_t zall_bytes = 0;
+  void* d_stage = nullptr;           // H2D staging (cpsel_select_kth_host)
+  size_t stage_bytes = 0;
+  // pinned host mirrors
+  DevPass* h_pass = nullptr;
+  DevInit* h_init = nullptr;
+  RadixState* h_radix = nullptr;
+  DevPass* h_gather = nullptr;
+  DevInit* h_gather_init = nullptr;
+  // LMS workspace
+  LmsWorkspace lms;
+  // multi-GPU
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  // last trace
+  std::vector<cpsel_trace_row> trace;
+  // kernel timing (record_timing)
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+cpsel_status fail(cpsel_ctx* c, cpsel_status s, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+  }
+  return s;
+}
+
+#define CK(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(ctx, e_ == cudaErrorMemoryAllocation ? CPSEL_ENOMEM : CPSEL_ECUDA,     \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__);   \
+  } while (0)
+
+#define NK(expr)                                                                                 \
+  do {                                                                                           \
+    ncclResult_t r_ = (expr);                                                                    \
+    if (r_ != ncclSuccess)                                                                       \
+      return fail(ctx, CPSEL_ENCCL, "%s: %s", #expr, nccl_api().GetErrorString(r_));             \
+  } while (0)
+
+size_t elem_size(int dt) { return dt == kF32 ? 4 : 8; }
+
+cpsel_status ensure(cpsel_ctx* ctx, void** p, size_t* have, size_t need) {
+  if (*have >= need && *p) return CPSEL_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  size_t sz = std::max<size_t>(need, 256);
+  CK(cudaMalloc(p, sz));
+  *have = sz;
+  return CPSEL_OK;
+}
+
+// ---------------------------------------------------------------------------------- keys
+uint64_t key_of(double v, int dt) {
+  if (dt == kF32) {
+    float f = (float)v;
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    return (u & 0x80000000u) ? (uint32_t)~u : (u | 0x80000000u);
+  }
+  uint64_t u;
+  memcpy(&u, &v, 8);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+double from_key(uint64_t k, int dt) {
+  if (dt == kF32) {
+    uint32_t kk = (uint32_t)k;
+    uint32_t u = (kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk;
+    float f;
+    memcpy(&f, &u, 4);
+    return f;
+  }
+  uint64_t u = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+  double v;
+  memcpy(&v, &u, 8);
+  return v;
+}
+
+// Round t to the dtype and nudge it strictly inside ]yL, yR[ (R9).
+double snap(double t, double yL, double yR, int dt) {
+  if (dt == kF32) {
+    const float fl = (float)yL, fr = (float)yR;
+    float f = std::isfinite(t) ? (float)t : (float)(0.5 * yL + 0.5 * yR);
+    if (!(f > fl)) f = std::nextafterf(fl, INFINITY);
+    if (!(f < fr)) f = std::nextafterf(fr, -INFINITY);
+    return f;
+  }
+  double f = std::isfinite(t) ? t : 0.5 * yL + 0.5 * yR;
+  if (!(f > yL)) f = std::nextafter(yL, INFINITY);
+  if (!(f < yR)) f = std::nextafter(yR, -INFINITY);
+  return f;
+}
+
+// Ordered-key bisection point of ]yL, yR[ (safeguard, R7).
+double key_mid(double yL, double yR, int dt) {
+  const uint64_t a = key_of(yL, dt), b = key_of(yR, dt);
+  return from_key(a + (b - a) / 2, dt);
+}
+
+double canonical_zero(double v) { return v == 0.0 ? 0.0 : v; }
+
+// ============================================================================================
+// Back ends: what one 'reduction' means on a given substrate.
+struct Backend {
+  virtual ~Backend() = default;
+  virtual cpsel_status init(cpsel_init_stats* out) = 0;
+  virtual cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* out,
+                            uint64_t* z_lo, uint64_t* z_hi) = 0;
+  // side 0: (yL,t) half of the last compacting pass, 1: (t,yR) half, 2: all of x
+  virtual cpsel_status select(int side, uint64_t r, double* out) = 0;
+  virtual std::string message() const = 0;
+  // kernels launched / CUDA-event milliseconds of the last step (0 if not timed)
+  uint32_t launches = 0;
+  double step_ms = 0.0;
+};
+
+// ------------------------------------------------------------------------ one GPU
+struct GpuBackend : Backend {
+  cpsel_ctx* ctx;
+  const void* x;
+  uint64_t n;
+  int dt;
+  uint64_t zlo = 0, zhi = 0, zcap_elems = 0;
+  GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_) : ctx(c), x(x_), n(n_), dt(dt_) {}
+  std::string message() const override { return ctx->err; }
+  bool timed() const { return ctx->cfg.record_timing != 0; }
+  cudaError_t tic() { return timed() ? cudaEventRecord(ctx->ev0, ctx->stream) : cudaSuccess; }
+  cudaError_t toc() { return timed() ? cudaEventRecord(ctx->ev1, ctx->stream) : cudaSuccess; }
+  void read_ms() {  // after the stream synchronised
+    step_ms = 0.0;
+    float ms = 0.f;
+    if (timed() && cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) step_ms = ms;
+  }
+
+  cpsel_status init(cpsel_init_stats* o) override {
+    InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init};
+    CK(tic());
+    CK(launch_init(dt, a, ctx->shape, ctx->stream));
+    CK(toc());
+    CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    read_ms();
+    launches = 1;
+    const DevInit& r = *ctx->h_init;
+    o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
+    o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
+    return CPSEL_OK;
+  }
+  cpsel_status ensure_z(uint64_t m) {
+    cpsel_status s = ensure(ctx, &ctx->d_z, &ctx->z_bytes, (size_t)m * elem_size(dt));
+    if (s != CPSEL_OK) return s;
+    zcap_elems = ctx->z_bytes / elem_size(dt);
+    return CPSEL_OK;
+  }
+  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
+                    uint64_t* z_hi) override {
+    PassArgs a{};
+    a.x = x; a.n = n; a.t = t; a.y_lo = yL; a.y_hi = yR;
+    a.mode = compact ? kCompact : kHot;
+    a.z = ctx->d_z; a.z_cap = zcap_elems; a.cursors = ctx->d_cursors;
+    a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
+    CK(tic());
+    CK(launch_pass(dt, a, ctx->shape, ctx->stream));
+    CK(toc());
+    CK(cudaMemcpyAsync(ctx->h_pass, ctx->d_pass, sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    read_ms();
+    launches = 1;
+    const DevPass& r = *ctx->h_pass;
+    o->c_lt = r.c_lt; o->c_eq = r.c_eq; o->c_lo = r.c_lo; o->c_hi = r.c_hi;
+    o->L_lo = r.L_lo; o->L_hi = r.L_hi; o->P = r.P; o->N = r.N; o->pred = r.pred; o->succ = r.succ;
+    zlo = r.z_lo; zhi = r.z_hi;
+    *z_lo = r.z_lo; *z_hi = r.z_hi;
+    return CPSEL_OK;
+  }
+  cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out) {
+    CK(tic());
+    CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream));
+    CK(toc());
+    CK(cudaMemcpyAsync(ctx->h_radix, ctx->d_radix, sizeof(RadixState), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    read_ms();
+    launches = dt == kF32 ? 7 : 13;
+    *out = ctx->h_radix->value;
+    return CPSEL_OK;
+  }
+  cpsel_status select(int side, uint64_t r, double* out) override {
+    const size_t es = elem_size(dt);
+    if (side == 2) return select_on(x, n, r, out);
+    if (side == 0) return select_on(ctx->d_z, zlo, r, out);
+    return select_on(static_cast<char*>(ctx->d_z) + (zcap_elems - zhi) * es, zhi, r, out);
+  }
+};
+
+// ------------------------------------------------------------------------ G GPUs (NCCL)
+struct ShardedBackend : GpuBackend {
+  std::vector<uint64_t> n_rank;               // shard sizes
+  std::vector<uint64_t> zlo_rank, zhi_rank;   // per-rank compaction counts of the last pass
+  cpsel_init_stats combined{};
+  uint64_t n_global = 0;
+  ShardedBackend(cpsel_ctx* c, const void* x_, uint64_t n_local, int dt_) : GpuBackend(c, x_, n_local, dt_) {}
+
+  // All-gather the per-rank init records and combine them in rank order (R17).
+  cpsel_status gather_init() {
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    if (n > 0) {
+      InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init};
+      CK(launch_init(dt, a, ctx->shape, ctx->stream));
+    } else {
+      DevInit e{};
+      e.vmin = INFINITY; e.vmax = -INFINITY;
+      *ctx->h_init = e;
+      CK(cudaMemcpyAsync(ctx->d_init, ctx->h_init, sizeof(DevInit), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    // carry the shard size in the pad word
+    CK(cudaMemcpyAsync(&ctx->d_init->pad, &n, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    NK(nc.AllGather(ctx->d_init, ctx->d_gather_init, sizeof(DevInit), ncclUint8, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_gather_init, ctx->d_gather_init, G * sizeof(DevInit), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    n_rank.assign(G, 0);
+    combined = cpsel_init_stats{};
+    combined.vmin = INFINITY; combined.vmax = -INFINITY;
+    n_global = 0;
+    bool have_x0 = false;
+    double S = 0.0;
+    for (int q = 0; q < G; ++q) {
+      const DevInit& r = ctx->h_gather_init[q];
+      n_rank[q] = r.pad;
+      n_global += r.pad;
+      if (r.pad == 0) continue;
+      if (r.vmin < combined.vmin) { combined.vmin = r.vmin; combined.cnt_min = r.cnt_min; }
+      else if (r.vmin == combined.vmin) combined.cnt_min += r.cnt_min;
+      if (r.vmax > combined.vmax) { combined.vmax = r.vmax; combined.cnt_max = r.cnt_max; }
+      else if (r.vmax == combined.vmax) combined.cnt_max += r.cnt_max;
+      combined.nonfinite += r.nonfinite;
+      if (!have_x0) { combined.x0 = r.x0; have_x0 = true; }
+      S += r.S + (double)r.pad * (r.x0 - combined.x0);
+    }
+    combined.S = S;
+    return CPSEL_OK;
+  }
+  cpsel_status init(cpsel_init_stats* o) override {
+    *o = combined;
+    return CPSEL_OK;
+  }
+  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
+                    uint64_t* z_hi) override {
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    if (n > 0) {
+      PassArgs a{};
+      a.x = x; a.n = n; a.t = t; a.y_lo = yL; a.y_hi = yR;
+      a.mode = compact ? kCompact : kHot;
+      a.z = ctx->d_z; a.z_cap = zcap_elems; a.cursors = ctx->d_cursors;
+      a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
+      CK(tic());
+      CK(launch_pass(dt, a, ctx->shape, ctx->stream));
+      CK(toc());
+      launches = 1;
+    } else {
+      launches = 0;
+      DevPass e{};
+      e.pred = -INFINITY; e.succ = INFINITY;
+      *ctx->h_pass = e;
+      CK(cudaMemcpyAsync(ctx->d_pass, ctx->h_pass, sizeof(DevPass), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (n > 0) read_ms(); else step_ms = 0.0;
+    // fixed rank-order combine: identical bytes on every rank (R17)
+    cpsel_pass_stats s{};
+    s.pred = -INFINITY; s.succ = INFINITY;
+    uint64_t tlo = 0, thi = 0;
+    zlo_rank.assign(G, 0);
+    zhi_rank.assign(G, 0);
+    for (int q = 0; q < G; ++q) {
+      const DevPass& r = ctx->h_gather[q];
+      s.c_lt += r.c_lt; s.c_eq += r.c_eq; s.c_lo += r.c_lo; s.c_hi += r.c_hi;
+      s.L_lo += r.L_lo; s.L_hi += r.L_hi; s.P += r.P; s.N += r.N;
+      s.pred = std::max(s.pred, r.pred); s.succ = std::min(s.succ, r.succ);
+      zlo_rank[q] = r.z_lo; zhi_rank[q] = r.z_hi;
+      tlo += r.z_lo; thi += r.z_hi;
+    }
+    *o = s;
+    zlo = ctx->h_gather[ctx->rank].z_lo;
+    zhi = ctx->h_gather[ctx->rank].z_hi;
+    *z_lo = tlo; *z_hi = thi;
+    return CPSEL_OK;
+  }
+  // all-gather-v of per-rank segments (grouped broadcasts), then the same select on every rank
+  cpsel_status select(int side, uint64_t r, double* out) override {
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    const size_t es = elem_size(dt);
+    std::vector<uint64_t> cnt(G);
+    const void* mine = nullptr;
+    for (int q = 0; q < G; ++q) cnt[q] = side == 2 ? n_rank[q] : side == 0 ? zlo_rank[q] : zhi_rank[q];
+    if (side == 2) mine = x;
+    else if (side == 0) mine = ctx->d_z;
+    else mine = static_cast<char*>(ctx->d_z) + (zcap_elems - zhi) * es;
+    uint64_t total = 0;
+    for (int q = 0; q < G; ++q) total += cnt[q];
+    cpsel_status st = ensure(ctx, &ctx->d_zall, &ctx->zall_bytes, (size_t)total * es);
+    if (st != CPSEL_OK) return st;
+    NK(nc.GroupStart());
+    uint64_t off = 0;
+    for (int q = 0; q < G; ++q) {
+      if (cnt[q]) {
+        NK(nc.Broadcast(q == ctx->rank ? mine : nullptr, static_cast<char*>(ctx->d_zall) + off * es,
+                        (size_t)cnt[q] * es, ncclUint8, q, ctx->comm, ctx->stream));
+      }
+      off += cnt[q];
+    }
+    NK(nc.GroupEnd());
+    return select_on(ctx->d_zall, total, r, out);
+  }
+};
+
+// ------------------------------------------------------------------------ host callbacks
+struct HostBackend : Backend {
+  const cpsel_host_backend* be;
+  std::string msg;
+  explicit HostBackend(const cpsel_host_backend* b) : be(b) {}
+  std::string message() const override { return msg; }
+  cpsel_status init(cpsel_init_stats* o) override {
+    if (be->init(be->user, o) != 0) { msg = "init callback failed"; return CPSEL_EINTERNAL; }
+    return CPSEL_OK;
+  }
+  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
+                    uint64_t* z_hi) override {
+    if (be->pass(be->user, t, yL, yR, compact ? 1 : 0, o) != 0) { msg = "pass callback failed"; return CPSEL_EINTERNAL; }
+    // the callback reports c_lo/c_hi; those are the compacted halves
+    *z_lo = compact ? o->c_lo : 0;
+    *z_hi = compact ? o->c_hi : 0;
+    return CPSEL_OK;
+  }
+  cpsel_status select(int side, uint64_t r, double* out) override {
+    if (be->select(be->user, side, r, out) != 0) { msg = "select callback failed"; return CPSEL_EINTERNAL; }
+    return CPSEL_OK;
+  }
+};
+
+// ============================================================================================
+// The cutting-plane driver (Algorithm 1 + hybrid finish), shared by all back ends.
+//
+// Bracket invariant: c_le(yL) < k <= c_lt(yR), i.e. yL < x_(k) < yR, interior m = c_lt(yR)-c_le(yL).
+// Cuts: F_k's right derivative at yL, left derivative at yR (R4, tightest cuts).  Kelley's step
+// 1.1 with those cuts is exactly the mean of the open-bracket interior (App. A / pinned in
+// tests/test_oracle_pins.py::test_appendix_A_kelley_step_is_interior_mean_exact_rationals);
+// the driver evaluates it from bracket-local sums (no cancellation, R11).
+cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_config& cfg, uint64_t z_cap,
+                   double* value, cpsel_info* info, std::vector<cpsel_trace_row>* trace) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t es = elem_size(dt);
+  cpsel_info inf{};
+  if (trace) trace->clear();
+  auto done = [&](double v, uint32_t reason) {
+    *value = canonical_zero(v);
+    inf.exit_reason = reason;
+    inf.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (info) *info = inf;
+    return CPSEL_OK;
+  };
+  // step 0: one reduction -> x_(1), x_(n), sum
+  cpsel_init_stats rec{};
+  cpsel_status st = be.init(&rec);
+  if (st != CPSEL_OK) return st;
+  inf.passes = 1;
+  inf.launches += be.launches;
+  inf.kernel_ms_init = be.step_ms;
+  inf.bytes_moved = n * es;
+  if (rec.nonfinite) return CPSEL_ENONFINITE;
+  if (k <= rec.cnt_min) return done(rec.vmin, 0);
+  if (k > n - rec.cnt_max) return done(rec.vmax, 1);
+  if (n <= cfg.direct_threshold && !cfg.force_cp) {
+    double v;
+    st = be.select(2, k, &v);
+    if (st != CPSEL_OK) return st;
+    inf.launches += be.launches;
+    inf.kernel_ms_select = be.step_ms;
+    inf.z_count = n;
+    inf.bytes_moved += (uint64_t)(dt == kF32 ? 3 : 6) * n * es;
+    return done(v, 6);
+  }
+  double yL = rec.vmin, yR = rec.vmax;
+  uint64_t c_le_L = rec.cnt_min, c_lt_R = n - rec.cnt_max;
+  long double N_L = 0.0L, P_R = 0.0L;  // N(yL) = sum (yL-x)^+ = 0 at the min; P(yR) = 0 at the max
+  uint64_t m = c_lt_R - c_le_L;       // >= 1
+  // first iterate: mean of the interior (App. A) from the shifted sum
+  double t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
+                          (double)m;
+  int slow = 0;
+  bool bisect = false;
+  const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
+  for (uint32_t it = 1;; ++it) {
+    if (it > cfg.max_iters) {
+      if (info) *info = inf;
+      return CPSEL_EINTERNAL;
+    }
+    uint32_t kind = 0;
+    if (bisect) {
+      t = key_mid(yL, yR, dt);
+      kind = 1;
+      inf.fallback_steps++;
+    }
+    const double tq = snap(t, yL, yR, dt);
+    if (!(tq > yL && tq < yR)) {
+      if (info) *info = inf;
+      return CPSEL_EINTERNAL;  // impossible while m >= 1
+    }
+    const bool compact = m <= z_cap;
+    cpsel_pass_stats s{};
+    uint64_t zl = 0, zh = 0;
+    st = be.pass(tq, yL, yR, compact, &s, &zl, &zh);
+    if (st != CPSEL_OK) return st;
+    inf.launches += be.launches;
+    inf.kernel_ms_passes += be.step_ms;
+    inf.passes++;
+    inf.cp_iters++;
+    inf.bytes_moved += n * es + (compact ? (zl + zh) * es : 0);
+    const uint64_t c_lt = s.c_lt, c_le = s.c_lt + s.c_eq;
+    // F_k(t) from positive terms only (App. A identities; Eq. 2 with paper-k = n-k+1, R2)
+    const long double N_t = N_L + (long double)c_le_L * ((long double)tq - yL) + s.L_lo;
+    const long double P_t = P_R + (long double)(n - c_lt_R) * ((long double)yR - tq) + s.L_hi;
+    cpsel_trace_row row{};
+    row.t = tq;
+    row.F = (double)(wP * P_t + wN * N_t);
+    row.c_lt = c_lt;
+    row.c_eq = c_le - c_lt;
+    row.kind = kind;
+    row.compacted = compact ? 1 : 0;
+    row.kernel_ms = be.step_ms;
+    // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
+    if (c_lt < k && k <= c_le) {
+      if (trace && cfg.record_trace) trace->push_back(row);
+      return done(tq, 2);
+    }
+    const uint64_t m_old = m;
+    int side;
+    if (c_le < k) {  // dF(t) < 0: y_L <- t (sign per R1)
+      const uint64_t c_hi = c_lt_R - c_le;
+      if (c_le + 1 == k) {  // x_(k) is the successor of t (P:L192 footnote, mirrored)
+        row.interior = 0;
+        if (trace && cfg.record_trace) trace->push_back(row);
+        return done(s.succ, 4);
+      }
+      if (compact && zh != c_hi) {
+        if (info) *info = inf;
+        return CPSEL_EINTERNAL;
+      }
+      yL = tq; N_L = N_t; c_le_L = c_le; m = c_hi;
+      t = tq + s.L_hi / (double)c_hi;  // mean of ]t, yR[ (App. A)
+      side = 1;
+    } else {  // c_lt >= k: y_R <- t
+      const uint64_t c_lo = c_lt - c_le_L;
+      if (c_lt == k) {  // x_(k) = largest x < t (P:L192 footnote)
+        row.interior = 0;
+        if (trace && cfg.record_trace) trace->push_back(row);
+        return done(s.pred, 3);
+      }
+      if (compact && zl != c_lo) {
+        if (info) *info = inf;
+        return CPSEL_EINTERNAL;
+      }
+      yR = tq; P_R = P_t; c_lt_R = c_lt; m = c_lo;
+      t = tq - s.L_lo / (double)c_lo;  // mean of ]yL, t[ (App. A)
+      side = 0;
+    }
+    row.interior = m;
+    if (trace && cfg.record_trace) trace->push_back(row);
+    if (compact) {  // hybrid finish: exact selection in the kept half
+      double v;
+      const uint64_t r = k - c_le_L;
+      st = be.select(side, r, &v);
+      if (st != CPSEL_OK) return st;
+      inf.launches += be.launches;
+      inf.kernel_ms_select = be.step_ms;
+      inf.z_count = m;
+      inf.bytes_moved += (uint64_t)(dt == kF32 ? 3 : 6) * m * es;
+      return done(v, 5);
+    }
+    // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
+    // ordered-key bisection until progress resumes (bounds the pass count on any input)
+    if (m > m_old - m_old / 8) {
+      if (++slow >= 2) bisect = true;
+    } else {
+      slow = 0;
+      bisect = false;
+    }
+  }
+}
+
+uint64_t auto_z_cap(uint64_t n, const cpsel_config& cfg) {
+  if (cfg.z_cap) return cfg.z_cap;
+  uint64_t z = n / 16;
+  z = std::max<uint64_t>(z, 1ull << 16);
+  z = std::min<uint64_t>(z, 1ull << 24);
+  return z;
+}
+
+cpsel_status check_common(cpsel_ctx* ctx, const void* p, uint64_t n, cpsel_dtype dtype) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!p) return fail(ctx, CPSEL_EINVAL, "null array pointer");
+  if (n == 0) return fail(ctx, CPSEL_EINVAL, "n == 0");
+  if (dtype != CPSEL_F32 && dtype != CPSEL_F64) return fail(ctx, CPSEL_EINVAL, "bad dtype %d", (int)dtype);
+  if (reinterpret_cast<uintptr_t>(p) % elem_size(dtype)) return fail(ctx, CPSEL_EINVAL, "misaligned element pointer");
+  return CPSEL_OK;
+}
+
+void store_value(double v, cpsel_dtype dt, void* h_out) {
+  if (dt == CPSEL_F32) {
+    float f = (float)v;
+    memcpy(h_out, &f, 4);
+  } else {
+    memcpy(h_out, &v, 8);
+  }
+}
+
+cpsel_status run_single(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k, void* h_out,
+                        cpsel_info* info) {
+  GpuBackend be(ctx, d_x, n, (int)dtype);
+  const uint64_t zc = std::min<uint64_t>(auto_z_cap(n, ctx->cfg), n);
+  cpsel_status s = be.ensure_z(zc);
+  if (s != CPSEL_OK) return s;
+  double v = 0;
+  s = drive(be, n, (int)dtype, k, ctx->cfg, zc, &v, info, &ctx->trace);
+  if (s == CPSEL_ENONFINITE) return fail(ctx, s, "input holds NaN or Inf");
+  if (s == CPSEL_EINTERNAL) return fail(ctx, s, "cutting-plane safeguard tripped (iteration cap / inconsistent counts)");
+  if (s != CPSEL_OK) return s;
+  store_value(v, dtype, h_out);
+  return CPSEL_OK;
+}
+
+}  // namespace
+
+// ============================================================================================
+// C ABI
+extern "C" {
+
+const char* cpsel_status_string(cpsel_status s) {
+  switch (s) {
+    case CPSEL_OK: return "ok";
+    case CPSEL_EINVAL: return "invalid argument";
+    case CPSEL_ERANK: return "rank out of range";
+    case CPSEL_ENONFINITE: return "non-finite input";
+    case CPSEL_ECUDA: return "CUDA error";
+    case CPSEL_ENCCL: return "NCCL error";
+    case CPSEL_ENOMEM: return "out of memory";
+    case CPSEL_EINTERNAL: return "internal safeguard";
+  }
+  return "unknown status";
+}
+
+void cpsel_config_default(cpsel_config* c) {
+  if (!c) return;
+  memset(c, 0, sizeof *c);
+  c->z_cap = 0;
+  c->direct_threshold = 1ull << 17;
+  c->max_iters = 200;
+  c->force_cp = 0;
+  c->record_trace = 1;
+  c->record_timing = 0;
+}
+
+cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
+  if (!out) return CPSEL_EINVAL;
+  *out = nullptr;
+  cpsel_ctx* ctx = new cpsel_ctx();
+  ctx->device = device;
+  cpsel_config_default(&ctx->cfg);
+  DeviceGuard g(device);
+  auto bail = [&](cpsel_status s) {
+    // keep ctx for the message? the caller has no handle yet: print to stderr
+    fprintf(stderr, "cpsel_create: %s\n", ctx->err.c_str());
+    cpsel_destroy(ctx);
+    return s;
+  };
+#define CKC(expr)                                                                         \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      fail(ctx, CPSEL_ECUDA, "%s: %s", #expr, cudaGetErrorString(e_));                    \
+      return bail(e_ == cudaErrorMemoryAllocation ? CPSEL_ENOMEM : CPSEL_ECUDA);          \
+    }                                                                                     \
+  } while (0)
+  CKC(cudaSetDevice(device));
+  if (cuda_stream) {
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  CKC(query_shapes(device, &ctx->shape));
+  CKC(cudaMalloc(&ctx->d_partials, partial_bytes_needed(ctx->shape)));
+  CKC(cudaMalloc(&ctx->d_ticket, 256));
+  CKC(cudaMemset(ctx->d_ticket, 0, 256));
+  CKC(cudaMalloc(&ctx->d_cursors, 256));
+  CKC(cudaMemset(ctx->d_cursors, 0, 256));
+  CKC(cudaMalloc(&ctx->d_pass, sizeof(DevPass)));
+  CKC(cudaMalloc(&ctx->d_init, sizeof(DevInit)));
+  CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
+  CKC(cudaMalloc(&ctx->d_hist, 2048 * sizeof(unsigned)));
+  CKC(cudaMemset(ctx->d_hist, 0, 2048 * sizeof(unsigned)));
+  CKC(cudaHostAlloc(&ctx->h_pass, sizeof(DevPass), cudaHostAllocDefault));
+  CKC(cudaHostAlloc(&ctx->h_init, sizeof(DevInit), cudaHostAllocDefault));
+  CKC(cudaHostAlloc(&ctx->h_radix, sizeof(RadixState), cudaHostAllocDefault));
+  CKC(cudaEventCreate(&ctx->ev0));
+  CKC(cudaEventCreate(&ctx->ev1));
+  CKC(cudaDeviceSynchronize());
+#undef CKC
+  *out = ctx;
+  return CPSEL_OK;
+}
+
+void cpsel_destroy(cpsel_ctx* ctx) {
+  if (!ctx) return;
+  {
+    DeviceGuard g(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
+    void* dev[] = {ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
+                   ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_z, ctx->d_zall, ctx->d_stage};
+    for (void* p : dev)
+      if (p) cudaFree(p);
+    lms_free(ctx->lms);
+    void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init};
+    for (void* p : host)
+      if (p) cudaFreeHost(p);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+}
+
+const char* cpsel_last_error(const cpsel_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+cpsel_status cpsel_set_config(cpsel_ctx* ctx, const cpsel_config* cfg) {
+  if (!ctx || !cfg) return CPSEL_EINVAL;
+  if (cfg->max_iters == 0) return fail(ctx, CPSEL_EINVAL, "max_iters must be >= 1");
+  ctx->cfg = *cfg;
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_get_config(const cpsel_ctx* ctx, cpsel_config* cfg) {
+  if (!ctx || !cfg) return CPSEL_EINVAL;
+  *cfg = ctx->cfg;
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_set_stream(cpsel_ctx* ctx, void* cuda_stream) {
+  if (!ctx) return CPSEL_EINVAL;
+  DeviceGuard g(ctx->device);
+  if (ctx->own_stream && ctx->stream) {
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamDestroy(ctx->stream);
+    ctx->own_stream = false;
+  }
+  if (cuda_stream) {
+    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
+  } else {
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    ctx->own_stream = true;
+  }
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_select_kth(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k,
+                              void* h_out, cpsel_info* info) {
+  cpsel_status s = check_common(ctx, d_x, n, dtype);
+  if (s != CPSEL_OK) return s;
+  if (!h_out) return fail(ctx, CPSEL_EINVAL, "null h_out");
+  if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k=%llu outside [1,%llu]", (unsigned long long)k, (unsigned long long)n);
+  DeviceGuard g(ctx->device);
+  return run_single(ctx, d_x, n, dtype, k, h_out, info);
+}
+
+cpsel_status cpsel_median(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, void* h_out,
+                          cpsel_info* info) {
+  return cpsel_select_kth(ctx, d_x, n, dtype, (n + 1) / 2, h_out, info);
+}
+
+cpsel_status cpsel_select_kth_host(cpsel_ctx* ctx, const void* h_x, uint64_t n, cpsel_dtype dtype, uint64_t k,
+                                   void* h_out, cpsel_info* info) {
+  cpsel_status s = check_common(ctx, h_x, n, dtype);
+  if (s != CPSEL_OK) return s;
+  if (!h_out) return fail(ctx, CPSEL_EINVAL, "null h_out");
+  if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k=%llu outside [1,%llu]", (unsigned long long)k, (unsigned long long)n);
+  DeviceGuard g(ctx->device);
+  const size_t bytes = (size_t)n * elem_size(dtype);
+  s = ensure(ctx, &ctx->d_stage, &ctx->stage_bytes, bytes);
+  if (s != CPSEL_OK) return s;
+  CK(cudaMemcpyAsync(ctx->d_stage, h_x, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  return run_single(ctx, ctx->d_stage, n, dtype, k, h_out, info);
+}
+
+cpsel_status cpsel_eval(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, double t, double y_lo,
+                        double y_hi, cpsel_pass_stats* out) {
+  cpsel_status s = check_common(ctx, d_x, n, dtype);
+  if (s != CPSEL_OK) return s;
+  if (!out) return fail(ctx, CPSEL_EINVAL, "null out");
+  auto representable = [&](double v) { return dtype == CPSEL_F64 || (double)(float)v == v; };
+  if (std::isnan(t) || std::isnan(y_lo) || std::isnan(y_hi) || !representable(t) || !representable(y_lo) ||
+      !representable(y_hi))
+    return fail(ctx, CPSEL_EINVAL, "t / bracket not representable in the dtype");
+  DeviceGuard g(ctx->device);
+  PassArgs a{};
+  a.x = d_x; a.n = n; a.t = t; a.y_lo = y_lo; a.y_hi = y_hi; a.mode = kDirect;
+  a.cursors = ctx->d_cursors; a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
+  CK(launch_pass((int)dtype, a, ctx->shape, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_pass, ctx->d_pass, sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  const DevPass& r = *ctx->h_pass;
+  out->c_lt = r.c_lt; out->c_eq = r.c_eq; out->c_lo = r.c_lo; out->c_hi = r.c_hi;
+  out->L_lo = r.L_lo; out->L_hi = r.L_hi; out->P = r.P; out->N = r.N; out->pred = r.pred; out->succ = r.succ;
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_init(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, cpsel_init_stats* out) {
+  cpsel_status s = check_common(ctx, d_x, n, dtype);
+  if (s != CPSEL_OK) return s;
+  if (!out) return fail(ctx, CPSEL_EINVAL, "null out");
+  DeviceGuard g(ctx->device);
+  GpuBackend be(ctx, d_x, n, (int)dtype);
+  return be.init(out);
+}
+
+cpsel_status cpsel_small_select(cpsel_ctx* ctx, const void* d_z, uint64_t m, cpsel_dtype dtype, uint64_t r,
+                                void* h_out) {
+  cpsel_status s = check_common(ctx, d_z, m, dtype);
+  if (s != CPSEL_OK) return s;
+  if (!h_out) return fail(ctx, CPSEL_EINVAL, "null h_out");
+  if (r < 1 || r > m) return fail(ctx, CPSEL_ERANK, "r outside [1,m]");
+  DeviceGuard g(ctx->device);
+  GpuBackend be(ctx, d_z, m, (int)dtype);
+  double v;
+  s = be.select_on(d_z, m, r, &v);
+  if (s != CPSEL_OK) return s;
+  store_value(canonical_zero(v), dtype, h_out);
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_get_trace(const cpsel_ctx* ctx, cpsel_trace_row* rows, uint32_t max_rows, uint32_t* n_rows) {
+  if (!ctx || !n_rows) return CPSEL_EINVAL;
+  *n_rows = (uint32_t)ctx->trace.size();
+  if (rows)
+    for (uint32_t i = 0; i < max_rows && i < ctx->trace.size(); ++i) rows[i] = ctx->trace[i];
+  return CPSEL_OK;
+}
+
+// ------------------------------------------------------------------------ multi-GPU
+cpsel_status cpsel_nccl_unique_id(void* id_out128) {
+  if (!id_out128) return CPSEL_EINVAL;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return CPSEL_ENCCL;
+  ncclUniqueId id;
+  if (nc.GetUniqueId(&id) != ncclSuccess) return CPSEL_ENCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  memcpy(id_out128, &id, 128);
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int world) {
+  if (!ctx || !id128 || world < 1 || rank < 0 || rank >= world) return CPSEL_EINVAL;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return fail(ctx, CPSEL_ENCCL, "NCCL unavailable: %s", nc.load_error);
+  DeviceGuard g(ctx->device);
+  if (ctx->comm) {
+    nc.CommDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId id;
+  memcpy(&id, id128, 128);
+  NK(nc.CommInitRank(&ctx->comm, world, id, rank));
+  ctx->rank = rank;
+  ctx->world = world;
+  if (ctx->d_gather) cudaFree(ctx->d_gather);
+  if (ctx->d_gather_init) cudaFree(ctx->d_gather_init);
+  if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
+  if (ctx->h_gather_init) cudaFreeHost(ctx->h_gather_init);
+  CK(cudaMalloc(&ctx->d_gather, world * sizeof(DevPass)));
+  CK(cudaMalloc(&ctx->d_gather_init, world * sizeof(DevInit)));
+  CK(cudaHostAlloc(&ctx->h_gather, world * sizeof(DevPass), cudaHostAllocDefault));
+  CK(cudaHostAlloc(&ctx->h_gather_init, world * sizeof(DevInit), cudaHostAllocDefault));
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint64_t n_local, cpsel_dtype dtype,
+                                      uint64_t k, void* h_out, cpsel_info* info) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!ctx->comm) return fail(ctx, CPSEL_ENCCL, "cpsel_comm_init has not been called");
+  if (n_local > 0 && !d_shard) return fail(ctx, CPSEL_EINVAL, "null shard pointer");
+  if (dtype != CPSEL_F32 && dtype != CPSEL_F64) return fail(ctx, CPSEL_EINVAL, "bad dtype");
+  if (!h_out) return fail(ctx, CPSEL_EINVAL, "null h_out");
+  DeviceGuard g(ctx->device);
+  ShardedBackend be(ctx, d_shard, n_local, (int)dtype);
+  cpsel_status s = be.gather_init();
+  if (s != CPSEL_OK) return s;
+  const uint64_t n = be.n_global;
+  if (n == 0) return fail(ctx, CPSEL_EINVAL, "global n == 0");
+  if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
+  const uint64_t zc = std::min<uint64_t>(auto_z_cap(n, ctx->cfg), n);
+  s = be.ensure_z(std::max<uint64_t>(std::min<uint64_t>(zc, n_local), 1));
+  if (s != CPSEL_OK) return s;
+  double v = 0;
+  s = drive(be, n, (int)dtype, k, ctx->cfg, zc, &v, info, &ctx->trace);
+  if (s == CPSEL_ENONFINITE) return fail(ctx, s, "input holds NaN or Inf");
+  if (s == CPSEL_EINTERNAL) return fail(ctx, s, "cutting-plane safeguard tripped");
+  if (s != CPSEL_OK) return s;
+  store_value(v, dtype, h_out);
+  return CPSEL_OK;
+}
+
+// ------------------------------------------------------------------------ host-only driver
+cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dtype dtype, uint64_t k,
+                              const cpsel_config* cfg, double* value_out, cpsel_info* info, cpsel_trace_row* trace,
+                              uint32_t max_rows, uint32_t* n_rows) {
+  if (!be || !be->init || !be->pass || !be->select || !value_out) return CPSEL_EINVAL;
+  if (dtype != CPSEL_F32 && dtype != CPSEL_F64) return CPSEL_EINVAL;
+  if (n == 0) return CPSEL_EINVAL;
+  if (k < 1 || k > n) return CPSEL_ERANK;
+  cpsel_config c;
+  if (cfg) c = *cfg; else cpsel_config_default(&c);
+  HostBackend hb(be);
+  std::vector<cpsel_trace_row> tr;
+  const uint64_t zc = std::min<uint64_t>(auto_z_cap(n, c), n);
+  cpsel_status s = drive(hb, n, (int)dtype, k, c, zc, value_out, info, &tr);
+  if (n_rows) *n_rows = (uint32_t)tr.size();
+  if (trace)
+    for (uint32_t i = 0; i < max_rows && i < tr.size(); ++i) trace[i] = tr[i];
+  return s;
+}
+
+// ------------------------------------------------------------------------ LMS
+cpsel_status cpsel_lms_residuals(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
+                                 const float* d_thetas, uint32_t C, float* d_S) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!d_X || !d_y || !d_thetas || !d_S) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
+  DeviceGuard g(ctx->device);
+  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t n, uint32_t C, uint64_t k,
+                                      float* d_out, cpsel_info* info) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!d_S || !d_out) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
+  DeviceGuard g(ctx->device);
+  LmsReport rep{};
+  cudaError_t e = batched_select(ctx->lms, d_S, n, C, k, d_out, ctx->cfg.max_iters, &rep, ctx->stream);
+  if (e == cudaErrorNotSupported) {
+    // column-by-column through the single-array path (same kernels, one column at a time)
+    std::vector<float> host(C);
+    for (uint32_t j = 0; j < C; ++j) {
+      cpsel_info ci{};
+      cpsel_status s = run_single(ctx, d_S + (size_t)j * n, n, CPSEL_F32, k, &host[j], &ci);
+      if (s != CPSEL_OK) return s;
+      rep.passes += ci.passes; rep.cp_iters += ci.cp_iters; rep.z_total += ci.z_count; rep.bytes += ci.bytes_moved;
+    }
+    CK(cudaMemcpyAsync(d_out, host.data(), C * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    e = cudaSuccess;
+  }
+  CK(e);
+  if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "input holds NaN or Inf");
+  if (info) {
+    memset(info, 0, sizeof *info);
+    info->passes = rep.passes;
+    info->cp_iters = rep.cp_iters;
+    info->z_count = rep.z_total;
+    info->bytes_moved = rep.bytes;
+    info->ms_total = rep.ms;
+  }
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_lms_objective(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
+                                 const float* d_thetas, uint32_t C, float* d_out, cpsel_info* info) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!d_X || !d_y || !d_thetas || !d_out) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
+  DeviceGuard g(ctx->device);
+  float* d_S = nullptr;
+  cpsel_status s = ensure(ctx, reinterpret_cast<void**>(&ctx->lms.S), &ctx->lms.S_bytes, (size_t)n * C * sizeof(float));
+  if (s != CPSEL_OK) return s;
+  d_S = ctx->lms.S;
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
+  s = cpsel_select_kth_batched(ctx, d_S, n, C, (n + 1) / 2, d_out, info);
+  if (info) info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return s;
+}
+
+}  // extern "C"

@@ -1,0 +1,90 @@
+// Internal interface between the host driver (cpsel_driver.cpp) and the sm_100a kernels
+// (cpsel_kernels.cu).  Not part of the public ABI (include/cpsel.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cpsel {
+
+enum Dtype : int { kF32 = 0, kF64 = 1 };
+
+// Result of one pass at t over bracket (y_lo, y_hi) (step a2), written by the last CTA.
+struct DevPass {
+  unsigned long long c_lt, c_eq;   // #{x<t}, #{x==t}  (global)
+  unsigned long long c_lo, c_hi;   // #{y_lo<x<t}, #{t<x<y_hi} (direct mode only; else 0)
+  double L_lo, L_hi;               // sum_{y_lo<x<t}(t-x), sum_{t<x<y_hi}(x-t)
+  double P, N;                     // direct mode only: sum (x-t)^+, sum (t-x)^+
+  double pred, succ;               // max{y_lo<x<t}, min{t<x<y_hi}
+  unsigned long long z_lo, z_hi;   // elements written by the fused compaction (a4)
+};
+static_assert(sizeof(DevPass) == 96, "DevPass layout");
+
+// Result of the init pass (step a1).
+struct DevInit {
+  double vmin, vmax, S, x0;
+  unsigned long long cnt_min, cnt_max, nonfinite, pad;
+};
+
+// Per-CTA partial of a pass (grid reduction scratch).
+struct PassPartial {
+  unsigned long long c_lt, c_eq, c_lo, c_hi;
+  double L_lo, L_hi, P, N, pred, succ;
+};
+struct InitPartial {
+  double vmin, vmax, S, pad;
+  unsigned long long cnt_min, cnt_max, nonfinite, pad2;
+};
+
+// Device-side state of the radix select (step a5).
+struct RadixState {
+  unsigned long long prefix, mask;   // ordered-key bits fixed so far
+  unsigned long long r;              // remaining 1-based rank inside the prefix class
+  unsigned long long count;          // candidates in the prefix class (diagnostic)
+  double value;                      // the selected element (after the last round)
+  unsigned long long key;
+};
+
+enum PassMode : int { kHot = 0, kCompact = 1, kDirect = 2 };
+
+struct PassArgs {
+  const void* x;
+  uint64_t n;
+  double t, y_lo, y_hi;              // representable in the dtype
+  int mode;
+  void* z;                           // compaction target (mode kCompact), capacity z_cap
+  uint64_t z_cap;
+  unsigned long long* cursors;       // [0]=lo count, [1]=hi count; self-resetting
+  void* partials;                    // >= grid PassPartial
+  unsigned int* ticket;              // self-resetting grid ticket
+  DevPass* out;                      // device (or mapped host) result
+};
+
+struct InitArgs {
+  const void* x;
+  uint64_t n;
+  void* partials;
+  unsigned int* ticket;
+  DevInit* out;
+};
+
+struct LaunchShape {
+  int num_sms;
+  int grid_pass[2][3];   // [dtype][mode]
+  int grid_init[2];
+  int grid_hist[2];
+};
+
+// Query occupancy and fill the persistent grid sizes (multiples of the SM count).
+cudaError_t query_shapes(int device, LaunchShape* shape);
+size_t partial_bytes_needed(const LaunchShape& shape);
+
+cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st);
+cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
+
+// Radix select of the r-th smallest (1-based) of z[0..m) (any element alignment).
+// hist: >= 2048 unsigned ints, zero on entry, left zeroed.  state: device RadixState.
+// On completion state->value holds the element (as double).
+cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
+                                unsigned int* hist, const LaunchShape& s, cudaStream_t st);
+
+}  // namespace cpsel

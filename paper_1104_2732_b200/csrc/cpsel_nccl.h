@@ -1,0 +1,26 @@
+// Run-time binding of NCCL (internal).  The library does not link libnccl: it resolves the
+// copy already loaded in the process (torch's NCCL when torch.distributed is in use), else the
+// system libnccl.so.2, so exactly one NCCL instance serves the process.
+#pragma once
+#include <nccl.h>
+
+namespace cpsel {
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  const char* load_error = "";
+};
+
+// Resolve once (thread-safe); returns the table (check .ok).
+const NcclApi& nccl_api();
+
+}  // namespace cpsel

@@ -1,0 +1,84 @@
+"""Numpy data steps for libcpsel's host-only driver (cpsel_drive_host).
+
+The driver (C++) decides every query point; these callbacks only evaluate one pass over a
+(possibly sharded) numpy array, exactly as the CUDA kernels would, and combine shards through
+an optional `comm` (gloo all-gather).  Test infrastructure, not the product path."""
+import math
+
+import numpy as np
+
+
+class NumpyShard:
+    def __init__(self, x, comm=None):
+        self.x = np.ascontiguousarray(x)
+        self.comm = comm  # callable: obj -> list of objs from every rank (rank order)
+        self.kept = None
+
+    def _gather(self, obj):
+        return [obj] if self.comm is None else self.comm(obj)
+
+    def init(self):
+        x = self.x
+        if x.size:
+            mn, mx = x.min(), x.max()
+            rec = {"vmin": float(mn), "vmax": float(mx), "cnt_min": int((x == mn).sum()),
+                   "cnt_max": int((x == mx).sum()), "nonfinite": int((~np.isfinite(x)).sum()),
+                   "x0": float(x[0]), "S": float(np.sum(x.astype(np.float64) - np.float64(x[0]))), "n": x.size}
+        else:
+            rec = {"vmin": math.inf, "vmax": -math.inf, "cnt_min": 0, "cnt_max": 0, "nonfinite": 0,
+                   "x0": 0.0, "S": 0.0, "n": 0}
+        out = None
+        S = 0.0
+        for r in self._gather(rec):
+            if r["n"] == 0:
+                continue
+            if out is None:
+                out = dict(r)
+                S = r["S"]
+                continue
+            if r["vmin"] < out["vmin"]:
+                out["vmin"], out["cnt_min"] = r["vmin"], r["cnt_min"]
+            elif r["vmin"] == out["vmin"]:
+                out["cnt_min"] += r["cnt_min"]
+            if r["vmax"] > out["vmax"]:
+                out["vmax"], out["cnt_max"] = r["vmax"], r["cnt_max"]
+            elif r["vmax"] == out["vmax"]:
+                out["cnt_max"] += r["cnt_max"]
+            out["nonfinite"] += r["nonfinite"]
+            S += r["S"] + r["n"] * (r["x0"] - out["x0"])
+        out["S"] = S
+        return out
+
+    def pass_(self, t, lo, hi, compact):
+        x = self.x
+        t64, lo64, hi64 = np.float64(t), np.float64(lo), np.float64(hi)
+        lt, gt = x < t64, x > t64
+        mlo, mhi = lt & (x > lo64), gt & (x < hi64)
+        xd = x.astype(np.float64)
+        mine = {"c_lt": int(lt.sum()), "c_eq": int((x == t64).sum()), "c_lo": int(mlo.sum()),
+                "c_hi": int(mhi.sum()), "L_lo": float(np.sum(t64 - xd[mlo])), "L_hi": float(np.sum(xd[mhi] - t64)),
+                "P": 0.0, "N": 0.0,
+                "pred": float(x[mlo].max()) if mlo.any() else -math.inf,
+                "succ": float(x[mhi].min()) if mhi.any() else math.inf}
+        if compact:
+            self.kept = (x[mlo].copy(), x[mhi].copy())
+        out = {k: 0 for k in mine}
+        out["pred"], out["succ"] = -math.inf, math.inf
+        for r in self._gather(mine):
+            for k in ("c_lt", "c_eq", "c_lo", "c_hi", "L_lo", "L_hi"):
+                out[k] += r[k]
+            out["pred"] = max(out["pred"], r["pred"])
+            out["succ"] = min(out["succ"], r["succ"])
+        return out
+
+    def select(self, side, r):
+        part = self.x if side == 2 else self.kept[side]
+        allz = np.concatenate(self._gather(part))
+        return float(np.partition(allz, r - 1)[r - 1])
+
+
+def drive(x, k, dtype, comm=None, config=None):
+    import paper_1104_2732_b200 as cp
+    be = NumpyShard(x, comm)
+    n = x.size if comm is None else sum(comm(x.size))
+    return cp.drive_host(n, k, dtype, be.init, be.pass_, be.select, config)

@@ -1,0 +1,251 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (north_star): the selected element bit-exact (after -0 -> +0), every count exact, F and the
+pass sums within relative 1e-6 (float32) / 1e-12 (float64)."""
+import math
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+REL = {"f32": 1e-6, "f64": 1e-12}
+
+
+@pytest.fixture(scope="module")
+def cp():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1104_2732_b200 as cp
+    cp.load()
+    return cp
+
+
+def tdev(x):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def canon(v):
+    return 0.0 if v == 0 else v
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+# ----------------------------------------------------------------------------- a1: init
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("n,off", [(1, 0), (2, 1), (7, 3), (1_000_003, 0), (1_000_003, 1), (4_194_305, 3)])
+def test_init_reduction(cp, dtype, n, off):
+    x = datagen.make("mix3", n + off, dtype)[off:]       # ragged tail + misaligned start
+    s = cp.init_stats(tdev(datagen.make("mix3", n + off, dtype))[off:])
+    rec = O.init_record(x)
+    assert s["vmin"] == rec["min"] and s["vmax"] == rec["max"]
+    assert s["cnt_min"] == rec["cnt_min"] and s["cnt_max"] == rec["cnt_max"] and s["nonfinite"] == 0
+    assert s["x0"] == float(x[0])
+    ref = float(rec["sum"] - x.size * O.LD(float(x[0])))
+    assert s["S"] == pytest.approx(ref, rel=REL[dtype] * 10, abs=1e-9 * x.size)
+
+
+def test_init_counts_nonfinite(cp):
+    for bad in (np.nan, np.inf, -np.inf):
+        x = datagen.make("normal", 100_000, "f32")
+        x[777] = bad
+        assert cp.init_stats(tdev(x))["nonfinite"] == 1
+
+
+# ----------------------------------------------------------------------------- a2: one pass
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("dist", ["normal", "mix1", "dup256", "cauchy"])
+def test_eval_pass_matches_oracle(cp, dtype, dist):
+    n = 1_000_003
+    x = datagen.make(dist, n, dtype)
+    xd = tdev(x)
+    rng = np.random.default_rng(1)
+    npdt = np.float32 if dtype == "f32" else np.float64
+    qs = np.quantile(x, [0.01, 0.2, 0.45, 0.5, 0.55, 0.8, 0.99]).astype(npdt)
+    cases = [(x[5], -math.inf, math.inf), (x[n // 2], x[n // 3], x[2 * n // 3])]
+    for _ in range(6):
+        a, t, b = np.sort(rng.choice(qs, 3))
+        cases.append((t, a, b))
+    for t, lo, hi in cases:
+        t, lo, hi = float(npdt(t)), float(lo), float(hi)
+        g = cp.eval(xd, t, lo, hi)
+        r = O.pass_stats(x, t, lo, hi)
+        for key in ("c_lt", "c_eq", "c_lo", "c_hi"):
+            assert g[key] == r[key], key
+        assert g["pred"] == r["pred"] and g["succ"] == r["succ"]
+        for key in ("L_lo", "L_hi", "P", "N"):
+            assert g[key] == pytest.approx(float(r[key]), rel=REL[dtype], abs=1e-300), key
+
+
+def test_eval_misaligned_and_tiny(cp):
+    for n in (1, 2, 3, 5, 9, 33, 257, 4099):
+        for off in (0, 1, 2, 3):
+            x = datagen.make("normal", n + off, "f32")
+            xd = tdev(x)[off:]
+            xs = x[off:]
+            t = float(xs[len(xs) // 2])
+            g = cp.eval(xd, t, -math.inf, math.inf)
+            r = O.pass_stats(xs, t, -math.inf, math.inf)
+            assert (g["c_lt"], g["c_eq"], g["c_lo"], g["c_hi"]) == (r["c_lt"], r["c_eq"], r["c_lo"], r["c_hi"])
+            assert g["N"] == pytest.approx(float(r["N"]), rel=1e-6, abs=1e-30)
+
+
+# ----------------------------------------------------------------------------- a5: small select
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_small_select(cp, dtype):
+    rng = np.random.default_rng(2)
+    npdt = np.float32 if dtype == "f32" else np.float64
+    for m in (1, 2, 3, 31, 1000, 65_537, 1_000_001):
+        z = (rng.standard_normal(m) * 10 ** rng.uniform(-30, 30, m)).astype(npdt)
+        z[rng.integers(0, m, m // 10 + 1)] = 0.0
+        z[rng.integers(0, m, m // 10 + 1)] = -0.0
+        z[rng.integers(0, m, m // 7 + 1)] = z[0]
+        zd = tdev(z)
+        for r in sorted({1, 2, m // 3 or 1, (m + 1) // 2, m}):
+            got = cp.small_select(zd, r)
+            assert canon(got) == float(O.order_statistic(z, r))
+            assert math.copysign(1, got) > 0 or got != 0
+
+
+# ----------------------------------------------------------------------------- end to end
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_select_tiny_all_ranks(cp, dtype):
+    rng = np.random.default_rng(3)
+    npdt = np.float32 if dtype == "f32" else np.float64
+    for force in (0, 1):
+        cp.set_config(force_cp=force, z_cap=1 if force else 0)
+        for _ in range(60):
+            n = int(rng.integers(1, 12))
+            x = rng.choice(np.array([0.0, -0.0, 1.0, 1.0, -2.0, 3.5, 1e9, -1e9, 7.0]), n).astype(npdt)
+            xd = tdev(x)
+            for k in range(1, n + 1):
+                assert canon(cp.select_kth(xd, k)) == float(O.order_statistic(x, k))
+    cp.set_config(force_cp=0, z_cap=0)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_select_distributions_forced_cp(cp, dtype):
+    """Every distribution x ranks, through the cutting-plane passes (force_cp) with several
+    compaction thresholds, n spanning many tiles plus a ragged tail."""
+    n = 300_007
+    for dist in datagen.ALL_DISTS:
+        x = datagen.make(dist, n, dtype)
+        xd = tdev(x)
+        for k in sorted({1, 2, n // 10, O.median_rank(n), n - 1, n}):
+            want = float(O.order_statistic(x, k))
+            for zc in (0, 512, 50_000):
+                cp.set_config(force_cp=1, z_cap=zc)
+                v, info = cp.select_kth(xd, k, return_info=True)
+                assert canon(v) == want, (dist, k, zc, info)
+                assert info["passes"] == info["cp_iters"] + 1
+    cp.set_config(force_cp=0, z_cap=0)
+
+
+def test_select_direct_path_config0(cp):
+    """BASELINE configs[0]: median of n=1e5 float32 uniform (n <= direct_threshold -> direct select)."""
+    x = datagen.make("uniform", 100_000, "f32")
+    v, info = cp.median(tdev(x), return_info=True)
+    assert canon(v) == float(O.median(x))
+    assert info["exit"] in ("direct_select", "init_min", "init_max")
+
+
+@pytest.mark.parametrize("dist", datagen.BENCH_DISTS)
+def test_select_config1_2pow24_f32(cp, dist):
+    """BASELINE configs[1]: n=2^24 float32, k in {median, 1, n/10, n-1}."""
+    n = 1 << 24
+    xd = datagen.make(dist, n, "f32", device="cuda")
+    x = host(xd)
+    for k in (O.median_rank(n), 1, n // 10, n - 1):
+        v, info = cp.select_kth(xd, k, return_info=True)
+        assert canon(v) == float(O.order_statistic(x, k)), (dist, k, info)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "normal"])
+def test_select_config2_2pow28_f64(cp, dist):
+    """BASELINE configs[2]: k-th order statistic of n=2^28 float64 vs the sort-based oracle."""
+    n = 1 << 28
+    xd = datagen.make(dist, n, "f64", device="cuda")
+    x = host(xd)
+    for k in (O.median_rank(n), n // 10):
+        v, info = cp.select_kth(xd, k, return_info=True)
+        assert canon(v) == float(O.order_statistic(x, k)), (dist, k, info)
+    del xd
+
+
+def test_select_bench_size_2pow30_f32(cp):
+    """The bench workload (n=2^30 float32) in the launch configuration bench.py times: the result
+    is checked by the rank invariant #{x<v} <= k-1 < #{x<=v} computed by the oracle on the host copy."""
+    import torch
+    n = 1 << 30
+    for dist in ("uniform", "dup256"):
+        xd = datagen.make(dist, n, "f32", device="cuda")
+        k = O.median_rank(n)
+        v, info = cp.median(xd, return_info=True)
+        x = host(xd)
+        del xd
+        torch.cuda.empty_cache()
+        c_lt, c_eq = O.rank_counts(x, v)
+        assert c_lt <= k - 1 < c_lt + c_eq, (dist, info)
+        del x
+
+
+def test_trace_replay_F_parity(cp):
+    """Every cutting-plane pass of a real run: counts exact and F_k(t) within 1e-6 / 1e-12
+    relative of the oracle's direct long-double evaluation at the same t."""
+    for dtype in ("f32", "f64"):
+        for dist in ("normal", "mix4", "cauchy"):
+            x = datagen.make(dist, 2_000_003, dtype)
+            xd = tdev(x)
+            for k in (O.median_rank(x.size), 1000):
+                cp.set_config(force_cp=1, z_cap=1000)
+                cp.select_kth(xd, k)
+                tr = cp.get_trace()
+                assert tr
+                for row in tr:
+                    ref = O.eval_at(x, k, row["t"], -math.inf, math.inf)
+                    assert (row["c_lt"], row["c_eq"]) == (ref["c_lt"], ref["c_eq"])
+                    assert row["F"] == pytest.approx(float(ref["F"]), rel=REL[dtype])
+    cp.set_config(force_cp=0, z_cap=0)
+
+
+def test_host_buffer_path(cp):
+    import torch
+    x = datagen.make("normal", 3_000_001, "f32")
+    xt = torch.from_numpy(x).pin_memory()
+    k = 1_234_567
+    assert canon(cp.select_kth_host(xt, k)) == float(O.order_statistic(x, k))
+
+
+def test_errors_fail_loudly(cp):
+    import torch
+    x = datagen.make("normal", 1000, "f32")
+    xd = tdev(x)
+    with pytest.raises(ValueError):
+        cp.select_kth(xd, 0)
+    with pytest.raises(ValueError):
+        cp.select_kth(xd, 1001)
+    x[3] = np.nan
+    with pytest.raises(ValueError):
+        cp.median(tdev(x))
+    with pytest.raises(ValueError):
+        cp.median(torch.from_numpy(x))          # CPU tensor: no CPU fallback
+    with pytest.raises(ValueError):
+        cp.median(torch.ones(10, device="cuda", dtype=torch.float16))
+
+
+def test_sharded_world1_nccl(cp):
+    """The NCCL sharded entry point with world size 1 equals the single-GPU result."""
+    import torch
+    uid = cp.nccl_unique_id()
+    cp.comm_init(uid, 0, 1, torch.cuda.current_device())
+    for dist, dtype in (("normal", "f32"), ("mix5", "f64"), ("dup256", "f32")):
+        x = datagen.make(dist, 1_000_003, dtype)
+        xd = tdev(x)
+        for k in (1, 77, O.median_rank(x.size), x.size):
+            assert canon(cp.select_kth_sharded(xd, k)) == float(O.order_statistic(x, k))
