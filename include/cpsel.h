@@ -47,11 +47,14 @@ typedef struct cpsel_ctx cpsel_ctx;
 
 /* Tunables.  cpsel_config_default() fills the defaults noted here. */
 typedef struct {
-  uint64_t z_cap;            /* compaction threshold on the bracket interior count m:
-                                the pass whose current interior m <= z_cap also copies the
-                                interior into z (P:L196 copy_if, R8).  0 = auto. */
+  uint64_t z_cap;            /* compaction threshold on the bracket interior count m: the first
+                                pass whose interior m <= z_cap also copies the two halves of the
+                                bracket (split at t) out (P:L196 copy_if, R8); later passes run on
+                                the kept half only and compact again.  0 = auto (n/2). */
   uint64_t direct_threshold; /* n <= this: skip the cutting plane, select on x directly
                                 (P:L311 'radix sort ... most efficient up to 2^21').  Default 2^17 */
+  uint64_t select_cap;       /* a kept half of <= select_cap elements is finished by the exact
+                                radix select (P:L196 'sort z', R21).  0 = auto (2^20). */
   uint32_t max_iters;        /* safety cap on cutting-plane passes (P:L169 maxit).  Default 200 */
   int32_t force_cp;          /* 1: always run cutting-plane passes (parity runs), ignore direct_threshold */
   int32_t record_trace;      /* 1: keep the per-iteration trace (cpsel_get_trace).  Default 1 */
@@ -98,6 +101,7 @@ typedef struct {
   double F;               /* F_k(t) = (k-1/2) P(t) + (n-k+1/2) N(t)  (Eq. 2, R2) via App. A identities */
   uint64_t c_lt, c_eq;    /* exact counts at t */
   uint64_t interior;      /* bracket interior count after the update */
+  uint64_t scanned;       /* elements this pass read (x, or the compacted bracket) */
   uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard */
   uint32_t compacted;     /* 1 if this pass also wrote z */
   double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
@@ -183,11 +187,15 @@ typedef struct {
   void* user;
   /* init reduction over the whole (possibly sharded) array: fill *out. */
   int (*init)(void* user, cpsel_init_stats* out);
-  /* one pass at t over bracket (y_lo, y_hi); fill c_lt, c_eq, L_lo, L_hi, pred, succ of *out.
-     If compact != 0 the callee must also retain {y_lo < x < t} and {t < x < y_hi}. */
+  /* one pass at t over bracket (y_lo, y_hi) of the current array (x at first); fill c_lt, c_eq,
+     c_lo, c_hi, L_lo, L_hi, pred, succ of *out, counts local to the current array.  If
+     compact != 0 the callee must also retain {y_lo < x < t} and {t < x < y_hi}. */
   int (*pass)(void* user, double t, double y_lo, double y_hi, int compact, cpsel_pass_stats* out);
-  /* exact selection of the r-th smallest (1-based) of the retained half (side 0: (y_lo,t),
-     side 1: (t,y_hi)) of the last compacting pass, or of all of x if side == 2. */
+  /* make the retained half `side` (0: (y_lo,t), 1: (t,y_hi)) of the last compacting pass the
+     array every later pass (and select side 2) runs on. */
+  int (*adopt)(void* user, int side);
+  /* exact selection of the r-th smallest (1-based) of the retained half `side` of the last
+     compacting pass, or of the current array if side == 2. */
   int (*select)(void* user, int side, uint64_t r, double* value_out);
 } cpsel_host_backend;
 cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dtype dtype,

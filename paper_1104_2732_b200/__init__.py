@@ -34,7 +34,8 @@ class CpselError(RuntimeError):
 
 
 class Config(C.Structure):
-    _fields_ = [("z_cap", C.c_uint64), ("direct_threshold", C.c_uint64), ("max_iters", C.c_uint32),
+    _fields_ = [("z_cap", C.c_uint64), ("direct_threshold", C.c_uint64), ("select_cap", C.c_uint64),
+                ("max_iters", C.c_uint32),
                 ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32)]
 
 
@@ -69,7 +70,8 @@ class InitStats(C.Structure):
 
 class TraceRow(C.Structure):
     _fields_ = [("t", C.c_double), ("F", C.c_double), ("c_lt", C.c_uint64), ("c_eq", C.c_uint64),
-                ("interior", C.c_uint64), ("kind", C.c_uint32), ("compacted", C.c_uint32),
+                ("interior", C.c_uint64), ("scanned", C.c_uint64), ("kind", C.c_uint32),
+                ("compacted", C.c_uint32),
                 ("kernel_ms", C.c_double)]
 
     def as_dict(self):
@@ -79,10 +81,12 @@ class TraceRow(C.Structure):
 _INIT_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(InitStats))
 _PASS_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_int, C.POINTER(PassStats))
 _SEL_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.POINTER(C.c_double))
+_ADOPT_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 
 
 class HostBackend(C.Structure):
-    _fields_ = [("user", C.c_void_p), ("init", _INIT_CB), ("pass_", _PASS_CB), ("select", _SEL_CB)]
+    _fields_ = [("user", C.c_void_p), ("init", _INIT_CB), ("pass_", _PASS_CB), ("adopt", _ADOPT_CB),
+                ("select", _SEL_CB)]
 
 
 # every symbol the header declares (tests check the library exports exactly these)
@@ -405,10 +409,11 @@ def select_kth_sharded(shard, k: int, return_info: bool = False):
 
 
 # ------------------------------------------------------------------------------------------ host driver
-def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, select_fn, config: dict | None = None):
-    """Run libcpsel's cutting-plane driver with Python callbacks for the three data steps
+def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, adopt_fn, select_fn, config: dict | None = None):
+    """Run libcpsel's cutting-plane driver with Python callbacks for the data steps
     (init_fn() -> dict of InitStats fields; pass_fn(t, y_lo, y_hi, compact) -> dict of PassStats
-    fields; select_fn(side, r) -> float).  No GPU involved: used to test the host logic."""
+    fields over the current array; adopt_fn(side); select_fn(side, r) -> float).  No GPU
+    involved: used to test the host logic."""
     lib = load()
     errors = []
 
@@ -440,7 +445,15 @@ def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, select_fn, config: 
             errors.append(e)
             return 1
 
-    cbs = (_INIT_CB(_init), _PASS_CB(_pass), _SEL_CB(_sel))
+    def _adopt(_u, side):
+        try:
+            adopt_fn(side)
+            return 0
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            return 1
+
+    cbs = (_INIT_CB(_init), _PASS_CB(_pass), _ADOPT_CB(_adopt), _SEL_CB(_sel))
     be = HostBackend(None, *cbs)
     cfg = Config()
     lib.cpsel_config_default(C.byref(cfg))

@@ -42,8 +42,8 @@ struct cpsel_ctx {
   unsigned int* d_hist = nullptr;
   DevPass* d_gather = nullptr;       // G x DevPass (sharded)
   DevInit* d_gather_init = nullptr;  // G x DevInit (sharded)
-  void* d_z = nullptr;               // compaction target
-  size_t z_bytes = 0;
+  void* d_zb[2] = {nullptr, nullptr}; // ping-pong compaction buffers
+  size_t zb_bytes[2] = {0, 0};
   void* d_zall = nullptr;            // all-gathered bracket contents (sharded)
   size_t zall_bytes = 0;
   void* d_stage = nullptr;           // H2D staging (cpsel_select_kth_host)
@@ -170,17 +170,27 @@ double canonical_zero(double v) { return v == 0.0 ? 0.0 : v; }
 
 // ============================================================================================
 // Back ends: what one 'reduction' means on a given substrate.
+//
+// A back end owns a "current array": x at first; after a compacting pass the driver may adopt
+// one half of it (multi-level compaction), so later passes read only the bracket
+// contents.  Counts a back end returns are local to the current array; the driver adds the
+// number of elements dropped below it (D_lo) to get global counts.
 struct Backend {
   virtual ~Backend() = default;
   virtual cpsel_status init(cpsel_init_stats* out) = 0;
+  // one pass at t over the current array; if compact, also copy ]yL,t[ and ]t,yR[ out
+  // (z_lo/z_hi: elements written, summed over ranks)
   virtual cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* out,
                             uint64_t* z_lo, uint64_t* z_hi) = 0;
-  // side 0: (yL,t) half of the last compacting pass, 1: (t,yR) half, 2: all of x
+  // current array <- half `side` (0: ]yL,t[, 1: ]t,yR[) of the last compacting pass
+  virtual cpsel_status adopt(int side) = 0;
+  // r-th smallest (1-based) of half `side` of the last compacting pass, or of the current array (2)
   virtual cpsel_status select(int side, uint64_t r, double* out) = 0;
   virtual std::string message() const = 0;
-  // kernels launched / CUDA-event milliseconds of the last step (0 if not timed)
+  // kernels launched / CUDA-event milliseconds / local elements read, of the last step
   uint32_t launches = 0;
   double step_ms = 0.0;
+  uint64_t scanned = 0;
 };
 
 // ------------------------------------------------------------------------ one GPU
@@ -189,8 +199,14 @@ struct GpuBackend : Backend {
   const void* x;
   uint64_t n;
   int dt;
-  uint64_t zlo = 0, zhi = 0, zcap_elems = 0;
-  GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_) : ctx(c), x(x_), n(n_), dt(dt_) {}
+  const void* cur;           // current array
+  uint64_t n_cur;
+  int cur_buf = -1;          // -1: x, else ping-pong buffer index
+  int tgt = 0;               // buffer written by the last compacting pass
+  uint64_t cap = 0;          // capacity (elements) of each ping-pong buffer
+  uint64_t zlo = 0, zhi = 0; // local halves written by the last compacting pass
+  GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
+      : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
   bool timed() const { return ctx->cfg.record_timing != 0; }
   cudaError_t tic() { return timed() ? cudaEventRecord(ctx->ev0, ctx->stream) : cudaSuccess; }
@@ -200,46 +216,88 @@ struct GpuBackend : Backend {
     float ms = 0.f;
     if (timed() && cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) step_ms = ms;
   }
+  char* buf(int i) const { return static_cast<char*>(ctx->d_zb[i]); }
+  const void* half_ptr(int side) const {
+    return side == 0 ? (const void*)buf(tgt) : (const void*)(buf(tgt) + (cap - zhi) * elem_size(dt));
+  }
+  uint64_t half_n(int side) const { return side == 0 ? zlo : zhi; }
 
-  cpsel_status init(cpsel_init_stats* o) override {
+  // init kernel (fast form, then the checked form if anything came out non-finite)
+  cpsel_status run_init(bool sync_result) {
     InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init};
     CK(tic());
-    CK(launch_init(dt, a, ctx->shape, ctx->stream));
+    CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
     CK(toc());
+    launches = 1;
+    scanned = n;
     CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     read_ms();
-    launches = 1;
+    const DevInit& r = *ctx->h_init;
+    if (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax)) {
+      CK(launch_init(dt, a, ctx->shape, ctx->stream, true));
+      launches = 2;
+      if (sync_result) {
+        CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+      }
+    }
+    return CPSEL_OK;
+  }
+  cpsel_status init(cpsel_init_stats* o) override {
+    cpsel_status st = run_init(true);
+    if (st != CPSEL_OK) return st;
     const DevInit& r = *ctx->h_init;
     o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
     o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
     return CPSEL_OK;
   }
+  // two ping-pong compaction buffers of m elements each
   cpsel_status ensure_z(uint64_t m) {
-    cpsel_status s = ensure(ctx, &ctx->d_z, &ctx->z_bytes, (size_t)m * elem_size(dt));
-    if (s != CPSEL_OK) return s;
-    zcap_elems = ctx->z_bytes / elem_size(dt);
+    const size_t es = elem_size(dt);
+    for (int i = 0; i < 2; ++i) {
+      cpsel_status s = ensure(ctx, &ctx->d_zb[i], &ctx->zb_bytes[i], (size_t)std::max<uint64_t>(m, 1) * es);
+      if (s != CPSEL_OK) return s;
+    }
+    cap = std::min(ctx->zb_bytes[0], ctx->zb_bytes[1]) / es;
     return CPSEL_OK;
   }
-  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
-                    uint64_t* z_hi) override {
+  cpsel_status launch_local_pass(double t, double yL, double yR, bool compact) {
     PassArgs a{};
-    a.x = x; a.n = n; a.t = t; a.y_lo = yL; a.y_hi = yR;
+    a.x = cur; a.n = n_cur; a.t = t; a.y_lo = yL; a.y_hi = yR;
     a.mode = compact ? kCompact : kHot;
-    a.z = ctx->d_z; a.z_cap = zcap_elems; a.cursors = ctx->d_cursors;
+    if (compact) {
+      tgt = (cur_buf == 0) ? 1 : 0;
+      a.z = buf(tgt);
+      a.z_cap = cap;
+    }
+    a.cursors = ctx->d_cursors;
     a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
     CK(tic());
     CK(launch_pass(dt, a, ctx->shape, ctx->stream));
     CK(toc());
+    launches = 1;
+    scanned = n_cur;
+    return CPSEL_OK;
+  }
+  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
+                    uint64_t* z_hi) override {
+    cpsel_status st = launch_local_pass(t, yL, yR, compact);
+    if (st != CPSEL_OK) return st;
     CK(cudaMemcpyAsync(ctx->h_pass, ctx->d_pass, sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     read_ms();
-    launches = 1;
     const DevPass& r = *ctx->h_pass;
     o->c_lt = r.c_lt; o->c_eq = r.c_eq; o->c_lo = r.c_lo; o->c_hi = r.c_hi;
     o->L_lo = r.L_lo; o->L_hi = r.L_hi; o->P = r.P; o->N = r.N; o->pred = r.pred; o->succ = r.succ;
-    zlo = r.z_lo; zhi = r.z_hi;
+    if (compact) { zlo = r.z_lo; zhi = r.z_hi; }
     *z_lo = r.z_lo; *z_hi = r.z_hi;
+    return CPSEL_OK;
+  }
+  cpsel_status adopt(int side) override {
+    cur = half_ptr(side);
+    n_cur = half_n(side);
+    cur_buf = tgt;
     return CPSEL_OK;
   }
   cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out) {
@@ -250,21 +308,21 @@ struct GpuBackend : Backend {
     CK(cudaStreamSynchronize(ctx->stream));
     read_ms();
     launches = dt == kF32 ? 7 : 13;
+    scanned = m;
     *out = ctx->h_radix->value;
     return CPSEL_OK;
   }
   cpsel_status select(int side, uint64_t r, double* out) override {
-    const size_t es = elem_size(dt);
-    if (side == 2) return select_on(x, n, r, out);
-    if (side == 0) return select_on(ctx->d_z, zlo, r, out);
-    return select_on(static_cast<char*>(ctx->d_z) + (zcap_elems - zhi) * es, zhi, r, out);
+    if (side == 2) return select_on(cur, n_cur, r, out);
+    return select_on(half_ptr(side), half_n(side), r, out);
   }
 };
 
 // ------------------------------------------------------------------------ G GPUs (NCCL)
 struct ShardedBackend : GpuBackend {
   std::vector<uint64_t> n_rank;               // shard sizes
-  std::vector<uint64_t> zlo_rank, zhi_rank;   // per-rank compaction counts of the last pass
+  std::vector<uint64_t> cur_rank;             // current-array sizes per rank
+  std::vector<uint64_t> zlo_rank, zhi_rank;   // per-rank halves of the last compacting pass
   cpsel_init_stats combined{};
   uint64_t n_global = 0;
   ShardedBackend(cpsel_ctx* c, const void* x_, uint64_t n_local, int dt_) : GpuBackend(c, x_, n_local, dt_) {}
@@ -274,20 +332,24 @@ struct ShardedBackend : GpuBackend {
     const NcclApi& nc = nccl_api();
     const int G = ctx->world;
     if (n > 0) {
-      InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init};
-      CK(launch_init(dt, a, ctx->shape, ctx->stream));
+      cpsel_status st = run_init(false);  // leaves the (checked) record in d_init
+      if (st != CPSEL_OK) return st;
     } else {
+      launches = 0;
       DevInit e{};
       e.vmin = INFINITY; e.vmax = -INFINITY;
       *ctx->h_init = e;
       CK(cudaMemcpyAsync(ctx->d_init, ctx->h_init, sizeof(DevInit), cudaMemcpyHostToDevice, ctx->stream));
     }
     // carry the shard size in the pad word
-    CK(cudaMemcpyAsync(&ctx->d_init->pad, &n, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
+    *reinterpret_cast<uint64_t*>(&ctx->h_init[0].pad) = n;
+    CK(cudaMemcpyAsync(&ctx->d_init->pad, &ctx->h_init[0].pad, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
     NK(nc.AllGather(ctx->d_init, ctx->d_gather_init, sizeof(DevInit), ncclUint8, ctx->comm, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_gather_init, ctx->d_gather_init, G * sizeof(DevInit), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    if (n == 0) step_ms = 0.0;
+    scanned = n;
     n_rank.assign(G, 0);
     combined = cpsel_init_stats{};
     combined.vmin = INFINITY; combined.vmax = -INFINITY;
@@ -308,6 +370,7 @@ struct ShardedBackend : GpuBackend {
       S += r.S + (double)r.pad * (r.x0 - combined.x0);
     }
     combined.S = S;
+    cur_rank = n_rank;
     return CPSEL_OK;
   }
   cpsel_status init(cpsel_init_stats* o) override {
@@ -318,18 +381,13 @@ struct ShardedBackend : GpuBackend {
                     uint64_t* z_hi) override {
     const NcclApi& nc = nccl_api();
     const int G = ctx->world;
-    if (n > 0) {
-      PassArgs a{};
-      a.x = x; a.n = n; a.t = t; a.y_lo = yL; a.y_hi = yR;
-      a.mode = compact ? kCompact : kHot;
-      a.z = ctx->d_z; a.z_cap = zcap_elems; a.cursors = ctx->d_cursors;
-      a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
-      CK(tic());
-      CK(launch_pass(dt, a, ctx->shape, ctx->stream));
-      CK(toc());
-      launches = 1;
+    if (n_cur > 0) {
+      cpsel_status st = launch_local_pass(t, yL, yR, compact);
+      if (st != CPSEL_OK) return st;
     } else {
       launches = 0;
+      scanned = 0;
+      if (compact) tgt = (cur_buf == 0) ? 1 : 0;
       DevPass e{};
       e.pred = -INFINITY; e.succ = INFINITY;
       *ctx->h_pass = e;
@@ -338,38 +396,42 @@ struct ShardedBackend : GpuBackend {
     NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (n > 0) read_ms(); else step_ms = 0.0;
+    if (n_cur > 0) read_ms(); else step_ms = 0.0;
     // fixed rank-order combine: identical bytes on every rank (R17)
     cpsel_pass_stats s{};
     s.pred = -INFINITY; s.succ = INFINITY;
     uint64_t tlo = 0, thi = 0;
-    zlo_rank.assign(G, 0);
-    zhi_rank.assign(G, 0);
+    if (compact) {
+      zlo_rank.assign(G, 0);
+      zhi_rank.assign(G, 0);
+    }
     for (int q = 0; q < G; ++q) {
       const DevPass& r = ctx->h_gather[q];
       s.c_lt += r.c_lt; s.c_eq += r.c_eq; s.c_lo += r.c_lo; s.c_hi += r.c_hi;
       s.L_lo += r.L_lo; s.L_hi += r.L_hi; s.P += r.P; s.N += r.N;
       s.pred = std::max(s.pred, r.pred); s.succ = std::min(s.succ, r.succ);
-      zlo_rank[q] = r.z_lo; zhi_rank[q] = r.z_hi;
+      if (compact) { zlo_rank[q] = r.z_lo; zhi_rank[q] = r.z_hi; }
       tlo += r.z_lo; thi += r.z_hi;
     }
     *o = s;
-    zlo = ctx->h_gather[ctx->rank].z_lo;
-    zhi = ctx->h_gather[ctx->rank].z_hi;
+    if (compact) {
+      zlo = ctx->h_gather[ctx->rank].z_lo;
+      zhi = ctx->h_gather[ctx->rank].z_hi;
+    }
     *z_lo = tlo; *z_hi = thi;
     return CPSEL_OK;
+  }
+  cpsel_status adopt(int side) override {
+    cur_rank = side == 0 ? zlo_rank : zhi_rank;
+    return GpuBackend::adopt(side);
   }
   // all-gather-v of per-rank segments (grouped broadcasts), then the same select on every rank
   cpsel_status select(int side, uint64_t r, double* out) override {
     const NcclApi& nc = nccl_api();
     const int G = ctx->world;
     const size_t es = elem_size(dt);
-    std::vector<uint64_t> cnt(G);
-    const void* mine = nullptr;
-    for (int q = 0; q < G; ++q) cnt[q] = side == 2 ? n_rank[q] : side == 0 ? zlo_rank[q] : zhi_rank[q];
-    if (side == 2) mine = x;
-    else if (side == 0) mine = ctx->d_z;
-    else mine = static_cast<char*>(ctx->d_z) + (zcap_elems - zhi) * es;
+    const std::vector<uint64_t>& cnt = side == 2 ? cur_rank : side == 0 ? zlo_rank : zhi_rank;
+    const void* mine = side == 2 ? cur : half_ptr(side);
     uint64_t total = 0;
     for (int q = 0; q < G; ++q) total += cnt[q];
     cpsel_status st = ensure(ctx, &ctx->d_zall, &ctx->zall_bytes, (size_t)total * es);
@@ -401,9 +463,13 @@ struct HostBackend : Backend {
   cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
                     uint64_t* z_hi) override {
     if (be->pass(be->user, t, yL, yR, compact ? 1 : 0, o) != 0) { msg = "pass callback failed"; return CPSEL_EINTERNAL; }
-    // the callback reports c_lo/c_hi; those are the compacted halves
+    // the callback reports c_lo/c_hi over its current array; those are the compacted halves
     *z_lo = compact ? o->c_lo : 0;
     *z_hi = compact ? o->c_hi : 0;
+    return CPSEL_OK;
+  }
+  cpsel_status adopt(int side) override {
+    if (be->adopt(be->user, side) != 0) { msg = "adopt callback failed"; return CPSEL_EINTERNAL; }
     return CPSEL_OK;
   }
   cpsel_status select(int side, uint64_t r, double* out) override {
@@ -420,8 +486,13 @@ struct HostBackend : Backend {
 // 1.1 with those cuts is exactly the mean of the open-bracket interior (App. A / pinned in
 // tests/test_oracle_pins.py::test_appendix_A_kelley_step_is_interior_mean_exact_rationals);
 // the driver evaluates it from bracket-local sums (no cancellation, R11).
+//
+// Compaction (P:L196 copy_if, R8): the first pass whose interior m <= z_cap copies both halves
+// of the bracket (split at t) out; the kept half becomes the array of all later passes (every
+// later pass compacts again), until the kept half has <= select_cap elements, which are then
+// selected exactly by radix select (P:L196 'sort z', R21).
 cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_config& cfg, uint64_t z_cap,
-                   double* value, cpsel_info* info, std::vector<cpsel_trace_row>* trace) {
+                   uint64_t select_cap, double* value, cpsel_info* info, std::vector<cpsel_trace_row>* trace) {
   const auto t0 = std::chrono::steady_clock::now();
   const size_t es = elem_size(dt);
   cpsel_info inf{};
@@ -433,6 +504,15 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     if (info) *info = inf;
     return CPSEL_OK;
   };
+  auto do_select = [&](int side, uint64_t r, double* v) {
+    cpsel_status s2 = be.select(side, r, v);
+    if (s2 != CPSEL_OK) return s2;
+    inf.launches += be.launches;
+    inf.kernel_ms_select = be.step_ms;
+    inf.z_count = be.scanned;
+    inf.bytes_moved += (uint64_t)(dt == kF32 ? 3 : 6) * be.scanned * es;
+    return CPSEL_OK;
+  };
   // step 0: one reduction -> x_(1), x_(n), sum
   cpsel_init_stats rec{};
   cpsel_status st = be.init(&rec);
@@ -440,24 +520,22 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   inf.passes = 1;
   inf.launches += be.launches;
   inf.kernel_ms_init = be.step_ms;
-  inf.bytes_moved = n * es;
+  inf.bytes_moved = be.scanned * es;
   if (rec.nonfinite) return CPSEL_ENONFINITE;
   if (k <= rec.cnt_min) return done(rec.vmin, 0);
   if (k > n - rec.cnt_max) return done(rec.vmax, 1);
   if (n <= cfg.direct_threshold && !cfg.force_cp) {
     double v;
-    st = be.select(2, k, &v);
+    st = do_select(2, k, &v);
     if (st != CPSEL_OK) return st;
-    inf.launches += be.launches;
-    inf.kernel_ms_select = be.step_ms;
-    inf.z_count = n;
-    inf.bytes_moved += (uint64_t)(dt == kF32 ? 3 : 6) * n * es;
     return done(v, 6);
   }
   double yL = rec.vmin, yR = rec.vmax;
   uint64_t c_le_L = rec.cnt_min, c_lt_R = n - rec.cnt_max;
   long double N_L = 0.0L, P_R = 0.0L;  // N(yL) = sum (yL-x)^+ = 0 at the min; P(yR) = 0 at the max
   uint64_t m = c_lt_R - c_le_L;       // >= 1
+  uint64_t D_lo = 0;                   // elements of x below the current array
+  bool on_z = false;                   // the current array is a compacted bracket
   // first iterate: mean of the interior (App. A) from the shifted sum
   double t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
                           (double)m;
@@ -480,7 +558,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       if (info) *info = inf;
       return CPSEL_EINTERNAL;  // impossible while m >= 1
     }
-    const bool compact = m <= z_cap;
+    const bool compact = on_z || m <= z_cap;
     cpsel_pass_stats s{};
     uint64_t zl = 0, zh = 0;
     st = be.pass(tq, yL, yR, compact, &s, &zl, &zh);
@@ -489,8 +567,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     inf.kernel_ms_passes += be.step_ms;
     inf.passes++;
     inf.cp_iters++;
-    inf.bytes_moved += n * es + (compact ? (zl + zh) * es : 0);
-    const uint64_t c_lt = s.c_lt, c_le = s.c_lt + s.c_eq;
+    inf.bytes_moved += be.scanned * es + (compact ? (zl + zh) * es : 0);
+    const uint64_t c_lt = D_lo + s.c_lt, c_le = c_lt + s.c_eq;  // global counts at t
     // F_k(t) from positive terms only (App. A identities; Eq. 2 with paper-k = n-k+1, R2)
     const long double N_t = N_L + (long double)c_le_L * ((long double)tq - yL) + s.L_lo;
     const long double P_t = P_R + (long double)(n - c_lt_R) * ((long double)yR - tq) + s.L_hi;
@@ -502,6 +580,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     row.kind = kind;
     row.compacted = compact ? 1 : 0;
     row.kernel_ms = be.step_ms;
+    row.scanned = be.scanned;
     // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
     if (c_lt < k && k <= c_le) {
       if (trace && cfg.record_trace) trace->push_back(row);
@@ -511,7 +590,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     int side;
     if (c_le < k) {  // dF(t) < 0: y_L <- t (sign per R1)
       const uint64_t c_hi = c_lt_R - c_le;
-      if (c_le + 1 == k) {  // x_(k) is the successor of t (P:L192 footnote, mirrored)
+      if (c_le + 1 == k && std::isfinite(s.succ)) {  // x_(k) = successor of t (P:L192 footnote, mirrored)
         row.interior = 0;
         if (trace && cfg.record_trace) trace->push_back(row);
         return done(s.succ, 4);
@@ -525,7 +604,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       side = 1;
     } else {  // c_lt >= k: y_R <- t
       const uint64_t c_lo = c_lt - c_le_L;
-      if (c_lt == k) {  // x_(k) = largest x < t (P:L192 footnote)
+      if (c_lt == k && std::isfinite(s.pred)) {  // x_(k) = largest x < t (P:L192 footnote)
         row.interior = 0;
         if (trace && cfg.record_trace) trace->push_back(row);
         return done(s.pred, 3);
@@ -540,16 +619,17 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     }
     row.interior = m;
     if (trace && cfg.record_trace) trace->push_back(row);
-    if (compact) {  // hybrid finish: exact selection in the kept half
-      double v;
-      const uint64_t r = k - c_le_L;
-      st = be.select(side, r, &v);
+    if (compact) {
+      if (m <= select_cap) {  // hybrid finish: exact selection in the kept half
+        double v;
+        st = do_select(side, k - c_le_L, &v);
+        if (st != CPSEL_OK) return st;
+        return done(v, 5);
+      }
+      st = be.adopt(side);  // continue the cutting plane on the kept half only
       if (st != CPSEL_OK) return st;
-      inf.launches += be.launches;
-      inf.kernel_ms_select = be.step_ms;
-      inf.z_count = m;
-      inf.bytes_moved += (uint64_t)(dt == kF32 ? 3 : 6) * m * es;
-      return done(v, 5);
+      D_lo = c_le_L;
+      on_z = true;
     }
     // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
     // ordered-key bisection until progress resumes (bounds the pass count on any input)
@@ -563,12 +643,11 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
 }
 
 uint64_t auto_z_cap(uint64_t n, const cpsel_config& cfg) {
-  if (cfg.z_cap) return cfg.z_cap;
-  uint64_t z = n / 16;
-  z = std::max<uint64_t>(z, 1ull << 16);
-  z = std::min<uint64_t>(z, 1ull << 24);
-  return z;
+  if (cfg.z_cap) return std::min<uint64_t>(cfg.z_cap, n);
+  return std::max<uint64_t>(n / 2, 1);  // compact from the second pass on
 }
+
+uint64_t auto_select_cap(const cpsel_config& cfg) { return cfg.select_cap ? cfg.select_cap : (1ull << 20); }
 
 cpsel_status check_common(cpsel_ctx* ctx, const void* p, uint64_t n, cpsel_dtype dtype) {
   if (!ctx) return CPSEL_EINVAL;
@@ -591,11 +670,12 @@ void store_value(double v, cpsel_dtype dt, void* h_out) {
 cpsel_status run_single(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k, void* h_out,
                         cpsel_info* info) {
   GpuBackend be(ctx, d_x, n, (int)dtype);
-  const uint64_t zc = std::min<uint64_t>(auto_z_cap(n, ctx->cfg), n);
-  cpsel_status s = be.ensure_z(zc);
+  const uint64_t zc = auto_z_cap(n, ctx->cfg);
+  cpsel_status s = CPSEL_OK;
+  if (n > ctx->cfg.direct_threshold || ctx->cfg.force_cp) s = be.ensure_z(zc);
   if (s != CPSEL_OK) return s;
   double v = 0;
-  s = drive(be, n, (int)dtype, k, ctx->cfg, zc, &v, info, &ctx->trace);
+  s = drive(be, n, (int)dtype, k, ctx->cfg, zc, auto_select_cap(ctx->cfg), &v, info, &ctx->trace);
   if (s == CPSEL_ENONFINITE) return fail(ctx, s, "input holds NaN or Inf");
   if (s == CPSEL_EINTERNAL) return fail(ctx, s, "cutting-plane safeguard tripped (iteration cap / inconsistent counts)");
   if (s != CPSEL_OK) return s;
@@ -628,6 +708,7 @@ void cpsel_config_default(cpsel_config* c) {
   memset(c, 0, sizeof *c);
   c->z_cap = 0;
   c->direct_threshold = 1ull << 17;
+  c->select_cap = 0;
   c->max_iters = 200;
   c->force_cp = 0;
   c->record_trace = 1;
@@ -691,7 +772,8 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
     void* dev[] = {ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
-                   ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_z, ctx->d_zall, ctx->d_stage};
+                   ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
+                   ctx->d_stage};
     for (void* p : dev)
       if (p) cudaFree(p);
     lms_free(ctx->lms);
@@ -871,11 +953,11 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
   const uint64_t n = be.n_global;
   if (n == 0) return fail(ctx, CPSEL_EINVAL, "global n == 0");
   if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
-  const uint64_t zc = std::min<uint64_t>(auto_z_cap(n, ctx->cfg), n);
+  const uint64_t zc = auto_z_cap(n, ctx->cfg);
   s = be.ensure_z(std::max<uint64_t>(std::min<uint64_t>(zc, n_local), 1));
   if (s != CPSEL_OK) return s;
   double v = 0;
-  s = drive(be, n, (int)dtype, k, ctx->cfg, zc, &v, info, &ctx->trace);
+  s = drive(be, n, (int)dtype, k, ctx->cfg, zc, auto_select_cap(ctx->cfg), &v, info, &ctx->trace);
   if (s == CPSEL_ENONFINITE) return fail(ctx, s, "input holds NaN or Inf");
   if (s == CPSEL_EINTERNAL) return fail(ctx, s, "cutting-plane safeguard tripped");
   if (s != CPSEL_OK) return s;
@@ -887,7 +969,7 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
 cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dtype dtype, uint64_t k,
                               const cpsel_config* cfg, double* value_out, cpsel_info* info, cpsel_trace_row* trace,
                               uint32_t max_rows, uint32_t* n_rows) {
-  if (!be || !be->init || !be->pass || !be->select || !value_out) return CPSEL_EINVAL;
+  if (!be || !be->init || !be->pass || !be->adopt || !be->select || !value_out) return CPSEL_EINVAL;
   if (dtype != CPSEL_F32 && dtype != CPSEL_F64) return CPSEL_EINVAL;
   if (n == 0) return CPSEL_EINVAL;
   if (k < 1 || k > n) return CPSEL_ERANK;
@@ -895,8 +977,8 @@ cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dt
   if (cfg) c = *cfg; else cpsel_config_default(&c);
   HostBackend hb(be);
   std::vector<cpsel_trace_row> tr;
-  const uint64_t zc = std::min<uint64_t>(auto_z_cap(n, c), n);
-  cpsel_status s = drive(hb, n, (int)dtype, k, c, zc, value_out, info, &tr);
+  const uint64_t zc = auto_z_cap(n, c);
+  cpsel_status s = drive(hb, n, (int)dtype, k, c, zc, auto_select_cap(c), value_out, info, &tr);
   if (n_rows) *n_rows = (uint32_t)tr.size();
   if (trace)
     for (uint32_t i = 0; i < max_rows && i < tr.size(); ++i) trace[i] = tr[i];

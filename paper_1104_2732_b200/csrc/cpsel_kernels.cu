@@ -220,37 +220,54 @@ __device__ bool grid_finish(const P& mine, P* partials, unsigned int* ticket, P*
 
 // ------------------------------------------------------------------------------------------
 // Step a1: init reduction.
-template <typename T> struct InitFn {
+// Fast form: per 16-byte vector a min/max of its lanes (FMNMX) and a rarely-taken branch that
+// updates (min, #min) / (max, #max) only when the vector reaches the running extreme; the shifted
+// sum doubles as the non-finite detector (NaN/Inf make it non-finite; the host then re-runs the
+// CHECKED form, which counts non-finite elements exactly).
+template <typename T, bool CHECKED> struct InitFn {
   T mn, mx, x0;
   unsigned cmn, cmx, nonfin;
   double S;
   T g[4];
   __device__ InitFn(T x0_) : mn(tinf<T>()), mx(-tinf<T>()), x0(x0_), cmn(0), cmx(0), nonfin(0), S(0) {}
-  __device__ __forceinline__ void elem(T v, int u) {
-    nonfin += !(fabs(v) <= (sizeof(T) == 4 ? (T)FLT_MAX : (T)DBL_MAX));
+  __device__ __forceinline__ void slow(T v) {
     if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
     if (v > mx) { mx = v; cmx = 1; } else if (v == mx) ++cmx;
-    g[u & 3] += v - x0;
   }
   __device__ __forceinline__ void group_begin() { g[0] = g[1] = g[2] = g[3] = T(0); }
   __device__ __forceinline__ void group_end() { S += (double)((g[0] + g[1]) + (g[2] + g[3])); }
+  __device__ __forceinline__ void vec_elems(const float4& v, int u) {
+    const float lo = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
+    const float hi = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+    if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); slow(v.z); slow(v.w); }
+    g[u & 3] += ((v.x - x0) + (v.y - x0)) + ((v.z - x0) + (v.w - x0));
+    if (CHECKED)
+      nonfin += !(fabsf(v.x) <= FLT_MAX) + !(fabsf(v.y) <= FLT_MAX) + !(fabsf(v.z) <= FLT_MAX) + !(fabsf(v.w) <= FLT_MAX);
+  }
+  __device__ __forceinline__ void vec_elems(const double2& v, int u) {
+    const double lo = fmin(v.x, v.y), hi = fmax(v.x, v.y);
+    if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); }
+    g[u & 3] += (v.x - x0) + (v.y - x0);
+    if (CHECKED) nonfin += !(fabs(v.x) <= DBL_MAX) + !(fabs(v.y) <= DBL_MAX);
+  }
   template <bool MASKED, typename V> __device__ __forceinline__ void vec(const V& v, bool ok, int u) {
     if (MASKED && !ok) return;
-#pragma unroll
-    for (int j = 0; j < VecOf<T>::N; ++j) elem(lane_of(v, j), u);
+    vec_elems(v, u);
   }
   __device__ __forceinline__ void scalar(T v, bool ok) {
     if (!ok) return;
     group_begin();
-    elem(v, 0);
+    slow(v);
+    g[0] = v - x0;
+    if (CHECKED) nonfin += !(fabs(v) <= (sizeof(T) == 4 ? (T)FLT_MAX : (T)DBL_MAX));
     group_end();
   }
 };
 
-template <typename T, int UNROLL>
+template <typename T, int UNROLL, bool CHECKED>
 __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   const T* x = static_cast<const T*>(a.x);
-  InitFn<T> f(x[0]);
+  InitFn<T, CHECKED> f(x[0]);
   stream_array<T, UNROLL>(x, a.n, f);
   InitPartial p;
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
@@ -294,11 +311,16 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
     const bool lo = lt && (v > yL);
     const bool hi = gt && (v < yR);
     const T d = t - v;
-    if (MODE == kHot || MODE == kCompact) {
+    if (MODE == kHot) {
+      // the hot form: no pred/succ (the driver uses them only on small compacted brackets).
+      // Written as predicated PTX so every accumulation is ONE predicated instruction
+      // (10 issue slots per element: 5 compares, 1 sub, 4 predicated adds).
+      if (ok) hot_elem(v, glo[u], ghi[u]);
+    } else if (MODE == kCompact) {
       // ok is always true here for unmasked calls; masked calls pass ok explicitly
       if (ok) {
-        c_lt += lt;
-        c_eq += (v == t);
+        if (lt) ++c_lt;
+        if (v == t) ++c_eq;
         if (lo) { glo[u] += d; pred = tmax(pred, v); }
         if (hi) { ghi[u] -= d; succ = tmin(succ, v); }
       }
@@ -318,6 +340,36 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
       push(ok && lo, v, s_lo, n_lo);
       push(ok && hi, v, s_hi, n_hi);
     }
+  }
+  __device__ __forceinline__ void hot_elem(float v, float& glo_, float& ghi_) {
+    asm("{\n\t.reg .pred plt, pgt, peq, plo, phi;\n\t.reg .f32 d;\n\t"
+        "setp.lt.f32 plt, %4, %5;\n\t"
+        "setp.gt.f32 pgt, %4, %5;\n\t"
+        "setp.eq.f32 peq, %4, %5;\n\t"
+        "setp.gt.and.f32 plo, %4, %6, plt;\n\t"
+        "setp.lt.and.f32 phi, %4, %7, pgt;\n\t"
+        "sub.rn.f32 d, %5, %4;\n\t"
+        "@plt add.u32 %0, %0, 1;\n\t"
+        "@peq add.u32 %1, %1, 1;\n\t"
+        "@plo add.rn.f32 %2, %2, d;\n\t"
+        "@phi sub.rn.f32 %3, %3, d;\n\t}"
+        : "+r"(c_lt), "+r"(c_eq), "+f"(glo_), "+f"(ghi_)
+        : "f"(v), "f"(t), "f"(yL), "f"(yR));
+  }
+  __device__ __forceinline__ void hot_elem(double v, double& glo_, double& ghi_) {
+    asm("{\n\t.reg .pred plt, pgt, peq, plo, phi;\n\t.reg .f64 d;\n\t"
+        "setp.lt.f64 plt, %4, %5;\n\t"
+        "setp.gt.f64 pgt, %4, %5;\n\t"
+        "setp.eq.f64 peq, %4, %5;\n\t"
+        "setp.gt.and.f64 plo, %4, %6, plt;\n\t"
+        "setp.lt.and.f64 phi, %4, %7, pgt;\n\t"
+        "sub.rn.f64 d, %5, %4;\n\t"
+        "@plt add.u32 %0, %0, 1;\n\t"
+        "@peq add.u32 %1, %1, 1;\n\t"
+        "@plo add.rn.f64 %2, %2, d;\n\t"
+        "@phi sub.rn.f64 %3, %3, d;\n\t}"
+        : "+r"(c_lt), "+r"(c_eq), "+d"(glo_), "+d"(ghi_)
+        : "d"(v), "d"(t), "d"(yL), "d"(yR));
   }
   __device__ __forceinline__ void push(bool f, T v, T* s, int& cnt) {
     const unsigned m = __ballot_sync(FULL, f);
@@ -562,9 +614,9 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
   OCC(kF32, float, kHot) OCC(kF32, float, kCompact) OCC(kF32, float, kDirect)
   OCC(kF64, double, kHot) OCC(kF64, double, kCompact) OCC(kF64, double, kDirect)
 #undef OCC
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<float, 4>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<float, 4, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_init[kF32] = s->num_sms * (b > 0 ? b : 1);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<double, 4>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<double, 4, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_init[kF64] = s->num_sms * (b > 0 ? b : 1);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist_kernel<float>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_hist[kF32] = s->num_sms * (b > 0 ? b : 1);
@@ -589,13 +641,15 @@ static int clamp_grid(int grid, uint64_t n, int per_cta) {
   return grid;
 }
 
-cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st) {
+cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked) {
   if (dtype == kF32) {
     const int grid = clamp_grid(s.grid_init[kF32], a.n, kBlock * 4 * 4);
-    init_kernel<float, 4><<<grid, kBlock, 0, st>>>(a);
+    if (checked) init_kernel<float, 4, true><<<grid, kBlock, 0, st>>>(a);
+    else init_kernel<float, 4, false><<<grid, kBlock, 0, st>>>(a);
   } else {
     const int grid = clamp_grid(s.grid_init[kF64], a.n, kBlock * 4 * 2);
-    init_kernel<double, 4><<<grid, kBlock, 0, st>>>(a);
+    if (checked) init_kernel<double, 4, true><<<grid, kBlock, 0, st>>>(a);
+    else init_kernel<double, 4, false><<<grid, kBlock, 0, st>>>(a);
   }
   return cudaGetLastError();
 }

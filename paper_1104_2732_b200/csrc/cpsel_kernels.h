@@ -78,7 +78,9 @@ struct LaunchShape {
 cudaError_t query_shapes(int device, LaunchShape* shape);
 size_t partial_bytes_needed(const LaunchShape& shape);
 
-cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st);
+// checked=false: fast form (nonfinite stays 0; a non-finite input shows as a non-finite S/min/max);
+// checked=true: counts non-finite elements exactly.
+cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
 cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
 
 // Radix select of the r-th smallest (1-based) of z[0..m) (any element alignment).

@@ -13,6 +13,7 @@ class NumpyShard:
         self.x = np.ascontiguousarray(x)
         self.comm = comm  # callable: obj -> list of objs from every rank (rank order)
         self.kept = None
+        self.cur = self.x
 
     def _gather(self, obj):
         return [obj] if self.comm is None else self.comm(obj)
@@ -50,7 +51,7 @@ class NumpyShard:
         return out
 
     def pass_(self, t, lo, hi, compact):
-        x = self.x
+        x = self.cur
         t64, lo64, hi64 = np.float64(t), np.float64(lo), np.float64(hi)
         lt, gt = x < t64, x > t64
         mlo, mhi = lt & (x > lo64), gt & (x < hi64)
@@ -71,8 +72,11 @@ class NumpyShard:
             out["succ"] = min(out["succ"], r["succ"])
         return out
 
+    def adopt(self, side):
+        self.cur = self.kept[side]
+
     def select(self, side, r):
-        part = self.x if side == 2 else self.kept[side]
+        part = self.cur if side == 2 else self.kept[side]
         allz = np.concatenate(self._gather(part))
         return float(np.partition(allz, r - 1)[r - 1])
 
@@ -81,4 +85,4 @@ def drive(x, k, dtype, comm=None, config=None):
     import paper_1104_2732_b200 as cp
     be = NumpyShard(x, comm)
     n = x.size if comm is None else sum(comm(x.size))
-    return cp.drive_host(n, k, dtype, be.init, be.pass_, be.select, config)
+    return cp.drive_host(n, k, dtype, be.init, be.pass_, be.adopt, be.select, config)

@@ -107,7 +107,7 @@ def test_small_select(cp, dtype):
         z[rng.integers(0, m, m // 10 + 1)] = -0.0
         z[rng.integers(0, m, m // 7 + 1)] = z[0]
         zd = tdev(z)
-        for r in sorted({1, 2, m // 3 or 1, (m + 1) // 2, m}):
+        for r in sorted({1, min(2, m), m // 3 or 1, (m + 1) // 2, m}):
             got = cp.small_select(zd, r)
             assert canon(got) == float(O.order_statistic(z, r))
             assert math.copysign(1, got) > 0 or got != 0
@@ -119,14 +119,14 @@ def test_select_tiny_all_ranks(cp, dtype):
     rng = np.random.default_rng(3)
     npdt = np.float32 if dtype == "f32" else np.float64
     for force in (0, 1):
-        cp.set_config(force_cp=force, z_cap=1 if force else 0)
+        cp.set_config(force_cp=force, z_cap=1 if force else 0, select_cap=1 if force else 0)
         for _ in range(60):
             n = int(rng.integers(1, 12))
             x = rng.choice(np.array([0.0, -0.0, 1.0, 1.0, -2.0, 3.5, 1e9, -1e9, 7.0]), n).astype(npdt)
             xd = tdev(x)
             for k in range(1, n + 1):
                 assert canon(cp.select_kth(xd, k)) == float(O.order_statistic(x, k))
-    cp.set_config(force_cp=0, z_cap=0)
+    cp.set_config(force_cp=0, z_cap=0, select_cap=0)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
@@ -139,12 +139,12 @@ def test_select_distributions_forced_cp(cp, dtype):
         xd = tdev(x)
         for k in sorted({1, 2, n // 10, O.median_rank(n), n - 1, n}):
             want = float(O.order_statistic(x, k))
-            for zc in (0, 512, 50_000):
-                cp.set_config(force_cp=1, z_cap=zc)
+            for zc, sc in ((0, 0), (512, 0), (50_000, 0), (0, 64), (10**9, 1000)):
+                cp.set_config(force_cp=1, z_cap=zc, select_cap=sc)
                 v, info = cp.select_kth(xd, k, return_info=True)
-                assert canon(v) == want, (dist, k, zc, info)
+                assert canon(v) == want, (dist, k, zc, sc, info)
                 assert info["passes"] == info["cp_iters"] + 1
-    cp.set_config(force_cp=0, z_cap=0)
+    cp.set_config(force_cp=0, z_cap=0, select_cap=0)
 
 
 def test_select_direct_path_config0(cp):

@@ -28,7 +28,8 @@ def test_driver_matches_oracle_distributions(dtype):
         x = datagen.make(dist, 20_011, dtype)
         n = x.size
         for k in sorted({1, 2, n // 10, O.median_rank(n), n - 1, n}):
-            for cfg in ({"force_cp": 1, "z_cap": 64}, {"force_cp": 1, "z_cap": 4096}, {}):
+            for cfg in ({"force_cp": 1, "z_cap": 64}, {"force_cp": 1, "z_cap": 4096}, {},
+                        {"force_cp": 1, "select_cap": 16}, {"force_cp": 1, "select_cap": 1, "z_cap": 10_000}):
                 v, info, trace = drive(x, k, dtype, config=cfg)
                 assert canon(v) == float(O.order_statistic(x, k)), (dist, k, cfg, info)
                 assert info["passes"] == info["cp_iters"] + 1          # maxit+1 reductions
@@ -42,7 +43,8 @@ def test_driver_tiny_all_ranks_with_ties_and_signed_zero():
         for dtype in ("f32", "f64"):
             xd = x.astype(np.float32 if dtype == "f32" else np.float64)
             for k in range(1, n + 1):
-                for cfg in ({"force_cp": 1, "z_cap": 1}, {"force_cp": 1, "z_cap": 3}):
+                for cfg in ({"force_cp": 1, "z_cap": 1}, {"force_cp": 1, "z_cap": 3},
+                            {"force_cp": 1, "select_cap": 1}):
                     v, info, _ = drive(xd, k, dtype, config=cfg)
                     assert canon(v) == float(O.order_statistic(xd, k))
 
@@ -124,7 +126,7 @@ def _sharded_worker(rank, world, port, cases, q):
         x = datagen.make(dist_name, n, dtype)
         bounds = [0] + split + [n]
         shard = x[bounds[rank]:bounds[rank + 1]]
-        v, info, trace = drive(shard, k, dtype, comm=comm, config={"force_cp": 1, "z_cap": zc})
+        v, info, trace = drive(shard, k, dtype, comm=comm, config={"force_cp": 1, "z_cap": zc, "select_cap": 50})
         results.append((v, info["passes"], [(r["t"], r["c_lt"], r["c_eq"]) for r in trace]))
     q.put((rank, results))
     dist.destroy_process_group()
