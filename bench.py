@@ -193,9 +193,11 @@ def main():
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    traces = []
     for _ in range(a.steps):
         for x in xs:
             infos.append(select(x)[1])
+            traces.append(cp.get_trace(local))
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -207,15 +209,30 @@ def main():
         ms = float(t.item())
     value = len(xs) * n_global / (ms / 1e3)
 
-    # dominant kernel: the cutting-plane pass (algorithmic bytes = one read of the shard)
-    pass_ms = [i["kernel_ms_passes"] / max(i["cp_iters"], 1) for i in infos if i["cp_iters"]]
+    # Dominant kernel: pass_kernel (the cutting-plane pass, a2, incl. its fused compaction a4).
+    # Algorithmic bytes of one launch = 4 x (elements read + elements written), from the trace;
+    # achieved = sum of those bytes / sum of the CUDA-event durations of the launches.
+    rows = [r for tr in traces for r in tr]
     init_ms = [i["kernel_ms_init"] for i in infos]
     sel_ms = [i["kernel_ms_select"] for i in infos]
     iters = [i["cp_iters"] for i in infos]
-    bytes_per_pass = n * 4
-    avg_pass_ms = statistics.fmean(pass_ms) if pass_ms else float("nan")
     peak, peak_src = peaks()
-    achieved = bytes_per_pass / (avg_pass_ms / 1e3) / 1e9
+
+    def cls(sel):
+        rr = [r for r in rows if sel(r)]
+        by = sum(4 * (r["scanned"] + r["written"]) for r in rr)
+        ms = sum(r["kernel_ms"] for r in rr)
+        return {"launches": len(rr), "bytes": by, "ms": ms,
+                "GBps": (by / (ms / 1e3) / 1e9) if ms > 0 else None}
+
+    all_pass = cls(lambda r: True)
+    hot_x = cls(lambda r: not r["compacted"] and r["scanned"] == n)
+    comp_x = cls(lambda r: r["compacted"] and r["scanned"] == n)
+    z_pass = cls(lambda r: r["scanned"] < n)
+    init_GBps = (n * 4 * len(init_ms)) / (sum(init_ms) / 1e3) / 1e9 if sum(init_ms) > 0 else None
+    achieved = all_pass["GBps"]
+    avg_pass_ms = all_pass["ms"] / max(all_pass["launches"], 1)
+    bytes_per_pass = all_pass["bytes"] / max(all_pass["launches"], 1)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_pass_traffic.json")
     if os.path.exists(tp):
@@ -284,8 +301,11 @@ def main():
                        "z_cap": a.z_cap or "auto"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "pass_kernel<float,hot> (a2)", "bytes_per_launch": bytes_per_pass,
-                         "avg_launch_ms": avg_pass_ms, "peak_source": peak_src},
+                         "kernel": "pass_kernel<float,*> (a2 + fused a4), all launches in the timed region",
+                         "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms,
+                         "peak_source": peak_src,
+                         "classes": {"hot_full_pass": hot_x, "compacting_full_pass": comp_x,
+                                     "bracket_passes": z_pass, "init_GBps": init_GBps}},
             "cp_iters": {"mean": statistics.fmean(iters), "min": min(iters), "max": max(iters)},
             "kernel_ms_per_step": {"init": sum(init_ms) / a.steps, "passes": sum(i["kernel_ms_passes"] for i in infos) / a.steps,
                                    "select": sum(sel_ms) / a.steps, "all": step_kernel_ms},

@@ -102,14 +102,16 @@ typedef struct {
   uint64_t c_lt, c_eq;    /* exact counts at t */
   uint64_t interior;      /* bracket interior count after the update */
   uint64_t scanned;       /* elements this pass read (x, or the compacted bracket) */
+  uint64_t written;       /* elements this pass wrote (compaction of both bracket halves) */
   uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard */
   uint32_t compacted;     /* 1 if this pass also wrote z */
   double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
 } cpsel_trace_row;
 
 /* ---- context ------------------------------------------------------------------------- */
-/* device: CUDA ordinal; cuda_stream: a cudaStream_t on that device, or NULL for a private
- * non-blocking stream.  *out receives the new ctx. */
+/* device: CUDA ordinal; cuda_stream: a cudaStream_t on that device, or NULL for the legacy
+ * default stream (so work is ordered after whatever the caller enqueued there).  *out receives
+ * the new ctx. */
 cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out);
 void cpsel_destroy(cpsel_ctx* ctx);
 const char* cpsel_last_error(const cpsel_ctx* ctx);
@@ -117,7 +119,8 @@ const char* cpsel_status_string(cpsel_status s);
 void cpsel_config_default(cpsel_config* cfg);
 cpsel_status cpsel_set_config(cpsel_ctx* ctx, const cpsel_config* cfg);
 cpsel_status cpsel_get_config(const cpsel_ctx* ctx, cpsel_config* cfg);
-/* Re-target the ctx stream (e.g. torch's current stream) without recreating scratch. */
+/* Re-target the ctx stream (e.g. torch's current stream; NULL = legacy default stream) without
+ * recreating scratch. */
 cpsel_status cpsel_set_stream(cpsel_ctx* ctx, void* cuda_stream);
 
 /* ---- selection (north_star: select_kth(x, n, k), median(x, n)) -------------------------- */

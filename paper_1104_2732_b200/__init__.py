@@ -70,7 +70,7 @@ class InitStats(C.Structure):
 
 class TraceRow(C.Structure):
     _fields_ = [("t", C.c_double), ("F", C.c_double), ("c_lt", C.c_uint64), ("c_eq", C.c_uint64),
-                ("interior", C.c_uint64), ("scanned", C.c_uint64), ("kind", C.c_uint32),
+                ("interior", C.c_uint64), ("scanned", C.c_uint64), ("written", C.c_uint64), ("kind", C.c_uint32),
                 ("compacted", C.c_uint32),
                 ("kernel_ms", C.c_double)]
 
@@ -163,6 +163,8 @@ class _Ctx:
         self._stream = None
 
     def bind_stream(self, stream_ptr: int):
+        # torch's default stream has handle 0 = the legacy default stream, which the C ABI
+        # takes as NULL; any other handle is used as given
         if stream_ptr != self._stream:
             _check(self, load().cpsel_set_stream(self.handle, C.c_void_p(stream_ptr)))
             self._stream = stream_ptr

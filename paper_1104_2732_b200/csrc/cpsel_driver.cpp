@@ -581,6 +581,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     row.compacted = compact ? 1 : 0;
     row.kernel_ms = be.step_ms;
     row.scanned = be.scanned;
+    row.written = compact ? zl + zh : 0;
     // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
     if (c_lt < k && k <= c_le) {
       if (trace && cfg.record_trace) trace->push_back(row);
@@ -737,12 +738,8 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
     }                                                                                     \
   } while (0)
   CKC(cudaSetDevice(device));
-  if (cuda_stream) {
-    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
-  } else {
-    CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    ctx->own_stream = true;
-  }
+  // NULL selects the legacy default stream (the stream torch's default "current stream" is)
+  ctx->stream = static_cast<cudaStream_t>(cuda_stream);
   CKC(query_shapes(device, &ctx->shape));
   CKC(cudaMalloc(&ctx->d_partials, partial_bytes_needed(ctx->shape)));
   CKC(cudaMalloc(&ctx->d_ticket, 256));
@@ -769,7 +766,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
   if (!ctx) return;
   {
     DeviceGuard g(ctx->device);
-    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
     void* dev[] = {ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
@@ -810,12 +807,7 @@ cpsel_status cpsel_set_stream(cpsel_ctx* ctx, void* cuda_stream) {
     cudaStreamDestroy(ctx->stream);
     ctx->own_stream = false;
   }
-  if (cuda_stream) {
-    ctx->stream = static_cast<cudaStream_t>(cuda_stream);
-  } else {
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    ctx->own_stream = true;
-  }
+  ctx->stream = static_cast<cudaStream_t>(cuda_stream);  // NULL: the legacy default stream
   return CPSEL_OK;
 }
 
@@ -1007,19 +999,7 @@ cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t
   DeviceGuard g(ctx->device);
   LmsReport rep{};
   cudaError_t e = batched_select(ctx->lms, d_S, n, C, k, d_out, ctx->cfg.max_iters, &rep, ctx->stream);
-  if (e == cudaErrorNotSupported) {
-    // column-by-column through the single-array path (same kernels, one column at a time)
-    std::vector<float> host(C);
-    for (uint32_t j = 0; j < C; ++j) {
-      cpsel_info ci{};
-      cpsel_status s = run_single(ctx, d_S + (size_t)j * n, n, CPSEL_F32, k, &host[j], &ci);
-      if (s != CPSEL_OK) return s;
-      rep.passes += ci.passes; rep.cp_iters += ci.cp_iters; rep.z_total += ci.z_count; rep.bytes += ci.bytes_moved;
-    }
-    CK(cudaMemcpyAsync(d_out, host.data(), C * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    e = cudaSuccess;
-  }
+  if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a column");
   CK(e);
   if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "input holds NaN or Inf");
   if (info) {
@@ -1029,6 +1009,8 @@ cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t
     info->z_count = rep.z_total;
     info->bytes_moved = rep.bytes;
     info->ms_total = rep.ms;
+    info->kernel_ms_passes = rep.ms;
+    info->launches = 1;
   }
   return CPSEL_OK;
 }

@@ -75,7 +75,8 @@ template <> __device__ __forceinline__ double tinf() { return __longlong_as_doub
 // Any element alignment is accepted: the unaligned head and the tail (< VE elements each)
 // are processed as scalars by warp 0 of the last CTA.
 template <typename T, int UNROLL, typename F>
-__device__ __forceinline__ void stream_array(const T* __restrict__ x, uint64_t n, F& f) {
+__device__ __forceinline__ void stream_array(const T* __restrict__ x, uint64_t n, F& f,
+                                             unsigned part, unsigned nparts) {
   using V = typename VecOf<T>::V;
   constexpr int VE = VecOf<T>::N;
   const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
@@ -84,8 +85,8 @@ __device__ __forceinline__ void stream_array(const T* __restrict__ x, uint64_t n
   const V* __restrict__ xv = reinterpret_cast<const V*>(x + head);
   const uint64_t nvec = (n - head) / VE;
   constexpr uint64_t TILE = (uint64_t)kBlock * UNROLL;
-  const uint64_t stride = (uint64_t)gridDim.x * TILE;
-  uint64_t base = (uint64_t)blockIdx.x * TILE;
+  const uint64_t stride = (uint64_t)nparts * TILE;
+  uint64_t base = (uint64_t)part * TILE;
   for (; base + TILE <= nvec; base += stride) {
     V v[UNROLL];
 #pragma unroll
@@ -109,7 +110,7 @@ __device__ __forceinline__ void stream_array(const T* __restrict__ x, uint64_t n
     for (int u = 0; u < UNROLL; ++u) f.template vec<true>(v[u], ok[u], u);
     f.group_end();
   }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x < 32) {
+  if (part == nparts - 1 && threadIdx.x < 32) {
     const uint64_t tail0 = head + nvec * VE;
     const uint64_t ntail = n - tail0;  // < VE
     const int lane = threadIdx.x;
@@ -268,7 +269,7 @@ template <typename T, int UNROLL, bool CHECKED>
 __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   const T* x = static_cast<const T*>(a.x);
   InitFn<T, CHECKED> f(x[0]);
-  stream_array<T, UNROLL>(x, a.n, f);
+  stream_array<T, UNROLL>(x, a.n, f, blockIdx.x, gridDim.x);
   InitPartial p;
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
@@ -287,60 +288,39 @@ __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
 
 // ------------------------------------------------------------------------------------------
 // Step a2 (+ a4): one cutting-plane pass.
-template <typename T> constexpr int stage_cap() { return sizeof(T) == 4 ? 1024 : 512; }
+// Compaction (a4) is block-synchronous per tile: every thread keeps the flags of its
+// UNROLL*VE elements, the block scans the (lo,hi) counts (warp shuffles + one smem round), ONE
+// thread reserves the block's output ranges with one atomicAdd per half per tile, and every
+// thread then writes its elements straight to their final positions (lo half growing up from
+// z[0], hi half growing down from z[z_cap-1]).  Output order is unspecified (z is a multiset).
+struct CompactShared {
+  unsigned warp_incl[kWarps];  // per-warp inclusive totals, packed lo | hi << 16
+  unsigned warp_excl[kWarps];  // per-warp exclusive block prefix, packed
+  unsigned tot;                // group totals, packed
+  unsigned n[2];               // elements staged in the smem buffers (lo, hi)
+  unsigned long long base[2];  // reserved output offsets of a flush
+};
+// smem staging: per half 2 x (block group) elements; a half is flushed (one atomicAdd, coalesced
+// stores) once more than one group's worth is staged
+template <typename T> constexpr int stage_elems() { return 2 * kBlock * 4 * VecOf<T>::N; }
+template <typename T> constexpr size_t compact_smem_bytes() { return 2 * stage_elems<T>() * sizeof(T); }
 
 template <typename T, int MODE, int UNROLL> struct PassFn {
   static constexpr int VE = VecOf<T>::N;
-  static constexpr int CAPW = stage_cap<T>();
-  static constexpr int GROUP_MAX = 32 * UNROLL * VE;  // elements a warp can add per group
+  static constexpr int G = UNROLL * VE;  // elements per thread per group (<= 16)
   T t, yL, yR;
   unsigned c_lt, c_eq, c_lo, c_hi;
   double L_lo, L_hi, P, N;
   T pred, succ;
   T glo[UNROLL], ghi[UNROLL], gP[UNROLL], gN[UNROLL];
   // compaction (MODE == kCompact)
-  T* s_lo; T* s_hi;
-  int n_lo, n_hi;
+  T vals[G];
+  unsigned lo_bits, hi_bits;
+  CompactShared* cs;
   T* z;
   uint64_t z_cap;
   unsigned long long* cursors;
 
-  __device__ __forceinline__ void elem(T v, bool ok, int u) {
-    const bool lt = v < t;
-    const bool gt = v > t;
-    const bool lo = lt && (v > yL);
-    const bool hi = gt && (v < yR);
-    const T d = t - v;
-    if (MODE == kHot) {
-      // the hot form: no pred/succ (the driver uses them only on small compacted brackets).
-      // Written as predicated PTX so every accumulation is ONE predicated instruction
-      // (10 issue slots per element: 5 compares, 1 sub, 4 predicated adds).
-      if (ok) hot_elem(v, glo[u], ghi[u]);
-    } else if (MODE == kCompact) {
-      // ok is always true here for unmasked calls; masked calls pass ok explicitly
-      if (ok) {
-        if (lt) ++c_lt;
-        if (v == t) ++c_eq;
-        if (lo) { glo[u] += d; pred = tmax(pred, v); }
-        if (hi) { ghi[u] -= d; succ = tmin(succ, v); }
-      }
-    } else {
-      if (ok) {
-        c_lt += lt;
-        c_eq += (v == t);
-        c_lo += lo;
-        c_hi += hi;
-        if (lo) { glo[u] += d; pred = tmax(pred, v); }
-        if (hi) { ghi[u] -= d; succ = tmin(succ, v); }
-        if (lt) gN[u] += d;
-        if (gt) gP[u] -= d;
-      }
-    }
-    if (MODE == kCompact) {
-      push(ok && lo, v, s_lo, n_lo);
-      push(ok && hi, v, s_hi, n_hi);
-    }
-  }
   __device__ __forceinline__ void hot_elem(float v, float& glo_, float& ghi_) {
     asm("{\n\t.reg .pred plt, pgt, peq, plo, phi;\n\t.reg .f32 d;\n\t"
         "setp.lt.f32 plt, %4, %5;\n\t"
@@ -371,30 +351,44 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
         : "+r"(c_lt), "+r"(c_eq), "+d"(glo_), "+d"(ghi_)
         : "d"(v), "d"(t), "d"(yL), "d"(yR));
   }
-  __device__ __forceinline__ void push(bool f, T v, T* s, int& cnt) {
-    const unsigned m = __ballot_sync(FULL, f);
-    if (f) s[cnt + __popc(m & lanemask_lt())] = v;
-    cnt += __popc(m);
-  }
-  __device__ __forceinline__ void flush(T* s, int& cnt, int side) {
-    __syncwarp();
-    const int lane = threadIdx.x & 31;
-    unsigned long long base = 0;
-    if (lane == 0 && cnt) base = atomicAdd(&cursors[side], (unsigned long long)cnt);
-    base = __shfl_sync(FULL, base, 0);
-    for (int i = lane; i < cnt; i += 32) {
-      const uint64_t pos = base + (uint64_t)i;
-      if (side == 0) z[pos] = s[i];
-      else z[z_cap - 1 - pos] = s[i];
+
+  // one element; idx = position inside the thread's group (compaction bookkeeping)
+  __device__ __forceinline__ void elem(T v, bool ok, int u, int idx) {
+    if (MODE == kHot) {
+      // the hot form: no pred/succ (the driver uses them only on small compacted brackets).
+      // Predicated PTX: 10 issue slots per element (5 compares, 1 sub, 4 predicated adds).
+      if (ok) hot_elem(v, glo[u], ghi[u]);
+      return;
     }
-    __syncwarp();
-    cnt = 0;
+    const bool lt = v < t;
+    const bool gt = v > t;
+    const bool lo = ok && lt && (v > yL);
+    const bool hi = ok && gt && (v < yR);
+    const T d = t - v;
+    if (ok) {
+      if (lt) ++c_lt;
+      if (v == t) ++c_eq;
+    }
+    if (lo) { glo[u] += d; pred = tmax(pred, v); }
+    if (hi) { ghi[u] -= d; succ = tmin(succ, v); }
+    if (MODE == kDirect) {
+      if (lo) ++c_lo;
+      if (hi) ++c_hi;
+      if (ok && lt) gN[u] += d;
+      if (ok && gt) gP[u] -= d;
+    }
+    if (MODE == kCompact) {
+      vals[idx] = v;
+      lo_bits |= (unsigned)lo << idx;
+      hi_bits |= (unsigned)hi << idx;
+    }
   }
   __device__ __forceinline__ void group_begin() {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) { glo[u] = ghi[u] = T(0); if (MODE == kDirect) gP[u] = gN[u] = T(0); }
+    if (MODE == kCompact) lo_bits = hi_bits = 0u;
   }
-  __device__ __forceinline__ void group_end() {
+  __device__ __forceinline__ void sum_group() {
     // pairwise combine of the per-vector partials, then one fp64 add (R10)
     T a = glo[0], b = ghi[0], c = gP[0], d = gN[0];
     if (UNROLL == 4) {
@@ -408,45 +402,114 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
     L_lo += (double)a;
     L_hi += (double)b;
     if (MODE == kDirect) { P += (double)c; N += (double)d; }
-    if (MODE == kCompact) {
-      if (n_lo > CAPW - GROUP_MAX) flush(s_lo, n_lo, 0);
-      if (n_hi > CAPW - GROUP_MAX) flush(s_hi, n_hi, 1);
+  }
+  T* sbuf;  // smem staging: [0, CAPS) lo, [CAPS, 2 CAPS) hi
+  static constexpr int CAPS = stage_elems<T>();
+  // coalesced write-out of one staged half (all threads of the CTA call it)
+  __device__ __forceinline__ void flush(int side, unsigned cnt) {
+    if (threadIdx.x == 0) cs->base[side] = atomicAdd(&cursors[side], (unsigned long long)cnt);
+    __syncthreads();
+    const uint64_t base = cs->base[side];
+    const T* src = sbuf + side * CAPS;
+    if (side == 0) {
+      for (unsigned i = threadIdx.x; i < cnt; i += kBlock) z[base + i] = src[i];
+    } else {
+      for (unsigned i = threadIdx.x; i < cnt; i += kBlock) z[z_cap - 1 - (base + i)] = src[i];
     }
+    __syncthreads();
+  }
+  // final flush after the stream (all threads)
+  __device__ __forceinline__ void finish() {
+    __syncthreads();
+    const unsigned nlo = cs->n[0], nhi = cs->n[1];
+    if (nlo) flush(0, nlo);
+    if (nhi) flush(1, nhi);
+  }
+  // block-synchronous compaction of this group (all threads of the CTA call it): block scan of
+  // the (lo, hi) counts, scatter into the smem staging buffers, flush a half when full
+  __device__ __forceinline__ void compact_group() {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned packed = (unsigned)__popc(lo_bits) | ((unsigned)__popc(hi_bits) << 16);
+    unsigned incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) cs->warp_incl[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+      const unsigned tot = lane < kWarps ? cs->warp_incl[lane] : 0u;
+      unsigned sc = tot;
+#pragma unroll
+      for (int o = 1; o < kWarps; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, sc, o);
+        if (lane >= o) sc += y;
+      }
+      if (lane < kWarps) cs->warp_excl[lane] = sc - tot;
+      if (lane == kWarps - 1) cs->tot = sc;
+    }
+    __syncthreads();
+    const unsigned pre = cs->warp_excl[w] + (incl - packed);
+    const unsigned tot = cs->tot;
+    const unsigned n0 = cs->n[0], n1 = cs->n[1];
+    unsigned plo = n0 + (pre & 0xffffu);
+    unsigned phi = n1 + (pre >> 16);
+    T* slo = sbuf;
+    T* shi = sbuf + CAPS;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if ((lo_bits >> j) & 1u) slo[plo++] = vals[j];
+      if ((hi_bits >> j) & 1u) shi[phi++] = vals[j];
+    }
+    unsigned nlo = n0 + (tot & 0xffffu), nhi = n1 + (tot >> 16);
+    __syncthreads();
+    if (nlo > (unsigned)(CAPS / 2)) { flush(0, nlo); nlo = 0; }
+    if (nhi > (unsigned)(CAPS / 2)) { flush(1, nhi); nhi = 0; }
+    if (threadIdx.x == 0) { cs->n[0] = nlo; cs->n[1] = nhi; }
+  }
+  __device__ __forceinline__ void group_end() {
+    sum_group();
+    if (MODE == kCompact) compact_group();
   }
   template <bool MASKED, typename V> __device__ __forceinline__ void vec(const V& v, bool ok, int u) {
 #pragma unroll
-    for (int j = 0; j < VE; ++j) elem(lane_of(v, j), MASKED ? ok : true, u);
+    for (int j = 0; j < VE; ++j) elem(lane_of(v, j), MASKED ? ok : true, u, u * VE + j);
   }
+  // head/tail elements (warp 0 of the last CTA only): compaction by per-element atomics
   __device__ __forceinline__ void scalar(T v, bool ok) {
     group_begin();
-    elem(v, ok, 0);
-    group_end();
+    elem(v, ok, 0, 0);
+    sum_group();
+    if (MODE == kCompact) {
+      if (lo_bits & 1u) z[atomicAdd(&cursors[0], 1ull)] = v;
+      if (hi_bits & 1u) z[z_cap - 1 - atomicAdd(&cursors[1], 1ull)] = v;
+    }
   }
 };
 
 template <typename T, int MODE, int UNROLL>
 __global__ void __launch_bounds__(kBlock) pass_kernel(PassArgs a) {
   using Fn = PassFn<T, MODE, UNROLL>;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ CompactShared cs;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
   Fn f;
   f.t = (T)a.t; f.yL = (T)a.y_lo; f.yR = (T)a.y_hi;
   f.c_lt = f.c_eq = f.c_lo = f.c_hi = 0;
   f.L_lo = f.L_hi = f.P = f.N = 0.0;
   f.pred = -tinf<T>(); f.succ = tinf<T>();
-  f.n_lo = f.n_hi = 0;
+  f.lo_bits = f.hi_bits = 0u;
   if (MODE == kCompact) {
-    T* base = reinterpret_cast<T*>(smem_raw) + (size_t)(threadIdx.x >> 5) * 2 * Fn::CAPW;
-    f.s_lo = base;
-    f.s_hi = base + Fn::CAPW;
+    f.cs = &cs;
+    f.sbuf = reinterpret_cast<T*>(dyn_smem);
     f.z = static_cast<T*>(a.z);
     f.z_cap = a.z_cap;
     f.cursors = a.cursors;
+    if (threadIdx.x == 0) cs.n[0] = cs.n[1] = 0u;
+    __syncthreads();
   }
-  stream_array<T, UNROLL>(static_cast<const T*>(a.x), a.n, f);
-  if (MODE == kCompact) {
-    f.flush(f.s_lo, f.n_lo, 0);
-    f.flush(f.s_hi, f.n_hi, 1);
-  }
+  stream_array<T, UNROLL>(static_cast<const T*>(a.x), a.n, f, blockIdx.x, gridDim.x);
+  if (MODE == kCompact) f.finish();
   PassPartial p;
   p.c_lt = f.c_lt; p.c_eq = f.c_eq; p.c_lo = f.c_lo; p.c_hi = f.c_hi;
   p.L_lo = f.L_lo; p.L_hi = f.L_hi; p.P = f.P; p.N = f.N;
@@ -526,7 +589,7 @@ __global__ void __launch_bounds__(kBlock) hist_kernel(const T* z, uint64_t m, co
   f.mask = st->mask;
   f.shift = shift;
   f.dmask = (1u << bits) - 1u;
-  stream_array<T, 2>(z, m, f);
+  stream_array<T, 2>(z, m, f, blockIdx.x, gridDim.x);
   __syncthreads();
   for (int i = threadIdx.x; i < kBins; i += kBlock)
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
@@ -575,30 +638,219 @@ __global__ void radix_init_kernel(RadixState* st, unsigned long long r, unsigned
   st->prefix = 0; st->mask = 0; st->r = r; st->count = m; st->value = 0; st->key = 0;
 }
 
-template <typename T, int MODE, int UNROLL> constexpr size_t pass_smem() {
-  return MODE == kCompact ? (size_t)kWarps * 2 * stage_cap<T>() * sizeof(T) : 0;
-}
+template <typename T, int MODE> constexpr size_t pass_smem() { return MODE == kCompact ? compact_smem_bytes<T>() : 0; }
 
 template <typename T, int MODE>
 cudaError_t launch_pass_t(const PassArgs& a, int grid, cudaStream_t st) {
-  constexpr int U = 4;
-  constexpr size_t sm = pass_smem<T, MODE, U>();
-  pass_kernel<T, MODE, U><<<grid, kBlock, sm, st>>>(a);
+  pass_kernel<T, MODE, 4><<<grid, kBlock, pass_smem<T, MODE>(), st>>>(a);
   return cudaGetLastError();
 }
 
-template <typename T, int MODE> cudaError_t set_attrs() {
-  constexpr size_t sm = pass_smem<T, MODE, 4>();
-  if (sm > 48 * 1024)
-    return cudaFuncSetAttribute(pass_kernel<T, MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  return cudaSuccess;
+template <typename T, int MODE> cudaError_t occ_pass(int* blocks) {
+  if (pass_smem<T, MODE>() > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(pass_kernel<T, MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pass_smem<T, MODE>());
+    if (e != cudaSuccess) return e;
+  }
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, pass_kernel<T, MODE, 4>, kBlock, pass_smem<T, MODE>());
 }
 
-template <typename T, int MODE> cudaError_t occ_pass(int* blocks) {
-  cudaError_t e = set_attrs<T, MODE>();
-  if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, pass_kernel<T, MODE, 4>, kBlock,
-                                                       pass_smem<T, MODE, 4>());
+// ------------------------------------------------------------------------------------------
+// Step a8: batched selection (LMS: one k-th order statistic per column of S).  One CTA runs the
+// whole method on one column at a time (work-stealing over columns): the init reduction, the
+// Kelley iterations with the driver step on thread 0 (device-side driver, same rules as the host
+// driver), multi-level compaction into the CTA's private ping-pong buffers, and an exact finish
+// on <= 32 elements by warp-wide rank counting.
+__device__ __forceinline__ float snap_dev(double t, float yL, float yR) {
+  float f = isfinite(t) ? __double2float_rn(t) : __double2float_rn(0.5 * (double)yL + 0.5 * (double)yR);
+  if (!(f > yL)) f = nextafterf(yL, tinf<float>());
+  if (!(f < yR)) f = nextafterf(yR, -tinf<float>());
+  return f;
+}
+__device__ __forceinline__ float key_mid_dev(float yL, float yR) {
+  const unsigned a = (unsigned)okey(yL), b = (unsigned)okey(yR);
+  return (float)from_key_f32((unsigned long long)(a + (b - a) / 2));
+}
+
+struct BatchState {
+  const float* cur;
+  unsigned long long n_cur, c_le_L, c_lt_R, D_lo, m, k_r;
+  unsigned long long cursors[2];
+  double t;
+  float yL, yR, tq, result;
+  int col, on_z, slow, bisect, phase, compact, cur_buf, tgt, side, iters;
+};
+
+template <int MODE>
+__device__ __forceinline__ PassPartial batch_pass(BatchState& st, float* zbuf, uint64_t cap, float* sbuf) {
+  using Fn = PassFn<float, MODE, 4>;
+  __shared__ CompactShared cs;
+  Fn f;
+  f.sbuf = sbuf;
+  if (MODE == kCompact) {
+    if (threadIdx.x == 0) cs.n[0] = cs.n[1] = 0u;
+    __syncthreads();
+  }
+  f.t = st.tq; f.yL = st.yL; f.yR = st.yR;
+  f.c_lt = f.c_eq = f.c_lo = f.c_hi = 0;
+  f.L_lo = f.L_hi = f.P = f.N = 0.0;
+  f.pred = -tinf<float>(); f.succ = tinf<float>();
+  f.lo_bits = f.hi_bits = 0u;
+  f.cs = &cs;
+  f.z = zbuf;
+  f.z_cap = cap;
+  f.cursors = st.cursors;
+  stream_array<float, 4>(st.cur, st.n_cur, f, 0u, 1u);
+  if (MODE == kCompact) f.finish();
+  PassPartial p;
+  p.c_lt = f.c_lt; p.c_eq = f.c_eq; p.c_lo = f.c_lo; p.c_hi = f.c_hi;
+  p.L_lo = f.L_lo; p.L_hi = f.L_hi; p.P = f.P; p.N = f.N;
+  p.pred = (double)f.pred; p.succ = (double)f.succ;
+  return block_reduce(p);
+}
+
+__global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) {
+  __shared__ BatchState st;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  float* sbuf = reinterpret_cast<float*>(dyn_smem);
+  const uint64_t n = a.n, k = a.k;
+  float* my0 = a.scratch + (size_t)blockIdx.x * 2 * a.cap;
+  float* my1 = my0 + a.cap;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      st.col = (int)atomicAdd(a.next_col, 1u);
+      st.cursors[0] = st.cursors[1] = 0ull;
+    }
+    __syncthreads();
+    if (st.col >= (int)a.C) break;
+    const float* x = a.S + (size_t)st.col * n;
+    // ---- a1: init reduction over the column
+    {
+      InitFn<float, true> f(x[0]);
+      stream_array<float, 4>(x, n, f, 0u, 1u);
+      InitPartial p;
+      p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
+      p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
+      p = block_reduce(p);
+      if (threadIdx.x == 0) {
+        st.phase = 0;
+        st.iters = 0;
+        atomicAdd(&a.stats[0], 1ull);
+        atomicAdd(&a.stats[1], (unsigned long long)(4 * n));
+        if (p.nonfinite) {
+          st.result = __int_as_float(0x7fc00000);
+          atomicAdd(&a.stats[3], 1ull);
+          st.phase = 1;
+        } else if (k <= p.cnt_min) {
+          st.result = (float)p.vmin; st.phase = 1;
+        } else if (k > n - p.cnt_max) {
+          st.result = (float)p.vmax; st.phase = 1;
+        } else {
+          st.yL = (float)p.vmin; st.yR = (float)p.vmax;
+          st.c_le_L = p.cnt_min; st.c_lt_R = n - p.cnt_max;
+          st.m = st.c_lt_R - st.c_le_L;
+          st.D_lo = 0; st.on_z = 0; st.slow = 0; st.bisect = 0;
+          st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
+          const double x0 = (double)x[0];
+          st.t = x0 + (p.S - (double)p.cnt_min * (p.vmin - x0) - (double)p.cnt_max * (p.vmax - x0)) / (double)st.m;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- a2/a3/a4: Kelley iterations
+    while (st.phase == 0) {
+      if (threadIdx.x == 0) {
+        const double tt = st.bisect ? (double)key_mid_dev(st.yL, st.yR) : st.t;
+        st.tq = snap_dev(tt, st.yL, st.yR);
+        st.compact = st.on_z || st.m <= a.cap;
+        st.tgt = (st.cur_buf == 0) ? 1 : 0;
+      }
+      __syncthreads();
+      float* zbuf = st.tgt == 0 ? my0 : my1;
+      PassPartial tot = st.compact ? batch_pass<kCompact>(st, zbuf, a.cap, sbuf) : batch_pass<kHot>(st, zbuf, a.cap, sbuf);
+      __syncthreads();  // compaction cursors complete
+      if (threadIdx.x == 0) {
+        const unsigned long long zl = st.cursors[0], zh = st.cursors[1];
+        st.cursors[0] = st.cursors[1] = 0ull;
+        atomicAdd(&a.stats[0], 1ull);
+        atomicAdd(&a.stats[1], (unsigned long long)(4 * (st.n_cur + (st.compact ? zl + zh : 0))));
+        const unsigned long long c_lt = st.D_lo + tot.c_lt, c_le = c_lt + tot.c_eq;
+        const float tq = st.tq;
+        const unsigned long long m_old = st.m;
+        if (++st.iters > (int)a.max_iters) {
+          st.result = __int_as_float(0x7fc00000);
+          atomicAdd(&a.stats[2], 1ull);
+          st.phase = 1;
+        } else if (c_lt < k && k <= c_le) {
+          st.result = tq; st.phase = 1;
+        } else if (c_le < k) {
+          const unsigned long long c_hi = st.c_lt_R - c_le;
+          if (c_le + 1 == k && isfinite(tot.succ)) {
+            st.result = (float)tot.succ; st.phase = 1;
+          } else {
+            st.yL = tq; st.c_le_L = c_le; st.m = c_hi;
+            st.t = (double)tq + tot.L_hi / (double)c_hi;
+            st.side = 1;
+          }
+        } else {
+          const unsigned long long c_lo = c_lt - st.c_le_L;
+          if (c_lt == k && isfinite(tot.pred)) {
+            st.result = (float)tot.pred; st.phase = 1;
+          } else {
+            st.yR = tq; st.c_lt_R = c_lt; st.m = c_lo;
+            st.t = (double)tq - tot.L_lo / (double)c_lo;
+            st.side = 0;
+          }
+        }
+        if (st.phase == 0) {
+          if (st.compact) {
+            float* base = st.tgt == 0 ? my0 : my1;
+            st.cur = st.side == 0 ? base : base + (a.cap - zh);
+            st.n_cur = st.side == 0 ? zl : zh;
+            st.cur_buf = st.tgt;
+            st.D_lo = st.c_le_L;
+            st.on_z = 1;
+            if (st.m <= 32) {
+              st.k_r = k - st.c_le_L;  // rank inside the kept half
+              st.phase = 2;
+            }
+          }
+          if (st.m > m_old - m_old / 8) {
+            if (++st.slow >= 2) st.bisect = 1;
+          } else {
+            st.slow = 0;
+            st.bisect = 0;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- a5: exact finish on <= 32 elements (warp 0 counts ranks)
+    if (st.phase == 2 && threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      const int cnt = (int)st.n_cur;
+      const float v = lane < cnt ? st.cur[lane] : tinf<float>();
+      unsigned below = 0, le = 0;
+      for (int j = 0; j < cnt; ++j) {
+        const float w = __shfl_sync(FULL, v, j);
+        below += (w < v);
+        le += (w <= v);
+      }
+      const bool mine = lane < cnt && below < st.k_r && st.k_r <= le;
+      const unsigned who = __ballot_sync(FULL, mine);
+      const float sel = __shfl_sync(FULL, v, who ? __ffs(who) - 1 : 0);
+      if (lane == 0) {
+        st.result = who ? sel : __int_as_float(0x7fc00000);
+        if (!who) atomicAdd(&a.stats[2], 1ull);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const float r = st.result;
+      a.out[st.col] = r == 0.0f ? 0.0f : r;  // canonical +0 (R13)
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace
@@ -695,4 +947,21 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   return cudaGetLastError();
 }
 
+}  // namespace cpsel
+
+namespace cpsel {
+cudaError_t launch_batched_select(const BatchArgs& a, int grid, cudaStream_t st) {
+  constexpr size_t sm = compact_smem_bytes<float>();
+  cudaError_t e = cudaFuncSetAttribute(batched_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  batched_select_kernel<<<grid, kBlock, sm, st>>>(a);
+  return cudaGetLastError();
+}
+int batched_blocks_per_sm() {
+  constexpr size_t sm = compact_smem_bytes<float>();
+  cudaFuncSetAttribute(batched_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int b = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, batched_select_kernel, kBlock, sm);
+  return b > 0 ? b : 1;
+}
 }  // namespace cpsel

@@ -89,4 +89,20 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned int* hist, const LaunchShape& s, cudaStream_t st);
 
+// Step a8: per-column k-th smallest of S (n x C column-major, float32), one CTA per column.
+struct BatchArgs {
+  const float* S;
+  uint64_t n;
+  uint32_t C;
+  uint64_t k;
+  float* out;                  // device, C results
+  float* scratch;              // grid x 2 x cap floats (per-CTA ping-pong compaction buffers)
+  uint64_t cap;                // elements per buffer; a column compacts once its interior <= cap
+  unsigned* next_col;          // work counter, zero on entry
+  unsigned long long* stats;   // [0] passes, [1] bytes, [2] safeguard trips, [3] non-finite columns
+  uint32_t max_iters;
+};
+cudaError_t launch_batched_select(const BatchArgs& a, int grid, cudaStream_t st);
+int batched_blocks_per_sm();
+
 }  // namespace cpsel

@@ -11,8 +11,10 @@ constexpr int kLmsMaxP = 16;
 struct LmsWorkspace {
   float* S = nullptr;          // n x C column-major squared residuals (cpsel_lms_objective)
   size_t S_bytes = 0;
-  void* dev = nullptr;         // batched-driver device state
+  void* dev = nullptr;         // batched-select scratch (per-CTA ping-pong buffers) + counters
   size_t dev_bytes = 0;
+  void* img = nullptr;         // packed TF32 hi/lo operand images of X and Theta
+  size_t img_bytes = 0;
   void* host = nullptr;        // pinned mirror
   size_t host_bytes = 0;
 };
