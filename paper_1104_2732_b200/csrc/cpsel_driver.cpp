@@ -568,7 +568,10 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     inf.passes++;
     inf.cp_iters++;
     inf.bytes_moved += be.scanned * es + (compact ? (zl + zh) * es : 0);
-    const uint64_t c_lt = D_lo + s.c_lt, c_le = c_lt + s.c_eq;  // global counts at t
+    // global counts at t; a compaction pass carries no counters: they follow exactly from the
+    // compaction totals (#lo = #{yL<x<t}, #hi = #{t<x<yR}, and every x == t is interior)
+    const uint64_t c_lt = compact ? c_le_L + zl : D_lo + s.c_lt;
+    const uint64_t c_le = compact ? c_lt + (m - zl - zh) : c_lt + s.c_eq;
     // F_k(t) from positive terms only (App. A identities; Eq. 2 with paper-k = n-k+1, R2)
     const long double N_t = N_L + (long double)c_le_L * ((long double)tq - yL) + s.L_lo;
     const long double P_t = P_R + (long double)(n - c_lt_R) * ((long double)yR - tq) + s.L_hi;

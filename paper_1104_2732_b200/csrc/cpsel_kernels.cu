@@ -302,7 +302,8 @@ struct CompactShared {
 };
 // smem staging: per half 2 x (block group) elements; a half is flushed (one atomicAdd, coalesced
 // stores) once more than one group's worth is staged
-template <typename T> constexpr int stage_elems() { return 2 * kBlock * 4 * VecOf<T>::N; }
+template <typename T> __host__ __device__ constexpr int group_elems() { return kBlock * 4 * VecOf<T>::N; }
+template <typename T> __host__ __device__ constexpr int stage_elems() { return group_elems<T>() + group_elems<T>() / 2; }
 template <typename T> constexpr size_t compact_smem_bytes() { return 2 * stage_elems<T>() * sizeof(T); }
 
 template <typename T, int MODE, int UNROLL> struct PassFn {
@@ -352,12 +353,47 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
         : "d"(v), "d"(t), "d"(yL), "d"(yR));
   }
 
+  __device__ __forceinline__ void compact_elem(float v, float& glo_, float& ghi_, int idx) {
+    asm("{\n\t.reg .pred plt, pgt, plo, phi;\n\t.reg .f32 d;\n\t"
+        "setp.lt.f32 plt, %4, %5;\n\t"
+        "setp.gt.f32 pgt, %4, %5;\n\t"
+        "setp.gt.and.f32 plo, %4, %6, plt;\n\t"
+        "setp.lt.and.f32 phi, %4, %7, pgt;\n\t"
+        "sub.rn.f32 d, %5, %4;\n\t"
+        "@plo add.rn.f32 %0, %0, d;\n\t"
+        "@phi sub.rn.f32 %1, %1, d;\n\t"
+        "@plo or.b32 %2, %2, %8;\n\t"
+        "@phi or.b32 %3, %3, %8;\n\t}"
+        : "+f"(glo_), "+f"(ghi_), "+r"(lo_bits), "+r"(hi_bits)
+        : "f"(v), "f"(t), "f"(yL), "f"(yR), "r"(1u << idx));
+  }
+  __device__ __forceinline__ void compact_elem(double v, double& glo_, double& ghi_, int idx) {
+    asm("{\n\t.reg .pred plt, pgt, plo, phi;\n\t.reg .f64 d;\n\t"
+        "setp.lt.f64 plt, %4, %5;\n\t"
+        "setp.gt.f64 pgt, %4, %5;\n\t"
+        "setp.gt.and.f64 plo, %4, %6, plt;\n\t"
+        "setp.lt.and.f64 phi, %4, %7, pgt;\n\t"
+        "sub.rn.f64 d, %5, %4;\n\t"
+        "@plo add.rn.f64 %0, %0, d;\n\t"
+        "@phi sub.rn.f64 %1, %1, d;\n\t"
+        "@plo or.b32 %2, %2, %8;\n\t"
+        "@phi or.b32 %3, %3, %8;\n\t}"
+        : "+d"(glo_), "+d"(ghi_), "+r"(lo_bits), "+r"(hi_bits)
+        : "d"(v), "d"(t), "d"(yL), "d"(yR), "r"(1u << idx));
+  }
   // one element; idx = position inside the thread's group (compaction bookkeeping)
   __device__ __forceinline__ void elem(T v, bool ok, int u, int idx) {
     if (MODE == kHot) {
       // the hot form: no pred/succ (the driver uses them only on small compacted brackets).
       // Predicated PTX: 10 issue slots per element (5 compares, 1 sub, 4 predicated adds).
       if (ok) hot_elem(v, glo[u], ghi[u]);
+      return;
+    }
+    if (MODE == kCompact) {
+      // compaction form: no counters (the driver derives c_lt = c_le(yL) + #lo and
+      // c_eq = m - #lo - #hi from the compaction totals), no pred/succ; 9 issue slots
+      if (ok) compact_elem(v, glo[u], ghi[u], idx);
+      vals[idx] = v;
       return;
     }
     const bool lt = v < t;
@@ -376,11 +412,6 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
       if (hi) ++c_hi;
       if (ok && lt) gN[u] += d;
       if (ok && gt) gP[u] -= d;
-    }
-    if (MODE == kCompact) {
-      vals[idx] = v;
-      lo_bits |= (unsigned)lo << idx;
-      hi_bits |= (unsigned)hi << idx;
     }
   }
   __device__ __forceinline__ void group_begin() {
@@ -418,12 +449,13 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
     }
     __syncthreads();
   }
+  unsigned n_lo = 0, n_hi = 0;  // staged counts (block-uniform, kept in every thread)
   // final flush after the stream (all threads)
   __device__ __forceinline__ void finish() {
     __syncthreads();
-    const unsigned nlo = cs->n[0], nhi = cs->n[1];
-    if (nlo) flush(0, nlo);
-    if (nhi) flush(1, nhi);
+    if (n_lo) flush(0, n_lo);
+    if (n_hi) flush(1, n_hi);
+    n_lo = n_hi = 0;
   }
   // block-synchronous compaction of this group (all threads of the CTA call it): block scan of
   // the (lo, hi) counts, scatter into the smem staging buffers, flush a half when full
@@ -452,9 +484,8 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
     __syncthreads();
     const unsigned pre = cs->warp_excl[w] + (incl - packed);
     const unsigned tot = cs->tot;
-    const unsigned n0 = cs->n[0], n1 = cs->n[1];
-    unsigned plo = n0 + (pre & 0xffffu);
-    unsigned phi = n1 + (pre >> 16);
+    unsigned plo = n_lo + (pre & 0xffffu);
+    unsigned phi = n_hi + (pre >> 16);
     T* slo = sbuf;
     T* shi = sbuf + CAPS;
 #pragma unroll
@@ -462,11 +493,15 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
       if ((lo_bits >> j) & 1u) slo[plo++] = vals[j];
       if ((hi_bits >> j) & 1u) shi[phi++] = vals[j];
     }
-    unsigned nlo = n0 + (tot & 0xffffu), nhi = n1 + (tot >> 16);
-    __syncthreads();
-    if (nlo > (unsigned)(CAPS / 2)) { flush(0, nlo); nlo = 0; }
-    if (nhi > (unsigned)(CAPS / 2)) { flush(1, nhi); nhi = 0; }
-    if (threadIdx.x == 0) { cs->n[0] = nlo; cs->n[1] = nhi; }
+    n_lo += tot & 0xffffu;
+    n_hi += tot >> 16;
+    // a flush is due once another full group might not fit
+    constexpr unsigned THR = (unsigned)(CAPS - group_elems<T>());
+    if (n_lo > THR || n_hi > THR) {
+      __syncthreads();  // staged writes visible
+      if (n_lo > THR) { flush(0, n_lo); n_lo = 0; }
+      if (n_hi > THR) { flush(1, n_hi); n_hi = 0; }
+    }
   }
   __device__ __forceinline__ void group_end() {
     sum_group();
@@ -484,6 +519,7 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
     if (MODE == kCompact) {
       if (lo_bits & 1u) z[atomicAdd(&cursors[0], 1ull)] = v;
       if (hi_bits & 1u) z[z_cap - 1 - atomicAdd(&cursors[1], 1ull)] = v;
+      lo_bits = hi_bits = 0u;
     }
   }
 };
@@ -774,7 +810,9 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
         st.cursors[0] = st.cursors[1] = 0ull;
         atomicAdd(&a.stats[0], 1ull);
         atomicAdd(&a.stats[1], (unsigned long long)(4 * (st.n_cur + (st.compact ? zl + zh : 0))));
-        const unsigned long long c_lt = st.D_lo + tot.c_lt, c_le = c_lt + tot.c_eq;
+        // compaction passes carry no counters: derive them from the compaction totals
+        const unsigned long long c_lt = st.compact ? st.c_le_L + zl : st.D_lo + tot.c_lt;
+        const unsigned long long c_le = st.compact ? c_lt + (st.m - zl - zh) : c_lt + tot.c_eq;
         const float tq = st.tq;
         const unsigned long long m_old = st.m;
         if (++st.iters > (int)a.max_iters) {

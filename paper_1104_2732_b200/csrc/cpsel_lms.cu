@@ -11,9 +11,10 @@
 //             hi*hi + hi*lo + lo*hi for each K-half (3xTF32, ~fp32-accurate products), into one of
 //             two TMEM accumulators (2 x 256 columns), then tcgen05.commit to the smem-empty and the
 //             TMEM-full barriers;
-//   warps 2-5: epilogue — tcgen05.ld 32x32b.x32 (TMEM lane = row), r = acc - y_i, s = r*r, and a
-//             coalesced store into column-major S (each warp-store = 32 consecutive rows of one
-//             column = 128 B), then arrive on the TMEM-empty barrier.
+//   warps 2-9: epilogue — two warps per TMEM lane quarter, each on 128 of the 256 columns:
+//             tcgen05.ld 32x32b.x32 (TMEM lane = row), r = acc - y_i, s = r*r, and a coalesced
+//             store into column-major S (each warp-store = 32 consecutive rows of one column =
+//             128 B, pointer-stepped by n), then arrive on the TMEM-empty barrier.
 // The stage is HBM-write bound (4 bytes of S per 2p flops); the tensor cores keep the contraction
 // off the FP32 pipes so the epilogue can stream S at full bandwidth.
 #include <cstdint>
@@ -32,7 +33,8 @@ constexpr int B_HALF = TN * KP * 4;  // 16 KB
 constexpr int A_IMG = 2 * A_HALF;    // 16 KB per M tile
 constexpr int B_IMG = 2 * B_HALF;    // 32 KB per N tile
 constexpr int STAGE = A_IMG + B_IMG; // 48 KB
-constexpr int kThreads = 192;        // 6 warps
+constexpr int kEpiWarps = 8;         // 2 per TMEM lane quarter, each on half of the 256 columns
+constexpr int kThreads = 32 * (2 + kEpiWarps);
 
 // byte offset of element (row, k) in a K-major no-swizzle core-matrix image
 __host__ __device__ constexpr uint32_t core_off(int row, int k) {
@@ -150,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1) residual_tc_kernel(ResidualArgs a
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);
+      mbar_init(&tempty[i], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -202,8 +204,9 @@ __global__ void __launch_bounds__(kThreads, 1) residual_tc_kernel(ResidualArgs a
       __syncwarp();
     }
   } else {
-    // ---------------- epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    // ---------------- epilogue: warps 2..9 -> TMEM lane quarter (warp % 4), column half
     const int q = warp & 3;
+    const uint32_t cbeg = (uint32_t)((warp - 2) >> 2) * (TN / 2);
     uint32_t it = 0;
     for (uint32_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const uint32_t s = it & 1, ph = (it >> 1) & 1;
@@ -211,22 +214,31 @@ __global__ void __launch_bounds__(kThreads, 1) residual_tc_kernel(ResidualArgs a
       const uint64_t row = (uint64_t)mt * TM + q * 32 + lane;
       const bool row_ok = row < a.n;
       const float yi = row_ok ? a.y[row] : 0.f;
+      const uint32_t col_first = nt * TN + cbeg;
+      const bool full = col_first + TN / 2 <= a.C;
+      float* p = a.S + (size_t)col_first * a.n + row;
       mbar_wait(&tfull[s], ph);
       asm volatile("tcgen05.fence::after_thread_sync;");
-      const uint32_t col0 = nt * TN;
-      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * TN;
+      const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * TN + cbeg;
 #pragma unroll 1
-      for (int c0 = 0; c0 < TN; c0 += 32) {
+      for (uint32_t c0 = 0; c0 < TN / 2; c0 += 32) {
         uint32_t r[32];
         TMEM_LD32(taddr + c0, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (row_ok) {
+          if (full) {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const uint32_t col = col0 + c0 + j;
-            if (col < a.C) {
+            for (int j = 0; j < 32; ++j) {
               const float res = __uint_as_float(r[j]) - yi;
-              a.S[(size_t)col * a.n + row] = res * res;
+              __stcs(p, res * res);
+              p += a.n;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              const float res = __uint_as_float(r[j]) - yi;
+              if (col_first + c0 + j < a.C) __stcs(p, res * res);
+              p += a.n;
             }
           }
         }
