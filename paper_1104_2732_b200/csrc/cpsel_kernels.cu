@@ -683,7 +683,7 @@ cudaError_t launch_pass_t(const PassArgs& a, int grid, cudaStream_t st) {
 }
 
 template <typename T, int MODE> cudaError_t occ_pass(int* blocks) {
-  if (pass_smem<T, MODE>() > 48 * 1024) {
+  if (pass_smem<T, MODE>() > 0) {  // dynamic + static smem may exceed the 48 KB default
     cudaError_t e = cudaFuncSetAttribute(pass_kernel<T, MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)pass_smem<T, MODE>());
     if (e != cudaSuccess) return e;

@@ -112,5 +112,5 @@ def test_lms_config4_full_size(cp):
         assert got[j] == O.order_statistic(col, k)
     del S
     torch.cuda.empty_cache()
-    # candidates with the smallest perturbation fit best (LMS is minimised near theta*)
-    assert np.argmin(got) < 1024
+    # candidates with the smallest perturbations (sigma ~ 1e-3) fit far better than sigma ~ 1
+    assert got[:64].max() < got[-64:].min()
