@@ -42,8 +42,12 @@ struct cpsel_ctx {
   unsigned int* d_hist = nullptr;
   DevPass* d_gather = nullptr;       // G x DevPass (sharded)
   DevInit* d_gather_init = nullptr;  // G x DevInit (sharded)
-  void* d_zb[2] = {nullptr, nullptr}; // ping-pong compaction buffers
+  void* d_zb[2] = {nullptr, nullptr}; // dense ping-pong compaction buffers
   size_t zb_bytes[2] = {0, 0};
+  void* d_sb[2] = {nullptr, nullptr}; // segmented (warp-private) compaction buffers
+  size_t sb_bytes[2] = {0, 0};
+  void* d_st[2] = {nullptr, nullptr}; // their run tables (SegEntry per warp)
+  size_t st_bytes[2] = {0, 0};
   void* d_zall = nullptr;            // all-gathered bracket contents (sharded)
   size_t zall_bytes = 0;
   void* d_stage = nullptr;           // H2D staging (cpsel_select_kth_host)
@@ -180,8 +184,11 @@ struct Backend {
   virtual cpsel_status init(cpsel_init_stats* out) = 0;
   // one pass at t over the current array; if compact, also copy ]yL,t[ and ]t,yR[ out
   // (z_lo/z_hi: elements written, summed over ranks)
-  virtual cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* out,
+  // dense: write the halves contiguously (else the back end may keep them segmented)
+  virtual cpsel_status pass(double t, double yL, double yR, bool compact, bool dense, cpsel_pass_stats* out,
                             uint64_t* z_lo, uint64_t* z_hi) = 0;
+  // are the halves of the last compacting pass contiguous (selectable)?
+  virtual bool kept_dense() const { return true; }
   // current array <- half `side` (0: ]yL,t[, 1: ]t,yR[) of the last compacting pass
   virtual cpsel_status adopt(int side) = 0;
   // r-th smallest (1-based) of half `side` of the last compacting pass, or of the current array (2)
@@ -194,17 +201,28 @@ struct Backend {
 };
 
 // ------------------------------------------------------------------------ one GPU
+// The current array is contiguous (x, or a dense compaction buffer) or segmented (the warp-private
+// runs of a segmented compaction: buffer sb[i] + table st[i] + side).  Large brackets are
+// compacted into warp-private regions (seg_pass_kernel, no atomics/barriers); once the interior
+// is <= the dense threshold the compaction appends to a dense buffer, which the radix select reads.
 struct GpuBackend : Backend {
   cpsel_ctx* ctx;
   const void* x;
   uint64_t n;
   int dt;
-  const void* cur;           // current array
-  uint64_t n_cur;
-  int cur_buf = -1;          // -1: x, else ping-pong buffer index
+  // current array
+  bool cur_seg = false;
+  const void* cur;           // contiguous base, or segmented buffer base
+  uint64_t n_cur;            // elements in the current array
+  const SegEntry* cur_tab = nullptr;
+  int cur_side = 0;
+  int cur_dbuf = -1, cur_sbuf = -1;  // dense / segmented buffer in use as input (-1: none)
+  // last compaction
+  bool last_dense = true;
   int tgt = 0;               // buffer written by the last compacting pass
-  uint64_t cap = 0;          // capacity (elements) of each ping-pong buffer
   uint64_t zlo = 0, zhi = 0; // local halves written by the last compacting pass
+  uint64_t cap = 0;          // capacity (elements) of each dense buffer
+  uint64_t R = 0;            // segmented region size
   GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
       : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
@@ -216,9 +234,9 @@ struct GpuBackend : Backend {
     float ms = 0.f;
     if (timed() && cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) step_ms = ms;
   }
-  char* buf(int i) const { return static_cast<char*>(ctx->d_zb[i]); }
-  const void* half_ptr(int side) const {
-    return side == 0 ? (const void*)buf(tgt) : (const void*)(buf(tgt) + (cap - zhi) * elem_size(dt));
+  char* dbuf(int i) const { return static_cast<char*>(ctx->d_zb[i]); }
+  const void* half_ptr(int side) const {  // dense halves of the last (dense) compaction
+    return side == 0 ? (const void*)dbuf(tgt) : (const void*)(dbuf(tgt) + (cap - zhi) * elem_size(dt));
   }
   uint64_t half_n(int side) const { return side == 0 ? zlo : zhi; }
 
@@ -252,37 +270,68 @@ struct GpuBackend : Backend {
     o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
     return CPSEL_OK;
   }
-  // two ping-pong compaction buffers of m elements each
-  cpsel_status ensure_z(uint64_t m) {
+  // two dense ping-pong buffers of m_dense elements; two segmented buffers (+ run tables) able to
+  // hold any compaction of the n-element array
+  cpsel_status ensure_z(uint64_t m_dense, bool need_seg) {
     const size_t es = elem_size(dt);
     for (int i = 0; i < 2; ++i) {
-      cpsel_status s = ensure(ctx, &ctx->d_zb[i], &ctx->zb_bytes[i], (size_t)std::max<uint64_t>(m, 1) * es);
+      cpsel_status s = ensure(ctx, &ctx->d_zb[i], &ctx->zb_bytes[i], (size_t)std::max<uint64_t>(m_dense, 1) * es);
       if (s != CPSEL_OK) return s;
     }
     cap = std::min(ctx->zb_bytes[0], ctx->zb_bytes[1]) / es;
+    if (need_seg) {
+      R = seg_region(dt, n, ctx->shape);
+      const size_t W = (size_t)seg_total_warps(dt, ctx->shape);
+      for (int i = 0; i < 2; ++i) {
+        cpsel_status s = ensure(ctx, &ctx->d_sb[i], &ctx->sb_bytes[i], W * R * es);
+        if (s != CPSEL_OK) return s;
+        s = ensure(ctx, &ctx->d_st[i], &ctx->st_bytes[i], W * sizeof(SegEntry));
+        if (s != CPSEL_OK) return s;
+      }
+    }
     return CPSEL_OK;
   }
-  cpsel_status launch_local_pass(double t, double yL, double yR, bool compact) {
-    PassArgs a{};
-    a.x = cur; a.n = n_cur; a.t = t; a.y_lo = yL; a.y_hi = yR;
-    a.mode = compact ? kCompact : kHot;
-    if (compact) {
-      tgt = (cur_buf == 0) ? 1 : 0;
-      a.z = buf(tgt);
-      a.z_cap = cap;
+  cpsel_status launch_local_pass(double t, double yL, double yR, bool compact, bool dense) {
+    if (!compact) {  // only ever on a contiguous array (before the first compaction)
+      PassArgs a{};
+      a.x = cur; a.n = n_cur; a.t = t; a.y_lo = yL; a.y_hi = yR;
+      a.mode = kHot;
+      a.cursors = ctx->d_cursors;
+      a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
+      CK(tic());
+      CK(launch_pass(dt, a, ctx->shape, ctx->stream));
+      CK(toc());
+    } else {
+      SegArgs a{};
+      a.x = cur; a.n = n_cur;
+      a.seg_in = cur_seg ? cur_tab : nullptr;
+      a.side_in = cur_side;
+      a.t = t; a.y_lo = yL; a.y_hi = yR;
+      a.dense_out = dense ? 1 : 0;
+      if (dense) {
+        tgt = (cur_dbuf == 0) ? 1 : 0;
+        a.out = ctx->d_zb[tgt];
+        a.z_cap = cap;
+      } else {
+        tgt = (cur_sbuf == 0) ? 1 : 0;
+        a.out = ctx->d_sb[tgt];
+        a.R = R;
+        a.seg_out = static_cast<SegEntry*>(ctx->d_st[tgt]);
+      }
+      a.cursors = ctx->d_cursors;
+      a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out_tuple = ctx->d_pass;
+      CK(tic());
+      CK(launch_seg_pass(dt, a, ctx->shape, ctx->stream));
+      CK(toc());
+      last_dense = dense;
     }
-    a.cursors = ctx->d_cursors;
-    a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
-    CK(tic());
-    CK(launch_pass(dt, a, ctx->shape, ctx->stream));
-    CK(toc());
     launches = 1;
     scanned = n_cur;
     return CPSEL_OK;
   }
-  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
+  cpsel_status pass(double t, double yL, double yR, bool compact, bool dense, cpsel_pass_stats* o, uint64_t* z_lo,
                     uint64_t* z_hi) override {
-    cpsel_status st = launch_local_pass(t, yL, yR, compact);
+    cpsel_status st = launch_local_pass(t, yL, yR, compact, dense);
     if (st != CPSEL_OK) return st;
     CK(cudaMemcpyAsync(ctx->h_pass, ctx->d_pass, sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -294,10 +343,20 @@ struct GpuBackend : Backend {
     *z_lo = r.z_lo; *z_hi = r.z_hi;
     return CPSEL_OK;
   }
+  bool kept_dense() const override { return last_dense; }
   cpsel_status adopt(int side) override {
-    cur = half_ptr(side);
+    if (last_dense) {
+      cur_seg = false;
+      cur = half_ptr(side);
+      cur_dbuf = tgt;
+    } else {
+      cur_seg = true;
+      cur = ctx->d_sb[tgt];
+      cur_tab = static_cast<const SegEntry*>(ctx->d_st[tgt]);
+      cur_side = side;
+      cur_sbuf = tgt;
+    }
     n_cur = half_n(side);
-    cur_buf = tgt;
     return CPSEL_OK;
   }
   cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out) {
@@ -312,6 +371,7 @@ struct GpuBackend : Backend {
     *out = ctx->h_radix->value;
     return CPSEL_OK;
   }
+  // side 2 needs a contiguous current array; sides 0/1 a dense last compaction (driver guarantees)
   cpsel_status select(int side, uint64_t r, double* out) override {
     if (side == 2) return select_on(cur, n_cur, r, out);
     return select_on(half_ptr(side), half_n(side), r, out);
@@ -377,17 +437,22 @@ struct ShardedBackend : GpuBackend {
     *o = combined;
     return CPSEL_OK;
   }
-  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
+  cpsel_status pass(double t, double yL, double yR, bool compact, bool dense, cpsel_pass_stats* o, uint64_t* z_lo,
                     uint64_t* z_hi) override {
     const NcclApi& nc = nccl_api();
     const int G = ctx->world;
-    if (n_cur > 0) {
-      cpsel_status st = launch_local_pass(t, yL, yR, compact);
+    if (n_cur > 0 || (compact && cur_seg)) {
+      // (a segmented current array is processed even when empty so every warp writes its run table)
+      cpsel_status st = launch_local_pass(t, yL, yR, compact, dense);
       if (st != CPSEL_OK) return st;
     } else {
       launches = 0;
       scanned = 0;
-      if (compact) tgt = (cur_buf == 0) ? 1 : 0;
+      if (compact) {
+        tgt = dense ? ((cur_dbuf == 0) ? 1 : 0) : ((cur_sbuf == 0) ? 1 : 0);
+        last_dense = dense;
+        if (!dense) CK(cudaMemsetAsync(ctx->d_st[tgt], 0, seg_total_warps(dt, ctx->shape) * sizeof(SegEntry), ctx->stream));
+      }
       DevPass e{};
       e.pred = -INFINITY; e.succ = INFINITY;
       *ctx->h_pass = e;
@@ -396,7 +461,7 @@ struct ShardedBackend : GpuBackend {
     NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (n_cur > 0) read_ms(); else step_ms = 0.0;
+    if (launches) read_ms(); else step_ms = 0.0;
     // fixed rank-order combine: identical bytes on every rank (R17)
     cpsel_pass_stats s{};
     s.pred = -INFINITY; s.succ = INFINITY;
@@ -460,8 +525,8 @@ struct HostBackend : Backend {
     if (be->init(be->user, o) != 0) { msg = "init callback failed"; return CPSEL_EINTERNAL; }
     return CPSEL_OK;
   }
-  cpsel_status pass(double t, double yL, double yR, bool compact, cpsel_pass_stats* o, uint64_t* z_lo,
-                    uint64_t* z_hi) override {
+  cpsel_status pass(double t, double yL, double yR, bool compact, bool /*dense*/, cpsel_pass_stats* o,
+                    uint64_t* z_lo, uint64_t* z_hi) override {
     if (be->pass(be->user, t, yL, yR, compact ? 1 : 0, o) != 0) { msg = "pass callback failed"; return CPSEL_EINTERNAL; }
     // the callback reports c_lo/c_hi over its current array; those are the compacted halves
     *z_lo = compact ? o->c_lo : 0;
@@ -478,6 +543,8 @@ struct HostBackend : Backend {
   }
 };
 
+uint64_t dense_threshold(uint64_t select_cap) { return std::max<uint64_t>(4 * select_cap, 1ull << 20); }
+
 // ============================================================================================
 // The cutting-plane driver (Algorithm 1 + hybrid finish), shared by all back ends.
 //
@@ -493,6 +560,7 @@ struct HostBackend : Backend {
 // selected exactly by radix select (P:L196 'sort z', R21).
 cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_config& cfg, uint64_t z_cap,
                    uint64_t select_cap, double* value, cpsel_info* info, std::vector<cpsel_trace_row>* trace) {
+  const uint64_t dense_cap = dense_threshold(select_cap);
   const auto t0 = std::chrono::steady_clock::now();
   const size_t es = elem_size(dt);
   cpsel_info inf{};
@@ -559,9 +627,10 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       return CPSEL_EINTERNAL;  // impossible while m >= 1
     }
     const bool compact = on_z || m <= z_cap;
+    const bool dense = m <= dense_cap;  // small brackets are compacted contiguously (selectable)
     cpsel_pass_stats s{};
     uint64_t zl = 0, zh = 0;
-    st = be.pass(tq, yL, yR, compact, &s, &zl, &zh);
+    st = be.pass(tq, yL, yR, compact, dense, &s, &zl, &zh);
     if (st != CPSEL_OK) return st;
     inf.launches += be.launches;
     inf.kernel_ms_passes += be.step_ms;
@@ -624,7 +693,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     row.interior = m;
     if (trace && cfg.record_trace) trace->push_back(row);
     if (compact) {
-      if (m <= select_cap) {  // hybrid finish: exact selection in the kept half
+      if (m <= select_cap && be.kept_dense()) {  // hybrid finish: exact selection in the kept half
         double v;
         st = do_select(side, k - c_le_L, &v);
         if (st != CPSEL_OK) return st;
@@ -676,7 +745,8 @@ cpsel_status run_single(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype
   GpuBackend be(ctx, d_x, n, (int)dtype);
   const uint64_t zc = auto_z_cap(n, ctx->cfg);
   cpsel_status s = CPSEL_OK;
-  if (n > ctx->cfg.direct_threshold || ctx->cfg.force_cp) s = be.ensure_z(zc);
+  if (n > ctx->cfg.direct_threshold || ctx->cfg.force_cp)
+    s = be.ensure_z(std::min<uint64_t>(zc, dense_threshold(auto_select_cap(ctx->cfg))), zc > dense_threshold(auto_select_cap(ctx->cfg)));
   if (s != CPSEL_OK) return s;
   double v = 0;
   s = drive(be, n, (int)dtype, k, ctx->cfg, zc, auto_select_cap(ctx->cfg), &v, info, &ctx->trace);
@@ -773,7 +843,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
     void* dev[] = {ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
-                   ctx->d_stage};
+                   ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};
     for (void* p : dev)
       if (p) cudaFree(p);
     lms_free(ctx->lms);
@@ -949,7 +1019,10 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
   if (n == 0) return fail(ctx, CPSEL_EINVAL, "global n == 0");
   if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
   const uint64_t zc = auto_z_cap(n, ctx->cfg);
-  s = be.ensure_z(std::max<uint64_t>(std::min<uint64_t>(zc, n_local), 1));
+  {
+    const uint64_t dc = dense_threshold(auto_select_cap(ctx->cfg));
+    s = be.ensure_z(std::max<uint64_t>(std::min<uint64_t>(std::min(zc, dc), n_local), 1), zc > dc);
+  }
   if (s != CPSEL_OK) return s;
   double v = 0;
   s = drive(be, n, (int)dtype, k, ctx->cfg, zc, auto_select_cap(ctx->cfg), &v, info, &ctx->trace);

@@ -692,6 +692,256 @@ template <typename T, int MODE> cudaError_t occ_pass(int* blocks) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Step a2+a4, segmented form: warp-private compaction (no atomics for regions, no block barriers).
+constexpr int kSegU = 4;  // vectors per lane per group
+
+template <typename T> struct WarpSeg {
+  static constexpr int VE = VecOf<T>::N;
+  static constexpr int G = kSegU * VE;       // elements per lane per group
+  static constexpr int GW = 32 * G;          // elements per warp per group
+  T t, yL, yR;
+  T vals[G];
+  unsigned lo_bits, hi_bits;
+  T glo[kSegU], ghi[kSegU];
+  double L_lo, L_hi;
+  unsigned long long n_lo, n_hi;             // warp-uniform: elements written so far
+  T* stage;                                  // this warp's smem: [0,GW) lo, [GW,2GW) hi
+  // output
+  int dense;
+  T* out;
+  uint64_t reg_lo, reg_end;                  // region [reg_lo, reg_end) (segmented out)
+  unsigned long long* cursors;               // dense out
+  uint64_t z_cap;
+
+  __device__ __forceinline__ void elem(float v, int u, int idx) {
+    asm("{\n\t.reg .pred plt, pgt, plo, phi;\n\t.reg .f32 d;\n\t"
+        "setp.lt.f32 plt, %4, %5;\n\t"
+        "setp.gt.f32 pgt, %4, %5;\n\t"
+        "setp.gt.and.f32 plo, %4, %6, plt;\n\t"
+        "setp.lt.and.f32 phi, %4, %7, pgt;\n\t"
+        "sub.rn.f32 d, %5, %4;\n\t"
+        "@plo add.rn.f32 %0, %0, d;\n\t"
+        "@phi sub.rn.f32 %1, %1, d;\n\t"
+        "@plo or.b32 %2, %2, %8;\n\t"
+        "@phi or.b32 %3, %3, %8;\n\t}"
+        : "+f"(glo[u]), "+f"(ghi[u]), "+r"(lo_bits), "+r"(hi_bits)
+        : "f"(v), "f"(t), "f"(yL), "f"(yR), "r"(1u << idx));
+    vals[idx] = v;
+  }
+  __device__ __forceinline__ void elem(double v, int u, int idx) {
+    asm("{\n\t.reg .pred plt, pgt, plo, phi;\n\t.reg .f64 d;\n\t"
+        "setp.lt.f64 plt, %4, %5;\n\t"
+        "setp.gt.f64 pgt, %4, %5;\n\t"
+        "setp.gt.and.f64 plo, %4, %6, plt;\n\t"
+        "setp.lt.and.f64 phi, %4, %7, pgt;\n\t"
+        "sub.rn.f64 d, %5, %4;\n\t"
+        "@plo add.rn.f64 %0, %0, d;\n\t"
+        "@phi sub.rn.f64 %1, %1, d;\n\t"
+        "@plo or.b32 %2, %2, %8;\n\t"
+        "@phi or.b32 %3, %3, %8;\n\t}"
+        : "+d"(glo[u]), "+d"(ghi[u]), "+r"(lo_bits), "+r"(hi_bits)
+        : "d"(v), "d"(t), "d"(yL), "d"(yR), "r"(1u << idx));
+    vals[idx] = v;
+  }
+  __device__ __forceinline__ void begin() {
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) glo[u] = ghi[u] = T(0);
+    lo_bits = hi_bits = 0u;
+  }
+  // close a group: sums to fp64, warp scan of the counts, stage, coalesced write-out
+  __device__ __forceinline__ void end() {
+    L_lo += (double)((glo[0] + glo[1]) + (glo[2] + glo[3]));
+    L_hi += (double)((ghi[0] + ghi[1]) + (ghi[2] + ghi[3]));
+    const int lane = threadIdx.x & 31;
+    const unsigned packed = (unsigned)__popc(lo_bits) | ((unsigned)__popc(hi_bits) << 16);
+    unsigned incl = packed;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned tot = __shfl_sync(FULL, incl, 31);
+    if (tot == 0u) return;
+    const unsigned pre = incl - packed;
+    unsigned plo = pre & 0xffffu, phi = pre >> 16;
+    T* slo = stage;
+    T* shi = stage + GW;
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      if ((lo_bits >> j) & 1u) slo[plo++] = vals[j];
+      if ((hi_bits >> j) & 1u) shi[phi++] = vals[j];
+    }
+    __syncwarp();
+    const unsigned nlo = tot & 0xffffu, nhi = tot >> 16;
+    T* dlo;
+    T* dhi;
+    if (dense) {
+      unsigned long long blo = 0, bhi = 0;
+      if (lane == 0) {
+        if (nlo) blo = atomicAdd(&cursors[0], (unsigned long long)nlo);
+        if (nhi) bhi = atomicAdd(&cursors[1], (unsigned long long)nhi);
+      }
+      blo = __shfl_sync(FULL, blo, 0);
+      bhi = __shfl_sync(FULL, bhi, 0);
+      dlo = out + blo;
+      dhi = out + (z_cap - bhi - nhi);
+    } else {
+      dlo = out + reg_lo + n_lo;
+      dhi = out + (reg_end - n_hi - nhi);
+    }
+    for (unsigned i = lane; i < nlo; i += 32) dlo[i] = slo[i];
+    for (unsigned i = lane; i < nhi; i += 32) dhi[i] = shi[i];
+    n_lo += nlo;
+    n_hi += nhi;
+    __syncwarp();
+  }
+};
+
+// one warp, one group of up to 32*kSegU vectors starting at vector index v0 (lane-strided)
+template <typename T, bool MASKED>
+__device__ __forceinline__ void seg_group(WarpSeg<T>& f, const typename VecOf<T>::V* __restrict__ xv, uint64_t v0,
+                                          uint64_t nvec) {
+  using V = typename VecOf<T>::V;
+  constexpr int VE = VecOf<T>::N;
+  const int lane = threadIdx.x & 31;
+  V v[kSegU];
+  bool ok[kSegU];
+#pragma unroll
+  for (int u = 0; u < kSegU; ++u) {
+    const uint64_t i = v0 + (uint64_t)u * 32 + lane;
+    ok[u] = !MASKED || i < nvec;
+    if (ok[u]) v[u] = ld_stream(xv + i);
+  }
+  f.begin();
+#pragma unroll
+  for (int u = 0; u < kSegU; ++u) {
+    if (ok[u]) {
+#pragma unroll
+      for (int j = 0; j < VE; ++j) f.elem(lane_of(v[u], j), u, u * VE + j);
+    }
+  }
+  f.end();
+}
+
+// up to 32 scattered scalars (one per lane): x[idx] for lanes with ok
+template <typename T>
+__device__ __forceinline__ void seg_scalars(WarpSeg<T>& f, T v, bool ok) {
+  f.begin();
+  if (ok) f.elem(v, 0, 0);
+  f.end();
+}
+
+// a whole contiguous run [p, p+c) processed by one warp
+template <typename T>
+__device__ __forceinline__ void seg_run(WarpSeg<T>& f, const T* __restrict__ p, uint64_t c) {
+  using V = typename VecOf<T>::V;
+  constexpr int VE = VecOf<T>::N;
+  const int lane = threadIdx.x & 31;
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(p) / sizeof(T)) & (VE - 1);
+  uint64_t head = mis ? (VE - mis) : 0;
+  if (head > c) head = c;
+  const V* xv = reinterpret_cast<const V*>(p + head);
+  const uint64_t nvec = (c - head) / VE;
+  const uint64_t tail0 = head + nvec * VE, ntail = c - tail0;
+  // head and tail scalars (< VE each) in one masked group
+  {
+    const bool okh = (uint64_t)lane < head;
+    const bool okt = (uint64_t)lane >= head && (uint64_t)lane < head + ntail;
+    T v = T(0);
+    if (okh) v = p[lane];
+    if (okt) v = p[tail0 + (lane - head)];
+    if (head + ntail) seg_scalars(f, v, okh || okt);
+  }
+  constexpr uint64_t GV = 32 * kSegU;
+  uint64_t v0 = 0;
+  for (; v0 + GV <= nvec; v0 += GV) seg_group<T, false>(f, xv, v0, nvec);
+  if (v0 < nvec) seg_group<T, true>(f, xv, v0, nvec);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
+  using F = WarpSeg<T>;
+  __shared__ __align__(16) T stage_all[kWarps * 2 * F::GW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
+  const uint64_t Wtot = (uint64_t)gridDim.x * kWarps;
+  F f;
+  f.t = (T)a.t; f.yL = (T)a.y_lo; f.yR = (T)a.y_hi;
+  f.L_lo = f.L_hi = 0.0;
+  f.n_lo = f.n_hi = 0;
+  f.stage = stage_all + (size_t)w * 2 * F::GW;
+  f.dense = a.dense_out;
+  f.out = static_cast<T*>(a.out);
+  f.reg_lo = W * a.R;
+  f.reg_end = (W + 1) * a.R;
+  f.cursors = a.cursors;
+  f.z_cap = a.z_cap;
+  if (a.seg_in == nullptr) {
+    // contiguous input: warp-strided groups over the 16-B aligned body; the unaligned head and
+    // the tail go to the last warp
+    using V = typename VecOf<T>::V;
+    constexpr int VE = VecOf<T>::N;
+    const T* x = static_cast<const T*>(a.x);
+    const uint64_t n = a.n;
+    const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
+    uint64_t head = mis ? (VE - mis) : 0;
+    if (head > n) head = n;
+    const V* xv = reinterpret_cast<const V*>(x + head);
+    const uint64_t nvec = (n - head) / VE;
+    constexpr uint64_t GV = 32 * kSegU;
+    const uint64_t nfull = nvec / GV;
+    for (uint64_t g = W; g < nfull; g += Wtot) seg_group<T, false>(f, xv, g * GV, nvec);
+    if (nfull * GV < nvec && W == nfull % Wtot) seg_group<T, true>(f, xv, nfull * GV, nvec);
+    if (W == Wtot - 1) {
+      const uint64_t tail0 = head + nvec * VE, ntail = n - tail0;
+      const bool okh = (uint64_t)lane < head;
+      const bool okt = (uint64_t)lane >= head && (uint64_t)lane < head + ntail;
+      T v = T(0);
+      if (okh) v = x[lane];
+      if (okt) v = x[tail0 + (lane - head)];
+      if (head + ntail) seg_scalars(f, v, okh || okt);
+    }
+  } else {
+    const SegEntry e = a.seg_in[W];
+    const T* base = static_cast<const T*>(a.x);
+    seg_run(f, base + e.off[a.side_in], e.cnt[a.side_in]);
+  }
+  if (!a.dense_out && lane == 0) {
+    SegEntry o;
+    o.off[0] = f.reg_lo;
+    o.cnt[0] = f.n_lo;
+    o.off[1] = f.reg_end - f.n_hi;
+    o.cnt[1] = f.n_hi;
+    a.seg_out[W] = o;
+  }
+  PassPartial p;
+  p.c_lt = p.c_eq = 0;
+  p.c_lo = lane == 0 ? f.n_lo : 0;   // warp totals, counted once per warp
+  p.c_hi = lane == 0 ? f.n_hi : 0;
+  p.L_lo = f.L_lo; p.L_hi = f.L_hi; p.P = 0; p.N = 0;
+  p.pred = -tinf<double>(); p.succ = tinf<double>();
+  p = block_reduce(p);
+  PassPartial id;
+  id.c_lt = id.c_eq = id.c_lo = id.c_hi = 0;
+  id.L_lo = id.L_hi = id.P = id.N = 0;
+  id.pred = -tinf<double>(); id.succ = tinf<double>();
+  PassPartial tot;
+  if (grid_finish(p, static_cast<PassPartial*>(a.partials), a.ticket, &tot, id) && threadIdx.x == 0) {
+    DevPass r;
+    r.c_lt = r.c_eq = 0;
+    r.c_lo = tot.c_lo; r.c_hi = tot.c_hi;
+    r.L_lo = tot.L_lo; r.L_hi = tot.L_hi; r.P = 0; r.N = 0;
+    r.pred = tot.pred; r.succ = tot.succ;
+    r.z_lo = tot.c_lo; r.z_hi = tot.c_hi;
+    if (a.dense_out) {
+      a.cursors[0] = 0ull;
+      a.cursors[1] = 0ull;
+    }
+    *a.out_tuple = r;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Step a8: batched selection (LMS: one k-th order statistic per column of S).  One CTA runs the
 // whole method on one column at a time (work-stealing over columns): the init reduction, the
 // Kelley iterations with the driver step on thread 0 (device-side driver, same rules as the host
@@ -904,6 +1154,10 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
   OCC(kF32, float, kHot) OCC(kF32, float, kCompact) OCC(kF32, float, kDirect)
   OCC(kF64, double, kHot) OCC(kF64, double, kCompact) OCC(kF64, double, kDirect)
 #undef OCC
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<float>, kBlock, 0)) != cudaSuccess) return e;
+  s->grid_seg[kF32] = s->num_sms * (b > 0 ? b : 1);
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<double>, kBlock, 0)) != cudaSuccess) return e;
+  s->grid_seg[kF64] = s->num_sms * (b > 0 ? b : 1);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<float, 4, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_init[kF32] = s->num_sms * (b > 0 ? b : 1);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<double, 4, false>, kBlock, 0)) != cudaSuccess) return e;
@@ -918,6 +1172,7 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
 size_t partial_bytes_needed(const LaunchShape& s) {
   int g = 0;
   for (int d = 0; d < 2; ++d) {
+    g = g > s.grid_seg[d] ? g : s.grid_seg[d];
     for (int m = 0; m < 3; ++m) g = g > s.grid_pass[d][m] ? g : s.grid_pass[d][m];
     g = g > s.grid_init[d] ? g : s.grid_init[d];
   }
@@ -959,6 +1214,22 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
     case kCompact: return launch_pass_t<double, kCompact>(a, grid, st);
     default: return launch_pass_t<double, kDirect>(a, grid, st);
   }
+}
+
+int seg_total_warps(int dtype, const LaunchShape& s) { return s.grid_seg[dtype] * kWarps; }
+
+uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s) {
+  const uint64_t ve = dtype == kF32 ? 4 : 2;
+  const uint64_t gw = 32 * kSegU * ve;  // elements per warp group
+  const uint64_t wt = (uint64_t)seg_total_warps(dtype, s);
+  const uint64_t groups = (n + gw - 1) / gw;
+  return ((groups + wt - 1) / wt + 1) * gw + 64;  // + one ragged group + head/tail scalars
+}
+
+cudaError_t launch_seg_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st) {
+  if (dtype == kF32) seg_pass_kernel<float><<<s.grid_seg[kF32], kBlock, 0, st>>>(a);
+  else seg_pass_kernel<double><<<s.grid_seg[kF64], kBlock, 0, st>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,

@@ -59,6 +59,35 @@ struct PassArgs {
   DevPass* out;                      // device (or mapped host) result
 };
 
+// Segmented compaction (a4, warp-private output regions).  The compacting pass is run by a fixed
+// number of warps Wtot; warp W writes the ]y_lo,t[ elements it sees upward from out[W*R] and the
+// ]t,y_hi[ elements downward from out[(W+1)*R - 1], and records both runs in seg[W].  A later pass
+// over the kept half lets warp W read run `side` of seg[W] (same Wtot, same R), so no atomics, no
+// block barriers and no data movement between warps are ever needed.
+struct SegEntry {
+  unsigned long long off[2];  // start offset (elements) of the lo / hi run
+  unsigned long long cnt[2];  // lengths
+};
+struct SegArgs {
+  // input: contiguous (seg_in == nullptr: x[0..n), warp-strided groups) or segmented
+  const void* x;
+  uint64_t n;                  // contiguous: elements; segmented: total (diagnostic)
+  const SegEntry* seg_in;
+  int side_in;
+  double t, y_lo, y_hi;
+  // output: dense_out == 0: warp regions of R elements in `out`, runs recorded in seg_out;
+  //         dense_out == 1: appended to z (lo up from 0, hi down from z_cap-1) via cursors
+  int dense_out;
+  void* out;
+  uint64_t R;
+  SegEntry* seg_out;
+  unsigned long long* cursors;
+  uint64_t z_cap;
+  void* partials;
+  unsigned int* ticket;
+  DevPass* out_tuple;
+};
+
 struct InitArgs {
   const void* x;
   uint64_t n;
@@ -72,6 +101,7 @@ struct LaunchShape {
   int grid_pass[2][3];   // [dtype][mode]
   int grid_init[2];
   int grid_hist[2];
+  int grid_seg[2];
 };
 
 // Query occupancy and fill the persistent grid sizes (multiples of the SM count).
@@ -80,6 +110,12 @@ size_t partial_bytes_needed(const LaunchShape& shape);
 
 // checked=false: fast form (nonfinite stays 0; a non-finite input shows as a non-finite S/min/max);
 // checked=true: counts non-finite elements exactly.
+// Warps of the segmented kernel (fixed per dtype; every level of one selection uses the same).
+int seg_total_warps(int dtype, const LaunchShape& s);
+// Region size R (elements per warp) able to hold any compaction of an n-element contiguous array.
+uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s);
+cudaError_t launch_seg_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st);
+
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
 cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
 
