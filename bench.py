@@ -301,7 +301,7 @@ def main():
                        "z_cap": a.z_cap or "auto"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "pass_kernel<float,*> (a2 + fused a4), all launches in the timed region",
+                         "kernel": "pass_kernel<float,hot> + seg_pass_kernel<float> (a2 + fused a4): every cutting-plane pass launched in the timed region",
                          "bytes_per_launch": bytes_per_pass, "avg_launch_ms": avg_pass_ms,
                          "peak_source": peak_src,
                          "classes": {"hot_full_pass": hot_x, "compacting_full_pass": comp_x,

@@ -60,6 +60,9 @@ typedef struct {
   int32_t record_trace;      /* 1: keep the per-iteration trace (cpsel_get_trace).  Default 1 */
   int32_t record_timing;     /* 1: time every kernel with CUDA events on the ctx stream (info / trace
                                 kernel_ms fields).  Default 0 */
+  int32_t init_cut;          /* 1: the init pass also evaluates one extra cut at a sample quantile of
+                                the target rank (R23), saving a full pass.  Default 1 */
+  int32_t reserved;
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -93,6 +96,10 @@ typedef struct {
   uint64_t cnt_min, cnt_max, nonfinite;
   double x0;              /* the shift x[0] */
   double S;               /* sum_i (x_i - x0), fp64 */
+  uint64_t has_cut;       /* 1 if the pass also evaluated the extra cut t0 (R23): */
+  double t0;              /*   the cut (an element of x) */
+  uint64_t c_lt0, c_eq0;  /*   #{x < t0}, #{x == t0} */
+  double N0, P0;          /*   sum (t0-x)^+, sum (x-t0)^+ */
 } cpsel_init_stats;
 
 /* One row per cutting-plane pass (R7 trace). */
@@ -103,7 +110,8 @@ typedef struct {
   uint64_t interior;      /* bracket interior count after the update */
   uint64_t scanned;       /* elements this pass read (x, or the compacted bracket) */
   uint64_t written;       /* elements this pass wrote (compaction of both bracket halves) */
-  uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard */
+  uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard,
+                             2 the init pass's extra cut (R23) */
   uint32_t compacted;     /* 1 if this pass also wrote z */
   double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
 } cpsel_trace_row;
@@ -158,7 +166,8 @@ cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t
  * (else CPSEL_EINVAL).  Computes every field of cpsel_pass_stats in a single read of x. */
 cpsel_status cpsel_eval(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, double t,
                         double y_lo, double y_hi, cpsel_pass_stats* out);
-/* The init reduction alone (step a1). */
+/* The init reduction alone (step a1); with init_cut it also evaluates the extra cut at the
+ * sample quantile of the median rank (R23). */
 cpsel_status cpsel_init(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype,
                         cpsel_init_stats* out);
 /* The small-set exact selection alone (step a5): r-th smallest (1-based) of d_z[0..m). */

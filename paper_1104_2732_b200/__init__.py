@@ -36,7 +36,8 @@ class CpselError(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("z_cap", C.c_uint64), ("direct_threshold", C.c_uint64), ("select_cap", C.c_uint64),
                 ("max_iters", C.c_uint32),
-                ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32)]
+                ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32),
+                ("init_cut", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -62,7 +63,9 @@ class PassStats(C.Structure):
 
 class InitStats(C.Structure):
     _fields_ = [("vmin", C.c_double), ("vmax", C.c_double), ("cnt_min", C.c_uint64), ("cnt_max", C.c_uint64),
-                ("nonfinite", C.c_uint64), ("x0", C.c_double), ("S", C.c_double)]
+                ("nonfinite", C.c_uint64), ("x0", C.c_double), ("S", C.c_double), ("has_cut", C.c_uint64),
+                ("t0", C.c_double), ("c_lt0", C.c_uint64), ("c_eq0", C.c_uint64), ("N0", C.c_double),
+                ("P0", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -423,7 +426,7 @@ def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, adopt_fn, select_fn
         try:
             d = init_fn()
             for f, _ in InitStats._fields_:
-                setattr(out.contents, f, d[f])
+                setattr(out.contents, f, d.get(f, 0))
             return 0
         except Exception as e:  # pragma: no cover - surfaced below
             errors.append(e)

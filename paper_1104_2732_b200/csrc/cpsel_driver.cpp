@@ -38,6 +38,7 @@ struct cpsel_ctx {
   unsigned long long* d_cursors = nullptr;
   DevPass* d_pass = nullptr;
   DevInit* d_init = nullptr;
+  void* d_t0 = nullptr;              // the extra cut of the init pass (R23)
   RadixState* d_radix = nullptr;
   unsigned int* d_hist = nullptr;
   DevPass* d_gather = nullptr;       // G x DevPass (sharded)
@@ -181,7 +182,8 @@ double canonical_zero(double v) { return v == 0.0 ? 0.0 : v; }
 // number of elements dropped below it (D_lo) to get global counts.
 struct Backend {
   virtual ~Backend() = default;
-  virtual cpsel_status init(cpsel_init_stats* out) = 0;
+  // k: the target rank (for the extra cut, R23)
+  virtual cpsel_status init(cpsel_init_stats* out, uint64_t k) = 0;
   // one pass at t over the current array; if compact, also copy ]yL,t[ and ]t,yR[ out
   // (z_lo/z_hi: elements written, summed over ranks)
   // dense: write the halves contiguously (else the back end may keep them segmented)
@@ -241,12 +243,13 @@ struct GpuBackend : Backend {
   uint64_t half_n(int side) const { return side == 0 ? zlo : zhi; }
 
   // init kernel (fast form, then the checked form if anything came out non-finite)
-  cpsel_status run_init(bool sync_result) {
-    InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init};
+  cpsel_status run_init(bool sync_result, uint64_t k, bool cut) {
+    InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init, cut ? ctx->d_t0 : nullptr};
     CK(tic());
+    if (cut) CK(launch_sample_cut(dt, x, n, k, ctx->d_t0, ctx->stream));
     CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
     CK(toc());
-    launches = 1;
+    launches = cut ? 2 : 1;
     scanned = n;
     CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
@@ -254,7 +257,7 @@ struct GpuBackend : Backend {
     const DevInit& r = *ctx->h_init;
     if (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax)) {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, true));
-      launches = 2;
+      launches += 1;
       if (sync_result) {
         CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
@@ -262,12 +265,13 @@ struct GpuBackend : Backend {
     }
     return CPSEL_OK;
   }
-  cpsel_status init(cpsel_init_stats* o) override {
-    cpsel_status st = run_init(true);
+  cpsel_status init(cpsel_init_stats* o, uint64_t k) override {
+    cpsel_status st = run_init(true, k, ctx->cfg.init_cut != 0 && n > 2);
     if (st != CPSEL_OK) return st;
     const DevInit& r = *ctx->h_init;
     o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
     o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
+    o->has_cut = r.has_cut; o->t0 = r.t0; o->c_lt0 = r.c_lt0; o->c_eq0 = r.c_eq0; o->N0 = r.N0; o->P0 = r.P0;
     return CPSEL_OK;
   }
   // two dense ping-pong buffers of m_dense elements; two segmented buffers (+ run tables) able to
@@ -321,7 +325,8 @@ struct GpuBackend : Backend {
       a.cursors = ctx->d_cursors;
       a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out_tuple = ctx->d_pass;
       CK(tic());
-      CK(launch_seg_pass(dt, a, ctx->shape, ctx->stream));
+      // a compacted current array holds only bracket-interior elements
+      CK(launch_seg_pass(dt, a, /*inside=*/cur != x, ctx->shape, ctx->stream));
       CK(toc());
       last_dense = dense;
     }
@@ -392,7 +397,7 @@ struct ShardedBackend : GpuBackend {
     const NcclApi& nc = nccl_api();
     const int G = ctx->world;
     if (n > 0) {
-      cpsel_status st = run_init(false);  // leaves the (checked) record in d_init
+      cpsel_status st = run_init(false, 0, false);  // leaves the (checked) record in d_init
       if (st != CPSEL_OK) return st;
     } else {
       launches = 0;
@@ -433,8 +438,8 @@ struct ShardedBackend : GpuBackend {
     cur_rank = n_rank;
     return CPSEL_OK;
   }
-  cpsel_status init(cpsel_init_stats* o) override {
-    *o = combined;
+  cpsel_status init(cpsel_init_stats* o, uint64_t) override {
+    *o = combined;  // no extra cut when sharded (it would need a cut common to all ranks)
     return CPSEL_OK;
   }
   cpsel_status pass(double t, double yL, double yR, bool compact, bool dense, cpsel_pass_stats* o, uint64_t* z_lo,
@@ -521,7 +526,7 @@ struct HostBackend : Backend {
   std::string msg;
   explicit HostBackend(const cpsel_host_backend* b) : be(b) {}
   std::string message() const override { return msg; }
-  cpsel_status init(cpsel_init_stats* o) override {
+  cpsel_status init(cpsel_init_stats* o, uint64_t) override {
     if (be->init(be->user, o) != 0) { msg = "init callback failed"; return CPSEL_EINTERNAL; }
     return CPSEL_OK;
   }
@@ -583,7 +588,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   };
   // step 0: one reduction -> x_(1), x_(n), sum
   cpsel_init_stats rec{};
-  cpsel_status st = be.init(&rec);
+  cpsel_status st = be.init(&rec, k);
   if (st != CPSEL_OK) return st;
   inf.passes = 1;
   inf.launches += be.launches;
@@ -610,6 +615,33 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   int slow = 0;
   bool bisect = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
+  // R23: the init pass's extra cut at t0 (a sample quantile of the target rank) — one more cut of
+  // the cutting-plane model, evaluated in the same read of x as the init reduction
+  if (rec.has_cut && rec.t0 > rec.vmin && rec.t0 < rec.vmax) {
+    const double t0 = rec.t0;
+    const uint64_t c_lt = rec.c_lt0, c_le = rec.c_lt0 + rec.c_eq0;
+    cpsel_trace_row row{};
+    row.t = t0;
+    row.F = (double)(wP * (long double)rec.P0 + wN * (long double)rec.N0);
+    row.c_lt = c_lt;
+    row.c_eq = rec.c_eq0;
+    row.kind = 2;
+    if (c_lt < k && k <= c_le) {
+      if (trace && cfg.record_trace) trace->push_back(row);
+      return done(t0, 2);
+    }
+    if (c_le < k) {  // y_L <- t0: interior ]t0, max[
+      const long double L_hi = (long double)rec.P0 - (long double)rec.cnt_max * ((long double)rec.vmax - t0);
+      yL = t0; N_L = rec.N0; c_le_L = c_le; m = c_lt_R - c_le;
+      t = t0 + (double)(L_hi / (long double)m);
+    } else {  // y_R <- t0: interior ]min, t0[
+      const long double L_lo = (long double)rec.N0 - (long double)rec.cnt_min * (t0 - (long double)rec.vmin);
+      yR = t0; P_R = rec.P0; c_lt_R = c_lt; m = c_lt - c_le_L;
+      t = t0 - (double)(L_lo / (long double)m);
+    }
+    row.interior = m;
+    if (trace && cfg.record_trace) trace->push_back(row);
+  }
   for (uint32_t it = 1;; ++it) {
     if (it > cfg.max_iters) {
       if (info) *info = inf;
@@ -717,7 +749,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
 
 uint64_t auto_z_cap(uint64_t n, const cpsel_config& cfg) {
   if (cfg.z_cap) return std::min<uint64_t>(cfg.z_cap, n);
-  return std::max<uint64_t>(n / 2, 1);  // compact from the second pass on
+  return std::max<uint64_t>(n / 8 * 5, 1);  // compact once the bracket holds <= 5/8 of x
 }
 
 uint64_t auto_select_cap(const cpsel_config& cfg) { return cfg.select_cap ? cfg.select_cap : (1ull << 20); }
@@ -787,6 +819,7 @@ void cpsel_config_default(cpsel_config* c) {
   c->force_cp = 0;
   c->record_trace = 1;
   c->record_timing = 0;
+  c->init_cut = 1;
 }
 
 cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
@@ -821,6 +854,7 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMemset(ctx->d_cursors, 0, 256));
   CKC(cudaMalloc(&ctx->d_pass, sizeof(DevPass)));
   CKC(cudaMalloc(&ctx->d_init, sizeof(DevInit)));
+  CKC(cudaMalloc(&ctx->d_t0, 16));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
   CKC(cudaMalloc(&ctx->d_hist, 2048 * sizeof(unsigned)));
   CKC(cudaMemset(ctx->d_hist, 0, 2048 * sizeof(unsigned)));
@@ -841,7 +875,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
-    void* dev[] = {ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
+    void* dev[] = {ctx->d_t0, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
                    ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};
     for (void* p : dev)
@@ -941,7 +975,7 @@ cpsel_status cpsel_init(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype
   if (!out) return fail(ctx, CPSEL_EINVAL, "null out");
   DeviceGuard g(ctx->device);
   GpuBackend be(ctx, d_x, n, (int)dtype);
-  return be.init(out);
+  return be.init(out, (n + 1) / 2);  // the extra cut (if enabled) targets the median rank
 }
 
 cpsel_status cpsel_small_select(cpsel_ctx* ctx, const void* d_z, uint64_t m, cpsel_dtype dtype, uint64_t r,

@@ -67,6 +67,25 @@ template <typename T> __device__ __forceinline__ T tinf();
 template <> __device__ __forceinline__ float tinf() { return __int_as_float(0x7f800000); }
 template <> __device__ __forceinline__ double tinf() { return __longlong_as_double(0x7ff0000000000000ll); }
 
+// Order-preserving integer keys of floats (radix select, sample cut, ordered-key bisection).
+__device__ __forceinline__ unsigned long long okey(float v) {
+  const unsigned u = __float_as_uint(v);
+  return (unsigned long long)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
+}
+__device__ __forceinline__ unsigned long long okey(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double from_key_f32(unsigned long long k) {
+  const unsigned kk = (unsigned)k;
+  const unsigned u = (kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk;
+  return (double)__uint_as_float(u);
+}
+__device__ __forceinline__ double from_key_f64(unsigned long long k) {
+  const unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
 // ------------------------------------------------------------------------------------------
 // Generic grid-stride stream over x[0..n) with 16-byte vector loads.  F provides
 //   template<bool MASKED> void vec(const V&, bool ok)   (all lanes call; ok=false -> no-op)
@@ -170,6 +189,10 @@ __device__ __forceinline__ void combine(InitPartial& a, const InitPartial& b) {
   else if (b.vmax == a.vmax) a.cnt_max += b.cnt_max;
   a.S += b.S;
   a.nonfinite += b.nonfinite;
+  a.N0 += b.N0;
+  a.P0 += b.P0;
+  a.c_lt0 += b.c_lt0;
+  a.c_eq0 += b.c_eq0;
 }
 
 __device__ InitPartial block_reduce(InitPartial p) {
@@ -225,19 +248,61 @@ __device__ bool grid_finish(const P& mine, P* partials, unsigned int* ticket, P*
 // updates (min, #min) / (max, #max) only when the vector reaches the running extreme; the shifted
 // sum doubles as the non-finite detector (NaN/Inf make it non-finite; the host then re-runs the
 // CHECKED form, which counts non-finite elements exactly).
-template <typename T, bool CHECKED> struct InitFn {
+// CUT: also evaluate the extra cut at t0 (R23) — counts and the two positive-part sums, as
+// predicated PTX (8 issue slots per element).
+template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
   T mn, mx, x0;
   unsigned cmn, cmx, nonfin;
   double S;
   T g[4];
+  T t0;
+  unsigned clt0 = 0, ceq0 = 0;
+  T gN[4], gP[4];
+  double N0 = 0, P0 = 0;
   __device__ InitFn(T x0_) : mn(tinf<T>()), mx(-tinf<T>()), x0(x0_), cmn(0), cmx(0), nonfin(0), S(0) {}
+  __device__ __forceinline__ void cut(float v, float& n_, float& p_) {
+    asm("{\n\t.reg .pred plt, pgt, peq;\n\t.reg .f32 d;\n\t"
+        "setp.lt.f32 plt, %4, %5;\n\t"
+        "setp.gt.f32 pgt, %4, %5;\n\t"
+        "setp.eq.f32 peq, %4, %5;\n\t"
+        "sub.rn.f32 d, %5, %4;\n\t"
+        "@plt add.u32 %0, %0, 1;\n\t"
+        "@peq add.u32 %1, %1, 1;\n\t"
+        "@plt add.rn.f32 %2, %2, d;\n\t"
+        "@pgt sub.rn.f32 %3, %3, d;\n\t}"
+        : "+r"(clt0), "+r"(ceq0), "+f"(n_), "+f"(p_)
+        : "f"(v), "f"(t0));
+  }
+  __device__ __forceinline__ void cut(double v, double& n_, double& p_) {
+    asm("{\n\t.reg .pred plt, pgt, peq;\n\t.reg .f64 d;\n\t"
+        "setp.lt.f64 plt, %4, %5;\n\t"
+        "setp.gt.f64 pgt, %4, %5;\n\t"
+        "setp.eq.f64 peq, %4, %5;\n\t"
+        "sub.rn.f64 d, %5, %4;\n\t"
+        "@plt add.u32 %0, %0, 1;\n\t"
+        "@peq add.u32 %1, %1, 1;\n\t"
+        "@plt add.rn.f64 %2, %2, d;\n\t"
+        "@pgt sub.rn.f64 %3, %3, d;\n\t}"
+        : "+r"(clt0), "+r"(ceq0), "+d"(n_), "+d"(p_)
+        : "d"(v), "d"(t0));
+  }
   __device__ __forceinline__ void slow(T v) {
     if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
     if (v > mx) { mx = v; cmx = 1; } else if (v == mx) ++cmx;
   }
-  __device__ __forceinline__ void group_begin() { g[0] = g[1] = g[2] = g[3] = T(0); }
-  __device__ __forceinline__ void group_end() { S += (double)((g[0] + g[1]) + (g[2] + g[3])); }
+  __device__ __forceinline__ void group_begin() {
+    g[0] = g[1] = g[2] = g[3] = T(0);
+    if (CUT) gN[0] = gN[1] = gN[2] = gN[3] = gP[0] = gP[1] = gP[2] = gP[3] = T(0);
+  }
+  __device__ __forceinline__ void group_end() {
+    S += (double)((g[0] + g[1]) + (g[2] + g[3]));
+    if (CUT) {
+      N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
+      P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+    }
+  }
   __device__ __forceinline__ void vec_elems(const float4& v, int u) {
+    if (CUT) { cut(v.x, gN[u & 3], gP[u & 3]); cut(v.y, gN[u & 3], gP[u & 3]); cut(v.z, gN[u & 3], gP[u & 3]); cut(v.w, gN[u & 3], gP[u & 3]); }
     const float lo = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
     const float hi = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
     if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); slow(v.z); slow(v.w); }
@@ -246,6 +311,7 @@ template <typename T, bool CHECKED> struct InitFn {
       nonfin += !(fabsf(v.x) <= FLT_MAX) + !(fabsf(v.y) <= FLT_MAX) + !(fabsf(v.z) <= FLT_MAX) + !(fabsf(v.w) <= FLT_MAX);
   }
   __device__ __forceinline__ void vec_elems(const double2& v, int u) {
+    if (CUT) { cut(v.x, gN[u & 3], gP[u & 3]); cut(v.y, gN[u & 3], gP[u & 3]); }
     const double lo = fmin(v.x, v.y), hi = fmax(v.x, v.y);
     if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); }
     g[u & 3] += (v.x - x0) + (v.y - x0);
@@ -260,29 +326,73 @@ template <typename T, bool CHECKED> struct InitFn {
     group_begin();
     slow(v);
     g[0] = v - x0;
+    if (CUT) cut(v, gN[0], gP[0]);
     if (CHECKED) nonfin += !(fabs(v) <= (sizeof(T) == 4 ? (T)FLT_MAX : (T)DBL_MAX));
     group_end();
   }
 };
 
-template <typename T, int UNROLL, bool CHECKED>
+template <typename T, int UNROLL, bool CHECKED, bool CUT>
 __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   const T* x = static_cast<const T*>(a.x);
-  InitFn<T, CHECKED> f(x[0]);
+  InitFn<T, CHECKED, CUT> f(x[0]);
+  if (CUT) f.t0 = *static_cast<const T*>(a.t0);
   stream_array<T, UNROLL>(x, a.n, f, blockIdx.x, gridDim.x);
   InitPartial p;
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
+  p.N0 = f.N0; p.P0 = f.P0; p.c_lt0 = f.clt0; p.c_eq0 = f.ceq0;
   p = block_reduce(p);
   InitPartial id;
   id.vmin = tinf<double>(); id.vmax = -tinf<double>(); id.S = 0; id.pad = 0;
   id.cnt_min = id.cnt_max = id.nonfinite = id.pad2 = 0;
+  id.N0 = id.P0 = 0; id.c_lt0 = id.c_eq0 = 0;
   InitPartial tot;
   if (grid_finish(p, static_cast<InitPartial*>(a.partials), a.ticket, &tot, id) && threadIdx.x == 0) {
     DevInit r;
     r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = tot.S; r.x0 = (double)x[0];
     r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite; r.pad = 0;
+    r.t0 = CUT ? (double)f.t0 : 0.0;
+    r.N0 = tot.N0; r.P0 = tot.P0; r.c_lt0 = tot.c_lt0; r.c_eq0 = tot.c_eq0;
+    r.has_cut = CUT ? 1ull : 0ull;
     *a.out = r;
+  }
+}
+
+// R23: the extra cut of the init pass — the sample quantile at the target rank among 2048 evenly
+// strided samples (bitonic sort of order-preserving keys in shared memory, one CTA).
+template <typename T>
+__global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ x, uint64_t n, uint64_t k, T* t0) {
+  constexpr int S = 2048;
+  __shared__ unsigned long long key[S];
+  const uint64_t m = n < (uint64_t)S ? n : (uint64_t)S;
+  for (int i = threadIdx.x; i < S; i += blockDim.x) {
+    if ((uint64_t)i < m) {
+      const uint64_t pos = (n == m) ? (uint64_t)i : ((uint64_t)i * n) / m + (n / m) / 2;
+      key[i] = okey(x[pos]);
+    } else {
+      key[i] = ~0ull;  // padding sorts last
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= S; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const unsigned long long a = key[lo], b = key[hi];
+        if ((a > b) == up) { key[lo] = b; key[hi] = a; }
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    double q = ((double)k - 0.5) / (double)n * (double)m;
+    uint64_t idx = q < 0 ? 0 : (uint64_t)q;
+    if (idx >= m) idx = m - 1;
+    const unsigned long long kk = key[idx];
+    *t0 = (T)(sizeof(T) == 4 ? from_key_f32(kk) : from_key_f64(kk));
   }
 }
 
@@ -574,24 +684,6 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(PassArgs a) {
 
 // ------------------------------------------------------------------------------------------
 // Step a5: radix select on order-preserving keys.
-__device__ __forceinline__ unsigned long long okey(float v) {
-  const unsigned u = __float_as_uint(v);
-  return (unsigned long long)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
-}
-__device__ __forceinline__ unsigned long long okey(double v) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
-}
-__device__ __forceinline__ double from_key_f32(unsigned long long k) {
-  const unsigned kk = (unsigned)k;
-  const unsigned u = (kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk;
-  return (double)__uint_as_float(u);
-}
-__device__ __forceinline__ double from_key_f64(unsigned long long k) {
-  const unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
-  return __longlong_as_double((long long)u);
-}
-
 constexpr int kRadixBits = 11;
 constexpr int kBins = 1 << kRadixBits;
 
@@ -695,7 +787,9 @@ template <typename T, int MODE> cudaError_t occ_pass(int* blocks) {
 // Step a2+a4, segmented form: warp-private compaction (no atomics for regions, no block barriers).
 constexpr int kSegU = 4;  // vectors per lane per group
 
-template <typename T> struct WarpSeg {
+// INSIDE: every input element is known to lie strictly inside ]y_lo, y_hi[ (the input is a kept
+// half of an earlier compaction), so the bracket tests are skipped (7 issue slots per element).
+template <typename T, bool INSIDE> struct WarpSeg {
   static constexpr int VE = VecOf<T>::N;
   static constexpr int G = kSegU * VE;       // elements per lane per group
   static constexpr int GW = 32 * G;          // elements per warp per group
@@ -714,6 +808,20 @@ template <typename T> struct WarpSeg {
   uint64_t z_cap;
 
   __device__ __forceinline__ void elem(float v, int u, int idx) {
+    if (INSIDE) {
+      asm("{\n\t.reg .pred plo, phi;\n\t.reg .f32 d;\n\t"
+          "setp.lt.f32 plo, %4, %5;\n\t"
+          "setp.gt.f32 phi, %4, %5;\n\t"
+          "sub.rn.f32 d, %5, %4;\n\t"
+          "@plo add.rn.f32 %0, %0, d;\n\t"
+          "@phi sub.rn.f32 %1, %1, d;\n\t"
+          "@plo or.b32 %2, %2, %6;\n\t"
+          "@phi or.b32 %3, %3, %6;\n\t}"
+          : "+f"(glo[u]), "+f"(ghi[u]), "+r"(lo_bits), "+r"(hi_bits)
+          : "f"(v), "f"(t), "r"(1u << idx));
+      vals[idx] = v;
+      return;
+    }
     asm("{\n\t.reg .pred plt, pgt, plo, phi;\n\t.reg .f32 d;\n\t"
         "setp.lt.f32 plt, %4, %5;\n\t"
         "setp.gt.f32 pgt, %4, %5;\n\t"
@@ -729,6 +837,20 @@ template <typename T> struct WarpSeg {
     vals[idx] = v;
   }
   __device__ __forceinline__ void elem(double v, int u, int idx) {
+    if (INSIDE) {
+      asm("{\n\t.reg .pred plo, phi;\n\t.reg .f64 d;\n\t"
+          "setp.lt.f64 plo, %4, %5;\n\t"
+          "setp.gt.f64 phi, %4, %5;\n\t"
+          "sub.rn.f64 d, %5, %4;\n\t"
+          "@plo add.rn.f64 %0, %0, d;\n\t"
+          "@phi sub.rn.f64 %1, %1, d;\n\t"
+          "@plo or.b32 %2, %2, %6;\n\t"
+          "@phi or.b32 %3, %3, %6;\n\t}"
+          : "+d"(glo[u]), "+d"(ghi[u]), "+r"(lo_bits), "+r"(hi_bits)
+          : "d"(v), "d"(t), "r"(1u << idx));
+      vals[idx] = v;
+      return;
+    }
     asm("{\n\t.reg .pred plt, pgt, plo, phi;\n\t.reg .f64 d;\n\t"
         "setp.lt.f64 plt, %4, %5;\n\t"
         "setp.gt.f64 pgt, %4, %5;\n\t"
@@ -798,8 +920,8 @@ template <typename T> struct WarpSeg {
 };
 
 // one warp, one group of up to 32*kSegU vectors starting at vector index v0 (lane-strided)
-template <typename T, bool MASKED>
-__device__ __forceinline__ void seg_group(WarpSeg<T>& f, const typename VecOf<T>::V* __restrict__ xv, uint64_t v0,
+template <typename T, bool MASKED, typename F>
+__device__ __forceinline__ void seg_group(F& f, const typename VecOf<T>::V* __restrict__ xv, uint64_t v0,
                                           uint64_t nvec) {
   using V = typename VecOf<T>::V;
   constexpr int VE = VecOf<T>::N;
@@ -824,16 +946,16 @@ __device__ __forceinline__ void seg_group(WarpSeg<T>& f, const typename VecOf<T>
 }
 
 // up to 32 scattered scalars (one per lane): x[idx] for lanes with ok
-template <typename T>
-__device__ __forceinline__ void seg_scalars(WarpSeg<T>& f, T v, bool ok) {
+template <typename T, typename F>
+__device__ __forceinline__ void seg_scalars(F& f, T v, bool ok) {
   f.begin();
   if (ok) f.elem(v, 0, 0);
   f.end();
 }
 
 // a whole contiguous run [p, p+c) processed by one warp
-template <typename T>
-__device__ __forceinline__ void seg_run(WarpSeg<T>& f, const T* __restrict__ p, uint64_t c) {
+template <typename T, typename F>
+__device__ __forceinline__ void seg_run(F& f, const T* __restrict__ p, uint64_t c) {
   using V = typename VecOf<T>::V;
   constexpr int VE = VecOf<T>::N;
   const int lane = threadIdx.x & 31;
@@ -850,7 +972,7 @@ __device__ __forceinline__ void seg_run(WarpSeg<T>& f, const T* __restrict__ p, 
     T v = T(0);
     if (okh) v = p[lane];
     if (okt) v = p[tail0 + (lane - head)];
-    if (head + ntail) seg_scalars(f, v, okh || okt);
+    if (head + ntail) seg_scalars<T>(f, v, okh || okt);
   }
   constexpr uint64_t GV = 32 * kSegU;
   uint64_t v0 = 0;
@@ -858,9 +980,9 @@ __device__ __forceinline__ void seg_run(WarpSeg<T>& f, const T* __restrict__ p, 
   if (v0 < nvec) seg_group<T, true>(f, xv, v0, nvec);
 }
 
-template <typename T>
+template <typename T, bool INSIDE>
 __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
-  using F = WarpSeg<T>;
+  using F = WarpSeg<T, INSIDE>;
   __shared__ __align__(16) T stage_all[kWarps * 2 * F::GW];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
@@ -899,12 +1021,12 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
       T v = T(0);
       if (okh) v = x[lane];
       if (okt) v = x[tail0 + (lane - head)];
-      if (head + ntail) seg_scalars(f, v, okh || okt);
+      if (head + ntail) seg_scalars<T>(f, v, okh || okt);
     }
   } else {
     const SegEntry e = a.seg_in[W];
     const T* base = static_cast<const T*>(a.x);
-    seg_run(f, base + e.off[a.side_in], e.cnt[a.side_in]);
+    seg_run<T>(f, base + e.off[a.side_in], e.cnt[a.side_in]);
   }
   if (!a.dense_out && lane == 0) {
     SegEntry o;
@@ -1154,13 +1276,13 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
   OCC(kF32, float, kHot) OCC(kF32, float, kCompact) OCC(kF32, float, kDirect)
   OCC(kF64, double, kHot) OCC(kF64, double, kCompact) OCC(kF64, double, kDirect)
 #undef OCC
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<float>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<float, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_seg[kF32] = s->num_sms * (b > 0 ? b : 1);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<double>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<double, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_seg[kF64] = s->num_sms * (b > 0 ? b : 1);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<float, 4, false>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<float, 4, false, true>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_init[kF32] = s->num_sms * (b > 0 ? b : 1);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<double, 4, false>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<double, 4, false, true>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_init[kF64] = s->num_sms * (b > 0 ? b : 1);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist_kernel<float>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_hist[kF32] = s->num_sms * (b > 0 ? b : 1);
@@ -1186,16 +1308,27 @@ static int clamp_grid(int grid, uint64_t n, int per_cta) {
   return grid;
 }
 
-cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked) {
-  if (dtype == kF32) {
-    const int grid = clamp_grid(s.grid_init[kF32], a.n, kBlock * 4 * 4);
-    if (checked) init_kernel<float, 4, true><<<grid, kBlock, 0, st>>>(a);
-    else init_kernel<float, 4, false><<<grid, kBlock, 0, st>>>(a);
+template <typename T>
+static void launch_init_t(const InitArgs& a, int grid, cudaStream_t st, bool checked) {
+  const bool cut = a.t0 != nullptr;
+  if (checked) {
+    if (cut) init_kernel<T, 4, true, true><<<grid, kBlock, 0, st>>>(a);
+    else init_kernel<T, 4, true, false><<<grid, kBlock, 0, st>>>(a);
   } else {
-    const int grid = clamp_grid(s.grid_init[kF64], a.n, kBlock * 4 * 2);
-    if (checked) init_kernel<double, 4, true><<<grid, kBlock, 0, st>>>(a);
-    else init_kernel<double, 4, false><<<grid, kBlock, 0, st>>>(a);
+    if (cut) init_kernel<T, 4, false, true><<<grid, kBlock, 0, st>>>(a);
+    else init_kernel<T, 4, false, false><<<grid, kBlock, 0, st>>>(a);
   }
+}
+
+cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked) {
+  if (dtype == kF32) launch_init_t<float>(a, clamp_grid(s.grid_init[kF32], a.n, kBlock * 4 * 4), st, checked);
+  else launch_init_t<double>(a, clamp_grid(s.grid_init[kF64], a.n, kBlock * 4 * 2), st, checked);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st) {
+  if (dtype == kF32) sample_cut_kernel<float><<<1, 1024, 0, st>>>(static_cast<const float*>(x), n, k, static_cast<float*>(t0));
+  else sample_cut_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(x), n, k, static_cast<double*>(t0));
   return cudaGetLastError();
 }
 
@@ -1226,9 +1359,15 @@ uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s) {
   return ((groups + wt - 1) / wt + 1) * gw + 64;  // + one ragged group + head/tail scalars
 }
 
-cudaError_t launch_seg_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st) {
-  if (dtype == kF32) seg_pass_kernel<float><<<s.grid_seg[kF32], kBlock, 0, st>>>(a);
-  else seg_pass_kernel<double><<<s.grid_seg[kF64], kBlock, 0, st>>>(a);
+cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const LaunchShape& s, cudaStream_t st) {
+  const int g = s.grid_seg[dtype];
+  if (dtype == kF32) {
+    if (inside) seg_pass_kernel<float, true><<<g, kBlock, 0, st>>>(a);
+    else seg_pass_kernel<float, false><<<g, kBlock, 0, st>>>(a);
+  } else {
+    if (inside) seg_pass_kernel<double, true><<<g, kBlock, 0, st>>>(a);
+    else seg_pass_kernel<double, false><<<g, kBlock, 0, st>>>(a);
+  }
   return cudaGetLastError();
 }
 

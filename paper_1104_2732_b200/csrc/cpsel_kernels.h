@@ -23,6 +23,9 @@ static_assert(sizeof(DevPass) == 96, "DevPass layout");
 struct DevInit {
   double vmin, vmax, S, x0;
   unsigned long long cnt_min, cnt_max, nonfinite, pad;
+  // extra cut at t0 evaluated in the same pass (R23): #x<t0, #x==t0, sum (t0-x)^+, sum (x-t0)^+
+  double t0, N0, P0;
+  unsigned long long c_lt0, c_eq0, has_cut;
 };
 
 // Per-CTA partial of a pass (grid reduction scratch).
@@ -33,6 +36,8 @@ struct PassPartial {
 struct InitPartial {
   double vmin, vmax, S, pad;
   unsigned long long cnt_min, cnt_max, nonfinite, pad2;
+  double N0, P0;
+  unsigned long long c_lt0, c_eq0;
 };
 
 // Device-side state of the radix select (step a5).
@@ -94,6 +99,7 @@ struct InitArgs {
   void* partials;
   unsigned int* ticket;
   DevInit* out;
+  const void* t0;   // device pointer to the extra cut (one element of the dtype), or nullptr
 };
 
 struct LaunchShape {
@@ -114,9 +120,13 @@ size_t partial_bytes_needed(const LaunchShape& shape);
 int seg_total_warps(int dtype, const LaunchShape& s);
 // Region size R (elements per warp) able to hold any compaction of an n-element contiguous array.
 uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s);
-cudaError_t launch_seg_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st);
+// inside: every input element lies strictly inside the bracket (input = a kept half)
+cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const LaunchShape& s, cudaStream_t st);
 
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
+// t0 <- the element of rank ~ (k - 1/2)/n among 2048 strided samples of x (one CTA); written to
+// *t0 as the dtype
+cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st);
 cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
 
 // Radix select of the r-th smallest (1-based) of z[0..m) (any element alignment).

@@ -9,8 +9,9 @@ import numpy as np
 
 
 class NumpyShard:
-    def __init__(self, x, comm=None):
+    def __init__(self, x, comm=None, cut_k=None):
         self.x = np.ascontiguousarray(x)
+        self.cut_k = cut_k  # evaluate the init pass's extra cut at a sample quantile of rank cut_k
         self.comm = comm  # callable: obj -> list of objs from every rank (rank order)
         self.kept = None
         self.cur = self.x
@@ -48,6 +49,16 @@ class NumpyShard:
             out["nonfinite"] += r["nonfinite"]
             S += r["S"] + r["n"] * (r["x0"] - out["x0"])
         out["S"] = S
+        if self.cut_k is not None and self.comm is None and x.size > 2:
+            n = x.size
+            m = min(n, 2048)
+            pos = np.arange(m) if n == m else (np.arange(m, dtype=np.int64) * n) // m + (n // m) // 2
+            smp = np.sort(x[pos])
+            q = int(min(max((self.cut_k - 0.5) / n * m, 0), m - 1))
+            t0 = np.float64(smp[q])
+            xd = x.astype(np.float64)
+            out.update(has_cut=1, t0=float(t0), c_lt0=int((x < t0).sum()), c_eq0=int((x == t0).sum()),
+                       N0=float(np.sum(t0 - xd[x < t0])), P0=float(np.sum(xd[x > t0] - t0)))
         return out
 
     def pass_(self, t, lo, hi, compact):
@@ -81,8 +92,8 @@ class NumpyShard:
         return float(np.partition(allz, r - 1)[r - 1])
 
 
-def drive(x, k, dtype, comm=None, config=None):
+def drive(x, k, dtype, comm=None, config=None, cut=False):
     import paper_1104_2732_b200 as cp
-    be = NumpyShard(x, comm)
+    be = NumpyShard(x, comm, cut_k=k if cut else None)
     n = x.size if comm is None else sum(comm(x.size))
     return cp.drive_host(n, k, dtype, be.init, be.pass_, be.adopt, be.select, config)

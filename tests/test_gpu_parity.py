@@ -51,6 +51,24 @@ def test_init_reduction(cp, dtype, n, off):
     assert s["S"] == pytest.approx(ref, rel=REL[dtype] * 10, abs=1e-9 * x.size)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("dist", ["uniform", "mix2", "dup256", "cauchy"])
+def test_init_extra_cut(cp, dtype, dist):
+    """R23: the init pass's extra cut — t0 is an element of x near the median rank, and the counts /
+    positive-part sums at t0 match the oracle's direct evaluation."""
+    n = 2_000_003
+    x = datagen.make(dist, n, dtype)
+    s = cp.init_stats(tdev(x))
+    assert s["has_cut"] == 1
+    t0 = s["t0"]
+    assert np.any(x == t0)
+    r = O.pass_stats(x, t0, -math.inf, math.inf)
+    assert (s["c_lt0"], s["c_eq0"]) == (r["c_lt"], r["c_eq"])
+    assert s["N0"] == pytest.approx(float(r["N"]), rel=REL[dtype], abs=1e-300)
+    assert s["P0"] == pytest.approx(float(r["P"]), rel=REL[dtype], abs=1e-300)
+    assert abs(r["c_lt"] - n / 2) < 0.05 * n          # a 2048-sample quantile lands near the median
+
+
 def test_init_counts_nonfinite(cp):
     for bad in (np.nan, np.inf, -np.inf):
         x = datagen.make("normal", 100_000, "f32")
@@ -139,12 +157,12 @@ def test_select_distributions_forced_cp(cp, dtype):
         xd = tdev(x)
         for k in sorted({1, 2, n // 10, O.median_rank(n), n - 1, n}):
             want = float(O.order_statistic(x, k))
-            for zc, sc in ((0, 0), (512, 0), (50_000, 0), (0, 64), (10**9, 1000)):
-                cp.set_config(force_cp=1, z_cap=zc, select_cap=sc)
+            for zc, sc, cut in ((0, 0, 1), (0, 0, 0), (512, 0, 1), (50_000, 0, 0), (0, 64, 1), (10**9, 1000, 1)):
+                cp.set_config(force_cp=1, z_cap=zc, select_cap=sc, init_cut=cut)
                 v, info = cp.select_kth(xd, k, return_info=True)
-                assert canon(v) == want, (dist, k, zc, sc, info)
+                assert canon(v) == want, (dist, k, zc, sc, cut, info)
                 assert info["passes"] == info["cp_iters"] + 1
-    cp.set_config(force_cp=0, z_cap=0, select_cap=0)
+    cp.set_config(force_cp=0, z_cap=0, select_cap=0, init_cut=1)
 
 
 def test_select_direct_path_config0(cp):

@@ -30,9 +30,10 @@ def test_driver_matches_oracle_distributions(dtype):
         for k in sorted({1, 2, n // 10, O.median_rank(n), n - 1, n}):
             for cfg in ({"force_cp": 1, "z_cap": 64}, {"force_cp": 1, "z_cap": 4096}, {},
                         {"force_cp": 1, "select_cap": 16}, {"force_cp": 1, "select_cap": 1, "z_cap": 10_000}):
-                v, info, trace = drive(x, k, dtype, config=cfg)
-                assert canon(v) == float(O.order_statistic(x, k)), (dist, k, cfg, info)
-                assert info["passes"] == info["cp_iters"] + 1          # maxit+1 reductions
+                for cut in (False, True):
+                    v, info, trace = drive(x, k, dtype, config=cfg, cut=cut)
+                    assert canon(v) == float(O.order_statistic(x, k)), (dist, k, cfg, cut, info)
+                    assert info["passes"] == info["cp_iters"] + 1          # maxit+1 reductions
 
 
 def test_driver_tiny_all_ranks_with_ties_and_signed_zero():
@@ -45,16 +46,18 @@ def test_driver_tiny_all_ranks_with_ties_and_signed_zero():
             for k in range(1, n + 1):
                 for cfg in ({"force_cp": 1, "z_cap": 1}, {"force_cp": 1, "z_cap": 3},
                             {"force_cp": 1, "select_cap": 1}):
-                    v, info, _ = drive(xd, k, dtype, config=cfg)
-                    assert canon(v) == float(O.order_statistic(xd, k))
+                    for cut in (False, True):
+                        v, info, _ = drive(xd, k, dtype, config=cfg, cut=cut)
+                        assert canon(v) == float(O.order_statistic(xd, k))
 
 
 def test_driver_trace_matches_oracle_replay():
-    """Every traced pass: counts exact, F within rel 1e-12 of the oracle's direct long-double F."""
+    """Every traced pass (incl. the init pass's extra cut): counts exact, F within rel 1e-12 of the
+    oracle's direct long-double F."""
     x = datagen.make("mix1", 50_000, "f64")
     k = O.median_rank(x.size)
-    v, info, trace = drive(x, k, "f64", config={"force_cp": 1, "z_cap": 100})
-    assert trace
+    v, info, trace = drive(x, k, "f64", config={"force_cp": 1, "z_cap": 100}, cut=True)
+    assert trace and trace[0]["kind"] == 2
     for row in trace:
         ref = O.eval_at(x, k, row["t"], -math.inf, math.inf)
         assert row["c_lt"] == ref["c_lt"] and row["c_eq"] == ref["c_eq"]
