@@ -95,7 +95,8 @@ typedef struct {
   double vmin, vmax;      /* exact */
   uint64_t cnt_min, cnt_max, nonfinite;
   double x0;              /* the shift x[0] */
-  double S;               /* sum_i (x_i - x0), fp64 */
+  double S;               /* sum_i (x_i - x0), fp64 (0 when has_cut: the first iterate then comes
+                             from the cut's sums and the pass skips this sum) */
   uint64_t has_cut;       /* 1 if the pass also evaluated the extra cut t0 (R23): */
   double t0;              /*   the cut (an element of x) */
   uint64_t c_lt0, c_eq0;  /*   #{x < t0}, #{x == t0} */

@@ -255,7 +255,12 @@ struct GpuBackend : Backend {
     CK(cudaStreamSynchronize(ctx->stream));
     read_ms();
     const DevInit& r = *ctx->h_init;
-    if (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax)) {
+    // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
+    // cut (which skips the shifted sum), as c_lt0 + c_eq0 + c_gt0 < n
+    const bool suspicious = cut ? (!std::isfinite(r.N0) || !std::isfinite(r.P0) || !std::isfinite(r.vmin) ||
+                                   !std::isfinite(r.vmax) || r.c_lt0 + r.c_eq0 + r.pad != n)
+                                : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
+    if (suspicious) {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, true));
       launches += 1;
       if (sync_result) {
@@ -610,8 +615,16 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   uint64_t D_lo = 0;                   // elements of x below the current array
   bool on_z = false;                   // the current array is a compacted bracket
   // first iterate: mean of the interior (App. A) from the shifted sum
-  double t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
-                          (double)m;
+  double t;
+  if (rec.has_cut && rec.t0 <= rec.vmin)  // the cut sits on the minimum: P0 = sum (x - min)
+    t = rec.vmin + (double)(((long double)rec.P0 - (long double)rec.cnt_max * ((long double)rec.vmax - rec.vmin)) /
+                           (long double)m);
+  else if (rec.has_cut && rec.t0 >= rec.vmax)  // on the maximum: N0 = sum (max - x)
+    t = rec.vmax - (double)(((long double)rec.N0 - (long double)rec.cnt_min * ((long double)rec.vmax - rec.vmin)) /
+                           (long double)m);
+  else  // (a cut strictly inside replaces this below)
+    t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
+                     (double)m;
   int slow = 0;
   bool bisect = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;

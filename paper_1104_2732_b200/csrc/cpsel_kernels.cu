@@ -191,6 +191,7 @@ __device__ __forceinline__ void combine(InitPartial& a, const InitPartial& b) {
   a.nonfinite += b.nonfinite;
   a.N0 += b.N0;
   a.P0 += b.P0;
+  a.pad2 += b.pad2;
   a.c_lt0 += b.c_lt0;
   a.c_eq0 += b.c_eq0;
 }
@@ -256,34 +257,39 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
   double S;
   T g[4];
   T t0;
-  unsigned clt0 = 0, ceq0 = 0;
+  unsigned clt0 = 0, ceq0 = 0, cgt0 = 0;
+  // with the cut the shifted sum is not needed (the first iterate comes from the cut's sums) and
+  // c_lt0 + c_eq0 + c_gt0 < n exposes NaN; the CHECKED re-run still computes everything
+  static constexpr bool SUM = !CUT || CHECKED;
   T gN[4], gP[4];
   double N0 = 0, P0 = 0;
   __device__ InitFn(T x0_) : mn(tinf<T>()), mx(-tinf<T>()), x0(x0_), cmn(0), cmx(0), nonfin(0), S(0) {}
   __device__ __forceinline__ void cut(float v, float& n_, float& p_) {
     asm("{\n\t.reg .pred plt, pgt, peq;\n\t.reg .f32 d;\n\t"
-        "setp.lt.f32 plt, %4, %5;\n\t"
-        "setp.gt.f32 pgt, %4, %5;\n\t"
-        "setp.eq.f32 peq, %4, %5;\n\t"
-        "sub.rn.f32 d, %5, %4;\n\t"
+        "setp.lt.f32 plt, %5, %6;\n\t"
+        "setp.gt.f32 pgt, %5, %6;\n\t"
+        "setp.eq.f32 peq, %5, %6;\n\t"
+        "sub.rn.f32 d, %6, %5;\n\t"
         "@plt add.u32 %0, %0, 1;\n\t"
         "@peq add.u32 %1, %1, 1;\n\t"
+        "@pgt add.u32 %4, %4, 1;\n\t"
         "@plt add.rn.f32 %2, %2, d;\n\t"
         "@pgt sub.rn.f32 %3, %3, d;\n\t}"
-        : "+r"(clt0), "+r"(ceq0), "+f"(n_), "+f"(p_)
+        : "+r"(clt0), "+r"(ceq0), "+f"(n_), "+f"(p_), "+r"(cgt0)
         : "f"(v), "f"(t0));
   }
   __device__ __forceinline__ void cut(double v, double& n_, double& p_) {
     asm("{\n\t.reg .pred plt, pgt, peq;\n\t.reg .f64 d;\n\t"
-        "setp.lt.f64 plt, %4, %5;\n\t"
-        "setp.gt.f64 pgt, %4, %5;\n\t"
-        "setp.eq.f64 peq, %4, %5;\n\t"
-        "sub.rn.f64 d, %5, %4;\n\t"
+        "setp.lt.f64 plt, %5, %6;\n\t"
+        "setp.gt.f64 pgt, %5, %6;\n\t"
+        "setp.eq.f64 peq, %5, %6;\n\t"
+        "sub.rn.f64 d, %6, %5;\n\t"
         "@plt add.u32 %0, %0, 1;\n\t"
         "@peq add.u32 %1, %1, 1;\n\t"
+        "@pgt add.u32 %4, %4, 1;\n\t"
         "@plt add.rn.f64 %2, %2, d;\n\t"
         "@pgt sub.rn.f64 %3, %3, d;\n\t}"
-        : "+r"(clt0), "+r"(ceq0), "+d"(n_), "+d"(p_)
+        : "+r"(clt0), "+r"(ceq0), "+d"(n_), "+d"(p_), "+r"(cgt0)
         : "d"(v), "d"(t0));
   }
   __device__ __forceinline__ void slow(T v) {
@@ -295,7 +301,7 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
     if (CUT) gN[0] = gN[1] = gN[2] = gN[3] = gP[0] = gP[1] = gP[2] = gP[3] = T(0);
   }
   __device__ __forceinline__ void group_end() {
-    S += (double)((g[0] + g[1]) + (g[2] + g[3]));
+    if (SUM) S += (double)((g[0] + g[1]) + (g[2] + g[3]));
     if (CUT) {
       N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
       P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
@@ -306,7 +312,7 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
     const float lo = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
     const float hi = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
     if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); slow(v.z); slow(v.w); }
-    g[u & 3] += ((v.x - x0) + (v.y - x0)) + ((v.z - x0) + (v.w - x0));
+    if (SUM) g[u & 3] += ((v.x - x0) + (v.y - x0)) + ((v.z - x0) + (v.w - x0));
     if (CHECKED)
       nonfin += !(fabsf(v.x) <= FLT_MAX) + !(fabsf(v.y) <= FLT_MAX) + !(fabsf(v.z) <= FLT_MAX) + !(fabsf(v.w) <= FLT_MAX);
   }
@@ -314,7 +320,7 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
     if (CUT) { cut(v.x, gN[u & 3], gP[u & 3]); cut(v.y, gN[u & 3], gP[u & 3]); }
     const double lo = fmin(v.x, v.y), hi = fmax(v.x, v.y);
     if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); }
-    g[u & 3] += (v.x - x0) + (v.y - x0);
+    if (SUM) g[u & 3] += (v.x - x0) + (v.y - x0);
     if (CHECKED) nonfin += !(fabs(v.x) <= DBL_MAX) + !(fabs(v.y) <= DBL_MAX);
   }
   template <bool MASKED, typename V> __device__ __forceinline__ void vec(const V& v, bool ok, int u) {
@@ -342,6 +348,7 @@ __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
   p.N0 = f.N0; p.P0 = f.P0; p.c_lt0 = f.clt0; p.c_eq0 = f.ceq0;
+  p.pad2 = f.cgt0;  // c_gt0 rides in the spare word
   p = block_reduce(p);
   InitPartial id;
   id.vmin = tinf<double>(); id.vmax = -tinf<double>(); id.S = 0; id.pad = 0;
@@ -351,7 +358,8 @@ __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   if (grid_finish(p, static_cast<InitPartial*>(a.partials), a.ticket, &tot, id) && threadIdx.x == 0) {
     DevInit r;
     r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = tot.S; r.x0 = (double)x[0];
-    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite; r.pad = 0;
+    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite;
+    r.pad = tot.pad2;  // c_gt0
     r.t0 = CUT ? (double)f.t0 : 0.0;
     r.N0 = tot.N0; r.P0 = tot.P0; r.c_lt0 = tot.c_lt0; r.c_eq0 = tot.c_eq0;
     r.has_cut = CUT ? 1ull : 0ull;
@@ -359,35 +367,39 @@ __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   }
 }
 
-// R23: the extra cut of the init pass — the sample quantile at the target rank among 2048 evenly
-// strided samples (bitonic sort of order-preserving keys in shared memory, one CTA).
+// R23: the extra cut of the init pass — the sample quantile at the target rank among 1024 evenly
+// strided samples: one CTA of 1024 threads, one key per thread, bitonic sort with warp shuffles
+// for strides < 32 and shared memory above.
 template <typename T>
 __global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ x, uint64_t n, uint64_t k, T* t0) {
-  constexpr int S = 2048;
+  constexpr int S = 1024;
   __shared__ unsigned long long key[S];
+  const int i = threadIdx.x;
   const uint64_t m = n < (uint64_t)S ? n : (uint64_t)S;
-  for (int i = threadIdx.x; i < S; i += blockDim.x) {
-    if ((uint64_t)i < m) {
-      const uint64_t pos = (n == m) ? (uint64_t)i : ((uint64_t)i * n) / m + (n / m) / 2;
-      key[i] = okey(x[pos]);
-    } else {
-      key[i] = ~0ull;  // padding sorts last
-    }
+  unsigned long long v = ~0ull;  // padding sorts last
+  if ((uint64_t)i < m) {
+    const uint64_t pos = (n == m) ? (uint64_t)i : ((uint64_t)i * n) / m + (n / m) / 2;
+    v = okey(x[pos]);
   }
-  __syncthreads();
   for (int size = 2; size <= S; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = ((lo & size) == 0);
-        const unsigned long long a = key[lo], b = key[hi];
-        if ((a > b) == up) { key[lo] = b; key[hi] = a; }
+      unsigned long long w;
+      if (stride >= 32) {
+        key[i] = v;
+        __syncthreads();
+        w = key[i ^ stride];
+        __syncthreads();
+      } else {
+        w = __shfl_xor_sync(FULL, v, stride);
       }
-      __syncthreads();
+      const bool up = (i & size) == 0, lower = (i & stride) == 0;
+      const unsigned long long lo = v < w ? v : w, hi = v < w ? w : v;
+      v = (up == lower) ? lo : hi;
     }
   }
-  if (threadIdx.x == 0) {
+  key[i] = v;
+  __syncthreads();
+  if (i == 0) {
     double q = ((double)k - 0.5) / (double)n * (double)m;
     uint64_t idx = q < 0 ? 0 : (uint64_t)q;
     if (idx >= m) idx = m - 1;
@@ -1080,6 +1092,25 @@ __device__ __forceinline__ float key_mid_dev(float yL, float yR) {
   return (float)from_key_f32((unsigned long long)(a + (b - a) / 2));
 }
 
+// ascending bitonic sort of S (power of 2) keys in shared memory, all threads of the CTA
+__device__ void block_bitonic_sort(unsigned long long* key, int S) {
+  for (int size = 2; size <= S; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = ((lo & size) == 0);
+        const unsigned long long x = key[lo], y = key[hi];
+        if ((x > y) == up) { key[lo] = y; key[hi] = x; }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+constexpr int kBatchSample = 2048;   // samples of the init pass's extra cut (R23)
+constexpr int kBatchFinish = 4096;   // kept halves this small are finished by a shared-memory sort
+
 struct BatchState {
   const float* cur;
   unsigned long long n_cur, c_le_L, c_lt_R, D_lo, m, k_r;
@@ -1132,13 +1163,38 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
     __syncthreads();
     if (st.col >= (int)a.C) break;
     const float* x = a.S + (size_t)st.col * n;
-    // ---- a1: init reduction over the column
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(dyn_smem);
+    // ---- R23: extra cut at the sample quantile of rank k (strided samples, smem bitonic sort)
+    const bool cut = n > 2;
+    if (cut) {
+      const uint64_t ms = n < (uint64_t)kBatchSample ? n : (uint64_t)kBatchSample;
+      for (int i = threadIdx.x; i < kBatchSample; i += kBlock) {
+        if ((uint64_t)i < ms) {
+          const uint64_t pos = (n == ms) ? (uint64_t)i : ((uint64_t)i * n) / ms + (n / ms) / 2;
+          keys[i] = okey(x[pos]);
+        } else {
+          keys[i] = ~0ull;
+        }
+      }
+      __syncthreads();
+      block_bitonic_sort(keys, kBatchSample);
+      if (threadIdx.x == 0) {
+        double q = ((double)k - 0.5) / (double)n * (double)ms;
+        uint64_t idx = q < 0 ? 0 : (uint64_t)q;
+        if (idx >= ms) idx = ms - 1;
+        st.tq = (float)from_key_f32(keys[idx]);
+      }
+      __syncthreads();
+    }
+    // ---- a1: init reduction over the column (+ the extra cut)
     {
-      InitFn<float, true> f(x[0]);
+      InitFn<float, true, true> f(x[0]);
+      f.t0 = cut ? st.tq : x[0];
       stream_array<float, 4>(x, n, f, 0u, 1u);
       InitPartial p;
       p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
       p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
+      p.N0 = f.N0; p.P0 = f.P0; p.c_lt0 = f.clt0; p.c_eq0 = f.ceq0;
       p = block_reduce(p);
       if (threadIdx.x == 0) {
         st.phase = 0;
@@ -1161,6 +1217,21 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
           const double x0 = (double)x[0];
           st.t = x0 + (p.S - (double)p.cnt_min * (p.vmin - x0) - (double)p.cnt_max * (p.vmax - x0)) / (double)st.m;
+          const float t0 = st.tq;
+          if (cut && (double)t0 > p.vmin && (double)t0 < p.vmax) {  // the extra cut (as the host driver)
+            const unsigned long long c_lt = p.c_lt0, c_le = p.c_lt0 + p.c_eq0;
+            if (c_lt < k && k <= c_le) {
+              st.result = t0; st.phase = 1;
+            } else if (c_le < k) {
+              const double L_hi = p.P0 - (double)p.cnt_max * (p.vmax - (double)t0);
+              st.yL = t0; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
+              st.t = (double)t0 + L_hi / (double)st.m;
+            } else {
+              const double L_lo = p.N0 - (double)p.cnt_min * ((double)t0 - p.vmin);
+              st.yR = t0; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
+              st.t = (double)t0 - L_lo / (double)st.m;
+            }
+          }
         }
       }
       __syncthreads();
@@ -1220,7 +1291,7 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
             st.cur_buf = st.tgt;
             st.D_lo = st.c_le_L;
             st.on_z = 1;
-            if (st.m <= 32) {
+            if (st.m <= (unsigned long long)kBatchFinish) {
               st.k_r = k - st.c_le_L;  // rank inside the kept half
               st.phase = 2;
             }
@@ -1235,24 +1306,15 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
       }
       __syncthreads();
     }
-    // ---- a5: exact finish on <= 32 elements (warp 0 counts ranks)
-    if (st.phase == 2 && threadIdx.x < 32) {
-      const int lane = threadIdx.x;
+    // ---- a5: exact finish on <= kBatchFinish elements: shared-memory bitonic sort of the keys
+    if (st.phase == 2) {
       const int cnt = (int)st.n_cur;
-      const float v = lane < cnt ? st.cur[lane] : tinf<float>();
-      unsigned below = 0, le = 0;
-      for (int j = 0; j < cnt; ++j) {
-        const float w = __shfl_sync(FULL, v, j);
-        below += (w < v);
-        le += (w <= v);
-      }
-      const bool mine = lane < cnt && below < st.k_r && st.k_r <= le;
-      const unsigned who = __ballot_sync(FULL, mine);
-      const float sel = __shfl_sync(FULL, v, who ? __ffs(who) - 1 : 0);
-      if (lane == 0) {
-        st.result = who ? sel : __int_as_float(0x7fc00000);
-        if (!who) atomicAdd(&a.stats[2], 1ull);
-      }
+      for (int i = threadIdx.x; i < kBatchFinish; i += kBlock) keys[i] = i < cnt ? okey(st.cur[i]) : ~0ull;
+      __syncthreads();
+      int S2 = 64;
+      while (S2 < cnt) S2 <<= 1;
+      block_bitonic_sort(keys, S2);
+      if (threadIdx.x == 0) st.result = (float)from_key_f32(keys[st.k_r - 1]);
     }
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -294,7 +294,7 @@ cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int grid = sms * batched_blocks_per_sm();
   if ((uint32_t)grid > C) grid = (int)C;
-  const uint64_t cap = n / 2 + 1;
+  const uint64_t cap = n / 8 * 5 + 1;  // a column compacts once its bracket holds <= 5/8 of it
   const size_t scratch = (size_t)grid * 2 * cap * sizeof(float);
   const size_t need = scratch + 256;
   if (w.dev_bytes < need) {

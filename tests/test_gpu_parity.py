@@ -42,7 +42,9 @@ def host(t):
 @pytest.mark.parametrize("n,off", [(1, 0), (2, 1), (7, 3), (1_000_003, 0), (1_000_003, 1), (4_194_305, 3)])
 def test_init_reduction(cp, dtype, n, off):
     x = datagen.make("mix3", n + off, dtype)[off:]       # ragged tail + misaligned start
+    cp.set_config(init_cut=0)                            # the shifted sum is computed without the cut
     s = cp.init_stats(tdev(datagen.make("mix3", n + off, dtype))[off:])
+    cp.set_config(init_cut=1)
     rec = O.init_record(x)
     assert s["vmin"] == rec["min"] and s["vmax"] == rec["max"]
     assert s["cnt_min"] == rec["cnt_min"] and s["cnt_max"] == rec["cnt_max"] and s["nonfinite"] == 0
