@@ -60,8 +60,8 @@ typedef struct {
   int32_t record_trace;      /* 1: keep the per-iteration trace (cpsel_get_trace).  Default 1 */
   int32_t record_timing;     /* 1: time every kernel with CUDA events on the ctx stream (info / trace
                                 kernel_ms fields).  Default 0 */
-  int32_t init_cut;          /* 1: the init pass also evaluates one extra cut at a sample quantile of
-                                the target rank (R23), saving a full pass.  Default 1 */
+  int32_t init_cut;          /* 1: the init pass also evaluates two extra cuts at sample quantiles
+                                bracketing the target rank (R23), saving passes.  Default 1 */
   int32_t reserved;
 } cpsel_config;
 
@@ -97,10 +97,12 @@ typedef struct {
   double x0;              /* the shift x[0] */
   double S;               /* sum_i (x_i - x0), fp64 (0 when has_cut: the first iterate then comes
                              from the cut's sums and the pass skips this sum) */
-  uint64_t has_cut;       /* 1 if the pass also evaluated the extra cut t0 (R23): */
-  double t0;              /*   the cut (an element of x) */
-  uint64_t c_lt0, c_eq0;  /*   #{x < t0}, #{x == t0} */
-  double N0, P0;          /*   sum (t0-x)^+, sum (x-t0)^+ */
+  uint64_t has_cut;       /* 2 if the pass also evaluated the two extra cuts t_lo <= t_hi (R23): */
+  double t_lo, t_hi;      /*   sample quantiles bracketing rank k (elements of x) */
+  uint64_t c_lt_lo, c_eq_lo, c_lt_hi, c_eq_hi;  /* #{x<t_lo}, #{x==t_lo}, #{x<t_hi}, #{x==t_hi} */
+  double N_lo;            /*   sum (t_lo - x)^+ */
+  double P_hi;            /*   sum (x - t_hi)^+ */
+  double I_in;            /*   sum over t_lo < x < t_hi of (x - t_lo) */
 } cpsel_init_stats;
 
 /* One row per cutting-plane pass (R7 trace). */
@@ -167,8 +169,8 @@ cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t
  * (else CPSEL_EINVAL).  Computes every field of cpsel_pass_stats in a single read of x. */
 cpsel_status cpsel_eval(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, double t,
                         double y_lo, double y_hi, cpsel_pass_stats* out);
-/* The init reduction alone (step a1); with init_cut it also evaluates the extra cut at the
- * sample quantile of the median rank (R23). */
+/* The init reduction alone (step a1); with init_cut it also evaluates the two extra cuts at the
+ * sample quantiles bracketing the median rank (R23). */
 cpsel_status cpsel_init(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype,
                         cpsel_init_stats* out);
 /* The small-set exact selection alone (step a5): r-th smallest (1-based) of d_z[0..m). */

@@ -38,7 +38,7 @@ struct cpsel_ctx {
   unsigned long long* d_cursors = nullptr;
   DevPass* d_pass = nullptr;
   DevInit* d_init = nullptr;
-  void* d_t0 = nullptr;              // the extra cut of the init pass (R23)
+  void* d_t0 = nullptr;              // the two extra cuts of the init pass (R23)
   RadixState* d_radix = nullptr;
   unsigned int* d_hist = nullptr;
   DevPass* d_gather = nullptr;       // G x DevPass (sharded)
@@ -256,9 +256,10 @@ struct GpuBackend : Backend {
     read_ms();
     const DevInit& r = *ctx->h_init;
     // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
-    // cut (which skips the shifted sum), as c_lt0 + c_eq0 + c_gt0 < n
-    const bool suspicious = cut ? (!std::isfinite(r.N0) || !std::isfinite(r.P0) || !std::isfinite(r.vmin) ||
-                                   !std::isfinite(r.vmax) || r.c_lt0 + r.c_eq0 + r.pad != n)
+    // cuts (which skip the shifted sum), as #x<t_hi + #x=t_hi + #x>t_hi < n
+    const bool suspicious = cut ? (!std::isfinite(r.N_lo) || !std::isfinite(r.P_hi) || !std::isfinite(r.I_in) ||
+                                   !std::isfinite(r.vmin) || !std::isfinite(r.vmax) ||
+                                   r.c_lt_hi + r.c_eq_hi + r.c_gt_hi != n)
                                 : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
     if (suspicious) {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, true));
@@ -276,7 +277,9 @@ struct GpuBackend : Backend {
     const DevInit& r = *ctx->h_init;
     o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
     o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
-    o->has_cut = r.has_cut; o->t0 = r.t0; o->c_lt0 = r.c_lt0; o->c_eq0 = r.c_eq0; o->N0 = r.N0; o->P0 = r.P0;
+    o->has_cut = r.has_cut; o->t_lo = r.t_lo; o->t_hi = r.t_hi;
+    o->c_lt_lo = r.c_lt_lo; o->c_eq_lo = r.c_eq_lo; o->c_lt_hi = r.c_lt_hi; o->c_eq_hi = r.c_eq_hi;
+    o->N_lo = r.N_lo; o->P_hi = r.P_hi; o->I_in = r.I_in;
     return CPSEL_OK;
   }
   // two dense ping-pong buffers of m_dense elements; two segmented buffers (+ run tables) able to
@@ -615,45 +618,69 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   uint64_t D_lo = 0;                   // elements of x below the current array
   bool on_z = false;                   // the current array is a compacted bracket
   // first iterate: mean of the interior (App. A) from the shifted sum
-  double t;
-  if (rec.has_cut && rec.t0 <= rec.vmin)  // the cut sits on the minimum: P0 = sum (x - min)
-    t = rec.vmin + (double)(((long double)rec.P0 - (long double)rec.cnt_max * ((long double)rec.vmax - rec.vmin)) /
-                           (long double)m);
-  else if (rec.has_cut && rec.t0 >= rec.vmax)  // on the maximum: N0 = sum (max - x)
-    t = rec.vmax - (double)(((long double)rec.N0 - (long double)rec.cnt_min * ((long double)rec.vmax - rec.vmin)) /
-                           (long double)m);
-  else  // (a cut strictly inside replaces this below)
-    t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
-                     (double)m;
+  // first iterate: mean of the interior (App. A) from the shifted sum (replaced below when the init
+  // pass also evaluated the two extra cuts, R23)
+  double t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
+                          (double)m;
   int slow = 0;
   bool bisect = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
-  // R23: the init pass's extra cut at t0 (a sample quantile of the target rank) — one more cut of
-  // the cutting-plane model, evaluated in the same read of x as the init reduction
-  if (rec.has_cut && rec.t0 > rec.vmin && rec.t0 < rec.vmax) {
-    const double t0 = rec.t0;
-    const uint64_t c_lt = rec.c_lt0, c_le = rec.c_lt0 + rec.c_eq0;
-    cpsel_trace_row row{};
-    row.t = t0;
-    row.F = (double)(wP * (long double)rec.P0 + wN * (long double)rec.N0);
-    row.c_lt = c_lt;
-    row.c_eq = rec.c_eq0;
-    row.kind = 2;
-    if (c_lt < k && k <= c_le) {
+  // R23: the init pass's two extra cuts t_lo <= t_hi (sample quantiles bracketing rank k) — two more
+  // cuts of the cutting-plane model, evaluated in the same read of x as the init reduction.  N and P
+  // at both cuts follow from the pass's sums: N(t_lo) = N_lo, P(t_hi) = P_hi,
+  // P(t_lo) = I + P_hi + #{x>=t_hi}(t_hi-t_lo), N(t_hi) = N_lo + #{x<t_hi}(t_hi-t_lo) - I.
+  if (rec.has_cut) {
+    const long double tl = rec.t_lo, th = rec.t_hi, dlh = th - tl;
+    const long double N_tl = rec.N_lo, P_th = rec.P_hi;
+    const long double P_tl = (long double)rec.I_in + P_th + (long double)(n - rec.c_lt_hi) * dlh;
+    const long double N_th = N_tl + (long double)rec.c_lt_hi * dlh - (long double)rec.I_in;
+    auto row_of = [&](double tt, uint64_t clt, uint64_t ceq, long double Nt, long double Pt) {
+      cpsel_trace_row r{};
+      r.t = tt; r.F = (double)(wP * Pt + wN * Nt); r.c_lt = clt; r.c_eq = ceq; r.kind = 2;
+      return r;
+    };
+    bool settled = false;  // the target is below t_lo: t_hi carries no further information
+    if (rec.t_lo > rec.vmin && rec.t_lo < rec.vmax) {
+      const uint64_t c_lt = rec.c_lt_lo, c_le = rec.c_lt_lo + rec.c_eq_lo;
+      cpsel_trace_row row = row_of(rec.t_lo, c_lt, rec.c_eq_lo, N_tl, P_tl);
+      if (c_lt < k && k <= c_le) {
+        if (trace && cfg.record_trace) trace->push_back(row);
+        return done(rec.t_lo, 2);
+      }
+      if (c_le < k) {  // y_L <- t_lo
+        yL = rec.t_lo; N_L = N_tl; c_le_L = c_le; m = c_lt_R - c_le;
+        const long double L_hi = P_tl - (long double)(n - c_lt_R) * ((long double)yR - tl);  // P_R = 0
+        t = rec.t_lo + (double)(L_hi / (long double)m);
+      } else {  // y_R <- t_lo: interior ]min, t_lo[
+        const long double L_lo = N_tl - (long double)c_le_L * (tl - (long double)yL);  // N_L = 0
+        yR = rec.t_lo; P_R = P_tl; c_lt_R = c_lt; m = c_lt - c_le_L;
+        t = rec.t_lo - (double)(L_lo / (long double)m);
+        settled = true;
+      }
+      row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);
-      return done(t0, 2);
     }
-    if (c_le < k) {  // y_L <- t0: interior ]t0, max[
-      const long double L_hi = (long double)rec.P0 - (long double)rec.cnt_max * ((long double)rec.vmax - t0);
-      yL = t0; N_L = rec.N0; c_le_L = c_le; m = c_lt_R - c_le;
-      t = t0 + (double)(L_hi / (long double)m);
-    } else {  // y_R <- t0: interior ]min, t0[
-      const long double L_lo = (long double)rec.N0 - (long double)rec.cnt_min * (t0 - (long double)rec.vmin);
-      yR = t0; P_R = rec.P0; c_lt_R = c_lt; m = c_lt - c_le_L;
-      t = t0 - (double)(L_lo / (long double)m);
+    if (!settled && rec.t_hi > yL && rec.t_hi < rec.vmax) {
+      const uint64_t c_lt = rec.c_lt_hi, c_le = rec.c_lt_hi + rec.c_eq_hi;
+      cpsel_trace_row row = row_of(rec.t_hi, c_lt, rec.c_eq_hi, N_th, P_th);
+      if (c_lt < k && k <= c_le) {
+        if (trace && cfg.record_trace) trace->push_back(row);
+        return done(rec.t_hi, 2);
+      }
+      if (c_lt >= k) {  // y_R <- t_hi: interior ]y_L, t_hi[
+        // sum_{y_L<x<t_hi} (x - y_L): the pass's I when y_L = t_lo, else via N (App. A identity)
+        const long double L_lo = (yL == rec.t_lo) ? (long double)(c_lt - c_le_L) * dlh - (long double)rec.I_in
+                                                  : N_th - N_L - (long double)c_le_L * (th - (long double)yL);
+        yR = rec.t_hi; P_R = P_th; c_lt_R = c_lt; m = c_lt - c_le_L;
+        t = rec.t_hi - (double)(L_lo / (long double)m);
+      } else {  // y_L <- t_hi: interior ]t_hi, max[
+        const long double L_hi = P_th - (long double)(n - c_lt_R) * ((long double)yR - th);  // P_R = 0
+        yL = rec.t_hi; N_L = N_th; c_le_L = c_le; m = c_lt_R - c_le;
+        t = rec.t_hi + (double)(L_hi / (long double)m);
+      }
+      row.interior = m;
+      if (trace && cfg.record_trace) trace->push_back(row);
     }
-    row.interior = m;
-    if (trace && cfg.record_trace) trace->push_back(row);
   }
   for (uint32_t it = 1;; ++it) {
     if (it > cfg.max_iters) {

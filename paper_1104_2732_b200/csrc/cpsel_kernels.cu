@@ -191,9 +191,8 @@ __device__ __forceinline__ void combine(InitPartial& a, const InitPartial& b) {
   a.nonfinite += b.nonfinite;
   a.N0 += b.N0;
   a.P0 += b.P0;
-  a.pad2 += b.pad2;
-  a.c_lt0 += b.c_lt0;
-  a.c_eq0 += b.c_eq0;
+  a.I0 += b.I0;
+  a.cA += b.cA; a.cB += b.cB; a.cC += b.cC; a.cD += b.cD; a.cE += b.cE;
 }
 
 __device__ InitPartial block_reduce(InitPartial p) {
@@ -249,48 +248,66 @@ __device__ bool grid_finish(const P& mine, P* partials, unsigned int* ticket, P*
 // updates (min, #min) / (max, #max) only when the vector reaches the running extreme; the shifted
 // sum doubles as the non-finite detector (NaN/Inf make it non-finite; the host then re-runs the
 // CHECKED form, which counts non-finite elements exactly).
-// CUT: also evaluate the extra cut at t0 (R23) — counts and the two positive-part sums, as
-// predicated PTX (8 issue slots per element).
+// CUT: also evaluate the two extra cuts t_lo <= t_hi of R23 (sample quantiles bracketing the
+// target rank) in the same read: #x<t_lo, #x=t_lo, #x<t_hi, #x=t_hi, #x>t_hi, N_lo = sum (t_lo-x)^+,
+// P_hi = sum (x-t_hi)^+ and the bracket-interior sum I = sum_{t_lo<x<t_hi} (x-t_lo), as predicated
+// PTX (16 issue slots per element, balanced over the ALU and FMA pipes: three of the five
+// counters are per-thread float counters, exact below 2^24).
 template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
   T mn, mx, x0;
   unsigned cmn, cmx, nonfin;
   double S;
   T g[4];
-  T t0;
-  unsigned clt0 = 0, ceq0 = 0, cgt0 = 0;
-  // with the cut the shifted sum is not needed (the first iterate comes from the cut's sums) and
-  // c_lt0 + c_eq0 + c_gt0 < n exposes NaN; the CHECKED re-run still computes everything
+  T tl, th;
+  unsigned cA = 0, cC = 0;        // #x<t_lo, #x<t_hi
+  float fB = 0, fD = 0, fE = 0;   // #x=t_lo, #x=t_hi, #x>t_hi (exact while < 2^24 per thread)
+  // with the cuts the shifted sum is not needed (the first iterate comes from the cuts' sums) and
+  // a NaN shows as counts not adding up to n; the CHECKED re-run still computes everything
   static constexpr bool SUM = !CUT || CHECKED;
-  T gN[4], gP[4];
-  double N0 = 0, P0 = 0;
+  T gN[4], gP[4], gI[4];
+  double N0 = 0, P0 = 0, I0 = 0;
   __device__ InitFn(T x0_) : mn(tinf<T>()), mx(-tinf<T>()), x0(x0_), cmn(0), cmx(0), nonfin(0), S(0) {}
-  __device__ __forceinline__ void cut(float v, float& n_, float& p_) {
-    asm("{\n\t.reg .pred plt, pgt, peq;\n\t.reg .f32 d;\n\t"
-        "setp.lt.f32 plt, %5, %6;\n\t"
-        "setp.gt.f32 pgt, %5, %6;\n\t"
-        "setp.eq.f32 peq, %5, %6;\n\t"
-        "sub.rn.f32 d, %6, %5;\n\t"
-        "@plt add.u32 %0, %0, 1;\n\t"
-        "@peq add.u32 %1, %1, 1;\n\t"
-        "@pgt add.u32 %4, %4, 1;\n\t"
-        "@plt add.rn.f32 %2, %2, d;\n\t"
-        "@pgt sub.rn.f32 %3, %3, d;\n\t}"
-        : "+r"(clt0), "+r"(ceq0), "+f"(n_), "+f"(p_), "+r"(cgt0)
-        : "f"(v), "f"(t0));
+  __device__ __forceinline__ void cut(float v, float& n_, float& p_, float& i_) {
+    asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f32 dl, dh;\n\t"
+        "setp.lt.f32 pA, %8, %9;\n\t"
+        "setp.eq.f32 pB, %8, %9;\n\t"
+        "setp.lt.f32 pC, %8, %10;\n\t"
+        "setp.eq.f32 pD, %8, %10;\n\t"
+        "setp.gt.f32 pE, %8, %10;\n\t"
+        "setp.gt.and.f32 pI, %8, %9, pC;\n\t"
+        "sub.rn.f32 dl, %9, %8;\n\t"
+        "sub.rn.f32 dh, %8, %10;\n\t"
+        "@pA add.u32 %0, %0, 1;\n\t"
+        "@pC add.u32 %1, %1, 1;\n\t"
+        "@pB add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pD add.rn.f32 %3, %3, 0f3F800000;\n\t"
+        "@pE add.rn.f32 %4, %4, 0f3F800000;\n\t"
+        "@pA add.rn.f32 %5, %5, dl;\n\t"
+        "@pE add.rn.f32 %6, %6, dh;\n\t"
+        "@pI sub.rn.f32 %7, %7, dl;\n\t}"
+        : "+r"(cA), "+r"(cC), "+f"(fB), "+f"(fD), "+f"(fE), "+f"(n_), "+f"(p_), "+f"(i_)
+        : "f"(v), "f"(tl), "f"(th));
   }
-  __device__ __forceinline__ void cut(double v, double& n_, double& p_) {
-    asm("{\n\t.reg .pred plt, pgt, peq;\n\t.reg .f64 d;\n\t"
-        "setp.lt.f64 plt, %5, %6;\n\t"
-        "setp.gt.f64 pgt, %5, %6;\n\t"
-        "setp.eq.f64 peq, %5, %6;\n\t"
-        "sub.rn.f64 d, %6, %5;\n\t"
-        "@plt add.u32 %0, %0, 1;\n\t"
-        "@peq add.u32 %1, %1, 1;\n\t"
-        "@pgt add.u32 %4, %4, 1;\n\t"
-        "@plt add.rn.f64 %2, %2, d;\n\t"
-        "@pgt sub.rn.f64 %3, %3, d;\n\t}"
-        : "+r"(clt0), "+r"(ceq0), "+d"(n_), "+d"(p_), "+r"(cgt0)
-        : "d"(v), "d"(t0));
+  __device__ __forceinline__ void cut(double v, double& n_, double& p_, double& i_) {
+    asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f64 dl, dh;\n\t"
+        "setp.lt.f64 pA, %8, %9;\n\t"
+        "setp.eq.f64 pB, %8, %9;\n\t"
+        "setp.lt.f64 pC, %8, %10;\n\t"
+        "setp.eq.f64 pD, %8, %10;\n\t"
+        "setp.gt.f64 pE, %8, %10;\n\t"
+        "setp.gt.and.f64 pI, %8, %9, pC;\n\t"
+        "sub.rn.f64 dl, %9, %8;\n\t"
+        "sub.rn.f64 dh, %8, %10;\n\t"
+        "@pA add.u32 %0, %0, 1;\n\t"
+        "@pC add.u32 %1, %1, 1;\n\t"
+        "@pB add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pD add.rn.f32 %3, %3, 0f3F800000;\n\t"
+        "@pE add.rn.f32 %4, %4, 0f3F800000;\n\t"
+        "@pA add.rn.f64 %5, %5, dl;\n\t"
+        "@pE add.rn.f64 %6, %6, dh;\n\t"
+        "@pI sub.rn.f64 %7, %7, dl;\n\t}"
+        : "+r"(cA), "+r"(cC), "+f"(fB), "+f"(fD), "+f"(fE), "+d"(n_), "+d"(p_), "+d"(i_)
+        : "d"(v), "d"(tl), "d"(th));
   }
   __device__ __forceinline__ void slow(T v) {
     if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
@@ -298,17 +315,24 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
   }
   __device__ __forceinline__ void group_begin() {
     g[0] = g[1] = g[2] = g[3] = T(0);
-    if (CUT) gN[0] = gN[1] = gN[2] = gN[3] = gP[0] = gP[1] = gP[2] = gP[3] = T(0);
+    if (CUT)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) gN[u] = gP[u] = gI[u] = T(0);
   }
   __device__ __forceinline__ void group_end() {
     if (SUM) S += (double)((g[0] + g[1]) + (g[2] + g[3]));
     if (CUT) {
       N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
       P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+      I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
     }
   }
   __device__ __forceinline__ void vec_elems(const float4& v, int u) {
-    if (CUT) { cut(v.x, gN[u & 3], gP[u & 3]); cut(v.y, gN[u & 3], gP[u & 3]); cut(v.z, gN[u & 3], gP[u & 3]); cut(v.w, gN[u & 3], gP[u & 3]); }
+    if (CUT) {
+      const int w = u & 3;
+      cut(v.x, gN[w], gP[w], gI[w]); cut(v.y, gN[w], gP[w], gI[w]);
+      cut(v.z, gN[w], gP[w], gI[w]); cut(v.w, gN[w], gP[w], gI[w]);
+    }
     const float lo = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
     const float hi = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
     if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); slow(v.z); slow(v.w); }
@@ -317,7 +341,10 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
       nonfin += !(fabsf(v.x) <= FLT_MAX) + !(fabsf(v.y) <= FLT_MAX) + !(fabsf(v.z) <= FLT_MAX) + !(fabsf(v.w) <= FLT_MAX);
   }
   __device__ __forceinline__ void vec_elems(const double2& v, int u) {
-    if (CUT) { cut(v.x, gN[u & 3], gP[u & 3]); cut(v.y, gN[u & 3], gP[u & 3]); }
+    if (CUT) {
+      const int w = u & 3;
+      cut(v.x, gN[w], gP[w], gI[w]); cut(v.y, gN[w], gP[w], gI[w]);
+    }
     const double lo = fmin(v.x, v.y), hi = fmax(v.x, v.y);
     if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); }
     if (SUM) g[u & 3] += (v.x - x0) + (v.y - x0);
@@ -332,7 +359,7 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
     group_begin();
     slow(v);
     g[0] = v - x0;
-    if (CUT) cut(v, gN[0], gP[0]);
+    if (CUT) cut(v, gN[0], gP[0], gI[0]);
     if (CHECKED) nonfin += !(fabs(v) <= (sizeof(T) == 4 ? (T)FLT_MAX : (T)DBL_MAX));
     group_end();
   }
@@ -342,27 +369,32 @@ template <typename T, int UNROLL, bool CHECKED, bool CUT>
 __global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
   const T* x = static_cast<const T*>(a.x);
   InitFn<T, CHECKED, CUT> f(x[0]);
-  if (CUT) f.t0 = *static_cast<const T*>(a.t0);
+  if (CUT) {
+    f.tl = static_cast<const T*>(a.t0)[0];
+    f.th = static_cast<const T*>(a.t0)[1];
+  }
   stream_array<T, UNROLL>(x, a.n, f, blockIdx.x, gridDim.x);
   InitPartial p;
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
-  p.N0 = f.N0; p.P0 = f.P0; p.c_lt0 = f.clt0; p.c_eq0 = f.ceq0;
-  p.pad2 = f.cgt0;  // c_gt0 rides in the spare word
+  p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
+  p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = f.cC; p.cD = (unsigned long long)f.fD;
+  p.cE = (unsigned long long)f.fE;
   p = block_reduce(p);
   InitPartial id;
   id.vmin = tinf<double>(); id.vmax = -tinf<double>(); id.S = 0; id.pad = 0;
   id.cnt_min = id.cnt_max = id.nonfinite = id.pad2 = 0;
-  id.N0 = id.P0 = 0; id.c_lt0 = id.c_eq0 = 0;
+  id.N0 = id.P0 = id.I0 = 0; id.cA = id.cB = id.cC = id.cD = id.cE = 0;
   InitPartial tot;
   if (grid_finish(p, static_cast<InitPartial*>(a.partials), a.ticket, &tot, id) && threadIdx.x == 0) {
     DevInit r;
     r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = tot.S; r.x0 = (double)x[0];
-    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite;
-    r.pad = tot.pad2;  // c_gt0
-    r.t0 = CUT ? (double)f.t0 : 0.0;
-    r.N0 = tot.N0; r.P0 = tot.P0; r.c_lt0 = tot.c_lt0; r.c_eq0 = tot.c_eq0;
-    r.has_cut = CUT ? 1ull : 0ull;
+    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite; r.pad = 0;
+    r.t_lo = CUT ? (double)f.tl : 0.0;
+    r.t_hi = CUT ? (double)f.th : 0.0;
+    r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
+    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB; r.c_lt_hi = tot.cC; r.c_eq_hi = tot.cD; r.c_gt_hi = tot.cE;
+    r.has_cut = CUT ? 2ull : 0ull;
     *a.out = r;
   }
 }
@@ -400,11 +432,16 @@ __global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ 
   key[i] = v;
   __syncthreads();
   if (i == 0) {
-    double q = ((double)k - 0.5) / (double)n * (double)m;
-    uint64_t idx = q < 0 ? 0 : (uint64_t)q;
-    if (idx >= m) idx = m - 1;
-    const unsigned long long kk = key[idx];
-    *t0 = (T)(sizeof(T) == 4 ? from_key_f32(kk) : from_key_f64(kk));
+    // ranks q -/+ 3.5 binomial standard deviations (+2): the target lies between the two cuts with
+    // overwhelming probability on any input order (the cuts are exact either way)
+    const double md = (double)m;
+    const double q = ((double)k - 0.5) / (double)n * md;
+    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+    const double ql = floor(q - w), qh = ceil(q + w);
+    const uint64_t il = ql < 0 ? 0 : (uint64_t)ql;
+    const uint64_t ih = qh >= md ? m - 1 : (uint64_t)qh;
+    t0[0] = (T)(sizeof(T) == 4 ? from_key_f32(key[il]) : from_key_f64(key[il]));
+    t0[1] = (T)(sizeof(T) == 4 ? from_key_f32(key[ih]) : from_key_f64(key[ih]));
   }
 }
 
@@ -1116,7 +1153,7 @@ struct BatchState {
   unsigned long long n_cur, c_le_L, c_lt_R, D_lo, m, k_r;
   unsigned long long cursors[2];
   double t;
-  float yL, yR, tq, result;
+  float yL, yR, tq, result, cut_lo, cut_hi;
   int col, on_z, slow, bisect, phase, compact, cur_buf, tgt, side, iters;
 };
 
@@ -1164,7 +1201,7 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
     if (st.col >= (int)a.C) break;
     const float* x = a.S + (size_t)st.col * n;
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(dyn_smem);
-    // ---- R23: extra cut at the sample quantile of rank k (strided samples, smem bitonic sort)
+    // ---- R23: two extra cuts at sample quantiles bracketing rank k (strided samples, smem sort)
     const bool cut = n > 2;
     if (cut) {
       const uint64_t ms = n < (uint64_t)kBatchSample ? n : (uint64_t)kBatchSample;
@@ -1179,22 +1216,29 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
       __syncthreads();
       block_bitonic_sort(keys, kBatchSample);
       if (threadIdx.x == 0) {
-        double q = ((double)k - 0.5) / (double)n * (double)ms;
-        uint64_t idx = q < 0 ? 0 : (uint64_t)q;
-        if (idx >= ms) idx = ms - 1;
-        st.tq = (float)from_key_f32(keys[idx]);
+        const double md = (double)ms;
+        const double q = ((double)k - 0.5) / (double)n * md;
+        const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+        const double ql = floor(q - w), qh = ceil(q + w);
+        const uint64_t il = ql < 0 ? 0 : (uint64_t)ql;
+        const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
+        st.cut_lo = (float)from_key_f32(keys[il]);
+        st.cut_hi = (float)from_key_f32(keys[ih]);
       }
       __syncthreads();
     }
-    // ---- a1: init reduction over the column (+ the extra cut)
+    // ---- a1: init reduction over the column (+ the two extra cuts)
     {
       InitFn<float, true, true> f(x[0]);
-      f.t0 = cut ? st.tq : x[0];
+      f.tl = cut ? st.cut_lo : x[0];
+      f.th = cut ? st.cut_hi : x[0];
       stream_array<float, 4>(x, n, f, 0u, 1u);
       InitPartial p;
       p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
       p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
-      p.N0 = f.N0; p.P0 = f.P0; p.c_lt0 = f.clt0; p.c_eq0 = f.ceq0;
+      p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
+      p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = f.cC; p.cD = (unsigned long long)f.fD;
+      p.cE = (unsigned long long)f.fE;
       p = block_reduce(p);
       if (threadIdx.x == 0) {
         st.phase = 0;
@@ -1217,19 +1261,39 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
           const double x0 = (double)x[0];
           st.t = x0 + (p.S - (double)p.cnt_min * (p.vmin - x0) - (double)p.cnt_max * (p.vmax - x0)) / (double)st.m;
-          const float t0 = st.tq;
-          if (cut && (double)t0 > p.vmin && (double)t0 < p.vmax) {  // the extra cut (as the host driver)
-            const unsigned long long c_lt = p.c_lt0, c_le = p.c_lt0 + p.c_eq0;
-            if (c_lt < k && k <= c_le) {
-              st.result = t0; st.phase = 1;
-            } else if (c_le < k) {
-              const double L_hi = p.P0 - (double)p.cnt_max * (p.vmax - (double)t0);
-              st.yL = t0; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
-              st.t = (double)t0 + L_hi / (double)st.m;
-            } else {
-              const double L_lo = p.N0 - (double)p.cnt_min * ((double)t0 - p.vmin);
-              st.yR = t0; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
-              st.t = (double)t0 - L_lo / (double)st.m;
+          if (cut) {  // the two extra cuts, exactly as the host driver applies them
+            const double tl = st.cut_lo, th = st.cut_hi, dlh = th - tl;
+            const double P_tl = p.I0 + p.P0 + (double)(n - p.cC) * dlh;
+            bool settled = false;
+            if (tl > p.vmin && tl < p.vmax) {
+              const unsigned long long c_lt = p.cA, c_le = p.cA + p.cB;
+              if (c_lt < k && k <= c_le) {
+                st.result = (float)tl; st.phase = 1; settled = true;
+              } else if (c_le < k) {
+                st.yL = (float)tl; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
+                st.t = tl + (P_tl - (double)(n - st.c_lt_R) * ((double)st.yR - tl)) / (double)st.m;
+              } else {
+                const double L_lo = p.N0 - (double)st.c_le_L * (tl - (double)st.yL);
+                st.yR = (float)tl; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
+                st.t = tl - L_lo / (double)st.m;
+                settled = true;
+              }
+            }
+            if (!settled && th > (double)st.yL && th < p.vmax) {
+              const unsigned long long c_lt = p.cC, c_le = p.cC + p.cD;
+              if (c_lt < k && k <= c_le) {
+                st.result = (float)th; st.phase = 1;
+              } else if (c_lt >= k) {
+                const double N_th = p.N0 + (double)p.cC * dlh - p.I0;
+                const double L_lo = ((double)st.yL == tl) ? (double)(c_lt - st.c_le_L) * dlh - p.I0
+                                                          : N_th - (double)st.c_le_L * (th - (double)st.yL);
+                st.yR = (float)th; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
+                st.t = th - L_lo / (double)st.m;
+              } else {
+                const double L_hi = p.P0 - (double)(n - st.c_lt_R) * ((double)st.yR - th);
+                st.yL = (float)th; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
+                st.t = th + L_hi / (double)st.m;
+              }
             }
           }
         }

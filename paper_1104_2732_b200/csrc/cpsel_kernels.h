@@ -23,9 +23,9 @@ static_assert(sizeof(DevPass) == 96, "DevPass layout");
 struct DevInit {
   double vmin, vmax, S, x0;
   unsigned long long cnt_min, cnt_max, nonfinite, pad;
-  // extra cut at t0 evaluated in the same pass (R23): #x<t0, #x==t0, sum (t0-x)^+, sum (x-t0)^+
-  double t0, N0, P0;
-  unsigned long long c_lt0, c_eq0, has_cut;
+  // the two extra cuts t_lo <= t_hi evaluated in the same pass (R23)
+  double t_lo, t_hi, N_lo, P_hi, I_in;
+  unsigned long long c_lt_lo, c_eq_lo, c_lt_hi, c_eq_hi, c_gt_hi, has_cut;
 };
 
 // Per-CTA partial of a pass (grid reduction scratch).
@@ -36,8 +36,8 @@ struct PassPartial {
 struct InitPartial {
   double vmin, vmax, S, pad;
   unsigned long long cnt_min, cnt_max, nonfinite, pad2;
-  double N0, P0;
-  unsigned long long c_lt0, c_eq0;
+  double N0, P0, I0, pad3;
+  unsigned long long cA, cB, cC, cD, cE, pad4;
 };
 
 // Device-side state of the radix select (step a5).
@@ -99,7 +99,7 @@ struct InitArgs {
   void* partials;
   unsigned int* ticket;
   DevInit* out;
-  const void* t0;   // device pointer to the extra cut (one element of the dtype), or nullptr
+  const void* t0;   // device pointer to the two extra cuts t_lo, t_hi (elements of the dtype), or nullptr
 };
 
 struct LaunchShape {
@@ -124,8 +124,7 @@ uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s);
 cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const LaunchShape& s, cudaStream_t st);
 
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
-// t0 <- the element of rank ~ (k - 1/2)/n among 2048 strided samples of x (one CTA); written to
-// *t0 as the dtype
+// t0[0], t0[1] <- the sample quantiles bracketing rank k (1024 strided samples of x, one CTA)
 cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st);
 cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
 

@@ -50,15 +50,22 @@ class NumpyShard:
             S += r["S"] + r["n"] * (r["x0"] - out["x0"])
         out["S"] = S
         if self.cut_k is not None and self.comm is None and x.size > 2:
+            # R23: two cuts at the sample quantiles bracketing rank k (1024 strided samples)
             n = x.size
-            m = min(n, 2048)
+            m = min(n, 1024)
             pos = np.arange(m) if n == m else (np.arange(m, dtype=np.int64) * n) // m + (n // m) // 2
             smp = np.sort(x[pos])
-            q = int(min(max((self.cut_k - 0.5) / n * m, 0), m - 1))
-            t0 = np.float64(smp[q])
+            q = (self.cut_k - 0.5) / n * m
+            w = 3.5 * math.sqrt(max(q * (m - q) / m, 0.0)) + 2.0
+            il, ih = max(int(math.floor(q - w)), 0), min(int(math.ceil(q + w)), m - 1)
+            tl, th = np.float64(smp[il]), np.float64(smp[ih])
             xd = x.astype(np.float64)
-            out.update(has_cut=1, t0=float(t0), c_lt0=int((x < t0).sum()), c_eq0=int((x == t0).sum()),
-                       N0=float(np.sum(t0 - xd[x < t0])), P0=float(np.sum(xd[x > t0] - t0)))
+            inner = (x > tl) & (x < th)
+            out.update(has_cut=2, t_lo=float(tl), t_hi=float(th),
+                       c_lt_lo=int((x < tl).sum()), c_eq_lo=int((x == tl).sum()),
+                       c_lt_hi=int((x < th).sum()), c_eq_hi=int((x == th).sum()),
+                       N_lo=float(np.sum(tl - xd[x < tl])), P_hi=float(np.sum(xd[x > th] - th)),
+                       I_in=float(np.sum(xd[inner] - tl)))
         return out
 
     def pass_(self, t, lo, hi, compact):

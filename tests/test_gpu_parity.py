@@ -56,19 +56,26 @@ def test_init_reduction(cp, dtype, n, off):
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 @pytest.mark.parametrize("dist", ["uniform", "mix2", "dup256", "cauchy"])
 def test_init_extra_cut(cp, dtype, dist):
-    """R23: the init pass's extra cut — t0 is an element of x near the median rank, and the counts /
-    positive-part sums at t0 match the oracle's direct evaluation."""
+    """R23: the init pass's two extra cuts — t_lo <= t_hi are elements of x bracketing the median
+    rank, and the counts / sums at them match the oracle's direct evaluation."""
     n = 2_000_003
     x = datagen.make(dist, n, dtype)
     s = cp.init_stats(tdev(x))
-    assert s["has_cut"] == 1
-    t0 = s["t0"]
-    assert np.any(x == t0)
-    r = O.pass_stats(x, t0, -math.inf, math.inf)
-    assert (s["c_lt0"], s["c_eq0"]) == (r["c_lt"], r["c_eq"])
-    assert s["N0"] == pytest.approx(float(r["N"]), rel=REL[dtype], abs=1e-300)
-    assert s["P0"] == pytest.approx(float(r["P"]), rel=REL[dtype], abs=1e-300)
-    assert abs(r["c_lt"] - n / 2) < 0.05 * n          # a 2048-sample quantile lands near the median
+    assert s["has_cut"] == 2
+    tl, th = s["t_lo"], s["t_hi"]
+    assert tl <= th and np.any(x == tl) and np.any(x == th)
+    rl = O.pass_stats(x, tl, -math.inf, math.inf)
+    rh = O.pass_stats(x, th, tl, th)
+    assert (s["c_lt_lo"], s["c_eq_lo"]) == (rl["c_lt"], rl["c_eq"])
+    assert (s["c_lt_hi"], s["c_eq_hi"]) == (rh["c_lt"], rh["c_eq"])
+    assert s["N_lo"] == pytest.approx(float(rl["N"]), rel=REL[dtype], abs=1e-300)
+    assert s["P_hi"] == pytest.approx(float(rh["P"]), rel=REL[dtype], abs=1e-300)
+    # I = sum_{t_lo<x<t_hi} (x - t_lo) = L_hi of a pass at t_lo with bracket upper end t_hi
+    ri = O.pass_stats(x, tl, -math.inf, th)
+    assert s["I_in"] == pytest.approx(float(ri["L_hi"]), rel=REL[dtype], abs=1e-300)
+    k = O.median_rank(n)
+    assert rl["c_lt"] < k <= rh["c_lt"] + rh["c_eq"]        # the cuts bracket the target
+    assert rh["c_lt"] - rl["c_lt"] < 0.2 * n                 # ... tightly (1024 samples, +-3.5 sd)
 
 
 def test_init_counts_nonfinite(cp):
