@@ -191,6 +191,11 @@ struct Backend {
                             uint64_t* z_lo, uint64_t* z_hi) = 0;
   // are the halves of the last compacting pass contiguous (selectable)?
   virtual bool kept_dense() const { return true; }
+  // did the init pass also copy out the elements strictly between its two cuts (R23)?  If so,
+  // adopt_init() makes them the current array.
+  virtual bool init_compacted() const { return false; }
+  virtual uint64_t init_written() const { return 0; }
+  virtual cpsel_status adopt_init() { return CPSEL_EINTERNAL; }
   // current array <- half `side` (0: ]yL,t[, 1: ]t,yR[) of the last compacting pass
   virtual cpsel_status adopt(int side) = 0;
   // r-th smallest (1-based) of half `side` of the last compacting pass, or of the current array (2)
@@ -225,6 +230,8 @@ struct GpuBackend : Backend {
   uint64_t zlo = 0, zhi = 0; // local halves written by the last compacting pass
   uint64_t cap = 0;          // capacity (elements) of each dense buffer
   uint64_t R = 0;            // segmented region size
+  bool init_seg_done = false;  // the init pass wrote ]t_lo, t_hi[ into segmented buffer 0
+  uint64_t init_n_in = 0;
   GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
       : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
@@ -245,9 +252,20 @@ struct GpuBackend : Backend {
   // init kernel (fast form, then the checked form if anything came out non-finite)
   cpsel_status run_init(bool sync_result, uint64_t k, bool cut) {
     InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init, cut ? ctx->d_t0 : nullptr};
+    // with the segmented buffers in place the init pass also copies out ]t_lo, t_hi[ (R23)
+    const bool fuse = cut && R > 0;
+    init_seg_done = false;
     CK(tic());
     if (cut) CK(launch_sample_cut(dt, x, n, k, ctx->d_t0, ctx->stream));
-    CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
+    if (fuse) {
+      SegArgs sa{};
+      sa.out = ctx->d_sb[0];
+      sa.R = R;
+      sa.seg_out = static_cast<SegEntry*>(ctx->d_st[0]);
+      CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream));
+    } else {
+      CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
+    }
     CK(toc());
     launches = cut ? 2 : 1;
     scanned = n;
@@ -261,6 +279,10 @@ struct GpuBackend : Backend {
                                    !std::isfinite(r.vmin) || !std::isfinite(r.vmax) ||
                                    r.c_lt_hi + r.c_eq_hi + r.c_gt_hi != n)
                                 : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
+    if (!suspicious && fuse) {
+      init_seg_done = true;
+      init_n_in = r.pad;
+    }
     if (suspicious) {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, true));
       launches += 1;
@@ -357,6 +379,17 @@ struct GpuBackend : Backend {
     return CPSEL_OK;
   }
   bool kept_dense() const override { return last_dense; }
+  bool init_compacted() const override { return init_seg_done; }
+  uint64_t init_written() const override { return init_n_in; }
+  cpsel_status adopt_init() override {
+    cur_seg = true;
+    cur = ctx->d_sb[0];
+    cur_tab = static_cast<const SegEntry*>(ctx->d_st[0]);
+    cur_side = 0;
+    cur_sbuf = 0;
+    n_cur = init_n_in;
+    return CPSEL_OK;
+  }
   cpsel_status adopt(int side) override {
     if (last_dense) {
       cur_seg = false;
@@ -680,6 +713,18 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       }
       row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);
+    }
+    // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
+    if (be.init_compacted() && yL == rec.t_lo && yR == rec.t_hi) {
+      if (m != be.init_written()) {
+        if (info) *info = inf;
+        return CPSEL_EINTERNAL;
+      }
+      st = be.adopt_init();
+      if (st != CPSEL_OK) return st;
+      inf.bytes_moved += m * es;
+      D_lo = c_le_L;
+      on_z = true;
     }
   }
   for (uint32_t it = 1;; ++it) {

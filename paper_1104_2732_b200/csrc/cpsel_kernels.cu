@@ -182,6 +182,23 @@ __device__ PassPartial block_reduce(PassPartial p) {
   return p;
 }
 
+// fold a partial written by another CTA straight from L2 (ld.global.cg), field by field
+__device__ __forceinline__ void combine_from(PassPartial& a, const PassPartial* b) {
+  a.c_lt += __ldcg(&b->c_lt); a.c_eq += __ldcg(&b->c_eq); a.c_lo += __ldcg(&b->c_lo); a.c_hi += __ldcg(&b->c_hi);
+  a.L_lo += __ldcg(&b->L_lo); a.L_hi += __ldcg(&b->L_hi); a.P += __ldcg(&b->P); a.N += __ldcg(&b->N);
+  a.pred = fmax(a.pred, __ldcg(&b->pred)); a.succ = fmin(a.succ, __ldcg(&b->succ));
+}
+__device__ __forceinline__ void combine_from(InitPartial& a, const InitPartial* b) {
+  const double mn = __ldcg(&b->vmin), mx = __ldcg(&b->vmax);
+  const unsigned long long cmn = __ldcg(&b->cnt_min), cmx = __ldcg(&b->cnt_max);
+  if (mn < a.vmin) { a.vmin = mn; a.cnt_min = cmn; } else if (mn == a.vmin) a.cnt_min += cmn;
+  if (mx > a.vmax) { a.vmax = mx; a.cnt_max = cmx; } else if (mx == a.vmax) a.cnt_max += cmx;
+  a.S += __ldcg(&b->S); a.N0 += __ldcg(&b->N0); a.P0 += __ldcg(&b->P0); a.I0 += __ldcg(&b->I0);
+  a.nonfinite += __ldcg(&b->nonfinite); a.pad2 += __ldcg(&b->pad2);
+  a.cA += __ldcg(&b->cA); a.cB += __ldcg(&b->cB); a.cC += __ldcg(&b->cC); a.cD += __ldcg(&b->cD);
+  a.cE += __ldcg(&b->cE);
+}
+
 __device__ __forceinline__ void combine(InitPartial& a, const InitPartial& b) {
   if (b.vmin < a.vmin) { a.vmin = b.vmin; a.cnt_min = b.cnt_min; }
   else if (b.vmin == a.vmin) a.cnt_min += b.cnt_min;
@@ -192,21 +209,34 @@ __device__ __forceinline__ void combine(InitPartial& a, const InitPartial& b) {
   a.N0 += b.N0;
   a.P0 += b.P0;
   a.I0 += b.I0;
+  a.pad2 += b.pad2;
   a.cA += b.cA; a.cB += b.cB; a.cC += b.cC; a.cD += b.cD; a.cE += b.cE;
 }
 
+// Reduce one InitPartial per thread to thread 0 of the block: warp butterflies, then the warps.
 __device__ InitPartial block_reduce(InitPartial p) {
-  __shared__ InitPartial sh[kBlock];
-  sh[threadIdx.x] = p;
-  __syncthreads();
-  // fixed-shape tree over the block
-  for (int s = kBlock / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) combine(sh[threadIdx.x], sh[threadIdx.x + s]);
-    __syncthreads();
+  __shared__ InitPartial sh[kWarps];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // field by field (few live registers): (min, #min) and (max, #max) pairs, then plain sums
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double mn = __shfl_xor_sync(FULL, p.vmin, o);
+    const unsigned long long cmn = __shfl_xor_sync(FULL, p.cnt_min, o);
+    if (mn < p.vmin) { p.vmin = mn; p.cnt_min = cmn; } else if (mn == p.vmin) p.cnt_min += cmn;
+    const double mx = __shfl_xor_sync(FULL, p.vmax, o);
+    const unsigned long long cmx = __shfl_xor_sync(FULL, p.cnt_max, o);
+    if (mx > p.vmax) { p.vmax = mx; p.cnt_max = cmx; } else if (mx == p.vmax) p.cnt_max += cmx;
   }
-  InitPartial r = sh[0];
+  p.S = warp_sum(p.S); p.N0 = warp_sum(p.N0); p.P0 = warp_sum(p.P0); p.I0 = warp_sum(p.I0);
+  p.nonfinite = warp_sum(p.nonfinite); p.pad2 = warp_sum(p.pad2);
+  p.cA = warp_sum(p.cA); p.cB = warp_sum(p.cB); p.cC = warp_sum(p.cC); p.cD = warp_sum(p.cD);
+  p.cE = warp_sum(p.cE);
+  if (lane == 0) sh[w] = p;
   __syncthreads();
-  return r;
+  if (threadIdx.x == 0)
+    for (int i = 1; i < kWarps; ++i) combine(p, sh[i]);
+  __syncthreads();
+  return p;
 }
 
 // Last-CTA finish: every CTA stores its partial, the last one to arrive folds all partials in a
@@ -224,16 +254,7 @@ __device__ bool grid_finish(const P& mine, P* partials, unsigned int* ticket, P*
   if (!s_last) return false;
   __threadfence();
   P acc = identity;
-  static_assert(sizeof(P) % 8 == 0, "partial must be 8-byte words");
-  for (unsigned i = threadIdx.x; i < gridDim.x; i += kBlock) {
-    P q;
-    // ld.global.cg: read at L2 (the partials were written by other CTAs)
-    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(partials + i);
-    unsigned long long* dst = reinterpret_cast<unsigned long long*>(&q);
-#pragma unroll
-    for (int w = 0; w < (int)(sizeof(P) / 8); ++w) dst[w] = __ldcg(src + w);
-    combine(acc, q);
-  }
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += kBlock) combine_from(acc, partials + i);
   acc = block_reduce(acc);
   if (threadIdx.x == 0) {
     *total = acc;
@@ -366,7 +387,7 @@ template <typename T, bool CHECKED, bool CUT = false> struct InitFn {
 };
 
 template <typename T, int UNROLL, bool CHECKED, bool CUT>
-__global__ void __launch_bounds__(kBlock) init_kernel(InitArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
   const T* x = static_cast<const T*>(a.x);
   InitFn<T, CHECKED, CUT> f(x[0]);
   if (CUT) {
@@ -1113,6 +1134,216 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// Steps a1 + a4 fused (R23): the init reduction, the two extra cuts and the copy_if of the elements
+// strictly between the cuts, in ONE read of x.  Warp-strided groups and the warp-private region
+// layout of seg_pass_kernel (the interior lands in run 0 of each warp's entry), so the following
+// cutting-plane passes read it as a segmented array.
+template <typename T> struct InitSeg {
+  static constexpr int VE = VecOf<T>::N;
+  static constexpr int G = kSegU * VE;
+  static constexpr int GW = 32 * G;
+  T mn, mx, tl, th;
+  unsigned cmn = 0, cmx = 0, cA = 0, cC = 0;
+  float fB = 0, fD = 0, fE = 0;
+  T gN[kSegU], gP[kSegU], gI[kSegU];
+  double N0 = 0, P0 = 0, I0 = 0;
+  T vals[G];
+  unsigned bits;
+  unsigned long long n_in = 0;  // warp-uniform: interior elements written
+  T* stage;
+  T* out;
+  uint64_t reg_lo;
+
+  __device__ __forceinline__ void slow(T v) {
+    if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
+    if (v > mx) { mx = v; cmx = 1; } else if (v == mx) ++cmx;
+  }
+  __device__ __forceinline__ void cut(float v, int u, int idx) {
+    asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f32 dl, dh;\n\t"
+        "setp.lt.f32 pA, %9, %10;\n\t"
+        "setp.eq.f32 pB, %9, %10;\n\t"
+        "setp.lt.f32 pC, %9, %11;\n\t"
+        "setp.eq.f32 pD, %9, %11;\n\t"
+        "setp.gt.f32 pE, %9, %11;\n\t"
+        "setp.gt.and.f32 pI, %9, %10, pC;\n\t"
+        "sub.rn.f32 dl, %10, %9;\n\t"
+        "sub.rn.f32 dh, %9, %11;\n\t"
+        "@pA add.u32 %0, %0, 1;\n\t"
+        "@pC add.u32 %1, %1, 1;\n\t"
+        "@pB add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pD add.rn.f32 %3, %3, 0f3F800000;\n\t"
+        "@pE add.rn.f32 %4, %4, 0f3F800000;\n\t"
+        "@pA add.rn.f32 %5, %5, dl;\n\t"
+        "@pE add.rn.f32 %6, %6, dh;\n\t"
+        "@pI sub.rn.f32 %7, %7, dl;\n\t"
+        "@pI or.b32 %8, %8, %12;\n\t}"
+        : "+r"(cA), "+r"(cC), "+f"(fB), "+f"(fD), "+f"(fE), "+f"(gN[u]), "+f"(gP[u]), "+f"(gI[u]), "+r"(bits)
+        : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
+    vals[idx] = v;
+  }
+  __device__ __forceinline__ void cut(double v, int u, int idx) {
+    asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f64 dl, dh;\n\t"
+        "setp.lt.f64 pA, %9, %10;\n\t"
+        "setp.eq.f64 pB, %9, %10;\n\t"
+        "setp.lt.f64 pC, %9, %11;\n\t"
+        "setp.eq.f64 pD, %9, %11;\n\t"
+        "setp.gt.f64 pE, %9, %11;\n\t"
+        "setp.gt.and.f64 pI, %9, %10, pC;\n\t"
+        "sub.rn.f64 dl, %10, %9;\n\t"
+        "sub.rn.f64 dh, %9, %11;\n\t"
+        "@pA add.u32 %0, %0, 1;\n\t"
+        "@pC add.u32 %1, %1, 1;\n\t"
+        "@pB add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pD add.rn.f32 %3, %3, 0f3F800000;\n\t"
+        "@pE add.rn.f32 %4, %4, 0f3F800000;\n\t"
+        "@pA add.rn.f64 %5, %5, dl;\n\t"
+        "@pE add.rn.f64 %6, %6, dh;\n\t"
+        "@pI sub.rn.f64 %7, %7, dl;\n\t"
+        "@pI or.b32 %8, %8, %12;\n\t}"
+        : "+r"(cA), "+r"(cC), "+f"(fB), "+f"(fD), "+f"(fE), "+d"(gN[u]), "+d"(gP[u]), "+d"(gI[u]), "+r"(bits)
+        : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
+    vals[idx] = v;
+  }
+  __device__ __forceinline__ void begin() {
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = gI[u] = T(0);
+    bits = 0u;
+  }
+  __device__ __forceinline__ void vec(const float4& v, int u) {
+    cut(v.x, u, u * 4 + 0); cut(v.y, u, u * 4 + 1); cut(v.z, u, u * 4 + 2); cut(v.w, u, u * 4 + 3);
+    const float lo = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
+    const float hi = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
+    if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); slow(v.z); slow(v.w); }
+  }
+  __device__ __forceinline__ void vec(const double2& v, int u) {
+    cut(v.x, u, u * 2 + 0); cut(v.y, u, u * 2 + 1);
+    const double lo = fmin(v.x, v.y), hi = fmax(v.x, v.y);
+    if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); }
+  }
+  __device__ __forceinline__ void end() {
+    N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
+    P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
+    const int lane = threadIdx.x & 31;
+    const unsigned cnt = (unsigned)__popc(bits);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned tot = __shfl_sync(FULL, incl, 31);
+    if (tot == 0u) return;
+    unsigned pos = incl - cnt;
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      if ((bits >> j) & 1u) stage[pos++] = vals[j];
+    __syncwarp();
+    T* dst = out + reg_lo + n_in;
+    for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    n_in += tot;
+    __syncwarp();
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArgs a) {
+  using F = InitSeg<T>;
+  using V = typename VecOf<T>::V;
+  constexpr int VE = VecOf<T>::N;
+  __shared__ __align__(16) T stage_all[kWarps * F::GW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
+  const uint64_t Wtot = (uint64_t)gridDim.x * kWarps;
+  const T* x = static_cast<const T*>(ia.x);
+  const uint64_t n = ia.n;
+  F f;
+  f.mn = tinf<T>(); f.mx = -tinf<T>();
+  f.tl = static_cast<const T*>(ia.t0)[0];
+  f.th = static_cast<const T*>(ia.t0)[1];
+  f.stage = stage_all + (size_t)w * F::GW;
+  f.out = static_cast<T*>(a.out);
+  f.reg_lo = W * a.R;
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
+  uint64_t head = mis ? (VE - mis) : 0;
+  if (head > n) head = n;
+  const V* xv = reinterpret_cast<const V*>(x + head);
+  const uint64_t nvec = (n - head) / VE;
+  constexpr uint64_t GV = 32 * kSegU;
+  const uint64_t nfull = nvec / GV;
+  for (uint64_t g = W; g < nfull; g += Wtot) {
+    V v[kSegU];
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + g * GV + (uint64_t)u * 32 + lane);
+    f.begin();
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) f.vec(v[u], u);
+    f.end();
+  }
+  if (nfull * GV < nvec && W == nfull % Wtot) {  // the ragged group
+    V v[kSegU];
+    bool ok[kSegU];
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) {
+      const uint64_t i = nfull * GV + (uint64_t)u * 32 + lane;
+      ok[u] = i < nvec;
+      if (ok[u]) v[u] = ld_stream(xv + i);
+    }
+    f.begin();
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u)
+      if (ok[u]) f.vec(v[u], u);
+    f.end();
+  }
+  if (W == Wtot - 1) {  // unaligned head + tail scalars
+    const uint64_t tail0 = head + nvec * VE, ntail = n - tail0;
+    const bool okh = (uint64_t)lane < head;
+    const bool okt = (uint64_t)lane >= head && (uint64_t)lane < head + ntail;
+    if (head + ntail) {
+      f.begin();
+      if (okh || okt) {
+        const T v = okh ? x[lane] : x[tail0 + (lane - head)];
+        f.cut(v, 0, 0);
+        f.slow(v);
+      }
+      f.end();
+    }
+  }
+  if (lane == 0) {
+    SegEntry o;
+    o.off[0] = f.reg_lo;
+    o.cnt[0] = f.n_in;
+    o.off[1] = f.reg_lo + a.R;
+    o.cnt[1] = 0;
+    a.seg_out[W] = o;
+  }
+  InitPartial p;
+  p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = 0; p.pad = 0;
+  p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = 0;
+  p.pad2 = lane == 0 ? f.n_in : 0;  // interior elements written (counted once per warp)
+  p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
+  p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = f.cC; p.cD = (unsigned long long)f.fD;
+  p.cE = (unsigned long long)f.fE;
+  p = block_reduce(p);
+  InitPartial id;
+  id.vmin = tinf<double>(); id.vmax = -tinf<double>(); id.S = 0; id.pad = 0;
+  id.cnt_min = id.cnt_max = id.nonfinite = id.pad2 = 0;
+  id.N0 = id.P0 = id.I0 = 0; id.cA = id.cB = id.cC = id.cD = id.cE = 0;
+  InitPartial tot;
+  if (grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id) && threadIdx.x == 0) {
+    DevInit r;
+    r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = 0; r.x0 = (double)x[0];
+    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = 0;
+    r.pad = tot.pad2;  // interior elements written
+    r.t_lo = (double)f.tl; r.t_hi = (double)f.th;
+    r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
+    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB; r.c_lt_hi = tot.cC; r.c_eq_hi = tot.cD; r.c_gt_hi = tot.cE;
+    r.has_cut = 3ull;  // two cuts + the interior compacted
+    *ia.out = r;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Step a8: batched selection (LMS: one k-th order statistic per column of S).  One CTA runs the
 // whole method on one column at a time (work-stealing over columns): the init reduction, the
 // Kelley iterations with the driver step on thread 0 (device-side driver, same rules as the host
@@ -1476,6 +1707,13 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 }
 
 int seg_total_warps(int dtype, const LaunchShape& s) { return s.grid_seg[dtype] * kWarps; }
+
+cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, const LaunchShape& s, cudaStream_t st) {
+  // the same grid as seg_pass_kernel: its warp regions / run table are what later passes read
+  if (dtype == kF32) init_seg_kernel<float><<<s.grid_seg[kF32], kBlock, 0, st>>>(ia, a);
+  else init_seg_kernel<double><<<s.grid_seg[kF64], kBlock, 0, st>>>(ia, a);
+  return cudaGetLastError();
+}
 
 uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s) {
   const uint64_t ve = dtype == kF32 ? 4 : 2;

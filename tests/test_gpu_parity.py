@@ -174,6 +174,29 @@ def test_select_distributions_forced_cp(cp, dtype):
     cp.set_config(force_cp=0, z_cap=0, select_cap=0, init_cut=1)
 
 
+def test_select_adversarial_orders_and_sample_positions(cp):
+    """The two extra cuts come from strided samples (R23): poison exactly those positions so the cuts
+    miss the target, and feed sorted / reverse-sorted / two-valued / constant arrays — the result
+    must stay exact (the cuts are exact either way; the compacted bracket is simply not used)."""
+    n = 3_000_017
+    base = datagen.make("normal", n, "f32")
+    m = 1024
+    pos = (np.arange(m, dtype=np.int64) * n) // m + (n // m) // 2
+    cases = {}
+    x = base.copy(); x[pos] = -7.0; cases["samples_low"] = x
+    x = base.copy(); x[pos] = 9.0; cases["samples_high"] = x
+    x = base.copy(); x[pos] = np.float32(np.median(base)); cases["samples_at_median"] = x
+    cases["sorted"] = np.sort(base)
+    cases["reversed"] = np.sort(base)[::-1].copy()
+    x = np.where(base < 0, np.float32(-1.0), np.float32(2.0)); cases["two_valued"] = x
+    cases["constant"] = np.full(n, 3.5, np.float32)
+    for name, x in cases.items():
+        xd = tdev(x)
+        for k in (1, 17, n // 3, O.median_rank(n), n - 5, n):
+            v, info = cp.select_kth(xd, k, return_info=True)
+            assert canon(v) == float(O.order_statistic(x, k)), (name, k, info)
+
+
 def test_select_direct_path_config0(cp):
     """BASELINE configs[0]: median of n=1e5 float32 uniform (n <= direct_threshold -> direct select)."""
     x = datagen.make("uniform", 100_000, "f32")
