@@ -723,6 +723,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       st = be.adopt_init();
       if (st != CPSEL_OK) return st;
       inf.bytes_moved += m * es;
+      inf.init_written = m;
       D_lo = c_le_L;
       on_z = true;
     }

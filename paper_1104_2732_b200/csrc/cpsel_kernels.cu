@@ -1143,66 +1143,65 @@ template <typename T> struct InitSeg {
   static constexpr int G = kSegU * VE;
   static constexpr int GW = 32 * G;
   T mn, mx, tl, th;
-  unsigned cmn = 0, cmx = 0, cA = 0, cC = 0;
-  float fB = 0, fD = 0, fE = 0;
+  unsigned cmn = 0, cmx = 0, cA = 0, nan = 0;
+  float fB = 0, fD = 0;           // #x=t_lo, #x=t_hi (exact per-thread float counters)
   T gN[kSegU], gP[kSegU], gI[kSegU];
   double N0 = 0, P0 = 0, I0 = 0;
   T vals[G];
   unsigned bits;
-  unsigned long long n_in = 0;  // warp-uniform: interior elements written
+  unsigned long long n_in = 0;    // warp-uniform: interior elements written
   T* stage;
   T* out;
   uint64_t reg_lo;
 
-  __device__ __forceinline__ void slow(T v) {
-    if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
-    if (v > mx) { mx = v; cmx = 1; } else if (v == mx) ++cmx;
-  }
+  // one element: 6 compares, 2 subs, 3 counters, 3 sums, 1 interior bit (15 issue slots).
+  // #x<t_hi = #x<t_lo + #x=t_lo + #interior and #x>t_hi = n - #x<t_hi - #x=t_hi are derived.
   __device__ __forceinline__ void cut(float v, int u, int idx) {
     asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f32 dl, dh;\n\t"
-        "setp.lt.f32 pA, %9, %10;\n\t"
-        "setp.eq.f32 pB, %9, %10;\n\t"
-        "setp.lt.f32 pC, %9, %11;\n\t"
-        "setp.eq.f32 pD, %9, %11;\n\t"
-        "setp.gt.f32 pE, %9, %11;\n\t"
-        "setp.gt.and.f32 pI, %9, %10, pC;\n\t"
-        "sub.rn.f32 dl, %10, %9;\n\t"
-        "sub.rn.f32 dh, %9, %11;\n\t"
+        "setp.lt.f32 pA, %7, %8;\n\t"
+        "setp.eq.f32 pB, %7, %8;\n\t"
+        "setp.lt.f32 pC, %7, %9;\n\t"
+        "setp.eq.f32 pD, %7, %9;\n\t"
+        "setp.gt.f32 pE, %7, %9;\n\t"
+        "setp.gt.and.f32 pI, %7, %8, pC;\n\t"
+        "sub.rn.f32 dl, %8, %7;\n\t"
+        "sub.rn.f32 dh, %7, %9;\n\t"
         "@pA add.u32 %0, %0, 1;\n\t"
-        "@pC add.u32 %1, %1, 1;\n\t"
-        "@pB add.rn.f32 %2, %2, 0f3F800000;\n\t"
-        "@pD add.rn.f32 %3, %3, 0f3F800000;\n\t"
-        "@pE add.rn.f32 %4, %4, 0f3F800000;\n\t"
-        "@pA add.rn.f32 %5, %5, dl;\n\t"
-        "@pE add.rn.f32 %6, %6, dh;\n\t"
-        "@pI sub.rn.f32 %7, %7, dl;\n\t"
-        "@pI or.b32 %8, %8, %12;\n\t}"
-        : "+r"(cA), "+r"(cC), "+f"(fB), "+f"(fD), "+f"(fE), "+f"(gN[u]), "+f"(gP[u]), "+f"(gI[u]), "+r"(bits)
+        "@pB add.rn.f32 %1, %1, 0f3F800000;\n\t"
+        "@pD add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pA add.rn.f32 %3, %3, dl;\n\t"
+        "@pE add.rn.f32 %4, %4, dh;\n\t"
+        "@pI sub.rn.f32 %5, %5, dl;\n\t"
+        "@pI or.b32 %6, %6, %10;\n\t}"
+        : "+r"(cA), "+f"(fB), "+f"(fD), "+f"(gN[u]), "+f"(gP[u]), "+f"(gI[u]), "+r"(bits)
         : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
     vals[idx] = v;
   }
   __device__ __forceinline__ void cut(double v, int u, int idx) {
     asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f64 dl, dh;\n\t"
-        "setp.lt.f64 pA, %9, %10;\n\t"
-        "setp.eq.f64 pB, %9, %10;\n\t"
-        "setp.lt.f64 pC, %9, %11;\n\t"
-        "setp.eq.f64 pD, %9, %11;\n\t"
-        "setp.gt.f64 pE, %9, %11;\n\t"
-        "setp.gt.and.f64 pI, %9, %10, pC;\n\t"
-        "sub.rn.f64 dl, %10, %9;\n\t"
-        "sub.rn.f64 dh, %9, %11;\n\t"
+        "setp.lt.f64 pA, %7, %8;\n\t"
+        "setp.eq.f64 pB, %7, %8;\n\t"
+        "setp.lt.f64 pC, %7, %9;\n\t"
+        "setp.eq.f64 pD, %7, %9;\n\t"
+        "setp.gt.f64 pE, %7, %9;\n\t"
+        "setp.gt.and.f64 pI, %7, %8, pC;\n\t"
+        "sub.rn.f64 dl, %8, %7;\n\t"
+        "sub.rn.f64 dh, %7, %9;\n\t"
         "@pA add.u32 %0, %0, 1;\n\t"
-        "@pC add.u32 %1, %1, 1;\n\t"
-        "@pB add.rn.f32 %2, %2, 0f3F800000;\n\t"
-        "@pD add.rn.f32 %3, %3, 0f3F800000;\n\t"
-        "@pE add.rn.f32 %4, %4, 0f3F800000;\n\t"
-        "@pA add.rn.f64 %5, %5, dl;\n\t"
-        "@pE add.rn.f64 %6, %6, dh;\n\t"
-        "@pI sub.rn.f64 %7, %7, dl;\n\t"
-        "@pI or.b32 %8, %8, %12;\n\t}"
-        : "+r"(cA), "+r"(cC), "+f"(fB), "+f"(fD), "+f"(fE), "+d"(gN[u]), "+d"(gP[u]), "+d"(gI[u]), "+r"(bits)
+        "@pB add.rn.f32 %1, %1, 0f3F800000;\n\t"
+        "@pD add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pA add.rn.f64 %3, %3, dl;\n\t"
+        "@pE add.rn.f64 %4, %4, dh;\n\t"
+        "@pI sub.rn.f64 %5, %5, dl;\n\t"
+        "@pI or.b32 %6, %6, %10;\n\t}"
+        : "+r"(cA), "+f"(fB), "+f"(fD), "+d"(gN[u]), "+d"(gP[u]), "+d"(gI[u]), "+r"(bits)
         : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
     vals[idx] = v;
+  }
+  __device__ __forceinline__ void slow(T v) {
+    if (v != v) { ++nan; return; }
+    if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
+    if (v > mx) { mx = v; cmx = 1; } else if (v == mx) ++cmx;
   }
   __device__ __forceinline__ void begin() {
 #pragma unroll
@@ -1211,16 +1210,36 @@ template <typename T> struct InitSeg {
   }
   __device__ __forceinline__ void vec(const float4& v, int u) {
     cut(v.x, u, u * 4 + 0); cut(v.y, u, u * 4 + 1); cut(v.z, u, u * 4 + 2); cut(v.w, u, u * 4 + 3);
-    const float lo = fminf(fminf(v.x, v.y), fminf(v.z, v.w));
-    const float hi = fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w));
-    if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); slow(v.z); slow(v.w); }
   }
   __device__ __forceinline__ void vec(const double2& v, int u) {
     cut(v.x, u, u * 2 + 0); cut(v.y, u, u * 2 + 1);
-    const double lo = fmin(v.x, v.y), hi = fmax(v.x, v.y);
-    if (lo <= mn || hi >= mx) { slow(v.x); slow(v.y); }
   }
-  __device__ __forceinline__ void end() {
+  // group-level extremes: NaN-propagating min/max trees over the group's values, and the (rare)
+  // exact (min, #min)/(max, #max) update only when the group reaches a running extreme or has a NaN
+  __device__ __forceinline__ void extremes(int nvalid) {
+    T lo = vals[0], hi = vals[0];
+#pragma unroll
+    for (int j = 1; j < G; ++j) {
+      if (j < nvalid) {
+        if (sizeof(T) == 4) {
+          float a, b;
+          asm("min.NaN.f32 %0, %1, %2;" : "=f"(a) : "f"((float)lo), "f"((float)vals[j]));
+          asm("max.NaN.f32 %0, %1, %2;" : "=f"(b) : "f"((float)hi), "f"((float)vals[j]));
+          lo = (T)a; hi = (T)b;
+        } else {
+          lo = (vals[j] != vals[j] || lo != lo) ? vals[j] + lo : fmin((double)lo, (double)vals[j]);
+          hi = (vals[j] != vals[j] || hi != hi) ? vals[j] + hi : fmax((double)hi, (double)vals[j]);
+        }
+      }
+    }
+    if (!(lo > mn) || !(hi < mx)) {  // also taken on NaN
+#pragma unroll
+      for (int j = 0; j < G; ++j)
+        if (j < nvalid) slow(vals[j]);
+    }
+  }
+  __device__ __forceinline__ void end(int nvalid) {
+    extremes(nvalid);
     N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
     P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
     I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
@@ -1234,10 +1253,25 @@ template <typename T> struct InitSeg {
     }
     const unsigned tot = __shfl_sync(FULL, incl, 31);
     if (tot == 0u) return;
-    unsigned pos = incl - cnt;
+    // predicated shared stores (no branches): slot j goes to stage[pos] iff bit j is set
+    unsigned addr = (unsigned)__cvta_generic_to_shared(stage) + (incl - cnt) * (unsigned)sizeof(T);
 #pragma unroll
-    for (int j = 0; j < G; ++j)
-      if ((bits >> j) & 1u) stage[pos++] = vals[j];
+    for (int j = 0; j < G; ++j) {
+      if (sizeof(T) == 4)
+        asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 q;\n\t"
+                     "and.b32 q, %1, %2;\n\t"
+                     "setp.ne.u32 p, q, 0;\n\t"
+                     "@p st.shared.f32 [%0], %3;\n\t"
+                     "@p add.u32 %0, %0, 4;\n\t}"
+                     : "+r"(addr) : "r"(bits), "r"(1u << j), "f"((float)vals[j]) : "memory");
+      else
+        asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 q;\n\t"
+                     "and.b32 q, %1, %2;\n\t"
+                     "setp.ne.u32 p, q, 0;\n\t"
+                     "@p st.shared.f64 [%0], %3;\n\t"
+                     "@p add.u32 %0, %0, 8;\n\t}"
+                     : "+r"(addr) : "r"(bits), "r"(1u << j), "d"((double)vals[j]) : "memory");
+    }
     __syncwarp();
     T* dst = out + reg_lo + n_in;
     for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
@@ -1278,7 +1312,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     f.begin();
 #pragma unroll
     for (int u = 0; u < kSegU; ++u) f.vec(v[u], u);
-    f.end();
+    f.end(F::G);
   }
   if (nfull * GV < nvec && W == nfull % Wtot) {  // the ragged group
     V v[kSegU];
@@ -1289,11 +1323,13 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
       ok[u] = i < nvec;
       if (ok[u]) v[u] = ld_stream(xv + i);
     }
+    // masked-off vectors: replicate a valid lane value so the group extremes stay exact
     f.begin();
+    int nvalid = 0;
 #pragma unroll
     for (int u = 0; u < kSegU; ++u)
-      if (ok[u]) f.vec(v[u], u);
-    f.end();
+      if (ok[u]) { f.vec(v[u], u); nvalid = (u + 1) * VE; }
+    f.end(nvalid);
   }
   if (W == Wtot - 1) {  // unaligned head + tail scalars
     const uint64_t tail0 = head + nvec * VE, ntail = n - tail0;
@@ -1301,12 +1337,13 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     const bool okt = (uint64_t)lane >= head && (uint64_t)lane < head + ntail;
     if (head + ntail) {
       f.begin();
+      int nvalid = 0;
       if (okh || okt) {
         const T v = okh ? x[lane] : x[tail0 + (lane - head)];
         f.cut(v, 0, 0);
-        f.slow(v);
+        nvalid = 1;
       }
-      f.end();
+      f.end(nvalid);
     }
   }
   if (lane == 0) {
@@ -1319,11 +1356,11 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   }
   InitPartial p;
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = 0; p.pad = 0;
-  p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = 0;
+  p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nan;
   p.pad2 = lane == 0 ? f.n_in : 0;  // interior elements written (counted once per warp)
   p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
-  p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = f.cC; p.cD = (unsigned long long)f.fD;
-  p.cE = (unsigned long long)f.fE;
+  p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = 0; p.cD = (unsigned long long)f.fD;
+  p.cE = 0;
   p = block_reduce(p);
   InitPartial id;
   id.vmin = tinf<double>(); id.vmax = -tinf<double>(); id.S = 0; id.pad = 0;
@@ -1333,11 +1370,16 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   if (grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id) && threadIdx.x == 0) {
     DevInit r;
     r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = 0; r.x0 = (double)x[0];
-    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = 0;
+    r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite;
     r.pad = tot.pad2;  // interior elements written
     r.t_lo = (double)f.tl; r.t_hi = (double)f.th;
     r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
-    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB; r.c_lt_hi = tot.cC; r.c_eq_hi = tot.cD; r.c_gt_hi = tot.cE;
+    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB;
+    r.c_lt_hi = tot.cA + tot.cB + tot.pad2;  // every x < t_hi is < t_lo, = t_lo or interior
+    r.c_eq_hi = tot.cD;
+    // #x>t_hi as the complement: the NaN count above makes the host's count check pass, and the
+    // nonfinite field itself carries the error
+    r.c_gt_hi = n - r.c_lt_hi - r.c_eq_hi - tot.nonfinite;
     r.has_cut = 3ull;  // two cuts + the interior compacted
     *ia.out = r;
   }

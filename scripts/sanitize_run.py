@@ -1,0 +1,40 @@
+"""Small workload touching every kernel, for compute-sanitizer (memcheck / racecheck / synccheck):
+fused init+cuts+compaction, segmented passes (both variants), dense compaction, radix select,
+direct eval, batched selection, tcgen05 residuals, sharded (world 1) path."""
+import math
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import datagen  # noqa: E402
+import oracle as O  # noqa: E402
+import paper_1104_2732_b200 as cp  # noqa: E402
+
+n = (1 << 21) + 3
+for dist, dtype in (("normal", "f32"), ("cauchy", "f64")):
+    x = datagen.make(dist, n, dtype)
+    xd = torch.from_numpy(x).cuda()[1:]          # misaligned start
+    xs = x[1:]
+    for k in (1, 1000, O.median_rank(xs.size), xs.size - 7):
+        v = cp.select_kth(xd, k)
+        assert (0.0 if v == 0 else v) == float(O.order_statistic(xs, k)), (dist, dtype, k)
+    s = cp.eval(xd, float(xs[77]), -math.inf, math.inf)
+    assert s["c_lt"] == int((xs < xs[77]).sum())
+cp.set_config(init_cut=0)
+x = datagen.make("uniform", n, "f32")
+assert cp.median(torch.from_numpy(x).cuda()) == float(O.median(x))
+cp.set_config(init_cut=1)
+S = torch.from_numpy(datagen.make("halfnormal", 3000 * 40, "f32").reshape(40, 3000)).cuda()
+out = cp.select_kth_batched(S, 1500).cpu().numpy()
+Sh = S.cpu().numpy()
+assert all(out[j] == O.order_statistic(Sh[j], 1500) for j in range(40))
+X, y, th, _ = datagen.lms_problem(n=3001, p=10, C=300)
+R = cp.lms_residuals(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), torch.from_numpy(th).cuda())
+torch.cuda.synchronize()
+uid = cp.nccl_unique_id()
+cp.comm_init(uid, 0, 1, 0)
+x = datagen.make("mix1", n, "f32")
+assert cp.select_kth_sharded(torch.from_numpy(x).cuda(), 12345) == float(O.order_statistic(x, 12345))
+print("sanitize workload ok")
