@@ -622,10 +622,14 @@ template <typename T, int MODE, int UNROLL> struct PassFn {
     __syncthreads();
     const uint64_t base = cs->base[side];
     const T* src = sbuf + side * CAPS;
+    // (bounded: a speculative compaction — the batched init's ]t_lo, t_hi[ copy — may overflow
+    // z_cap; the cursor still counts everything and the caller then does not use the copy)
     if (side == 0) {
-      for (unsigned i = threadIdx.x; i < cnt; i += kBlock) z[base + i] = src[i];
+      for (unsigned i = threadIdx.x; i < cnt; i += kBlock)
+        if (base + i < z_cap) z[base + i] = src[i];
     } else {
-      for (unsigned i = threadIdx.x; i < cnt; i += kBlock) z[z_cap - 1 - (base + i)] = src[i];
+      for (unsigned i = threadIdx.x; i < cnt; i += kBlock)
+        if (base + i < z_cap) z[z_cap - 1 - (base + i)] = src[i];
     }
     __syncthreads();
   }
@@ -1385,6 +1389,45 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   }
 }
 
+// The batched kernel's init pass: the per-element step of init_seg_kernel (stats + two cuts +
+// interior bit) with the block-level dense compaction of PassFn (one CTA per column, the interior
+// ]t_lo, t_hi[ goes to the CTA's buffer from index 0).
+struct BatchInitFn : InitSeg<float> {
+  PassFn<float, kCompact, 4> pc;
+  int nvalid = 0;
+  __device__ __forceinline__ void group_begin() {
+    begin();
+    nvalid = 0;
+  }
+  template <bool MASKED, typename V> __device__ __forceinline__ void vec(const V& v, bool ok, int u) {
+    if (MASKED && !ok) return;
+    InitSeg<float>::vec(v, u);
+    nvalid = (u + 1) * 4;
+  }
+  __device__ __forceinline__ void group_end() {
+    extremes(nvalid);
+    N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
+    P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
+#pragma unroll
+    for (int j = 0; j < 16; ++j) pc.vals[j] = vals[j];
+    pc.lo_bits = bits;
+    pc.hi_bits = 0u;
+    pc.compact_group();
+  }
+  // head/tail scalars (warp 0 only): per-element atomics on the (shared) cursor
+  __device__ __forceinline__ void scalar(float v, bool ok) {
+    begin();
+    if (ok) cut(v, 0, 0);
+    extremes(ok ? 1 : 0);
+    N0 += (double)gN[0]; P0 += (double)gP[0]; I0 += (double)gI[0];
+    if (bits & 1u) {
+      const unsigned long long pos = atomicAdd(&pc.cursors[0], 1ull);
+      if (pos < pc.z_cap) pc.z[pos] = v;
+    }
+  }
+};
+
 // ------------------------------------------------------------------------------------------
 // Step a8: batched selection (LMS: one k-th order statistic per column of S).  One CTA runs the
 // whole method on one column at a time (work-stealing over columns): the init reduction, the
@@ -1500,19 +1543,36 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
       }
       __syncthreads();
     }
-    // ---- a1: init reduction over the column (+ the two extra cuts)
+    // ---- a1 + a4: init reduction over the column, the two extra cuts and the copy_if of
+    //      ]t_lo, t_hi[ into this CTA's buffer 0, in one read (R23)
     {
-      InitFn<float, true, true> f(x[0]);
+      __shared__ CompactShared cs;
+      BatchInitFn f;
+      f.mn = tinf<float>(); f.mx = -tinf<float>();
       f.tl = cut ? st.cut_lo : x[0];
       f.th = cut ? st.cut_hi : x[0];
+      f.pc.cs = &cs;
+      f.pc.sbuf = sbuf;
+      f.pc.z = my0;
+      f.pc.z_cap = a.cap;
+      f.pc.cursors = st.cursors;
+      __syncthreads();
       stream_array<float, 4>(x, n, f, 0u, 1u);
+      f.pc.finish();
       InitPartial p;
-      p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = f.S; p.pad = 0;
-      p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nonfin; p.pad2 = 0;
+      p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = 0; p.pad = 0;
+      p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nan; p.pad2 = 0;
       p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
-      p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = f.cC; p.cD = (unsigned long long)f.fD;
-      p.cE = (unsigned long long)f.fE;
+      p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = 0; p.cD = (unsigned long long)f.fD; p.cE = 0;
       p = block_reduce(p);
+      __syncthreads();  // compaction cursor final
+      if (threadIdx.x == 0) {
+        const unsigned long long written = st.cursors[0];
+        st.cursors[0] = st.cursors[1] = 0ull;
+        p.cC = p.cA + p.cB + written;  // every x < t_hi is < t_lo, = t_lo or interior
+        p.pad2 = written;
+        atomicAdd(&a.stats[1], (unsigned long long)(4 * written));
+      }
       if (threadIdx.x == 0) {
         st.phase = 0;
         st.iters = 0;
@@ -1532,8 +1592,7 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
           st.m = st.c_lt_R - st.c_le_L;
           st.D_lo = 0; st.on_z = 0; st.slow = 0; st.bisect = 0;
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
-          const double x0 = (double)x[0];
-          st.t = x0 + (p.S - (double)p.cnt_min * (p.vmin - x0) - (double)p.cnt_max * (p.vmax - x0)) / (double)st.m;
+          st.t = 0.5 * p.vmin + 0.5 * p.vmax;  // only used if neither cut lies strictly inside
           if (cut) {  // the two extra cuts, exactly as the host driver applies them
             const double tl = st.cut_lo, th = st.cut_hi, dlh = th - tl;
             const double P_tl = p.I0 + p.P0 + (double)(n - p.cC) * dlh;
@@ -1567,6 +1626,12 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
                 st.yL = (float)th; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
                 st.t = th + L_hi / (double)st.m;
               }
+            }
+            // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
+            if (st.phase == 0 && (double)st.yL == tl && (double)st.yR == th && st.m == p.pad2 && p.pad2 <= a.cap) {
+              st.cur = my0; st.n_cur = p.pad2; st.cur_buf = 0;
+              st.D_lo = st.c_le_L; st.on_z = 1;
+              if (st.m <= (unsigned long long)kBatchFinish) { st.k_r = k - st.c_le_L; st.phase = 2; }
             }
           }
         }
