@@ -1148,8 +1148,8 @@ template <typename T> struct InitSeg {
   static constexpr int GW = 32 * G;
   T mn, mx, tl, th;
   unsigned cmn = 0, cmx = 0, cA = 0, nan = 0;
-  float fB = 0, fD = 0;           // #x=t_lo, #x=t_hi (exact per-thread float counters)
-  T gN[kSegU], gP[kSegU], gI[kSegU];
+  float fB = 0, fD = 0;           // #x<=t_lo, #x<=t_hi (exact per-thread float counters)
+  T gN[kSegU], gP[kSegU];
   double N0 = 0, P0 = 0, I0 = 0;
   T vals[G];
   unsigned bits;
@@ -1158,58 +1158,48 @@ template <typename T> struct InitSeg {
   T* out;
   uint64_t reg_lo;
 
-  // one element: 6 compares, 2 subs, 3 counters, 3 sums, 1 interior bit (15 issue slots).
-  // #x<t_hi = #x<t_lo + #x=t_lo + #interior and #x>t_hi = n - #x<t_hi - #x=t_hi are derived.
+  // one element: 4 compares, 2 subs, 3 counters, 2 sums, 1 interior bit (12 issue slots):
+  //   cA = #x<t_lo, cLE = #x<=t_lo, cLH = #x<=t_hi, N += (t_lo-x) on x<t_lo, P += (x-t_hi) on x>t_hi,
+  //   interior bit on t_lo<x<t_hi.  The interior sum is taken while its elements are copied out.
   __device__ __forceinline__ void cut(float v, int u, int idx) {
-    asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f32 dl, dh;\n\t"
-        "setp.lt.f32 pA, %7, %8;\n\t"
-        "setp.eq.f32 pB, %7, %8;\n\t"
-        "setp.lt.f32 pC, %7, %9;\n\t"
-        "setp.eq.f32 pD, %7, %9;\n\t"
-        "setp.gt.f32 pE, %7, %9;\n\t"
-        "setp.gt.and.f32 pI, %7, %8, pC;\n\t"
-        "sub.rn.f32 dl, %8, %7;\n\t"
-        "sub.rn.f32 dh, %7, %9;\n\t"
+    asm("{\n\t.reg .pred pA, pL, pH, pI;\n\t.reg .f32 dl, dh;\n\t"
+        "setp.lt.f32 pA, %6, %7;\n\t"
+        "setp.le.f32 pL, %6, %7;\n\t"
+        "setp.le.f32 pH, %6, %8;\n\t"
+        "setp.lt.and.f32 pI, %6, %8, !pL;\n\t"
+        "sub.rn.f32 dl, %7, %6;\n\t"
+        "sub.rn.f32 dh, %6, %8;\n\t"
         "@pA add.u32 %0, %0, 1;\n\t"
-        "@pB add.rn.f32 %1, %1, 0f3F800000;\n\t"
-        "@pD add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pL add.rn.f32 %1, %1, 0f3F800000;\n\t"
+        "@pH add.rn.f32 %2, %2, 0f3F800000;\n\t"
         "@pA add.rn.f32 %3, %3, dl;\n\t"
-        "@pE add.rn.f32 %4, %4, dh;\n\t"
-        "@pI sub.rn.f32 %5, %5, dl;\n\t"
-        "@pI or.b32 %6, %6, %10;\n\t}"
-        : "+r"(cA), "+f"(fB), "+f"(fD), "+f"(gN[u]), "+f"(gP[u]), "+f"(gI[u]), "+r"(bits)
+        "@!pH add.rn.f32 %4, %4, dh;\n\t"
+        "@pI or.b32 %5, %5, %9;\n\t}"
+        : "+r"(cA), "+f"(fB), "+f"(fD), "+f"(gN[u]), "+f"(gP[u]), "+r"(bits)
         : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
     vals[idx] = v;
   }
   __device__ __forceinline__ void cut(double v, int u, int idx) {
-    asm("{\n\t.reg .pred pA, pB, pC, pD, pE, pI;\n\t.reg .f64 dl, dh;\n\t"
-        "setp.lt.f64 pA, %7, %8;\n\t"
-        "setp.eq.f64 pB, %7, %8;\n\t"
-        "setp.lt.f64 pC, %7, %9;\n\t"
-        "setp.eq.f64 pD, %7, %9;\n\t"
-        "setp.gt.f64 pE, %7, %9;\n\t"
-        "setp.gt.and.f64 pI, %7, %8, pC;\n\t"
-        "sub.rn.f64 dl, %8, %7;\n\t"
-        "sub.rn.f64 dh, %7, %9;\n\t"
+    asm("{\n\t.reg .pred pA, pL, pH, pI;\n\t.reg .f64 dl, dh;\n\t"
+        "setp.lt.f64 pA, %6, %7;\n\t"
+        "setp.le.f64 pL, %6, %7;\n\t"
+        "setp.le.f64 pH, %6, %8;\n\t"
+        "setp.lt.and.f64 pI, %6, %8, !pL;\n\t"
+        "sub.rn.f64 dl, %7, %6;\n\t"
+        "sub.rn.f64 dh, %6, %8;\n\t"
         "@pA add.u32 %0, %0, 1;\n\t"
-        "@pB add.rn.f32 %1, %1, 0f3F800000;\n\t"
-        "@pD add.rn.f32 %2, %2, 0f3F800000;\n\t"
+        "@pL add.rn.f32 %1, %1, 0f3F800000;\n\t"
+        "@pH add.rn.f32 %2, %2, 0f3F800000;\n\t"
         "@pA add.rn.f64 %3, %3, dl;\n\t"
-        "@pE add.rn.f64 %4, %4, dh;\n\t"
-        "@pI sub.rn.f64 %5, %5, dl;\n\t"
-        "@pI or.b32 %6, %6, %10;\n\t}"
-        : "+r"(cA), "+f"(fB), "+f"(fD), "+d"(gN[u]), "+d"(gP[u]), "+d"(gI[u]), "+r"(bits)
+        "@!pH add.rn.f64 %4, %4, dh;\n\t"
+        "@pI or.b32 %5, %5, %9;\n\t}"
+        : "+r"(cA), "+f"(fB), "+f"(fD), "+d"(gN[u]), "+d"(gP[u]), "+r"(bits)
         : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
     vals[idx] = v;
   }
-  __device__ __forceinline__ void slow(T v) {
-    if (v != v) { ++nan; return; }
-    if (v < mn) { mn = v; cmn = 1; } else if (v == mn) ++cmn;
-    if (v > mx) { mx = v; cmx = 1; } else if (v == mx) ++cmx;
-  }
   __device__ __forceinline__ void begin() {
 #pragma unroll
-    for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = gI[u] = T(0);
+    for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = T(0);
     bits = 0u;
   }
   __device__ __forceinline__ void vec(const float4& v, int u) {
@@ -1218,35 +1208,67 @@ template <typename T> struct InitSeg {
   __device__ __forceinline__ void vec(const double2& v, int u) {
     cut(v.x, u, u * 2 + 0); cut(v.y, u, u * 2 + 1);
   }
-  // group-level extremes: NaN-propagating min/max trees over the group's values, and the (rare)
-  // exact (min, #min)/(max, #max) update only when the group reaches a running extreme or has a NaN
-  __device__ __forceinline__ void extremes(int nvalid) {
-    T lo = vals[0], hi = vals[0];
-#pragma unroll
-    for (int j = 1; j < G; ++j) {
-      if (j < nvalid) {
-        if (sizeof(T) == 4) {
-          float a, b;
-          asm("min.NaN.f32 %0, %1, %2;" : "=f"(a) : "f"((float)lo), "f"((float)vals[j]));
-          asm("max.NaN.f32 %0, %1, %2;" : "=f"(b) : "f"((float)hi), "f"((float)vals[j]));
-          lo = (T)a; hi = (T)b;
-        } else {
-          lo = (vals[j] != vals[j] || lo != lo) ? vals[j] + lo : fmin((double)lo, (double)vals[j]);
-          hi = (vals[j] != vals[j] || hi != hi) ? vals[j] + hi : fmax((double)hi, (double)vals[j]);
-        }
-      }
+  // group-level extremes: NaN-propagating min/max trees over the thread's values and a warp vote
+  // against the WARP-UNIFORM running (min, max); only a group that reaches a running extreme or holds
+  // a NaN takes the (warp-uniform) exact update.  Warp-level records are rare (~H(groups)/groups),
+  // where per-thread records would send most warps down the slow path early on.  Must be called by
+  // all 32 lanes.
+  __device__ __forceinline__ static T nan_min(T a, T b) {
+    if (sizeof(T) == 4) {
+      float r;
+      asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"((float)a), "f"((float)b));
+      return (T)r;
     }
-    if (!(lo > mn) || !(hi < mx)) {  // also taken on NaN
+    return (a != a || b != b) ? a + b : (T)fmin((double)a, (double)b);
+  }
+  __device__ __forceinline__ static T nan_max(T a, T b) {
+    if (sizeof(T) == 4) {
+      float r;
+      asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"((float)a), "f"((float)b));
+      return (T)r;
+    }
+    return (a != a || b != b) ? a + b : (T)fmax((double)a, (double)b);
+  }
+  __device__ __forceinline__ void extremes(int nvalid) {
+    T lo = nvalid > 0 ? vals[0] : tinf<T>(), hi = nvalid > 0 ? vals[0] : -tinf<T>();
+#pragma unroll
+    for (int j = 1; j < G; ++j)
+      if (j < nvalid) { lo = nan_min(lo, vals[j]); hi = nan_max(hi, vals[j]); }
+    const bool need = !(lo > mn) || !(hi < mx);  // also taken on NaN
+    if (__any_sync(FULL, need)) slow_group(nvalid, lo, hi);
+  }
+  __device__ __forceinline__ void slow_group(int nvalid, T lo, T hi) {
+    if (__any_sync(FULL, lo != lo || hi != hi)) {  // NaNs: count them, extremes over the rest
+      lo = tinf<T>(); hi = -tinf<T>();
 #pragma unroll
       for (int j = 0; j < G; ++j)
-        if (j < nvalid) slow(vals[j]);
+        if (j < nvalid) {
+          const T v = vals[j];
+          if (v != v) ++nan;
+          else { lo = v < lo ? v : lo; hi = v > hi ? v : hi; }
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const T a = __shfl_xor_sync(FULL, lo, o), b = __shfl_xor_sync(FULL, hi, o);
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    if (lo < mn) { mn = lo; cmn = 0; }
+    if (hi > mx) { mx = hi; cmx = 0; }
+    if (lo == mn) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) cmn += (j < nvalid && vals[j] == mn) ? 1u : 0u;
+    }
+    if (hi == mx) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) cmx += (j < nvalid && vals[j] == mx) ? 1u : 0u;
     }
   }
   __device__ __forceinline__ void end(int nvalid) {
     extremes(nvalid);
     N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
     P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
-    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
     const int lane = threadIdx.x & 31;
     const unsigned cnt = (unsigned)__popc(bits);
     unsigned incl = cnt;
@@ -1258,27 +1280,19 @@ template <typename T> struct InitSeg {
     const unsigned tot = __shfl_sync(FULL, incl, 31);
     if (tot == 0u) return;
     // predicated shared stores (no branches): slot j goes to stage[pos] iff bit j is set
-    unsigned addr = (unsigned)__cvta_generic_to_shared(stage) + (incl - cnt) * (unsigned)sizeof(T);
+    T* sp = stage + (incl - cnt);
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      if (sizeof(T) == 4)
-        asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 q;\n\t"
-                     "and.b32 q, %1, %2;\n\t"
-                     "setp.ne.u32 p, q, 0;\n\t"
-                     "@p st.shared.f32 [%0], %3;\n\t"
-                     "@p add.u32 %0, %0, 4;\n\t}"
-                     : "+r"(addr) : "r"(bits), "r"(1u << j), "f"((float)vals[j]) : "memory");
-      else
-        asm volatile("{\n\t.reg .pred p;\n\t.reg .b32 q;\n\t"
-                     "and.b32 q, %1, %2;\n\t"
-                     "setp.ne.u32 p, q, 0;\n\t"
-                     "@p st.shared.f64 [%0], %3;\n\t"
-                     "@p add.u32 %0, %0, 8;\n\t}"
-                     : "+r"(addr) : "r"(bits), "r"(1u << j), "d"((double)vals[j]) : "memory");
-    }
+    for (int j = 0; j < G; ++j)
+      if (bits & (1u << j)) *sp++ = vals[j];
     __syncwarp();
     T* dst = out + reg_lo + n_in;
-    for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    T isum = T(0);  // sum over the copied interior of (x - t_lo)
+    for (unsigned i = lane; i < tot; i += 32) {
+      const T v = stage[i];
+      dst[i] = v;
+      isum += v - tl;
+    }
+    I0 += (double)isum;
     n_in += tot;
     __syncwarp();
   }
@@ -1363,6 +1377,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nan;
   p.pad2 = lane == 0 ? f.n_in : 0;  // interior elements written (counted once per warp)
   p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
+  // cB carries #x<=t_lo, cD #x<=t_hi (converted to the equality counts below)
   p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = 0; p.cD = (unsigned long long)f.fD;
   p.cE = 0;
   p = block_reduce(p);
@@ -1378,9 +1393,9 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.pad = tot.pad2;  // interior elements written
     r.t_lo = (double)f.tl; r.t_hi = (double)f.th;
     r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
-    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB;
-    r.c_lt_hi = tot.cA + tot.cB + tot.pad2;  // every x < t_hi is < t_lo, = t_lo or interior
-    r.c_eq_hi = tot.cD;
+    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB - tot.cA;
+    r.c_lt_hi = tot.cB + tot.pad2;  // every x < t_hi is <= t_lo or interior
+    r.c_eq_hi = tot.cD - r.c_lt_hi;
     // #x>t_hi as the complement: the NaN count above makes the host's count check pass, and the
     // nonfinite field itself carries the error
     r.c_gt_hi = n - r.c_lt_hi - r.c_eq_hi - tot.nonfinite;
@@ -1408,7 +1423,12 @@ struct BatchInitFn : InitSeg<float> {
     extremes(nvalid);
     N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
     P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
-    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
+    // the interior sum: over this thread's interior elements (bits), in the group
+    float isum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if ((bits >> j) & 1u) isum += vals[j] - tl;
+    I0 += (double)isum;
 #pragma unroll
     for (int j = 0; j < 16; ++j) pc.vals[j] = vals[j];
     pc.lo_bits = bits;
@@ -1420,7 +1440,8 @@ struct BatchInitFn : InitSeg<float> {
     begin();
     if (ok) cut(v, 0, 0);
     extremes(ok ? 1 : 0);
-    N0 += (double)gN[0]; P0 += (double)gP[0]; I0 += (double)gI[0];
+    N0 += (double)gN[0]; P0 += (double)gP[0];
+    if (bits & 1u) I0 += (double)(v - tl);
     if (bits & 1u) {
       const unsigned long long pos = atomicAdd(&pc.cursors[0], 1ull);
       if (pos < pc.z_cap) pc.z[pos] = v;
@@ -1569,7 +1590,10 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
       if (threadIdx.x == 0) {
         const unsigned long long written = st.cursors[0];
         st.cursors[0] = st.cursors[1] = 0ull;
-        p.cC = p.cA + p.cB + written;  // every x < t_hi is < t_lo, = t_lo or interior
+        // cB, cD arrive as #x<=t_lo, #x<=t_hi: convert to the equality counts
+        p.cC = p.cB + written;  // every x < t_hi is <= t_lo or interior
+        p.cB = p.cB - p.cA;
+        p.cD = p.cD - p.cC;
         p.pad2 = written;
         atomicAdd(&a.stats[1], (unsigned long long)(4 * written));
       }
