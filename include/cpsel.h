@@ -100,7 +100,10 @@ typedef struct {
                              from the cut's sums and the pass skips this sum) */
   uint64_t has_cut;       /* 2 if the pass also evaluated the two extra cuts t_lo <= t_hi (R23): */
   double t_lo, t_hi;      /*   sample quantiles bracketing rank k (elements of x) */
-  uint64_t c_lt_lo, c_eq_lo, c_lt_hi, c_eq_hi;  /* #{x<t_lo}, #{x==t_lo}, #{x<t_hi}, #{x==t_hi} */
+  uint64_t c_le_lo, c_lt_hi; /* #{x<=t_lo}, #{x<t_hi}: the counts a bracket update needs at each cut
+                             when the target lies between them; a cut beyond the target moves to the
+                             adjacent float, where the missing count is the known one (R24) */
+  uint64_t reserved_cut[2];
   double N_lo;            /*   sum (t_lo - x)^+ */
   double P_hi;            /*   sum (x - t_hi)^+ */
   double I_in;            /*   sum over t_lo < x < t_hi of (x - t_lo) */
@@ -110,7 +113,7 @@ typedef struct {
 typedef struct {
   double t;               /* query point (an element of the dtype) */
   double F;               /* F_k(t) = (k-1/2) P(t) + (n-k+1/2) N(t)  (Eq. 2, R2) via App. A identities */
-  uint64_t c_lt, c_eq;    /* exact counts at t */
+  uint64_t c_lt, c_eq;    /* exact counts at t (UINT64_MAX: not evaluated — the init cuts, R24) */
   uint64_t interior;      /* bracket interior count after the update */
   uint64_t scanned;       /* elements this pass read (x, or the compacted bracket) */
   uint64_t written;       /* elements this pass wrote (compaction of both bracket halves) */

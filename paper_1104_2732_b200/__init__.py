@@ -65,8 +65,8 @@ class PassStats(C.Structure):
 class InitStats(C.Structure):
     _fields_ = [("vmin", C.c_double), ("vmax", C.c_double), ("cnt_min", C.c_uint64), ("cnt_max", C.c_uint64),
                 ("nonfinite", C.c_uint64), ("x0", C.c_double), ("S", C.c_double), ("has_cut", C.c_uint64),
-                ("t_lo", C.c_double), ("t_hi", C.c_double), ("c_lt_lo", C.c_uint64), ("c_eq_lo", C.c_uint64),
-                ("c_lt_hi", C.c_uint64), ("c_eq_hi", C.c_uint64), ("N_lo", C.c_double), ("P_hi", C.c_double),
+                ("t_lo", C.c_double), ("t_hi", C.c_double), ("c_le_lo", C.c_uint64), ("c_lt_hi", C.c_uint64),
+                ("reserved_cut0", C.c_uint64), ("reserved_cut1", C.c_uint64), ("N_lo", C.c_double), ("P_hi", C.c_double),
                 ("I_in", C.c_double)]
 
     def as_dict(self):

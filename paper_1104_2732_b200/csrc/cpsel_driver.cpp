@@ -276,8 +276,7 @@ struct GpuBackend : Backend {
     // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
     // cuts (which skip the shifted sum), as #x<t_hi + #x=t_hi + #x>t_hi < n
     const bool suspicious = cut ? (!std::isfinite(r.N_lo) || !std::isfinite(r.P_hi) || !std::isfinite(r.I_in) ||
-                                   !std::isfinite(r.vmin) || !std::isfinite(r.vmax) ||
-                                   r.c_lt_hi + r.c_eq_hi + r.c_gt_hi != n)
+                                   !std::isfinite(r.vmin) || !std::isfinite(r.vmax) || r.nonfinite != 0)
                                 : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
     if (!suspicious && fuse) {
       init_seg_done = true;
@@ -300,7 +299,7 @@ struct GpuBackend : Backend {
     o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
     o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
     o->has_cut = r.has_cut; o->t_lo = r.t_lo; o->t_hi = r.t_hi;
-    o->c_lt_lo = r.c_lt_lo; o->c_eq_lo = r.c_eq_lo; o->c_lt_hi = r.c_lt_hi; o->c_eq_hi = r.c_eq_hi;
+    o->c_le_lo = r.c_le_lo; o->c_lt_hi = r.c_lt_hi;
     o->N_lo = r.N_lo; o->P_hi = r.P_hi; o->I_in = r.I_in;
     return CPSEL_OK;
   }
@@ -665,7 +664,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   if (rec.has_cut) {
     const long double tl = rec.t_lo, th = rec.t_hi, dlh = th - tl;
     const long double N_tl = rec.N_lo, P_th = rec.P_hi;
-    const long double P_tl = (long double)rec.I_in + P_th + (long double)(n - rec.c_lt_hi) * dlh;
+    const long double P_tl = (long double)rec.I_in + P_th + (long double)(n - rec.c_lt_hi) * dlh;  // R24
     const long double N_th = N_tl + (long double)rec.c_lt_hi * dlh - (long double)rec.I_in;
     auto row_of = [&](double tt, uint64_t clt, uint64_t ceq, long double Nt, long double Pt) {
       cpsel_trace_row r{};
@@ -673,43 +672,47 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       return r;
     };
     bool settled = false;  // the target is below t_lo: t_hi carries no further information
+    // R24: the pass counts #x<=t_lo and #x<t_hi only — what the bracket update needs when the
+    // target lies between the cuts (the usual case).  A cut on the far side of the target moves to
+    // the adjacent float, where the missing count is the known one: #x<next(t_lo) = #x<=t_lo,
+    // #x<=prev(t_hi) = #x<t_hi (no element lies strictly between a float and its neighbour).
+    const bool f32 = dt == kF32;
+    auto next_up = [&](double v) { return f32 ? (double)std::nextafterf((float)v, INFINITY) : std::nextafter(v, INFINITY); };
+    auto next_dn = [&](double v) { return f32 ? (double)std::nextafterf((float)v, -INFINITY) : std::nextafter(v, -INFINITY); };
+    constexpr uint64_t kUnknown = ~0ull;
     if (rec.t_lo > rec.vmin && rec.t_lo < rec.vmax) {
-      const uint64_t c_lt = rec.c_lt_lo, c_le = rec.c_lt_lo + rec.c_eq_lo;
-      cpsel_trace_row row = row_of(rec.t_lo, c_lt, rec.c_eq_lo, N_tl, P_tl);
-      if (c_lt < k && k <= c_le) {
-        if (trace && cfg.record_trace) trace->push_back(row);
-        return done(rec.t_lo, 2);
-      }
+      const uint64_t c_le = rec.c_le_lo;
+      cpsel_trace_row row = row_of(rec.t_lo, kUnknown, kUnknown, N_tl, P_tl);
       if (c_le < k) {  // y_L <- t_lo
         yL = rec.t_lo; N_L = N_tl; c_le_L = c_le; m = c_lt_R - c_le;
         const long double L_hi = P_tl - (long double)(n - c_lt_R) * ((long double)yR - tl);  // P_R = 0
         t = rec.t_lo + (double)(L_hi / (long double)m);
-      } else {  // y_R <- t_lo: interior ]min, t_lo[
-        const long double L_lo = N_tl - (long double)c_le_L * (tl - (long double)yL);  // N_L = 0
-        yR = rec.t_lo; P_R = P_tl; c_lt_R = c_lt; m = c_lt - c_le_L;
-        t = rec.t_lo - (double)(L_lo / (long double)m);
+      } else {  // y_R <- next(t_lo): interior ]min, next(t_lo)[
+        const double yr = next_up(rec.t_lo);
+        const long double N_r = N_tl + (long double)c_le * ((long double)yr - tl);
+        const long double L_lo = N_r - (long double)c_le_L * ((long double)yr - (long double)yL);  // N_L = 0
+        yR = yr; P_R = P_tl - (long double)(n - c_le) * ((long double)yr - tl); c_lt_R = c_le; m = c_le - c_le_L;
+        t = yr - (double)(L_lo / (long double)m);
         settled = true;
       }
       row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);
     }
     if (!settled && rec.t_hi > yL && rec.t_hi < rec.vmax) {
-      const uint64_t c_lt = rec.c_lt_hi, c_le = rec.c_lt_hi + rec.c_eq_hi;
-      cpsel_trace_row row = row_of(rec.t_hi, c_lt, rec.c_eq_hi, N_th, P_th);
-      if (c_lt < k && k <= c_le) {
-        if (trace && cfg.record_trace) trace->push_back(row);
-        return done(rec.t_hi, 2);
-      }
+      const uint64_t c_lt = rec.c_lt_hi;
+      cpsel_trace_row row = row_of(rec.t_hi, c_lt, kUnknown, N_th, P_th);
       if (c_lt >= k) {  // y_R <- t_hi: interior ]y_L, t_hi[
         // sum_{y_L<x<t_hi} (x - y_L): the pass's I when y_L = t_lo, else via N (App. A identity)
         const long double L_lo = (yL == rec.t_lo) ? (long double)(c_lt - c_le_L) * dlh - (long double)rec.I_in
                                                   : N_th - N_L - (long double)c_le_L * (th - (long double)yL);
         yR = rec.t_hi; P_R = P_th; c_lt_R = c_lt; m = c_lt - c_le_L;
         t = rec.t_hi - (double)(L_lo / (long double)m);
-      } else {  // y_L <- t_hi: interior ]t_hi, max[
-        const long double L_hi = P_th - (long double)(n - c_lt_R) * ((long double)yR - th);  // P_R = 0
-        yL = rec.t_hi; N_L = N_th; c_le_L = c_le; m = c_lt_R - c_le;
-        t = rec.t_hi + (double)(L_hi / (long double)m);
+      } else {  // y_L <- prev(t_hi): interior ]prev(t_hi), max[
+        const double yl = next_dn(rec.t_hi);
+        const long double P_l = P_th + (long double)(n - c_lt) * (th - (long double)yl);
+        const long double L_hi = P_l - (long double)(n - c_lt_R) * ((long double)yR - (long double)yl);  // P_R = 0
+        yL = yl; N_L = N_th - (long double)c_lt * (th - (long double)yl); c_le_L = c_lt; m = c_lt_R - c_lt;
+        t = yl + (double)(L_hi / (long double)m);
       }
       row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);

@@ -414,7 +414,9 @@ __global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
     r.t_lo = CUT ? (double)f.tl : 0.0;
     r.t_hi = CUT ? (double)f.th : 0.0;
     r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
-    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB; r.c_lt_hi = tot.cC; r.c_eq_hi = tot.cD; r.c_gt_hi = tot.cE;
+    r.c_le_lo = tot.cA + tot.cB; r.c_lt_hi = tot.cC; r.res0 = r.res1 = r.res2 = 0;
+    // a NaN is in none of <t_hi, =t_hi, >t_hi: the fast form reports the shortfall (CHECKED counts all)
+    if (CUT && !CHECKED) r.nonfinite = a.n - tot.cC - tot.cD - tot.cE;
     r.has_cut = CUT ? 2ull : 0ull;
     *a.out = r;
   }
@@ -1147,8 +1149,8 @@ template <typename T> struct InitSeg {
   static constexpr int G = kSegU * VE;
   static constexpr int GW = 32 * G;
   T mn, mx, tl, th;
-  unsigned cmn = 0, cmx = 0, cA = 0, nan = 0;
-  float fB = 0, fD = 0;           // #x<=t_lo, #x<=t_hi (exact per-thread float counters)
+  unsigned cmn = 0, cmx = 0, nan = 0;
+  float fL = 0;                   // #x<=t_lo (exact per-thread float counter, < 2^24 per thread)
   T gN[kSegU], gP[kSegU];
   double N0 = 0, P0 = 0, I0 = 0;
   T vals[G];
@@ -1158,42 +1160,37 @@ template <typename T> struct InitSeg {
   T* out;
   uint64_t reg_lo;
 
-  // one element: 4 compares, 2 subs, 3 counters, 2 sums, 1 interior bit (12 issue slots):
-  //   cA = #x<t_lo, cLE = #x<=t_lo, cLH = #x<=t_hi, N += (t_lo-x) on x<t_lo, P += (x-t_hi) on x>t_hi,
-  //   interior bit on t_lo<x<t_hi.  The interior sum is taken while its elements are copied out.
+  // one element: 3 compares, 2 subs, 1 counter, 2 sums, 1 interior bit (9 issue slots):
+  //   fL = #x<=t_lo, N += (t_lo-x) on x<=t_lo, P += (x-t_hi) on x>t_hi, interior bit on t_lo<x<t_hi.
+  //   #x<t_hi = #x<=t_lo + #interior; the interior sum is taken while its elements are copied out.
+  //   (#x==t_lo and #x==t_hi are not needed, R24.)
   __device__ __forceinline__ void cut(float v, int u, int idx) {
-    asm("{\n\t.reg .pred pA, pL, pH, pI;\n\t.reg .f32 dl, dh;\n\t"
-        "setp.lt.f32 pA, %6, %7;\n\t"
-        "setp.le.f32 pL, %6, %7;\n\t"
-        "setp.le.f32 pH, %6, %8;\n\t"
-        "setp.lt.and.f32 pI, %6, %8, !pL;\n\t"
-        "sub.rn.f32 dl, %7, %6;\n\t"
-        "sub.rn.f32 dh, %6, %8;\n\t"
-        "@pA add.u32 %0, %0, 1;\n\t"
-        "@pL add.rn.f32 %1, %1, 0f3F800000;\n\t"
-        "@pH add.rn.f32 %2, %2, 0f3F800000;\n\t"
-        "@pA add.rn.f32 %3, %3, dl;\n\t"
-        "@!pH add.rn.f32 %4, %4, dh;\n\t"
-        "@pI or.b32 %5, %5, %9;\n\t}"
-        : "+r"(cA), "+f"(fB), "+f"(fD), "+f"(gN[u]), "+f"(gP[u]), "+r"(bits)
+    asm("{\n\t.reg .pred pL, pH, pI;\n\t.reg .f32 dl, dh;\n\t"
+        "setp.le.f32 pL, %4, %5;\n\t"
+        "setp.gt.f32 pH, %4, %6;\n\t"
+        "setp.lt.and.f32 pI, %4, %6, !pL;\n\t"
+        "sub.rn.f32 dl, %5, %4;\n\t"
+        "sub.rn.f32 dh, %4, %6;\n\t"
+        "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+        "@pL add.rn.f32 %1, %1, dl;\n\t"
+        "@pH add.rn.f32 %2, %2, dh;\n\t"
+        "@pI or.b32 %3, %3, %7;\n\t}"
+        : "+f"(fL), "+f"(gN[u]), "+f"(gP[u]), "+r"(bits)
         : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
     vals[idx] = v;
   }
   __device__ __forceinline__ void cut(double v, int u, int idx) {
-    asm("{\n\t.reg .pred pA, pL, pH, pI;\n\t.reg .f64 dl, dh;\n\t"
-        "setp.lt.f64 pA, %6, %7;\n\t"
-        "setp.le.f64 pL, %6, %7;\n\t"
-        "setp.le.f64 pH, %6, %8;\n\t"
-        "setp.lt.and.f64 pI, %6, %8, !pL;\n\t"
-        "sub.rn.f64 dl, %7, %6;\n\t"
-        "sub.rn.f64 dh, %6, %8;\n\t"
-        "@pA add.u32 %0, %0, 1;\n\t"
-        "@pL add.rn.f32 %1, %1, 0f3F800000;\n\t"
-        "@pH add.rn.f32 %2, %2, 0f3F800000;\n\t"
-        "@pA add.rn.f64 %3, %3, dl;\n\t"
-        "@!pH add.rn.f64 %4, %4, dh;\n\t"
-        "@pI or.b32 %5, %5, %9;\n\t}"
-        : "+r"(cA), "+f"(fB), "+f"(fD), "+d"(gN[u]), "+d"(gP[u]), "+r"(bits)
+    asm("{\n\t.reg .pred pL, pH, pI;\n\t.reg .f64 dl, dh;\n\t"
+        "setp.le.f64 pL, %4, %5;\n\t"
+        "setp.gt.f64 pH, %4, %6;\n\t"
+        "setp.lt.and.f64 pI, %4, %6, !pL;\n\t"
+        "sub.rn.f64 dl, %5, %4;\n\t"
+        "sub.rn.f64 dh, %4, %6;\n\t"
+        "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+        "@pL add.rn.f64 %1, %1, dl;\n\t"
+        "@pH add.rn.f64 %2, %2, dh;\n\t"
+        "@pI or.b32 %3, %3, %7;\n\t}"
+        : "+f"(fL), "+d"(gN[u]), "+d"(gP[u]), "+r"(bits)
         : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
     vals[idx] = v;
   }
@@ -1377,9 +1374,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nan;
   p.pad2 = lane == 0 ? f.n_in : 0;  // interior elements written (counted once per warp)
   p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
-  // cB carries #x<=t_lo, cD #x<=t_hi (converted to the equality counts below)
-  p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = 0; p.cD = (unsigned long long)f.fD;
-  p.cE = 0;
+  p.cA = (unsigned long long)f.fL; p.cB = p.cC = p.cD = p.cE = 0;  // cA = #x<=t_lo
   p = block_reduce(p);
   InitPartial id;
   id.vmin = tinf<double>(); id.vmax = -tinf<double>(); id.S = 0; id.pad = 0;
@@ -1393,12 +1388,9 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.pad = tot.pad2;  // interior elements written
     r.t_lo = (double)f.tl; r.t_hi = (double)f.th;
     r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
-    r.c_lt_lo = tot.cA; r.c_eq_lo = tot.cB - tot.cA;
-    r.c_lt_hi = tot.cB + tot.pad2;  // every x < t_hi is <= t_lo or interior
-    r.c_eq_hi = tot.cD - r.c_lt_hi;
-    // #x>t_hi as the complement: the NaN count above makes the host's count check pass, and the
-    // nonfinite field itself carries the error
-    r.c_gt_hi = n - r.c_lt_hi - r.c_eq_hi - tot.nonfinite;
+    r.c_le_lo = tot.cA;
+    r.c_lt_hi = tot.cA + tot.pad2;  // every x < t_hi is <= t_lo or interior
+    r.res0 = r.res1 = r.res2 = 0;
     r.has_cut = 3ull;  // two cuts + the interior compacted
     *ia.out = r;
   }
@@ -1584,16 +1576,13 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
       p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = 0; p.pad = 0;
       p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nan; p.pad2 = 0;
       p.N0 = f.N0; p.P0 = f.P0; p.I0 = f.I0;
-      p.cA = f.cA; p.cB = (unsigned long long)f.fB; p.cC = 0; p.cD = (unsigned long long)f.fD; p.cE = 0;
+      p.cA = (unsigned long long)f.fL; p.cB = p.cC = p.cD = p.cE = 0;  // cA = #x<=t_lo
       p = block_reduce(p);
       __syncthreads();  // compaction cursor final
       if (threadIdx.x == 0) {
         const unsigned long long written = st.cursors[0];
         st.cursors[0] = st.cursors[1] = 0ull;
-        // cB, cD arrive as #x<=t_lo, #x<=t_hi: convert to the equality counts
-        p.cC = p.cB + written;  // every x < t_hi is <= t_lo or interior
-        p.cB = p.cB - p.cA;
-        p.cD = p.cD - p.cC;
+        p.cC = p.cA + written;  // #x<t_hi: every x < t_hi is <= t_lo or interior
         p.pad2 = written;
         atomicAdd(&a.stats[1], (unsigned long long)(4 * written));
       }
@@ -1621,34 +1610,36 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
             const double tl = st.cut_lo, th = st.cut_hi, dlh = th - tl;
             const double P_tl = p.I0 + p.P0 + (double)(n - p.cC) * dlh;
             bool settled = false;
+            // R24: #x<=t_lo and #x<t_hi only; a cut on the far side of the target becomes the
+            // adjacent float (next(t_lo) / prev(t_hi)), where the missing count is the known one
             if (tl > p.vmin && tl < p.vmax) {
-              const unsigned long long c_lt = p.cA, c_le = p.cA + p.cB;
-              if (c_lt < k && k <= c_le) {
-                st.result = (float)tl; st.phase = 1; settled = true;
-              } else if (c_le < k) {
+              const unsigned long long c_le = p.cA;
+              if (c_le < k) {
                 st.yL = (float)tl; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
                 st.t = tl + (P_tl - (double)(n - st.c_lt_R) * ((double)st.yR - tl)) / (double)st.m;
-              } else {
-                const double L_lo = p.N0 - (double)st.c_le_L * (tl - (double)st.yL);
-                st.yR = (float)tl; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
-                st.t = tl - L_lo / (double)st.m;
+              } else {  // y_R <- next(t_lo): #x<next(t_lo) = #x<=t_lo
+                const double yr = (double)nextafterf((float)tl, INFINITY);
+                const double N_r = p.N0 + (double)c_le * (yr - tl);
+                const double L_lo = N_r - (double)st.c_le_L * (yr - (double)st.yL);
+                st.yR = (float)yr; st.c_lt_R = c_le; st.m = c_le - st.c_le_L;
+                st.t = yr - L_lo / (double)st.m;
                 settled = true;
               }
             }
             if (!settled && th > (double)st.yL && th < p.vmax) {
-              const unsigned long long c_lt = p.cC, c_le = p.cC + p.cD;
-              if (c_lt < k && k <= c_le) {
-                st.result = (float)th; st.phase = 1;
-              } else if (c_lt >= k) {
-                const double N_th = p.N0 + (double)p.cC * dlh - p.I0;
+              const unsigned long long c_lt = p.cC;
+              const double N_th = p.N0 + (double)p.cC * dlh - p.I0;
+              if (c_lt >= k) {
                 const double L_lo = ((double)st.yL == tl) ? (double)(c_lt - st.c_le_L) * dlh - p.I0
                                                           : N_th - (double)st.c_le_L * (th - (double)st.yL);
                 st.yR = (float)th; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
                 st.t = th - L_lo / (double)st.m;
-              } else {
-                const double L_hi = p.P0 - (double)(n - st.c_lt_R) * ((double)st.yR - th);
-                st.yL = (float)th; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
-                st.t = th + L_hi / (double)st.m;
+              } else {  // y_L <- prev(t_hi): #x<=prev(t_hi) = #x<t_hi
+                const double yl = (double)nextafterf((float)th, -INFINITY);
+                const double P_l = p.P0 + (double)(n - c_lt) * (th - yl);
+                const double L_hi = P_l - (double)(n - st.c_lt_R) * ((double)st.yR - yl);
+                st.yL = (float)yl; st.c_le_L = c_lt; st.m = st.c_lt_R - c_lt;
+                st.t = yl + L_hi / (double)st.m;
               }
             }
             // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it

@@ -25,7 +25,8 @@ struct DevInit {
   unsigned long long cnt_min, cnt_max, nonfinite, pad;
   // the two extra cuts t_lo <= t_hi evaluated in the same pass (R23)
   double t_lo, t_hi, N_lo, P_hi, I_in;
-  unsigned long long c_lt_lo, c_eq_lo, c_lt_hi, c_eq_hi, c_gt_hi, has_cut;
+  // #x<=t_lo and #x<t_hi: the counts the bracket update needs at each cut (R24)
+  unsigned long long c_le_lo, c_lt_hi, res0, res1, res2, has_cut;
 };
 
 // Per-CTA partial of a pass (grid reduction scratch).
