@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdarg>
@@ -66,8 +67,20 @@ struct cpsel_ctx {
   int rank = 0, world = 1;
   // last trace
   std::vector<cpsel_trace_row> trace;
-  // kernel timing (record_timing)
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // kernel timing (record_timing): a pool of (start, end) event pairs, one pair per step of a
+  // selection, resolved once the selection is over (no synchronisation between steps)
+  std::vector<cudaEvent_t> evpool;
+  // result mailbox in mapped pinned memory: the finishing thread of a pass/init/select kernel
+  // writes its result here and then bumps the flag the host spins on (no copy, no stream sync)
+  struct Mailbox {
+    DevPass pass;
+    DevInit init;
+    double radix_value;
+    unsigned long long seq_pass, seq_init, seq_radix;
+  };
+  Mailbox* mb = nullptr;      // host view
+  Mailbox* mb_dev = nullptr;  // device view of the same memory
+  unsigned long long seq = 0;
 };
 
 namespace {
@@ -201,10 +214,12 @@ struct Backend {
   // r-th smallest (1-based) of half `side` of the last compacting pass, or of the current array (2)
   virtual cpsel_status select(int side, uint64_t r, double* out) = 0;
   virtual std::string message() const = 0;
-  // kernels launched / CUDA-event milliseconds / local elements read, of the last step
+  // kernels launched / timing slot (record_timing; -1: none) / local elements read, of the last step
   uint32_t launches = 0;
-  double step_ms = 0.0;
+  int slot = -1;
   uint64_t scanned = 0;
+  // CUDA-event milliseconds of a step's timing slot (waits for it); 0 if none
+  virtual double slot_ms(int) { return 0.0; }
 };
 
 // ------------------------------------------------------------------------ one GPU
@@ -232,16 +247,60 @@ struct GpuBackend : Backend {
   uint64_t R = 0;            // segmented region size
   bool init_seg_done = false;  // the init pass wrote ]t_lo, t_hi[ into segmented buffer 0
   uint64_t init_n_in = 0;
+  unsigned long long mail_seq = 0;
   GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
       : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
   bool timed() const { return ctx->cfg.record_timing != 0; }
-  cudaError_t tic() { return timed() ? cudaEventRecord(ctx->ev0, ctx->stream) : cudaSuccess; }
-  cudaError_t toc() { return timed() ? cudaEventRecord(ctx->ev1, ctx->stream) : cudaSuccess; }
-  void read_ms() {  // after the stream synchronised
-    step_ms = 0.0;
+  int next_slot = 0;
+  bool use_mail = true;  // results through the mapped mailbox (one GPU); false: device tuple + copy
+  cudaError_t tic() {
+    slot = -1;
+    if (!timed()) return cudaSuccess;
+    while (ctx->evpool.size() < 2 * (size_t)(next_slot + 1)) {
+      cudaEvent_t e;
+      cudaError_t err = cudaEventCreate(&e);
+      if (err != cudaSuccess) return err;
+      ctx->evpool.push_back(e);
+    }
+    return cudaEventRecord(ctx->evpool[2 * next_slot], ctx->stream);
+  }
+  cudaError_t toc() {
+    if (!timed()) return cudaSuccess;
+    slot = next_slot++;
+    return cudaEventRecord(ctx->evpool[2 * slot + 1], ctx->stream);
+  }
+  double slot_ms(int s) override {
+    if (s < 0 || 2 * (size_t)s + 1 >= ctx->evpool.size()) return 0.0;
     float ms = 0.f;
-    if (timed() && cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1) == cudaSuccess) step_ms = ms;
+    if (cudaEventSynchronize(ctx->evpool[2 * s + 1]) != cudaSuccess) return 0.0;
+    if (cudaEventElapsedTime(&ms, ctx->evpool[2 * s], ctx->evpool[2 * s + 1]) != cudaSuccess) return 0.0;
+    return ms;
+  }
+  // spin until the kernel published `seq` into the mailbox flag (a failed launch or a kernel that
+  // ended without publishing is detected through the stream)
+  cpsel_status wait_mail(const unsigned long long* flag, unsigned long long seq) {
+    const volatile unsigned long long* f = flag;
+    for (uint32_t i = 1;; ++i) {
+      if (*f == seq) {
+        std::atomic_thread_fence(std::memory_order_acquire);
+        return CPSEL_OK;
+      }
+      if ((i & 255u) == 0u) {
+        const cudaError_t e = cudaStreamQuery(ctx->stream);
+        if (e == cudaSuccess) {
+          if (*f == seq) {
+            std::atomic_thread_fence(std::memory_order_acquire);
+            return CPSEL_OK;
+          }
+          return fail(ctx, CPSEL_EINTERNAL, "kernel finished without publishing its result");
+        }
+        if (e != cudaErrorNotReady) return fail(ctx, CPSEL_ECUDA, "%s", cudaGetErrorString(e));
+      }
+#if defined(__x86_64__)
+      __builtin_ia32_pause();
+#endif
+    }
   }
   char* dbuf(int i) const { return static_cast<char*>(ctx->d_zb[i]); }
   const void* half_ptr(int side) const {  // dense halves of the last (dense) compaction
@@ -252,6 +311,11 @@ struct GpuBackend : Backend {
   // init kernel (fast form, then the checked form if anything came out non-finite)
   cpsel_status run_init(bool sync_result, uint64_t k, bool cut) {
     InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init, cut ? ctx->d_t0 : nullptr};
+    if (use_mail) {
+      a.out = &ctx->mb_dev->init;
+      a.done = &ctx->mb_dev->seq_init;
+      a.seq = ++ctx->seq;
+    }
     // with the segmented buffers in place the init pass also copies out ]t_lo, t_hi[ (R23)
     const bool fuse = cut && R > 0;
     init_seg_done = false;
@@ -269,9 +333,14 @@ struct GpuBackend : Backend {
     CK(toc());
     launches = cut ? 2 : 1;
     scanned = n;
-    CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    read_ms();
+    if (use_mail) {
+      cpsel_status w = wait_mail(&ctx->mb->seq_init, a.seq);
+      if (w != CPSEL_OK) return w;
+      *ctx->h_init = ctx->mb->init;
+    } else {
+      CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+    }
     const DevInit& r = *ctx->h_init;
     // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
     // cuts (which skip the shifted sum), as #x<t_hi + #x=t_hi + #x>t_hi < n
@@ -283,9 +352,14 @@ struct GpuBackend : Backend {
       init_n_in = r.pad;
     }
     if (suspicious) {
+      if (use_mail) a.seq = ++ctx->seq;
       CK(launch_init(dt, a, ctx->shape, ctx->stream, true));
       launches += 1;
-      if (sync_result) {
+      if (use_mail) {
+        cpsel_status w = wait_mail(&ctx->mb->seq_init, a.seq);
+        if (w != CPSEL_OK) return w;
+        *ctx->h_init = ctx->mb->init;
+      } else if (sync_result) {
         CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
       }
@@ -331,6 +405,11 @@ struct GpuBackend : Backend {
       a.mode = kHot;
       a.cursors = ctx->d_cursors;
       a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out = ctx->d_pass;
+      if (use_mail) {
+        a.out = &ctx->mb_dev->pass;
+        a.done = &ctx->mb_dev->seq_pass;
+        a.seq = mail_seq = ++ctx->seq;
+      }
       CK(tic());
       CK(launch_pass(dt, a, ctx->shape, ctx->stream));
       CK(toc());
@@ -353,6 +432,11 @@ struct GpuBackend : Backend {
       }
       a.cursors = ctx->d_cursors;
       a.partials = ctx->d_partials; a.ticket = ctx->d_ticket; a.out_tuple = ctx->d_pass;
+      if (use_mail) {
+        a.out_tuple = &ctx->mb_dev->pass;
+        a.done = &ctx->mb_dev->seq_pass;
+        a.seq = mail_seq = ++ctx->seq;
+      }
       CK(tic());
       // a compacted current array holds only bracket-interior elements
       CK(launch_seg_pass(dt, a, /*inside=*/cur != x, ctx->shape, ctx->stream));
@@ -367,10 +451,9 @@ struct GpuBackend : Backend {
                     uint64_t* z_hi) override {
     cpsel_status st = launch_local_pass(t, yL, yR, compact, dense);
     if (st != CPSEL_OK) return st;
-    CK(cudaMemcpyAsync(ctx->h_pass, ctx->d_pass, sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    read_ms();
-    const DevPass& r = *ctx->h_pass;
+    st = wait_mail(&ctx->mb->seq_pass, mail_seq);
+    if (st != CPSEL_OK) return st;
+    const DevPass r = ctx->mb->pass;
     o->c_lt = r.c_lt; o->c_eq = r.c_eq; o->c_lo = r.c_lo; o->c_hi = r.c_hi;
     o->L_lo = r.L_lo; o->L_hi = r.L_hi; o->P = r.P; o->N = r.N; o->pred = r.pred; o->succ = r.succ;
     if (compact) { zlo = r.z_lo; zhi = r.z_hi; }
@@ -406,14 +489,23 @@ struct GpuBackend : Backend {
   }
   cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out) {
     CK(tic());
-    CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream));
-    CK(toc());
-    CK(cudaMemcpyAsync(ctx->h_radix, ctx->d_radix, sizeof(RadixState), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    read_ms();
+    if (use_mail) {
+      const unsigned long long seq = ++ctx->seq;
+      CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
+                             &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, seq));
+      CK(toc());
+      cpsel_status w = wait_mail(&ctx->mb->seq_radix, seq);
+      if (w != CPSEL_OK) return w;
+      *out = ctx->mb->radix_value;
+    } else {
+      CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream));
+      CK(toc());
+      CK(cudaMemcpyAsync(ctx->h_radix, ctx->d_radix, sizeof(RadixState), cudaMemcpyDeviceToHost, ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      *out = ctx->h_radix->value;
+    }
     launches = dt == kF32 ? 7 : 13;
     scanned = m;
-    *out = ctx->h_radix->value;
     return CPSEL_OK;
   }
   // side 2 needs a contiguous current array; sides 0/1 a dense last compaction (driver guarantees)
@@ -430,7 +522,9 @@ struct ShardedBackend : GpuBackend {
   std::vector<uint64_t> zlo_rank, zhi_rank;   // per-rank halves of the last compacting pass
   cpsel_init_stats combined{};
   uint64_t n_global = 0;
-  ShardedBackend(cpsel_ctx* c, const void* x_, uint64_t n_local, int dt_) : GpuBackend(c, x_, n_local, dt_) {}
+  ShardedBackend(cpsel_ctx* c, const void* x_, uint64_t n_local, int dt_) : GpuBackend(c, x_, n_local, dt_) {
+    use_mail = false;  // the per-rank tuples are all-gathered from device memory
+  }
 
   // All-gather the per-rank init records and combine them in rank order (R17).
   cpsel_status gather_init() {
@@ -453,7 +547,7 @@ struct ShardedBackend : GpuBackend {
     CK(cudaMemcpyAsync(ctx->h_gather_init, ctx->d_gather_init, G * sizeof(DevInit), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (n == 0) step_ms = 0.0;
+    if (n == 0) slot = -1;
     scanned = n;
     n_rank.assign(G, 0);
     combined = cpsel_init_stats{};
@@ -493,6 +587,7 @@ struct ShardedBackend : GpuBackend {
     } else {
       launches = 0;
       scanned = 0;
+      slot = -1;
       if (compact) {
         tgt = dense ? ((cur_dbuf == 0) ? 1 : 0) : ((cur_sbuf == 0) ? 1 : 0);
         last_dense = dense;
@@ -506,7 +601,6 @@ struct ShardedBackend : GpuBackend {
     NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
     CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (launches) read_ms(); else step_ms = 0.0;
     // fixed rank-order combine: identical bytes on every rank (R17)
     cpsel_pass_stats s{};
     s.pred = -INFINITY; s.succ = INFINITY;
@@ -610,10 +704,24 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   const size_t es = elem_size(dt);
   cpsel_info inf{};
   if (trace) trace->clear();
+  // record_timing: timing slots of the steps (init, each pass with its trace row, select), resolved
+  // once the selection is over
+  int init_slot = -1, select_slot = -1;
+  std::vector<std::pair<int, long>> pass_slots;
   auto done = [&](double v, uint32_t reason) {
     *value = canonical_zero(v);
     inf.exit_reason = reason;
     inf.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (cfg.record_timing) {
+      inf.kernel_ms_init = be.slot_ms(init_slot);
+      inf.kernel_ms_select = be.slot_ms(select_slot);
+      inf.kernel_ms_passes = 0.0;
+      for (const auto& ps : pass_slots) {
+        const double ms = be.slot_ms(ps.first);
+        inf.kernel_ms_passes += ms;
+        if (trace && ps.second >= 0 && ps.second < (long)trace->size()) (*trace)[ps.second].kernel_ms = ms;
+      }
+    }
     if (info) *info = inf;
     return CPSEL_OK;
   };
@@ -621,7 +729,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     cpsel_status s2 = be.select(side, r, v);
     if (s2 != CPSEL_OK) return s2;
     inf.launches += be.launches;
-    inf.kernel_ms_select = be.step_ms;
+    select_slot = be.slot;
     inf.z_count = be.scanned;
     inf.bytes_moved += (uint64_t)(dt == kF32 ? 3 : 6) * be.scanned * es;
     return CPSEL_OK;
@@ -632,7 +740,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   if (st != CPSEL_OK) return st;
   inf.passes = 1;
   inf.launches += be.launches;
-  inf.kernel_ms_init = be.step_ms;
+  init_slot = be.slot;
   inf.bytes_moved = be.scanned * es;
   if (rec.nonfinite) return CPSEL_ENONFINITE;
   if (k <= rec.cnt_min) return done(rec.vmin, 0);
@@ -754,7 +862,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     st = be.pass(tq, yL, yR, compact, dense, &s, &zl, &zh);
     if (st != CPSEL_OK) return st;
     inf.launches += be.launches;
-    inf.kernel_ms_passes += be.step_ms;
+    // the pass's trace row (if recorded) is the next one pushed
+    pass_slots.emplace_back(be.slot, (trace && cfg.record_trace) ? (long)trace->size() : -1L);
     inf.passes++;
     inf.cp_iters++;
     inf.bytes_moved += be.scanned * es + (compact ? (zl + zh) * es : 0);
@@ -772,7 +881,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     row.c_eq = c_le - c_lt;
     row.kind = kind;
     row.compacted = compact ? 1 : 0;
-    row.kernel_ms = be.step_ms;
+    row.kernel_ms = 0.0;  // filled from the timing slot when the selection ends
     row.scanned = be.scanned;
     row.written = compact ? zl + zh : 0;
     // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
@@ -950,8 +1059,9 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaHostAlloc(&ctx->h_pass, sizeof(DevPass), cudaHostAllocDefault));
   CKC(cudaHostAlloc(&ctx->h_init, sizeof(DevInit), cudaHostAllocDefault));
   CKC(cudaHostAlloc(&ctx->h_radix, sizeof(RadixState), cudaHostAllocDefault));
-  CKC(cudaEventCreate(&ctx->ev0));
-  CKC(cudaEventCreate(&ctx->ev1));
+  CKC(cudaHostAlloc(&ctx->mb, sizeof(cpsel_ctx::Mailbox), cudaHostAllocMapped));
+  memset(ctx->mb, 0, sizeof(cpsel_ctx::Mailbox));
+  CKC(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->mb_dev), ctx->mb, 0));
   CKC(cudaDeviceSynchronize());
 #undef CKC
   *out = ctx;
@@ -970,11 +1080,10 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     for (void* p : dev)
       if (p) cudaFree(p);
     lms_free(ctx->lms);
-    void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init};
+    void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init, ctx->mb};
     for (void* p : host)
       if (p) cudaFreeHost(p);
-    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
-    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   }
   delete ctx;

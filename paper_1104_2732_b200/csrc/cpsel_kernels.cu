@@ -141,6 +141,16 @@ __device__ __forceinline__ void stream_array(const T* __restrict__ x, uint64_t n
 }
 
 // ------------------------------------------------------------------------------------------
+// Result mailbox: after the finishing thread wrote the result (possibly into mapped host memory),
+// make it visible system-wide, then set the flag the host spins on.
+__device__ __forceinline__ void publish_done(unsigned long long* done, unsigned long long seq) {
+  if (done) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(done) = seq;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // Block / grid reduction helpers (fixed order -> deterministic for a fixed grid).
 template <typename V> __device__ __forceinline__ V warp_sum(V v) {
 #pragma unroll
@@ -419,6 +429,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
     if (CUT && !CHECKED) r.nonfinite = a.n - tot.cC - tot.cD - tot.cE;
     r.has_cut = CUT ? 2ull : 0ull;
     *a.out = r;
+    publish_done(a.done, a.seq);
   }
 }
 
@@ -755,6 +766,7 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(PassArgs a) {
       a.cursors[1] = 0ull;
     }
     *a.out = r;
+    publish_done(a.done, a.seq);
   }
 }
 
@@ -802,7 +814,8 @@ __global__ void __launch_bounds__(kBlock) hist_kernel(const T* z, uint64_t m, co
 // One CTA of 1024 threads: find the digit holding rank r, extend the prefix, clear hist.
 template <typename T>
 __global__ void __launch_bounds__(1024) pick_kernel(RadixState* st, unsigned* hist, int shift, int bits,
-                                                    int last) {
+                                                    int last, double* vout, unsigned long long* done,
+                                                    unsigned long long seq) {
   __shared__ unsigned long long scan[1024];
   const int tid = threadIdx.x;
   const int nb = 1 << bits;  // <= 2048: two bins per thread
@@ -832,6 +845,8 @@ __global__ void __launch_bounds__(1024) pick_kernel(RadixState* st, unsigned* hi
     if (last) {
       st->key = st->prefix;
       st->value = (sizeof(T) == 4) ? from_key_f32(st->prefix) : from_key_f64(st->prefix);
+      if (vout) *vout = st->value;
+      publish_done(done, seq);
     }
   }
   if (2 * tid < kBins) hist[2 * tid] = 0u;
@@ -1136,6 +1151,7 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
       a.cursors[1] = 0ull;
     }
     *a.out_tuple = r;
+    publish_done(a.done, a.seq);
   }
 }
 
@@ -1393,6 +1409,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.res0 = r.res1 = r.res2 = 0;
     r.has_cut = 3ull;  // two cuts + the interior compacted
     *ia.out = r;
+    publish_done(ia.done, ia.seq);
   }
 }
 
@@ -1858,7 +1875,8 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 }
 
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
-                                unsigned* hist, const LaunchShape& s, cudaStream_t st) {
+                                unsigned* hist, const LaunchShape& s, cudaStream_t st, double* vout,
+                                unsigned long long* done, unsigned long long seq) {
   radix_init_kernel<<<1, 1, 0, st>>>(state, r, m);
   // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10
   static const int plan32[] = {21, 11, 10, 11, 0, 10};
@@ -1871,11 +1889,11 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
     if (dtype == kF32) {
       const int grid = clamp_grid(s.grid_hist[kF32], m, kBlock * 2 * 4);
       hist_kernel<float><<<grid, kBlock, 0, st>>>(static_cast<const float*>(z), m, state, shift, bits, hist);
-      pick_kernel<float><<<1, 1024, 0, st>>>(state, hist, shift, bits, last);
+      pick_kernel<float><<<1, 1024, 0, st>>>(state, hist, shift, bits, last, vout, done, seq);
     } else {
       const int grid = clamp_grid(s.grid_hist[kF64], m, kBlock * 2 * 2);
       hist_kernel<double><<<grid, kBlock, 0, st>>>(static_cast<const double*>(z), m, state, shift, bits, hist);
-      pick_kernel<double><<<1, 1024, 0, st>>>(state, hist, shift, bits, last);
+      pick_kernel<double><<<1, 1024, 0, st>>>(state, hist, shift, bits, last, vout, done, seq);
     }
   }
   return cudaGetLastError();

@@ -63,6 +63,8 @@ struct PassArgs {
   void* partials;                    // >= grid PassPartial
   unsigned int* ticket;              // self-resetting grid ticket
   DevPass* out;                      // device (or mapped host) result
+  unsigned long long* done;          // optional (mapped host) mailbox flag: set to seq after *out is written
+  unsigned long long seq;
 };
 
 // Segmented compaction (a4, warp-private output regions).  The compacting pass is run by a fixed
@@ -92,6 +94,8 @@ struct SegArgs {
   void* partials;
   unsigned int* ticket;
   DevPass* out_tuple;
+  unsigned long long* done;    // optional mailbox flag (see PassArgs)
+  unsigned long long seq;
 };
 
 struct InitArgs {
@@ -101,6 +105,8 @@ struct InitArgs {
   unsigned int* ticket;
   DevInit* out;
   const void* t0;   // device pointer to the two extra cuts t_lo, t_hi (elements of the dtype), or nullptr
+  unsigned long long* done;  // optional mailbox flag (see PassArgs)
+  unsigned long long seq;
 };
 
 struct LaunchShape {
@@ -136,8 +142,12 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 // Radix select of the r-th smallest (1-based) of z[0..m) (any element alignment).
 // hist: >= 2048 unsigned ints, zero on entry, left zeroed.  state: device RadixState.
 // On completion state->value holds the element (as double).
+// vout/done/seq (optional): the last round also writes the value to *vout (mapped host memory)
+// and then sets *done = seq.
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
-                                unsigned int* hist, const LaunchShape& s, cudaStream_t st);
+                                unsigned int* hist, const LaunchShape& s, cudaStream_t st,
+                                double* vout = nullptr, unsigned long long* done = nullptr,
+                                unsigned long long seq = 0);
 
 // Step a8: per-column k-th smallest of S (n x C column-major, float32), one CTA per column.
 struct BatchArgs {
