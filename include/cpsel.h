@@ -62,7 +62,10 @@ typedef struct {
                                 kernel_ms fields).  Default 0 */
   int32_t init_cut;          /* 1: the init pass also evaluates two extra cuts at sample quantiles
                                 bracketing the target rank (R23), saving passes.  Default 1 */
-  int32_t reserved;
+  int32_t objective;         /* 1: every trace row carries F_k(t): the init pass also sums
+                                (t_lo-x)^+ and (x-t_hi)^+ (4 more issue slots per element).
+                                0: rows after the init cuts report F = NaN — the iterates never
+                                need F (App. A: interior means), R25.  Default 0 */
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -98,7 +101,8 @@ typedef struct {
   double x0;              /* the shift x[0] */
   double S;               /* sum_i (x_i - x0), fp64 (0 when has_cut: the first iterate then comes
                              from the cut's sums and the pass skips this sum) */
-  uint64_t has_cut;       /* 2 if the pass also evaluated the two extra cuts t_lo <= t_hi (R23): */
+  uint64_t has_cut;       /* bit 1 (2): the pass also evaluated the two extra cuts t_lo <= t_hi (R23);
+                             bit 0 (1): it also copied ]t_lo, t_hi[ out; bit 2 (4): N_lo, P_hi valid */
   double t_lo, t_hi;      /*   sample quantiles bracketing rank k (elements of x) */
   uint64_t c_le_lo, c_lt_hi; /* #{x<=t_lo}, #{x<t_hi}: the counts a bracket update needs at each cut
                              when the target lies between them; a cut beyond the target moves to the

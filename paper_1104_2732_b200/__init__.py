@@ -37,7 +37,7 @@ class Config(C.Structure):
     _fields_ = [("z_cap", C.c_uint64), ("direct_threshold", C.c_uint64), ("select_cap", C.c_uint64),
                 ("max_iters", C.c_uint32),
                 ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32),
-                ("init_cut", C.c_int32), ("reserved", C.c_int32)]
+                ("init_cut", C.c_int32), ("objective", C.c_int32)]
 
 
 class Info(C.Structure):

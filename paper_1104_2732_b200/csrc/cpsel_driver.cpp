@@ -326,7 +326,7 @@ struct GpuBackend : Backend {
       sa.out = ctx->d_sb[0];
       sa.R = R;
       sa.seg_out = static_cast<SegEntry*>(ctx->d_st[0]);
-      CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream));
+      CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
     }
@@ -771,7 +771,13 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   // P(t_lo) = I + P_hi + #{x>=t_hi}(t_hi-t_lo), N(t_hi) = N_lo + #{x<t_hi}(t_hi-t_lo) - I.
   if (rec.has_cut) {
     const long double tl = rec.t_lo, th = rec.t_hi, dlh = th - tl;
-    const long double N_tl = rec.N_lo, P_th = rec.P_hi;
+    // R25: without the init pass's positive-part sums, F_k (and so every later row's F) is unknown;
+    // the iterate never needs it: the usual bracket ]t_lo, t_hi[ starts from its interior mean
+    // t_lo + I/m, any other from the midpoint
+    const bool sums = (rec.has_cut & 4) != 0;
+    const long double N_tl = sums ? (long double)rec.N_lo : (long double)NAN;
+    const long double P_th = sums ? (long double)rec.P_hi : (long double)NAN;
+    t = NAN;
     const long double P_tl = (long double)rec.I_in + P_th + (long double)(n - rec.c_lt_hi) * dlh;  // R24
     const long double N_th = N_tl + (long double)rec.c_lt_hi * dlh - (long double)rec.I_in;
     auto row_of = [&](double tt, uint64_t clt, uint64_t ceq, long double Nt, long double Pt) {
@@ -825,6 +831,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);
     }
+    if (!std::isfinite(t)) t = 0.5 * yL + 0.5 * yR;
     // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
     if (be.init_compacted() && yL == rec.t_lo && yR == rec.t_hi) {
       if (m != be.init_written()) {

@@ -427,7 +427,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
     r.c_le_lo = tot.cA + tot.cB; r.c_lt_hi = tot.cC; r.res0 = r.res1 = r.res2 = 0;
     // a NaN is in none of <t_hi, =t_hi, >t_hi: the fast form reports the shortfall (CHECKED counts all)
     if (CUT && !CHECKED) r.nonfinite = a.n - tot.cC - tot.cD - tot.cE;
-    r.has_cut = CUT ? 2ull : 0ull;
+    r.has_cut = CUT ? 6ull : 0ull;  // two cuts, with N_lo / P_hi
     *a.out = r;
     publish_done(a.done, a.seq);
   }
@@ -1160,59 +1160,85 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
 // strictly between the cuts, in ONE read of x.  Warp-strided groups and the warp-private region
 // layout of seg_pass_kernel (the interior lands in run 0 of each warp's entry), so the following
 // cutting-plane passes read it as a segmented array.
-template <typename T> struct InitSeg {
+// SUMS: also accumulate N(t_lo) = sum (t_lo-x)^+ and P(t_hi) = sum (x-t_hi)^+ (only the reported
+// objective values need them, R25)
+template <typename T, bool SUMS> struct InitSeg {
   static constexpr int VE = VecOf<T>::N;
   static constexpr int G = kSegU * VE;
   static constexpr int GW = 32 * G;
   T mn, mx, tl, th;
   unsigned cmn = 0, cmx = 0, nan = 0;
   float fL = 0;                   // #x<=t_lo (exact per-thread float counter, < 2^24 per thread)
-  T gN[kSegU], gP[kSegU];
+  T gN[kSegU], gP[kSegU], gI[kSegU];
   double N0 = 0, P0 = 0, I0 = 0;
   T vals[G];
   unsigned bits;
   unsigned long long n_in = 0;    // warp-uniform: interior elements written
-  T* stage;
   T* out;
   uint64_t reg_lo;
 
-  // one element: 3 compares, 2 subs, 1 counter, 2 sums, 1 interior bit (9 issue slots):
-  //   fL = #x<=t_lo, N += (t_lo-x) on x<=t_lo, P += (x-t_hi) on x>t_hi, interior bit on t_lo<x<t_hi.
-  //   #x<t_hi = #x<=t_lo + #interior; the interior sum is taken while its elements are copied out.
+  // one element, SUMS: 3 compares, 2 subs, 1 counter, 3 sums, 1 interior bit (10 issue slots):
+  //   fL = #x<=t_lo, N += (t_lo-x) on x<=t_lo, P += (x-t_hi) on x>t_hi, I += (x-t_lo) and the
+  //   interior bit on t_lo<x<t_hi.  #x<t_hi = #x<=t_lo + #interior.
+  //   !SUMS: fL, I and the interior bit only (6 slots).
   //   (#x==t_lo and #x==t_hi are not needed, R24.)
   __device__ __forceinline__ void cut(float v, int u, int idx) {
-    asm("{\n\t.reg .pred pL, pH, pI;\n\t.reg .f32 dl, dh;\n\t"
-        "setp.le.f32 pL, %4, %5;\n\t"
-        "setp.gt.f32 pH, %4, %6;\n\t"
-        "setp.lt.and.f32 pI, %4, %6, !pL;\n\t"
-        "sub.rn.f32 dl, %5, %4;\n\t"
-        "sub.rn.f32 dh, %4, %6;\n\t"
-        "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
-        "@pL add.rn.f32 %1, %1, dl;\n\t"
-        "@pH add.rn.f32 %2, %2, dh;\n\t"
-        "@pI or.b32 %3, %3, %7;\n\t}"
-        : "+f"(fL), "+f"(gN[u]), "+f"(gP[u]), "+r"(bits)
-        : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
+    if (SUMS)
+      asm("{\n\t.reg .pred pL, pH, pI;\n\t.reg .f32 dl, dh;\n\t"
+          "setp.le.f32 pL, %5, %6;\n\t"
+          "setp.gt.f32 pH, %5, %7;\n\t"
+          "setp.lt.and.f32 pI, %5, %7, !pL;\n\t"
+          "sub.rn.f32 dl, %6, %5;\n\t"
+          "sub.rn.f32 dh, %5, %7;\n\t"
+          "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+          "@pL add.rn.f32 %1, %1, dl;\n\t"
+          "@pH add.rn.f32 %2, %2, dh;\n\t"
+          "@pI sub.rn.f32 %3, %3, dl;\n\t"
+          "@pI or.b32 %4, %4, %8;\n\t}"
+          : "+f"(fL), "+f"(gN[u]), "+f"(gP[u]), "+f"(gI[u]), "+r"(bits)
+          : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
+    else
+      asm("{\n\t.reg .pred pL, pI;\n\t.reg .f32 dl;\n\t"
+          "setp.le.f32 pL, %3, %4;\n\t"
+          "setp.lt.and.f32 pI, %3, %5, !pL;\n\t"
+          "sub.rn.f32 dl, %3, %4;\n\t"
+          "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+          "@pI add.rn.f32 %1, %1, dl;\n\t"
+          "@pI or.b32 %2, %2, %6;\n\t}"
+          : "+f"(fL), "+f"(gI[u]), "+r"(bits)
+          : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
     vals[idx] = v;
   }
   __device__ __forceinline__ void cut(double v, int u, int idx) {
-    asm("{\n\t.reg .pred pL, pH, pI;\n\t.reg .f64 dl, dh;\n\t"
-        "setp.le.f64 pL, %4, %5;\n\t"
-        "setp.gt.f64 pH, %4, %6;\n\t"
-        "setp.lt.and.f64 pI, %4, %6, !pL;\n\t"
-        "sub.rn.f64 dl, %5, %4;\n\t"
-        "sub.rn.f64 dh, %4, %6;\n\t"
-        "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
-        "@pL add.rn.f64 %1, %1, dl;\n\t"
-        "@pH add.rn.f64 %2, %2, dh;\n\t"
-        "@pI or.b32 %3, %3, %7;\n\t}"
-        : "+f"(fL), "+d"(gN[u]), "+d"(gP[u]), "+r"(bits)
-        : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
+    if (SUMS)
+      asm("{\n\t.reg .pred pL, pH, pI;\n\t.reg .f64 dl, dh;\n\t"
+          "setp.le.f64 pL, %5, %6;\n\t"
+          "setp.gt.f64 pH, %5, %7;\n\t"
+          "setp.lt.and.f64 pI, %5, %7, !pL;\n\t"
+          "sub.rn.f64 dl, %6, %5;\n\t"
+          "sub.rn.f64 dh, %5, %7;\n\t"
+          "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+          "@pL add.rn.f64 %1, %1, dl;\n\t"
+          "@pH add.rn.f64 %2, %2, dh;\n\t"
+          "@pI sub.rn.f64 %3, %3, dl;\n\t"
+          "@pI or.b32 %4, %4, %8;\n\t}"
+          : "+f"(fL), "+d"(gN[u]), "+d"(gP[u]), "+d"(gI[u]), "+r"(bits)
+          : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
+    else
+      asm("{\n\t.reg .pred pL, pI;\n\t.reg .f64 dl;\n\t"
+          "setp.le.f64 pL, %3, %4;\n\t"
+          "setp.lt.and.f64 pI, %3, %5, !pL;\n\t"
+          "sub.rn.f64 dl, %3, %4;\n\t"
+          "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+          "@pI add.rn.f64 %1, %1, dl;\n\t"
+          "@pI or.b32 %2, %2, %6;\n\t}"
+          : "+f"(fL), "+d"(gI[u]), "+r"(bits)
+          : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
     vals[idx] = v;
   }
   __device__ __forceinline__ void begin() {
 #pragma unroll
-    for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = T(0);
+    for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = gI[u] = T(0);
     bits = 0u;
   }
   __device__ __forceinline__ void vec(const float4& v, int u) {
@@ -1280,8 +1306,11 @@ template <typename T> struct InitSeg {
   }
   __device__ __forceinline__ void end(int nvalid) {
     extremes(nvalid);
-    N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
-    P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+    if (SUMS) {
+      N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
+      P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+    }
+    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
     const int lane = threadIdx.x & 31;
     const unsigned cnt = (unsigned)__popc(bits);
     unsigned incl = cnt;
@@ -1292,31 +1321,21 @@ template <typename T> struct InitSeg {
     }
     const unsigned tot = __shfl_sync(FULL, incl, 31);
     if (tot == 0u) return;
-    // predicated shared stores (no branches): slot j goes to stage[pos] iff bit j is set
-    T* sp = stage + (incl - cnt);
+    // predicated stores straight into the warp's region (the order inside a run is free):
+    // lane l writes its interior elements at [excl_l, incl_l) of this group's slice
+    T* dp = out + reg_lo + n_in + (incl - cnt);
 #pragma unroll
     for (int j = 0; j < G; ++j)
-      if (bits & (1u << j)) *sp++ = vals[j];
-    __syncwarp();
-    T* dst = out + reg_lo + n_in;
-    T isum = T(0);  // sum over the copied interior of (x - t_lo)
-    for (unsigned i = lane; i < tot; i += 32) {
-      const T v = stage[i];
-      dst[i] = v;
-      isum += v - tl;
-    }
-    I0 += (double)isum;
+      if (bits & (1u << j)) *dp++ = vals[j];
     n_in += tot;
-    __syncwarp();
   }
 };
 
-template <typename T>
+template <typename T, bool SUMS>
 __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArgs a) {
-  using F = InitSeg<T>;
+  using F = InitSeg<T, SUMS>;
   using V = typename VecOf<T>::V;
   constexpr int VE = VecOf<T>::N;
-  __shared__ __align__(16) T stage_all[kWarps * F::GW];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
   const uint64_t Wtot = (uint64_t)gridDim.x * kWarps;
@@ -1326,7 +1345,6 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   f.mn = tinf<T>(); f.mx = -tinf<T>();
   f.tl = static_cast<const T*>(ia.t0)[0];
   f.th = static_cast<const T*>(ia.t0)[1];
-  f.stage = stage_all + (size_t)w * F::GW;
   f.out = static_cast<T*>(a.out);
   f.reg_lo = W * a.R;
   const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
@@ -1407,7 +1425,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.c_le_lo = tot.cA;
     r.c_lt_hi = tot.cA + tot.pad2;  // every x < t_hi is <= t_lo or interior
     r.res0 = r.res1 = r.res2 = 0;
-    r.has_cut = 3ull;  // two cuts + the interior compacted
+    r.has_cut = SUMS ? 7ull : 3ull;  // two cuts + the interior compacted (+ N_lo, P_hi)
     *ia.out = r;
     publish_done(ia.done, ia.seq);
   }
@@ -1416,7 +1434,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
 // The batched kernel's init pass: the per-element step of init_seg_kernel (stats + two cuts +
 // interior bit) with the block-level dense compaction of PassFn (one CTA per column, the interior
 // ]t_lo, t_hi[ goes to the CTA's buffer from index 0).
-struct BatchInitFn : InitSeg<float> {
+struct BatchInitFn : InitSeg<float, false> {
   PassFn<float, kCompact, 4> pc;
   int nvalid = 0;
   __device__ __forceinline__ void group_begin() {
@@ -1425,19 +1443,12 @@ struct BatchInitFn : InitSeg<float> {
   }
   template <bool MASKED, typename V> __device__ __forceinline__ void vec(const V& v, bool ok, int u) {
     if (MASKED && !ok) return;
-    InitSeg<float>::vec(v, u);
+    InitSeg<float, false>::vec(v, u);
     nvalid = (u + 1) * 4;
   }
   __device__ __forceinline__ void group_end() {
     extremes(nvalid);
-    N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
-    P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
-    // the interior sum: over this thread's interior elements (bits), in the group
-    float isum = 0.f;
-#pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if ((bits >> j) & 1u) isum += vals[j] - tl;
-    I0 += (double)isum;
+    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
 #pragma unroll
     for (int j = 0; j < 16; ++j) pc.vals[j] = vals[j];
     pc.lo_bits = bits;
@@ -1449,8 +1460,7 @@ struct BatchInitFn : InitSeg<float> {
     begin();
     if (ok) cut(v, 0, 0);
     extremes(ok ? 1 : 0);
-    N0 += (double)gN[0]; P0 += (double)gP[0];
-    if (bits & 1u) I0 += (double)(v - tl);
+    I0 += (double)gI[0];
     if (bits & 1u) {
       const unsigned long long pos = atomicAdd(&pc.cursors[0], 1ull);
       if (pos < pc.z_cap) pc.z[pos] = v;
@@ -1623,42 +1633,34 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
           st.D_lo = 0; st.on_z = 0; st.slow = 0; st.bisect = 0;
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
           st.t = 0.5 * p.vmin + 0.5 * p.vmax;  // only used if neither cut lies strictly inside
-          if (cut) {  // the two extra cuts, exactly as the host driver applies them
-            const double tl = st.cut_lo, th = st.cut_hi, dlh = th - tl;
-            const double P_tl = p.I0 + p.P0 + (double)(n - p.cC) * dlh;
-            bool settled = false;
-            // R24: #x<=t_lo and #x<t_hi only; a cut on the far side of the target becomes the
-            // adjacent float (next(t_lo) / prev(t_hi)), where the missing count is the known one
+          if (cut) {  // the two extra cuts, as the host driver applies them (R23-R25)
+            // the batched init pass keeps only #x<=t_lo, the interior count and sum: the usual
+            // bracket ]t_lo, t_hi[ starts from its interior mean (App. A); a cut on the far side of
+            // the target moves to the adjacent float and the iteration starts from the midpoint
+            const double tl = st.cut_lo, th = st.cut_hi;
+            bool settled = false, mean_ok = false;
             if (tl > p.vmin && tl < p.vmax) {
               const unsigned long long c_le = p.cA;
               if (c_le < k) {
                 st.yL = (float)tl; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
-                st.t = tl + (P_tl - (double)(n - st.c_lt_R) * ((double)st.yR - tl)) / (double)st.m;
               } else {  // y_R <- next(t_lo): #x<next(t_lo) = #x<=t_lo
-                const double yr = (double)nextafterf((float)tl, INFINITY);
-                const double N_r = p.N0 + (double)c_le * (yr - tl);
-                const double L_lo = N_r - (double)st.c_le_L * (yr - (double)st.yL);
-                st.yR = (float)yr; st.c_lt_R = c_le; st.m = c_le - st.c_le_L;
-                st.t = yr - L_lo / (double)st.m;
+                st.yR = nextafterf((float)tl, INFINITY); st.c_lt_R = c_le; st.m = c_le - st.c_le_L;
                 settled = true;
               }
             }
             if (!settled && th > (double)st.yL && th < p.vmax) {
               const unsigned long long c_lt = p.cC;
-              const double N_th = p.N0 + (double)p.cC * dlh - p.I0;
               if (c_lt >= k) {
-                const double L_lo = ((double)st.yL == tl) ? (double)(c_lt - st.c_le_L) * dlh - p.I0
-                                                          : N_th - (double)st.c_le_L * (th - (double)st.yL);
                 st.yR = (float)th; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
-                st.t = th - L_lo / (double)st.m;
+                if ((double)st.yL == tl) {  // interior ]t_lo, t_hi[: mean = t_lo + I / m
+                  st.t = tl + p.I0 / (double)st.m;
+                  mean_ok = true;
+                }
               } else {  // y_L <- prev(t_hi): #x<=prev(t_hi) = #x<t_hi
-                const double yl = (double)nextafterf((float)th, -INFINITY);
-                const double P_l = p.P0 + (double)(n - c_lt) * (th - yl);
-                const double L_hi = P_l - (double)(n - st.c_lt_R) * ((double)st.yR - yl);
-                st.yL = (float)yl; st.c_le_L = c_lt; st.m = st.c_lt_R - c_lt;
-                st.t = yl + L_hi / (double)st.m;
+                st.yL = nextafterf((float)th, -INFINITY); st.c_le_L = c_lt; st.m = st.c_lt_R - c_lt;
               }
             }
+            if (!mean_ok) st.t = 0.5 * (double)st.yL + 0.5 * (double)st.yR;
             // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
             if (st.phase == 0 && (double)st.yL == tl && (double)st.yR == th && st.m == p.pad2 && p.pad2 <= a.cap) {
               st.cur = my0; st.n_cur = p.pad2; st.cur_buf = 0;
@@ -1847,10 +1849,17 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 
 int seg_total_warps(int dtype, const LaunchShape& s) { return s.grid_seg[dtype] * kWarps; }
 
-cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, const LaunchShape& s, cudaStream_t st) {
+cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, const LaunchShape& s, cudaStream_t st,
+                            bool sums) {
   // the same grid as seg_pass_kernel: its warp regions / run table are what later passes read
-  if (dtype == kF32) init_seg_kernel<float><<<s.grid_seg[kF32], kBlock, 0, st>>>(ia, a);
-  else init_seg_kernel<double><<<s.grid_seg[kF64], kBlock, 0, st>>>(ia, a);
+  const int g = s.grid_seg[dtype];
+  if (dtype == kF32) {
+    if (sums) init_seg_kernel<float, true><<<g, kBlock, 0, st>>>(ia, a);
+    else init_seg_kernel<float, false><<<g, kBlock, 0, st>>>(ia, a);
+  } else {
+    if (sums) init_seg_kernel<double, true><<<g, kBlock, 0, st>>>(ia, a);
+    else init_seg_kernel<double, false><<<g, kBlock, 0, st>>>(ia, a);
+  }
   return cudaGetLastError();
 }
 

@@ -130,7 +130,9 @@ uint64_t seg_region(int dtype, uint64_t n, const LaunchShape& s);
 // The init reduction + both extra cuts + the copy_if of ]t_lo, t_hi[ into run 0 of each warp's
 // region (a.out / a.R / a.seg_out) in one read (R23); DevInit.pad = interior elements written,
 // has_cut = 3.  ia.t0 must hold the two cuts.
-cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, const LaunchShape& s, cudaStream_t st);
+// sums: also N_lo = sum (t_lo-x)^+ and P_hi = sum (x-t_hi)^+ (has_cut = 7), else has_cut = 3 (R25).
+cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, const LaunchShape& s, cudaStream_t st,
+                            bool sums);
 // inside: every input element lies strictly inside the bracket (input = a kept half)
 cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const LaunchShape& s, cudaStream_t st);
 

@@ -61,7 +61,7 @@ class NumpyShard:
             tl, th = np.float64(smp[il]), np.float64(smp[ih])
             xd = x.astype(np.float64)
             inner = (x > tl) & (x < th)
-            out.update(has_cut=2, t_lo=float(tl), t_hi=float(th),
+            out.update(has_cut=6, t_lo=float(tl), t_hi=float(th),
                        c_le_lo=int((x <= tl).sum()), c_lt_hi=int((x < th).sum()),
                        N_lo=float(np.sum(tl - xd[x < tl])), P_hi=float(np.sum(xd[x > th] - th)),
                        I_in=float(np.sum(xd[inner] - tl)))

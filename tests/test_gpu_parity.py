@@ -61,7 +61,7 @@ def test_init_extra_cut(cp, dtype, dist):
     n = 2_000_003
     x = datagen.make(dist, n, dtype)
     s = cp.init_stats(tdev(x))
-    assert s["has_cut"] == 2
+    assert s["has_cut"] & 2 and s["has_cut"] & 4          # cuts, with the positive-part sums
     tl, th = s["t_lo"], s["t_hi"]
     assert tl <= th and np.any(x == tl) and np.any(x == th)
     rl = O.pass_stats(x, tl, -math.inf, math.inf)
@@ -256,7 +256,7 @@ def test_trace_replay_F_parity(cp):
             x = datagen.make(dist, 2_000_003, dtype)
             xd = tdev(x)
             for k in (O.median_rank(x.size), 1000):
-                cp.set_config(force_cp=1, z_cap=1000)
+                cp.set_config(force_cp=1, z_cap=1000, objective=1)
                 cp.select_kth(xd, k)
                 tr = cp.get_trace()
                 assert tr
@@ -267,7 +267,31 @@ def test_trace_replay_F_parity(cp):
                     else:
                         assert (row["c_lt"], row["c_eq"]) == (ref["c_lt"], ref["c_eq"])
                     assert row["F"] == pytest.approx(float(ref["F"]), rel=REL[dtype])
-    cp.set_config(force_cp=0, z_cap=0)
+    cp.set_config(force_cp=0, z_cap=0, objective=0)
+
+
+@pytest.mark.parametrize("objective", [0, 1])
+def test_fused_init_trace(cp, objective):
+    """The fused init pass (cuts + copy-out of ]t_lo, t_hi[, R23) at a size where the segmented
+    buffers exist: value exact; with objective=1 every row's F_k(t) matches the oracle, with
+    objective=0 the rows after the cuts carry F = NaN (R25) and the counts stay exact."""
+    x = datagen.make("normal", (1 << 23) + 77, "f32")
+    xd = tdev(x)
+    k = O.median_rank(x.size)
+    cp.set_config(objective=objective)
+    v, info = cp.select_kth(xd, k, return_info=True)
+    tr = cp.get_trace()
+    cp.set_config(objective=0)
+    assert v == O.order_statistic(x, k)
+    assert info["init_written"] > 0 and tr[0]["kind"] == 2
+    for row in tr:
+        ref = O.eval_at(x, k, row["t"], -math.inf, math.inf)
+        if row["kind"] != 2:
+            assert (row["c_lt"], row["c_eq"]) == (ref["c_lt"], ref["c_eq"])
+        if objective:
+            assert row["F"] == pytest.approx(float(ref["F"]), rel=REL["f32"])
+        else:
+            assert math.isnan(row["F"])
 
 
 def test_host_buffer_path(cp):
