@@ -66,6 +66,10 @@ typedef struct {
                                 (t_lo-x)^+ and (x-t_hi)^+ (4 more issue slots per element).
                                 0: rows after the init cuts report F = NaN — the iterates never
                                 need F (App. A: interior means), R25.  Default 0 */
+  int32_t pass_cuts;         /* 1: a compacted bracket larger than select_cap is cut at two sample
+                                quantiles of its own, keeping only what lies between them (R26,
+                                multi-point step).  Ignored with objective=1.  Default 1 */
+  int32_t reserved;
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -207,6 +211,11 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
  * the CPU tests (world-size-2 gloo tests of the sharded combine) to exercise the exact host
  * logic the GPU path runs.  Each callback returns 0 on success. */
 typedef struct {
+  double t_a, t_b;        /* the two cuts */
+  double I;               /* sum over t_a < x < t_b of (x - t_a) */
+  uint64_t le_a, inner;   /* #{x <= t_a}, #{t_a < x < t_b} (local to the current array) */
+} cpsel_cut_stats;
+typedef struct {
   void* user;
   /* init reduction over the whole (possibly sharded) array: fill *out. */
   int (*init)(void* user, cpsel_init_stats* out);
@@ -220,6 +229,11 @@ typedef struct {
   /* exact selection of the r-th smallest (1-based) of the retained half `side` of the last
      compacting pass, or of the current array if side == 2. */
   int (*select)(void* user, int side, uint64_t r, double* value_out);
+  /* optional (NULL: none): the R26 cut pass over the current array, which is exactly the bracket
+     interior — two sample cuts t_a <= t_b (elements of it) around its local rank r; fill *out with
+     #{x <= t_a}, #{t_a < x < t_b}, sum over the latter of (x - t_a), and retain that set as
+     half 0 of a compacting pass. */
+  int (*cut)(void* user, uint64_t r, cpsel_cut_stats* out);
 } cpsel_host_backend;
 cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dtype dtype,
                               uint64_t k, const cpsel_config* cfg, double* value_out,

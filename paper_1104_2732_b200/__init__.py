@@ -37,7 +37,8 @@ class Config(C.Structure):
     _fields_ = [("z_cap", C.c_uint64), ("direct_threshold", C.c_uint64), ("select_cap", C.c_uint64),
                 ("max_iters", C.c_uint32),
                 ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32),
-                ("init_cut", C.c_int32), ("objective", C.c_int32)]
+                ("init_cut", C.c_int32), ("objective", C.c_int32),
+                ("pass_cuts", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Info(C.Structure):
@@ -89,9 +90,17 @@ _SEL_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.POINTER(C.c_do
 _ADOPT_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 
 
+class CutStats(C.Structure):
+    _fields_ = [("t_a", C.c_double), ("t_b", C.c_double), ("I", C.c_double), ("le_a", C.c_uint64),
+                ("inner", C.c_uint64)]
+
+
+_CUT_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.POINTER(CutStats))
+
+
 class HostBackend(C.Structure):
     _fields_ = [("user", C.c_void_p), ("init", _INIT_CB), ("pass_", _PASS_CB), ("adopt", _ADOPT_CB),
-                ("select", _SEL_CB)]
+                ("select", _SEL_CB), ("cut", _CUT_CB)]
 
 
 # every symbol the header declares (tests check the library exports exactly these)
@@ -416,10 +425,12 @@ def select_kth_sharded(shard, k: int, return_info: bool = False):
 
 
 # ------------------------------------------------------------------------------------------ host driver
-def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, adopt_fn, select_fn, config: dict | None = None):
+def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, adopt_fn, select_fn, config: dict | None = None,
+               cut_fn=None):
     """Run libcpsel's cutting-plane driver with Python callbacks for the data steps
     (init_fn() -> dict of InitStats fields; pass_fn(t, y_lo, y_hi, compact) -> dict of PassStats
-    fields over the current array; adopt_fn(side); select_fn(side, r) -> float).  No GPU
+    fields over the current array; adopt_fn(side); select_fn(side, r) -> float; optional
+    cut_fn(r) -> dict of CutStats fields, the R26 cut pass).  No GPU
     involved: used to test the host logic."""
     lib = load()
     errors = []
@@ -460,7 +471,18 @@ def drive_host(n: int, k: int, dtype: str, init_fn, pass_fn, adopt_fn, select_fn
             errors.append(e)
             return 1
 
-    cbs = (_INIT_CB(_init), _PASS_CB(_pass), _ADOPT_CB(_adopt), _SEL_CB(_sel))
+    def _cut(_u, r, out):
+        try:
+            d = cut_fn(r)
+            for f, _ in CutStats._fields_:
+                setattr(out.contents, f, d[f])
+            return 0
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+            return 1
+
+    cbs = (_INIT_CB(_init), _PASS_CB(_pass), _ADOPT_CB(_adopt), _SEL_CB(_sel),
+           _CUT_CB(_cut) if cut_fn is not None else C.cast(None, _CUT_CB))
     be = HostBackend(None, *cbs)
     cfg = Config()
     lib.cpsel_config_default(C.byref(cfg))

@@ -211,6 +211,17 @@ struct Backend {
   virtual cpsel_status adopt_init() { return CPSEL_EINTERNAL; }
   // current array <- half `side` (0: ]yL,t[, 1: ]t,yR[) of the last compacting pass
   virtual cpsel_status adopt(int side) = 0;
+  // R26 cut pass over the current array (exactly the bracket interior, m elements): two sample
+  // cuts t_a <= t_b around local rank r, #x<=t_a, the copy_if of ]t_a, t_b[ (dense if asked) and
+  // its sum of (x - t_a).  adopt(0) then makes the copy the current array.
+  struct CutResult {
+    double ta, tb, I;
+    uint64_t le_a, inner;  // local #x<=t_a, #]t_a,t_b[
+  };
+  virtual bool has_cut_pass() const { return false; }
+  virtual cpsel_status cut_pass(uint64_t /*r*/, bool /*dense*/, CutResult*) { return CPSEL_EINTERNAL; }
+  // the bracket shrank without a compaction: the current array now also holds elements outside it
+  virtual void set_inexact() {}
   // r-th smallest (1-based) of half `side` of the last compacting pass, or of the current array (2)
   virtual cpsel_status select(int side, uint64_t r, double* out) = 0;
   virtual std::string message() const = 0;
@@ -248,6 +259,7 @@ struct GpuBackend : Backend {
   bool init_seg_done = false;  // the init pass wrote ]t_lo, t_hi[ into segmented buffer 0
   uint64_t init_n_in = 0;
   unsigned long long mail_seq = 0;
+  bool cur_exact = true;     // a compacted current array holds exactly the bracket interior
   GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
       : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
@@ -438,8 +450,9 @@ struct GpuBackend : Backend {
         a.seq = mail_seq = ++ctx->seq;
       }
       CK(tic());
-      // a compacted current array holds only bracket-interior elements
-      CK(launch_seg_pass(dt, a, /*inside=*/cur != x, ctx->shape, ctx->stream));
+      // a compacted current array holds only bracket-interior elements (unless a cut pass moved
+      // the bracket without compacting, R26)
+      CK(launch_seg_pass(dt, a, /*inside=*/cur != x && cur_exact, ctx->shape, ctx->stream));
       CK(toc());
       last_dense = dense;
     }
@@ -463,7 +476,49 @@ struct GpuBackend : Backend {
   bool kept_dense() const override { return last_dense; }
   bool init_compacted() const override { return init_seg_done; }
   uint64_t init_written() const override { return init_n_in; }
+  void set_inexact() override { cur_exact = false; }
+  bool has_cut_pass() const override { return use_mail && R > 0; }
+  cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
+    if (cur_seg) CK(launch_sample_seg(dt, cur, cur_tab, cur_side, seg_total_warps(dt, ctx->shape), n_cur, r, ctx->d_t0,
+                                      ctx->stream));
+    else CK(launch_sample_cut(dt, cur, n_cur, r, ctx->d_t0, ctx->stream));
+    SegArgs a{};
+    a.x = cur; a.n = n_cur;
+    a.seg_in = cur_seg ? cur_tab : nullptr;
+    a.side_in = cur_side;
+    a.cuts = ctx->d_t0;
+    a.dense_out = dense ? 1 : 0;
+    if (dense) {
+      tgt = (cur_dbuf == 0) ? 1 : 0;
+      a.out = ctx->d_zb[tgt];
+      a.z_cap = cap;
+    } else {
+      tgt = (cur_sbuf == 0) ? 1 : 0;
+      a.out = ctx->d_sb[tgt];
+      a.R = R;
+      a.seg_out = static_cast<SegEntry*>(ctx->d_st[tgt]);
+    }
+    a.cursors = ctx->d_cursors;
+    a.partials = ctx->d_partials; a.ticket = ctx->d_ticket;
+    a.out_tuple = &ctx->mb_dev->pass;
+    a.done = &ctx->mb_dev->seq_pass;
+    a.seq = mail_seq = ++ctx->seq;
+    CK(tic());
+    CK(launch_cut_pass(dt, a, ctx->shape, ctx->stream));
+    CK(toc());
+    launches = 2;
+    scanned = n_cur;
+    cpsel_status st = wait_mail(&ctx->mb->seq_pass, mail_seq);
+    if (st != CPSEL_OK) return st;
+    const DevPass rr = ctx->mb->pass;
+    o->ta = rr.pred; o->tb = rr.succ; o->I = rr.L_lo;
+    o->le_a = rr.c_lt; o->inner = rr.z_lo;
+    last_dense = dense;
+    zlo = rr.z_lo; zhi = 0;
+    return CPSEL_OK;
+  }
   cpsel_status adopt_init() override {
+    cur_exact = true;
     cur_seg = true;
     cur = ctx->d_sb[0];
     cur_tab = static_cast<const SegEntry*>(ctx->d_st[0]);
@@ -473,6 +528,7 @@ struct GpuBackend : Backend {
     return CPSEL_OK;
   }
   cpsel_status adopt(int side) override {
+    cur_exact = true;
     if (last_dense) {
       cur_seg = false;
       cur = half_ptr(side);
@@ -680,6 +736,13 @@ struct HostBackend : Backend {
     if (be->select(be->user, side, r, out) != 0) { msg = "select callback failed"; return CPSEL_EINTERNAL; }
     return CPSEL_OK;
   }
+  bool has_cut_pass() const override { return be->cut != nullptr; }
+  cpsel_status cut_pass(uint64_t r, bool, CutResult* o) override {
+    cpsel_cut_stats c{};
+    if (be->cut(be->user, r, &c) != 0) { msg = "cut callback failed"; return CPSEL_EINTERNAL; }
+    o->ta = c.t_a; o->tb = c.t_b; o->I = c.I; o->le_a = c.le_a; o->inner = c.inner;
+    return CPSEL_OK;
+  }
 };
 
 uint64_t dense_threshold(uint64_t select_cap) { return std::max<uint64_t>(4 * select_cap, 1ull << 20); }
@@ -765,6 +828,11 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   int slow = 0;
   bool bisect = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
+  const bool f32 = dt == kF32;
+  auto next_up = [&](double v) { return f32 ? (double)std::nextafterf((float)v, INFINITY) : std::nextafter(v, INFINITY); };
+  auto next_dn = [&](double v) { return f32 ? (double)std::nextafterf((float)v, -INFINITY) : std::nextafter(v, -INFINITY); };
+  constexpr uint64_t kUnknown = ~0ull;
+  bool exact = true;  // the current (compacted) array holds exactly the bracket interior
   // R23: the init pass's two extra cuts t_lo <= t_hi (sample quantiles bracketing rank k) — two more
   // cuts of the cutting-plane model, evaluated in the same read of x as the init reduction.  N and P
   // at both cuts follow from the pass's sums: N(t_lo) = N_lo, P(t_hi) = P_hi,
@@ -790,10 +858,6 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     // target lies between the cuts (the usual case).  A cut on the far side of the target moves to
     // the adjacent float, where the missing count is the known one: #x<next(t_lo) = #x<=t_lo,
     // #x<=prev(t_hi) = #x<t_hi (no element lies strictly between a float and its neighbour).
-    const bool f32 = dt == kF32;
-    auto next_up = [&](double v) { return f32 ? (double)std::nextafterf((float)v, INFINITY) : std::nextafter(v, INFINITY); };
-    auto next_dn = [&](double v) { return f32 ? (double)std::nextafterf((float)v, -INFINITY) : std::nextafter(v, -INFINITY); };
-    constexpr uint64_t kUnknown = ~0ull;
     if (rec.t_lo > rec.vmin && rec.t_lo < rec.vmax) {
       const uint64_t c_le = rec.c_le_lo;
       cpsel_trace_row row = row_of(rec.t_lo, kUnknown, kUnknown, N_tl, P_tl);
@@ -850,6 +914,65 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     if (it > cfg.max_iters) {
       if (info) *info = inf;
       return CPSEL_EINTERNAL;
+    }
+    // R26 (multi-point step): a compacted current array that is exactly the bracket
+    // interior and too large for the exact selection is cut at two sample quantiles of its own
+    // around the local target rank; the copy keeps only ]t_a, t_b[ (~10% of the array) instead of
+    // both halves of a Kelley split.  Not with objective=1 (F at the sample cuts would need two
+    // more sums per element).
+    if (cfg.pass_cuts && !cfg.objective && on_z && exact && !bisect && m > select_cap && be.has_cut_pass()) {
+      Backend::CutResult cr{};
+      st = be.cut_pass(k - c_le_L, m <= dense_cap, &cr);
+      if (st != CPSEL_OK) return st;
+      inf.launches += be.launches;
+      inf.passes++;
+      inf.cp_iters++;
+      inf.bytes_moved += be.scanned * es + cr.inner * es;
+      pass_slots.emplace_back(be.slot, (trace && cfg.record_trace) ? (long)trace->size() : -1L);
+      const uint64_t le_a = c_le_L + cr.le_a, lt_b = le_a + cr.inner;
+      cpsel_trace_row row{};
+      row.t = cr.ta;
+      row.F = NAN;
+      row.c_lt = kUnknown; row.c_eq = kUnknown;  // #x<=t_a = le_a and #x<t_b = lt_b, see below
+      row.kind = 3;
+      row.compacted = 1;
+      row.scanned = be.scanned;
+      row.written = cr.inner;
+      N_L = P_R = NAN;  // F is not tracked through sample cuts
+      if (le_a < k && k <= lt_b && cr.ta < cr.tb) {  // the usual case: continue on the copy of ]t_a, t_b[
+        yL = cr.ta; yR = cr.tb; c_le_L = le_a; c_lt_R = lt_b; m = cr.inner;
+        row.interior = m;
+        if (trace && cfg.record_trace) trace->push_back(row);
+        st = be.adopt(0);
+        if (st != CPSEL_OK) return st;
+        D_lo = c_le_L;
+        exact = true;
+        if (m <= select_cap && be.kept_dense()) {
+          double v;
+          st = do_select(0, k - c_le_L, &v);
+          if (st != CPSEL_OK) return st;
+          return done(v, 5);
+        }
+        t = cr.ta + cr.I / (double)m;  // interior mean (App. A)
+        slow = 0;
+        continue;
+      }
+      // the target is outside the sample cuts: the bracket moves to the adjacent float of the cut
+      // (R24); the current array is kept and now holds elements outside the bracket.  (With
+      // t_a == t_b — duplicates in the sample — #x<t_b is not le_a + inner: one cut at t_a.)
+      if (k <= le_a) {
+        yR = next_up(cr.ta); c_lt_R = le_a; m = le_a - c_le_L;
+      } else if (cr.ta == cr.tb) {
+        yL = cr.ta; c_le_L = le_a; m = c_lt_R - le_a;
+      } else {
+        yL = next_dn(cr.tb); c_le_L = lt_b; m = c_lt_R - lt_b;
+      }
+      row.interior = m;
+      if (trace && cfg.record_trace) trace->push_back(row);
+      exact = false;
+      be.set_inexact();
+      t = 0.5 * yL + 0.5 * yR;
+      continue;
     }
     uint32_t kind = 0;
     if (bisect) {
@@ -940,6 +1063,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       if (st != CPSEL_OK) return st;
       D_lo = c_le_L;
       on_z = true;
+      exact = true;
     }
     // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
     // ordered-key bisection until progress resumes (bounds the pass count on any input)
@@ -1025,6 +1149,7 @@ void cpsel_config_default(cpsel_config* c) {
   c->record_trace = 1;
   c->record_timing = 0;
   c->init_cut = 1;
+  c->pass_cuts = 1;
 }
 
 cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {

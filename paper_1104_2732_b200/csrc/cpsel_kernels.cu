@@ -436,17 +436,15 @@ __global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
 // R23: the extra cut of the init pass — the sample quantile at the target rank among 1024 evenly
 // strided samples: one CTA of 1024 threads, one key per thread, bitonic sort with warp shuffles
 // for strides < 32 and shared memory above.
+// Sort the block's 1024 sample keys (one per thread, padding = ~0 sorts last) and write the two
+// cuts bracketing local rank r of an m-element array, from ms real samples: ranks q -/+ 3.5
+// binomial standard deviations (+2) of the sample.  The target lies between the two cuts with
+// overwhelming probability on any input order (the cuts are exact either way).
 template <typename T>
-__global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ x, uint64_t n, uint64_t k, T* t0) {
+__device__ __forceinline__ void sample_sort_pick(unsigned long long v, unsigned long long* key, uint64_t ms,
+                                                 uint64_t m, uint64_t r, T* t0) {
   constexpr int S = 1024;
-  __shared__ unsigned long long key[S];
   const int i = threadIdx.x;
-  const uint64_t m = n < (uint64_t)S ? n : (uint64_t)S;
-  unsigned long long v = ~0ull;  // padding sorts last
-  if ((uint64_t)i < m) {
-    const uint64_t pos = (n == m) ? (uint64_t)i : ((uint64_t)i * n) / m + (n / m) / 2;
-    v = okey(x[pos]);
-  }
   for (int size = 2; size <= S; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       unsigned long long w;
@@ -466,17 +464,76 @@ __global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ 
   key[i] = v;
   __syncthreads();
   if (i == 0) {
-    // ranks q -/+ 3.5 binomial standard deviations (+2): the target lies between the two cuts with
-    // overwhelming probability on any input order (the cuts are exact either way)
-    const double md = (double)m;
-    const double q = ((double)k - 0.5) / (double)n * md;
+    const double md = (double)ms;
+    const double q = ((double)r - 0.5) / (double)m * md;
     const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
     const double ql = floor(q - w), qh = ceil(q + w);
     const uint64_t il = ql < 0 ? 0 : (uint64_t)ql;
-    const uint64_t ih = qh >= md ? m - 1 : (uint64_t)qh;
+    const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
     t0[0] = (T)(sizeof(T) == 4 ? from_key_f32(key[il]) : from_key_f64(key[il]));
     t0[1] = (T)(sizeof(T) == 4 ? from_key_f32(key[ih]) : from_key_f64(key[ih]));
   }
+}
+
+// R23: the two extra cuts of the init pass — 1024 evenly strided samples of x[0..n), cuts around
+// rank k.  (Also used for a contiguous current array with its local rank, R26.)
+template <typename T>
+__global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ x, uint64_t n, uint64_t k, T* t0) {
+  constexpr int S = 1024;
+  __shared__ unsigned long long key[S];
+  const int i = threadIdx.x;
+  const uint64_t m = n < (uint64_t)S ? n : (uint64_t)S;
+  unsigned long long v = ~0ull;  // padding sorts last
+  if ((uint64_t)i < m) {
+    const uint64_t pos = (n == m) ? (uint64_t)i : ((uint64_t)i * n) / m + (n / m) / 2;
+    v = okey(x[pos]);
+  }
+  sample_sort_pick<T>(v, key, m, n, k, t0);
+}
+
+// R26: the same for a segmented current array (the runs `side` of the Wtot warp entries, m
+// elements in total): sample i is element floor(i*m/1024) + (m/1024)/2 of the concatenated runs.
+template <typename T>
+__global__ void __launch_bounds__(1024) sample_seg_kernel(const T* __restrict__ base, const SegEntry* __restrict__ tab,
+                                                          int side, int Wtot, uint64_t m, uint64_t r, T* t0) {
+  constexpr int S = 1024;
+  __shared__ unsigned long long key[S];
+  __shared__ unsigned long long cstart[S];
+  const int i = threadIdx.x;
+  const int per = (Wtot + S - 1) / S;  // runs per chunk
+  const int w0 = i * per, w1 = min(w0 + per, Wtot);
+  unsigned long long c = 0;
+  for (int w = w0; w < w1; ++w) c += tab[w].cnt[side];
+  // inclusive block scan of the chunk totals
+  cstart[i] = c;
+  __syncthreads();
+  for (int off = 1; off < S; off <<= 1) {
+    const unsigned long long add = i >= off ? cstart[i - off] : 0ull;
+    __syncthreads();
+    cstart[i] += add;
+    __syncthreads();
+  }
+  const uint64_t ms = m < (uint64_t)S ? m : (uint64_t)S;
+  unsigned long long v = ~0ull;
+  if ((uint64_t)i < ms) {
+    uint64_t g = (m == ms) ? (uint64_t)i : ((uint64_t)i * m) / ms + (m / ms) / 2;
+    // first chunk whose inclusive total exceeds g
+    int lo = 0, hi = S - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (cstart[mid] > g) hi = mid; else lo = mid + 1;
+    }
+    g -= lo ? cstart[lo - 1] : 0ull;
+    for (int w = lo * per; w < min(lo * per + per, Wtot); ++w) {
+      const SegEntry e = tab[w];
+      if (g < e.cnt[side]) {
+        v = okey(base[e.off[side] + g]);
+        break;
+      }
+      g -= e.cnt[side];
+    }
+  }
+  sample_sort_pick<T>(v, key, ms, m, r, t0);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1150,6 +1207,164 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
       a.cursors[0] = 0ull;
       a.cursors[1] = 0ull;
     }
+    *a.out_tuple = r;
+    publish_done(a.done, a.seq);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// R26: the cut pass — two sample cuts t_a <= t_b of the current (compacted) array evaluated in one
+// read, with the copy_if of ]t_a, t_b[ (multi-point Kelley).  Every input element
+// lies inside the bracket, so the element step is the init pass's cut step without the extremes:
+// 6 issue slots (#x<=t_a, the interior bit and the interior sum).
+template <typename T> struct WarpCut {
+  static constexpr int VE = VecOf<T>::N;
+  static constexpr int G = kSegU * VE;
+  static constexpr int GW = 32 * G;
+  T ta, tb;
+  T vals[G];
+  unsigned bits;
+  float fL = 0.f;                  // #x<=t_a (exact per-thread float counter)
+  T gI[kSegU];
+  double I0 = 0.0;
+  unsigned long long n_in = 0;     // warp-uniform: elements written
+  T* stage;
+  int dense;
+  T* out;
+  uint64_t reg_lo;
+  unsigned long long* cursors;
+  __device__ __forceinline__ void elem(float v, int u, int idx) {
+    asm("{\n\t.reg .pred pL, pI;\n\t.reg .f32 dl;\n\t"
+        "setp.le.f32 pL, %3, %4;\n\t"
+        "setp.lt.and.f32 pI, %3, %5, !pL;\n\t"
+        "sub.rn.f32 dl, %3, %4;\n\t"
+        "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+        "@pI add.rn.f32 %1, %1, dl;\n\t"
+        "@pI or.b32 %2, %2, %6;\n\t}"
+        : "+f"(fL), "+f"(gI[u]), "+r"(bits)
+        : "f"(v), "f"(ta), "f"(tb), "r"(1u << idx));
+    vals[idx] = v;
+  }
+  __device__ __forceinline__ void elem(double v, int u, int idx) {
+    asm("{\n\t.reg .pred pL, pI;\n\t.reg .f64 dl;\n\t"
+        "setp.le.f64 pL, %3, %4;\n\t"
+        "setp.lt.and.f64 pI, %3, %5, !pL;\n\t"
+        "sub.rn.f64 dl, %3, %4;\n\t"
+        "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
+        "@pI add.rn.f64 %1, %1, dl;\n\t"
+        "@pI or.b32 %2, %2, %6;\n\t}"
+        : "+f"(fL), "+d"(gI[u]), "+r"(bits)
+        : "d"(v), "d"(ta), "d"(tb), "r"(1u << idx));
+    vals[idx] = v;
+  }
+  __device__ __forceinline__ void begin() {
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) gI[u] = T(0);
+    bits = 0u;
+  }
+  __device__ __forceinline__ void end() {
+    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
+    const int lane = threadIdx.x & 31;
+    const unsigned cnt = (unsigned)__popc(bits);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const unsigned tot = __shfl_sync(FULL, incl, 31);
+    if (tot == 0u) return;
+    T* sp = stage + (incl - cnt);
+#pragma unroll
+    for (int j = 0; j < G; ++j)
+      if (bits & (1u << j)) *sp++ = vals[j];
+    __syncwarp();
+    T* dst;
+    if (dense) {
+      unsigned long long b = 0;
+      if (lane == 0) b = atomicAdd(&cursors[0], (unsigned long long)tot);
+      dst = out + __shfl_sync(FULL, b, 0);
+    } else {
+      dst = out + reg_lo + n_in;
+    }
+    for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    n_in += tot;
+    __syncwarp();
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
+  using F = WarpCut<T>;
+  __shared__ __align__(16) T stage_all[kWarps * F::GW];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
+  const uint64_t Wtot = (uint64_t)gridDim.x * kWarps;
+  F f;
+  f.ta = static_cast<const T*>(a.cuts)[0];
+  f.tb = static_cast<const T*>(a.cuts)[1];
+  f.stage = stage_all + (size_t)w * F::GW;
+  f.dense = a.dense_out;
+  f.out = static_cast<T*>(a.out);
+  f.reg_lo = W * a.R;
+  f.cursors = a.cursors;
+  if (a.seg_in == nullptr) {
+    using V = typename VecOf<T>::V;
+    constexpr int VE = VecOf<T>::N;
+    const T* x = static_cast<const T*>(a.x);
+    const uint64_t n = a.n;
+    const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
+    uint64_t head = mis ? (VE - mis) : 0;
+    if (head > n) head = n;
+    const V* xv = reinterpret_cast<const V*>(x + head);
+    const uint64_t nvec = (n - head) / VE;
+    constexpr uint64_t GV = 32 * kSegU;
+    const uint64_t nfull = nvec / GV;
+    for (uint64_t g = W; g < nfull; g += Wtot) seg_group<T, false>(f, xv, g * GV, nvec);
+    if (nfull * GV < nvec && W == nfull % Wtot) seg_group<T, true>(f, xv, nfull * GV, nvec);
+    if (W == Wtot - 1) {
+      const uint64_t tail0 = head + nvec * VE, ntail = n - tail0;
+      const bool okh = (uint64_t)lane < head;
+      const bool okt = (uint64_t)lane >= head && (uint64_t)lane < head + ntail;
+      T v = T(0);
+      if (okh) v = x[lane];
+      if (okt) v = x[tail0 + (lane - head)];
+      if (head + ntail) seg_scalars<T>(f, v, okh || okt);
+    }
+  } else {
+    const SegEntry e = a.seg_in[W];
+    const T* base = static_cast<const T*>(a.x);
+    seg_run<T>(f, base + e.off[a.side_in], e.cnt[a.side_in]);
+  }
+  if (!a.dense_out && lane == 0) {
+    SegEntry o;
+    o.off[0] = f.reg_lo;
+    o.cnt[0] = f.n_in;
+    o.off[1] = f.reg_lo + a.R;
+    o.cnt[1] = 0;
+    a.seg_out[W] = o;
+  }
+  PassPartial p;
+  p.c_lt = (unsigned long long)f.fL;
+  p.c_eq = 0;
+  p.c_lo = lane == 0 ? f.n_in : 0;  // warp totals, counted once per warp
+  p.c_hi = 0;
+  p.L_lo = f.I0; p.L_hi = 0; p.P = 0; p.N = 0;
+  p.pred = -tinf<double>(); p.succ = tinf<double>();
+  p = block_reduce(p);
+  PassPartial id;
+  id.c_lt = id.c_eq = id.c_lo = id.c_hi = 0;
+  id.L_lo = id.L_hi = id.P = id.N = 0;
+  id.pred = -tinf<double>(); id.succ = tinf<double>();
+  PassPartial tot;
+  if (grid_finish(p, static_cast<PassPartial*>(a.partials), a.ticket, &tot, id) && threadIdx.x == 0) {
+    DevPass r;
+    r.c_lt = tot.c_lt; r.c_eq = 0;
+    r.c_lo = tot.c_lo; r.c_hi = 0;
+    r.L_lo = tot.L_lo; r.L_hi = 0; r.P = 0; r.N = 0;
+    r.pred = (double)f.ta; r.succ = (double)f.tb;
+    r.z_lo = tot.c_lo; r.z_hi = 0;
+    if (a.dense_out) a.cursors[0] = 0ull;
     *a.out_tuple = r;
     publish_done(a.done, a.seq);
   }
@@ -1880,6 +2095,25 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
     if (inside) seg_pass_kernel<double, true><<<g, kBlock, 0, st>>>(a);
     else seg_pass_kernel<double, false><<<g, kBlock, 0, st>>>(a);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
+                              uint64_t r, void* t0, cudaStream_t st) {
+  if (dtype == kF32)
+    sample_seg_kernel<float><<<1, 1024, 0, st>>>(static_cast<const float*>(base), tab, side, Wtot, m, r,
+                                                 static_cast<float*>(t0));
+  else
+    sample_seg_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(base), tab, side, Wtot, m, r,
+                                                  static_cast<double*>(t0));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st) {
+  // the segmented grid: its warp regions / run tables are what later passes read
+  const int g = s.grid_seg[dtype];
+  if (dtype == kF32) cut_pass_kernel<float><<<g, kBlock, 0, st>>>(a);
+  else cut_pass_kernel<double><<<g, kBlock, 0, st>>>(a);
   return cudaGetLastError();
 }
 

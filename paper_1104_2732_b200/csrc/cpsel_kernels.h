@@ -96,6 +96,7 @@ struct SegArgs {
   DevPass* out_tuple;
   unsigned long long* done;    // optional mailbox flag (see PassArgs)
   unsigned long long seq;
+  const void* cuts;            // cut pass (R26): device pointer to the two cuts t_a <= t_b
 };
 
 struct InitArgs {
@@ -135,6 +136,17 @@ cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, con
                             bool sums);
 // inside: every input element lies strictly inside the bracket (input = a kept half)
 cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const LaunchShape& s, cudaStream_t st);
+// R26: sample cuts of a compacted current array and the cut pass over it.
+// launch_sample_seg: t0[0..1] <- the two sample cuts around local rank r of the m-element
+// segmented array (runs `side` of tab[0..Wtot)).
+cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
+                              uint64_t r, void* t0, cudaStream_t st);
+// launch_cut_pass: one read of the current array (a.x / a.seg_in / a.side_in as for
+// launch_seg_pass, every element inside the bracket) at the two cuts a.cuts = {t_a, t_b}:
+// #x<=t_a, the copy_if of ]t_a, t_b[ (segmented run 0 of each warp region, or dense from z[0]) and
+// I = sum over it of (x - t_a).  Result tuple: c_lt = #x<=t_a, c_lo = z_lo = #]t_a,t_b[, L_lo = I,
+// pred = t_a, succ = t_b.
+cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st);
 
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
 // t0[0], t0[1] <- the sample quantiles bracketing rank k (1024 strided samples of x, one CTA)

@@ -9,8 +9,9 @@ import numpy as np
 
 
 class NumpyShard:
-    def __init__(self, x, comm=None, cut_k=None):
+    def __init__(self, x, comm=None, cut_k=None, cut_shift=0.0):
         self.x = np.ascontiguousarray(x)
+        self.cut_shift = cut_shift  # R26 cut pass: move the sample cuts by this fraction of the sample
         self.cut_k = cut_k  # evaluate the init pass's extra cut at a sample quantile of rank cut_k
         self.comm = comm  # callable: obj -> list of objs from every rank (rank order)
         self.kept = None
@@ -92,14 +93,35 @@ class NumpyShard:
     def adopt(self, side):
         self.cur = self.kept[side]
 
+    def cut(self, r):
+        """R26 cut pass over the current array (exactly the bracket interior): 1024 evenly strided
+        samples, cuts at sample ranks q -/+ (3.5 sd + 2) around local rank r (or, with
+        cut_shift, deliberately off target to drive the far-side branches), #x<=t_a, the copy of
+        ]t_a, t_b[ and its sum of (x - t_a)."""
+        x = self.cur
+        m = x.size
+        ms = min(m, 1024)
+        pos = np.arange(ms) if m == ms else (np.arange(ms, dtype=np.int64) * m) // ms + (m // ms) // 2
+        smp = np.sort(x[pos])
+        q = (r - 0.5) / m * ms + self.cut_shift * ms
+        w = 3.5 * math.sqrt(max(q * (ms - q) / ms, 0.0)) + 2.0
+        il = min(max(int(math.floor(q - w)), 0), ms - 1)
+        ih = min(max(int(math.ceil(q + w)), il), ms - 1)
+        ta, tb = smp[il], smp[ih]
+        inner = (x > ta) & (x < tb)
+        self.kept = (x[inner].copy(), None)
+        return {"t_a": float(ta), "t_b": float(tb), "le_a": int((x <= ta).sum()), "inner": int(inner.sum()),
+                "I": float(np.sum(x[inner].astype(np.float64) - np.float64(ta)))}
+
     def select(self, side, r):
         part = self.cur if side == 2 else self.kept[side]
         allz = np.concatenate(self._gather(part))
         return float(np.partition(allz, r - 1)[r - 1])
 
 
-def drive(x, k, dtype, comm=None, config=None, cut=False):
+def drive(x, k, dtype, comm=None, config=None, cut=False, pass_cuts=False, cut_shift=0.0):
     import paper_1104_2732_b200 as cp
-    be = NumpyShard(x, comm, cut_k=k if cut else None)
+    be = NumpyShard(x, comm, cut_k=k if cut else None, cut_shift=cut_shift)
     n = x.size if comm is None else sum(comm(x.size))
-    return cp.drive_host(n, k, dtype, be.init, be.pass_, be.adopt, be.select, config)
+    return cp.drive_host(n, k, dtype, be.init, be.pass_, be.adopt, be.select, config,
+                         cut_fn=be.cut if (pass_cuts and comm is None) else None)

@@ -294,6 +294,29 @@ def test_fused_init_trace(cp, objective):
             assert math.isnan(row["F"])
 
 
+@pytest.mark.parametrize("order", ["random", "sorted", "reversed"])
+def test_pass_cuts_all_dists(cp, order):
+    """R26 cut passes on the GPU (segmented sample kernel + cut pass): exact on every distribution,
+    rank and input order (sorted input makes the warp runs value-ordered), and the cut passes do
+    run at this size."""
+    n = (1 << 23) + 77
+    saw_cut = False
+    for dist in datagen.ALL_DISTS:
+        x = datagen.make(dist, n, "f32")
+        if order == "sorted":
+            x = np.sort(x)
+        elif order == "reversed":
+            x = np.sort(x)[::-1].copy()
+        xd = tdev(x)
+        srt = np.sort(x)
+        for k in (3, n // 7, O.median_rank(n), n - n // 5, n - 2):
+            v = cp.select_kth(xd, k)
+            assert v == srt[k - 1], (dist, order, k)
+            saw_cut |= any(r["kind"] == 3 for r in cp.get_trace())
+        del xd
+    assert saw_cut
+
+
 def test_host_buffer_path(cp):
     import torch
     x = datagen.make("normal", 3_000_001, "f32")

@@ -36,6 +36,29 @@ def test_driver_matches_oracle_distributions(dtype):
                     assert info["passes"] == info["cp_iters"] + 1          # maxit+1 reductions
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("cut_shift", [0.0, 0.3, -0.3])
+def test_driver_pass_cuts(dtype, cut_shift):
+    """R26 cut passes (two sample cuts of the compacted bracket, copy of what lies between them):
+    exact on every distribution and rank, also when the cuts are deliberately off target
+    (cut_shift moves them by 30% of the sample: the far-side branches move the bracket to the
+    adjacent float and continue on the uncompacted array)."""
+    for dist in datagen.ALL_DISTS:
+        x = datagen.make(dist, 20_011, dtype)
+        n = x.size
+        for k in sorted({1, 2, n // 10, O.median_rank(n), n - 1, n}):
+            for cfg in ({"force_cp": 1, "z_cap": 15_000, "select_cap": 16},
+                        {"force_cp": 1, "z_cap": 20_011, "select_cap": 300}):
+                v, info, trace = drive(x, k, dtype, config=cfg, cut=True, pass_cuts=True, cut_shift=cut_shift)
+                assert canon(v) == float(O.order_statistic(x, k)), (dist, k, cfg, info)
+                assert info["passes"] == info["cp_iters"] + 1
+    # the cut passes do run (uniform data, median)
+    x = datagen.make("uniform", 20_011, dtype)
+    _, _, trace = drive(x, O.median_rank(x.size), dtype, config={"force_cp": 1, "select_cap": 16},
+                        cut=True, pass_cuts=True)
+    assert any(r["kind"] == 3 for r in trace)
+
+
 def test_driver_tiny_all_ranks_with_ties_and_signed_zero():
     rng = np.random.default_rng(5)
     for _ in range(300):
