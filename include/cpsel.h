@@ -111,10 +111,11 @@ typedef struct {
   uint64_t c_le_lo, c_lt_hi; /* #{x<=t_lo}, #{x<t_hi}: the counts a bracket update needs at each cut
                              when the target lies between them; a cut beyond the target moves to the
                              adjacent float, where the missing count is the known one (R24) */
-  uint64_t reserved_cut[2];
+  double t_est;           /*   the sample's estimate of x_(k) (starting iterate when I_in is not kept) */
+  uint64_t reserved_cut;
   double N_lo;            /*   sum (t_lo - x)^+ */
   double P_hi;            /*   sum (x - t_hi)^+ */
-  double I_in;            /*   sum over t_lo < x < t_hi of (x - t_lo) */
+  double I_in;            /*   sum over t_lo < x < t_hi of (x - t_lo)  (with N_lo, P_hi: bit 2 of has_cut) */
 } cpsel_init_stats;
 
 /* One row per cutting-plane pass (R7 trace). */
@@ -212,7 +213,7 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
  * logic the GPU path runs.  Each callback returns 0 on success. */
 typedef struct {
   double t_a, t_b;        /* the two cuts */
-  double I;               /* sum over t_a < x < t_b of (x - t_a) */
+  double t_est;           /* the sample's estimate of x_(k) (the next starting iterate) */
   uint64_t le_a, inner;   /* #{x <= t_a}, #{t_a < x < t_b} (local to the current array) */
 } cpsel_cut_stats;
 typedef struct {
@@ -231,8 +232,8 @@ typedef struct {
   int (*select)(void* user, int side, uint64_t r, double* value_out);
   /* optional (NULL: none): the R26 cut pass over the current array, which is exactly the bracket
      interior — two sample cuts t_a <= t_b (elements of it) around its local rank r; fill *out with
-     #{x <= t_a}, #{t_a < x < t_b}, sum over the latter of (x - t_a), and retain that set as
-     half 0 of a compacting pass. */
+     them, the sample's estimate of the target, #{x <= t_a} and #{t_a < x < t_b}, and retain the
+     latter set as half 0 of a compacting pass. */
   int (*cut)(void* user, uint64_t r, cpsel_cut_stats* out);
 } cpsel_host_backend;
 cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dtype dtype,

@@ -67,7 +67,7 @@ class InitStats(C.Structure):
     _fields_ = [("vmin", C.c_double), ("vmax", C.c_double), ("cnt_min", C.c_uint64), ("cnt_max", C.c_uint64),
                 ("nonfinite", C.c_uint64), ("x0", C.c_double), ("S", C.c_double), ("has_cut", C.c_uint64),
                 ("t_lo", C.c_double), ("t_hi", C.c_double), ("c_le_lo", C.c_uint64), ("c_lt_hi", C.c_uint64),
-                ("reserved_cut0", C.c_uint64), ("reserved_cut1", C.c_uint64), ("N_lo", C.c_double), ("P_hi", C.c_double),
+                ("t_est", C.c_double), ("reserved_cut", C.c_uint64), ("N_lo", C.c_double), ("P_hi", C.c_double),
                 ("I_in", C.c_double)]
 
     def as_dict(self):
@@ -91,7 +91,7 @@ _ADOPT_CB = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int)
 
 
 class CutStats(C.Structure):
-    _fields_ = [("t_a", C.c_double), ("t_b", C.c_double), ("I", C.c_double), ("le_a", C.c_uint64),
+    _fields_ = [("t_a", C.c_double), ("t_b", C.c_double), ("t_est", C.c_double), ("le_a", C.c_uint64),
                 ("inner", C.c_uint64)]
 
 

@@ -215,7 +215,7 @@ struct Backend {
   // cuts t_a <= t_b around local rank r, #x<=t_a, the copy_if of ]t_a, t_b[ (dense if asked) and
   // its sum of (x - t_a).  adopt(0) then makes the copy the current array.
   struct CutResult {
-    double ta, tb, I;
+    double ta, tb, t_est;  // the cuts and the sample's estimate of x_(k)
     uint64_t le_a, inner;  // local #x<=t_a, #]t_a,t_b[
   };
   virtual bool has_cut_pass() const { return false; }
@@ -357,6 +357,7 @@ struct GpuBackend : Backend {
     // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
     // cuts (which skip the shifted sum), as #x<t_hi + #x=t_hi + #x>t_hi < n
     const bool suspicious = cut ? (!std::isfinite(r.N_lo) || !std::isfinite(r.P_hi) || !std::isfinite(r.I_in) ||
+                                   !std::isfinite(r.t_est) ||
                                    !std::isfinite(r.vmin) || !std::isfinite(r.vmax) || r.nonfinite != 0)
                                 : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
     if (!suspicious && fuse) {
@@ -385,7 +386,7 @@ struct GpuBackend : Backend {
     o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
     o->nonfinite = r.nonfinite; o->x0 = r.x0; o->S = r.S;
     o->has_cut = r.has_cut; o->t_lo = r.t_lo; o->t_hi = r.t_hi;
-    o->c_le_lo = r.c_le_lo; o->c_lt_hi = r.c_lt_hi;
+    o->c_le_lo = r.c_le_lo; o->c_lt_hi = r.c_lt_hi; o->t_est = r.t_est;
     o->N_lo = r.N_lo; o->P_hi = r.P_hi; o->I_in = r.I_in;
     return CPSEL_OK;
   }
@@ -511,7 +512,7 @@ struct GpuBackend : Backend {
     cpsel_status st = wait_mail(&ctx->mb->seq_pass, mail_seq);
     if (st != CPSEL_OK) return st;
     const DevPass rr = ctx->mb->pass;
-    o->ta = rr.pred; o->tb = rr.succ; o->I = rr.L_lo;
+    o->ta = rr.pred; o->tb = rr.succ; o->t_est = rr.L_lo;
     o->le_a = rr.c_lt; o->inner = rr.z_lo;
     last_dense = dense;
     zlo = rr.z_lo; zhi = 0;
@@ -740,7 +741,7 @@ struct HostBackend : Backend {
   cpsel_status cut_pass(uint64_t r, bool, CutResult* o) override {
     cpsel_cut_stats c{};
     if (be->cut(be->user, r, &c) != 0) { msg = "cut callback failed"; return CPSEL_EINTERNAL; }
-    o->ta = c.t_a; o->tb = c.t_b; o->I = c.I; o->le_a = c.le_a; o->inner = c.inner;
+    o->ta = c.t_a; o->tb = c.t_b; o->t_est = c.t_est; o->le_a = c.le_a; o->inner = c.inner;
     return CPSEL_OK;
   }
 };
@@ -895,6 +896,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);
     }
+    // without the sums the interior sum I is not kept either: start from the sample's estimate
+    if (!sums) t = (rec.t_est > yL && rec.t_est < yR) ? rec.t_est : (double)NAN;
     if (!std::isfinite(t)) t = 0.5 * yL + 0.5 * yR;
     // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
     if (be.init_compacted() && yL == rec.t_lo && yR == rec.t_hi) {
@@ -953,7 +956,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
           if (st != CPSEL_OK) return st;
           return done(v, 5);
         }
-        t = cr.ta + cr.I / (double)m;  // interior mean (App. A)
+        // next iterate (if any pass still needs one): the sample's estimate of x_(k)
+        t = (cr.t_est > cr.ta && cr.t_est < cr.tb) ? cr.t_est : 0.5 * cr.ta + 0.5 * cr.tb;
         slow = 0;
         continue;
       }
@@ -1184,7 +1188,7 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMemset(ctx->d_cursors, 0, 256));
   CKC(cudaMalloc(&ctx->d_pass, sizeof(DevPass)));
   CKC(cudaMalloc(&ctx->d_init, sizeof(DevInit)));
-  CKC(cudaMalloc(&ctx->d_t0, 16));
+  CKC(cudaMalloc(&ctx->d_t0, 32));  // t_lo, t_hi, the sample estimate
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
   CKC(cudaMalloc(&ctx->d_hist, 2048 * sizeof(unsigned)));
   CKC(cudaMemset(ctx->d_hist, 0, 2048 * sizeof(unsigned)));

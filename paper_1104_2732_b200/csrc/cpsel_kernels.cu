@@ -20,8 +20,10 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cpsel_kernels.h"
+#include "cpsel_ptx.h"
 
 namespace cpsel {
 namespace {
@@ -424,7 +426,8 @@ __global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
     r.t_lo = CUT ? (double)f.tl : 0.0;
     r.t_hi = CUT ? (double)f.th : 0.0;
     r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
-    r.c_le_lo = tot.cA + tot.cB; r.c_lt_hi = tot.cC; r.res0 = r.res1 = r.res2 = 0;
+    r.c_le_lo = tot.cA + tot.cB; r.c_lt_hi = tot.cC; r.res1 = r.res2 = 0;
+    r.t_est = CUT ? (double)static_cast<const T*>(a.t0)[2] : 0.0;
     // a NaN is in none of <t_hi, =t_hi, >t_hi: the fast form reports the shortfall (CHECKED counts all)
     if (CUT && !CHECKED) r.nonfinite = a.n - tot.cC - tot.cD - tot.cE;
     r.has_cut = CUT ? 6ull : 0ull;  // two cuts, with N_lo / P_hi
@@ -472,6 +475,10 @@ __device__ __forceinline__ void sample_sort_pick(unsigned long long v, unsigned 
     const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
     t0[0] = (T)(sizeof(T) == 4 ? from_key_f32(key[il]) : from_key_f64(key[il]));
     t0[1] = (T)(sizeof(T) == 4 ? from_key_f32(key[ih]) : from_key_f64(key[ih]));
+    // the sample's own estimate of the target (a starting iterate where no interior sum is kept)
+    const double qm = floor(q);
+    const uint64_t im = qm < 0 ? 0 : (qm >= md ? ms - 1 : (uint64_t)qm);
+    t0[2] = (T)(sizeof(T) == 4 ? from_key_f32(key[im]) : from_key_f64(key[im]));
   }
 }
 
@@ -1225,8 +1232,6 @@ template <typename T> struct WarpCut {
   T vals[G];
   unsigned bits;
   float fL = 0.f;                  // #x<=t_a (exact per-thread float counter)
-  T gI[kSegU];
-  double I0 = 0.0;
   unsigned long long n_in = 0;     // warp-uniform: elements written
   T* stage;
   int dense;
@@ -1234,36 +1239,29 @@ template <typename T> struct WarpCut {
   uint64_t reg_lo;
   unsigned long long* cursors;
   __device__ __forceinline__ void elem(float v, int u, int idx) {
-    asm("{\n\t.reg .pred pL, pI;\n\t.reg .f32 dl;\n\t"
-        "setp.le.f32 pL, %3, %4;\n\t"
-        "setp.lt.and.f32 pI, %3, %5, !pL;\n\t"
-        "sub.rn.f32 dl, %3, %4;\n\t"
+    asm("{\n\t.reg .pred pL, pI;\n\t"
+        "setp.le.f32 pL, %2, %3;\n\t"
+        "setp.lt.and.f32 pI, %2, %4, !pL;\n\t"
         "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
-        "@pI add.rn.f32 %1, %1, dl;\n\t"
-        "@pI or.b32 %2, %2, %6;\n\t}"
-        : "+f"(fL), "+f"(gI[u]), "+r"(bits)
+        "@pI or.b32 %1, %1, %5;\n\t}"
+        : "+f"(fL), "+r"(bits)
         : "f"(v), "f"(ta), "f"(tb), "r"(1u << idx));
+    (void)u;
     vals[idx] = v;
   }
   __device__ __forceinline__ void elem(double v, int u, int idx) {
-    asm("{\n\t.reg .pred pL, pI;\n\t.reg .f64 dl;\n\t"
-        "setp.le.f64 pL, %3, %4;\n\t"
-        "setp.lt.and.f64 pI, %3, %5, !pL;\n\t"
-        "sub.rn.f64 dl, %3, %4;\n\t"
+    asm("{\n\t.reg .pred pL, pI;\n\t"
+        "setp.le.f64 pL, %2, %3;\n\t"
+        "setp.lt.and.f64 pI, %2, %4, !pL;\n\t"
         "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
-        "@pI add.rn.f64 %1, %1, dl;\n\t"
-        "@pI or.b32 %2, %2, %6;\n\t}"
-        : "+f"(fL), "+d"(gI[u]), "+r"(bits)
+        "@pI or.b32 %1, %1, %5;\n\t}"
+        : "+f"(fL), "+r"(bits)
         : "d"(v), "d"(ta), "d"(tb), "r"(1u << idx));
+    (void)u;
     vals[idx] = v;
   }
-  __device__ __forceinline__ void begin() {
-#pragma unroll
-    for (int u = 0; u < kSegU; ++u) gI[u] = T(0);
-    bits = 0u;
-  }
+  __device__ __forceinline__ void begin() { bits = 0u; }
   __device__ __forceinline__ void end() {
-    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
     const int lane = threadIdx.x & 31;
     const unsigned cnt = (unsigned)__popc(bits);
     unsigned incl = cnt;
@@ -1349,7 +1347,7 @@ __global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
   p.c_eq = 0;
   p.c_lo = lane == 0 ? f.n_in : 0;  // warp totals, counted once per warp
   p.c_hi = 0;
-  p.L_lo = f.I0; p.L_hi = 0; p.P = 0; p.N = 0;
+  p.L_lo = 0; p.L_hi = 0; p.P = 0; p.N = 0;
   p.pred = -tinf<double>(); p.succ = tinf<double>();
   p = block_reduce(p);
   PassPartial id;
@@ -1361,7 +1359,8 @@ __global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
     DevPass r;
     r.c_lt = tot.c_lt; r.c_eq = 0;
     r.c_lo = tot.c_lo; r.c_hi = 0;
-    r.L_lo = tot.L_lo; r.L_hi = 0; r.P = 0; r.N = 0;
+    r.L_lo = (double)static_cast<const T*>(a.cuts)[2];  // the sample's estimate of x_(k)
+    r.L_hi = 0; r.P = 0; r.N = 0;
     r.pred = (double)f.ta; r.succ = (double)f.tb;
     r.z_lo = tot.c_lo; r.z_hi = 0;
     if (a.dense_out) a.cursors[0] = 0ull;
@@ -1391,11 +1390,12 @@ template <typename T, bool SUMS> struct InitSeg {
   unsigned long long n_in = 0;    // warp-uniform: interior elements written
   T* out;
   uint64_t reg_lo;
+  T* stage;                       // this warp's GW-element staging buffer (shared memory)
 
   // one element, SUMS: 3 compares, 2 subs, 1 counter, 3 sums, 1 interior bit (10 issue slots):
   //   fL = #x<=t_lo, N += (t_lo-x) on x<=t_lo, P += (x-t_hi) on x>t_hi, I += (x-t_lo) and the
   //   interior bit on t_lo<x<t_hi.  #x<t_hi = #x<=t_lo + #interior.
-  //   !SUMS: fL, I and the interior bit only (6 slots).
+  //   !SUMS: fL and the interior bit only (4 slots; the next iterate comes from the sample, R25).
   //   (#x==t_lo and #x==t_hi are not needed, R24.)
   __device__ __forceinline__ void cut(float v, int u, int idx) {
     if (SUMS)
@@ -1413,14 +1413,12 @@ template <typename T, bool SUMS> struct InitSeg {
           : "+f"(fL), "+f"(gN[u]), "+f"(gP[u]), "+f"(gI[u]), "+r"(bits)
           : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
     else
-      asm("{\n\t.reg .pred pL, pI;\n\t.reg .f32 dl;\n\t"
-          "setp.le.f32 pL, %3, %4;\n\t"
-          "setp.lt.and.f32 pI, %3, %5, !pL;\n\t"
-          "sub.rn.f32 dl, %3, %4;\n\t"
+      asm("{\n\t.reg .pred pL, pI;\n\t"
+          "setp.le.f32 pL, %2, %3;\n\t"
+          "setp.lt.and.f32 pI, %2, %4, !pL;\n\t"
           "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
-          "@pI add.rn.f32 %1, %1, dl;\n\t"
-          "@pI or.b32 %2, %2, %6;\n\t}"
-          : "+f"(fL), "+f"(gI[u]), "+r"(bits)
+          "@pI or.b32 %1, %1, %5;\n\t}"
+          : "+f"(fL), "+r"(bits)
           : "f"(v), "f"(tl), "f"(th), "r"(1u << idx));
     vals[idx] = v;
   }
@@ -1440,20 +1438,19 @@ template <typename T, bool SUMS> struct InitSeg {
           : "+f"(fL), "+d"(gN[u]), "+d"(gP[u]), "+d"(gI[u]), "+r"(bits)
           : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
     else
-      asm("{\n\t.reg .pred pL, pI;\n\t.reg .f64 dl;\n\t"
-          "setp.le.f64 pL, %3, %4;\n\t"
-          "setp.lt.and.f64 pI, %3, %5, !pL;\n\t"
-          "sub.rn.f64 dl, %3, %4;\n\t"
+      asm("{\n\t.reg .pred pL, pI;\n\t"
+          "setp.le.f64 pL, %2, %3;\n\t"
+          "setp.lt.and.f64 pI, %2, %4, !pL;\n\t"
           "@pL add.rn.f32 %0, %0, 0f3F800000;\n\t"
-          "@pI add.rn.f64 %1, %1, dl;\n\t"
-          "@pI or.b32 %2, %2, %6;\n\t}"
-          : "+f"(fL), "+d"(gI[u]), "+r"(bits)
+          "@pI or.b32 %1, %1, %5;\n\t}"
+          : "+f"(fL), "+r"(bits)
           : "d"(v), "d"(tl), "d"(th), "r"(1u << idx));
     vals[idx] = v;
   }
   __device__ __forceinline__ void begin() {
+    if (SUMS)
 #pragma unroll
-    for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = gI[u] = T(0);
+      for (int u = 0; u < kSegU; ++u) gN[u] = gP[u] = gI[u] = T(0);
     bits = 0u;
   }
   __device__ __forceinline__ void vec(const float4& v, int u) {
@@ -1524,8 +1521,8 @@ template <typename T, bool SUMS> struct InitSeg {
     if (SUMS) {
       N0 += (double)((gN[0] + gN[1]) + (gN[2] + gN[3]));
       P0 += (double)((gP[0] + gP[1]) + (gP[2] + gP[3]));
+      I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
     }
-    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
     const int lane = threadIdx.x & 31;
     const unsigned cnt = (unsigned)__popc(bits);
     unsigned incl = cnt;
@@ -1536,12 +1533,16 @@ template <typename T, bool SUMS> struct InitSeg {
     }
     const unsigned tot = __shfl_sync(FULL, incl, 31);
     if (tot == 0u) return;
-    // predicated stores straight into the warp's region (the order inside a run is free):
-    // lane l writes its interior elements at [excl_l, incl_l) of this group's slice
-    T* dp = out + reg_lo + n_in + (incl - cnt);
+    // predicated shared stores: lane l stages its interior elements at [excl_l, incl_l), then
+    // the warp writes the group's run out coalesced (the order inside a run is free)
+    T* sp = stage + (incl - cnt);
 #pragma unroll
     for (int j = 0; j < G; ++j)
-      if (bits & (1u << j)) *dp++ = vals[j];
+      if (bits & (1u << j)) *sp++ = vals[j];
+    __syncwarp();
+    T* dst = out + reg_lo + n_in;
+    for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    __syncwarp();
     n_in += tot;
   }
 };
@@ -1569,14 +1570,18 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   const uint64_t nvec = (n - head) / VE;
   constexpr uint64_t GV = 32 * kSegU;
   const uint64_t nfull = nvec / GV;
-  for (uint64_t g = W; g < nfull; g += Wtot) {
-    V v[kSegU];
+  {
+    __shared__ __align__(16) T stage_all[kWarps * F::GW];
+    f.stage = stage_all + (size_t)w * F::GW;
+    for (uint64_t g = W; g < nfull; g += Wtot) {
+      V v[kSegU];
 #pragma unroll
-    for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + g * GV + (uint64_t)u * 32 + lane);
-    f.begin();
+      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + g * GV + (uint64_t)u * 32 + lane);
+      f.begin();
 #pragma unroll
-    for (int u = 0; u < kSegU; ++u) f.vec(v[u], u);
-    f.end(F::G);
+      for (int u = 0; u < kSegU; ++u) f.vec(v[u], u);
+      f.end(F::G);
+    }
   }
   if (nfull * GV < nvec && W == nfull % Wtot) {  // the ragged group
     V v[kSegU];
@@ -1639,7 +1644,8 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.N_lo = tot.N0; r.P_hi = tot.P0; r.I_in = tot.I0;
     r.c_le_lo = tot.cA;
     r.c_lt_hi = tot.cA + tot.pad2;  // every x < t_hi is <= t_lo or interior
-    r.res0 = r.res1 = r.res2 = 0;
+    r.t_est = (double)static_cast<const T*>(ia.t0)[2];
+    r.res1 = r.res2 = 0;
     r.has_cut = SUMS ? 7ull : 3ull;  // two cuts + the interior compacted (+ N_lo, P_hi)
     *ia.out = r;
     publish_done(ia.done, ia.seq);
@@ -1663,7 +1669,6 @@ struct BatchInitFn : InitSeg<float, false> {
   }
   __device__ __forceinline__ void group_end() {
     extremes(nvalid);
-    I0 += (double)((gI[0] + gI[1]) + (gI[2] + gI[3]));
 #pragma unroll
     for (int j = 0; j < 16; ++j) pc.vals[j] = vals[j];
     pc.lo_bits = bits;
@@ -1675,7 +1680,7 @@ struct BatchInitFn : InitSeg<float, false> {
     begin();
     if (ok) cut(v, 0, 0);
     extremes(ok ? 1 : 0);
-    I0 += (double)gI[0];
+
     if (bits & 1u) {
       const unsigned long long pos = atomicAdd(&pc.cursors[0], 1ull);
       if (pos < pc.z_cap) pc.z[pos] = v;
@@ -1724,7 +1729,7 @@ struct BatchState {
   unsigned long long n_cur, c_le_L, c_lt_R, D_lo, m, k_r;
   unsigned long long cursors[2];
   double t;
-  float yL, yR, tq, result, cut_lo, cut_hi;
+  float yL, yR, tq, result, cut_lo, cut_hi, cut_mid;
   int col, on_z, slow, bisect, phase, compact, cur_buf, tgt, side, iters;
 };
 
@@ -1795,6 +1800,8 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
         const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
         st.cut_lo = (float)from_key_f32(keys[il]);
         st.cut_hi = (float)from_key_f32(keys[ih]);
+        const double qm = floor(q);
+        st.cut_mid = (float)from_key_f32(keys[qm < 0 ? 0 : (qm >= md ? ms - 1 : (uint64_t)qm)]);
       }
       __syncthreads();
     }
@@ -1849,9 +1856,10 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
           st.t = 0.5 * p.vmin + 0.5 * p.vmax;  // only used if neither cut lies strictly inside
           if (cut) {  // the two extra cuts, as the host driver applies them (R23-R25)
-            // the batched init pass keeps only #x<=t_lo, the interior count and sum: the usual
-            // bracket ]t_lo, t_hi[ starts from its interior mean (App. A); a cut on the far side of
-            // the target moves to the adjacent float and the iteration starts from the midpoint
+            // the batched init pass keeps only #x<=t_lo and the interior count: the usual bracket
+            // ]t_lo, t_hi[ starts from the sample's estimate of the target (R25); a cut on the far
+            // side of the target moves to the adjacent float and the iteration starts from the
+            // midpoint
             const double tl = st.cut_lo, th = st.cut_hi;
             bool settled = false, mean_ok = false;
             if (tl > p.vmin && tl < p.vmax) {
@@ -1867,8 +1875,8 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
               const unsigned long long c_lt = p.cC;
               if (c_lt >= k) {
                 st.yR = (float)th; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
-                if ((double)st.yL == tl) {  // interior ]t_lo, t_hi[: mean = t_lo + I / m
-                  st.t = tl + p.I0 / (double)st.m;
+                if ((double)st.yL == tl && st.cut_mid > st.yL && st.cut_mid < st.yR) {
+                  st.t = st.cut_mid;  // the sample's estimate of the target (R25)
                   mean_ok = true;
                 }
               } else {  // y_L <- prev(t_hi): #x<=prev(t_hi) = #x<t_hi

@@ -26,7 +26,9 @@ struct DevInit {
   // the two extra cuts t_lo <= t_hi evaluated in the same pass (R23)
   double t_lo, t_hi, N_lo, P_hi, I_in;
   // #x<=t_lo and #x<t_hi: the counts the bracket update needs at each cut (R24)
-  unsigned long long c_le_lo, c_lt_hi, res0, res1, res2, has_cut;
+  unsigned long long c_le_lo, c_lt_hi;
+  double t_est;                    // the sample's estimate of x_(k) (a starting iterate)
+  unsigned long long res1, res2, has_cut;
 };
 
 // Per-CTA partial of a pass (grid reduction scratch).

@@ -96,8 +96,8 @@ class NumpyShard:
     def cut(self, r):
         """R26 cut pass over the current array (exactly the bracket interior): 1024 evenly strided
         samples, cuts at sample ranks q -/+ (3.5 sd + 2) around local rank r (or, with
-        cut_shift, deliberately off target to drive the far-side branches), #x<=t_a, the copy of
-        ]t_a, t_b[ and its sum of (x - t_a)."""
+        cut_shift, deliberately off target to drive the far-side branches), the sample estimate of
+        the target, #x<=t_a and the copy of ]t_a, t_b[."""
         x = self.cur
         m = x.size
         ms = min(m, 1024)
@@ -108,10 +108,11 @@ class NumpyShard:
         il = min(max(int(math.floor(q - w)), 0), ms - 1)
         ih = min(max(int(math.ceil(q + w)), il), ms - 1)
         ta, tb = smp[il], smp[ih]
+        te = smp[min(max(int(math.floor(q)), 0), ms - 1)]
         inner = (x > ta) & (x < tb)
         self.kept = (x[inner].copy(), None)
-        return {"t_a": float(ta), "t_b": float(tb), "le_a": int((x <= ta).sum()), "inner": int(inner.sum()),
-                "I": float(np.sum(x[inner].astype(np.float64) - np.float64(ta)))}
+        return {"t_a": float(ta), "t_b": float(tb), "t_est": float(te), "le_a": int((x <= ta).sum()),
+                "inner": int(inner.sum())}
 
     def select(self, side, r):
         part = self.cur if side == 2 else self.kept[side]
