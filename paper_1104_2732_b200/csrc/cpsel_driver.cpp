@@ -356,8 +356,14 @@ struct GpuBackend : Backend {
     const DevInit& r = *ctx->h_init;
     // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
     // cuts (which skip the shifted sum), as #x<t_hi + #x=t_hi + #x>t_hi < n
+    // R27: without the extremes' multiplicities the driver brackets with their outer neighbours,
+    // which must be finite (else the checked form below counts them)
+    const bool f32 = dt == kF32;
+    const double out_lo = f32 ? (double)std::nextafterf((float)r.vmin, -INFINITY) : std::nextafter(r.vmin, -INFINITY);
+    const double out_hi = f32 ? (double)std::nextafterf((float)r.vmax, INFINITY) : std::nextafter(r.vmax, INFINITY);
     const bool suspicious = cut ? (!std::isfinite(r.N_lo) || !std::isfinite(r.P_hi) || !std::isfinite(r.I_in) ||
                                    !std::isfinite(r.t_est) ||
+                                   ((r.has_cut & 8) && !(std::isfinite(out_lo) && std::isfinite(out_hi))) ||
                                    !std::isfinite(r.vmin) || !std::isfinite(r.vmax) || r.nonfinite != 0)
                                 : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
     if (!suspicious && fuse) {
@@ -807,21 +813,26 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   init_slot = be.slot;
   inf.bytes_moved = be.scanned * es;
   if (rec.nonfinite) return CPSEL_ENONFINITE;
-  if (k <= rec.cnt_min) return done(rec.vmin, 0);
-  if (k > n - rec.cnt_max) return done(rec.vmax, 1);
+  const bool f32 = dt == kF32;
+  auto next_up = [&](double v) { return f32 ? (double)std::nextafterf((float)v, INFINITY) : std::nextafter(v, INFINITY); };
+  auto next_dn = [&](double v) { return f32 ? (double)std::nextafterf((float)v, -INFINITY) : std::nextafter(v, -INFINITY); };
+  // R27: a fused init pass does not count the multiplicities of min and max; the bracket then
+  // starts at their outer neighbours, where the counts are known: #x<=prev(min) = 0, #x<next(max) = n
+  const bool ext_counts = (rec.has_cut & 8) == 0;
+  if (ext_counts && k <= rec.cnt_min) return done(rec.vmin, 0);
+  if (ext_counts && k > n - rec.cnt_max) return done(rec.vmax, 1);
   if (n <= cfg.direct_threshold && !cfg.force_cp) {
     double v;
     st = do_select(2, k, &v);
     if (st != CPSEL_OK) return st;
     return done(v, 6);
   }
-  double yL = rec.vmin, yR = rec.vmax;
-  uint64_t c_le_L = rec.cnt_min, c_lt_R = n - rec.cnt_max;
-  long double N_L = 0.0L, P_R = 0.0L;  // N(yL) = sum (yL-x)^+ = 0 at the min; P(yR) = 0 at the max
+  double yL = ext_counts ? rec.vmin : next_dn(rec.vmin), yR = ext_counts ? rec.vmax : next_up(rec.vmax);
+  uint64_t c_le_L = ext_counts ? rec.cnt_min : 0, c_lt_R = ext_counts ? n - rec.cnt_max : n;
+  long double N_L = 0.0L, P_R = 0.0L;  // N(yL) = sum (yL-x)^+ = 0 at (or below) the min; P(yR) = 0 at (or above) the max
   uint64_t m = c_lt_R - c_le_L;       // >= 1
   uint64_t D_lo = 0;                   // elements of x below the current array
   bool on_z = false;                   // the current array is a compacted bracket
-  // first iterate: mean of the interior (App. A) from the shifted sum
   // first iterate: mean of the interior (App. A) from the shifted sum (replaced below when the init
   // pass also evaluated the two extra cuts, R23)
   double t = rec.x0 + (rec.S - (double)rec.cnt_min * (rec.vmin - rec.x0) - (double)rec.cnt_max * (rec.vmax - rec.x0)) /
@@ -829,9 +840,6 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   int slow = 0;
   bool bisect = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
-  const bool f32 = dt == kF32;
-  auto next_up = [&](double v) { return f32 ? (double)std::nextafterf((float)v, INFINITY) : std::nextafter(v, INFINITY); };
-  auto next_dn = [&](double v) { return f32 ? (double)std::nextafterf((float)v, -INFINITY) : std::nextafter(v, -INFINITY); };
   constexpr uint64_t kUnknown = ~0ull;
   bool exact = true;  // the current (compacted) array holds exactly the bracket interior
   // R23: the init pass's two extra cuts t_lo <= t_hi (sample quantiles bracketing rank k) — two more
@@ -859,7 +867,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     // target lies between the cuts (the usual case).  A cut on the far side of the target moves to
     // the adjacent float, where the missing count is the known one: #x<next(t_lo) = #x<=t_lo,
     // #x<=prev(t_hi) = #x<t_hi (no element lies strictly between a float and its neighbour).
-    if (rec.t_lo > rec.vmin && rec.t_lo < rec.vmax) {
+    if (rec.t_lo > yL && rec.t_lo < yR) {
       const uint64_t c_le = rec.c_le_lo;
       cpsel_trace_row row = row_of(rec.t_lo, kUnknown, kUnknown, N_tl, P_tl);
       if (c_le < k) {  // y_L <- t_lo
@@ -877,7 +885,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       row.interior = m;
       if (trace && cfg.record_trace) trace->push_back(row);
     }
-    if (!settled && rec.t_hi > yL && rec.t_hi < rec.vmax) {
+    if (!settled && rec.t_hi > yL && rec.t_hi < yR) {
       const uint64_t c_lt = rec.c_lt_hi;
       cpsel_trace_row row = row_of(rec.t_hi, c_lt, kUnknown, N_th, P_th);
       if (c_lt >= k) {  // y_R <- t_hi: interior ]y_L, t_hi[

@@ -1460,8 +1460,9 @@ template <typename T, bool SUMS> struct InitSeg {
     cut(v.x, u, u * 2 + 0); cut(v.y, u, u * 2 + 1);
   }
   // group-level extremes: NaN-propagating min/max trees over the thread's values and a warp vote
-  // against the WARP-UNIFORM running (min, max); only a group that reaches a running extreme or holds
-  // a NaN takes the (warp-uniform) exact update.  Warp-level records are rare (~H(groups)/groups),
+  // against the WARP-UNIFORM running (min, max); only a group that beats a running extreme or holds
+  // a NaN takes the (warp-uniform) update.  The multiplicities of min and max are not counted (R27):
+  // the driver brackets with their outer neighbours instead.  Warp-level records are rare (~H(groups)/groups),
   // where per-thread records would send most warps down the slow path early on.  Must be called by
   // all 32 lanes.
   __device__ __forceinline__ static T nan_min(T a, T b) {
@@ -1485,7 +1486,7 @@ template <typename T, bool SUMS> struct InitSeg {
 #pragma unroll
     for (int j = 1; j < G; ++j)
       if (j < nvalid) { lo = nan_min(lo, vals[j]); hi = nan_max(hi, vals[j]); }
-    const bool need = !(lo > mn) || !(hi < mx);  // also taken on NaN
+    const bool need = !(lo >= mn) || !(hi <= mx);  // a new extreme, or a NaN
     if (__any_sync(FULL, need)) slow_group(nvalid, lo, hi);
   }
   __device__ __forceinline__ void slow_group(int nvalid, T lo, T hi) {
@@ -1505,16 +1506,8 @@ template <typename T, bool SUMS> struct InitSeg {
       lo = a < lo ? a : lo;
       hi = b > hi ? b : hi;
     }
-    if (lo < mn) { mn = lo; cmn = 0; }
-    if (hi > mx) { mx = hi; cmx = 0; }
-    if (lo == mn) {
-#pragma unroll
-      for (int j = 0; j < G; ++j) cmn += (j < nvalid && vals[j] == mn) ? 1u : 0u;
-    }
-    if (hi == mx) {
-#pragma unroll
-      for (int j = 0; j < G; ++j) cmx += (j < nvalid && vals[j] == mx) ? 1u : 0u;
-    }
+    mn = lo < mn ? lo : mn;
+    mx = hi > mx ? hi : mx;
   }
   __device__ __forceinline__ void end(int nvalid) {
     extremes(nvalid);
@@ -1646,7 +1639,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.c_lt_hi = tot.cA + tot.pad2;  // every x < t_hi is <= t_lo or interior
     r.t_est = (double)static_cast<const T*>(ia.t0)[2];
     r.res1 = r.res2 = 0;
-    r.has_cut = SUMS ? 7ull : 3ull;  // two cuts + the interior compacted (+ N_lo, P_hi)
+    r.has_cut = SUMS ? 15ull : 11ull;  // two cuts + the interior compacted (+ N_lo, P_hi), no #min/#max
     *ia.out = r;
     publish_done(ia.done, ia.seq);
   }
@@ -1844,14 +1837,12 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
           st.result = __int_as_float(0x7fc00000);
           atomicAdd(&a.stats[3], 1ull);
           st.phase = 1;
-        } else if (k <= p.cnt_min) {
-          st.result = (float)p.vmin; st.phase = 1;
-        } else if (k > n - p.cnt_max) {
-          st.result = (float)p.vmax; st.phase = 1;
         } else {
-          st.yL = (float)p.vmin; st.yR = (float)p.vmax;
-          st.c_le_L = p.cnt_min; st.c_lt_R = n - p.cnt_max;
-          st.m = st.c_lt_R - st.c_le_L;
+          // the bracket starts just outside the extremes (their multiplicities are not counted,
+          // R27): #x<=prev(min) = 0, #x<next(max) = n
+          st.yL = nextafterf((float)p.vmin, -INFINITY); st.yR = nextafterf((float)p.vmax, INFINITY);
+          st.c_le_L = 0; st.c_lt_R = n;
+          st.m = n;
           st.D_lo = 0; st.on_z = 0; st.slow = 0; st.bisect = 0;
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
           st.t = 0.5 * p.vmin + 0.5 * p.vmax;  // only used if neither cut lies strictly inside
@@ -1862,7 +1853,7 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
             // midpoint
             const double tl = st.cut_lo, th = st.cut_hi;
             bool settled = false, mean_ok = false;
-            if (tl > p.vmin && tl < p.vmax) {
+            if (tl > (double)st.yL && tl < (double)st.yR) {
               const unsigned long long c_le = p.cA;
               if (c_le < k) {
                 st.yL = (float)tl; st.c_le_L = c_le; st.m = st.c_lt_R - c_le;
@@ -1871,7 +1862,7 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
                 settled = true;
               }
             }
-            if (!settled && th > (double)st.yL && th < p.vmax) {
+            if (!settled && th > (double)st.yL && th < (double)st.yR) {
               const unsigned long long c_lt = p.cC;
               if (c_lt >= k) {
                 st.yR = (float)th; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
@@ -1884,6 +1875,7 @@ __global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) 
               }
             }
             if (!mean_ok) st.t = 0.5 * (double)st.yL + 0.5 * (double)st.yR;
+            if (!isfinite(st.t)) st.t = 0.5 * p.vmin + 0.5 * p.vmax;
             // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
             if (st.phase == 0 && (double)st.yL == tl && (double)st.yR == th && st.m == p.pad2 && p.pad2 <= a.cap) {
               st.cur = my0; st.n_cur = p.pad2; st.cur_buf = 0;

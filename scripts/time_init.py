@@ -1,6 +1,8 @@
-"""Time the init pass (and the rest of one selection) of a 2^30 f32 median with CUDA events:
-python scripts/time_init.py [dist] — prints mean kernel ms per selection part."""
+"""Time one selection's parts with CUDA events (record_timing) and the host overhead around them:
+python scripts/time_init.py [dist] [log2n] — mean kernel ms (init / passes / select), the driver's
+own wall time (info.ms_total) and the Python call's wall time."""
 import sys
+import time
 
 import torch
 
@@ -9,13 +11,20 @@ import datagen  # noqa: E402
 import paper_1104_2732_b200 as cp  # noqa: E402
 
 dist = sys.argv[1] if len(sys.argv) > 1 else "uniform"
-x = datagen.make(dist, 1 << 30, "f32", device="cuda")
+lg = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+x = datagen.make(dist, 1 << lg, "f32", device="cuda")
 torch.cuda.synchronize()
 cp.set_config(record_timing=1)
 for _ in range(3):
     cp.median(x)
-ini, pas, sel = [], [], []
-for _ in range(10):
+ini, pas, sel, tot, wall, passes = [], [], [], [], [], []
+for _ in range(20):
+    t0 = time.perf_counter()
     v, info = cp.median(x, return_info=True)
+    wall.append(1e3 * (time.perf_counter() - t0))
     ini.append(info["kernel_ms_init"]); pas.append(info["kernel_ms_passes"]); sel.append(info["kernel_ms_select"])
-print(f"{dist}: init {sum(ini)/len(ini):.4f} ms  passes {sum(pas)/len(pas):.4f} ms  select {sum(sel)/len(sel):.4f} ms")
+    tot.append(info["ms_total"]); passes.append(info["passes"])
+m = lambda a: sum(a) / len(a)  # noqa: E731
+k = m(ini) + m(pas) + m(sel)
+print(f"{dist} 2^{lg}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  kernels {k:.4f}  "
+      f"driver wall {m(tot):.4f}  python wall {m(wall):.4f} ms  passes/call {m(passes):.1f}")

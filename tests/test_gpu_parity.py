@@ -319,6 +319,22 @@ def test_pass_cuts_all_dists(cp, order):
     assert saw_cut
 
 
+@pytest.mark.parametrize("case", ["normal", "dup256", "flt_max"])
+def test_fused_init_extreme_ranks(cp, case):
+    """R27: the fused init pass does not count #min/#max — the bracket starts at their outer
+    neighbours; ranks at the very ends still come out exact, and +-FLT_MAX (outer neighbour
+    infinite) falls back to the checked init with counts."""
+    n = (1 << 23) + 77
+    x = datagen.make("dup256" if case == "dup256" else "normal", n, "f32")
+    if case == "flt_max":
+        x[[5, 77, 1000]] = np.float32(np.finfo(np.float32).max)
+        x[[6, 78]] = -np.float32(np.finfo(np.float32).max)
+    xd = tdev(x)
+    srt = np.sort(x)
+    for k in (1, 2, 3, n // 2, n - 2, n - 1, n):
+        assert cp.select_kth(xd, k) == srt[k - 1], (case, k)
+
+
 def test_host_buffer_path(cp):
     import torch
     x = datagen.make("normal", 3_000_001, "f32")
