@@ -207,6 +207,15 @@ cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int wo
 cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint64_t n_local,
                                       cpsel_dtype dtype, uint64_t k, void* h_out, cpsel_info* info);
 
+/* R28: cuts common to all ranks from their pooled samples — the host step of the sharded init and
+ * cut passes, exported for the CPU (gloo) tests.  keys: G blocks of 1024 order-preserving sample
+ * keys (f32: sign-flipped bits in the low 32; f64: sign-flipped 64 bits), block g sorted ascending
+ * with its min(m[g], 1024) valid keys first; m[g]: elements of rank g's array; r: the target rank
+ * (1-based) in the concatenation.  out3 <- t_a, t_b, the pooled estimate of the target.
+ * Errors: CPSEL_EINVAL (null pointers, G == 0, no element at all). */
+cpsel_status cpsel_pooled_cuts(const uint64_t* keys, const uint64_t* m, uint32_t G, uint64_t r, cpsel_dtype dtype,
+                               double* out3);
+
 /* ---- host-only driver (no GPU needed) ------------------------------------------------------ */
 /* The same cutting-plane driver, with the three device steps supplied as callbacks.  Used by
  * the CPU tests (world-size-2 gloo tests of the sharded combine) to exercise the exact host

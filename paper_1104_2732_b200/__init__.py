@@ -109,7 +109,7 @@ SYMBOLS = [
     "cpsel_set_config", "cpsel_get_config", "cpsel_set_stream", "cpsel_select_kth", "cpsel_median",
     "cpsel_select_kth_host", "cpsel_lms_objective", "cpsel_lms_residuals", "cpsel_select_kth_batched",
     "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_nccl_unique_id",
-    "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host",
+    "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host", "cpsel_pooled_cuts",
 ]
 
 _lib = None
@@ -156,6 +156,7 @@ def load():
             "cpsel_select_kth_sharded": (I, [P, P, U64, I, U64, P, C.POINTER(Info)]),
             "cpsel_drive_host": (I, [C.POINTER(HostBackend), U64, I, U64, C.POINTER(Config), C.POINTER(D),
                                      C.POINTER(Info), C.POINTER(TraceRow), U32, C.POINTER(U32)]),
+            "cpsel_pooled_cuts": (I, [P, P, U32, U64, I, C.POINTER(D)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -422,6 +423,20 @@ def select_kth_sharded(shard, k: int, return_info: bool = False):
     _check(ctx, load().cpsel_select_kth_sharded(ctx.handle, ptr, shard.numel(), dt, int(k), out, C.byref(info)))
     v = _out_value(out, dt)
     return (v, info.as_dict()) if return_info else v
+
+
+def pooled_cuts(keys, m, r: int, dtype: str):
+    """R28 host step: cuts (t_a, t_b, estimate) common to all ranks from their pooled sample keys
+    (keys: G x 1024 uint64 order-preserving keys, each block sorted with min(m[g],1024) valid first)."""
+    import numpy as np
+    k = np.ascontiguousarray(keys, dtype=np.uint64)
+    mm = np.ascontiguousarray(m, dtype=np.uint64)
+    out = (C.c_double * 3)()
+    st = load().cpsel_pooled_cuts(k.ctypes.data_as(C.c_void_p), mm.ctypes.data_as(C.c_void_p), int(mm.size), int(r),
+                                   F32 if dtype == "f32" else F64, out)
+    if st != OK:
+        raise CpselError(st, load().cpsel_status_string(st).decode())
+    return out[0], out[1], out[2]
 
 
 # ------------------------------------------------------------------------------------------ host driver

@@ -60,6 +60,12 @@ struct cpsel_ctx {
   RadixState* h_radix = nullptr;
   DevPass* h_gather = nullptr;
   DevInit* h_gather_init = nullptr;
+  // sharded sample cuts (R28): this rank's 1024 sorted sample keys, all ranks' (G x 1024), shard sizes
+  unsigned long long* d_keys = nullptr;
+  unsigned long long* d_keys_all = nullptr;
+  unsigned long long* h_keys_all = nullptr;
+  unsigned long long* d_sizes = nullptr;     // [0] this rank's, [1..G] all ranks'
+  unsigned long long* h_sizes = nullptr;
   // LMS workspace
   LmsWorkspace lms;
   // multi-GPU
@@ -321,7 +327,8 @@ struct GpuBackend : Backend {
   uint64_t half_n(int side) const { return side == 0 ? zlo : zhi; }
 
   // init kernel (fast form, then the checked form if anything came out non-finite)
-  cpsel_status run_init(bool sync_result, uint64_t k, bool cut) {
+  // presampled: d_t0 already holds the cuts (sharded: pooled across ranks, R28)
+  cpsel_status run_init(bool sync_result, uint64_t k, bool cut, bool presampled = false) {
     InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init, cut ? ctx->d_t0 : nullptr};
     if (use_mail) {
       a.out = &ctx->mb_dev->init;
@@ -332,7 +339,7 @@ struct GpuBackend : Backend {
     const bool fuse = cut && R > 0;
     init_seg_done = false;
     CK(tic());
-    if (cut) CK(launch_sample_cut(dt, x, n, k, ctx->d_t0, ctx->stream));
+    if (cut && !presampled) CK(launch_sample_cut(dt, x, n, k, ctx->d_t0, ctx->stream));
     if (fuse) {
       SegArgs sa{};
       sa.out = ctx->d_sb[0];
@@ -579,6 +586,40 @@ struct GpuBackend : Backend {
 };
 
 // ------------------------------------------------------------------------ G GPUs (NCCL)
+// R28: cuts common to all ranks from their pooled samples.  keys: G blocks of 1024 sorted sample
+// keys (block g holds ms_g = min(m_g, 1024) samples of rank g's m_g elements, padding after them);
+// each sample of rank g stands for m_g / ms_g elements.  Same ranks q -/+ (3.5 sd + 2) as the
+// one-array pick, in units of the pooled sample; every rank computes the same cuts from the same
+// bytes.  Returns false if there is no sample at all.
+bool pooled_pick(const unsigned long long* keys, const std::vector<uint64_t>& m, uint64_t r, int dt, double out[3]) {
+  const int G = (int)m.size();
+  std::vector<std::pair<unsigned long long, double>> smp;
+  uint64_t M = 0, S = 0;
+  for (int g = 0; g < G; ++g) {
+    const uint64_t ms = std::min<uint64_t>(m[g], 1024);
+    M += m[g];
+    S += ms;
+    for (uint64_t i = 0; i < ms; ++i) smp.emplace_back(keys[(size_t)g * 1024 + i], (double)m[g] / (double)ms);
+  }
+  if (smp.empty() || M == 0) return false;
+  std::sort(smp.begin(), smp.end());
+  const double Sd = (double)S;
+  const double qs = ((double)r - 0.5) / (double)M * Sd;
+  const double ws = 3.5 * std::sqrt(std::max(qs * (Sd - qs) / Sd, 0.0)) + 2.0;
+  const double scale = (double)M / Sd;  // elements per pooled sample
+  const double pos[3] = {(qs - ws) * scale, (qs + ws) * scale, qs * scale};
+  for (int j = 0; j < 3; ++j) {
+    double c = 0.0;
+    size_t i = 0;
+    for (; i + 1 < smp.size(); ++i) {
+      c += smp[i].second;
+      if (c > pos[j]) break;
+    }
+    out[j] = from_key(smp[i].first, dt);
+  }
+  return true;
+}
+
 struct ShardedBackend : GpuBackend {
   std::vector<uint64_t> n_rank;               // shard sizes
   std::vector<uint64_t> cur_rank;             // current-array sizes per rank
@@ -635,8 +676,174 @@ struct ShardedBackend : GpuBackend {
     cur_rank = n_rank;
     return CPSEL_OK;
   }
-  cpsel_status init(cpsel_init_stats* o, uint64_t) override {
-    *o = combined;  // no extra cut when sharded (it would need a cut common to all ranks)
+  // every rank's shard size (one tiny all-gather), before the buffers are sized
+  cpsel_status exchange_sizes() {
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    ctx->h_sizes[0] = n;
+    CK(cudaMemcpyAsync(ctx->d_sizes, ctx->h_sizes, sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->stream));
+    NK(nc.AllGather(ctx->d_sizes, ctx->d_sizes + 1, 1, ncclUint64, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_sizes + 1, ctx->d_sizes + 1, G * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    n_rank.assign(ctx->h_sizes + 1, ctx->h_sizes + 1 + G);
+    n_global = 0;
+    for (uint64_t v : n_rank) n_global += v;
+    return CPSEL_OK;
+  }
+  // R28: cuts around pooled rank r of the ranks' current arrays (m_rank elements each; the raw x
+  // when `on_x`) into d_t0 on every rank, identical everywhere; t[0..2] = t_a, t_b, estimate
+  cpsel_status pooled_t0(bool on_x, const std::vector<uint64_t>& m_rank, uint64_t r, double t[3]) {
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    if (on_x || !cur_seg)
+      CK(launch_sample_cut(dt, on_x ? x : cur, on_x ? n : n_cur, 1, ctx->d_t0, ctx->stream, 1024, ctx->d_keys));
+    else
+      CK(launch_sample_seg(dt, cur, cur_tab, cur_side, seg_total_warps(dt, ctx->shape), n_cur, 1, ctx->d_t0,
+                           ctx->stream, 1024, ctx->d_keys));
+    NK(nc.AllGather(ctx->d_keys, ctx->d_keys_all, 1024, ncclUint64, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_keys_all, ctx->d_keys_all, (size_t)G * 1024 * sizeof(unsigned long long),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!pooled_pick(ctx->h_keys_all, m_rank, r, dt, t)) return fail(ctx, CPSEL_EINTERNAL, "no samples");
+    unsigned char buf[24];
+    for (int j = 0; j < 3; ++j) {
+      if (dt == kF32) {
+        const float f = (float)t[j];
+        memcpy(buf + 4 * j, &f, 4);
+      } else {
+        memcpy(buf + 8 * j, &t[j], 8);
+      }
+    }
+    CK(cudaMemcpyAsync(ctx->d_t0, buf, dt == kF32 ? 12 : 24, cudaMemcpyHostToDevice, ctx->stream));
+    return CPSEL_OK;
+  }
+  // the init pass: with cuts (R23/R28) every rank runs the fused init at the pooled cuts and the
+  // records are all-gathered and combined in rank order; else the plain init (gather_init)
+  bool sharded_fused = false;
+  uint64_t init_total = 0;
+  std::vector<uint64_t> init_rank;
+  cpsel_status init(cpsel_init_stats* o, uint64_t k) override {
+    const bool cut = ctx->cfg.init_cut != 0 && n_global > 2 && R > 0;
+    sharded_fused = false;
+    if (!cut) {
+      cpsel_status st = gather_init();
+      if (st != CPSEL_OK) return st;
+      *o = combined;
+      return CPSEL_OK;
+    }
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    double tc[3];
+    cpsel_status st = pooled_t0(true, n_rank, k, tc);
+    if (st != CPSEL_OK) return st;
+    if (n > 0) {
+      st = run_init(false, k, true, /*presampled=*/true);  // launches: the sample kernel + the init
+      if (st != CPSEL_OK) return st;
+    } else {
+      launches = 1;
+      slot = -1;
+      DevInit e{};
+      e.vmin = INFINITY; e.vmax = -INFINITY;
+      e.has_cut = 11;  // an empty shard: nothing below, inside or above the cuts
+      *ctx->h_init = e;
+      CK(cudaMemcpyAsync(ctx->d_init, ctx->h_init, sizeof(DevInit), cudaMemcpyHostToDevice, ctx->stream));
+      // every warp of the (empty) segmented array has an empty run
+      CK(cudaMemsetAsync(ctx->d_st[0], 0, seg_total_warps(dt, ctx->shape) * sizeof(SegEntry), ctx->stream));
+      init_seg_done = true;
+      init_n_in = 0;
+    }
+    NK(nc.AllGather(ctx->d_init, ctx->d_gather_init, sizeof(DevInit), ncclUint8, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_gather_init, ctx->d_gather_init, G * sizeof(DevInit), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    scanned = n;
+    cpsel_init_stats c{};
+    c.vmin = INFINITY; c.vmax = -INFINITY;
+    c.has_cut = 11;  // two cuts, the interior compacted, no sums, no #min/#max (R27)
+    c.t_lo = tc[0]; c.t_hi = tc[1]; c.t_est = tc[2];
+    init_rank.assign(G, 0);
+    init_total = 0;
+    bool all_fused = true;
+    for (int q = 0; q < G; ++q) {
+      const DevInit& r = ctx->h_gather_init[q];
+      if (n_rank[q] == 0) continue;
+      c.vmin = std::min(c.vmin, r.vmin);
+      c.vmax = std::max(c.vmax, r.vmax);
+      c.nonfinite += r.nonfinite;
+      c.c_le_lo += r.c_le_lo;
+      c.c_lt_hi += r.c_lt_hi;
+      if ((r.has_cut & 11) != 11) all_fused = false;  // a rank fell back to the checked init
+      init_rank[q] = r.pad;
+      init_total += r.pad;
+    }
+    if (!all_fused || !std::isfinite(c.vmin) || !std::isfinite(c.vmax)) {
+      // a rank saw NaN/Inf (or could not bracket from the extremes' neighbours): the plain path
+      cpsel_status s2 = gather_init();
+      if (s2 != CPSEL_OK) return s2;
+      *o = combined;
+      return CPSEL_OK;
+    }
+    sharded_fused = true;
+    cur_rank = n_rank;
+    *o = c;
+    return CPSEL_OK;
+  }
+  bool init_compacted() const override { return sharded_fused; }
+  uint64_t init_written() const override { return init_total; }
+  cpsel_status adopt_init() override {
+    cpsel_status st = GpuBackend::adopt_init();
+    cur_rank = init_rank;
+    return st;
+  }
+  // R26 + R28: the cut pass with cuts pooled across ranks; tuples all-gathered, combined in rank order
+  bool has_cut_pass() const override { return R > 0; }
+  cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
+    const NcclApi& nc = nccl_api();
+    const int G = ctx->world;
+    double tc[3];
+    cpsel_status st = pooled_t0(false, cur_rank, r, tc);
+    if (st != CPSEL_OK) return st;
+    SegArgs a{};
+    a.x = cur; a.n = n_cur;
+    a.seg_in = cur_seg ? cur_tab : nullptr;
+    a.side_in = cur_side;
+    a.cuts = ctx->d_t0;
+    a.dense_out = dense ? 1 : 0;
+    if (dense) {
+      tgt = (cur_dbuf == 0) ? 1 : 0;
+      a.out = ctx->d_zb[tgt];
+      a.z_cap = cap;
+    } else {
+      tgt = (cur_sbuf == 0) ? 1 : 0;
+      a.out = ctx->d_sb[tgt];
+      a.R = R;
+      a.seg_out = static_cast<SegEntry*>(ctx->d_st[tgt]);
+    }
+    a.cursors = ctx->d_cursors;
+    a.partials = ctx->d_partials; a.ticket = ctx->d_ticket;
+    a.out_tuple = ctx->d_pass;
+    CK(tic());
+    CK(launch_cut_pass(dt, a, ctx->shape, ctx->stream));  // also for an empty array: run tables
+    CK(toc());
+    launches = 2;
+    scanned = n_cur;
+    NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    o->ta = tc[0]; o->tb = tc[1]; o->t_est = tc[2];
+    o->le_a = 0; o->inner = 0;
+    zlo_rank.assign(G, 0);
+    zhi_rank.assign(G, 0);
+    for (int q = 0; q < G; ++q) {
+      const DevPass& rr = ctx->h_gather[q];
+      o->le_a += rr.c_lt;
+      o->inner += rr.z_lo;
+      zlo_rank[q] = rr.z_lo;
+    }
+    last_dense = dense;
+    zlo = ctx->h_gather[ctx->rank].z_lo;
+    zhi = 0;
     return CPSEL_OK;
   }
   cpsel_status pass(double t, double yL, double yR, bool compact, bool dense, cpsel_pass_stats* o, uint64_t* z_lo,
@@ -1220,11 +1427,13 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
     void* dev[] = {ctx->d_t0, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
+                   ctx->d_keys, ctx->d_keys_all, ctx->d_sizes,
                    ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};
     for (void* p : dev)
       if (p) cudaFree(p);
     lms_free(ctx->lms);
-    void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init, ctx->mb};
+    void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init, ctx->mb,
+                    ctx->h_keys_all, ctx->h_sizes};
     for (void* p : host)
       if (p) cudaFreeHost(p);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
@@ -1373,10 +1582,20 @@ cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int wo
   if (ctx->d_gather_init) cudaFree(ctx->d_gather_init);
   if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
   if (ctx->h_gather_init) cudaFreeHost(ctx->h_gather_init);
+  if (ctx->d_keys) cudaFree(ctx->d_keys);
+  if (ctx->d_keys_all) cudaFree(ctx->d_keys_all);
+  if (ctx->h_keys_all) cudaFreeHost(ctx->h_keys_all);
+  if (ctx->d_sizes) cudaFree(ctx->d_sizes);
+  if (ctx->h_sizes) cudaFreeHost(ctx->h_sizes);
   CK(cudaMalloc(&ctx->d_gather, world * sizeof(DevPass)));
   CK(cudaMalloc(&ctx->d_gather_init, world * sizeof(DevInit)));
   CK(cudaHostAlloc(&ctx->h_gather, world * sizeof(DevPass), cudaHostAllocDefault));
   CK(cudaHostAlloc(&ctx->h_gather_init, world * sizeof(DevInit), cudaHostAllocDefault));
+  CK(cudaMalloc(&ctx->d_keys, 1024 * sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->d_keys_all, (size_t)world * 1024 * sizeof(unsigned long long)));
+  CK(cudaHostAlloc(&ctx->h_keys_all, (size_t)world * 1024 * sizeof(unsigned long long), cudaHostAllocDefault));
+  CK(cudaMalloc(&ctx->d_sizes, (size_t)(world + 1) * sizeof(unsigned long long)));
+  CK(cudaHostAlloc(&ctx->h_sizes, (size_t)(world + 1) * sizeof(unsigned long long), cudaHostAllocDefault));
   return CPSEL_OK;
 }
 
@@ -1389,7 +1608,7 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
   if (!h_out) return fail(ctx, CPSEL_EINVAL, "null h_out");
   DeviceGuard g(ctx->device);
   ShardedBackend be(ctx, d_shard, n_local, (int)dtype);
-  cpsel_status s = be.gather_init();
+  cpsel_status s = be.exchange_sizes();
   if (s != CPSEL_OK) return s;
   const uint64_t n = be.n_global;
   if (n == 0) return fail(ctx, CPSEL_EINVAL, "global n == 0");
@@ -1407,6 +1626,15 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
   if (s != CPSEL_OK) return s;
   store_value(v, dtype, h_out);
   return CPSEL_OK;
+}
+
+cpsel_status cpsel_pooled_cuts(const uint64_t* keys, const uint64_t* m, uint32_t G, uint64_t r, cpsel_dtype dtype,
+                               double* out3) {
+  if (!keys || !m || !out3 || G == 0) return CPSEL_EINVAL;
+  if (dtype != CPSEL_F32 && dtype != CPSEL_F64) return CPSEL_EINVAL;
+  std::vector<uint64_t> mm(m, m + G);
+  return pooled_pick(reinterpret_cast<const unsigned long long*>(keys), mm, r, (int)dtype, out3) ? CPSEL_OK
+                                                                                                 : CPSEL_EINVAL;
 }
 
 // ------------------------------------------------------------------------ host-only driver

@@ -443,9 +443,10 @@ __global__ void __launch_bounds__(kBlock, 4) init_kernel(InitArgs a) {
 // cuts bracketing local rank r of an m-element array, from ms real samples: ranks q -/+ 3.5
 // binomial standard deviations (+2) of the sample.  The target lies between the two cuts with
 // overwhelming probability on any input order (the cuts are exact either way).
+// keys_out != nullptr: write the sorted sample keys there instead (R28, pooled across ranks).
 template <typename T>
 __device__ __forceinline__ void sample_sort_pick(unsigned long long v, unsigned long long* key, uint64_t ms,
-                                                 uint64_t m, uint64_t r, T* t0) {
+                                                 uint64_t m, uint64_t r, T* t0, unsigned long long* keys_out) {
   constexpr int S = 1024;
   const int i = threadIdx.x;
   for (int size = 2; size <= S; size <<= 1) {
@@ -466,6 +467,10 @@ __device__ __forceinline__ void sample_sort_pick(unsigned long long v, unsigned 
   }
   key[i] = v;
   __syncthreads();
+  if (keys_out) {
+    keys_out[i] = v;
+    return;
+  }
   if (i == 0) {
     const double md = (double)ms;
     const double q = ((double)r - 0.5) / (double)m * md;
@@ -485,24 +490,26 @@ __device__ __forceinline__ void sample_sort_pick(unsigned long long v, unsigned 
 // R23: the two extra cuts of the init pass — 1024 evenly strided samples of x[0..n), cuts around
 // rank k.  (Also used for a contiguous current array with its local rank, R26.)
 template <typename T>
-__global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ x, uint64_t n, uint64_t k, T* t0) {
+__global__ void __launch_bounds__(1024) sample_cut_kernel(const T* __restrict__ x, uint64_t n, uint64_t k, T* t0,
+                                                          uint32_t smax, unsigned long long* keys_out) {
   constexpr int S = 1024;
   __shared__ unsigned long long key[S];
   const int i = threadIdx.x;
-  const uint64_t m = n < (uint64_t)S ? n : (uint64_t)S;
+  const uint64_t m = n < (uint64_t)smax ? n : (uint64_t)smax;
   unsigned long long v = ~0ull;  // padding sorts last
   if ((uint64_t)i < m) {
     const uint64_t pos = (n == m) ? (uint64_t)i : ((uint64_t)i * n) / m + (n / m) / 2;
     v = okey(x[pos]);
   }
-  sample_sort_pick<T>(v, key, m, n, k, t0);
+  sample_sort_pick<T>(v, key, m, n, k, t0, keys_out);
 }
 
 // R26: the same for a segmented current array (the runs `side` of the Wtot warp entries, m
 // elements in total): sample i is element floor(i*m/1024) + (m/1024)/2 of the concatenated runs.
 template <typename T>
 __global__ void __launch_bounds__(1024) sample_seg_kernel(const T* __restrict__ base, const SegEntry* __restrict__ tab,
-                                                          int side, int Wtot, uint64_t m, uint64_t r, T* t0) {
+                                                          int side, int Wtot, uint64_t m, uint64_t r, T* t0,
+                                                          uint32_t smax, unsigned long long* keys_out) {
   constexpr int S = 1024;
   __shared__ unsigned long long key[S];
   __shared__ unsigned long long cstart[S];
@@ -520,7 +527,7 @@ __global__ void __launch_bounds__(1024) sample_seg_kernel(const T* __restrict__ 
     cstart[i] += add;
     __syncthreads();
   }
-  const uint64_t ms = m < (uint64_t)S ? m : (uint64_t)S;
+  const uint64_t ms = m < (uint64_t)smax ? m : (uint64_t)smax;
   unsigned long long v = ~0ull;
   if ((uint64_t)i < ms) {
     uint64_t g = (m == ms) ? (uint64_t)i : ((uint64_t)i * m) / ms + (m / ms) / 2;
@@ -540,7 +547,7 @@ __global__ void __launch_bounds__(1024) sample_seg_kernel(const T* __restrict__ 
       g -= e.cnt[side];
     }
   }
-  sample_sort_pick<T>(v, key, ms, m, r, t0);
+  sample_sort_pick<T>(v, key, ms, m, r, t0, keys_out);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2039,9 +2046,14 @@ cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cuda
   return cudaGetLastError();
 }
 
-cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st) {
-  if (dtype == kF32) sample_cut_kernel<float><<<1, 1024, 0, st>>>(static_cast<const float*>(x), n, k, static_cast<float*>(t0));
-  else sample_cut_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(x), n, k, static_cast<double*>(t0));
+cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st,
+                              uint32_t smax, unsigned long long* keys_out) {
+  if (dtype == kF32)
+    sample_cut_kernel<float><<<1, 1024, 0, st>>>(static_cast<const float*>(x), n, k, static_cast<float*>(t0), smax,
+                                                 keys_out);
+  else
+    sample_cut_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(x), n, k, static_cast<double*>(t0), smax,
+                                                  keys_out);
   return cudaGetLastError();
 }
 
@@ -2099,13 +2111,13 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 }
 
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
-                              uint64_t r, void* t0, cudaStream_t st) {
+                              uint64_t r, void* t0, cudaStream_t st, uint32_t smax, unsigned long long* keys_out) {
   if (dtype == kF32)
     sample_seg_kernel<float><<<1, 1024, 0, st>>>(static_cast<const float*>(base), tab, side, Wtot, m, r,
-                                                 static_cast<float*>(t0));
+                                                 static_cast<float*>(t0), smax, keys_out);
   else
     sample_seg_kernel<double><<<1, 1024, 0, st>>>(static_cast<const double*>(base), tab, side, Wtot, m, r,
-                                                  static_cast<double*>(t0));
+                                                  static_cast<double*>(t0), smax, keys_out);
   return cudaGetLastError();
 }
 

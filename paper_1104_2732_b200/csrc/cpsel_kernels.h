@@ -141,8 +141,11 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 // R26: sample cuts of a compacted current array and the cut pass over it.
 // launch_sample_seg: t0[0..1] <- the two sample cuts around local rank r of the m-element
 // segmented array (runs `side` of tab[0..Wtot)).
+// smax (<= 1024): samples drawn; keys_out != nullptr: write the sorted sample keys (order-preserving
+// 64-bit keys, padding ~0) there instead of picking cuts (pooled across ranks, R28).
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
-                              uint64_t r, void* t0, cudaStream_t st);
+                              uint64_t r, void* t0, cudaStream_t st, uint32_t smax = 1024,
+                              unsigned long long* keys_out = nullptr);
 // launch_cut_pass: one read of the current array (a.x / a.seg_in / a.side_in as for
 // launch_seg_pass, every element inside the bracket) at the two cuts a.cuts = {t_a, t_b}:
 // #x<=t_a, the copy_if of ]t_a, t_b[ (segmented run 0 of each warp region, or dense from z[0]) and
@@ -152,7 +155,8 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
 // t0[0], t0[1] <- the sample quantiles bracketing rank k (1024 strided samples of x, one CTA)
-cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st);
+cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st,
+                              uint32_t smax = 1024, unsigned long long* keys_out = nullptr);
 cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
 
 // Radix select of the r-th smallest (1-based) of z[0..m) (any element alignment).

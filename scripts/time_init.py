@@ -12,19 +12,30 @@ import paper_1104_2732_b200 as cp  # noqa: E402
 
 dist = sys.argv[1] if len(sys.argv) > 1 else "uniform"
 lg = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+sharded = len(sys.argv) > 3 and sys.argv[3] == "sharded"  # the NCCL path at world size 1
 x = datagen.make(dist, 1 << lg, "f32", device="cuda")
 torch.cuda.synchronize()
 cp.set_config(record_timing=1)
+if sharded:
+    cp.comm_init(cp.nccl_unique_id(), 0, 1, torch.cuda.current_device())
+
+
+def run():
+    if sharded:
+        return cp.select_kth_sharded(x, (x.numel() + 1) // 2, return_info=True)
+    return cp.median(x, return_info=True)
+
+
 for _ in range(3):
-    cp.median(x)
+    run()
 ini, pas, sel, tot, wall, passes = [], [], [], [], [], []
 for _ in range(20):
     t0 = time.perf_counter()
-    v, info = cp.median(x, return_info=True)
+    v, info = run()
     wall.append(1e3 * (time.perf_counter() - t0))
     ini.append(info["kernel_ms_init"]); pas.append(info["kernel_ms_passes"]); sel.append(info["kernel_ms_select"])
     tot.append(info["ms_total"]); passes.append(info["passes"])
 m = lambda a: sum(a) / len(a)  # noqa: E731
 k = m(ini) + m(pas) + m(sel)
-print(f"{dist} 2^{lg}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  kernels {k:.4f}  "
+print(f"{dist} 2^{lg}{' sharded' if sharded else ''}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  kernels {k:.4f}  "
       f"driver wall {m(tot):.4f}  python wall {m(wall):.4f} ms  passes/call {m(passes):.1f}")

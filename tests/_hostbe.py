@@ -8,6 +8,24 @@ import math
 import numpy as np
 
 
+def sample_keys(x, smax=1024):
+    """Sorted order-preserving keys of min(len(x), smax) evenly strided samples of x, padded to 1024
+    with ~0 (the layout the R28 pooled pick takes)."""
+    m = x.size
+    ms = min(m, smax)
+    pos = np.arange(ms) if m == ms else (np.arange(ms, dtype=np.int64) * m) // ms + (m // ms) // 2
+    v = x[pos]
+    if v.dtype == np.float32:
+        u = v.view(np.uint32).astype(np.uint64)
+        k = np.where(u >> 31, (~u) & 0xFFFFFFFF, u | 0x80000000)
+    else:
+        u = v.view(np.uint64)
+        k = np.where(u >> 63, ~u, u | np.uint64(1 << 63))
+    out = np.full(1024, np.iinfo(np.uint64).max, dtype=np.uint64)
+    out[:ms] = np.sort(k.astype(np.uint64))
+    return out
+
+
 class NumpyShard:
     def __init__(self, x, comm=None, cut_k=None, cut_shift=0.0):
         self.x = np.ascontiguousarray(x)
@@ -50,6 +68,20 @@ class NumpyShard:
             out["nonfinite"] += r["nonfinite"]
             S += r["S"] + r["n"] * (r["x0"] - out["x0"])
         out["S"] = S
+        if self.cut_k is not None and self.comm is not None and sum(self._gather(x.size)) > 2:
+            # R28: cuts common to all ranks from the pooled samples, statistics summed over ranks
+            import paper_1104_2732_b200 as cp
+            sizes = self._gather(x.size)
+            keys = np.stack(self._gather(sample_keys(x)))
+            dt = "f32" if x.dtype == np.float32 else "f64"
+            tl, th, te = cp.pooled_cuts(keys, sizes, self.cut_k, dt)
+            xd = x.astype(np.float64)
+            inner = (x > tl) & (x < th)
+            mine = {"c_le_lo": int((x <= tl).sum()), "c_lt_hi": int((x < th).sum()),
+                    "N_lo": float(np.sum(tl - xd[x < tl])), "P_hi": float(np.sum(xd[x > th] - th)),
+                    "I_in": float(np.sum(xd[inner] - tl))}
+            tot = {key: sum(r[key] for r in self._gather(mine)) for key in mine}
+            out.update(has_cut=6, t_lo=float(tl), t_hi=float(th), t_est=float(te), **tot)
         if self.cut_k is not None and self.comm is None and x.size > 2:
             # R23: two cuts at the sample quantiles bracketing rank k (1024 strided samples)
             n = x.size
@@ -99,6 +131,16 @@ class NumpyShard:
         cut_shift, deliberately off target to drive the far-side branches), the sample estimate of
         the target, #x<=t_a and the copy of ]t_a, t_b[."""
         x = self.cur
+        if self.comm is not None:  # R28: pooled across ranks (the current arrays' sizes as weights)
+            import paper_1104_2732_b200 as cp
+            sizes = self._gather(x.size)
+            keys = np.stack(self._gather(sample_keys(x)))
+            ta, tb, te = cp.pooled_cuts(keys, sizes, r, "f32" if x.dtype == np.float32 else "f64")
+            inner = (x > ta) & (x < tb)
+            self.kept = (x[inner].copy(), None)
+            both = self._gather((int((x <= ta).sum()), int(inner.sum())))
+            return {"t_a": ta, "t_b": tb, "t_est": te, "le_a": sum(a for a, _ in both),
+                    "inner": sum(b for _, b in both)}
         m = x.size
         ms = min(m, 1024)
         pos = np.arange(ms) if m == ms else (np.arange(ms, dtype=np.int64) * m) // ms + (m // ms) // 2
@@ -125,4 +167,4 @@ def drive(x, k, dtype, comm=None, config=None, cut=False, pass_cuts=False, cut_s
     be = NumpyShard(x, comm, cut_k=k if cut else None, cut_shift=cut_shift)
     n = x.size if comm is None else sum(comm(x.size))
     return cp.drive_host(n, k, dtype, be.init, be.pass_, be.adopt, be.select, config,
-                         cut_fn=be.cut if (pass_cuts and comm is None) else None)
+                         cut_fn=be.cut if pass_cuts else None)

@@ -370,3 +370,17 @@ def test_sharded_world1_nccl(cp):
         xd = tdev(x)
         for k in (1, 77, O.median_rank(x.size), x.size):
             assert canon(cp.select_kth_sharded(xd, k)) == float(O.order_statistic(x, k))
+    # large enough for the fused init at pooled sample cuts and the cut passes (R26-R28)
+    cp.set_config(select_cap=1 << 16)
+    try:
+        for dist in ("uniform", "cauchy", "dup256"):
+            x = datagen.make(dist, (1 << 23) + 77, "f32")
+            xd = tdev(x)
+            srt = np.sort(x)
+            for k in (1, 3, x.size // 10, x.size - 1, O.median_rank(x.size)):
+                v, info = cp.select_kth_sharded(xd, k, return_info=True)
+                assert v == srt[k - 1], (dist, k)
+            assert info["init_written"] > 0                  # (the median: the cuts bracket it)
+            assert any(r["kind"] == 3 for r in cp.get_trace())
+    finally:
+        cp.set_config(select_cap=0)

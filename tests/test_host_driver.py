@@ -59,6 +59,27 @@ def test_driver_pass_cuts(dtype, cut_shift):
     assert any(r["kind"] == 3 for r in trace)
 
 
+def test_pooled_cuts_bracket_the_pooled_rank():
+    """R28: cuts pooled from uneven shards' samples (weights m_g / #samples_g) bracket the pooled
+    order statistic, are sample values of the shards, and the estimate lies between them."""
+    import paper_1104_2732_b200 as cp
+    from tests._hostbe import sample_keys
+    rng = np.random.default_rng(28)
+    for dtype in ("f32", "f64"):
+        npdt = np.float32 if dtype == "f32" else np.float64
+        for sizes in ([300_000, 5_000, 0, 120_000], [1000, 1000], [7, 200_000], [3]):
+            shards = [rng.standard_normal(m).astype(npdt) * (g + 1) + g for g, m in enumerate(sizes)]
+            allx = np.concatenate(shards)
+            srt = np.sort(allx)
+            keys = np.stack([sample_keys(sh) for sh in shards])
+            for r in sorted({1, max(allx.size // 10, 1), (allx.size + 1) // 2, allx.size}):
+                ta, tb, te = cp.pooled_cuts(keys, sizes, r, dtype)
+                assert ta <= te <= tb
+                assert any(np.any(sh == ta) for sh in shards) and any(np.any(sh == tb) for sh in shards)
+                if 10 < r < allx.size - 10 and allx.size > 1000:
+                    assert ta <= srt[r - 1] <= tb, (sizes, r)
+
+
 def test_driver_tiny_all_ranks_with_ties_and_signed_zero():
     rng = np.random.default_rng(5)
     for _ in range(300):
@@ -156,8 +177,10 @@ def _sharded_worker(rank, world, port, cases, q):
         x = datagen.make(dist_name, n, dtype)
         bounds = [0] + split + [n]
         shard = x[bounds[rank]:bounds[rank + 1]]
-        v, info, trace = drive(shard, k, dtype, comm=comm, config={"force_cp": 1, "z_cap": zc, "select_cap": 50})
-        results.append((v, info["passes"], [(r["t"], r["c_lt"], r["c_eq"]) for r in trace]))
+        for cuts in (False, True):   # plain, and with the pooled sample cuts of R28 (init + cut passes)
+            v, info, trace = drive(shard, k, dtype, comm=comm, config={"force_cp": 1, "z_cap": zc, "select_cap": 50},
+                                   cut=cuts, pass_cuts=cuts)
+            results.append((v, info["passes"], [(r["t"], r["c_lt"], r["c_eq"], r["kind"]) for r in trace]))
     q.put((rank, results))
     dist.destroy_process_group()
 
@@ -186,5 +209,8 @@ def test_sharded_host_logic_gloo_world2():
     for i, (dist_name, n_, dtype, k, zc, split) in enumerate(cases):
         x = datagen.make(dist_name, n_, dtype)
         expect = float(O.order_statistic(x, k))
-        assert canon(got[0][i][0]) == expect and canon(got[1][i][0]) == expect
-        assert got[0][i][1:] == got[1][i][1:]                 # identical driver decisions
+        for j in (2 * i, 2 * i + 1):
+            assert canon(got[0][j][0]) == expect and canon(got[1][j][0]) == expect
+            assert got[0][j][1:] == got[1][j][1:]             # identical driver decisions
+    # the pooled cuts ran (kind-2 init cuts and kind-3 cut passes) in the median case
+    assert any(row[3] == 2 for row in got[0][1][2]) and any(row[3] == 3 for row in got[0][1][2])
