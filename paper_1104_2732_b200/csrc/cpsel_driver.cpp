@@ -40,6 +40,7 @@ struct cpsel_ctx {
   DevPass* d_pass = nullptr;
   DevInit* d_init = nullptr;
   void* d_t0 = nullptr;              // the two extra cuts of the init pass (R23)
+  void* d_skeys = nullptr;           // gathered sample keys (R29)
   RadixState* d_radix = nullptr;
   unsigned int* d_hist = nullptr;
   DevPass* d_gather = nullptr;       // G x DevPass (sharded)
@@ -339,7 +340,8 @@ struct GpuBackend : Backend {
     const bool fuse = cut && R > 0;
     init_seg_done = false;
     CK(tic());
-    if (cut && !presampled) CK(launch_sample_cut(dt, x, n, k, ctx->d_t0, ctx->stream));
+    if (cut && !presampled)
+      CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream));
     if (fuse) {
       SegArgs sa{};
       sa.out = ctx->d_sb[0];
@@ -493,9 +495,8 @@ struct GpuBackend : Backend {
   void set_inexact() override { cur_exact = false; }
   bool has_cut_pass() const override { return use_mail && R > 0; }
   cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
-    if (cur_seg) CK(launch_sample_seg(dt, cur, cur_tab, cur_side, seg_total_warps(dt, ctx->shape), n_cur, r, ctx->d_t0,
-                                      ctx->stream));
-    else CK(launch_sample_cut(dt, cur, n_cur, r, ctx->d_t0, ctx->stream));
+    CK(launch_sample_select(dt, cur, n_cur, cur_seg ? cur_tab : nullptr, cur_side, seg_total_warps(dt, ctx->shape), r,
+                            ctx->d_t0, ctx->d_skeys, ctx->stream));
     SegArgs a{};
     a.x = cur; a.n = n_cur;
     a.seg_in = cur_seg ? cur_tab : nullptr;
@@ -1404,6 +1405,7 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMalloc(&ctx->d_pass, sizeof(DevPass)));
   CKC(cudaMalloc(&ctx->d_init, sizeof(DevInit)));
   CKC(cudaMalloc(&ctx->d_t0, 32));  // t_lo, t_hi, the sample estimate
+  CKC(cudaMalloc(&ctx->d_skeys, kSampleKeyBytes));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
   CKC(cudaMalloc(&ctx->d_hist, 2048 * sizeof(unsigned)));
   CKC(cudaMemset(ctx->d_hist, 0, 2048 * sizeof(unsigned)));
@@ -1425,7 +1427,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
-    void* dev[] = {ctx->d_t0, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
+    void* dev[] = {ctx->d_t0, ctx->d_skeys, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
                    ctx->d_keys, ctx->d_keys_all, ctx->d_sizes,
                    ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};

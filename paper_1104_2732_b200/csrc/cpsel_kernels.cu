@@ -551,6 +551,176 @@ __global__ void __launch_bounds__(1024) sample_seg_kernel(const T* __restrict__ 
 }
 
 // ------------------------------------------------------------------------------------------
+// R29: the sample cuts from a LARGE sample — 32768 (f32) / 16384 (f64) evenly strided samples of
+// the current array (contiguous, or the runs `side` of a segmented one), kept in registers as
+// order-preserving keys, and the three sample order statistics (ranks q - w, q + w and q) found
+// by one-CTA MSB radix select of all three at once (11-bit digits, smem histograms), not a sort.
+// With 32768 samples the two cuts keep ~2% of the array between them (vs ~11% with 1024).
+template <typename T> struct SampleKey;
+template <> struct SampleKey<float> {
+  using K = unsigned;
+  static constexpr int KPT = 32, ROUNDS = 3;
+  __device__ static K key(float v) { return (unsigned)okey(v); }
+  __device__ static float val(K k) { return (float)from_key_f32(k); }
+  __device__ static int shift(int r) { return r == 0 ? 21 : (r == 1 ? 10 : 0); }
+  __device__ static int bits(int r) { return r == 2 ? 10 : 11; }
+};
+template <> struct SampleKey<double> {
+  using K = unsigned long long;
+  static constexpr int KPT = 16, ROUNDS = 6;
+  __device__ static K key(double v) { return okey(v); }
+  __device__ static double val(K k) { return from_key_f64(k); }
+  __device__ static int shift(int r) { return r < 4 ? 53 - 11 * r : (r == 4 ? 10 : 0); }
+  __device__ static int bits(int r) { return r < 4 ? 11 : 10; }
+};
+struct SampleSel {
+  unsigned hist[3][2048];
+  unsigned long long prefix[3], mask[3], rank[3];
+};
+constexpr int kGatherMaxWarps = 5888;  // run-table entries a gather CTA can scan in shared memory (46 KB)
+
+// Gather: sample s (one per thread of kSampleCtas<T> CTAs) is element floor(s*m/ms) + (m/ms)/2 of
+// the array (contiguous x, or the concatenation of the runs `side` of tab[0..Wtot)), written as an
+// order-preserving key; padding keys ~0 beyond ms.  Many CTAs, so the scattered loads of the
+// sample are spread over the SMs.
+template <typename T> constexpr int kSampleCtas = SampleKey<T>::KPT;
+template <typename T>
+__global__ void __launch_bounds__(1024) sample_gather_kernel(const T* __restrict__ x, uint64_t m,
+                                                             const SegEntry* __restrict__ tab, int side, int Wtot,
+                                                             typename SampleKey<T>::K* __restrict__ keys) {
+  using SK = SampleKey<T>;
+  using K = typename SK::K;
+  constexpr uint64_t S = 1024ull * SK::KPT;
+  __shared__ unsigned long long pre[kGatherMaxWarps];  // inclusive prefix of the run lengths
+  __shared__ unsigned long long wsum[32];
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const uint64_t ms = m < S ? m : S;
+  const uint64_t smp = (uint64_t)blockIdx.x * 1024 + i;
+  if (tab) {
+    // every CTA scans the whole (small) run table: per-thread chunk sums, warp and block scans
+    const int per = (Wtot + 1023) / 1024;
+    const int w0 = i * per, w1 = min(w0 + per, Wtot);
+    unsigned long long c = 0;
+    for (int w = w0; w < w1; ++w) {
+      c += tab[w].cnt[side];
+      pre[w] = c;
+    }
+    unsigned long long incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned long long v = wsum[lane], inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      wsum[lane] = inc - v;  // exclusive warp offsets
+    }
+    __syncthreads();
+    const unsigned long long base = wsum[warp] + incl - c;  // exclusive offset of this thread's chunk
+    for (int w = w0; w < w1; ++w) pre[w] += base;
+    __syncthreads();
+  }
+  K key = ~K(0);
+  if (smp < ms) {
+    uint64_t g = (m == ms) ? smp : (smp * m) / ms + (m / ms) / 2;
+    if (!tab) {
+      key = SK::key(x[g]);
+    } else {
+      int lo = 0, hi = Wtot - 1;  // first run whose inclusive prefix exceeds g
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (pre[mid] > g) hi = mid; else lo = mid + 1;
+      }
+      g -= lo ? pre[lo - 1] : 0ull;
+      key = SK::key(x[tab[lo].off[side] + g]);
+    }
+  }
+  if (smp < S) keys[smp] = key;
+}
+
+// Select: one CTA of 1024 threads holds the KPT keys per thread in registers and finds the three
+// sample order statistics (ranks q - w, q + w and q; q the local target rank r scaled to the
+// sample) by MSB radix select of all three at once (11-bit digits, smem histograms) — no sort.
+template <typename T>
+__global__ void __launch_bounds__(1024) sample_select_kernel(const typename SampleKey<T>::K* __restrict__ keys_in,
+                                                             uint64_t m, uint64_t r, T* t0) {
+  using SK = SampleKey<T>;
+  using K = typename SK::K;
+  constexpr int KPT = SK::KPT;
+  constexpr uint64_t S = 1024ull * KPT;
+  __shared__ SampleSel sh;
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  const uint64_t ms = m < S ? m : S;
+  K keys[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) keys[j] = keys_in[(uint64_t)j * 1024 + i];
+  if (i == 0) {
+    const double md = (double)ms;
+    const double q = ((double)r - 0.5) / (double)m * md;
+    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+    const double qq[3] = {floor(q - w), ceil(q + w), floor(q)};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      sh.rank[t] = qq[t] < 0 ? 0 : (qq[t] >= md ? ms - 1 : (uint64_t)qq[t]);  // 0-based
+      sh.prefix[t] = 0;
+      sh.mask[t] = 0;
+    }
+  }
+  for (int rd = 0; rd < SK::ROUNDS; ++rd) {
+    const int shift = SK::shift(rd), nb = 1 << SK::bits(rd);
+    for (int b = i; b < 3 * 2048; b += 1024) (&sh.hist[0][0])[b] = 0u;
+    __syncthreads();
+    const K p0 = (K)sh.prefix[0], p1 = (K)sh.prefix[1], p2 = (K)sh.prefix[2];
+    const K m0 = (K)sh.mask[0], m1 = (K)sh.mask[1], m2 = (K)sh.mask[2];
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      const K k = keys[j];
+      const unsigned d = (unsigned)(k >> shift) & (unsigned)(nb - 1);
+      if ((k & m0) == p0) atomicAdd(&sh.hist[0][d], 1u);
+      if ((k & m1) == p1) atomicAdd(&sh.hist[1][d], 1u);
+      if ((k & m2) == p2) atomicAdd(&sh.hist[2][d], 1u);
+    }
+    __syncthreads();
+    if (warp < 3) {  // warp t finds the digit holding rank[t] (running prefix over 32-bin chunks)
+      const int t = warp;
+      unsigned long long before = 0;
+      const unsigned long long rk = sh.rank[t];
+      for (int b0 = 0; b0 < nb; b0 += 32) {
+        const unsigned h = sh.hist[t][b0 + lane];
+        unsigned incl = h;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const bool hit = before + incl > rk && before + incl - h <= rk;
+        const unsigned hm = __ballot_sync(FULL, hit);
+        if (hm) {
+          const int src = __ffs(hm) - 1;
+          const unsigned ex = __shfl_sync(FULL, incl - h, src);
+          if (lane == 0) {
+            sh.prefix[t] |= (unsigned long long)(b0 + src) << shift;
+            sh.mask[t] |= (unsigned long long)(nb - 1) << shift;
+            sh.rank[t] = rk - (before + ex);
+          }
+          break;
+        }
+        before += __shfl_sync(FULL, incl, 31);
+      }
+    }
+    __syncthreads();
+  }
+  if (i < 3) t0[i] = SK::val((K)sh.prefix[i]);
+}
+
+// ------------------------------------------------------------------------------------------
 // Step a2 (+ a4): one cutting-plane pass.
 // Compaction (a4) is block-synchronous per tile: every thread keeps the flags of its
 // UNROLL*VE elements, the block scans the (lo,hi) counts (warp shuffles + one smem round), ONE
@@ -2106,6 +2276,22 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
   } else {
     if (inside) seg_pass_kernel<double, true><<<g, kBlock, 0, st>>>(a);
     else seg_pass_kernel<double, false><<<g, kBlock, 0, st>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
+                                 uint64_t r, void* t0, void* keys, cudaStream_t st) {
+  if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
+  if (dtype == kF32) {
+    auto* kk = static_cast<SampleKey<float>::K*>(keys);
+    sample_gather_kernel<float><<<kSampleCtas<float>, 1024, 0, st>>>(static_cast<const float*>(x), m, tab, side, Wtot, kk);
+    sample_select_kernel<float><<<1, 1024, 0, st>>>(kk, m, r, static_cast<float*>(t0));
+  } else {
+    auto* kk = static_cast<SampleKey<double>::K*>(keys);
+    sample_gather_kernel<double><<<kSampleCtas<double>, 1024, 0, st>>>(static_cast<const double*>(x), m, tab, side, Wtot,
+                                                                       kk);
+    sample_select_kernel<double><<<1, 1024, 0, st>>>(kk, m, r, static_cast<double*>(t0));
   }
   return cudaGetLastError();
 }

@@ -141,6 +141,14 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 // R26: sample cuts of a compacted current array and the cut pass over it.
 // launch_sample_seg: t0[0..1] <- the two sample cuts around local rank r of the m-element
 // segmented array (runs `side` of tab[0..Wtot)).
+// R29: t0[0..2] <- the cuts around local rank r (1-based) of the m-element current array and the
+// sample estimate, from 32768 (f32) / 16384 (f64) evenly strided samples: contiguous x (tab ==
+// nullptr) or the runs `side` of the segmented array (base x, tab[0..Wtot)).
+// keys: device scratch of kSampleKeyBytes (the gathered sample).  Two launches: a many-CTA gather of
+// the sample keys and a one-CTA radix select of the three sample order statistics.
+constexpr size_t kSampleKeyBytes = 32768 * 4 > 16384 * 8 ? 32768 * 4 : 16384 * 8;
+cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
+                                 uint64_t r, void* t0, void* keys, cudaStream_t st);
 // smax (<= 1024): samples drawn; keys_out != nullptr: write the sorted sample keys (order-preserving
 // 64-bit keys, padding ~0) there instead of picking cuts (pooled across ranks, R28).
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
