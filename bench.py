@@ -229,7 +229,8 @@ def main():
     hot_x = cls(lambda r: r["kind"] != 2 and not r["compacted"] and r["scanned"] == n)
     comp_x = cls(lambda r: r["kind"] != 2 and r["compacted"] and r["scanned"] == n)
     z_pass = cls(lambda r: r["kind"] != 2 and r["scanned"] < n)
-    # the init pass (sample cut + init reduction with the two cuts and the fused copy_if, R23)
+    # the init pass (init_seg_kernel alone: the init reduction with the two cuts and the fused copy_if,
+    # R23; its sample kernels are timed separately, R29)
     init_bytes = sum(4 * (n + i["init_written"]) for i in infos)
     init_ms_tot = sum(init_ms)
     init_cls = {"launches": len(infos), "bytes": init_bytes, "ms": init_ms_tot,
@@ -249,7 +250,8 @@ def main():
         with open(tp) as f:
             tj = json.load(f)
         traffic = tj.get(dom_name.split("<")[0], {}).get("dram_bytes_per_launch")
-    step_kernel_ms = sum(i["kernel_ms_init"] + i["kernel_ms_passes"] + i["kernel_ms_select"] for i in infos) / a.steps
+    step_kernel_ms = sum(i["kernel_ms_init"] + i["kernel_ms_passes"] + i["kernel_ms_select"] + i["kernel_ms_sample"]
+                         for i in infos) / a.steps
     launches = sum(i["launches"] for i in infos)
     cp.set_config(local, z_cap=a.z_cap, record_timing=0)
 
@@ -319,7 +321,9 @@ def main():
                                      "bracket_passes": z_pass, "all_cp_passes": all_pass}},
             "cp_iters": {"mean": statistics.fmean(iters), "min": min(iters), "max": max(iters)},
             "kernel_ms_per_step": {"init": sum(init_ms) / a.steps, "passes": sum(i["kernel_ms_passes"] for i in infos) / a.steps,
-                                   "select": sum(sel_ms) / a.steps, "all": step_kernel_ms},
+                                   "select": sum(sel_ms) / a.steps,
+                                   "sample": sum(i["kernel_ms_sample"] for i in infos) / a.steps,
+                                   "all": step_kernel_ms},
             "gpu_launches": launches,
             "clocks": clk,
             "e2e": e2e,

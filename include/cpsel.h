@@ -87,6 +87,7 @@ typedef struct {
   double kernel_ms_passes; /* record_timing: sum over the cutting-plane pass kernels */
   double kernel_ms_select; /* record_timing: the small-set selection kernels */
   uint64_t init_written;   /* elements the init pass copied out (fused compaction of ]t_lo, t_hi[, R23) */
+  double kernel_ms_sample; /* record_timing: the sample-cut kernels (gather + select, R29), not in the above */
 } cpsel_info;
 
 /* One objective pass at t (Fig. 1 'Objective'), see cpsel_eval. */

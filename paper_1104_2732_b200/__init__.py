@@ -46,7 +46,7 @@ class Info(C.Structure):
                 ("exit_reason", C.c_uint32), ("z_count", C.c_uint64), ("bytes_moved", C.c_uint64),
                 ("ms_total", C.c_double), ("launches", C.c_uint32), ("reserved", C.c_uint32),
                 ("kernel_ms_init", C.c_double), ("kernel_ms_passes", C.c_double), ("kernel_ms_select", C.c_double),
-                ("init_written", C.c_uint64)]
+                ("init_written", C.c_uint64), ("kernel_ms_sample", C.c_double)]
 
     def as_dict(self):
         d = {f: getattr(self, f) for f, _ in self._fields_}

@@ -235,6 +235,7 @@ struct Backend {
   // kernels launched / timing slot (record_timing; -1: none) / local elements read, of the last step
   uint32_t launches = 0;
   int slot = -1;
+  int sample_slot = -1;  // the sample-cut kernels of the last step (R29), if timed separately
   uint64_t scanned = 0;
   // CUDA-event milliseconds of a step's timing slot (waits for it); 0 if none
   virtual double slot_ms(int) { return 0.0; }
@@ -340,8 +341,13 @@ struct GpuBackend : Backend {
     const bool fuse = cut && R > 0;
     init_seg_done = false;
     CK(tic());
-    if (cut && !presampled)
+    sample_slot = -1;
+    if (cut && !presampled) {
       CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream));
+      CK(toc());
+      sample_slot = slot;
+      CK(tic());
+    }
     if (fuse) {
       SegArgs sa{};
       sa.out = ctx->d_sb[0];
@@ -495,8 +501,11 @@ struct GpuBackend : Backend {
   void set_inexact() override { cur_exact = false; }
   bool has_cut_pass() const override { return use_mail && R > 0; }
   cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
+    CK(tic());
     CK(launch_sample_select(dt, cur, n_cur, cur_seg ? cur_tab : nullptr, cur_side, seg_total_warps(dt, ctx->shape), r,
                             ctx->d_t0, ctx->d_skeys, ctx->stream));
+    CK(toc());
+    sample_slot = slot;
     SegArgs a{};
     a.x = cur; a.n = n_cur;
     a.seg_in = cur_seg ? cur_tab : nullptr;
@@ -986,6 +995,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   // once the selection is over
   int init_slot = -1, select_slot = -1;
   std::vector<std::pair<int, long>> pass_slots;
+  std::vector<int> sample_slots;
   auto done = [&](double v, uint32_t reason) {
     *value = canonical_zero(v);
     inf.exit_reason = reason;
@@ -993,6 +1003,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     if (cfg.record_timing) {
       inf.kernel_ms_init = be.slot_ms(init_slot);
       inf.kernel_ms_select = be.slot_ms(select_slot);
+      inf.kernel_ms_sample = 0.0;
+      for (int ss : sample_slots) inf.kernel_ms_sample += be.slot_ms(ss);
       inf.kernel_ms_passes = 0.0;
       for (const auto& ps : pass_slots) {
         const double ms = be.slot_ms(ps.first);
@@ -1019,6 +1031,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   inf.passes = 1;
   inf.launches += be.launches;
   init_slot = be.slot;
+  if (be.sample_slot >= 0) sample_slots.push_back(be.sample_slot);
   inf.bytes_moved = be.scanned * es;
   if (rec.nonfinite) return CPSEL_ENONFINITE;
   const bool f32 = dt == kF32;
@@ -1050,6 +1063,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
   constexpr uint64_t kUnknown = ~0ull;
   bool exact = true;  // the current (compacted) array holds exactly the bracket interior
+  bool cuts_stalled = false;  // R26 cut passes stopped making progress
+  bool free_step = false;     // the next pass's iterate was not a Kelley step (progress not judged)
   // R23: the init pass's two extra cuts t_lo <= t_hi (sample quantiles bracketing rank k) — two more
   // cuts of the cutting-plane model, evaluated in the same read of x as the init reduction.  N and P
   // at both cuts follow from the pass's sums: N(t_lo) = N_lo, P(t_hi) = P_hi,
@@ -1114,6 +1129,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     }
     // without the sums the interior sum I is not kept either: start from the sample's estimate
     if (!sums) t = (rec.t_est > yL && rec.t_est < yR) ? rec.t_est : (double)NAN;
+    free_step = !sums;
     if (!std::isfinite(t)) t = 0.5 * yL + 0.5 * yR;
     // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
     if (be.init_compacted() && yL == rec.t_lo && yR == rec.t_hi) {
@@ -1139,7 +1155,9 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     // around the local target rank; the copy keeps only ]t_a, t_b[ (~10% of the array) instead of
     // both halves of a Kelley split.  Not with objective=1 (F at the sample cuts would need two
     // more sums per element).
-    if (cfg.pass_cuts && !cfg.objective && on_z && exact && !bisect && m > select_cap && be.has_cut_pass()) {
+    if (cfg.pass_cuts && !cfg.objective && on_z && exact && !bisect && !cuts_stalled && m > select_cap &&
+        be.has_cut_pass()) {
+      const uint64_t m_before = m;
       Backend::CutResult cr{};
       st = be.cut_pass(k - c_le_L, m <= dense_cap, &cr);
       if (st != CPSEL_OK) return st;
@@ -1148,6 +1166,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       inf.cp_iters++;
       inf.bytes_moved += be.scanned * es + cr.inner * es;
       pass_slots.emplace_back(be.slot, (trace && cfg.record_trace) ? (long)trace->size() : -1L);
+      if (be.sample_slot >= 0) sample_slots.push_back(be.sample_slot);
       const uint64_t le_a = c_le_L + cr.le_a, lt_b = le_a + cr.inner;
       cpsel_trace_row row{};
       row.t = cr.ta;
@@ -1160,6 +1179,9 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       N_L = P_R = NAN;  // F is not tracked through sample cuts
       if (le_a < k && k <= lt_b && cr.ta < cr.tb) {  // the usual case: continue on the copy of ]t_a, t_b[
         yL = cr.ta; yR = cr.tb; c_le_L = le_a; c_lt_R = lt_b; m = cr.inner;
+        // a sample that cannot split the bracket (e.g. one repeated value inside it) hands over to
+        // Kelley passes for the rest of the selection
+        if (m > m_before / 2) cuts_stalled = true;
         row.interior = m;
         if (trace && cfg.record_trace) trace->push_back(row);
         st = be.adopt(0);
@@ -1175,6 +1197,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
         // next iterate (if any pass still needs one): the sample's estimate of x_(k)
         t = (cr.t_est > cr.ta && cr.t_est < cr.tb) ? cr.t_est : 0.5 * cr.ta + 0.5 * cr.tb;
         slow = 0;
+        free_step = true;
         continue;
       }
       // the target is outside the sample cuts: the bracket moves to the adjacent float of the cut
@@ -1191,7 +1214,12 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       if (trace && cfg.record_trace) trace->push_back(row);
       exact = false;
       be.set_inexact();
-      t = 0.5 * yL + 0.5 * yR;
+      cuts_stalled = true;  // the rest of this selection runs Kelley passes
+      // next iterate: the sample's estimate of x_(k) if it lies inside (it is typically the value
+      // a one-sided miss came from, e.g. a repeated value), else the midpoint; not a Kelley step,
+      // so it does not count towards the progress safeguard
+      t = (cr.t_est > yL && cr.t_est < yR) ? cr.t_est : 0.5 * yL + 0.5 * yR;
+      free_step = true;
       continue;
     }
     uint32_t kind = 0;
@@ -1287,7 +1315,9 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     }
     // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
     // ordered-key bisection until progress resumes (bounds the pass count on any input)
-    if (m > m_old - m_old / 8) {
+    if (free_step) {
+      free_step = false;
+    } else if (m > m_old - m_old / 8) {
       if (++slow >= 2) bisect = true;
     } else {
       slow = 0;

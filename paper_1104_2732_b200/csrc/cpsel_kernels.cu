@@ -557,9 +557,12 @@ __global__ void __launch_bounds__(1024) sample_seg_kernel(const T* __restrict__ 
 // by one-CTA MSB radix select of all three at once (11-bit digits, smem histograms), not a sort.
 // With 32768 samples the two cuts keep ~2% of the array between them (vs ~11% with 1024).
 template <typename T> struct SampleKey;
+// ROUNDS: MSB digits resolved; the cuts are the bounds of the remaining key class (f32: 10 bits =
+// 2^10 ulps, f64: 20 bits) — any float is a valid cut, only its rank precision matters.
 template <> struct SampleKey<float> {
   using K = unsigned;
-  static constexpr int KPT = 32, ROUNDS = 3;
+  static constexpr int KPT = 32, ROUNDS = 2;
+  static constexpr K KLO = 0x00800000u, KHI = 0xff7fffffu;  // keys of -FLT_MAX, +FLT_MAX
   __device__ static K key(float v) { return (unsigned)okey(v); }
   __device__ static float val(K k) { return (float)from_key_f32(k); }
   __device__ static int shift(int r) { return r == 0 ? 21 : (r == 1 ? 10 : 0); }
@@ -567,7 +570,8 @@ template <> struct SampleKey<float> {
 };
 template <> struct SampleKey<double> {
   using K = unsigned long long;
-  static constexpr int KPT = 16, ROUNDS = 6;
+  static constexpr int KPT = 16, ROUNDS = 4;
+  static constexpr K KLO = 0x0010000000000000ull, KHI = 0xffefffffffffffffull;  // keys of -DBL_MAX, +DBL_MAX
   __device__ static K key(double v) { return okey(v); }
   __device__ static double val(K k) { return from_key_f64(k); }
   __device__ static int shift(int r) { return r < 4 ? 53 - 11 * r : (r == 4 ? 10 : 0); }
@@ -575,6 +579,7 @@ template <> struct SampleKey<double> {
 };
 struct SampleSel {
   unsigned hist[3][2048];
+  unsigned csum[3][32];
   unsigned long long prefix[3], mask[3], rank[3];
 };
 constexpr int kGatherMaxWarps = 5888;  // run-table entries a gather CTA can scan in shared memory (46 KB)
@@ -583,9 +588,10 @@ constexpr int kGatherMaxWarps = 5888;  // run-table entries a gather CTA can sca
 // the array (contiguous x, or the concatenation of the runs `side` of tab[0..Wtot)), written as an
 // order-preserving key; padding keys ~0 beyond ms.  Many CTAs, so the scattered loads of the
 // sample are spread over the SMs.
-template <typename T> constexpr int kSampleCtas = SampleKey<T>::KPT;
+constexpr int kGatherThreads = 256;
+template <typename T> constexpr int kSampleCtas = SampleKey<T>::KPT * 1024 / kGatherThreads;
 template <typename T>
-__global__ void __launch_bounds__(1024) sample_gather_kernel(const T* __restrict__ x, uint64_t m,
+__global__ void __launch_bounds__(kGatherThreads) sample_gather_kernel(const T* __restrict__ x, uint64_t m,
                                                              const SegEntry* __restrict__ tab, int side, int Wtot,
                                                              typename SampleKey<T>::K* __restrict__ keys) {
   using SK = SampleKey<T>;
@@ -594,11 +600,12 @@ __global__ void __launch_bounds__(1024) sample_gather_kernel(const T* __restrict
   __shared__ unsigned long long pre[kGatherMaxWarps];  // inclusive prefix of the run lengths
   __shared__ unsigned long long wsum[32];
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  constexpr int NW = kGatherThreads / 32;
   const uint64_t ms = m < S ? m : S;
-  const uint64_t smp = (uint64_t)blockIdx.x * 1024 + i;
+  const uint64_t smp = (uint64_t)blockIdx.x * kGatherThreads + i;
   if (tab) {
     // every CTA scans the whole (small) run table: per-thread chunk sums, warp and block scans
-    const int per = (Wtot + 1023) / 1024;
+    const int per = (Wtot + kGatherThreads - 1) / kGatherThreads;
     const int w0 = i * per, w1 = min(w0 + per, Wtot);
     unsigned long long c = 0;
     for (int w = w0; w < w1; ++w) {
@@ -614,13 +621,13 @@ __global__ void __launch_bounds__(1024) sample_gather_kernel(const T* __restrict
     if (lane == 31) wsum[warp] = incl;
     __syncthreads();
     if (warp == 0) {
-      unsigned long long v = wsum[lane], inc = v;
+      unsigned long long v = lane < NW ? wsum[lane] : 0ull, inc = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const unsigned long long y = __shfl_up_sync(FULL, inc, o);
         if (lane >= o) inc += y;
       }
-      wsum[lane] = inc - v;  // exclusive warp offsets
+      if (lane < NW) wsum[lane] = inc - v;  // exclusive warp offsets
     }
     __syncthreads();
     const unsigned long long base = wsum[warp] + incl - c;  // exclusive offset of this thread's chunk
@@ -661,6 +668,23 @@ __global__ void __launch_bounds__(1024) sample_select_kernel(const typename Samp
   K keys[KPT];
 #pragma unroll
   for (int j = 0; j < KPT; ++j) keys[j] = keys_in[(uint64_t)j * 1024 + i];
+  // sort this thread's keys (bitonic network in registers)
+#pragma unroll
+  for (int size = 2; size <= KPT; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int l = j ^ stride;
+        if (l > j) {
+          const K a = keys[j], b = keys[l];
+          const bool up = (j & size) == 0;
+          keys[j] = up ? (a < b ? a : b) : (a < b ? b : a);
+          keys[l] = up ? (a < b ? b : a) : (a < b ? a : b);
+        }
+      }
+    }
+  }
   if (i == 0) {
     const double md = (double)ms;
     const double q = ((double)r - 0.5) / (double)m * md;
@@ -679,45 +703,98 @@ __global__ void __launch_bounds__(1024) sample_select_kernel(const typename Samp
     __syncthreads();
     const K p0 = (K)sh.prefix[0], p1 = (K)sh.prefix[1], p2 = (K)sh.prefix[2];
     const K m0 = (K)sh.mask[0], m1 = (K)sh.mask[1], m2 = (K)sh.mask[2];
+    // each thread's keys are sorted, so the keys of a prefix class are contiguous and their digits
+    // non-decreasing: one shared atomic per run of equal digits (the leading digits of a sample
+    // are highly concentrated — per-key atomics would serialise on a few bins)
+    const int ntg = rd == 0 ? 1 : 3;  // round 0: every prefix is empty, one histogram serves all
 #pragma unroll
-    for (int j = 0; j < KPT; ++j) {
-      const K k = keys[j];
-      const unsigned d = (unsigned)(k >> shift) & (unsigned)(nb - 1);
-      if ((k & m0) == p0) atomicAdd(&sh.hist[0][d], 1u);
-      if ((k & m1) == p1) atomicAdd(&sh.hist[1][d], 1u);
-      if ((k & m2) == p2) atomicAdd(&sh.hist[2][d], 1u);
+    for (int t = 0; t < 3; ++t) {
+      if (t >= ntg) break;
+      const K pt = t == 0 ? p0 : (t == 1 ? p1 : p2), mt = t == 0 ? m0 : (t == 1 ? m1 : m2);
+      unsigned run = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const K k = keys[j];
+        const bool in = (k & mt) == pt;
+        const unsigned d = (unsigned)(k >> shift) & (unsigned)(nb - 1);
+        run += in ? 1u : 0u;
+        bool last = in;
+        if (j + 1 < KPT) {
+          const K kn = keys[j + 1 < KPT ? j + 1 : j];
+          last = in && (((kn & mt) != pt) || (((unsigned)(kn >> shift) & (unsigned)(nb - 1)) != d));
+        }
+        if (last) {
+          atomicAdd(&sh.hist[t][d], run);
+          run = 0;
+        }
+      }
     }
     __syncthreads();
-    if (warp < 3) {  // warp t finds the digit holding rank[t] (running prefix over 32-bin chunks)
+    if (rd == 0)
+      for (int b = i; b < 2048; b += 1024) sh.hist[1][b] = sh.hist[2][b] = sh.hist[0][b];
+    __syncthreads();
+    // digit search, two levels: warp w sums bins [64w, 64w+64) of each target, then warp t finds
+    // the 64-bin chunk and the bin holding rank[t]
+    {
+      const int c0 = warp * 64;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        unsigned v = (c0 + lane < nb ? sh.hist[t][c0 + lane] : 0u) + (c0 + 32 + lane < nb ? sh.hist[t][c0 + 32 + lane] : 0u);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) sh.csum[t][warp] = v;
+      }
+    }
+    __syncthreads();
+    if (warp < 3) {
       const int t = warp;
-      unsigned long long before = 0;
       const unsigned long long rk = sh.rank[t];
-      for (int b0 = 0; b0 < nb; b0 += 32) {
-        const unsigned h = sh.hist[t][b0 + lane];
-        unsigned incl = h;
+      // chunk: inclusive scan of the 32 chunk sums
+      const unsigned cs = sh.csum[t][lane];
+      unsigned incl = cs;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const unsigned hm = __ballot_sync(FULL, (unsigned long long)incl > rk);
+      const int c = __ffs(hm) - 1;  // first chunk whose inclusive total exceeds rk
+      unsigned long long before = __shfl_sync(FULL, incl - cs, c);
+      // bin inside the chunk (two 32-bin halves)
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const int b = c * 64 + half * 32 + lane;
+        const unsigned h = b < nb ? sh.hist[t][b] : 0u;
+        unsigned in2 = h;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-          const unsigned y = __shfl_up_sync(FULL, incl, o);
-          if (lane >= o) incl += y;
+          const unsigned y = __shfl_up_sync(FULL, in2, o);
+          if (lane >= o) in2 += y;
         }
-        const bool hit = before + incl > rk && before + incl - h <= rk;
-        const unsigned hm = __ballot_sync(FULL, hit);
-        if (hm) {
-          const int src = __ffs(hm) - 1;
-          const unsigned ex = __shfl_sync(FULL, incl - h, src);
+        const unsigned hb = __ballot_sync(FULL, before + in2 > rk);
+        if (hb) {
+          const int src = __ffs(hb) - 1;
+          const unsigned ex = __shfl_sync(FULL, in2 - h, src);
           if (lane == 0) {
-            sh.prefix[t] |= (unsigned long long)(b0 + src) << shift;
+            sh.prefix[t] |= (unsigned long long)(c * 64 + half * 32 + src) << shift;
             sh.mask[t] |= (unsigned long long)(nb - 1) << shift;
             sh.rank[t] = rk - (before + ex);
           }
           break;
         }
-        before += __shfl_sync(FULL, incl, 31);
+        before += __shfl_sync(FULL, in2, 31);
       }
     }
     __syncthreads();
   }
-  if (i < 3) t0[i] = SK::val((K)sh.prefix[i]);
+  if (i < 3) {
+    // t_a: the lower bound of its class, t_b: the upper bound, estimate: the lower bound — clamped
+    // to the finite keys
+    K kk = (K)sh.prefix[i];
+    if (i == 1) kk |= (K)~(K)sh.mask[1];
+    kk = kk < SK::KLO ? SK::KLO : (kk > SK::KHI ? SK::KHI : kk);
+    t0[i] = SK::val(kk);
+  }
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2285,12 +2362,13 @@ cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const Seg
   if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
   if (dtype == kF32) {
     auto* kk = static_cast<SampleKey<float>::K*>(keys);
-    sample_gather_kernel<float><<<kSampleCtas<float>, 1024, 0, st>>>(static_cast<const float*>(x), m, tab, side, Wtot, kk);
+    sample_gather_kernel<float><<<kSampleCtas<float>, kGatherThreads, 0, st>>>(static_cast<const float*>(x), m, tab,
+                                                                                side, Wtot, kk);
     sample_select_kernel<float><<<1, 1024, 0, st>>>(kk, m, r, static_cast<float*>(t0));
   } else {
     auto* kk = static_cast<SampleKey<double>::K*>(keys);
-    sample_gather_kernel<double><<<kSampleCtas<double>, 1024, 0, st>>>(static_cast<const double*>(x), m, tab, side, Wtot,
-                                                                       kk);
+    sample_gather_kernel<double><<<kSampleCtas<double>, kGatherThreads, 0, st>>>(static_cast<const double*>(x), m, tab,
+                                                                                  side, Wtot, kk);
     sample_select_kernel<double><<<1, 1024, 0, st>>>(kk, m, r, static_cast<double*>(t0));
   }
   return cudaGetLastError();

@@ -28,14 +28,15 @@ def run():
 
 for _ in range(3):
     run()
-ini, pas, sel, tot, wall, passes = [], [], [], [], [], []
+ini, pas, sel, tot, wall, passes, smp = [], [], [], [], [], [], []
 for _ in range(20):
     t0 = time.perf_counter()
     v, info = run()
     wall.append(1e3 * (time.perf_counter() - t0))
     ini.append(info["kernel_ms_init"]); pas.append(info["kernel_ms_passes"]); sel.append(info["kernel_ms_select"])
-    tot.append(info["ms_total"]); passes.append(info["passes"])
+    tot.append(info["ms_total"]); passes.append(info["passes"]); smp.append(info["kernel_ms_sample"])
 m = lambda a: sum(a) / len(a)  # noqa: E731
-k = m(ini) + m(pas) + m(sel)
-print(f"{dist} 2^{lg}{' sharded' if sharded else ''}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  kernels {k:.4f}  "
+k = m(ini) + m(pas) + m(sel) + m(smp)
+print(f"{dist} 2^{lg}{' sharded' if sharded else ''}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  "
+      f"sample {m(smp):.4f}  kernels {k:.4f}  "
       f"driver wall {m(tot):.4f}  python wall {m(wall):.4f} ms  passes/call {m(passes):.1f}")

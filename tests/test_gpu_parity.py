@@ -63,7 +63,7 @@ def test_init_extra_cut(cp, dtype, dist):
     s = cp.init_stats(tdev(x))
     assert s["has_cut"] & 2 and s["has_cut"] & 4          # cuts, with the positive-part sums
     tl, th = s["t_lo"], s["t_hi"]
-    assert tl <= th and np.any(x == tl) and np.any(x == th)
+    assert tl <= th and np.isfinite(tl) and np.isfinite(th)   # any floats (R29: key-class bounds)
     rl = O.pass_stats(x, tl, -math.inf, math.inf)
     rh = O.pass_stats(x, th, tl, th)
     assert s["c_le_lo"] == rl["c_lt"] + rl["c_eq"]
