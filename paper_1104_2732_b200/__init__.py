@@ -195,24 +195,28 @@ class _Ctx:
 _ctxs: dict[int, _Ctx] = {}
 
 
-def _ctx_for(t) -> _Ctx:
+def _current_stream(dev: int) -> int:
     import torch
-    if not (hasattr(t, "is_cuda") and t.is_cuda):
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)  # the cheap form of current_stream()
+    return raw(dev) if raw is not None else torch.cuda.current_stream(dev).cuda_stream
+
+
+def _ctx_for(t) -> _Ctx:
+    if not getattr(t, "is_cuda", False):
         raise ValueError("expected a CUDA tensor (no CPU fallback)")
-    dev = t.device.index if t.device.index is not None else torch.cuda.current_device()
+    dev = t.get_device()
     c = _ctxs.get(dev)
     if c is None:
         c = _ctxs[dev] = _Ctx(dev)
-    c.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+    c.bind_stream(_current_stream(dev))
     return c
 
 
 def _ctx_device(dev: int) -> _Ctx:
-    import torch
     c = _ctxs.get(dev)
     if c is None:
         c = _ctxs[dev] = _Ctx(dev)
-    c.bind_stream(torch.cuda.current_stream(dev).cuda_stream)
+    c.bind_stream(_current_stream(dev))
     return c
 
 
@@ -252,11 +256,15 @@ def select_kth(x, k: int, return_info: bool = False):
     x = _flat(x)
     ctx = _ctx_for(x)
     dt = _dtype_code(x)
-    out = C.create_string_buffer(8)
-    info = Info()
-    _check(ctx, load().cpsel_select_kth(ctx.handle, C.c_void_p(x.data_ptr()), x.numel(), dt, int(k), out,
-                                       C.byref(info)))
-    v = _out_value(out, dt)
+    lib = _lib or load()
+    if dt == F32:
+        out = C.c_float()
+    else:
+        out = C.c_double()
+    info = Info() if return_info else None
+    _check(ctx, lib.cpsel_select_kth(ctx.handle, x.data_ptr(), x.numel(), dt, k, C.byref(out),
+                                     C.byref(info) if info is not None else None))
+    v = out.value
     return (v, info.as_dict()) if return_info else v
 
 

@@ -589,14 +589,13 @@ constexpr int kGatherMaxWarps = 5888;  // run-table entries a gather CTA can sca
 // order-preserving key; padding keys ~0 beyond ms.  Many CTAs, so the scattered loads of the
 // sample are spread over the SMs.
 constexpr int kGatherThreads = 256;
-template <typename T> constexpr int kSampleCtas = SampleKey<T>::KPT * 1024 / kGatherThreads;
-template <typename T>
+template <typename T, int KPT>
 __global__ void __launch_bounds__(kGatherThreads) sample_gather_kernel(const T* __restrict__ x, uint64_t m,
                                                              const SegEntry* __restrict__ tab, int side, int Wtot,
                                                              typename SampleKey<T>::K* __restrict__ keys) {
   using SK = SampleKey<T>;
   using K = typename SK::K;
-  constexpr uint64_t S = 1024ull * SK::KPT;
+  constexpr uint64_t S = 1024ull * KPT;
   __shared__ unsigned long long pre[kGatherMaxWarps];  // inclusive prefix of the run lengths
   __shared__ unsigned long long wsum[32];
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
@@ -655,12 +654,11 @@ __global__ void __launch_bounds__(kGatherThreads) sample_gather_kernel(const T* 
 // Select: one CTA of 1024 threads holds the KPT keys per thread in registers and finds the three
 // sample order statistics (ranks q - w, q + w and q; q the local target rank r scaled to the
 // sample) by MSB radix select of all three at once (11-bit digits, smem histograms) — no sort.
-template <typename T>
+template <typename T, int KPT>
 __global__ void __launch_bounds__(1024) sample_select_kernel(const typename SampleKey<T>::K* __restrict__ keys_in,
                                                              uint64_t m, uint64_t r, T* t0) {
   using SK = SampleKey<T>;
   using K = typename SK::K;
-  constexpr int KPT = SK::KPT;
   constexpr uint64_t S = 1024ull * KPT;
   __shared__ SampleSel sh;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
@@ -2357,21 +2355,24 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
   return cudaGetLastError();
 }
 
-cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
-                                 uint64_t r, void* t0, void* keys, cudaStream_t st) {
-  if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
-  if (dtype == kF32) {
-    auto* kk = static_cast<SampleKey<float>::K*>(keys);
-    sample_gather_kernel<float><<<kSampleCtas<float>, kGatherThreads, 0, st>>>(static_cast<const float*>(x), m, tab,
-                                                                                side, Wtot, kk);
-    sample_select_kernel<float><<<1, 1024, 0, st>>>(kk, m, r, static_cast<float*>(t0));
-  } else {
-    auto* kk = static_cast<SampleKey<double>::K*>(keys);
-    sample_gather_kernel<double><<<kSampleCtas<double>, kGatherThreads, 0, st>>>(static_cast<const double*>(x), m, tab,
-                                                                                  side, Wtot, kk);
-    sample_select_kernel<double><<<1, 1024, 0, st>>>(kk, m, r, static_cast<double*>(t0));
-  }
+template <typename T, int KPT>
+cudaError_t sample_select_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
+                            void* keys, cudaStream_t st) {
+  auto* kk = static_cast<typename SampleKey<T>::K*>(keys);
+  sample_gather_kernel<T, KPT><<<KPT * 1024 / kGatherThreads, kGatherThreads, 0, st>>>(static_cast<const T*>(x), m, tab,
+                                                                                       side, Wtot, kk);
+  sample_select_kernel<T, KPT><<<1, 1024, 0, st>>>(kk, m, r, static_cast<T*>(t0));
   return cudaGetLastError();
+}
+
+cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
+                                 uint64_t r, void* t0, void* keys, cudaStream_t st, bool small) {
+  if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
+  if (dtype == kF32)
+    return small ? sample_select_t<float, 8>(x, m, tab, side, Wtot, r, t0, keys, st)
+                 : sample_select_t<float, SampleKey<float>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st);
+  return small ? sample_select_t<double, 4>(x, m, tab, side, Wtot, r, t0, keys, st)
+               : sample_select_t<double, SampleKey<double>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st);
 }
 
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,

@@ -147,8 +147,9 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 // keys: device scratch of kSampleKeyBytes (the gathered sample).  Two launches: a many-CTA gather of
 // the sample keys and a one-CTA radix select of the three sample order statistics.
 constexpr size_t kSampleKeyBytes = 32768 * 4 > 16384 * 8 ? 32768 * 4 : 16384 * 8;
+// small: 8192 (f32) / 4096 (f64) samples instead (the cut passes over an already small bracket).
 cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
-                                 uint64_t r, void* t0, void* keys, cudaStream_t st);
+                                 uint64_t r, void* t0, void* keys, cudaStream_t st, bool small = false);
 // smax (<= 1024): samples drawn; keys_out != nullptr: write the sorted sample keys (order-preserving
 // 64-bit keys, padding ~0) there instead of picking cuts (pooled across ranks, R28).
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
