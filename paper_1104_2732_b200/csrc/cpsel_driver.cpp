@@ -224,6 +224,7 @@ struct Backend {
   struct CutResult {
     double ta, tb, t_est;  // the cuts and the sample's estimate of x_(k)
     uint64_t le_a, inner;  // local #x<=t_a, #]t_a,t_b[
+    bool overflow;         // the (dense) copy did not fit: counts valid, nothing kept
   };
   virtual bool has_cut_pass() const { return false; }
   virtual cpsel_status cut_pass(uint64_t /*r*/, bool /*dense*/, CutResult*) { return CPSEL_EINTERNAL; }
@@ -495,12 +496,12 @@ struct GpuBackend : Backend {
     *z_lo = r.z_lo; *z_hi = r.z_hi;
     return CPSEL_OK;
   }
-  bool kept_dense() const override { return last_dense; }
   bool init_compacted() const override { return init_seg_done; }
   uint64_t init_written() const override { return init_n_in; }
   void set_inexact() override { cur_exact = false; }
   bool has_cut_pass() const override { return use_mail && R > 0; }
   cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
+    dense = false;  // one GPU: the radix select reads the segmented copy directly (no atomics)
     CK(tic());
     // a bracket already cut once holds ~2% of x: 8192 samples cut it to ~4% of itself, below select_cap
     CK(launch_sample_select(dt, cur, n_cur, cur_seg ? cur_tab : nullptr, cur_side, seg_total_warps(dt, ctx->shape), r,
@@ -538,6 +539,7 @@ struct GpuBackend : Backend {
     const DevPass rr = ctx->mb->pass;
     o->ta = rr.pred; o->tb = rr.succ; o->t_est = rr.L_lo;
     o->le_a = rr.c_lt; o->inner = rr.z_lo;
+    o->overflow = rr.c_eq != 0;
     last_dense = dense;
     zlo = rr.z_lo; zhi = 0;
     return CPSEL_OK;
@@ -568,31 +570,36 @@ struct GpuBackend : Backend {
     n_cur = half_n(side);
     return CPSEL_OK;
   }
-  cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out) {
+  // tab != nullptr: the runs `side` of a segmented array based at `base`
+  cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out, const SegEntry* tab = nullptr,
+                         int side = 0) {
     CK(tic());
     if (use_mail) {
       const unsigned long long seq = ++ctx->seq;
       CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
-                             &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, seq));
+                             &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, seq, tab, side, ctx->d_ticket));
       CK(toc());
       cpsel_status w = wait_mail(&ctx->mb->seq_radix, seq);
       if (w != CPSEL_OK) return w;
       *out = ctx->mb->radix_value;
     } else {
-      CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream));
+      CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream, nullptr, nullptr, 0,
+                             tab, side, ctx->d_ticket));
       CK(toc());
       CK(cudaMemcpyAsync(ctx->h_radix, ctx->d_radix, sizeof(RadixState), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
       *out = ctx->h_radix->value;
     }
-    launches = dt == kF32 ? 7 : 13;
+    launches = dt == kF32 ? 3 : 6;
     scanned = m;
     return CPSEL_OK;
   }
-  // side 2 needs a contiguous current array; sides 0/1 a dense last compaction (driver guarantees)
+  // the radix select reads dense and segmented arrays alike
+  bool kept_dense() const override { return true; }
   cpsel_status select(int side, uint64_t r, double* out) override {
-    if (side == 2) return select_on(cur, n_cur, r, out);
-    return select_on(half_ptr(side), half_n(side), r, out);
+    if (side == 2) return cur_seg ? select_on(cur, n_cur, r, out, cur_tab, cur_side) : select_on(cur, n_cur, r, out);
+    if (last_dense) return select_on(half_ptr(side), half_n(side), r, out);
+    return select_on(ctx->d_sb[tgt], half_n(side), r, out, static_cast<const SegEntry*>(ctx->d_st[tgt]), side);
   }
 };
 
@@ -640,6 +647,8 @@ struct ShardedBackend : GpuBackend {
   ShardedBackend(cpsel_ctx* c, const void* x_, uint64_t n_local, int dt_) : GpuBackend(c, x_, n_local, dt_) {
     use_mail = false;  // the per-rank tuples are all-gathered from device memory
   }
+  // the final all-gather-v sends each rank's kept part as one contiguous block
+  bool kept_dense() const override { return last_dense; }
 
   // All-gather the per-rank init records and combine them in rank order (R17).
   cpsel_status gather_init() {
@@ -844,12 +853,14 @@ struct ShardedBackend : GpuBackend {
     CK(cudaStreamSynchronize(ctx->stream));
     o->ta = tc[0]; o->tb = tc[1]; o->t_est = tc[2];
     o->le_a = 0; o->inner = 0;
+    o->overflow = false;
     zlo_rank.assign(G, 0);
     zhi_rank.assign(G, 0);
     for (int q = 0; q < G; ++q) {
       const DevPass& rr = ctx->h_gather[q];
       o->le_a += rr.c_lt;
       o->inner += rr.z_lo;
+      o->overflow |= rr.c_eq != 0;
       zlo_rank[q] = rr.z_lo;
     }
     last_dense = dense;
@@ -966,6 +977,7 @@ struct HostBackend : Backend {
     cpsel_cut_stats c{};
     if (be->cut(be->user, r, &c) != 0) { msg = "cut callback failed"; return CPSEL_EINTERNAL; }
     o->ta = c.t_a; o->tb = c.t_b; o->t_est = c.t_est; o->le_a = c.le_a; o->inner = c.inner;
+    o->overflow = false;
     return CPSEL_OK;
   }
 };
@@ -1160,7 +1172,9 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
         be.has_cut_pass()) {
       const uint64_t m_before = m;
       Backend::CutResult cr{};
-      st = be.cut_pass(k - c_le_L, m <= dense_cap, &cr);
+      // dense output (selectable right away) when the expected copy (~2-4% of m) surely fits; a
+      // copy that overflows the dense buffer is dropped and the pass still counts exactly
+      st = be.cut_pass(k - c_le_L, m <= 8 * dense_cap, &cr);
       if (st != CPSEL_OK) return st;
       inf.launches += be.launches;
       inf.passes++;
@@ -1178,6 +1192,18 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       row.scanned = be.scanned;
       row.written = cr.inner;
       N_L = P_R = NAN;  // F is not tracked through sample cuts
+      if (le_a < k && k <= lt_b && cr.ta < cr.tb && cr.overflow) {
+        // the target is between the cuts but the copy was not kept: the bracket still shrinks
+        yL = cr.ta; yR = cr.tb; c_le_L = le_a; c_lt_R = lt_b; m = cr.inner;
+        row.interior = m;
+        if (trace && cfg.record_trace) trace->push_back(row);
+        exact = false;
+        be.set_inexact();
+        cuts_stalled = true;
+        t = (cr.t_est > yL && cr.t_est < yR) ? cr.t_est : 0.5 * yL + 0.5 * yR;
+        free_step = true;
+        continue;
+      }
       if (le_a < k && k <= lt_b && cr.ta < cr.tb) {  // the usual case: continue on the copy of ]t_a, t_b[
         yL = cr.ta; yR = cr.tb; c_le_L = le_a; c_lt_R = lt_b; m = cr.inner;
         // a sample that cannot split the bracket (e.g. one repeated value inside it) hands over to

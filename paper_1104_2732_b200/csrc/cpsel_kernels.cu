@@ -1109,70 +1109,6 @@ template <typename T> struct HistFn {
   __device__ __forceinline__ void scalar(T v, bool ok) { elem(v, ok); }
 };
 
-template <typename T>
-__global__ void __launch_bounds__(kBlock) hist_kernel(const T* z, uint64_t m, const RadixState* st,
-                                                      int shift, int bits, unsigned* hist) {
-  __shared__ unsigned sh[kBins];
-  for (int i = threadIdx.x; i < kBins; i += kBlock) sh[i] = 0;
-  __syncthreads();
-  HistFn<T> f;
-  f.sh = sh;
-  f.prefix = st->prefix;
-  f.mask = st->mask;
-  f.shift = shift;
-  f.dmask = (1u << bits) - 1u;
-  stream_array<T, 2>(z, m, f, blockIdx.x, gridDim.x);
-  __syncthreads();
-  for (int i = threadIdx.x; i < kBins; i += kBlock)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-// One CTA of 1024 threads: find the digit holding rank r, extend the prefix, clear hist.
-template <typename T>
-__global__ void __launch_bounds__(1024) pick_kernel(RadixState* st, unsigned* hist, int shift, int bits,
-                                                    int last, double* vout, unsigned long long* done,
-                                                    unsigned long long seq) {
-  __shared__ unsigned long long scan[1024];
-  const int tid = threadIdx.x;
-  const int nb = 1 << bits;  // <= 2048: two bins per thread
-  const unsigned h0 = (2 * tid < nb) ? hist[2 * tid] : 0u;
-  const unsigned h1 = (2 * tid + 1 < nb) ? hist[2 * tid + 1] : 0u;
-  scan[tid] = (unsigned long long)h0 + h1;
-  __syncthreads();
-  for (int off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
-    const unsigned long long v = tid >= off ? scan[tid - off] : 0ull;
-    __syncthreads();
-    scan[tid] += v;
-    __syncthreads();
-  }
-  const unsigned long long r = st->r;
-  const unsigned long long before = scan[tid] - h0 - h1;  // exclusive prefix of bin 2*tid
-  int digit = -1;
-  unsigned long long below = 0, cnt = 0;
-  if (before < r && r <= before + h0) { digit = 2 * tid; below = before; cnt = h0; }
-  else if (before + h0 < r && r <= before + h0 + h1) { digit = 2 * tid + 1; below = before + h0; cnt = h1; }
-  __syncthreads();
-  if (digit >= 0) {
-    const unsigned long long dmask = (unsigned long long)(nb - 1) << shift;
-    st->prefix |= (unsigned long long)digit << shift;
-    st->mask |= dmask;
-    st->r = r - below;
-    st->count = cnt;
-    if (last) {
-      st->key = st->prefix;
-      st->value = (sizeof(T) == 4) ? from_key_f32(st->prefix) : from_key_f64(st->prefix);
-      if (vout) *vout = st->value;
-      publish_done(done, seq);
-    }
-  }
-  if (2 * tid < kBins) hist[2 * tid] = 0u;
-  if (2 * tid + 1 < kBins) hist[2 * tid + 1] = 0u;
-}
-
-__global__ void radix_init_kernel(RadixState* st, unsigned long long r, unsigned long long m) {
-  st->prefix = 0; st->mask = 0; st->r = r; st->count = m; st->value = 0; st->key = 0;
-}
-
 template <typename T, int MODE> constexpr size_t pass_smem() { return MODE == kCompact ? compact_smem_bytes<T>() : 0; }
 
 template <typename T, int MODE>
@@ -1387,6 +1323,121 @@ __device__ __forceinline__ void seg_run(F& f, const T* __restrict__ p, uint64_t 
   if (v0 < nvec) seg_group<T, true>(f, xv, v0, nvec);
 }
 
+// ------------------------------------------------------------------------------------------
+// Step a5, one launch per digit: the histogram of the digit over the prefix class, then the last
+// CTA to finish picks the digit holding the rank, extends the prefix and clears the histogram
+// (no separate pick / init launches).  Input: contiguous z[0..m) or the runs `side` of a segmented
+// array (one warp per run, the segmented grid).
+struct RadixSegFn {
+  unsigned* sh;
+  unsigned long long prefix, mask;
+  int shift;
+  unsigned dmask;
+  template <typename T> __device__ __forceinline__ void elem(T v, int, int) {
+    const unsigned long long k = okey(v);
+    if ((k & mask) == prefix) atomicAdd(&sh[(unsigned)(k >> shift) & dmask], 1u);
+  }
+  __device__ __forceinline__ void begin() {}
+  __device__ __forceinline__ void end() {}
+};
+
+struct RadixArgs {
+  const void* z;
+  uint64_t m;
+  const SegEntry* tab;  // nullptr: contiguous
+  int side;
+  RadixState* st;
+  unsigned* hist;       // kBins global counters, zero between rounds
+  unsigned* ticket;
+  int shift, bits, first, last;
+  uint64_t r;           // the rank (1-based), taken by the first round
+  double* vout;
+  unsigned long long* done;
+  unsigned long long seq;
+};
+
+template <typename T, bool SEG>
+__global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
+  __shared__ unsigned sh[2048];
+  __shared__ unsigned long long s_prefix, s_mask;
+  __shared__ bool s_last;
+  __shared__ unsigned wsum[kWarps];
+  for (int i = threadIdx.x; i < 2048; i += kBlock) sh[i] = 0;
+  if (threadIdx.x == 0) {
+    s_prefix = a.first ? 0ull : a.st->prefix;
+    s_mask = a.first ? 0ull : a.st->mask;
+  }
+  __syncthreads();
+  RadixSegFn f;
+  f.sh = sh;
+  f.prefix = s_prefix;
+  f.mask = s_mask;
+  f.shift = a.shift;
+  f.dmask = (1u << a.bits) - 1u;
+  if (SEG) {
+    const uint64_t W = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    const SegEntry e = a.tab[W];
+    seg_run<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
+  } else {
+    HistFn<T> hf;
+    hf.sh = sh; hf.prefix = s_prefix; hf.mask = s_mask; hf.shift = a.shift; hf.dmask = f.dmask;
+    stream_array<T, 2>(static_cast<const T*>(a.z), a.m, hf, blockIdx.x, gridDim.x);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += kBlock)
+    if (sh[i]) atomicAdd(&a.hist[i], sh[i]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // the pick: 8 bins per thread, block scan of the thread totals
+  const int nb = 1 << a.bits;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned h[8];
+  unsigned tsum = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int b = threadIdx.x * 8 + j;
+    h[j] = b < nb ? __ldcg(&a.hist[b]) : 0u;
+    tsum += h[j];
+  }
+  unsigned incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  unsigned wbase = 0;
+  for (int q = 0; q < w; ++q) wbase += wsum[q];
+  const unsigned long long r = a.first ? a.r : a.st->r;
+  unsigned long long before = wbase + incl - tsum;  // exclusive prefix of this thread's first bin
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (before < r && r <= before + h[j]) {
+      const int digit = threadIdx.x * 8 + j;
+      const unsigned long long dmask = (unsigned long long)(nb - 1) << a.shift;
+      const unsigned long long prefix = s_prefix | ((unsigned long long)digit << a.shift);
+      a.st->prefix = prefix;
+      a.st->mask = s_mask | dmask;
+      a.st->r = r - before;
+      a.st->count = h[j];
+      if (a.last) {
+        a.st->key = prefix;
+        a.st->value = (sizeof(T) == 4) ? from_key_f32(prefix) : from_key_f64(prefix);
+        if (a.vout) *a.vout = a.st->value;
+        publish_done(a.done, a.seq);
+      }
+    }
+    before += h[j];
+  }
+  for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist[i] = 0u;
+  if (threadIdx.x == 0) *a.ticket = 0u;
+}
+
 template <typename T, bool INSIDE>
 __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
   using F = WarpSeg<T, INSIDE>;
@@ -1490,6 +1541,7 @@ template <typename T> struct WarpCut {
   T* out;
   uint64_t reg_lo;
   unsigned long long* cursors;
+  uint64_t z_cap;                  // dense output capacity: a group that would overflow it is not written
   __device__ __forceinline__ void elem(float v, int u, int idx) {
     asm("{\n\t.reg .pred pL, pI;\n\t"
         "setp.le.f32 pL, %2, %3;\n\t"
@@ -1530,14 +1582,18 @@ template <typename T> struct WarpCut {
       if (bits & (1u << j)) *sp++ = vals[j];
     __syncwarp();
     T* dst;
+    bool fits = true;
     if (dense) {
       unsigned long long b = 0;
       if (lane == 0) b = atomicAdd(&cursors[0], (unsigned long long)tot);
-      dst = out + __shfl_sync(FULL, b, 0);
+      b = __shfl_sync(FULL, b, 0);
+      fits = b + tot <= z_cap;  // else the cursor total reports the overflow and nothing is kept
+      dst = out + b;
     } else {
       dst = out + reg_lo + n_in;
     }
-    for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    if (fits)
+      for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
     n_in += tot;
     __syncwarp();
   }
@@ -1558,6 +1614,7 @@ __global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
   f.out = static_cast<T*>(a.out);
   f.reg_lo = W * a.R;
   f.cursors = a.cursors;
+  f.z_cap = a.z_cap;
   if (a.seg_in == nullptr) {
     using V = typename VecOf<T>::V;
     constexpr int VE = VecOf<T>::N;
@@ -1609,7 +1666,8 @@ __global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
   PassPartial tot;
   if (grid_finish(p, static_cast<PassPartial*>(a.partials), a.ticket, &tot, id) && threadIdx.x == 0) {
     DevPass r;
-    r.c_lt = tot.c_lt; r.c_eq = 0;
+    r.c_lt = tot.c_lt;
+    r.c_eq = (a.dense_out && tot.c_lo > a.z_cap) ? 1ull : 0ull;  // the dense copy overflowed: not kept
     r.c_lo = tot.c_lo; r.c_hi = 0;
     r.L_lo = (double)static_cast<const T*>(a.cuts)[2];  // the sample's estimate of x_(k)
     r.L_hi = 0; r.P = 0; r.N = 0;
@@ -2249,9 +2307,9 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
   s->grid_init[kF32] = s->num_sms * (b > 0 ? b : 1);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, init_kernel<double, 4, false, true>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_init[kF64] = s->num_sms * (b > 0 ? b : 1);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist_kernel<float>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, radix_round_kernel<float, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_hist[kF32] = s->num_sms * (b > 0 ? b : 1);
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, hist_kernel<double>, kBlock, 0)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, radix_round_kernel<double, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_hist[kF64] = s->num_sms * (b > 0 ? b : 1);
   return cudaSuccess;
 }
@@ -2396,24 +2454,27 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned* hist, const LaunchShape& s, cudaStream_t st, double* vout,
-                                unsigned long long* done, unsigned long long seq) {
-  radix_init_kernel<<<1, 1, 0, st>>>(state, r, m);
+                                unsigned long long* done, unsigned long long seq, const SegEntry* tab, int side,
+                                unsigned* ticket) {
   // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10
   static const int plan32[] = {21, 11, 10, 11, 0, 10};
   static const int plan64[] = {53, 11, 42, 11, 31, 11, 20, 11, 10, 10, 0, 10};
   const int rounds = dtype == kF32 ? 3 : 6;
   const int* plan = dtype == kF32 ? plan32 : plan64;
+  RadixArgs a{};
+  a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
+  a.r = r; a.vout = vout; a.done = done; a.seq = seq;
   for (int i = 0; i < rounds; ++i) {
-    const int shift = plan[2 * i], bits = plan[2 * i + 1];
-    const int last = (i == rounds - 1);
+    a.shift = plan[2 * i]; a.bits = plan[2 * i + 1];
+    a.first = i == 0; a.last = i == rounds - 1;
+    const int grid = tab ? s.grid_seg[dtype]
+                         : clamp_grid(s.grid_hist[dtype], m, kBlock * 2 * (dtype == kF32 ? 4 : 2));
     if (dtype == kF32) {
-      const int grid = clamp_grid(s.grid_hist[kF32], m, kBlock * 2 * 4);
-      hist_kernel<float><<<grid, kBlock, 0, st>>>(static_cast<const float*>(z), m, state, shift, bits, hist);
-      pick_kernel<float><<<1, 1024, 0, st>>>(state, hist, shift, bits, last, vout, done, seq);
+      if (tab) radix_round_kernel<float, true><<<grid, kBlock, 0, st>>>(a);
+      else radix_round_kernel<float, false><<<grid, kBlock, 0, st>>>(a);
     } else {
-      const int grid = clamp_grid(s.grid_hist[kF64], m, kBlock * 2 * 2);
-      hist_kernel<double><<<grid, kBlock, 0, st>>>(static_cast<const double*>(z), m, state, shift, bits, hist);
-      pick_kernel<double><<<1, 1024, 0, st>>>(state, hist, shift, bits, last, vout, done, seq);
+      if (tab) radix_round_kernel<double, true><<<grid, kBlock, 0, st>>>(a);
+      else radix_round_kernel<double, false><<<grid, kBlock, 0, st>>>(a);
     }
   }
   return cudaGetLastError();

@@ -158,8 +158,8 @@ cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, 
 // launch_cut_pass: one read of the current array (a.x / a.seg_in / a.side_in as for
 // launch_seg_pass, every element inside the bracket) at the two cuts a.cuts = {t_a, t_b}:
 // #x<=t_a, the copy_if of ]t_a, t_b[ (segmented run 0 of each warp region, or dense from z[0]) and
-// I = sum over it of (x - t_a).  Result tuple: c_lt = #x<=t_a, c_lo = z_lo = #]t_a,t_b[, L_lo = I,
-// pred = t_a, succ = t_b.
+// the sample estimate.  Result tuple: c_lt = #x<=t_a, c_lo = z_lo = #]t_a,t_b[, L_lo = estimate,
+// pred = t_a, succ = t_b, c_eq = 1 if a dense copy would not fit z_cap (then it is not kept).
 cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st);
 
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
@@ -173,10 +173,13 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 // On completion state->value holds the element (as double).
 // vout/done/seq (optional): the last round also writes the value to *vout (mapped host memory)
 // and then sets *done = seq.
+// tab != nullptr: the input is the runs `side` of the segmented array based at z (tab[0..Wtot),
+// the segmented grid).  One launch per digit (f32: 3, f64: 6); the last CTA of each picks the digit
+// (ticket: a self-resetting grid counter).
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned int* hist, const LaunchShape& s, cudaStream_t st,
-                                double* vout = nullptr, unsigned long long* done = nullptr,
-                                unsigned long long seq = 0);
+                                double* vout, unsigned long long* done, unsigned long long seq,
+                                const SegEntry* tab, int side, unsigned int* ticket);
 
 // Step a8: per-column k-th smallest of S (n x C column-major, float32), one CTA per column.
 struct BatchArgs {
