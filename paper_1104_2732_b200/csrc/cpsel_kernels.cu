@@ -2064,7 +2064,7 @@ __device__ __forceinline__ PassPartial batch_pass(BatchState& st, float* zbuf, u
   return block_reduce(p);
 }
 
-__global__ void __launch_bounds__(kBlock, 2) batched_select_kernel(BatchArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) {
   __shared__ BatchState st;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   float* sbuf = reinterpret_cast<float*>(dyn_smem);
