@@ -2009,14 +2009,14 @@ __device__ __forceinline__ float key_mid_dev(float yL, float yR) {
 }
 
 // ascending bitonic sort of S (power of 2) keys in shared memory, all threads of the CTA
-__device__ void block_bitonic_sort(unsigned long long* key, int S) {
+template <typename K> __device__ void block_bitonic_sort(K* key, int S) {
   for (int size = 2; size <= S; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
         const int lo = 2 * i - (i & (stride - 1));
         const int hi = lo + stride;
         const bool up = ((lo & size) == 0);
-        const unsigned long long x = key[lo], y = key[hi];
+        const K x = key[lo], y = key[hi];
         if ((x > y) == up) { key[lo] = y; key[hi] = x; }
       }
       __syncthreads();
@@ -2024,7 +2024,8 @@ __device__ void block_bitonic_sort(unsigned long long* key, int S) {
   }
 }
 
-constexpr int kBatchSample = 2048;   // samples of the init pass's extra cut (R23)
+constexpr int kBatchSample = 2048;   // samples of the init pass's extra cuts (R23; 32-bit keys)
+constexpr int kBatchCutSample = 1024;  // samples of a cut pass over the compacted bracket (R26)
 constexpr int kBatchFinish = 4096;   // kept halves this small are finished by a shared-memory sort
 
 struct BatchState {
@@ -2033,8 +2034,37 @@ struct BatchState {
   unsigned long long cursors[2];
   double t;
   float yL, yR, tq, result, cut_lo, cut_hi, cut_mid;
-  int col, on_z, slow, bisect, phase, compact, cur_buf, tgt, side, iters;
+  int col, on_z, slow, bisect, phase, compact, cur_buf, tgt, side, iters, exact, cuts_stalled, free_step;
 };
+
+// Sorted 32-bit keys of ms strided samples of z[0..m) (ms <= S, padding ~0), then the cuts of
+// local rank r (1-based) in st.cut_lo / cut_hi / cut_mid (thread 0).  Block-wide.
+template <int S>
+__device__ void batch_sample_cuts(BatchState& st, unsigned* keys, const float* z, uint64_t m, uint64_t r) {
+  const uint64_t ms = m < (uint64_t)S ? m : (uint64_t)S;
+  for (int i = threadIdx.x; i < S; i += kBlock) {
+    if ((uint64_t)i < ms) {
+      const uint64_t pos = (m == ms) ? (uint64_t)i : ((uint64_t)i * m) / ms + (m / ms) / 2;
+      keys[i] = (unsigned)okey(z[pos]);
+    } else {
+      keys[i] = ~0u;
+    }
+  }
+  __syncthreads();
+  block_bitonic_sort(keys, S);
+  if (threadIdx.x == 0) {
+    const double md = (double)ms;
+    const double q = ((double)r - 0.5) / (double)m * md;
+    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+    const double ql = floor(q - w), qh = ceil(q + w), qm = floor(q);
+    const uint64_t il = ql < 0 ? 0 : (uint64_t)ql;
+    const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
+    st.cut_lo = (float)from_key_f32(keys[il]);
+    st.cut_hi = (float)from_key_f32(keys[ih]);
+    st.cut_mid = (float)from_key_f32(keys[qm < 0 ? 0 : (qm >= md ? ms - 1 : (uint64_t)qm)]);
+  }
+  __syncthreads();
+}
 
 template <int MODE>
 __device__ __forceinline__ PassPartial batch_pass(BatchState& st, float* zbuf, uint64_t cap, float* sbuf) {
@@ -2080,34 +2110,10 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
     if (st.col >= (int)a.C) break;
     const float* x = a.S + (size_t)st.col * n;
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(dyn_smem);
-    // ---- R23: two extra cuts at sample quantiles bracketing rank k (strided samples, smem sort)
+    unsigned* keys32 = reinterpret_cast<unsigned*>(dyn_smem);
+    // ---- R23/R29: two extra cuts at quantiles of 8192 strided samples bracketing rank k
     const bool cut = n > 2;
-    if (cut) {
-      const uint64_t ms = n < (uint64_t)kBatchSample ? n : (uint64_t)kBatchSample;
-      for (int i = threadIdx.x; i < kBatchSample; i += kBlock) {
-        if ((uint64_t)i < ms) {
-          const uint64_t pos = (n == ms) ? (uint64_t)i : ((uint64_t)i * n) / ms + (n / ms) / 2;
-          keys[i] = okey(x[pos]);
-        } else {
-          keys[i] = ~0ull;
-        }
-      }
-      __syncthreads();
-      block_bitonic_sort(keys, kBatchSample);
-      if (threadIdx.x == 0) {
-        const double md = (double)ms;
-        const double q = ((double)k - 0.5) / (double)n * md;
-        const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
-        const double ql = floor(q - w), qh = ceil(q + w);
-        const uint64_t il = ql < 0 ? 0 : (uint64_t)ql;
-        const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
-        st.cut_lo = (float)from_key_f32(keys[il]);
-        st.cut_hi = (float)from_key_f32(keys[ih]);
-        const double qm = floor(q);
-        st.cut_mid = (float)from_key_f32(keys[qm < 0 ? 0 : (qm >= md ? ms - 1 : (uint64_t)qm)]);
-      }
-      __syncthreads();
-    }
+    if (cut) batch_sample_cuts<kBatchSample>(st, keys32, x, n, k);
     // ---- a1 + a4: init reduction over the column, the two extra cuts and the copy_if of
     //      ]t_lo, t_hi[ into this CTA's buffer 0, in one read (R23)
     {
@@ -2154,6 +2160,7 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
           st.c_le_L = 0; st.c_lt_R = n;
           st.m = n;
           st.D_lo = 0; st.on_z = 0; st.slow = 0; st.bisect = 0;
+          st.exact = 1; st.cuts_stalled = 0; st.free_step = 0;
           st.cur = x; st.n_cur = n; st.cur_buf = -1; st.tgt = 0;
           st.t = 0.5 * p.vmin + 0.5 * p.vmax;  // only used if neither cut lies strictly inside
           if (cut) {  // the two extra cuts, as the host driver applies them (R23-R25)
@@ -2199,6 +2206,66 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
     }
     // ---- a2/a3/a4: Kelley iterations
     while (st.phase == 0) {
+      // R26 cut step: a compacted bracket larger than the shared-memory finish is cut at two
+      // quantiles of 1024 samples of its own; only what lies between them is copied
+      if (st.on_z && st.exact && !st.cuts_stalled && !st.bisect && st.m > (unsigned long long)kBatchFinish) {
+        batch_sample_cuts<kBatchCutSample>(st, keys32, st.cur, st.n_cur, k - st.c_le_L);
+        if (threadIdx.x == 0) st.tgt = (st.cur_buf == 0) ? 1 : 0;
+        __syncthreads();
+        float* zbuf = st.tgt == 0 ? my0 : my1;
+        __shared__ CompactShared cs2;
+        BatchInitFn f;
+        f.mn = tinf<float>(); f.mx = -tinf<float>();
+        f.tl = st.cut_lo; f.th = st.cut_hi;
+        f.pc.cs = &cs2; f.pc.sbuf = sbuf; f.pc.z = zbuf; f.pc.z_cap = a.cap; f.pc.cursors = st.cursors;
+        __syncthreads();
+        stream_array<float, 4>(st.cur, st.n_cur, f, 0u, 1u);
+        f.pc.finish();
+        unsigned long long le_loc = (unsigned long long)f.fL;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) le_loc += __shfl_xor_sync(FULL, le_loc, o);
+        __shared__ unsigned long long le_w[kWarps];
+        if ((threadIdx.x & 31) == 0) le_w[threadIdx.x >> 5] = le_loc;
+        __syncthreads();  // (also: compaction cursor final)
+        if (threadIdx.x == 0) {
+          unsigned long long le_part = 0;
+          for (int q = 0; q < kWarps; ++q) le_part += le_w[q];
+          const unsigned long long written = st.cursors[0];
+          st.cursors[0] = st.cursors[1] = 0ull;
+          atomicAdd(&a.stats[0], 1ull);
+          atomicAdd(&a.stats[1], (unsigned long long)(4 * (st.n_cur + written)));
+          const unsigned long long le_a = st.c_le_L + le_part, lt_b = le_a + written;
+          const float ta = st.cut_lo, tb = st.cut_hi;
+          const unsigned long long m_old = st.m;
+          if (++st.iters > (int)a.max_iters) {
+            st.result = __int_as_float(0x7fc00000);
+            atomicAdd(&a.stats[2], 1ull);
+            st.phase = 1;
+          } else if (le_a < k && k <= lt_b && ta < tb) {  // continue on the copy of ]t_a, t_b[
+            st.yL = ta; st.yR = tb; st.c_le_L = le_a; st.c_lt_R = lt_b; st.m = written;
+            st.cur = zbuf; st.n_cur = written; st.cur_buf = st.tgt; st.D_lo = le_a; st.exact = 1;
+            if (st.m > m_old / 2) st.cuts_stalled = 1;
+            st.t = (st.cut_mid > ta && st.cut_mid < tb) ? (double)st.cut_mid : 0.5 * (double)ta + 0.5 * (double)tb;
+            st.free_step = 1;
+            if (st.m <= (unsigned long long)kBatchFinish) { st.k_r = k - st.c_le_L; st.phase = 2; }
+          } else {  // the target is outside: move to the adjacent float of the cut (R24)
+            if (k <= le_a) {
+              st.yR = nextafterf(ta, INFINITY); st.c_lt_R = le_a; st.m = le_a - st.c_le_L;
+            } else if (ta == tb) {
+              st.yL = ta; st.c_le_L = le_a; st.m = st.c_lt_R - le_a;
+            } else {
+              st.yL = nextafterf(tb, -INFINITY); st.c_le_L = lt_b; st.m = st.c_lt_R - lt_b;
+            }
+            st.exact = 0;
+            st.cuts_stalled = 1;
+            st.t = (st.cut_mid > st.yL && st.cut_mid < st.yR) ? (double)st.cut_mid
+                                                               : 0.5 * (double)st.yL + 0.5 * (double)st.yR;
+            st.free_step = 1;
+          }
+        }
+        __syncthreads();
+        continue;
+      }
       if (threadIdx.x == 0) {
         const double tt = st.bisect ? (double)key_mid_dev(st.yL, st.yR) : st.t;
         st.tq = snap_dev(tt, st.yL, st.yR);
@@ -2252,12 +2319,15 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
             st.cur_buf = st.tgt;
             st.D_lo = st.c_le_L;
             st.on_z = 1;
+            st.exact = 1;
             if (st.m <= (unsigned long long)kBatchFinish) {
               st.k_r = k - st.c_le_L;  // rank inside the kept half
               st.phase = 2;
             }
           }
-          if (st.m > m_old - m_old / 8) {
+          if (st.free_step) {
+            st.free_step = 0;
+          } else if (st.m > m_old - m_old / 8) {
             if (++st.slow >= 2) st.bisect = 1;
           } else {
             st.slow = 0;
