@@ -173,6 +173,15 @@ cpsel_status cpsel_lms_objective(cpsel_ctx* ctx, const float* d_X, const float* 
  * (x_i . theta_j - y_i)^2 computed on the tensor cores (tcgen05, 3xTF32 split). */
 cpsel_status cpsel_lms_residuals(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n,
                                  uint32_t p, const float* d_thetas, uint32_t C, float* d_S);
+/* LTS (NEXT row): d_out[j] (float64, device) = the sum of the h smallest squared
+ * residuals of candidate j, computed as sum_{s<m_j} s + (h - #{s<m_j}) m_j (the rho/a,b form of
+ * P:L464-478, every s = m_j equal to m_j) with m_j = the h-th smallest squared residual, written to
+ * d_m[j] (float32, device).  Same residual and batched-selection stages as cpsel_lms_objective,
+ * then one fp64-accumulated reduction over S.  1 <= h <= n (the paper's h = [(n+p)/2] or
+ * (n+1)/2 is the caller's choice, R20).  Host-blocking. */
+cpsel_status cpsel_lts_objective(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n,
+                                 uint32_t p, const float* d_thetas, uint32_t C, uint64_t h,
+                                 double* d_out, float* d_m, cpsel_info* info);
 /* Batched selection: for each column j of d_S (n x C column-major) the k-th smallest
  * -> d_out[j] (float32, device). */
 cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t n, uint32_t C,

@@ -110,6 +110,7 @@ SYMBOLS = [
     "cpsel_select_kth_host", "cpsel_lms_objective", "cpsel_lms_residuals", "cpsel_select_kth_batched",
     "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_nccl_unique_id",
     "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host", "cpsel_pooled_cuts",
+    "cpsel_lts_objective",
 ]
 
 _lib = None
@@ -157,6 +158,7 @@ def load():
             "cpsel_drive_host": (I, [C.POINTER(HostBackend), U64, I, U64, C.POINTER(Config), C.POINTER(D),
                                      C.POINTER(Info), C.POINTER(TraceRow), U32, C.POINTER(U32)]),
             "cpsel_pooled_cuts": (I, [P, P, U32, U64, I, C.POINTER(D)]),
+            "cpsel_lts_objective": (I, [P, P, P, U64, U32, P, U32, U64, P, P, C.POINTER(Info)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -389,6 +391,21 @@ def lms_residuals(X, y, thetas, out=None):
     _check(ctx, load().cpsel_lms_residuals(ctx.handle, C.c_void_p(X.data_ptr()), C.c_void_p(y.data_ptr()), n, p,
                                            C.c_void_p(thetas.data_ptr()), Cn, C.c_void_p(out.data_ptr())))
     return out
+
+
+def lts_objective(X, y, thetas, h: int, return_info: bool = False):
+    """LTS objective per candidate (NEXT row): the sum of the h smallest squared
+    residuals (float64) and the h-th smallest itself (float32), for every row theta_j of thetas."""
+    import torch
+    n, p, Cn = _check_lms(X, y, thetas)
+    ctx = _ctx_for(X)
+    out = torch.empty(Cn, device=X.device, dtype=torch.float64)
+    m = torch.empty(Cn, device=X.device, dtype=torch.float32)
+    info = Info()
+    _check(ctx, load().cpsel_lts_objective(ctx.handle, C.c_void_p(X.data_ptr()), C.c_void_p(y.data_ptr()), n, p,
+                                           C.c_void_p(thetas.data_ptr()), Cn, int(h), C.c_void_p(out.data_ptr()),
+                                           C.c_void_p(m.data_ptr()), C.byref(info)))
+    return (out, m, info.as_dict()) if return_info else (out, m)
 
 
 def select_kth_batched(S, k: int, return_info: bool = False):

@@ -1772,4 +1772,26 @@ cpsel_status cpsel_lms_objective(cpsel_ctx* ctx, const float* d_X, const float* 
   return s;
 }
 
+cpsel_status cpsel_lts_objective(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
+                                 const float* d_thetas, uint32_t C, uint64_t h, double* d_out, float* d_m,
+                                 cpsel_info* info) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!d_X || !d_y || !d_thetas || !d_out || !d_m) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (h < 1 || h > n) return fail(ctx, CPSEL_ERANK, "h outside [1,n]");
+  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
+  DeviceGuard g(ctx->device);
+  cpsel_status s = ensure(ctx, reinterpret_cast<void**>(&ctx->lms.S), &ctx->lms.S_bytes, (size_t)n * C * sizeof(float));
+  if (s != CPSEL_OK) return s;
+  float* d_S = ctx->lms.S;
+  const auto t0 = std::chrono::steady_clock::now();
+  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
+  s = cpsel_select_kth_batched(ctx, d_S, n, C, h, d_m, info);
+  if (s != CPSEL_OK) return s;
+  CK(lts_reduce(d_S, n, C, h, d_m, d_out, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (info) info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return CPSEL_OK;
+}
+
 }  // extern "C"

@@ -262,6 +262,70 @@ cudaError_t lms_residuals(LmsWorkspace& w, const float* X, const float* y, uint6
   return cudaGetLastError();
 }
 
+// LTS (NEXT row §8f-2): given m_j = the h-th smallest of column j of S,
+// F_j = sum_{s < m_j} s + (h - #{s < m_j}) * m_j  (= the sum of the h smallest squared residuals,
+// the rho/a,b form with every s = m_j equal to m_j).  One CTA per column (grid-stride), fp64
+// accumulation, fixed-order block reduction.
+__global__ void __launch_bounds__(256) lts_reduce_kernel(const float* __restrict__ S, uint64_t n, uint32_t C,
+                                                         uint64_t h, const float* __restrict__ m,
+                                                         double* __restrict__ out) {
+  __shared__ double ws[8];
+  __shared__ unsigned long long wc[8];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (uint32_t j = blockIdx.x; j < C; j += gridDim.x) {
+    const float mj = m[j];
+    const float* col = S + (size_t)j * n;
+    double acc = 0.0;
+    unsigned long long cnt = 0;
+    // 16-byte body (columns are 4-float aligned when n % 4 == 0; else scalar)
+    const bool vec = ((reinterpret_cast<uintptr_t>(col) & 15) == 0);
+    uint64_t i0 = 0;
+    if (vec) {
+      const float4* c4 = reinterpret_cast<const float4*>(col);
+      const uint64_t nv = n / 4;
+      for (uint64_t v = threadIdx.x; v < nv; v += blockDim.x) {
+        const float4 q = __ldcs(c4 + v);
+        unsigned c = 0;
+        if (q.x < mj) { acc += (double)q.x; ++c; }
+        if (q.y < mj) { acc += (double)q.y; ++c; }
+        if (q.z < mj) { acc += (double)q.z; ++c; }
+        if (q.w < mj) { acc += (double)q.w; ++c; }
+        cnt += c;
+      }
+      i0 = nv * 4;
+    }
+    for (uint64_t i = i0 + threadIdx.x; i < n; i += blockDim.x) {
+      const float v = col[i];
+      if (v < mj) { acc += (double)v; ++cnt; }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    }
+    if (lane == 0) { ws[w] = acc; wc[w] = cnt; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double a = 0.0;
+      unsigned long long c = 0;
+      for (int q = 0; q < 8; ++q) { a += ws[q]; c += wc[q]; }
+      out[j] = a + (double)(h - c) * (double)mj;
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t lts_reduce(const float* S, uint64_t n, uint32_t C, uint64_t h, const float* m, double* out,
+                       cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = sms * 8;
+  if ((uint32_t)grid > C) grid = (int)C;
+  lts_reduce_kernel<<<grid, 256, 0, st>>>(S, n, C, h, m, out);
+  return cudaGetLastError();
+}
+
 cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t C, uint64_t k, float* out,
                            uint32_t max_iters, LmsReport* rep, cudaStream_t st) {
   int dev = 0, sms = 148;

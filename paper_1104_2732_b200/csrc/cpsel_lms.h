@@ -31,6 +31,9 @@ cudaError_t lms_residuals(LmsWorkspace& w, const float* X, const float* y, uint6
 // cudaErrorNotSupported if the iteration cap is reached.
 cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t C, uint64_t k, float* out,
                            uint32_t max_iters, LmsReport* rep, cudaStream_t st);
+// LTS objective per column from its h-th order statistic m[j] (fp64 out).
+cudaError_t lts_reduce(const float* S, uint64_t n, uint32_t C, uint64_t h, const float* m, double* out,
+                       cudaStream_t st);
 void lms_free(LmsWorkspace& w);
 
 }  // namespace cpsel

@@ -114,3 +114,22 @@ def test_lms_config4_full_size(cp):
     torch.cuda.empty_cache()
     # candidates with the smallest perturbations (sigma ~ 1e-3) fit far better than sigma ~ 1
     assert got[:64].max() < got[-64:].min()
+
+
+@pytest.mark.parametrize("h_rule", ["half", "n_plus_p"])
+def test_lts_objective_vs_oracle(cp, h_rule):
+    """NEXT row LTS: per candidate the sum of the h smallest squared residuals of the GPU's own S
+    (oracle rho/a,b form, fp64) within fp64 rounding, and the h-th smallest bit-exact; and the
+    true theta* fits far better than the sigma ~ 1 candidates."""
+    X, y, th, theta_star = datagen.lms_problem(n=100_003, p=10, C=300)
+    n, p = X.shape
+    h = (n + 1) // 2 if h_rule == "half" else (n + p) // 2      # R20: both readings
+    Xd, yd, thd = dev(X), dev(y), dev(th)
+    F, m = cp.lts_objective(Xd, yd, thd, h)
+    F, m = F.cpu().numpy(), m.cpu().numpy()
+    S = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+    for j in range(0, 300, 11):
+        assert m[j] == O.order_statistic(S[j], h)
+        ref = O.lts_objective(S[j].astype(np.float64), h)
+        assert F[j] == pytest.approx(ref, rel=1e-11), (j, F[j], ref)   # fp64 sums, different order
+    assert F[:16].max() < F[-16:].min()
