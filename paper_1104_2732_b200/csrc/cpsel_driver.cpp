@@ -344,7 +344,8 @@ struct GpuBackend : Backend {
     CK(tic());
     sample_slot = -1;
     if (cut && !presampled) {
-      CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream));
+      CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream,
+                              /*small=*/n <= (1ull << 26)));
       CK(toc());
       sample_slot = slot;
       CK(tic());
@@ -402,7 +403,9 @@ struct GpuBackend : Backend {
     return CPSEL_OK;
   }
   cpsel_status init(cpsel_init_stats* o, uint64_t k) override {
-    cpsel_status st = run_init(true, k, ctx->cfg.init_cut != 0 && n > 2);
+    // (an array the driver selects directly gets the plain init: the cuts would not be used)
+    cpsel_status st = run_init(true, k, ctx->cfg.init_cut != 0 && n > 2 &&
+                                            (n > ctx->cfg.direct_threshold || ctx->cfg.force_cp));
     if (st != CPSEL_OK) return st;
     const DevInit& r = *ctx->h_init;
     o->vmin = r.vmin; o->vmax = r.vmax; o->cnt_min = r.cnt_min; o->cnt_max = r.cnt_max;
@@ -1156,6 +1159,12 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       inf.init_written = m;
       D_lo = c_le_L;
       on_z = true;
+      if (m <= select_cap && be.kept_dense()) {  // the init's copy is already small: select in it
+        double v;
+        st = do_select(2, k - c_le_L, &v);
+        if (st != CPSEL_OK) return st;
+        return done(v, 5);
+      }
     }
   }
   for (uint32_t it = 1;; ++it) {

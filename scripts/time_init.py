@@ -13,7 +13,8 @@ import paper_1104_2732_b200 as cp  # noqa: E402
 dist = sys.argv[1] if len(sys.argv) > 1 else "uniform"
 lg = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 sharded = len(sys.argv) > 3 and sys.argv[3] == "sharded"  # the NCCL path at world size 1
-x = datagen.make(dist, 1 << lg, "f32", device="cuda")
+dtype = "f64" if "f64" in sys.argv else "f32"
+x = datagen.make(dist, 1 << lg, dtype, device="cuda")
 torch.cuda.synchronize()
 cp.set_config(record_timing=1)
 if sharded:
@@ -37,6 +38,6 @@ for _ in range(20):
     tot.append(info["ms_total"]); passes.append(info["passes"]); smp.append(info["kernel_ms_sample"])
 m = lambda a: sum(a) / len(a)  # noqa: E731
 k = m(ini) + m(pas) + m(sel) + m(smp)
-print(f"{dist} 2^{lg}{' sharded' if sharded else ''}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  "
+print(f"{dist} 2^{lg} {dtype}{' sharded' if sharded else ''}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  "
       f"sample {m(smp):.4f}  kernels {k:.4f}  "
       f"driver wall {m(tot):.4f}  python wall {m(wall):.4f} ms  passes/call {m(passes):.1f}")
