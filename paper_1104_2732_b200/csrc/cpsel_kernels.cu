@@ -1876,13 +1876,22 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   {
     __shared__ __align__(16) T stage_all[kWarps * F::GW];
     f.stage = stage_all + (size_t)w * F::GW;
-    for (uint64_t g = W; g < nfull; g += Wtot) {
-      V v[kSegU];
+    // software pipelined: the next group's loads are issued once the current group's values sit in
+    // f.vals, so they are in flight during its scan / staging / copy-out
+    V v[kSegU];
+    if (W < nfull) {
 #pragma unroll
-      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + g * GV + (uint64_t)u * 32 + lane);
+      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + W * GV + (uint64_t)u * 32 + lane);
+    }
+    for (uint64_t g = W; g < nfull; g += Wtot) {
       f.begin();
 #pragma unroll
       for (int u = 0; u < kSegU; ++u) f.vec(v[u], u);
+      const uint64_t gn = g + Wtot;
+      if (gn < nfull) {
+#pragma unroll
+        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + gn * GV + (uint64_t)u * 32 + lane);
+      }
       f.end(F::G);
     }
   }
