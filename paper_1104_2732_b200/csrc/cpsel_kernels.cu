@@ -1793,11 +1793,22 @@ template <typename T, bool SUMS> struct InitSeg {
   }
   __device__ __forceinline__ void extremes(int nvalid) {
     T lo = nvalid > 0 ? vals[0] : tinf<T>(), hi = nvalid > 0 ? vals[0] : -tinf<T>();
+    bool bad = false;  // f64: fmin/fmax drop NaNs, so they are flagged separately
+    if (sizeof(T) == 8 && nvalid > 0) bad = vals[0] != vals[0];
 #pragma unroll
     for (int j = 1; j < G; ++j)
-      if (j < nvalid) { lo = nan_min(lo, vals[j]); hi = nan_max(hi, vals[j]); }
-    const bool need = !(lo >= mn) || !(hi <= mx);  // a new extreme, or a NaN
-    if (__any_sync(FULL, need)) slow_group(nvalid, lo, hi);
+      if (j < nvalid) {
+        if (sizeof(T) == 4) {
+          lo = nan_min(lo, vals[j]);
+          hi = nan_max(hi, vals[j]);
+        } else {
+          lo = (T)fmin((double)lo, (double)vals[j]);
+          hi = (T)fmax((double)hi, (double)vals[j]);
+          bad |= vals[j] != vals[j];
+        }
+      }
+    const bool need = !(lo >= mn) || !(hi <= mx) || bad;  // a new extreme, or a NaN
+    if (__any_sync(FULL, need)) slow_group(nvalid, bad ? (T)NAN : lo, hi);
   }
   __device__ __forceinline__ void slow_group(int nvalid, T lo, T hi) {
     if (__any_sync(FULL, lo != lo || hi != hi)) {  // NaNs: count them, extremes over the rest

@@ -335,6 +335,20 @@ def test_fused_init_extreme_ranks(cp, case):
         assert cp.select_kth(xd, k) == srt[k - 1], (case, k)
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_fused_init_rejects_nonfinite(cp, dtype, bad):
+    """The fused init pass at a size with segmented buffers: one NaN / +-Inf anywhere is rejected
+    (ENONFINITE, R12) — NaNs are caught by the extremes' vote, +-Inf by the extremes themselves."""
+    n = (1 << 22) + 3
+    x = datagen.make("normal", n, dtype)
+    x[n // 3] = bad
+    with pytest.raises(ValueError):
+        cp.median(tdev(x))
+    x[n // 3] = 0.5
+    assert cp.median(tdev(x)) == float(np.sort(x)[(n + 1) // 2 - 1])
+
+
 def test_host_buffer_path(cp):
     import torch
     x = datagen.make("normal", 3_000_001, "f32")
