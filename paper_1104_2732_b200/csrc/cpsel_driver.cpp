@@ -41,6 +41,7 @@ struct cpsel_ctx {
   DevInit* d_init = nullptr;
   void* d_t0 = nullptr;              // the two extra cuts of the init pass (R23)
   void* d_skeys = nullptr;           // gathered sample keys (R29)
+  ChainState* d_chain = nullptr;     // device chain state (§8f-3)
   RadixState* d_radix = nullptr;
   unsigned int* d_hist = nullptr;
   DevPass* d_gather = nullptr;       // G x DevPass (sharded)
@@ -84,6 +85,7 @@ struct cpsel_ctx {
     DevInit init;
     double radix_value;
     unsigned long long seq_pass, seq_init, seq_radix;
+    ChainMail chain;  // the device chain's step decisions (§8f-3)
   };
   Mailbox* mb = nullptr;      // host view
   Mailbox* mb_dev = nullptr;  // device view of the same memory
@@ -269,6 +271,15 @@ struct GpuBackend : Backend {
   uint64_t init_n_in = 0;
   unsigned long long mail_seq = 0;
   bool cur_exact = true;     // a compacted current array holds exactly the bracket interior
+  // the device chain (§8f-3): with the fused init the usual continuation (a cut pass on the init's
+  // copy, the radix select of its copy) is launched right behind the init; the driver's requests
+  // take those results when they ask for exactly those steps
+  struct Spec {
+    bool active = false, cut_used = false, small = false;
+    unsigned long long seq_c0 = 0, seq_cut = 0, seq_c1 = 0, seq_radix = 0;
+    int sample_slot = -1, cut_slot = -1, radix_slot = -1;
+  } spec;
+  uint64_t chain_select_cap = 0;  // 0: no device chain
   GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
       : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
@@ -350,16 +361,31 @@ struct GpuBackend : Backend {
       sample_slot = slot;
       CK(tic());
     }
+    // the device chain (§8f-3) when its continuation is likely: the init's copy (~1-4% of n) will
+    // exceed the exact-selection cap
+    spec = Spec{};
+    const bool chain = fuse && use_mail && !presampled && chain_select_cap > 0 && ctx->cfg.pass_cuts &&
+                       !ctx->cfg.objective && n / 100 > chain_select_cap;
     if (fuse) {
       SegArgs sa{};
       sa.out = ctx->d_sb[0];
       sa.R = R;
       sa.seg_out = static_cast<SegEntry*>(ctx->d_st[0]);
+      if (chain) {
+        a.chain = ctx->d_chain;
+        a.chain_mail = &ctx->mb_dev->chain;
+        a.chain_seq = spec.seq_c0 = ++ctx->seq;
+        a.chain_k = k;
+        a.chain_cap = chain_select_cap;
+      }
       CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
     }
     CK(toc());
+    const int init_slot_ = slot;
+    if (chain) CK(launch_chain(k));
+    slot = init_slot_;
     launches = cut ? 2 : 1;
     scanned = n;
     if (use_mail) {
@@ -400,6 +426,60 @@ struct GpuBackend : Backend {
         CK(cudaStreamSynchronize(ctx->stream));
       }
     }
+    return CPSEL_OK;
+  }
+  // launch the usual continuation behind the init (kernels read m, r and go/no-go from the chain)
+  cudaError_t launch_chain(uint64_t k) {
+    cudaError_t e;
+    spec.active = true;
+    spec.small = true;  // the init's copy holds ~2% of n (the driver's own choice is checked on use)
+    const int W = seg_total_warps(dt, ctx->shape);
+    if ((e = tic()) != cudaSuccess) return e;
+    if ((e = launch_sample_select(dt, ctx->d_sb[0], 0, static_cast<const SegEntry*>(ctx->d_st[0]), 0, W, 0, ctx->d_t0,
+                                  ctx->d_skeys, ctx->stream, spec.small, ctx->d_chain, 0)) != cudaSuccess) return e;
+    if ((e = toc()) != cudaSuccess) return e;
+    spec.sample_slot = slot;
+    SegArgs a{};
+    a.x = ctx->d_sb[0]; a.n = 0;
+    a.seg_in = static_cast<const SegEntry*>(ctx->d_st[0]);
+    a.side_in = 0;
+    a.cuts = ctx->d_t0;
+    a.dense_out = 0;
+    a.out = ctx->d_sb[1];
+    a.R = R;
+    a.seg_out = static_cast<SegEntry*>(ctx->d_st[1]);
+    a.cursors = ctx->d_cursors;
+    a.partials = ctx->d_partials; a.ticket = ctx->d_ticket;
+    a.out_tuple = &ctx->mb_dev->pass;
+    a.done = &ctx->mb_dev->seq_pass;
+    a.seq = spec.seq_cut = ++ctx->seq;
+    a.chain = ctx->d_chain;
+    a.chain_out = ctx->d_chain;
+    a.chain_mail = &ctx->mb_dev->chain;
+    a.chain_seq = spec.seq_c1 = ++ctx->seq;
+    a.chain_k = k;
+    a.chain_cap = chain_select_cap;
+    if ((e = tic()) != cudaSuccess) return e;
+    if ((e = launch_cut_pass(dt, a, ctx->shape, ctx->stream)) != cudaSuccess) return e;
+    if ((e = toc()) != cudaSuccess) return e;
+    spec.cut_slot = slot;
+    spec.seq_radix = ++ctx->seq;
+    if ((e = tic()) != cudaSuccess) return e;
+    if ((e = launch_radix_select(dt, ctx->d_sb[1], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
+                                 &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
+                                 static_cast<const SegEntry*>(ctx->d_st[1]), 0, ctx->d_ticket, ctx->d_chain)) != cudaSuccess)
+      return e;
+    if ((e = toc()) != cudaSuccess) return e;
+    spec.radix_slot = slot;
+    return cudaSuccess;
+  }
+  // the chain's decision `which` (0: after the init, 1: after the cut pass), once published
+  cpsel_status chain_decision(int which, unsigned long long seq, bool* ok, uint64_t* m, uint64_t* r) {
+    cpsel_status w = wait_mail(&ctx->mb->chain.seq[which], seq);
+    if (w != CPSEL_OK) return w;
+    *ok = ctx->mb->chain.ok[which] != 0;
+    *m = ctx->mb->chain.m[which];
+    *r = ctx->mb->chain.r[which];
     return CPSEL_OK;
   }
   cpsel_status init(cpsel_init_stats* o, uint64_t k) override {
@@ -505,6 +585,30 @@ struct GpuBackend : Backend {
   bool has_cut_pass() const override { return use_mail && R > 0; }
   cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
     dense = false;  // one GPU: the radix select reads the segmented copy directly (no atomics)
+    if (spec.active && !spec.cut_used && cur_seg && cur_sbuf == 0 && cur == ctx->d_sb[0]) {
+      bool ok;
+      uint64_t cm, cr;
+      cpsel_status w = chain_decision(0, spec.seq_c0, &ok, &cm, &cr);
+      if (w != CPSEL_OK) return w;
+      if (ok && cr == r && cm == n_cur && spec.small == (n_cur <= (1ull << 26))) {  // the chain ran this pass
+        w = wait_mail(&ctx->mb->seq_pass, spec.seq_cut);
+        if (w != CPSEL_OK) return w;
+        const DevPass rr = ctx->mb->pass;
+        o->ta = rr.pred; o->tb = rr.succ; o->t_est = rr.L_lo;
+        o->le_a = rr.c_lt; o->inner = rr.z_lo;
+        o->overflow = rr.c_eq != 0;
+        tgt = 1;
+        last_dense = false;
+        zlo = rr.z_lo; zhi = 0;
+        launches = 3;
+        scanned = n_cur;
+        slot = spec.cut_slot;
+        sample_slot = spec.sample_slot;
+        spec.cut_used = true;
+        return CPSEL_OK;
+      }
+      spec.active = false;
+    }
     CK(tic());
     // a bracket already cut once holds ~2% of x: 8192 samples cut it to ~4% of itself, below select_cap
     CK(launch_sample_select(dt, cur, n_cur, cur_seg ? cur_tab : nullptr, cur_side, seg_total_warps(dt, ctx->shape), r,
@@ -600,6 +704,22 @@ struct GpuBackend : Backend {
   // the radix select reads dense and segmented arrays alike
   bool kept_dense() const override { return true; }
   cpsel_status select(int side, uint64_t r, double* out) override {
+    if (spec.active && spec.cut_used && side == 0 && !last_dense && tgt == 1) {
+      bool ok;
+      uint64_t cm, cr;
+      cpsel_status w = chain_decision(1, spec.seq_c1, &ok, &cm, &cr);
+      if (w != CPSEL_OK) return w;
+      spec.active = false;
+      if (ok && cr == r && cm == half_n(0)) {  // the chain ran this select
+        w = wait_mail(&ctx->mb->seq_radix, spec.seq_radix);
+        if (w != CPSEL_OK) return w;
+        *out = ctx->mb->radix_value;
+        launches = dt == kF32 ? 4 : 7;  // + the chain step kernels
+        scanned = cm;
+        slot = spec.radix_slot;
+        return CPSEL_OK;
+      }
+    }
     if (side == 2) return cur_seg ? select_on(cur, n_cur, r, out, cur_tab, cur_side) : select_on(cur, n_cur, r, out);
     if (last_dense) return select_on(half_ptr(side), half_n(side), r, out);
     return select_on(ctx->d_sb[tgt], half_n(side), r, out, static_cast<const SegEntry*>(ctx->d_st[tgt]), side);
@@ -1390,6 +1510,7 @@ void store_value(double v, cpsel_dtype dt, void* h_out) {
 cpsel_status run_single(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k, void* h_out,
                         cpsel_info* info) {
   GpuBackend be(ctx, d_x, n, (int)dtype);
+  be.chain_select_cap = auto_select_cap(ctx->cfg);
   const uint64_t zc = auto_z_cap(n, ctx->cfg);
   cpsel_status s = CPSEL_OK;
   if (n > ctx->cfg.direct_threshold || ctx->cfg.force_cp)
@@ -1472,6 +1593,7 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMalloc(&ctx->d_init, sizeof(DevInit)));
   CKC(cudaMalloc(&ctx->d_t0, 32));  // t_lo, t_hi, the sample estimate
   CKC(cudaMalloc(&ctx->d_skeys, kSampleKeyBytes));
+  CKC(cudaMalloc(&ctx->d_chain, sizeof(ChainState)));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
   CKC(cudaMalloc(&ctx->d_hist, 2048 * sizeof(unsigned)));
   CKC(cudaMemset(ctx->d_hist, 0, 2048 * sizeof(unsigned)));
@@ -1493,7 +1615,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
-    void* dev[] = {ctx->d_t0, ctx->d_skeys, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
+    void* dev[] = {ctx->d_t0, ctx->d_skeys, ctx->d_chain, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
                    ctx->d_keys, ctx->d_keys_all, ctx->d_sizes,
                    ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};

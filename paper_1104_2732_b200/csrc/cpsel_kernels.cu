@@ -592,10 +592,15 @@ constexpr int kGatherThreads = 256;
 template <typename T, int KPT>
 __global__ void __launch_bounds__(kGatherThreads) sample_gather_kernel(const T* __restrict__ x, uint64_t m,
                                                              const SegEntry* __restrict__ tab, int side, int Wtot,
-                                                             typename SampleKey<T>::K* __restrict__ keys) {
+                                                             typename SampleKey<T>::K* __restrict__ keys,
+                                                             const ChainState* chain, int which) {
   using SK = SampleKey<T>;
   using K = typename SK::K;
   constexpr uint64_t S = 1024ull * KPT;
+  if (chain) {  // a device-chain step: size from the chain, nothing to do unless the chain holds
+    if (!chain->ok[which]) return;
+    m = chain->m[which];
+  }
   __shared__ unsigned long long pre[kGatherMaxWarps];  // inclusive prefix of the run lengths
   __shared__ unsigned long long wsum[32];
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
@@ -656,9 +661,15 @@ __global__ void __launch_bounds__(kGatherThreads) sample_gather_kernel(const T* 
 // sample) by MSB radix select of all three at once (11-bit digits, smem histograms) — no sort.
 template <typename T, int KPT>
 __global__ void __launch_bounds__(1024) sample_select_kernel(const typename SampleKey<T>::K* __restrict__ keys_in,
-                                                             uint64_t m, uint64_t r, T* t0) {
+                                                             uint64_t m, uint64_t r, T* t0, const ChainState* chain,
+                                                             int which) {
   using SK = SampleKey<T>;
   using K = typename SK::K;
+  if (chain) {
+    if (!chain->ok[which]) return;
+    m = chain->m[which];
+    r = chain->r[which];
+  }
   constexpr uint64_t S = 1024ull * KPT;
   __shared__ SampleSel sh;
   const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
@@ -1351,6 +1362,7 @@ struct RadixArgs {
   unsigned* ticket;
   int shift, bits, first, last;
   uint64_t r;           // the rank (1-based), taken by the first round
+  const ChainState* chain;  // device chain: skip unless chain->ok[1]; rank chain->r[1]
   double* vout;
   unsigned long long* done;
   unsigned long long seq;
@@ -1358,6 +1370,10 @@ struct RadixArgs {
 
 template <typename T, bool SEG>
 __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
+  if (a.chain) {
+    if (!a.chain->ok[1]) return;
+    a.r = a.chain->r[1];
+  }
   __shared__ unsigned sh[2048];
   __shared__ unsigned long long s_prefix, s_mask;
   __shared__ bool s_last;
@@ -1523,6 +1539,47 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
 }
 
 // ------------------------------------------------------------------------------------------
+// The device chain's decisions (§8f-3), taken by the finishing thread of the init / cut pass.
+// Step 0 (after the init): the usual path holds if the init compacted ]t_lo, t_hi[, saw no
+// NaN/Inf, both cuts lie inside ]prev(min), next(max)[, differ and bracket rank k, and the copy is
+// too large for the exact selection — then the chain's cut pass cuts the copy around rank
+// k - #x<=t_lo.  Step 1 (after that cut pass): the target lies between its cuts, which differ, and
+// the copy is small enough for the radix select.  Each decision also goes to the host (mapped).
+template <typename T> __device__ __forceinline__ T nextafter_t(T v, bool up);
+template <> __device__ __forceinline__ float nextafter_t(float v, bool up) { return nextafterf(v, up ? INFINITY : -INFINITY); }
+template <> __device__ __forceinline__ double nextafter_t(double v, bool up) {
+  return ::nextafter(v, up ? (double)INFINITY : -(double)INFINITY);
+}
+template <typename T>
+__device__ void chain_decide0(const DevInit& r, uint64_t k, uint64_t cap, ChainState* cs, ChainMail* mail,
+                              unsigned long long seq) {
+  const double lo_out = (double)nextafter_t<T>((T)r.vmin, false), hi_out = (double)nextafter_t<T>((T)r.vmax, true);
+  const uint64_t written = r.pad;
+  const bool ok = (r.has_cut & 1) && r.nonfinite == 0 && isfinite(r.vmin) && isfinite(r.vmax) && isfinite(lo_out) &&
+                  isfinite(hi_out) && isfinite(r.t_est) && r.t_lo > lo_out && r.t_hi < hi_out && r.t_lo < r.t_hi &&
+                  r.c_le_lo < k && r.c_lt_hi >= k && written == r.c_lt_hi - r.c_le_lo && written > cap;
+  cs->ok[0] = ok ? 1ull : 0ull;
+  cs->m[0] = written;
+  cs->r[0] = k - r.c_le_lo;
+  cs->le_base = r.c_le_lo;
+  cs->ok[1] = 0;
+  mail->ok[0] = cs->ok[0]; mail->m[0] = cs->m[0]; mail->r[0] = cs->r[0];
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned long long*>(&mail->seq[0]) = seq;
+}
+__device__ void chain_decide1(const DevPass& p, uint64_t k, uint64_t cap, ChainState* cs, ChainMail* mail,
+                              unsigned long long seq) {
+  const uint64_t le_a = cs->le_base + p.c_lt, inner = p.z_lo, lt_b = le_a + inner;
+  const bool ok = cs->ok[0] && le_a < k && k <= lt_b && p.pred < p.succ && p.c_eq == 0 && inner <= cap;
+  cs->ok[1] = ok ? 1ull : 0ull;
+  cs->m[1] = inner;
+  cs->r[1] = k - le_a;
+  mail->ok[1] = cs->ok[1]; mail->m[1] = cs->m[1]; mail->r[1] = cs->r[1];
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned long long*>(&mail->seq[1]) = seq;
+}
+
+// ------------------------------------------------------------------------------------------
 // R26: the cut pass — two sample cuts t_a <= t_b of the current (compacted) array evaluated in one
 // read, with the copy_if of ]t_a, t_b[ (multi-point Kelley).  Every input element
 // lies inside the bracket, so the element step is the init pass's cut step without the extremes:
@@ -1602,6 +1659,7 @@ template <typename T> struct WarpCut {
 template <typename T>
 __global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
   using F = WarpCut<T>;
+  if (a.chain && !a.chain->ok[0]) return;  // a device-chain step whose chain did not hold
   __shared__ __align__(16) T stage_all[kWarps * F::GW];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
@@ -1676,6 +1734,7 @@ __global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
     if (a.dense_out) a.cursors[0] = 0ull;
     *a.out_tuple = r;
     publish_done(a.done, a.seq);
+    if (a.chain_out) chain_decide1(r, a.chain_k, a.chain_cap, a.chain_out, a.chain_mail, a.chain_seq);
   }
 }
 
@@ -1972,6 +2031,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.has_cut = SUMS ? 15ull : 11ull;  // two cuts + the interior compacted (+ N_lo, P_hi), no #min/#max
     *ia.out = r;
     publish_done(ia.done, ia.seq);
+    if (ia.chain) chain_decide0<T>(r, ia.chain_k, ia.chain_cap, ia.chain, ia.chain_mail, ia.chain_seq);
   }
 }
 
@@ -2505,23 +2565,26 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 
 template <typename T, int KPT>
 cudaError_t sample_select_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
-                            void* keys, cudaStream_t st) {
+                            void* keys, cudaStream_t st, const ChainState* chain, int which) {
   auto* kk = static_cast<typename SampleKey<T>::K*>(keys);
   sample_gather_kernel<T, KPT><<<KPT * 1024 / kGatherThreads, kGatherThreads, 0, st>>>(static_cast<const T*>(x), m, tab,
-                                                                                       side, Wtot, kk);
-  sample_select_kernel<T, KPT><<<1, 1024, 0, st>>>(kk, m, r, static_cast<T*>(t0));
+                                                                                       side, Wtot, kk, chain, which);
+  sample_select_kernel<T, KPT><<<1, 1024, 0, st>>>(kk, m, r, static_cast<T*>(t0), chain, which);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
-                                 uint64_t r, void* t0, void* keys, cudaStream_t st, bool small) {
+                                 uint64_t r, void* t0, void* keys, cudaStream_t st, bool small,
+                                 const ChainState* chain, int which) {
   if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
   if (dtype == kF32)
-    return small ? sample_select_t<float, 8>(x, m, tab, side, Wtot, r, t0, keys, st)
-                 : sample_select_t<float, SampleKey<float>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st);
-  return small ? sample_select_t<double, 4>(x, m, tab, side, Wtot, r, t0, keys, st)
-               : sample_select_t<double, SampleKey<double>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st);
+    return small ? sample_select_t<float, 8>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which)
+                 : sample_select_t<float, SampleKey<float>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which);
+  return small ? sample_select_t<double, 4>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which)
+               : sample_select_t<double, SampleKey<double>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which);
 }
+
+
 
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
                               uint64_t r, void* t0, cudaStream_t st, uint32_t smax, unsigned long long* keys_out) {
@@ -2545,7 +2608,7 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned* hist, const LaunchShape& s, cudaStream_t st, double* vout,
                                 unsigned long long* done, unsigned long long seq, const SegEntry* tab, int side,
-                                unsigned* ticket) {
+                                unsigned* ticket, const ChainState* chain) {
   // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10
   static const int plan32[] = {21, 11, 10, 11, 0, 10};
   static const int plan64[] = {53, 11, 42, 11, 31, 11, 20, 11, 10, 10, 0, 10};
@@ -2553,7 +2616,7 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   const int* plan = dtype == kF32 ? plan32 : plan64;
   RadixArgs a{};
   a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
-  a.r = r; a.vout = vout; a.done = done; a.seq = seq;
+  a.r = r; a.vout = vout; a.done = done; a.seq = seq; a.chain = chain;
   for (int i = 0; i < rounds; ++i) {
     a.shift = plan[2 * i]; a.bits = plan[2 * i + 1];
     a.first = i == 0; a.last = i == rounds - 1;

@@ -99,6 +99,27 @@ struct SegArgs {
   unsigned long long* done;    // optional mailbox flag (see PassArgs)
   unsigned long long seq;
   const void* cuts;            // cut pass (R26): device pointer to the two cuts t_a <= t_b
+  const struct ChainState* chain;  // device chain (§8f-3): skip unless chain->ok[0]
+  // device chain: the finishing thread also takes the chain's next decision (step 1)
+  struct ChainState* chain_out;
+  struct ChainMail* chain_mail;
+  unsigned long long chain_seq;
+  uint64_t chain_k, chain_cap;
+};
+
+// Device-side chain of the usual selection (NEXT row §8f-3): init -> cut pass -> radix select,
+// launched back to back; the step kernels between them decide on the device whether the usual
+// path holds (ok) and hand the next kernel its array size m and rank r.  The host consumes a
+// step's result only if its own driver asks for exactly that step.
+struct ChainState {
+  unsigned long long ok[2];   // [0]: cut pass on the init's copy, [1]: radix select of the cut's copy
+  unsigned long long m[2], r[2];
+  unsigned long long le_base;  // #x <= t_lo of the init (global count below the current array)
+};
+// the host-visible copy the step kernels publish (mapped memory), with a sequence flag each
+struct ChainMail {
+  unsigned long long ok[2], m[2], r[2];
+  unsigned long long seq[2];
 };
 
 struct InitArgs {
@@ -110,6 +131,11 @@ struct InitArgs {
   const void* t0;   // device pointer to the two extra cuts t_lo, t_hi (elements of the dtype), or nullptr
   unsigned long long* done;  // optional mailbox flag (see PassArgs)
   unsigned long long seq;
+  // device chain (§8f-3, init_seg_kernel): the finishing thread also takes the chain's step 0
+  struct ChainState* chain;
+  struct ChainMail* chain_mail;
+  unsigned long long chain_seq;
+  uint64_t chain_k, chain_cap;
 };
 
 struct LaunchShape {
@@ -149,7 +175,9 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 constexpr size_t kSampleKeyBytes = 32768 * 4 > 16384 * 8 ? 32768 * 4 : 16384 * 8;
 // small: 8192 (f32) / 4096 (f64) samples instead (the cut passes over an already small bracket).
 cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
-                                 uint64_t r, void* t0, void* keys, cudaStream_t st, bool small = false);
+                                 uint64_t r, void* t0, void* keys, cudaStream_t st, bool small = false,
+                                 const ChainState* chain = nullptr, int which = 0);
+
 // smax (<= 1024): samples drawn; keys_out != nullptr: write the sorted sample keys (order-preserving
 // 64-bit keys, padding ~0) there instead of picking cuts (pooled across ranks, R28).
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
@@ -179,7 +207,8 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned int* hist, const LaunchShape& s, cudaStream_t st,
                                 double* vout, unsigned long long* done, unsigned long long seq,
-                                const SegEntry* tab, int side, unsigned int* ticket);
+                                const SegEntry* tab, int side, unsigned int* ticket,
+                                const ChainState* chain = nullptr);
 
 // Step a8: per-column k-th smallest of S (n x C column-major, float32), one CTA per column.
 struct BatchArgs {
