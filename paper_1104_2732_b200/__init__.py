@@ -253,8 +253,9 @@ def _out_value(buf, dt: int) -> float:
 
 
 # ------------------------------------------------------------------------------------------ API
-def select_kth(x, k: int, return_info: bool = False):
-    """k-th smallest element (1-based) of the CUDA tensor x (float32/float64)."""
+def select_kth(x, k: int, return_info=False):
+    """k-th smallest element (1-based) of the CUDA tensor x (float32/float64).  return_info: True
+    adds the call's report as a dict, "raw" as the ctypes `Info` struct."""
     x = _flat(x)
     ctx = _ctx_for(x)
     dt = _dtype_code(x)
@@ -267,6 +268,8 @@ def select_kth(x, k: int, return_info: bool = False):
     _check(ctx, lib.cpsel_select_kth(ctx.handle, x.data_ptr(), x.numel(), dt, k, C.byref(out),
                                      C.byref(info) if info is not None else None))
     v = out.value
+    if return_info == "raw":  # the ctypes struct itself (no dict built: for tight timing loops)
+        return v, info
     return (v, info.as_dict()) if return_info else v
 
 

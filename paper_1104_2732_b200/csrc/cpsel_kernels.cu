@@ -22,6 +22,8 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "cpsel_kernels.h"
 #include "cpsel_ptx.h"
 
@@ -2563,6 +2565,238 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
   return cudaGetLastError();
 }
 
+// The same, as ONE launch over a cluster of 8 CTAs (8 SMs, distributed shared memory): every CTA
+// gathers KPT samples per thread straight into registers, builds its local histograms, and adds
+// them into CTA 0's through DSMEM atomics; CTA 0 picks the digits and the others read the new
+// prefixes back from it.  Replaces the global round trip of the keys and one launch, and spreads
+// the sorting / histogram work over 8 SMs.
+constexpr int kSampleCluster = 8;
+struct ClusterSel {
+  unsigned loc[3][2048];   // this CTA's histograms
+  unsigned glob[3][2048];  // CTA 0: the cluster's histograms
+  unsigned csum[3][32];
+  unsigned long long prefix[3], mask[3], rank[3];
+  unsigned long long wsum[32];
+};
+template <typename T, int KPT>
+__global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
+    sample_cluster_kernel(const T* __restrict__ x, uint64_t m, const SegEntry* __restrict__ tab, int side, int Wtot,
+                          uint64_t r, T* t0, const ChainState* chain, int which) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  using SK = SampleKey<T>;
+  using K = typename SK::K;
+  extern __shared__ __align__(16) unsigned char csm[];
+  ClusterSel& sh = *reinterpret_cast<ClusterSel*>(csm);
+  unsigned long long* pre = reinterpret_cast<unsigned long long*>(csm + sizeof(ClusterSel));  // run-table prefix
+  const unsigned crank = cl.block_rank();
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  bool go = true;
+  if (chain) {
+    go = chain->ok[which] != 0;
+    m = chain->m[which];
+    r = chain->r[which];
+  }
+  if (!go) return;  // uniform over the cluster (every CTA reads the same chain)
+  constexpr uint64_t S = (uint64_t)kSampleCluster * 1024 * KPT;
+  const uint64_t ms = m < S ? m : S;
+  if (tab) {  // this CTA's copy of the run-table prefix
+    const int per = (Wtot + 1023) / 1024;
+    const int w0 = i * per, w1 = min(w0 + per, Wtot);
+    unsigned long long c = 0;
+    for (int w = w0; w < w1; ++w) {
+      c += tab[w].cnt[side];
+      pre[w] = c;
+    }
+    unsigned long long incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) sh.wsum[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const unsigned long long v = sh.wsum[lane];
+      unsigned long long inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+        if (lane >= o) inc += y;
+      }
+      sh.wsum[lane] = inc - v;
+    }
+    __syncthreads();
+    const unsigned long long base = sh.wsum[warp] + incl - c;
+    for (int w = w0; w < w1; ++w) pre[w] += base;
+    __syncthreads();
+  }
+  K keys[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const uint64_t smp = ((uint64_t)j * kSampleCluster + crank) * 1024 + i;
+    keys[j] = ~K(0);
+    if (smp < ms) {
+      uint64_t g = (m == ms) ? smp : (smp * m) / ms + (m / ms) / 2;
+      if (!tab) {
+        keys[j] = SK::key(x[g]);
+      } else {
+        int lo = 0, hi = Wtot - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (pre[mid] > g) hi = mid; else lo = mid + 1;
+        }
+        g -= lo ? pre[lo - 1] : 0ull;
+        keys[j] = SK::key(x[tab[lo].off[side] + g]);
+      }
+    }
+  }
+#pragma unroll
+  for (int size = 2; size <= KPT; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int l = j ^ stride;
+        if (l > j) {
+          const K a = keys[j], b = keys[l];
+          const bool up = (j & size) == 0;
+          keys[j] = up ? (a < b ? a : b) : (a < b ? b : a);
+          keys[l] = up ? (a < b ? b : a) : (a < b ? a : b);
+        }
+      }
+    }
+  }
+  if (crank == 0 && i == 0) {
+    const double md = (double)ms;
+    const double q = ((double)r - 0.5) / (double)m * md;
+    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+    const double qq[3] = {floor(q - w), ceil(q + w), floor(q)};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      sh.rank[t] = qq[t] < 0 ? 0 : (qq[t] >= md ? ms - 1 : (uint64_t)qq[t]);
+      sh.prefix[t] = 0;
+      sh.mask[t] = 0;
+    }
+  }
+  unsigned* glob0 = cl.map_shared_rank(&sh.glob[0][0], 0);
+  ClusterSel* sh0 = cl.map_shared_rank(&sh, 0);
+  for (int rd = 0; rd < SK::ROUNDS; ++rd) {
+    const int shift = SK::shift(rd), nb = 1 << SK::bits(rd);
+    for (int b = i; b < 3 * 2048; b += 1024) {
+      (&sh.loc[0][0])[b] = 0u;
+      if (crank == 0) (&sh.glob[0][0])[b] = 0u;
+    }
+    cl.sync();  // CTA 0's prefixes and zeroed histograms visible to every CTA
+    const K p0 = (K)sh0->prefix[0], p1 = (K)sh0->prefix[1], p2 = (K)sh0->prefix[2];
+    const K m0 = (K)sh0->mask[0], m1 = (K)sh0->mask[1], m2 = (K)sh0->mask[2];
+    const int ntg = rd == 0 ? 1 : 3;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (t >= ntg) break;
+      const K pt = t == 0 ? p0 : (t == 1 ? p1 : p2), mt = t == 0 ? m0 : (t == 1 ? m1 : m2);
+      unsigned run = 0;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const K k = keys[j];
+        const bool in = (k & mt) == pt;
+        const unsigned d = (unsigned)(k >> shift) & (unsigned)(nb - 1);
+        run += in ? 1u : 0u;
+        bool last = in;
+        if (j + 1 < KPT) {
+          const K kn = keys[j + 1 < KPT ? j + 1 : j];
+          last = in && (((kn & mt) != pt) || (((unsigned)(kn >> shift) & (unsigned)(nb - 1)) != d));
+        }
+        if (last) {
+          atomicAdd(&sh.loc[t][d], run);
+          run = 0;
+        }
+      }
+    }
+    __syncthreads();
+    for (int b = i; b < ntg * 2048; b += 1024) {
+      const unsigned v = (&sh.loc[0][0])[b];
+      if (v) atomicAdd(glob0 + b, v);
+    }
+    cl.sync();  // the cluster's histograms complete in CTA 0
+    if (crank == 0) {
+      if (rd == 0)
+        for (int b = i; b < 2048; b += 1024) sh.glob[1][b] = sh.glob[2][b] = sh.glob[0][b];
+      __syncthreads();
+      const int c0 = warp * 64;
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        unsigned v = (c0 + lane < nb ? sh.glob[t][c0 + lane] : 0u) + (c0 + 32 + lane < nb ? sh.glob[t][c0 + 32 + lane] : 0u);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+        if (lane == 0) sh.csum[t][warp] = v;
+      }
+      __syncthreads();
+      if (warp < 3) {
+        const int t = warp;
+        const unsigned long long rk = sh.rank[t];
+        const unsigned cs = sh.csum[t][lane];
+        unsigned incl = cs;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned hm = __ballot_sync(FULL, (unsigned long long)incl > rk);
+        const int c = __ffs(hm) - 1;
+        unsigned long long before = __shfl_sync(FULL, incl - cs, c);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int b = c * 64 + half * 32 + lane;
+          const unsigned h = b < nb ? sh.glob[t][b] : 0u;
+          unsigned in2 = h;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, in2, o);
+            if (lane >= o) in2 += y;
+          }
+          const unsigned hb = __ballot_sync(FULL, before + in2 > rk);
+          if (hb) {
+            const int src = __ffs(hb) - 1;
+            const unsigned ex = __shfl_sync(FULL, in2 - h, src);
+            if (lane == 0) {
+              sh.prefix[t] |= (unsigned long long)(c * 64 + half * 32 + src) << shift;
+              sh.mask[t] |= (unsigned long long)(nb - 1) << shift;
+              sh.rank[t] = rk - (before + ex);
+            }
+            break;
+          }
+          before += __shfl_sync(FULL, in2, 31);
+        }
+      }
+    }
+    __syncthreads();  // CTA 0: the digit search is done before the next round clears its histograms
+  }
+  cl.sync();
+  if (crank == 0 && i < 3) {
+    K kk = (K)sh.prefix[i];
+    if (i == 1) kk |= (K)~(K)sh.mask[1];
+    kk = kk < SK::KLO ? SK::KLO : (kk > SK::KHI ? SK::KHI : kk);
+    t0[i] = SK::val(kk);
+  }
+}
+
+template <typename T, int KPT>
+cudaError_t sample_cluster_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
+                             cudaStream_t st, const ChainState* chain, int which) {
+  const size_t smem = sizeof(ClusterSel) + (tab ? (size_t)Wtot * 8 : 0);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(sample_cluster_kernel<T, KPT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(sizeof(ClusterSel) + 8 * kGatherMaxWarps));
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  sample_cluster_kernel<T, KPT><<<kSampleCluster, 1024, smem, st>>>(static_cast<const T*>(x), m, tab, side, Wtot, r,
+                                                                   static_cast<T*>(t0), chain, which);
+  return cudaGetLastError();
+}
+
 template <typename T, int KPT>
 cudaError_t sample_select_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
                             void* keys, cudaStream_t st, const ChainState* chain, int which) {
@@ -2577,11 +2811,13 @@ cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const Seg
                                  uint64_t r, void* t0, void* keys, cudaStream_t st, bool small,
                                  const ChainState* chain, int which) {
   if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
+  (void)keys;
+  // one cluster launch: 8 CTAs x 1024 threads x KPT samples (32768 / 8192 for f32, 16384 / 4096 f64)
   if (dtype == kF32)
-    return small ? sample_select_t<float, 8>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which)
-                 : sample_select_t<float, SampleKey<float>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which);
-  return small ? sample_select_t<double, 4>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which)
-               : sample_select_t<double, SampleKey<double>::KPT>(x, m, tab, side, Wtot, r, t0, keys, st, chain, which);
+    return small ? sample_cluster_t<float, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which)
+                 : sample_cluster_t<float, 4>(x, m, tab, side, Wtot, r, t0, st, chain, which);
+  return small ? sample_cluster_t<double, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which)
+               : sample_cluster_t<double, 2>(x, m, tab, side, Wtot, r, t0, st, chain, which);
 }
 
 
