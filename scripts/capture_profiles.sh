@@ -8,8 +8,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --csv --log-file $out/${tag}_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu \
   > $out/${tag}_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"init_seg|cut_pass|sample_gather|sample_select|seg_pass|radix_round" -c 14 \
+  -k regex:"init_seg|cut_pass|sample_cluster|seg_pass|radix_round" -c 14 \
   -o $out/${tag}_full python scripts/prof_kernels.py select > $out/${tag}_full.log 2>&1
-timeout 900 ncu --set full --clock-control none -k regex:"residual_tc|batched_select|pack_rows" -c 3 \
+timeout 900 ncu --set full --clock-control none -k regex:"residual_tc|batched_select|pack_rows|lts_reduce" -c 5 \
   -o $out/${tag}_lms python scripts/prof_kernels.py lms > $out/${tag}_lms.log 2>&1
 tail -c 400 $out/${tag}_bench.json
