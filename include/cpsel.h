@@ -69,7 +69,11 @@ typedef struct {
   int32_t pass_cuts;         /* 1: a compacted bracket larger than select_cap is cut at two sample
                                 quantiles of its own, keeping only what lies between them (R26,
                                 multi-point step).  Ignored with objective=1.  Default 1 */
-  int32_t reserved;
+  int32_t lms_fused;         /* 1: LMS/LTS objectives never store S: the residuals are recomputed
+                                on the tensor cores inside one fused pass that takes the init
+                                statistics, counts at two sample cuts per candidate and copies
+                                what lies between them (§8f-2); columns the copy cannot finish
+                                are stored and selected from S.  Used for n >= 16384.  Default 1 */
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -170,7 +174,9 @@ cpsel_status cpsel_lms_objective(cpsel_ctx* ctx, const float* d_X, const float* 
                                  uint32_t p, const float* d_thetas, uint32_t C, float* d_out,
                                  cpsel_info* info);
 /* The residual stage alone: d_S (float32, n x C column-major, column j at d_S + j*n) receives
- * (x_i . theta_j - y_i)^2 computed on the tensor cores (tcgen05, 3xTF32 split). */
+ * (x_i . theta_j - y_i)^2 computed on the tensor cores (tcgen05, 3xTF32 split) — by the kernel
+ * the objectives use under the current config (lms_fused), so the objectives are exactly the
+ * order statistics of this S. */
 cpsel_status cpsel_lms_residuals(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n,
                                  uint32_t p, const float* d_thetas, uint32_t C, float* d_S);
 /* LTS (NEXT row): d_out[j] (float64, device) = the sum of the h smallest squared

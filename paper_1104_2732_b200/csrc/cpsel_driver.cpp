@@ -1557,6 +1557,7 @@ void cpsel_config_default(cpsel_config* c) {
   c->record_timing = 0;
   c->init_cut = 1;
   c->pass_cuts = 1;
+  c->lms_fused = 1;
 }
 
 cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
@@ -1848,14 +1849,39 @@ cpsel_status cpsel_drive_host(const cpsel_host_backend* be, uint64_t n, cpsel_dt
 }
 
 // ------------------------------------------------------------------------ LMS
+static constexpr uint64_t kLmsFusedMinN = 1ull << 14;
+static bool lms_use_fused(const cpsel_ctx* ctx, uint64_t n) { return ctx->cfg.lms_fused && n >= kLmsFusedMinN; }
+
+static cpsel_status lms_validate(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
+                                 const float* d_thetas, uint32_t C, const void* d_out) {
+  if (!d_X || !d_y || !d_thetas || !d_out) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
+  return CPSEL_OK;
+}
+
+static void lms_info(cpsel_info* info, const LmsReport& rep, bool fused) {
+  if (!info) return;
+  memset(info, 0, sizeof *info);
+  info->passes = rep.passes;
+  info->cp_iters = rep.cp_iters;
+  info->z_count = rep.z_total;
+  info->bytes_moved = rep.bytes;
+  info->ms_total = rep.ms + rep.ms_fused;
+  info->kernel_ms_init = rep.ms_fused;
+  info->kernel_ms_passes = rep.ms;
+  info->fallback_steps = rep.fallback;
+  info->launches = fused ? 2 : 1;
+}
+
 cpsel_status cpsel_lms_residuals(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
                                  const float* d_thetas, uint32_t C, float* d_S) {
   if (!ctx) return CPSEL_EINVAL;
-  if (!d_X || !d_y || !d_thetas || !d_S) return fail(ctx, CPSEL_EINVAL, "null pointer");
-  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
-  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
+  cpsel_status s = lms_validate(ctx, d_X, d_y, n, p, d_thetas, C, d_S);
+  if (s != CPSEL_OK) return s;
   DeviceGuard g(ctx->device);
-  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
+  if (lms_use_fused(ctx, n)) CK(lms_fused_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
+  else CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   return CPSEL_OK;
 }
@@ -1872,33 +1898,48 @@ cpsel_status cpsel_select_kth_batched(cpsel_ctx* ctx, const float* d_S, uint64_t
   if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a column");
   CK(e);
   if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "input holds NaN or Inf");
-  if (info) {
-    memset(info, 0, sizeof *info);
-    info->passes = rep.passes;
-    info->cp_iters = rep.cp_iters;
-    info->z_count = rep.z_total;
-    info->bytes_moved = rep.bytes;
-    info->ms_total = rep.ms;
-    info->kernel_ms_passes = rep.ms;
-    info->launches = 1;
-  }
+  lms_info(info, rep, false);
   return CPSEL_OK;
+}
+
+// k-th smallest squared residual of every candidate (the fused path or residuals + batched select)
+static cpsel_status lms_kth(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
+                            const float* d_thetas, uint32_t C, uint64_t k, float* d_out, cpsel_info* info,
+                            bool* used_fused = nullptr) {
+  bool fused = lms_use_fused(ctx, n);
+  if (used_fused) *used_fused = false;
+  if (fused) {
+    cudaError_t ce = cudaSuccess;
+    const int chk = lms_fused_check(ctx->lms, d_X, d_y, n, p, d_thetas, C, ctx->stream, &ce);
+    if (chk < 0) CK(ce);
+    if (chk == 1) return fail(ctx, CPSEL_ENONFINITE, "X, y or thetas hold NaN or Inf");
+    fused = chk == 0;
+  }
+  if (fused) {
+    if (used_fused) *used_fused = true;
+    LmsReport rep{};
+    cudaError_t e = lms_fused_select(ctx->lms, d_X, d_y, n, p, d_thetas, C, k, d_out, ctx->cfg.max_iters, &rep,
+                                     ctx->stream);
+    if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a column");
+    CK(e);
+    if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "residuals hold NaN or Inf");
+    lms_info(info, rep, true);
+    return CPSEL_OK;
+  }
+  cpsel_status s = ensure(ctx, reinterpret_cast<void**>(&ctx->lms.S), &ctx->lms.S_bytes, (size_t)n * C * sizeof(float));
+  if (s != CPSEL_OK) return s;
+  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, ctx->lms.S, ctx->stream));
+  return cpsel_select_kth_batched(ctx, ctx->lms.S, n, C, k, d_out, info);
 }
 
 cpsel_status cpsel_lms_objective(cpsel_ctx* ctx, const float* d_X, const float* d_y, uint64_t n, uint32_t p,
                                  const float* d_thetas, uint32_t C, float* d_out, cpsel_info* info) {
   if (!ctx) return CPSEL_EINVAL;
-  if (!d_X || !d_y || !d_thetas || !d_out) return fail(ctx, CPSEL_EINVAL, "null pointer");
-  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
-  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
-  DeviceGuard g(ctx->device);
-  float* d_S = nullptr;
-  cpsel_status s = ensure(ctx, reinterpret_cast<void**>(&ctx->lms.S), &ctx->lms.S_bytes, (size_t)n * C * sizeof(float));
+  cpsel_status s = lms_validate(ctx, d_X, d_y, n, p, d_thetas, C, d_out);
   if (s != CPSEL_OK) return s;
-  d_S = ctx->lms.S;
+  DeviceGuard g(ctx->device);
   const auto t0 = std::chrono::steady_clock::now();
-  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
-  s = cpsel_select_kth_batched(ctx, d_S, n, C, (n + 1) / 2, d_out, info);
+  s = lms_kth(ctx, d_X, d_y, n, p, d_thetas, C, (n + 1) / 2, d_out, info);
   if (info) info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return s;
 }
@@ -1907,19 +1948,17 @@ cpsel_status cpsel_lts_objective(cpsel_ctx* ctx, const float* d_X, const float* 
                                  const float* d_thetas, uint32_t C, uint64_t h, double* d_out, float* d_m,
                                  cpsel_info* info) {
   if (!ctx) return CPSEL_EINVAL;
-  if (!d_X || !d_y || !d_thetas || !d_out || !d_m) return fail(ctx, CPSEL_EINVAL, "null pointer");
-  if (n == 0 || p == 0 || C == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  cpsel_status s = lms_validate(ctx, d_X, d_y, n, p, d_thetas, C, d_out);
+  if (s != CPSEL_OK) return s;
+  if (!d_m) return fail(ctx, CPSEL_EINVAL, "null pointer");
   if (h < 1 || h > n) return fail(ctx, CPSEL_ERANK, "h outside [1,n]");
-  if (p > kLmsMaxP) return fail(ctx, CPSEL_EINVAL, "p=%u > %d", p, kLmsMaxP);
   DeviceGuard g(ctx->device);
-  cpsel_status s = ensure(ctx, reinterpret_cast<void**>(&ctx->lms.S), &ctx->lms.S_bytes, (size_t)n * C * sizeof(float));
-  if (s != CPSEL_OK) return s;
-  float* d_S = ctx->lms.S;
   const auto t0 = std::chrono::steady_clock::now();
-  CK(lms_residuals(ctx->lms, d_X, d_y, n, p, d_thetas, C, d_S, ctx->stream));
-  s = cpsel_select_kth_batched(ctx, d_S, n, C, h, d_m, info);
+  bool fused = false;
+  s = lms_kth(ctx, d_X, d_y, n, p, d_thetas, C, h, d_m, info, &fused);
   if (s != CPSEL_OK) return s;
-  CK(lts_reduce(d_S, n, C, h, d_m, d_out, ctx->stream));
+  if (fused) CK(lms_fused_lts(ctx->lms, d_X, d_y, n, p, d_thetas, C, h, d_m, d_out, ctx->stream));
+  else CK(lts_reduce(ctx->lms.S, n, C, h, d_m, d_out, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (info) info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   return CPSEL_OK;

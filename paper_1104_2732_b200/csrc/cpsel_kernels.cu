@@ -2090,25 +2090,9 @@ __device__ __forceinline__ float key_mid_dev(float yL, float yR) {
   return (float)from_key_f32((unsigned long long)(a + (b - a) / 2));
 }
 
-// ascending bitonic sort of S (power of 2) keys in shared memory, all threads of the CTA
-template <typename K> __device__ void block_bitonic_sort(K* key, int S) {
-  for (int size = 2; size <= S; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = threadIdx.x; i < S / 2; i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1));
-        const int hi = lo + stride;
-        const bool up = ((lo & size) == 0);
-        const K x = key[lo], y = key[hi];
-        if ((x > y) == up) { key[lo] = y; key[hi] = x; }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 constexpr int kBatchSample = 2048;   // samples of the init pass's extra cuts (R23; 32-bit keys)
 constexpr int kBatchCutSample = 1024;  // samples of a cut pass over the compacted bracket (R26)
-constexpr int kBatchFinish = 4096;   // kept halves this small are finished by a shared-memory sort
+constexpr int kBatchFinish = 4096;   // kept halves this small are finished by a block radix select
 
 struct BatchState {
   const float* cur;
@@ -2119,33 +2103,219 @@ struct BatchState {
   int col, on_z, slow, bisect, phase, compact, cur_buf, tgt, side, iters, exact, cuts_stalled, free_step;
 };
 
-// Sorted 32-bit keys of ms strided samples of z[0..m) (ms <= S, padding ~0), then the cuts of
-// local rank r (1-based) in st.cut_lo / cut_hi / cut_mid (thread 0).  Block-wide.
+// Block-wide exact selection of NT order statistics of 32-bit keys held PER per thread (kBlock
+// threads): rk[t] = 0-based rank among all kBlock*PER keys (padding keys 0xffffffff sort last and
+// are never selected when rk[t] < #valid).  MSB radix select with 11/11/10-bit digits and one
+// shared-memory histogram per target (hist: NT x 2048 words); out[t] on every thread.  Replaces a
+// bitonic sort of the whole set (a5 / R26 sample cuts): 3 histogram rounds instead of log^2 stages.
+template <int PER, int NT>
+__device__ void block_radix_select(const unsigned (&key)[PER], unsigned* hist, const unsigned (&rk_in)[NT],
+                                   unsigned (&out)[NT]) {
+  __shared__ unsigned wsum[NT][kWarps];
+  __shared__ unsigned sel[NT][2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned prefix[NT], rk[NT], mask = 0u;
+#pragma unroll
+  for (int t = 0; t < NT; ++t) { prefix[t] = 0u; rk[t] = rk_in[t]; }
+#pragma unroll 1
+  for (int round = 0; round < 3; ++round) {
+    const int sh = round == 0 ? 21 : (round == 1 ? 10 : 0);
+    const unsigned dm = round == 2 ? 1023u : 2047u;
+    for (int b = tid; b < NT * 2048; b += kBlock) hist[b] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const unsigned d = (key[u] >> sh) & dm;
+#pragma unroll
+      for (int t = 0; t < NT; ++t)
+        if ((key[u] & mask) == prefix[t]) atomicAdd(&hist[t * 2048 + d], 1u);
+    }
+    __syncthreads();
+    constexpr int B = 2048 / kBlock;  // bins per thread
+    unsigned c[NT][B], incl[NT], tot[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      unsigned v = 0u;
+#pragma unroll
+      for (int b = 0; b < B; ++b) { c[t][b] = hist[t * 2048 + tid * B + b]; v += c[t][b]; }
+      tot[t] = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned w = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += w;
+      }
+      incl[t] = v;
+      if (lane == 31) wsum[t][wid] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      unsigned before = incl[t] - tot[t];
+      for (int w2 = 0; w2 < wid; ++w2) before += wsum[t][w2];
+      if (before <= rk[t] && rk[t] < before + tot[t]) {
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+          if (before <= rk[t] && rk[t] < before + c[t][b]) { sel[t][0] = (unsigned)(tid * B + b); sel[t][1] = before; }
+          before += c[t][b];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      prefix[t] |= sel[t][0] << sh;
+      rk[t] -= sel[t][1];
+    }
+    mask |= dm << sh;
+    __syncthreads();  // hist / sel reused
+  }
+#pragma unroll
+  for (int t = 0; t < NT; ++t) out[t] = prefix[t];
+}
+
+// The cuts of local rank r (1-based) of m elements from ms evenly strided samples of z[0..m)
+// (ms <= S): sample order statistics of ranks q -/+ (3.5 sd + 2) and q -> st.cut_lo / cut_hi /
+// cut_mid.  Block-wide; hist = NT x 2048 words of shared memory.
 template <int S>
-__device__ void batch_sample_cuts(BatchState& st, unsigned* keys, const float* z, uint64_t m, uint64_t r) {
+__device__ void batch_sample_cuts(BatchState& st, unsigned* hist, const float* z, uint64_t m, uint64_t r) {
+  constexpr int PER = S / kBlock;
   const uint64_t ms = m < (uint64_t)S ? m : (uint64_t)S;
-  for (int i = threadIdx.x; i < S; i += kBlock) {
-    if ((uint64_t)i < ms) {
-      const uint64_t pos = (m == ms) ? (uint64_t)i : ((uint64_t)i * m) / ms + (m / ms) / 2;
-      keys[i] = (unsigned)okey(z[pos]);
+  unsigned key[PER];
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const uint64_t i = (uint64_t)(threadIdx.x + u * kBlock);
+    if (i < ms) {
+      const uint64_t pos = (m == ms) ? i : (i * m) / ms + (m / ms) / 2;
+      key[u] = (unsigned)okey(z[pos]);
     } else {
-      keys[i] = ~0u;
+      key[u] = ~0u;
     }
   }
-  __syncthreads();
-  block_bitonic_sort(keys, S);
+  const double md = (double)ms;
+  const double q = ((double)r - 0.5) / (double)m * md;
+  const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+  const double ql = floor(q - w), qh = ceil(q + w), qm = floor(q);
+  const unsigned rk[3] = {ql < 0 ? 0u : (unsigned)ql, qh >= md ? (unsigned)(ms - 1) : (unsigned)qh,
+                          qm < 0 ? 0u : (qm >= md ? (unsigned)(ms - 1) : (unsigned)qm)};
+  unsigned out[3];
+  block_radix_select<PER, 3>(key, hist, rk, out);
   if (threadIdx.x == 0) {
-    const double md = (double)ms;
-    const double q = ((double)r - 0.5) / (double)m * md;
-    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
-    const double ql = floor(q - w), qh = ceil(q + w), qm = floor(q);
-    const uint64_t il = ql < 0 ? 0 : (uint64_t)ql;
-    const uint64_t ih = qh >= md ? ms - 1 : (uint64_t)qh;
-    st.cut_lo = (float)from_key_f32(keys[il]);
-    st.cut_hi = (float)from_key_f32(keys[ih]);
-    st.cut_mid = (float)from_key_f32(keys[qm < 0 ? 0 : (qm >= md ? ms - 1 : (uint64_t)qm)]);
+    st.cut_lo = (float)from_key_f32(out[0]);
+    st.cut_hi = (float)from_key_f32(out[1]);
+    st.cut_mid = (float)from_key_f32(out[2]);
   }
   __syncthreads();
+}
+
+// R23 for the fused LMS pass.  Ss holds, per column j, the residuals s of ms evenly strided sample
+// rows (computed by the fused tensor-core kernel in store mode: exactly elements of S).  Per column,
+// the bin edges around the sample order statistics of ranks q -/+ (3.5 sd + 2) and q (q the target
+// rank k scaled to the sample, as batch_sample_cuts) -> cuts[4j .. 4j+2] = t_lo, t_hi, t_mid.  Two
+// MSB digit rounds on the order-preserving keys: an 11-bit histogram of all keys, then 11-bit
+// histograms of the keys in each target's bin; t_lo is the lower edge of the lo target's final bin
+// (<= that sample order statistic), t_hi the upper edge of the hi target's (>=): cuts at most 2^10
+// key units (2^-13 relative) wider than the exact sample quantiles, which is all a cut needs — the
+// fused pass counts exactly at whatever values they are.  One CTA of 1024 threads per column.
+constexpr int kCutThreads = 1024;
+constexpr int kCutMaxPer = 16;   // <= 16384 samples
+__global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* __restrict__ Ss, uint32_t ms,
+                                                                  uint64_t n, uint32_t C, uint64_t k,
+                                                                  float* __restrict__ cuts) {
+  __shared__ unsigned hist[3][2048];
+  __shared__ unsigned wsum[3][32];
+  __shared__ unsigned sel[3][2];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  unsigned rank[3];
+  {
+    const double md = (double)ms;
+    const double q = ((double)k - 0.5) / (double)n * md;
+    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+    const double ql = floor(q - w), qh = ceil(q + w), qm = floor(q);
+    rank[0] = ql < 0 ? 0u : (unsigned)ql;
+    rank[1] = qh >= md ? ms - 1 : (unsigned)qh;
+    rank[2] = qm < 0 ? 0u : (qm >= md ? ms - 1 : (unsigned)qm);
+  }
+  for (uint32_t j = blockIdx.x; j < C; j += gridDim.x) {
+    const float* col = Ss + (size_t)j * ms;
+    unsigned key[kCutMaxPer];
+#pragma unroll
+    for (int u = 0; u < kCutMaxPer; ++u) {
+      const uint32_t i = tid + u * kCutThreads;
+      key[u] = i < ms ? (unsigned)okey(__ldcs(col + i)) : 0xffffffffu;  // padding sorts last
+    }
+    unsigned bin[3] = {0u, 0u, 0u}, rk[3] = {rank[0], rank[1], rank[2]};
+#pragma unroll 1
+    for (int round = 0; round < 2; ++round) {
+      const int nh = round == 0 ? 1 : 3;
+      for (int b = tid; b < nh * 2048; b += kCutThreads) (&hist[0][0])[b] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kCutMaxPer; ++u) {
+        if (round == 0) {
+          atomicAdd(&hist[0][key[u] >> 21], 1u);
+        } else {
+          const unsigned top = key[u] >> 21, d = (key[u] >> 10) & 2047u;
+#pragma unroll
+          for (int t = 0; t < 3; ++t)
+            if (top == bin[t]) atomicAdd(&hist[t][d], 1u);
+        }
+      }
+      __syncthreads();
+      unsigned c0[3], c1[3], incl[3];
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const int hsrc = round == 0 ? 0 : t;
+        c0[t] = hist[hsrc][2 * tid];
+        c1[t] = hist[hsrc][2 * tid + 1];
+        unsigned v = c0[t] + c1[t];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned w = __shfl_up_sync(0xffffffffu, v, o);
+          if (lane >= o) v += w;
+        }
+        incl[t] = v;
+        if (lane == 31) wsum[t][wid] = v;
+      }
+      __syncthreads();
+      if (wid == 0) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          unsigned v = wsum[t][lane];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned w = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += w;
+          }
+          wsum[t][lane] = v;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        const unsigned before = (wid ? wsum[t][wid - 1] : 0u) + incl[t] - c0[t] - c1[t];
+        if (before <= rk[t] && rk[t] < before + c0[t]) {
+          sel[t][0] = 2u * tid;
+          sel[t][1] = before;
+        } else if (before + c0[t] <= rk[t] && rk[t] < before + c0[t] + c1[t]) {
+          sel[t][0] = 2u * tid + 1u;
+          sel[t][1] = before + c0[t];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int t = 0; t < 3; ++t) {
+        bin[t] = round == 0 ? sel[t][0] : ((bin[t] << 11) | sel[t][0]);
+        rk[t] -= sel[t][1];
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {  // bin[t] = the top 22 bits of the target's key
+      cuts[4 * (size_t)j] = (float)from_key_f32(bin[0] << 10);
+      cuts[4 * (size_t)j + 1] = (float)from_key_f32((bin[1] << 10) | 1023u);
+      cuts[4 * (size_t)j + 2] = (float)from_key_f32((bin[2] << 10) | 512u);
+      cuts[4 * (size_t)j + 3] = 0.f;
+    }
+  }
 }
 
 template <int MODE>
@@ -2190,9 +2360,33 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
     }
     __syncthreads();
     if (st.col >= (int)a.C) break;
-    const float* x = a.S + (size_t)st.col * n;
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(dyn_smem);
+    const float* x = a.S ? a.S + (size_t)st.col * n : nullptr;
     unsigned* keys32 = reinterpret_cast<unsigned*>(dyn_smem);
+    if (a.f_le) {
+      // ---- fused LMS input: the fused residual pass took the init statistics, counted at the two
+      //      cuts and copied ]t_lo, t_hi[ out (a1 + R23 + a4); start from that bracket
+      if (threadIdx.x == 0) {
+        const int c = st.col;
+        const float tl = a.f_cuts[4 * (size_t)c], th = a.f_cuts[4 * (size_t)c + 1], tm = a.f_cuts[4 * (size_t)c + 2];
+        const unsigned long long le = a.f_le[c], written = a.f_cursor[c];
+        st.phase = 0;
+        st.iters = 0;
+        atomicAdd(&a.stats[0], 1ull);
+        if (tl < th && le < k && k <= le + written && written <= a.f_zcap) {
+          // the target lies in ]t_lo, t_hi[ (c_le(t_lo) < k <= c_lt(t_hi)) whose copy is z_j
+          st.yL = tl; st.yR = th; st.c_le_L = le; st.c_lt_R = le + written; st.m = written;
+          st.cur = a.f_z + (size_t)c * a.f_zcap; st.n_cur = written; st.cur_buf = -1;
+          st.D_lo = le; st.on_z = 1; st.slow = 0; st.bisect = 0;
+          st.exact = 1; st.cuts_stalled = 0; st.free_step = 0; st.tgt = 0;
+          st.t = (tm > tl && tm < th) ? (double)tm : 0.5 * (double)tl + 0.5 * (double)th;  // R25
+          if (st.m <= (unsigned long long)kBatchFinish) { st.k_r = k - st.c_le_L; st.phase = 2; }
+        } else {  // needs full passes over the column: deferred to the stored-S fallback
+          a.fail_list[atomicAdd(a.fail_count, 1u)] = (unsigned)c;
+          st.phase = 4;
+        }
+      }
+      __syncthreads();
+    } else {
     // ---- R23/R29: two extra cuts at quantiles of 8192 strided samples bracketing rank k
     const bool cut = n > 2;
     if (cut) batch_sample_cuts<kBatchSample>(st, keys32, x, n, k);
@@ -2285,6 +2479,7 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
         }
       }
       __syncthreads();
+    }
     }
     // ---- a2/a3/a4: Kelley iterations
     while (st.phase == 0) {
@@ -2419,20 +2614,25 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
       }
       __syncthreads();
     }
-    // ---- a5: exact finish on <= kBatchFinish elements: shared-memory bitonic sort of the keys
+    // ---- a5: exact finish on <= kBatchFinish elements: block radix select of their keys
     if (st.phase == 2) {
-      const int cnt = (int)st.n_cur;
-      for (int i = threadIdx.x; i < kBatchFinish; i += kBlock) keys[i] = i < cnt ? okey(st.cur[i]) : ~0ull;
-      __syncthreads();
-      int S2 = 64;
-      while (S2 < cnt) S2 <<= 1;
-      block_bitonic_sort(keys, S2);
-      if (threadIdx.x == 0) st.result = (float)from_key_f32(keys[st.k_r - 1]);
+      const uint32_t cnt = (uint32_t)st.n_cur;
+      constexpr int PER = kBatchFinish / kBlock;
+      unsigned key[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const uint32_t i = threadIdx.x + u * kBlock;
+        key[u] = i < cnt ? (unsigned)okey(st.cur[i]) : ~0u;
+      }
+      const unsigned rk[1] = {(unsigned)(st.k_r - 1)};
+      unsigned out[1];
+      block_radix_select<PER, 1>(key, keys32, rk, out);
+      if (threadIdx.x == 0) st.result = (float)from_key_f32(out[0]);
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && st.phase != 4) {
       const float r = st.result;
-      a.out[st.col] = r == 0.0f ? 0.0f : r;  // canonical +0 (R13)
+      a.out[a.out_map ? a.out_map[st.col] : (unsigned)st.col] = r == 0.0f ? 0.0f : r;  // canonical +0 (R13)
     }
     __syncthreads();
   }
@@ -2879,6 +3079,19 @@ cudaError_t launch_batched_select(const BatchArgs& a, int grid, cudaStream_t st)
   batched_select_kernel<<<grid, kBlock, sm, st>>>(a);
   return cudaGetLastError();
 }
+cudaError_t launch_lms_cuts(const float* Ss, uint32_t ms, uint64_t n, uint32_t C, uint64_t k, float* cuts,
+                            cudaStream_t st) {
+  if (ms > (uint32_t)(kCutThreads * kCutMaxPer)) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148, b = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lms_cuts_kernel, kCutThreads, 0);
+  uint32_t grid = (uint32_t)(sms * (b > 0 ? b : 1));
+  if (grid > C) grid = C;
+  lms_cuts_kernel<<<grid, kCutThreads, 0, st>>>(Ss, ms, n, C, k, cuts);
+  return cudaGetLastError();
+}
+
 int batched_blocks_per_sm() {
   constexpr size_t sm = compact_smem_bytes<float>();
   cudaFuncSetAttribute(batched_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

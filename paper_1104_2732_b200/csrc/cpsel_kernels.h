@@ -222,8 +222,26 @@ struct BatchArgs {
   unsigned* next_col;          // work counter, zero on entry
   unsigned long long* stats;   // [0] passes, [1] bytes, [2] safeguard trips, [3] non-finite columns
   uint32_t max_iters;
+  // fused LMS input (§8f-2): the fused residual pass already evaluated, per column, the two sample
+  // cuts f_cuts[4j], f_cuts[4j+1] (R23) — #s <= t_lo in f_le[j], the copy of ]t_lo, t_hi[ at
+  // f_z + j*f_zcap (f_cursor[j] elements) — so the kernel starts from that bracket instead of
+  // reading a column of S (the inputs were checked finite and overflow-free beforehand).  A column the copy cannot finish
+  // (target outside the cuts, copy overflow) is appended to fail_list and gets no output.
+  const float* f_cuts = nullptr;
+  const unsigned long long* f_le = nullptr;
+  const unsigned long long* f_cursor = nullptr;
+  const float* f_z = nullptr;
+  uint64_t f_zcap = 0;
+  unsigned* fail_list = nullptr;
+  unsigned* fail_count = nullptr;
+  const unsigned* out_map = nullptr;  // result of column c goes to out[out_map[c]] (nullable)
 };
 cudaError_t launch_batched_select(const BatchArgs& a, int grid, cudaStream_t st);
+// Per column j of the LMS problem: t_lo, t_hi, t_mid (cuts[4j..4j+2]) around the sample order
+// statistics bracketing rank k (R23 applied to the fused residual pass), from the residuals of ms
+// sample rows per column (Ss: C x ms, column-major).  ms <= 16384.
+cudaError_t launch_lms_cuts(const float* Ss, uint32_t ms, uint64_t n, uint32_t C, uint64_t k, float* cuts,
+                            cudaStream_t st);
 int batched_blocks_per_sm();
 
 }  // namespace cpsel

@@ -18,6 +18,8 @@
 // The stage is HBM-write bound (4 bytes of S per 2p flops); the tensor cores keep the contraction
 // off the FP32 pipes so the epilogue can stream S at full bandwidth.
 #include <cstdint>
+#include <cstring>
+#include <vector>
 
 #include "cpsel_kernels.h"
 #include "cpsel_ptx.h"
@@ -232,6 +234,349 @@ __global__ void __launch_bounds__(kThreads, 1) residual_tc_kernel(ResidualArgs a
 
 constexpr size_t kResidualSmem = 2 * STAGE + 1024 + 128 + 40 * 1024;  // ring + align + barriers; pad => 1 CTA/SM
 
+// ------------------------------------------------------------------------------------------
+// Fused residual pass (§8f-2 "fused GEMM-epilogue recompute"): the same 3xTF32 tcgen05 product,
+// transposed — candidates on the TMEM lanes (A = Theta image, 128 candidates per tile), rows on
+// the TMEM columns (B = X image, 256 rows per tile) — so each epilogue thread owns ONE candidate
+// column j and walks 32 consecutive rows per tcgen05.ld.  Nothing of S is stored: per element
+// s = (acc - y_i)^2 is counted against the column's two sample cuts (R23: #s <= t_lo), the
+// ones strictly between them are appended to the column's own buffer z_j (thread-private ring in
+// shared memory, flushed 16 at a time behind one atomicAdd on the column cursor), and the running
+// max (max.NaN: NaN/Inf detection and the upper end of the bracket) is kept.  Work is cut into
+// units (candidate tile, chunk of row tiles) so the per-column counters stay in registers for a
+// whole unit and are flushed once per unit.
+//   MODE kFuseCuts : the statistics above (the init pass a1 + R23 cuts + a4 copy of every column)
+//   MODE kFuseStore: s stored to S[slot[j]*n + row] for the columns with slot[j] >= 0 (fallback
+//                    columns, and the parity hook: the S the fused statistics were taken on)
+//   MODE kFuseLts  : sum_{s < m_j} s (fp64) and #{s < m_j} per column (LTS)
+constexpr int kFuseCuts = 0, kFuseStore = 1, kFuseLts = 2;
+constexpr int FN = 256;                    // rows per tile (TMEM columns per accumulator)
+constexpr int kFEpiWarps = 16;             // 4 per TMEM lane quarter, each on 64 of the 256 rows
+constexpr int kFYWarp = 2 + kFEpiWarps;    // the warp that stages y for each accumulator stage
+constexpr int kFThreads = 32 * (3 + kFEpiWarps);
+constexpr int kFRows = FN / 4;             // rows per epilogue warp per tile
+constexpr int kRing = 32;                  // staging slots per epilogue thread
+constexpr int kFlush = 16;                 // elements per flush
+constexpr uint32_t kSlot = 4;              // a thread's slots are consecutive words ...
+constexpr uint32_t kLaneStage = 4 * (kRing + 1);  // ... skewed by one word per thread (no bank conflicts)
+
+struct FusedArgs {
+  const unsigned char* a_img;   // Theta: n_ct x 16 KB (128 candidates per tile)
+  const unsigned char* b_img;   // X: n_rt x 32 KB (256 rows per tile)
+  const float* y;               // y, padded with zeros to n_rt * 256
+  uint64_t n;
+  uint32_t C, n_rt, rt_per_unit, n_chunks;
+  const uint32_t* ct_list;      // candidate tiles to run
+  uint32_t n_ct_list;
+  uint32_t b_ct_stride;         // 0: one X (and y) for all candidate tiles; else candidate tile ct reads
+                                // its own row tiles ct * b_ct_stride + rt (per-tile sample rows)
+  const float* cuts;            // kFuseCuts: 4 floats per column (t_lo, t_hi, t_mid, -)
+  unsigned long long* le;       // kFuseCuts: #s <= t_lo per column      | kFuseLts: #s < m_j
+  unsigned long long* cursor;   // kFuseCuts: elements of ]t_lo, t_hi[
+  float* z;                     // kFuseCuts: column j's interior at z + j * zcap
+  uint64_t zcap;
+  const int* slot;              // kFuseStore
+  float* S;                     // kFuseStore: slot-major columns of n
+  const float* m;               // kFuseLts: per column threshold m_j
+  double* sum;                  // kFuseLts: fp64 sum of s < m_j per (chunk, row quarter, column)
+};
+
+// s = (acc - y)^2 for two rows at once (FADD2/FMUL2: the same IEEE round-to-nearest results as
+// the scalar residual kernel's FADD, FMUL)
+__device__ __forceinline__ void resid2(uint32_t a0, uint32_t a1, unsigned long long y01, float& s0, float& s1) {
+  unsigned long long acc = ((unsigned long long)a1 << 32) | a0, d, sq;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(acc), "l"(y01));
+  asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sq) : "l"(d));
+  s0 = __uint_as_float((uint32_t)sq);
+  s1 = __uint_as_float((uint32_t)(sq >> 32));
+}
+
+// The per-element step of the fused cut pass (a1 + R23 + a4 on one residual): #s <= t_lo as a
+// float counter (exact: <= 2^24 per unit), s in ]t_lo, t_hi[ appended to the thread's staging
+// slots at shared address *ta.  A padded row enters as +Inf: counted nowhere.
+__device__ __forceinline__ void cut_elem(float s, float t_lo, float t_hi, float& lef, uint32_t& ta) {
+  asm volatile(
+      "{\n\t.reg .pred g, in;\n\t"
+      "setp.gt.f32 g, %2, %3;\n\t"
+      "@!g add.f32 %0, %0, 0f3F800000;\n\t"
+      "setp.lt.and.f32 in, %2, %4, g;\n\t"
+      "@in st.shared.f32 [%1], %2;\n\t"
+      "@in add.u32 %1, %1, %5;\n\t}"
+      : "+f"(lef), "+r"(ta)
+      : "f"(s), "f"(t_lo), "f"(t_hi), "n"(kSlot)
+      : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  unsigned char* stage[2] = {smem, smem + STAGE};
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + 2;
+  uint64_t* tfull = bars + 4;
+  uint64_t* tempty = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+  uint64_t* yfull = bars + 10;     // [2]: y of the tile in accumulator stage s has landed in ybuf[s]
+  float* ybuf = reinterpret_cast<float*>(smem + 2 * STAGE + 128);  // [2][FN]
+  const uint32_t ring_sa = smem_u32(smem + 2 * STAGE + 128 + 2 * FN * 4);  // 512 threads x kLaneStage B
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t units = a.n_ct_list * a.n_chunks;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], kFEpiWarps);
+      mbar_init(&yfull[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == kFYWarp) {
+    // ---------------- y stager: the tile's 256 y values into ybuf[s] once the epilogue released
+    //                  accumulator stage s (the epilogue reads them as shared-memory broadcasts)
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
+        const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
+        for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
+          const uint32_t s = it & 1, ph = (it >> 1) & 1;
+          mbar_wait_sleep(&tempty[s], ph ^ 1);
+          mbar_expect_tx(&yfull[s], FN * 4);
+          bulk_g2s(ybuf + s * FN, a.y + ((size_t)ct * a.b_ct_stride + rt) * FN, FN * 4, &yfull[s]);
+        }
+      }
+    }
+  } else if (warp == 0) {
+    // ---------------- producer: Theta tile (A) + X tile (B) per stage
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
+        const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
+        for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
+          const uint32_t s = it & 1, ph = (it >> 1) & 1;
+          mbar_wait_sleep(&empty[s], ph ^ 1);
+          mbar_expect_tx(&full[s], STAGE);
+          bulk_g2s(stage[s], a.a_img + (size_t)ct * A_IMG, A_IMG, &full[s]);
+          bulk_g2s(stage[s] + A_IMG, a.b_img + ((size_t)ct * a.b_ct_stride + rt) * B_IMG, B_IMG, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: D[j][i] = theta_j . x_i, the residual kernel's three products
+    uint32_t it = 0;
+    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const uint32_t ch = u / a.n_ct_list;
+      const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
+      for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
+        const uint32_t s = it & 1, ph = (it >> 1) & 1;
+        mbar_wait_sleep(&tempty[s], ph ^ 1);
+        mbar_wait_sleep(&full[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        if (lane == 0) {
+          const uint32_t d = tmem_base + s * FN;
+          const unsigned char* A = stage[s];
+          const unsigned char* B = stage[s] + A_IMG;
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint64_t ahi = sdesc(A + ks * 256), alo = sdesc(A + A_HALF + ks * 256);
+            const uint64_t bhi = sdesc(B + ks * 256), blo = sdesc(B + B_HALF + ks * 256);
+            mma_tf32(d, ahi, blo, ks > 0 ? 1u : 0u);  // x_lo * theta_hi (small terms first)
+            mma_tf32(d, alo, bhi, 1u);                // x_hi * theta_lo
+            mma_tf32(d, ahi, bhi, 1u);
+          }
+          mma_commit(&empty[s]);
+          mma_commit(&tfull[s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 2) {
+    // ---------------- epilogue: warps 2..17 -> TMEM lane quarter (warp % 4) = 32 candidates,
+    //                  row quarter rq: rows [rq*64, rq*64+64) of the tile
+    const int q = warp & 3;
+    const int rq = (warp - 2) >> 2;
+    const int e = threadIdx.x - 64;  // 0..511: this thread's staging slots
+    const uint32_t base_sa = ring_sa + kLaneStage * (uint32_t)e;
+    uint32_t it = 0;
+    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
+      const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
+      const uint32_t j = ct * TM + q * 32 + lane;
+      const bool col_ok = j < a.C;
+      float t_lo = 0.f, t_hi = 0.f, mj = 0.f;
+      int slot = -1;
+      if (MODE == kFuseCuts && col_ok) { t_lo = a.cuts[4 * (size_t)j]; t_hi = a.cuts[4 * (size_t)j + 1]; }
+      if (MODE == kFuseCuts && !col_ok) { t_lo = t_hi = -1.f; }  // counts nothing, copies nothing
+      if (MODE == kFuseStore && col_ok) slot = a.slot[j];
+      if (MODE == kFuseLts && col_ok) mj = a.m[j];
+      float lef = 0.f;
+      unsigned le = 0;
+      double lsum = 0.0;
+      uint32_t ta = base_sa;  // next free staging slot
+      for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
+        const uint32_t s = it & 1, ph = (it >> 1) & 1;
+        const uint64_t row0 = (uint64_t)rt * FN + rq * kFRows;
+        mbar_wait_sleep(&tfull[s], ph);
+        mbar_wait_sleep(&yfull[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * FN + rq * kFRows;
+        const ulonglong2* ys = reinterpret_cast<const ulonglong2*>(ybuf + s * FN + rq * kFRows);
+#pragma unroll 1
+        for (uint32_t c0 = 0; c0 < kFRows; c0 += 32) {
+          uint32_t r[32];
+          TMEM_LD32(taddr + c0, r);
+          const uint64_t rowc = row0 + c0;
+          ulonglong2 yv[8];
+#pragma unroll
+          for (int v = 0; v < 8; ++v) yv[v] = ys[c0 / 4 + v];
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          const int nvalid = rowc + 32 <= a.n ? 32 : (rowc >= a.n ? 0 : (int)(a.n - rowc));
+          if (MODE == kFuseCuts) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (nvalid == 32) {
+#pragma unroll
+                for (int jj = 0; jj < 16; jj += 2) {
+                  const int i = h * 16 + jj;
+                  const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+                  float s0, s1;
+                  resid2(r[i], r[i + 1], y01, s0, s1);
+                  cut_elem(s0, t_lo, t_hi, lef, ta);
+                  cut_elem(s1, t_lo, t_hi, lef, ta);
+                }
+              } else {  // the ragged end of x: padded rows enter as +Inf
+#pragma unroll
+                for (int jj = 0; jj < 16; jj += 2) {
+                  const int i = h * 16 + jj;
+                  const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+                  float s0, s1;
+                  resid2(r[i], r[i + 1], y01, s0, s1);
+                  cut_elem(i < nvalid ? s0 : __int_as_float(0x7f800000), t_lo, t_hi, lef, ta);
+                  cut_elem(i + 1 < nvalid ? s1 : __int_as_float(0x7f800000), t_lo, t_hi, lef, ta);
+                }
+              }
+              // warp-cooperative flush of every thread holding >= kFlush staged elements (at most
+              // 15 + 16 < kRing pending): each writes 16 to its column's copy as one coalesced
+              // 64-byte store of 16 lanes, and moves the rest to the front of its slots
+              const bool need = ta - base_sa >= kFlush * kSlot;
+              unsigned fm = __ballot_sync(0xffffffffu, need);
+              if (fm) {
+                unsigned long long pos = 0;
+                if (need) pos = atomicAdd(a.cursor + j, (unsigned long long)kFlush);
+                while (fm) {
+                  const int L = __ffs(fm) - 1;
+                  fm &= fm - 1;
+                  const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, L);
+                  const uint32_t cnt = (__shfl_sync(0xffffffffu, ta, L) - lb) / kSlot;
+                  const unsigned long long pl = __shfl_sync(0xffffffffu, pos, L);
+                  float v = 0.f;
+                  if ((uint32_t)lane < cnt) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + lane * kSlot));
+                  __syncwarp();
+                  if (lane < kFlush) {
+                    if (pl + lane < a.zcap) a.z[(size_t)(j - lane + L) * a.zcap + pl + lane] = v;
+                  } else if ((uint32_t)lane < cnt) {
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(lb + (lane - kFlush) * kSlot), "f"(v));
+                  }
+                  __syncwarp();
+                }
+                if (need) ta -= kFlush * kSlot;
+              }
+            }
+          } else if (MODE == kFuseStore) {
+            if (slot >= 0) {
+              float* dst = a.S + (size_t)slot * a.n + rowc;
+              if (nvalid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // 8 x 16-byte stores
+#pragma unroll
+                for (int i = 0; i < 32; i += 4) {
+                  float s0, s1, s2, s3;
+                  resid2(r[i], r[i + 1], yv[i >> 2].x, s0, s1);
+                  resid2(r[i + 2], r[i + 3], yv[i >> 2].y, s2, s3);
+                  __stcs(reinterpret_cast<float4*>(dst + i), make_float4(s0, s1, s2, s3));
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                  const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+                  float s0, s1;
+                  resid2(r[i], r[i + 1], y01, s0, s1);
+                  if (i < nvalid) __stcs(dst + i, s0);
+                  if (i + 1 < nvalid) __stcs(dst + i + 1, s1);
+                }
+              }
+            }
+          } else {
+            unsigned c = 0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+              float s0, s1;
+              resid2(r[i], r[i + 1], y01, s0, s1);
+              if (i < nvalid && s0 < mj) { lsum += (double)s0; ++c; }
+              if (i + 1 < nvalid && s1 < mj) { lsum += (double)s1; ++c; }
+            }
+            le += c;
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[s]);
+      }
+      // end of unit: flush this column's counters and the rest of its staging slots
+      if (MODE == kFuseCuts) {
+        const uint32_t cnt = (ta - base_sa) / kSlot;
+        unsigned long long pos = 0;
+        if (col_ok) {
+          atomicAdd(a.le + j, (unsigned long long)lef);
+          if (cnt) pos = atomicAdd(a.cursor + j, (unsigned long long)cnt);
+        }
+        unsigned fm = __ballot_sync(0xffffffffu, cnt > 0);
+        while (fm) {  // cooperative write-out of every thread's remaining staged elements
+          const int L = __ffs(fm) - 1;
+          fm &= fm - 1;
+          const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, L);
+          const uint32_t cl = __shfl_sync(0xffffffffu, cnt, L);
+          const unsigned long long pl = __shfl_sync(0xffffffffu, pos, L);
+          if ((uint32_t)lane < cl) {
+            float v;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + lane * kSlot));
+            if (pl + lane < a.zcap) a.z[(size_t)(j - lane + L) * a.zcap + pl + lane] = v;
+          }
+        }
+        __syncwarp();
+      } else if (MODE == kFuseLts && col_ok) {
+        atomicAdd(a.le + j, (unsigned long long)le);
+        a.sum[((size_t)ch * 4 + rq) * a.C + j] = lsum;  // fixed-order reduction afterwards
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+constexpr size_t kFusedSmem = 2 * STAGE + 1024 + 128 + 2 * FN * 4 + (size_t)kFEpiWarps * 32 * kLaneStage;  // ring, barriers, y, staging
+
+__global__ void pad_copy_kernel(const float* __restrict__ src, uint64_t n, float* __restrict__ dst, uint64_t n_pad) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (uint64_t)gridDim.x * blockDim.x)
+    dst[i] = i < n ? src[i] : 0.f;
+}
+
 }  // namespace
 
 cudaError_t lms_residuals(LmsWorkspace& w, const float* X, const float* y, uint64_t n, uint32_t p, const float* thetas,
@@ -326,14 +671,15 @@ cudaError_t lts_reduce(const float* S, uint64_t n, uint32_t C, uint64_t h, const
   return cudaGetLastError();
 }
 
-cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t C, uint64_t k, float* out,
-                           uint32_t max_iters, LmsReport* rep, cudaStream_t st) {
+// Scratch (per-CTA ping-pong buffers) + the counter block: next_col @0, stats[4] @64, fail_count @96.
+static cudaError_t run_batched(LmsWorkspace& w, BatchArgs a, LmsReport* rep, uint32_t* fail_count,
+                               cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int grid = sms * batched_blocks_per_sm();
-  if ((uint32_t)grid > C) grid = (int)C;
-  const uint64_t cap = n / 8 * 5 + 1;  // a column compacts once its bracket holds <= 5/8 of it
+  if ((uint32_t)grid > a.C) grid = (int)a.C;
+  const uint64_t cap = a.n / 8 * 5 + 1;  // a column compacts once its bracket holds <= 5/8 of it
   const size_t scratch = (size_t)grid * 2 * cap * sizeof(float);
   const size_t need = scratch + 256;
   if (w.dev_bytes < need) {
@@ -350,11 +696,13 @@ cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t
     w.host_bytes = 256;
   }
   unsigned char* base = static_cast<unsigned char*>(w.dev);
-  unsigned* next_col = reinterpret_cast<unsigned*>(base + scratch);
-  unsigned long long* stats = reinterpret_cast<unsigned long long*>(base + scratch + 64);
+  a.scratch = reinterpret_cast<float*>(base);
+  a.cap = cap;
+  a.next_col = reinterpret_cast<unsigned*>(base + scratch);
+  a.stats = reinterpret_cast<unsigned long long*>(base + scratch + 64);
+  if (a.f_le) a.fail_count = reinterpret_cast<unsigned*>(base + scratch + 96);
   cudaError_t e = cudaMemsetAsync(base + scratch, 0, 256, st);
   if (e != cudaSuccess) return e;
-  BatchArgs a{S, n, C, k, out, reinterpret_cast<float*>(base), cap, next_col, stats, max_iters};
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -362,7 +710,7 @@ cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t
   e = launch_batched_select(a, grid, st);
   if (e != cudaSuccess) return e;
   cudaEventRecord(e1, st);
-  e = cudaMemcpyAsync(w.host, stats, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  e = cudaMemcpyAsync(w.host, base + scratch + 64, 40, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
@@ -372,14 +720,361 @@ cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t
   cudaEventDestroy(e1);
   const unsigned long long* h = static_cast<const unsigned long long*>(w.host);
   if (rep) {
-    rep->passes = (uint32_t)h[0];
-    rep->cp_iters = (uint32_t)(h[0] - C);
-    rep->bytes = h[1];
-    rep->nonfinite = h[3];
-    rep->ms = ms;
+    rep->passes += (uint32_t)h[0];
+    rep->cp_iters += (uint32_t)(h[0] - a.C);
+    rep->bytes += h[1];
+    rep->nonfinite += h[3];
+    rep->ms += ms;
   }
+  if (fail_count) *fail_count = (uint32_t)(h[4] & 0xffffffffull);
   if (h[2]) return cudaErrorNotSupported;  // safeguard tripped on some column
   return cudaSuccess;
+}
+
+cudaError_t batched_select(LmsWorkspace& w, const float* S, uint64_t n, uint32_t C, uint64_t k, float* out,
+                           uint32_t max_iters, LmsReport* rep, cudaStream_t st) {
+  BatchArgs a{S, n, C, k, out, nullptr, 0, nullptr, nullptr, max_iters};
+  if (rep) *rep = LmsReport{};
+  return run_batched(w, a, rep, nullptr, st);
+}
+
+// ------------------------------------------------------------------------------------------
+// Fused path.  Geometry: candidate tiles of 128 (A = Theta), row tiles of 256 (B = X), units of
+// kRtPerUnit row tiles x one candidate tile.
+namespace {
+constexpr uint32_t kRtPerUnit = 16;
+
+struct FusedGeom {
+  uint32_t n_ct, n_rt, n_chunks, rt_per_unit = kRtPerUnit, b_ct_stride = 0;
+  unsigned char *a_img, *b_img;
+  float* y_pad;
+};
+
+__global__ void slot_map_kernel(int* slot, uint32_t C, const unsigned* list, uint32_t nlist) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < C; j += gridDim.x * blockDim.x) slot[j] = -1;
+  __syncthreads();  // (one CTA: launched with grid 1)
+  for (uint32_t i = threadIdx.x; i < nlist; i += blockDim.x) slot[list ? list[i] : i] = (int)i;
+}
+
+__global__ void lts_finish_kernel(const double* part, uint32_t nparts, uint32_t C, const unsigned long long* cnt,
+                                  uint64_t h, const float* m, double* out) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < C; j += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (uint32_t q = 0; q < nparts; ++q) acc += part[(size_t)q * C + j];  // fixed order
+    out[j] = acc + (double)(h - cnt[j]) * (double)m[j];
+  }
+}
+
+cudaError_t ensure_buf(void** p, size_t* have, size_t need) {
+  if (*have >= need) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  cudaError_t e = cudaMalloc(p, need);
+  if (e == cudaSuccess) *have = need;
+  return e;
+}
+
+cudaError_t fused_prepare(LmsWorkspace& w, const float* X, const float* y, uint64_t n, uint32_t p,
+                          const float* thetas, uint32_t C, FusedGeom& g, cudaStream_t st) {
+  g.n_ct = (C + TM - 1) / TM;
+  g.n_rt = (uint32_t)((n + FN - 1) / FN);
+  g.n_chunks = (g.n_rt + kRtPerUnit - 1) / kRtPerUnit;
+  const size_t need = (size_t)g.n_ct * A_IMG + (size_t)g.n_rt * B_IMG + (size_t)g.n_rt * FN * sizeof(float);
+  cudaError_t e = ensure_buf(&w.fimg, &w.fimg_bytes, need);
+  if (e != cudaSuccess) return e;
+  g.a_img = static_cast<unsigned char*>(w.fimg);
+  g.b_img = g.a_img + (size_t)g.n_ct * A_IMG;
+  g.y_pad = reinterpret_cast<float*>(g.b_img + (size_t)g.n_rt * B_IMG);
+  pack_rows_kernel<<<g.n_ct, TM, 0, st>>>(thetas, C, p, TM, g.a_img);
+  pack_rows_kernel<<<g.n_rt, FN, 0, st>>>(X, n, p, FN, g.b_img);
+  pad_copy_kernel<<<512, 256, 0, st>>>(y, n, g.y_pad, (uint64_t)g.n_rt * FN);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t fused_launch(const FusedGeom& g, FusedArgs a, uint32_t n_ct_list, cudaStream_t st) {
+  a.a_img = g.a_img;
+  a.b_img = g.b_img;
+  a.y = g.y_pad;
+  a.n_rt = g.n_rt;
+  a.rt_per_unit = g.rt_per_unit;
+  a.n_chunks = g.n_chunks;
+  a.b_ct_stride = g.b_ct_stride;
+  a.n_ct_list = n_ct_list;
+  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)kFusedSmem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const uint32_t units = n_ct_list * g.n_chunks;
+  const int grid = (int)(units < (uint32_t)sms ? units : (uint32_t)sms);
+  fused_tc_kernel<MODE><<<grid, kFThreads, kFusedSmem, st>>>(a);
+  return cudaGetLastError();
+}
+
+// per-column arrays in w.fcol
+struct FusedCols {
+  float* cuts;                 // 4C
+  unsigned long long* le;      // C
+  unsigned long long* cursor;  // C
+  int* slot;                   // C
+  unsigned* fail_list;         // C
+  unsigned* ct_list;           // n_ct
+  double* part;                // LTS partials (2 n_chunks x C)
+};
+
+cudaError_t fused_cols(LmsWorkspace& w, uint32_t C, const FusedGeom& g, bool lts, FusedCols& c) {
+  const size_t fixed = (size_t)C * (16 + 8 + 8 + 4 + 4 + 4) + (size_t)g.n_ct * 4 + 256;
+  const size_t part = lts ? (size_t)4 * g.n_chunks * C * sizeof(double) : 0;
+  cudaError_t e = ensure_buf(&w.fcol, &w.fcol_bytes, fixed + part);
+  if (e != cudaSuccess) return e;
+  unsigned char* b = static_cast<unsigned char*>(w.fcol);
+  c.part = reinterpret_cast<double*>(b);  // 8-byte aligned first
+  b += part;
+  c.le = reinterpret_cast<unsigned long long*>(b); b += (size_t)C * 8;
+  c.cursor = reinterpret_cast<unsigned long long*>(b); b += (size_t)C * 8;
+  c.cuts = reinterpret_cast<float*>(b); b += (size_t)C * 16;
+  c.slot = reinterpret_cast<int*>(b); b += (size_t)C * 4;
+  c.fail_list = reinterpret_cast<unsigned*>(b); b += (size_t)C * 4;
+  c.ct_list = reinterpret_cast<unsigned*>(b);
+  return cudaSuccess;
+}
+
+__global__ void iota_kernel(unsigned* v, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = i;
+}
+
+// R23 cuts of every column: the residuals of kLmsSamples evenly strided rows, computed by the fused
+// kernel in store mode (the same arithmetic: exactly elements of S), then the per-column cut search.
+// Each candidate tile draws its own rows (stride n/ms, a phase of its own): one shared row set would
+// make the sample error common to all columns, and near-identical candidates (close theta_j) would
+// then miss their cut window together.
+constexpr uint32_t kLmsSamples = 16384;
+__global__ void gather_sample_kernel(const float* __restrict__ X, const float* __restrict__ y, uint64_t n,
+                                     uint32_t p, uint32_t ms, float* __restrict__ Xs, float* __restrict__ ys) {
+  const uint32_t ct = blockIdx.y;
+  const uint64_t stride = n / ms;
+  const uint64_t phase = ((uint64_t)ct * 2654435761ull) % stride;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ms; i += gridDim.x * blockDim.x) {
+    const uint64_t row = ((uint64_t)i * n) / ms + phase;  // < n: i*n/ms + stride - 1 < n
+    float* xo = Xs + ((size_t)ct * ms + i) * p;
+    for (uint32_t l = 0; l < p; ++l) xo[l] = X[row * p + l];
+    ys[(size_t)ct * ms + i] = y[row];
+  }
+}
+
+cudaError_t fused_sample_cuts(LmsWorkspace& w, const FusedGeom& g, const float* X, const float* y, uint64_t n,
+                              uint32_t p, uint32_t C, uint64_t k, const FusedCols& c, cudaStream_t st) {
+  const uint32_t ms = kLmsSamples;
+  FusedGeom gs;
+  gs.n_ct = g.n_ct;
+  gs.n_rt = ms / FN;
+  gs.rt_per_unit = 1;
+  gs.n_chunks = gs.n_rt;
+  gs.b_ct_stride = gs.n_rt;
+  const size_t ss_bytes = (size_t)C * ms * sizeof(float);
+  const size_t img_bytes = (size_t)gs.n_ct * gs.n_rt * B_IMG;
+  const size_t need = ss_bytes + img_bytes + (size_t)gs.n_ct * ms * (p + 1) * sizeof(float);
+  cudaError_t e = ensure_buf(&w.fsamp, &w.fsamp_bytes, need);
+  if (e != cudaSuccess) return e;
+  unsigned char* b = static_cast<unsigned char*>(w.fsamp);
+  float* Ss = reinterpret_cast<float*>(b);
+  gs.b_img = b + ss_bytes;
+  float* ys = reinterpret_cast<float*>(gs.b_img + img_bytes);
+  float* Xs = ys + (size_t)gs.n_ct * ms;
+  gs.y_pad = ys;  // ms is a multiple of the row tile: no padding
+  gs.a_img = g.a_img;
+  gather_sample_kernel<<<dim3(ms / 256, gs.n_ct), 256, 0, st>>>(X, y, n, p, ms, Xs, ys);
+  pack_rows_kernel<<<gs.n_ct * gs.n_rt, FN, 0, st>>>(Xs, (uint64_t)gs.n_ct * ms, p, FN, gs.b_img);
+  slot_map_kernel<<<1, 1024, 0, st>>>(c.slot, C, nullptr, C);
+  FusedArgs a{};
+  a.n = ms; a.C = C; a.ct_list = c.ct_list; a.slot = c.slot; a.S = Ss;
+  if ((e = fused_launch<kFuseStore>(gs, a, gs.n_ct, st)) != cudaSuccess) return e;
+  return launch_lms_cuts(Ss, ms, n, C, k, c.cuts, st);
+}
+}  // namespace
+
+// Input check of the fused path: the fused pass does not test its residuals for NaN/Inf, so the
+// inputs are checked instead — every s = (x.theta - y)^2 is finite when X, y, Theta are finite and
+// B = sum_l max_i|X_il| max_j|theta_lj| + max_i|y_i| < 2^60 (|r| <= B(1 + 2^-20) with the 3xTF32
+// split and fp32 accumulation, so s < 2^121 < FLT_MAX).  out: [0] non-finite count, [1..p] max|X_l|,
+// [p+1..2p] max|theta_l|, [2p+1] max|y| (float bits; all values >= 0 so unsigned order = float order).
+__global__ void lms_check_kernel(const float* __restrict__ X, const float* __restrict__ y,
+                                 const float* __restrict__ th, uint64_t n, uint32_t p, uint32_t C,
+                                 unsigned* __restrict__ out) {
+  float mx[kLmsMaxP];
+#pragma unroll
+  for (int l = 0; l < kLmsMaxP; ++l) mx[l] = 0.f;
+  float my = 0.f, mt[kLmsMaxP];
+#pragma unroll
+  for (int l = 0; l < kLmsMaxP; ++l) mt[l] = 0.f;
+  unsigned bad = 0;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+#pragma unroll
+    for (int l = 0; l < kLmsMaxP; ++l)
+      if (l < (int)p) {
+        const float v = fabsf(X[i * p + l]);
+        bad += !(v <= 3.4028235e38f);
+        mx[l] = fmaxf(mx[l], v);
+      }
+    const float v = fabsf(y[i]);
+    bad += !(v <= 3.4028235e38f);
+    my = fmaxf(my, v);
+  }
+  for (uint64_t jj = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < C; jj += stride) {
+#pragma unroll
+    for (int l = 0; l < kLmsMaxP; ++l)
+      if (l < (int)p) {
+        const float v = fabsf(th[jj * p + l]);
+        bad += !(v <= 3.4028235e38f);
+        mt[l] = fmaxf(mt[l], v);
+      }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
+#pragma unroll
+    for (int l = 0; l < kLmsMaxP; ++l) {
+      mx[l] = fmaxf(mx[l], __shfl_xor_sync(0xffffffffu, mx[l], o));
+      mt[l] = fmaxf(mt[l], __shfl_xor_sync(0xffffffffu, mt[l], o));
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(out, bad);
+    for (uint32_t l = 0; l < p; ++l) {
+      atomicMax(out + 1 + l, __float_as_uint(mx[l]));
+      atomicMax(out + 1 + p + l, __float_as_uint(mt[l]));
+    }
+    atomicMax(out + 1 + 2 * p, __float_as_uint(my));
+  }
+}
+
+int lms_fused_check(LmsWorkspace& w, const float* X, const float* y, uint64_t n, uint32_t p, const float* thetas,
+                    uint32_t C, cudaStream_t st, cudaError_t* err) {
+  *err = ensure_buf(&w.fcol, &w.fcol_bytes, 256);
+  if (*err != cudaSuccess) return -1;
+  if (!w.host) {
+    *err = cudaHostAlloc(&w.host, 256, cudaHostAllocDefault);
+    if (*err != cudaSuccess) return -1;
+    w.host_bytes = 256;
+  }
+  unsigned* d = static_cast<unsigned*>(w.fcol);
+  if ((*err = cudaMemsetAsync(d, 0, 256, st)) != cudaSuccess) return -1;
+  lms_check_kernel<<<296, 256, 0, st>>>(X, y, thetas, n, p, C, d);
+  if ((*err = cudaMemcpyAsync(w.host, d, (2 * p + 2) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return -1;
+  if ((*err = cudaStreamSynchronize(st)) != cudaSuccess) return -1;
+  const unsigned* h = static_cast<const unsigned*>(w.host);
+  if (h[0]) return 1;
+  double B = 0.0;
+  for (uint32_t l = 0; l < p; ++l) {
+    float a, b;
+    memcpy(&a, h + 1 + l, 4);
+    memcpy(&b, h + 1 + p + l, 4);
+    B += (double)a * (double)b;
+  }
+  float my;
+  memcpy(&my, h + 1 + 2 * p, 4);
+  B += (double)my;
+  return B < 1152921504606846976.0 /* 2^60 */ ? 0 : 2;
+}
+
+cudaError_t lms_fused_residuals(LmsWorkspace& w, const float* X, const float* y, uint64_t n, uint32_t p,
+                                const float* thetas, uint32_t C, float* S, cudaStream_t st) {
+  FusedGeom g;
+  cudaError_t e = fused_prepare(w, X, y, n, p, thetas, C, g, st);
+  if (e != cudaSuccess) return e;
+  FusedCols c;
+  if ((e = fused_cols(w, C, g, false, c)) != cudaSuccess) return e;
+  slot_map_kernel<<<1, 1024, 0, st>>>(c.slot, C, nullptr, C);
+  iota_kernel<<<1, 256, 0, st>>>(c.ct_list, g.n_ct);
+  FusedArgs a{};
+  a.n = n; a.C = C; a.ct_list = c.ct_list; a.slot = c.slot; a.S = S;
+  return fused_launch<kFuseStore>(g, a, g.n_ct, st);
+}
+
+cudaError_t lms_fused_select(LmsWorkspace& w, const float* X, const float* y, uint64_t n, uint32_t p,
+                             const float* thetas, uint32_t C, uint64_t k, float* out, uint32_t max_iters,
+                             LmsReport* rep, cudaStream_t st) {
+  if (rep) *rep = LmsReport{};
+  FusedGeom g;
+  cudaError_t e = fused_prepare(w, X, y, n, p, thetas, C, g, st);
+  if (e != cudaSuccess) return e;
+  FusedCols c;
+  if ((e = fused_cols(w, C, g, false, c)) != cudaSuccess) return e;
+  // per-column copy of ]t_lo, t_hi[: the cuts keep ~2 x 3.5 sd of 4096 samples (<= ~5.6% of n);
+  // n/8 leaves room for any k (an overflowing column falls back, counts stay exact)
+  const uint64_t zcap = n / 8 + 64;
+  if ((e = ensure_buf(reinterpret_cast<void**>(&w.fz), &w.fz_bytes, (size_t)C * zcap * sizeof(float))) != cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(c.le, 0, (size_t)C * 16, st)) != cudaSuccess) return e;  // le + cursor
+  iota_kernel<<<1, 256, 0, st>>>(c.ct_list, g.n_ct);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  if ((e = fused_sample_cuts(w, g, X, y, n, p, C, k, c, st)) != cudaSuccess) return e;
+  FusedArgs a{};
+  a.n = n; a.C = C; a.ct_list = c.ct_list;
+  a.cuts = c.cuts; a.le = c.le; a.cursor = c.cursor; a.z = w.fz; a.zcap = zcap;
+  if ((e = fused_launch<kFuseCuts>(g, a, g.n_ct, st)) != cudaSuccess) return e;
+  cudaEventRecord(e1, st);
+  // continuation on the per-column copies
+  BatchArgs b{nullptr, n, C, k, out, nullptr, 0, nullptr, nullptr, max_iters};
+  b.f_cuts = c.cuts; b.f_le = c.le; b.f_cursor = c.cursor; b.f_z = w.fz; b.f_zcap = zcap;
+  b.fail_list = c.fail_list;
+  uint32_t nfail = 0;
+  e = run_batched(w, b, rep, &nfail, st);
+  float fms = 0.f;
+  cudaEventElapsedTime(&fms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rep) { rep->ms_fused = fms; rep->fallback = nfail; }
+  if (e != cudaSuccess) return e;
+  if (nfail == 0) return cudaSuccess;
+  // fallback: store S for the failed columns only (same kernel, same arithmetic), select from it
+  std::vector<unsigned> fl(nfail);
+  if ((e = cudaMemcpy(fl.data(), c.fail_list, nfail * sizeof(unsigned), cudaMemcpyDeviceToHost)) != cudaSuccess)
+    return e;
+  std::vector<unsigned> cts;
+  for (unsigned j : fl) {
+    const unsigned t = j / TM;
+    bool seen = false;
+    for (unsigned u : cts) seen |= (u == t);
+    if (!seen) cts.push_back(t);
+  }
+  if ((e = cudaMemcpyAsync(c.ct_list, cts.data(), cts.size() * sizeof(unsigned), cudaMemcpyHostToDevice, st)) !=
+      cudaSuccess)
+    return e;
+  if ((e = ensure_buf(reinterpret_cast<void**>(&w.fS), &w.fS_bytes, (size_t)nfail * n * sizeof(float))) != cudaSuccess)
+    return e;
+  slot_map_kernel<<<1, 1024, 0, st>>>(c.slot, C, c.fail_list, nfail);
+  FusedArgs sa{};
+  sa.n = n; sa.C = C; sa.ct_list = c.ct_list; sa.slot = c.slot; sa.S = w.fS;
+  if ((e = fused_launch<kFuseStore>(g, sa, (uint32_t)cts.size(), st)) != cudaSuccess) return e;
+  BatchArgs f{w.fS, n, nfail, k, out, nullptr, 0, nullptr, nullptr, max_iters};
+  f.out_map = c.fail_list;
+  return run_batched(w, f, rep, nullptr, st);
+}
+
+cudaError_t lms_fused_lts(LmsWorkspace& w, const float* X, const float* y, uint64_t n, uint32_t p,
+                          const float* thetas, uint32_t C, uint64_t h, const float* m, double* out, cudaStream_t st) {
+  FusedGeom g;
+  cudaError_t e = fused_prepare(w, X, y, n, p, thetas, C, g, st);
+  if (e != cudaSuccess) return e;
+  FusedCols c;
+  if ((e = fused_cols(w, C, g, true, c)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.le, 0, (size_t)C * 8, st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(c.part, 0, (size_t)4 * g.n_chunks * C * sizeof(double), st)) != cudaSuccess) return e;
+  iota_kernel<<<1, 256, 0, st>>>(c.ct_list, g.n_ct);
+  FusedArgs a{};
+  a.n = n; a.C = C; a.ct_list = c.ct_list; a.le = c.le; a.m = m; a.sum = c.part;
+  if ((e = fused_launch<kFuseLts>(g, a, g.n_ct, st)) != cudaSuccess) return e;
+  lts_finish_kernel<<<(C + 255) / 256, 256, 0, st>>>(c.part, 4 * g.n_chunks, C, c.le, h, m, out);
+  return cudaGetLastError();
 }
 
 void lms_free(LmsWorkspace& w) {
@@ -387,6 +1082,11 @@ void lms_free(LmsWorkspace& w) {
   if (w.dev) cudaFree(w.dev);
   if (w.img) cudaFree(w.img);
   if (w.host) cudaFreeHost(w.host);
+  if (w.fimg) cudaFree(w.fimg);
+  if (w.fcol) cudaFree(w.fcol);
+  if (w.fz) cudaFree(w.fz);
+  if (w.fS) cudaFree(w.fS);
+  if (w.fsamp) cudaFree(w.fsamp);
   w = LmsWorkspace{};
 }
 

@@ -133,3 +133,82 @@ def test_lts_objective_vs_oracle(cp, h_rule):
         ref = O.lts_objective(S[j].astype(np.float64), h)
         assert F[j] == pytest.approx(ref, rel=1e-11), (j, F[j], ref)   # fp64 sums, different order
     assert F[:16].max() < F[-16:].min()
+
+
+# ---------------------------------------------------------------------------------- fused path
+# §8f-2: with lms_fused=1 (default, n >= 16384) S is never stored: the residuals are recomputed in
+# the tcgen05 epilogue of one fused pass.  cpsel_lms_residuals returns the S of that same kernel
+# (store mode), so every selected value must be an order statistic of it, bit-exact.
+
+def _fused_problem(n=60_013, C=333, seed=5):
+    X, y, th, _ = datagen.lms_problem(n=n, p=10, C=C)
+    return X, y, th
+
+
+@pytest.mark.parametrize("which", ["k1", "tenth", "median", "n_minus_1", "n"])
+def test_fused_kth_every_column_bit_exact(cp, which):
+    """every column, ranks at both ends and the middle (k via the LTS entry point, whose m_j is
+    the fused k-th order statistic), against the oracle on the fused kernel's own S."""
+    X, y, th = _fused_problem()
+    n = X.shape[0]
+    h = {"k1": 1, "tenth": n // 10, "median": O.median_rank(n), "n_minus_1": n - 1, "n": n}[which]
+    Xd, yd, thd = dev(X), dev(y), dev(th)
+    F, m = cp.lts_objective(Xd, yd, thd, h)
+    m, F = m.cpu().numpy(), F.cpu().numpy()
+    S = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+    for j in range(th.shape[0]):
+        assert m[j] == O.order_statistic(S[j], h), (which, j)
+    for j in range(0, th.shape[0], 17):
+        ref = O.lts_objective(S[j].astype(np.float64), h)
+        assert F[j] == pytest.approx(ref, rel=1e-11), (j, F[j], ref)
+
+
+def test_fused_matches_unfused_path(cp):
+    """lms_fused=0 (S stored by the row-major residual kernel, then the batched select) and
+    lms_fused=1 agree within the 3xTF32 bound; each is bit-exact on its own S."""
+    X, y, th = _fused_problem(n=70_001, C=260)
+    Xd, yd, thd = dev(X), dev(y), dev(th)
+    k = O.median_rank(X.shape[0])
+    try:
+        cp.set_config(lms_fused=0)
+        g0 = cp.lms_objective(Xd, yd, thd).cpu().numpy()
+        S0 = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+    finally:
+        cp.set_config(lms_fused=1)
+    g1 = cp.lms_objective(Xd, yd, thd).cpu().numpy()
+    S1 = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+    for j in range(0, 260, 13):
+        assert g0[j] == O.order_statistic(S0[j], k)
+        assert g1[j] == O.order_statistic(S1[j], k)
+    assert np.all(np.abs(g0.astype(np.float64) - g1) <= np.max(np.abs(S0.astype(np.float64) - S1), axis=1) + 1e-30)
+
+
+def test_fused_fallback_columns(cp):
+    """Adversarial sample rows: y is huge exactly at the rows the cut stage samples (16384 evenly
+    strided rows per candidate tile of 128, phase (tile * 2654435761) mod stride), so every
+    column's sample cuts lie far above its median; the fused copy cannot finish any column and all
+    of them must go through the stored-S fallback — still bit-exact."""
+    X, y, th = _fused_problem(n=200_000, C=130)
+    n = X.shape[0]
+    ms = 16384                                                          # kLmsSamples
+    stride = n // ms
+    y = y.copy()
+    for ct in range((th.shape[0] + 127) // 128):
+        rows = (np.arange(ms, dtype=np.int64) * n) // ms + (ct * 2654435761) % stride
+        y[rows] = 1e4
+    Xd, yd, thd = dev(X), dev(y), dev(th)
+    got, info = cp.lms_objective(Xd, yd, thd, return_info=True)
+    got = got.cpu().numpy()
+    assert info["fallback_steps"] == th.shape[0]
+    S = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+    k = O.median_rank(n)
+    for j in range(th.shape[0]):
+        assert got[j] == O.order_statistic(S[j], k), j
+
+
+def test_fused_nonfinite_rejected(cp):
+    X, y, th = _fused_problem(n=20_000, C=40)
+    y = y.copy()
+    y[777] = np.nan
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        cp.lms_objective(dev(X), dev(y), dev(th))
