@@ -291,19 +291,22 @@ __device__ __forceinline__ void resid2(uint32_t a0, uint32_t a1, unsigned long l
   s1 = __uint_as_float((uint32_t)(sq >> 32));
 }
 
-// The per-element step of the fused cut pass (a1 + R23 + a4 on one residual): #s <= t_lo as a
-// float counter (exact: <= 2^24 per unit), s in ]t_lo, t_hi[ appended to the thread's staging
-// slots at shared address *ta.  A padded row enters as +Inf: counted nowhere.
-__device__ __forceinline__ void cut_elem(float s, float t_lo, float t_hi, float& lef, uint32_t& ta) {
+// The per-element step of the fused cut pass (a1 + R23 + a4 on one residual).  Every s is >= 0 (or
+// +Inf for a padded row), so float order is unsigned order of the bits: with d = bits(s) - lo1,
+// lo1 = bits(t_lo) + 1, s <= t_lo iff d wraps (its top bit is set: #s <= t_lo += d >> 31) and
+// t_lo < s < t_hi iff d < w, w = bits(t_hi) - lo1 (unsigned).  Interior s are appended to the
+// thread's staging slots at shared address ta.  5 instructions per element after the residual.
+__device__ __forceinline__ void cut_elem(float s, uint32_t lo1, uint32_t w, uint32_t& le, uint32_t& ta) {
   asm volatile(
-      "{\n\t.reg .pred g, in;\n\t"
-      "setp.gt.f32 g, %2, %3;\n\t"
-      "@!g add.f32 %0, %0, 0f3F800000;\n\t"
-      "setp.lt.and.f32 in, %2, %4, g;\n\t"
-      "@in st.shared.f32 [%1], %2;\n\t"
-      "@in add.u32 %1, %1, %5;\n\t}"
-      : "+f"(lef), "+r"(ta)
-      : "f"(s), "f"(t_lo), "f"(t_hi), "n"(kSlot)
+      "{\n\t.reg .pred in;\n\t.reg .u32 d, c;\n\t"
+      "sub.u32 d, %2, %3;\n\t"
+      "shr.u32 c, d, 31;\n\t"
+      "add.u32 %0, %0, c;\n\t"
+      "setp.lt.u32 in, d, %4;\n\t"
+      "@in st.shared.f32 [%1], %5;\n\t"
+      "@in add.u32 %1, %1, %6;\n\t}"
+      : "+r"(le), "+r"(ta)
+      : "r"(__float_as_uint(s)), "r"(lo1), "r"(w), "f"(s), "n"(kSlot)
       : "memory");
 }
 
@@ -417,14 +420,17 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
       const uint32_t j = ct * TM + q * 32 + lane;
       const bool col_ok = j < a.C;
-      float t_lo = 0.f, t_hi = 0.f, mj = 0.f;
+      float mj = 0.f;
+      uint32_t lo1 = 0x80000000u, wcut = 0u;  // a column past C: copies nothing (its counts are dropped)
       int slot = -1;
-      if (MODE == kFuseCuts && col_ok) { t_lo = a.cuts[4 * (size_t)j]; t_hi = a.cuts[4 * (size_t)j + 1]; }
-      if (MODE == kFuseCuts && !col_ok) { t_lo = t_hi = -1.f; }  // counts nothing, copies nothing
+      if (MODE == kFuseCuts && col_ok) {
+        const uint32_t bl = __float_as_uint(a.cuts[4 * (size_t)j]), bh = __float_as_uint(a.cuts[4 * (size_t)j + 1]);
+        lo1 = bl + 1u;
+        wcut = bh - lo1;  // the cuts are >= +0 and t_lo < t_hi
+      }
       if (MODE == kFuseStore && col_ok) slot = a.slot[j];
       if (MODE == kFuseLts && col_ok) mj = a.m[j];
-      float lef = 0.f;
-      unsigned le = 0;
+      uint32_t le = 0;
       double lsum = 0.0;
       uint32_t ta = base_sa;  // next free staging slot
       for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
@@ -455,8 +461,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
                   const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
                   float s0, s1;
                   resid2(r[i], r[i + 1], y01, s0, s1);
-                  cut_elem(s0, t_lo, t_hi, lef, ta);
-                  cut_elem(s1, t_lo, t_hi, lef, ta);
+                  cut_elem(s0, lo1, wcut, le, ta);
+                  cut_elem(s1, lo1, wcut, le, ta);
                 }
               } else {  // the ragged end of x: padded rows enter as +Inf
 #pragma unroll
@@ -465,8 +471,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
                   const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
                   float s0, s1;
                   resid2(r[i], r[i + 1], y01, s0, s1);
-                  cut_elem(i < nvalid ? s0 : __int_as_float(0x7f800000), t_lo, t_hi, lef, ta);
-                  cut_elem(i + 1 < nvalid ? s1 : __int_as_float(0x7f800000), t_lo, t_hi, lef, ta);
+                  cut_elem(i < nvalid ? s0 : __int_as_float(0x7f800000), lo1, wcut, le, ta);
+                  cut_elem(i + 1 < nvalid ? s1 : __int_as_float(0x7f800000), lo1, wcut, le, ta);
                 }
               }
               // warp-cooperative flush of every thread holding >= kFlush staged elements (at most
@@ -477,19 +483,28 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
               if (fm) {
                 unsigned long long pos = 0;
                 if (need) pos = atomicAdd(a.cursor + j, (unsigned long long)kFlush);
-                while (fm) {
-                  const int L = __ffs(fm) - 1;
+                while (fm) {  // two threads per round: half-warp h serves owner h
+                  const int A = __ffs(fm) - 1;
                   fm &= fm - 1;
-                  const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, L);
-                  const uint32_t cnt = (__shfl_sync(0xffffffffu, ta, L) - lb) / kSlot;
-                  const unsigned long long pl = __shfl_sync(0xffffffffu, pos, L);
-                  float v = 0.f;
-                  if ((uint32_t)lane < cnt) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + lane * kSlot));
+                  int Bo = -1;
+                  if (fm) {
+                    Bo = __ffs(fm) - 1;
+                    fm &= fm - 1;
+                  }
+                  const int l16 = lane & 15;
+                  const int owner = (lane < 16) ? A : Bo;
+                  const int src = owner < 0 ? A : owner;
+                  const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, src);
+                  const uint32_t cnt = (__shfl_sync(0xffffffffu, ta, src) - lb) / kSlot;
+                  const unsigned long long pl = __shfl_sync(0xffffffffu, pos, src);
+                  float v = 0.f, v2 = 0.f;
+                  const bool mv = owner >= 0 && (uint32_t)(kFlush + l16) < cnt;
+                  if (owner >= 0) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + l16 * kSlot));
+                  if (mv) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v2) : "r"(lb + (kFlush + l16) * kSlot));
                   __syncwarp();
-                  if (lane < kFlush) {
-                    if (pl + lane < a.zcap) a.z[(size_t)(j - lane + L) * a.zcap + pl + lane] = v;
-                  } else if ((uint32_t)lane < cnt) {
-                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(lb + (lane - kFlush) * kSlot), "f"(v));
+                  if (owner >= 0) {
+                    if (pl + l16 < a.zcap) a.z[(size_t)(j - lane + src) * a.zcap + pl + l16] = v;
+                    if (mv) asm volatile("st.shared.f32 [%0], %1;" ::"r"(lb + l16 * kSlot), "f"(v2));
                   }
                   __syncwarp();
                 }
@@ -540,7 +555,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         const uint32_t cnt = (ta - base_sa) / kSlot;
         unsigned long long pos = 0;
         if (col_ok) {
-          atomicAdd(a.le + j, (unsigned long long)lef);
+          atomicAdd(a.le + j, (unsigned long long)le);
           if (cnt) pos = atomicAdd(a.cursor + j, (unsigned long long)cnt);
         }
         unsigned fm = __ballot_sync(0xffffffffu, cnt > 0);
@@ -1005,7 +1020,7 @@ cudaError_t lms_fused_select(LmsWorkspace& w, const float* X, const float* y, ui
   if (e != cudaSuccess) return e;
   FusedCols c;
   if ((e = fused_cols(w, C, g, false, c)) != cudaSuccess) return e;
-  // per-column copy of ]t_lo, t_hi[: the cuts keep ~2 x 3.5 sd of 4096 samples (<= ~5.6% of n);
+  // per-column copy of ]t_lo, t_hi[: the cuts keep ~2 x 3.5 sd of 16384 samples (~2.8% of n);
   // n/8 leaves room for any k (an overflowing column falls back, counts stay exact)
   const uint64_t zcap = n / 8 + 64;
   if ((e = ensure_buf(reinterpret_cast<void**>(&w.fz), &w.fz_bytes, (size_t)C * zcap * sizeof(float))) != cudaSuccess)
