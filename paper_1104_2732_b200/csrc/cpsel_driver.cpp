@@ -85,6 +85,8 @@ struct cpsel_ctx {
     DevInit init;
     double radix_value;
     unsigned long long seq_pass, seq_init, seq_radix;
+    double direct_value;                        // exact_cluster_kernel (small arrays, §8f-3)
+    unsigned long long direct_bad, seq_direct;
     ChainMail chain;  // the device chain's step decisions (§8f-3)
   };
   Mailbox* mb = nullptr;      // host view
@@ -1507,8 +1509,63 @@ void store_value(double v, cpsel_dtype dt, void* h_out) {
   }
 }
 
+// Small arrays (n <= direct_threshold and <= the cluster's register capacity): the whole selection
+// is one exact_cluster_kernel launch and one mailbox wait (§8f-3, BASELINE configs[0]).
+cpsel_status run_direct(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k, void* h_out,
+                        cpsel_info* info) {
+  const auto t0 = std::chrono::steady_clock::now();
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const bool timed = ctx->cfg.record_timing != 0;
+  if (timed) {
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, ctx->stream));
+  }
+  const unsigned long long seq = ++ctx->seq;
+  CK(launch_exact_cluster((int)dtype, d_x, n, k, &ctx->mb_dev->direct_value, &ctx->mb_dev->direct_bad,
+                          &ctx->mb_dev->seq_direct, seq, ctx->stream));
+  if (timed) CK(cudaEventRecord(e1, ctx->stream));
+  const volatile unsigned long long* f = &ctx->mb->seq_direct;
+  for (uint32_t i = 1; *f != seq; ++i) {
+    if ((i & 255u) == 0u) {
+      const cudaError_t e = cudaStreamQuery(ctx->stream);
+      if (e == cudaSuccess && *f != seq) return fail(ctx, CPSEL_EINTERNAL, "kernel finished without publishing its result");
+      if (e != cudaSuccess && e != cudaErrorNotReady) return fail(ctx, CPSEL_ECUDA, "%s", cudaGetErrorString(e));
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
+  const double v = ctx->mb->direct_value;
+  const unsigned long long bad = ctx->mb->direct_bad;
+  float kms = 0.f;
+  if (timed) {
+    CK(cudaEventSynchronize(e1));
+    cudaEventElapsedTime(&kms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  ctx->trace.clear();
+  if (bad) return fail(ctx, CPSEL_ENONFINITE, "input holds NaN or Inf");
+  if (info) {
+    memset(info, 0, sizeof *info);
+    info->passes = 1;
+    info->exit_reason = 6;  // direct select
+    info->z_count = n;
+    info->bytes_moved = n * elem_size(dtype);
+    info->launches = 1;
+    info->kernel_ms_select = kms;
+    info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  store_value(v, dtype, h_out);
+  return CPSEL_OK;
+}
+
 cpsel_status run_single(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k, void* h_out,
                         cpsel_info* info) {
+  if (!ctx->cfg.force_cp && n <= ctx->cfg.direct_threshold && n <= exact_cluster_cap((int)dtype))
+    return run_direct(ctx, d_x, n, dtype, k, h_out, info);
   GpuBackend be(ctx, d_x, n, (int)dtype);
   be.chain_select_cap = auto_select_cap(ctx->cfg);
   const uint64_t zc = auto_z_cap(n, ctx->cfg);

@@ -2981,6 +2981,173 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
   }
 }
 
+// §8f-3 for small arrays (BASELINE configs[0], n = 1e5): the WHOLE selection as one launch.  The
+// array (m <= 8 x 1024 x KPT elements) is held in the registers of one 8-CTA cluster as
+// order-preserving keys, sorted per thread, and x_(r) is found by an exact MSB radix select (all
+// digit rounds: 3 for f32, 6 for f64) whose per-CTA run-aggregated histograms are merged into CTA 0
+// over distributed shared memory; non-finite keys are counted on the way (R12).  CTA 0 publishes the
+// value (canonical +0, R13) and the non-finite count into the mailbox: no init pass, no host round
+// trip between rounds.
+struct ExactSel {
+  unsigned loc[2048];
+  unsigned glob[2048];
+  unsigned csum[32];
+  unsigned long long prefix, mask, rank, bad;
+};
+template <typename T, int KPT>
+__global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
+    exact_cluster_kernel(const T* __restrict__ x, uint64_t m, uint64_t r, double* vout, unsigned long long* bad_out,
+                         unsigned long long* done, unsigned long long seq) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  using SK = SampleKey<T>;
+  using K = typename SK::K;
+  constexpr int ROUNDS = sizeof(T) == 4 ? 3 : 6;
+  __shared__ ExactSel sh;
+  const unsigned crank = cl.block_rank();
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  K keys[KPT];
+  unsigned bad = 0;
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const uint64_t g = ((uint64_t)j * kSampleCluster + crank) * 1024 + i;  // coalesced per warp
+    keys[j] = ~K(0);                                                      // padding: sorts last
+    if (g < m) {
+      keys[j] = SK::key(x[g]);
+      bad += (keys[j] < SK::KLO || keys[j] > SK::KHI) ? 1u : 0u;           // NaN, +-Inf
+    }
+  }
+#pragma unroll
+  for (int size = 2; size <= KPT; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int l = j ^ stride;
+        if (l > j) {
+          const K a = keys[j], b = keys[l];
+          const bool up = (j & size) == 0;
+          keys[j] = up ? (a < b ? a : b) : (a < b ? b : a);
+          keys[l] = up ? (a < b ? b : a) : (a < b ? a : b);
+        }
+      }
+    }
+  }
+  if (i == 0) {
+    sh.prefix = 0;
+    sh.mask = 0;
+    sh.rank = r - 1;
+    sh.bad = 0;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) bad += __shfl_xor_sync(FULL, bad, o);
+  ExactSel* sh0 = cl.map_shared_rank(&sh, 0);
+  cl.sync();  // CTA 0's state initialised
+  if (lane == 0 && bad) atomicAdd(&sh0->bad, (unsigned long long)bad);
+  for (int rd = 0; rd < ROUNDS; ++rd) {
+    const int shift = SK::shift(rd), nb = 1 << SK::bits(rd);
+    for (int b = i; b < 2048; b += 1024) {
+      sh.loc[b] = 0u;
+      if (crank == 0) sh.glob[b] = 0u;
+    }
+    cl.sync();  // CTA 0's prefix and zeroed histogram visible to every CTA
+    const K pt = (K)sh0->prefix, mt = (K)sh0->mask;
+    unsigned run = 0;
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {  // run-aggregated: the thread's keys are sorted
+      const K k = keys[j];
+      const bool in = (k & mt) == pt;
+      const unsigned d = (unsigned)(k >> shift) & (unsigned)(nb - 1);
+      run += in ? 1u : 0u;
+      bool last = in;
+      if (j + 1 < KPT) {
+        const K kn = keys[j + 1 < KPT ? j + 1 : j];
+        last = in && (((kn & mt) != pt) || (((unsigned)(kn >> shift) & (unsigned)(nb - 1)) != d));
+      }
+      if (last) {
+        atomicAdd(&sh.loc[d], run);
+        run = 0;
+      }
+    }
+    __syncthreads();
+    unsigned* glob0 = cl.map_shared_rank(&sh.glob[0], 0);
+    for (int b = i; b < 2048; b += 1024) {
+      const unsigned v = sh.loc[b];
+      if (v) atomicAdd(glob0 + b, v);
+    }
+    cl.sync();  // the cluster's histogram complete in CTA 0
+    if (crank == 0) {
+      const int c0 = warp * 64;
+      unsigned v = (c0 + lane < nb ? sh.glob[c0 + lane] : 0u) + (c0 + 32 + lane < nb ? sh.glob[c0 + 32 + lane] : 0u);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+      if (lane == 0) sh.csum[warp] = v;
+      __syncthreads();
+      if (warp == 0) {
+        const unsigned long long rk = sh.rank;
+        const unsigned cs = sh.csum[lane];
+        unsigned incl = cs;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(FULL, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const unsigned hm = __ballot_sync(FULL, (unsigned long long)incl > rk);
+        const int c = __ffs(hm) - 1;
+        unsigned long long before = __shfl_sync(FULL, incl - cs, c);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const int b = c * 64 + half * 32 + lane;
+          const unsigned h = b < nb ? sh.glob[b] : 0u;
+          unsigned in2 = h;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const unsigned y = __shfl_up_sync(FULL, in2, o);
+            if (lane >= o) in2 += y;
+          }
+          const unsigned hb = __ballot_sync(FULL, before + in2 > rk);
+          if (hb) {
+            const int src = __ffs(hb) - 1;
+            const unsigned ex = __shfl_sync(FULL, in2 - h, src);
+            if (lane == 0) {
+              sh.prefix |= (unsigned long long)(c * 64 + half * 32 + src) << shift;
+              sh.mask |= (unsigned long long)(nb - 1) << shift;
+              sh.rank = rk - (before + ex);
+            }
+            break;
+          }
+          before += __shfl_sync(FULL, in2, 31);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cl.sync();
+  if (crank == 0 && i == 0) {
+    const double v = (double)SK::val((K)sh.prefix);
+    *vout = v == 0.0 ? 0.0 : v;
+    *bad_out = sh.bad;
+    publish_done(done, seq);
+  }
+}
+
+constexpr int kExactKPT32 = 16, kExactKPT64 = 8;
+uint64_t exact_cluster_cap(int dtype) {
+  return (uint64_t)kSampleCluster * 1024 * (dtype == kF32 ? kExactKPT32 : kExactKPT64);
+}
+cudaError_t launch_exact_cluster(int dtype, const void* x, uint64_t m, uint64_t r, double* vout,
+                                 unsigned long long* bad_out, unsigned long long* done, unsigned long long seq,
+                                 cudaStream_t st) {
+  if (m == 0 || m > exact_cluster_cap(dtype) || r < 1 || r > m) return cudaErrorInvalidValue;
+  if (dtype == kF32)
+    exact_cluster_kernel<float, kExactKPT32><<<kSampleCluster, 1024, 0, st>>>(static_cast<const float*>(x), m, r, vout,
+                                                                              bad_out, done, seq);
+  else
+    exact_cluster_kernel<double, kExactKPT64><<<kSampleCluster, 1024, 0, st>>>(static_cast<const double*>(x), m, r,
+                                                                               vout, bad_out, done, seq);
+  return cudaGetLastError();
+}
+
 template <typename T, int KPT>
 cudaError_t sample_cluster_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
                              cudaStream_t st, const ChainState* chain, int which) {

@@ -204,6 +204,13 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 // tab != nullptr: the input is the runs `side` of the segmented array based at z (tab[0..Wtot),
 // the segmented grid).  One launch per digit (f32: 3, f64: 6); the last CTA of each picks the digit
 // (ticket: a self-resetting grid counter).
+// §8f-3 small arrays: x_(r) of x[0..m) (m <= exact_cluster_cap) by ONE 8-CTA cluster launch (exact
+// radix select in registers + DSMEM histograms); *vout = value (canonical +0), *bad_out = #NaN/Inf,
+// then `seq` published to *done.
+uint64_t exact_cluster_cap(int dtype);
+cudaError_t launch_exact_cluster(int dtype, const void* x, uint64_t m, uint64_t r, double* vout,
+                                 unsigned long long* bad_out, unsigned long long* done, unsigned long long seq,
+                                 cudaStream_t st);
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned int* hist, const LaunchShape& s, cudaStream_t st,
                                 double* vout, unsigned long long* done, unsigned long long seq,

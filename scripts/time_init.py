@@ -41,3 +41,7 @@ k = m(ini) + m(pas) + m(sel) + m(smp)
 print(f"{dist} 2^{lg} {dtype}{' sharded' if sharded else ''}: init {m(ini):.4f}  passes {m(pas):.4f}  select {m(sel):.4f}  "
       f"sample {m(smp):.4f}  kernels {k:.4f}  "
       f"driver wall {m(tot):.4f}  python wall {m(wall):.4f} ms  passes/call {m(passes):.1f}")
+if "--trace" in sys.argv:
+    for r in cp.get_trace(torch.cuda.current_device()):
+        print(f"  kind {r['kind']} scanned {r['scanned']:>11} written {r['written']:>10} interior {r['interior']:>11} "
+              f"compacted {r['compacted']} kernel_ms {r['kernel_ms']:.4f}")

@@ -205,6 +205,36 @@ def test_select_direct_path_config0(cp):
     assert info["exit"] in ("direct_select", "init_min", "init_max")
 
 
+@pytest.mark.parametrize("dtype,n", [("f32", 131_072), ("f32", 131_071), ("f32", 4097), ("f64", 65_536),
+                                     ("f64", 65_537), ("f64", 3)])
+def test_select_direct_one_launch_bounds(cp, dtype, n):
+    """§8f-3 small arrays: n <= direct_threshold and within the 8-CTA cluster's register capacity
+    (2^17 f32, 2^16 f64) is ONE exact_cluster_kernel launch; just above it the init + radix path.
+    Duplicates, signed zeros and a huge dynamic range; every rank class bit-exact."""
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal(n) * np.exp(rng.uniform(-30, 30, n))).astype(np.float32 if dtype == "f32" else np.float64)
+    x[::7] = x[n // 2]                                       # a value with many copies
+    x[1::11] = -0.0
+    x[2::13] = 0.0
+    xd = tdev(x)
+    for k in sorted({1, 2, n // 3, O.median_rank(n), n - 1, n}):
+        v, info = cp.select_kth(xd, k, return_info=True)
+        assert canon(v) == float(O.order_statistic(x, k)), (dtype, n, k, info)
+    cap = 131_072 if dtype == "f32" else 65_536
+    if n <= cap:
+        assert info["launches"] == 1 and info["exit"] == "direct_select"
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+def test_select_direct_one_launch_rejects_nonfinite(cp, bad):
+    x = datagen.make("uniform", 100_000, "f32")
+    x[99_999] = bad
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        cp.median(tdev(x))
+    x[99_999] = 0.5
+    assert canon(cp.median(tdev(x))) == float(O.median(x))
+
+
 @pytest.mark.parametrize("dist", datagen.BENCH_DISTS)
 def test_select_config1_2pow24_f32(cp, dist):
     """BASELINE configs[1]: n=2^24 float32, k in {median, 1, n/10, n-1}."""
