@@ -58,7 +58,10 @@ typedef struct {
   uint32_t max_iters;        /* safety cap on cutting-plane passes (P:L169 maxit).  Default 200 */
   int32_t force_cp;          /* 1: always run cutting-plane passes (parity runs), ignore direct_threshold */
   int32_t record_trace;      /* 1: keep the per-iteration trace (cpsel_get_trace).  Default 1 */
-  int32_t record_timing;     /* 1: time every kernel with CUDA events on the ctx stream (info / trace
+  int32_t record_timing;     /* 2: light — only each selection's init kernel is bracketed by CUDA
+                                events, kept in a ring read by cpsel_init_timings (nothing is read
+                                back during the calls).
+                                1: time every kernel with CUDA events on the ctx stream (info / trace
                                 kernel_ms fields).  Default 0 */
   int32_t init_cut;          /* 1: the init pass also evaluates two extra cuts at sample quantiles
                                 bracketing the target rank (R23), saving passes.  Default 1 */
@@ -206,6 +209,10 @@ cpsel_status cpsel_init(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype
 cpsel_status cpsel_small_select(cpsel_ctx* ctx, const void* d_z, uint64_t m, cpsel_dtype dtype,
                                 uint64_t r, void* h_out);
 /* Copy up to max_rows rows of the last call's trace into rows; *n_rows = rows available. */
+/* record_timing == 2: *n_out = init-kernel durations recorded since the last reset; ms[0..min(n,max))
+ * receives them (CUDA-event ms, in call order; waits for the events).  reset != 0 empties the ring.
+ * ms may be NULL (count only).  Errors: EINVAL (null ctx / n_out), ECUDA. */
+cpsel_status cpsel_init_timings(cpsel_ctx* ctx, double* ms, uint32_t max, uint32_t* n_out, int32_t reset);
 cpsel_status cpsel_get_trace(const cpsel_ctx* ctx, cpsel_trace_row* rows, uint32_t max_rows,
                              uint32_t* n_rows);
 

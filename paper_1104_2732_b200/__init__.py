@@ -108,7 +108,7 @@ SYMBOLS = [
     "cpsel_create", "cpsel_destroy", "cpsel_last_error", "cpsel_status_string", "cpsel_config_default",
     "cpsel_set_config", "cpsel_get_config", "cpsel_set_stream", "cpsel_select_kth", "cpsel_median",
     "cpsel_select_kth_host", "cpsel_lms_objective", "cpsel_lms_residuals", "cpsel_select_kth_batched",
-    "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_nccl_unique_id",
+    "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_init_timings", "cpsel_nccl_unique_id",
     "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host", "cpsel_pooled_cuts",
     "cpsel_lts_objective",
 ]
@@ -152,6 +152,7 @@ def load():
             "cpsel_init": (I, [P, P, U64, I, C.POINTER(InitStats)]),
             "cpsel_small_select": (I, [P, P, U64, I, U64, P]),
             "cpsel_get_trace": (I, [P, C.POINTER(TraceRow), U32, C.POINTER(U32)]),
+            "cpsel_init_timings": (I, [P, C.POINTER(D), U32, C.POINTER(U32), C.c_int32]),
             "cpsel_nccl_unique_id": (I, [P]),
             "cpsel_comm_init": (I, [P, P, I, I]),
             "cpsel_select_kth_sharded": (I, [P, P, U64, I, U64, P, C.POINTER(Info)]),
@@ -320,6 +321,17 @@ def small_select(z, r: int) -> float:
     out = C.create_string_buffer(8)
     _check(ctx, load().cpsel_small_select(ctx.handle, C.c_void_p(z.data_ptr()), z.numel(), dt, int(r), out))
     return _out_value(out, dt)
+
+
+def init_timings(device: int = 0, reset: bool = True) -> list:
+    """record_timing=2: the init-kernel durations (ms, CUDA events) of the selections since the last
+    reset, in call order."""
+    c = _ctx_device(device)
+    n = C.c_uint32()
+    _check(c, load().cpsel_init_timings(c.handle, None, 0, C.byref(n), 0))
+    buf = (C.c_double * max(n.value, 1))()
+    _check(c, load().cpsel_init_timings(c.handle, buf, n.value, C.byref(n), 1 if reset else 0))
+    return [buf[i] for i in range(n.value)]
 
 
 def get_trace(device: int = 0) -> list:

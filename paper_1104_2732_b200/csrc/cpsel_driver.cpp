@@ -78,6 +78,11 @@ struct cpsel_ctx {
   // kernel timing (record_timing): a pool of (start, end) event pairs, one pair per step of a
   // selection, resolved once the selection is over (no synchronisation between steps)
   std::vector<cudaEvent_t> evpool;
+  // record_timing == 2 ("light"): only the init kernel of each selection is bracketed by events,
+  // appended to this ring and resolved when the caller asks (cpsel_init_timings) — nothing is read
+  // back inside a selection, so the timing does not delay the next call
+  std::vector<cudaEvent_t> light_ev;
+  uint32_t light_n = 0;
   // result mailbox in mapped pinned memory: the finishing thread of a pass/init/select kernel
   // writes its result here and then bumps the flag the host spins on (no copy, no stream sync)
   struct Mailbox {
@@ -285,7 +290,17 @@ struct GpuBackend : Backend {
   GpuBackend(cpsel_ctx* c, const void* x_, uint64_t n_, int dt_)
       : ctx(c), x(x_), n(n_), dt(dt_), cur(x_), n_cur(n_) {}
   std::string message() const override { return ctx->err; }
-  bool timed() const { return ctx->cfg.record_timing != 0; }
+  bool timed() const { return ctx->cfg.record_timing == 1; }
+  bool light() const { return ctx->cfg.record_timing == 2; }
+  cudaError_t light_mark() {  // start/end of the init kernel in the light ring
+    if (ctx->light_ev.size() <= ctx->light_n) {
+      cudaEvent_t e;
+      cudaError_t err = cudaEventCreate(&e);
+      if (err != cudaSuccess) return err;
+      ctx->light_ev.push_back(e);
+    }
+    return cudaEventRecord(ctx->light_ev[ctx->light_n++], ctx->stream);
+  }
   int next_slot = 0;
   bool use_mail = true;  // results through the mapped mailbox (one GPU); false: device tuple + copy
   cudaError_t tic() {
@@ -363,6 +378,7 @@ struct GpuBackend : Backend {
       sample_slot = slot;
       CK(tic());
     }
+    if (light()) CK(light_mark());
     // the device chain (§8f-3) when its continuation is likely: the init's copy (~1-4% of n) will
     // exceed the exact-selection cap
     spec = Spec{};
@@ -385,6 +401,7 @@ struct GpuBackend : Backend {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
     }
     CK(toc());
+    if (light()) CK(light_mark());
     const int init_slot_ = slot;
     if (chain) CK(launch_chain(k));
     slot = init_slot_;
@@ -1138,7 +1155,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     *value = canonical_zero(v);
     inf.exit_reason = reason;
     inf.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    if (cfg.record_timing) {
+    if (cfg.record_timing == 1) {
       inf.kernel_ms_init = be.slot_ms(init_slot);
       inf.kernel_ms_select = be.slot_ms(select_slot);
       inf.kernel_ms_sample = 0.0;
@@ -1515,7 +1532,7 @@ cpsel_status run_direct(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype
                         cpsel_info* info) {
   const auto t0 = std::chrono::steady_clock::now();
   cudaEvent_t e0 = nullptr, e1 = nullptr;
-  const bool timed = ctx->cfg.record_timing != 0;
+  const bool timed = ctx->cfg.record_timing == 1;
   if (timed) {
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -1685,6 +1702,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     for (void* p : host)
       if (p) cudaFreeHost(p);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->light_ev) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   }
   delete ctx;
@@ -1789,6 +1807,21 @@ cpsel_status cpsel_small_select(cpsel_ctx* ctx, const void* d_z, uint64_t m, cps
   s = be.select_on(d_z, m, r, &v);
   if (s != CPSEL_OK) return s;
   store_value(canonical_zero(v), dtype, h_out);
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_init_timings(cpsel_ctx* ctx, double* ms, uint32_t max, uint32_t* n_out, int32_t reset) {
+  if (!ctx || !n_out) return CPSEL_EINVAL;
+  DeviceGuard g(ctx->device);
+  const uint32_t pairs = ctx->light_n / 2;
+  *n_out = pairs;
+  for (uint32_t i = 0; ms && i < pairs && i < max; ++i) {
+    float f = 0.f;
+    CK(cudaEventSynchronize(ctx->light_ev[2 * i + 1]));
+    CK(cudaEventElapsedTime(&f, ctx->light_ev[2 * i], ctx->light_ev[2 * i + 1]));
+    ms[i] = f;
+  }
+  if (reset) ctx->light_n = 0;
   return CPSEL_OK;
 }
 
