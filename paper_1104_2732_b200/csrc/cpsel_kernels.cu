@@ -2211,10 +2211,11 @@ __device__ void batch_sample_cuts(BatchState& st, unsigned* hist, const float* z
 // rows (computed by the fused tensor-core kernel in store mode: exactly elements of S).  Per column,
 // the bin edges around the sample order statistics of ranks q -/+ (3.5 sd + 2) and q (q the target
 // rank k scaled to the sample, as batch_sample_cuts) -> cuts[4j .. 4j+2] = t_lo, t_hi, t_mid.  Two
-// MSB digit rounds on the order-preserving keys: an 11-bit histogram of all keys, then 11-bit
-// histograms of the keys in each target's bin; t_lo is the lower edge of the lo target's final bin
-// (<= that sample order statistic), t_hi the upper edge of the hi target's (>=): cuts at most 2^10
-// key units (2^-13 relative) wider than the exact sample quantiles, which is all a cut needs — the
+// digit rounds on the order-preserving keys below their top bit (set for every s >= +0): an 11-bit
+// histogram of all keys (exponent + 3 mantissa bits), then 11-bit histograms of the
+// keys in each target's bin; t_lo is the lower edge of the lo target's final bin (<= that sample
+// order statistic), t_hi the upper edge of the hi target's (>=): cuts at most 2^9 key units (2^-14
+// relative) wider than the exact sample quantiles, which is all a cut needs — the
 // fused pass counts exactly at whatever values they are.  One CTA of 1024 threads per column.
 constexpr int kCutThreads = 1024;
 constexpr int kCutMaxPer = 16;   // <= 16384 samples
@@ -2252,9 +2253,9 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
 #pragma unroll
       for (int u = 0; u < kCutMaxPer; ++u) {
         if (round == 0) {
-          atomicAdd(&hist[0][key[u] >> 21], 1u);
+          atomicAdd(&hist[0][(key[u] >> 20) & 2047u], 1u);
         } else {
-          const unsigned top = key[u] >> 21, d = (key[u] >> 10) & 2047u;
+          const unsigned top = (key[u] >> 20) & 2047u, d = (key[u] >> 9) & 2047u;
 #pragma unroll
           for (int t = 0; t < 3; ++t)
             if (top == bin[t]) atomicAdd(&hist[t][d], 1u);
@@ -2309,10 +2310,10 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
       }
       __syncthreads();
     }
-    if (tid == 0) {  // bin[t] = the top 22 bits of the target's key
-      cuts[4 * (size_t)j] = (float)from_key_f32(bin[0] << 10);
-      cuts[4 * (size_t)j + 1] = (float)from_key_f32((bin[1] << 10) | 1023u);
-      cuts[4 * (size_t)j + 2] = (float)from_key_f32((bin[2] << 10) | 512u);
+    if (tid == 0) {  // bin[t] = key bits 30..9 of the target (bit 31 is set: every s >= +0)
+      cuts[4 * (size_t)j] = (float)from_key_f32(0x80000000u | (bin[0] << 9));
+      cuts[4 * (size_t)j + 1] = (float)from_key_f32(0x80000000u | (bin[1] << 9) | 511u);
+      cuts[4 * (size_t)j + 2] = (float)from_key_f32(0x80000000u | (bin[2] << 9) | 256u);
       cuts[4 * (size_t)j + 3] = 0.f;
     }
   }

@@ -212,3 +212,25 @@ def test_fused_nonfinite_rejected(cp):
     y[777] = np.nan
     with pytest.raises(ValueError, match="NaN or Inf"):
         cp.lms_objective(dev(X), dev(y), dev(th))
+
+
+@pytest.mark.parametrize("p,C", [(1, 1), (3, 129), (16, 200), (10, 1)])
+def test_fused_shapes(cp, p, C):
+    """Fused path for other predictor counts (K padding 1..16) and candidate counts (one column, a
+    ragged last candidate tile): every column bit-exact on the fused kernel's own S, and that S
+    within the 3xTF32 bound of fp64."""
+    n = 20_011                                                    # >= 16384: fused; ragged row tile
+    rng = np.random.default_rng(p * 1000 + C)
+    X = rng.standard_normal((n, p)).astype(np.float32)
+    y = (rng.standard_normal(n) * 2).astype(np.float32)
+    th = rng.standard_normal((C, p)).astype(np.float32)
+    Xd, yd, thd = dev(X), dev(y), dev(th)
+    got = cp.lms_objective(Xd, yd, thd).cpu().numpy()
+    S = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+    k = O.median_rank(n)
+    for j in range(C):
+        assert got[j] == O.order_statistic(S[j], k), j
+    R64 = X.astype(np.float64) @ th.astype(np.float64).T - y.astype(np.float64)[:, None]
+    ref = (R64 * R64).T
+    rb = residual_bound(X, y, th).T
+    assert np.all(np.abs(S.astype(np.float64) - ref) <= rb * (2 * np.sqrt(ref) + rb) + 2.0 ** -23 * ref + 1e-30)
