@@ -282,7 +282,7 @@ struct GpuBackend : Backend {
   // copy, the radix select of its copy) is launched right behind the init; the driver's requests
   // take those results when they ask for exactly those steps
   struct Spec {
-    bool active = false, cut_used = false, small = false;
+    bool active = false, cut_used = false, small = false, direct = false;
     unsigned long long seq_c0 = 0, seq_cut = 0, seq_c1 = 0, seq_radix = 0;
     int sample_slot = -1, cut_slot = -1, radix_slot = -1;
   } spec;
@@ -382,8 +382,11 @@ struct GpuBackend : Backend {
     // the device chain (§8f-3) when its continuation is likely: the init's copy (~1-4% of n) will
     // exceed the exact-selection cap
     spec = Spec{};
-    const bool chain = fuse && use_mail && !presampled && chain_select_cap > 0 && ctx->cfg.pass_cuts &&
-                       !ctx->cfg.objective && n / 100 > chain_select_cap;
+    // the init's copy holds ~2% of n: radix-select it right behind the init when it will fit the
+    // select cap (direct), else chain the R26 cut pass first
+    const bool chain_ok = fuse && use_mail && !presampled && chain_select_cap > 0 && !ctx->cfg.objective;
+    const bool direct = chain_ok && n / 25 <= chain_select_cap && n / 100 > (1ull << 20);
+    const bool chain = chain_ok && (direct || (ctx->cfg.pass_cuts && n / 100 > chain_select_cap));
     if (fuse) {
       SegArgs sa{};
       sa.out = ctx->d_sb[0];
@@ -392,9 +395,11 @@ struct GpuBackend : Backend {
       if (chain) {
         a.chain = ctx->d_chain;
         a.chain_mail = &ctx->mb_dev->chain;
-        a.chain_seq = spec.seq_c0 = ++ctx->seq;
+        a.chain_seq = ++ctx->seq;
+        if (direct) spec.seq_c1 = a.chain_seq; else spec.seq_c0 = a.chain_seq;
         a.chain_k = k;
         a.chain_cap = chain_select_cap;
+        a.chain_direct = direct ? 1 : 0;
       }
       CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
@@ -403,7 +408,7 @@ struct GpuBackend : Backend {
     CK(toc());
     if (light()) CK(light_mark());
     const int init_slot_ = slot;
-    if (chain) CK(launch_chain(k));
+    if (chain) CK(direct ? launch_chain_direct() : launch_chain(k));
     slot = init_slot_;
     launches = cut ? 2 : 1;
     scanned = n;
@@ -448,6 +453,21 @@ struct GpuBackend : Backend {
     return CPSEL_OK;
   }
   // launch the usual continuation behind the init (kernels read m, r and go/no-go from the chain)
+  // direct chain: the radix select of the init's segmented copy, gated by decision 1
+  cudaError_t launch_chain_direct() {
+    cudaError_t e;
+    spec.active = true;
+    spec.direct = true;
+    spec.seq_radix = ++ctx->seq;
+    if ((e = tic()) != cudaSuccess) return e;
+    if ((e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
+                                 &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
+                                 static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain)) != cudaSuccess)
+      return e;
+    if ((e = toc()) != cudaSuccess) return e;
+    spec.radix_slot = slot;
+    return cudaSuccess;
+  }
   cudaError_t launch_chain(uint64_t k) {
     cudaError_t e;
     spec.active = true;
@@ -604,7 +624,7 @@ struct GpuBackend : Backend {
   bool has_cut_pass() const override { return use_mail && R > 0; }
   cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
     dense = false;  // one GPU: the radix select reads the segmented copy directly (no atomics)
-    if (spec.active && !spec.cut_used && cur_seg && cur_sbuf == 0 && cur == ctx->d_sb[0]) {
+    if (spec.active && !spec.direct && !spec.cut_used && cur_seg && cur_sbuf == 0 && cur == ctx->d_sb[0]) {
       bool ok;
       uint64_t cm, cr;
       cpsel_status w = chain_decision(0, spec.seq_c0, &ok, &cm, &cr);
@@ -723,6 +743,22 @@ struct GpuBackend : Backend {
   // the radix select reads dense and segmented arrays alike
   bool kept_dense() const override { return true; }
   cpsel_status select(int side, uint64_t r, double* out) override {
+    if (spec.active && spec.direct && side == 2 && cur_seg && cur_sbuf == 0 && cur == ctx->d_sb[0] && cur_side == 0) {
+      bool ok;
+      uint64_t cm, cr;
+      cpsel_status w = chain_decision(1, spec.seq_c1, &ok, &cm, &cr);
+      if (w != CPSEL_OK) return w;
+      spec.active = false;
+      if (ok && cr == r && cm == n_cur) {  // the chain ran this select right behind the init
+        w = wait_mail(&ctx->mb->seq_radix, spec.seq_radix);
+        if (w != CPSEL_OK) return w;
+        *out = ctx->mb->radix_value;
+        launches = dt == kF32 ? 3 : 6;
+        scanned = cm;
+        slot = spec.radix_slot;
+        return CPSEL_OK;
+      }
+    }
     if (spec.active && spec.cut_used && side == 0 && !last_dense && tgt == 1) {
       bool ok;
       uint64_t cm, cr;
@@ -1124,7 +1160,9 @@ struct HostBackend : Backend {
   }
 };
 
-uint64_t dense_threshold(uint64_t select_cap) { return std::max<uint64_t>(4 * select_cap, 1ull << 20); }
+// brackets up to this size are compacted densely (4 x 2^20: independent of a larger select cap — the
+// radix select reads segmented arrays as well, and the fused init needs the segmented buffers)
+uint64_t dense_threshold(uint64_t select_cap) { return std::max<uint64_t>(4 * std::min<uint64_t>(select_cap, 1ull << 20), 1ull << 20); }
 
 // ============================================================================================
 // The cutting-plane driver (Algorithm 1 + hybrid finish), shared by all back ends.
@@ -1506,7 +1544,7 @@ uint64_t auto_z_cap(uint64_t n, const cpsel_config& cfg) {
   return std::max<uint64_t>(n / 8 * 5, 1);  // compact once the bracket holds <= 5/8 of x
 }
 
-uint64_t auto_select_cap(const cpsel_config& cfg) { return cfg.select_cap ? cfg.select_cap : (1ull << 20); }
+uint64_t auto_select_cap(const cpsel_config& cfg) { return cfg.select_cap ? cfg.select_cap : (1ull << 25); }
 
 cpsel_status check_common(cpsel_ctx* ctx, const void* p, uint64_t n, cpsel_dtype dtype) {
   if (!ctx) return CPSEL_EINVAL;

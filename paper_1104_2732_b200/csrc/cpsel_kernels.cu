@@ -1554,12 +1554,24 @@ template <> __device__ __forceinline__ double nextafter_t(double v, bool up) {
 }
 template <typename T>
 __device__ void chain_decide0(const DevInit& r, uint64_t k, uint64_t cap, ChainState* cs, ChainMail* mail,
-                              unsigned long long seq) {
+                              unsigned long long seq, int direct) {
   const double lo_out = (double)nextafter_t<T>((T)r.vmin, false), hi_out = (double)nextafter_t<T>((T)r.vmax, true);
   const uint64_t written = r.pad;
-  const bool ok = (r.has_cut & 1) && r.nonfinite == 0 && isfinite(r.vmin) && isfinite(r.vmax) && isfinite(lo_out) &&
-                  isfinite(hi_out) && isfinite(r.t_est) && r.t_lo > lo_out && r.t_hi < hi_out && r.t_lo < r.t_hi &&
-                  r.c_le_lo < k && r.c_lt_hi >= k && written == r.c_lt_hi - r.c_le_lo && written > cap;
+  const bool base = (r.has_cut & 1) && r.nonfinite == 0 && isfinite(r.vmin) && isfinite(r.vmax) && isfinite(lo_out) &&
+                    isfinite(hi_out) && isfinite(r.t_est) && r.t_lo > lo_out && r.t_hi < hi_out && r.t_lo < r.t_hi &&
+                    r.c_le_lo < k && r.c_lt_hi >= k && written == r.c_lt_hi - r.c_le_lo;
+  if (direct) {  // the radix select of the init's copy itself is next: decision 1 gates it
+    cs->ok[0] = 0;
+    cs->ok[1] = (base && written <= cap) ? 1ull : 0ull;
+    cs->m[1] = written;
+    cs->r[1] = k - r.c_le_lo;
+    cs->le_base = r.c_le_lo;
+    mail->ok[1] = cs->ok[1]; mail->m[1] = cs->m[1]; mail->r[1] = cs->r[1];
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(&mail->seq[1]) = seq;
+    return;
+  }
+  const bool ok = base && written > cap;
   cs->ok[0] = ok ? 1ull : 0ull;
   cs->m[0] = written;
   cs->r[0] = k - r.c_le_lo;
@@ -2033,7 +2045,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     r.has_cut = SUMS ? 15ull : 11ull;  // two cuts + the interior compacted (+ N_lo, P_hi), no #min/#max
     *ia.out = r;
     publish_done(ia.done, ia.seq);
-    if (ia.chain) chain_decide0<T>(r, ia.chain_k, ia.chain_cap, ia.chain, ia.chain_mail, ia.chain_seq);
+    if (ia.chain) chain_decide0<T>(r, ia.chain_k, ia.chain_cap, ia.chain, ia.chain_mail, ia.chain_seq, ia.chain_direct);
   }
 }
 

@@ -136,6 +136,7 @@ struct InitArgs {
   struct ChainMail* chain_mail;
   unsigned long long chain_seq;
   uint64_t chain_k, chain_cap;
+  int chain_direct;  // 1: the radix select runs right behind the init on its copy (gated by decision 1)
 };
 
 struct LaunchShape {

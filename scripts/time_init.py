@@ -16,7 +16,8 @@ sharded = len(sys.argv) > 3 and sys.argv[3] == "sharded"  # the NCCL path at wor
 dtype = "f64" if "f64" in sys.argv else "f32"
 x = datagen.make(dist, 1 << lg, dtype, device="cuda")
 torch.cuda.synchronize()
-cp.set_config(record_timing=1)
+import os
+cp.set_config(record_timing=1, select_cap=int(os.environ.get("SELECT_CAP", "0")))
 if sharded:
     cp.comm_init(cp.nccl_unique_id(), 0, 1, torch.cuda.current_device())
 
