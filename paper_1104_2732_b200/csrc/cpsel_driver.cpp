@@ -400,6 +400,8 @@ struct GpuBackend : Backend {
         a.chain_k = k;
         a.chain_cap = chain_select_cap;
         a.chain_direct = direct ? 1 : 0;
+        a.hist = direct ? ctx->d_hist : nullptr;  // the init takes radix round 0 of its copy
+        a.rst = ctx->d_radix;
       }
       CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
@@ -462,7 +464,8 @@ struct GpuBackend : Backend {
     if ((e = tic()) != cudaSuccess) return e;
     if ((e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
                                  &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
-                                 static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain)) != cudaSuccess)
+                                 static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain,
+                                 /*first_round=*/1)) != cudaSuccess)
       return e;
     if ((e = toc()) != cudaSuccess) return e;
     spec.radix_slot = slot;
@@ -753,7 +756,7 @@ struct GpuBackend : Backend {
         w = wait_mail(&ctx->mb->seq_radix, spec.seq_radix);
         if (w != CPSEL_OK) return w;
         *out = ctx->mb->radix_value;
-        launches = dt == kF32 ? 3 : 6;
+        launches = dt == kF32 ? 2 : 5;  // round 0 was taken by the init pass
         scanned = cm;
         slot = spec.radix_slot;
         return CPSEL_OK;

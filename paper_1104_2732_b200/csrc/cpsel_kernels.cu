@@ -49,6 +49,36 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+// the same with an L2 eviction policy (createpolicy): the init pass streams x with evict_first
+// so that its ~2% copy, stored with evict_last, stays in L2 for the radix rounds that read it next
+__device__ __forceinline__ float4 ld_stream(const float4* p, uint64_t pol) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p, uint64_t pol) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_keep(float* p, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ float lane_of(const float4& v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
 }
@@ -1110,8 +1140,14 @@ template <typename T> struct HistFn {
   int shift;
   unsigned dmask;
   __device__ __forceinline__ void elem(T v, bool ok) {
-    const unsigned long long k = okey(v);
-    if (ok && (k & mask) == prefix) atomicAdd(&sh[(unsigned)(k >> shift) & dmask], 1u);
+    if constexpr (sizeof(T) == 4) {
+      const unsigned u = __float_as_uint(v);
+      const unsigned k = u ^ ((unsigned)((int)u >> 31) | 0x80000000u);
+      if (ok && (k & (unsigned)mask) == (unsigned)prefix) atomicAdd(&sh[(k >> shift) & dmask], 1u);
+    } else {
+      const unsigned long long k = okey(v);
+      if (ok && (k & mask) == prefix) atomicAdd(&sh[(unsigned)(k >> shift) & dmask], 1u);
+    }
   }
   __device__ __forceinline__ void group_begin() {}
   __device__ __forceinline__ void group_end() {}
@@ -1336,6 +1372,54 @@ __device__ __forceinline__ void seg_run(F& f, const T* __restrict__ p, uint64_t 
   if (v0 < nvec) seg_group<T, true>(f, xv, v0, nvec);
 }
 
+// The same with the loads software-pipelined: the next group's vectors are in flight while the
+// current group is processed (a warp streams a whole run by itself, so without this every group is
+// one dependent memory round trip) — the radix rounds over the init's segmented copy.
+template <typename T, typename F>
+__device__ __forceinline__ void seg_run_pipe(F& f, const T* __restrict__ p, uint64_t c) {
+  using V = typename VecOf<T>::V;
+  constexpr int VE = VecOf<T>::N;
+  const int lane = threadIdx.x & 31;
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(p) / sizeof(T)) & (VE - 1);
+  uint64_t head = mis ? (VE - mis) : 0;
+  if (head > c) head = c;
+  const V* xv = reinterpret_cast<const V*>(p + head);
+  const uint64_t nvec = (c - head) / VE;
+  const uint64_t tail0 = head + nvec * VE, ntail = c - tail0;
+  {
+    const bool okh = (uint64_t)lane < head;
+    const bool okt = (uint64_t)lane >= head && (uint64_t)lane < head + ntail;
+    T v = T(0);
+    if (okh) v = p[lane];
+    if (okt) v = p[tail0 + (lane - head)];
+    if (head + ntail) seg_scalars<T>(f, v, okh || okt);
+  }
+  constexpr uint64_t GV = 32 * kSegU;
+  const uint64_t nfull = nvec / GV;
+  V cur[kSegU];
+  if (nfull > 0) {
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) cur[u] = ld_stream(xv + (uint64_t)u * 32 + lane);
+  }
+  for (uint64_t g = 0; g < nfull; ++g) {
+    V nxt[kSegU];
+    if (g + 1 < nfull) {
+#pragma unroll
+      for (int u = 0; u < kSegU; ++u) nxt[u] = ld_stream(xv + (g + 1) * GV + (uint64_t)u * 32 + lane);
+    }
+    f.begin();
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) {
+#pragma unroll
+      for (int j = 0; j < VE; ++j) f.elem(lane_of(cur[u], j), u, u * VE + j);
+    }
+    f.end();
+#pragma unroll
+    for (int u = 0; u < kSegU; ++u) cur[u] = nxt[u];
+  }
+  if (nfull * GV < nvec) seg_group<T, true>(f, xv, nfull * GV, nvec);
+}
+
 // ------------------------------------------------------------------------------------------
 // Step a5, one launch per digit: the histogram of the digit over the prefix class, then the last
 // CTA to finish picks the digit holding the rank, extends the prefix and clears the histogram
@@ -1343,12 +1427,25 @@ __device__ __forceinline__ void seg_run(F& f, const T* __restrict__ p, uint64_t 
 // array (one warp per run, the segmented grid).
 struct RadixSegFn {
   unsigned* sh;
+  unsigned sh_sa;  // shared-window address of sh
   unsigned long long prefix, mask;
   int shift;
   unsigned dmask;
   template <typename T> __device__ __forceinline__ void elem(T v, int, int) {
-    const unsigned long long k = okey(v);
-    if ((k & mask) == prefix) atomicAdd(&sh[(unsigned)(k >> shift) & dmask], 1u);
+    if constexpr (sizeof(T) == 4) {  // 32-bit key arithmetic, predicated reduction (no branch)
+      const unsigned u = __float_as_uint(v);
+      const unsigned k = u ^ ((unsigned)((int)u >> 31) | 0x80000000u);
+      const unsigned addr = sh_sa + 4u * ((k >> shift) & dmask);
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "setp.eq.u32 p, %0, %1;\n\t"
+          "@p red.shared.add.u32 [%2], 1;\n\t}" ::"r"(k & (unsigned)mask),
+          "r"((unsigned)prefix), "r"(addr)
+          : "memory");
+    } else {
+      const unsigned long long k = okey(v);
+      if ((k & mask) == prefix) atomicAdd(&sh[(unsigned)(k >> shift) & dmask], 1u);
+    }
   }
   __device__ __forceinline__ void begin() {}
   __device__ __forceinline__ void end() {}
@@ -1388,6 +1485,7 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   __syncthreads();
   RadixSegFn f;
   f.sh = sh;
+  f.sh_sa = (unsigned)__cvta_generic_to_shared(sh);
   f.prefix = s_prefix;
   f.mask = s_mask;
   f.shift = a.shift;
@@ -1395,7 +1493,7 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   if (SEG) {
     const uint64_t W = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
     const SegEntry e = a.tab[W];
-    seg_run<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
+    seg_run_pipe<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
   } else {
     HistFn<T> hf;
     hf.sh = sh; hf.prefix = s_prefix; hf.mask = s_mask; hf.shift = a.shift; hf.dmask = f.dmask;
@@ -1774,6 +1872,7 @@ template <typename T, bool SUMS> struct InitSeg {
   T* out;
   uint64_t reg_lo;
   T* stage;                       // this warp's GW-element staging buffer (shared memory)
+  unsigned* hist0 = nullptr;      // direct chain: shared-memory histogram of the copy's top digit
 
   // one element, SUMS: 3 compares, 2 subs, 1 counter, 3 sums, 1 interior bit (10 issue slots):
   //   fL = #x<=t_lo, N += (t_lo-x) on x<=t_lo, P += (x-t_hi) on x>t_hi, I += (x-t_lo) and the
@@ -1928,7 +2027,16 @@ template <typename T, bool SUMS> struct InitSeg {
       if (bits & (1u << j)) *sp++ = vals[j];
     __syncwarp();
     T* dst = out + reg_lo + n_in;
-    for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    if (hist0) {  // radix round 0 of the copy (direct chain): top digit of each copied element
+      const uint64_t keep = l2_policy_evict_last();  // the radix rounds read the copy next
+      for (unsigned i = lane; i < tot; i += 32) {
+        const T v = stage[i];
+        st_keep(dst + i, v, keep);
+        atomicAdd(&hist0[(unsigned)(okey(v) >> (sizeof(T) == 4 ? 21 : 53)) & 2047u], 1u);
+      }
+    } else {
+      for (unsigned i = lane; i < tot; i += 32) dst[i] = stage[i];
+    }
     __syncwarp();
     n_in += tot;
   }
@@ -1950,6 +2058,13 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   f.th = static_cast<const T*>(ia.t0)[1];
   f.out = static_cast<T*>(a.out);
   f.reg_lo = W * a.R;
+  __shared__ unsigned h0[2048];
+  const bool hist = ia.chain_direct && ia.hist;
+  if (hist) {
+    for (int i = threadIdx.x; i < 2048; i += kBlock) h0[i] = 0u;
+    __syncthreads();
+    f.hist0 = h0;
+  }
   const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
   uint64_t head = mis ? (VE - mis) : 0;
   if (head > n) head = n;
@@ -1963,9 +2078,10 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     // software pipelined: the next group's loads are issued once the current group's values sit in
     // f.vals, so they are in flight during its scan / staging / copy-out
     V v[kSegU];
+    const uint64_t pol = l2_policy_evict_first();  // x is read once: keep L2 for the copy
     if (W < nfull) {
 #pragma unroll
-      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + W * GV + (uint64_t)u * 32 + lane);
+      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + W * GV + (uint64_t)u * 32 + lane, pol);
     }
     for (uint64_t g = W; g < nfull; g += Wtot) {
       f.begin();
@@ -1974,7 +2090,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
       const uint64_t gn = g + Wtot;
       if (gn < nfull) {
 #pragma unroll
-        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + gn * GV + (uint64_t)u * 32 + lane);
+        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + gn * GV + (uint64_t)u * 32 + lane, pol);
       }
       f.end(F::G);
     }
@@ -2019,6 +2135,12 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     o.cnt[1] = 0;
     a.seg_out[W] = o;
   }
+  if (hist) {  // this CTA's round-0 histogram into the global one (before the grid finish's fence)
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += kBlock)
+      if (h0[i]) atomicAdd(&ia.hist[i], h0[i]);
+    __threadfence();  // every thread's reductions performed before the grid finish's ticket
+  }
   InitPartial p;
   p.vmin = (double)f.mn; p.vmax = (double)f.mx; p.S = 0; p.pad = 0;
   p.cnt_min = f.cmn; p.cnt_max = f.cmx; p.nonfinite = f.nan;
@@ -2031,7 +2153,50 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   id.cnt_min = id.cnt_max = id.nonfinite = id.pad2 = 0;
   id.N0 = id.P0 = id.I0 = 0; id.cA = id.cB = id.cC = id.cD = id.cE = 0;
   InitPartial tot;
-  if (grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id) && threadIdx.x == 0) {
+  const bool last = grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id);
+  if (!last) return;
+  if (hist) {
+    // radix round 0 of the copy (f32 digit 31..21, f64 63..53) for rank k - #x<=t_lo: the pick of
+    // radix_round_kernel (8 bins per thread, block scan), then the global histogram is cleared
+    __threadfence();
+    __shared__ unsigned wsum[kWarps];
+    __shared__ unsigned long long s_cle;  // grid_finish's totals are thread 0's alone
+    if (threadIdx.x == 0) s_cle = tot.cA;
+    const int wl = threadIdx.x & 31, ww = threadIdx.x >> 5;
+    unsigned h[8], tsum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      h[j] = __ldcg(&ia.hist[threadIdx.x * 8 + j]);
+      tsum += h[j];
+    }
+    unsigned incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (wl >= o) incl += y;
+    }
+    if (wl == 31) wsum[ww] = incl;
+    __syncthreads();
+    unsigned wbase = 0;
+    for (int q = 0; q < ww; ++q) wbase += wsum[q];
+    const unsigned long long rk = ia.chain_k > s_cle ? ia.chain_k - s_cle : 0ull;
+    unsigned long long before = wbase + incl - tsum;
+    const int sh0 = sizeof(T) == 4 ? 21 : 53;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (before < rk && rk <= before + h[j]) {
+        const unsigned long long digit = (unsigned long long)(threadIdx.x * 8 + j);
+        ia.rst->prefix = digit << sh0;
+        ia.rst->mask = 2047ull << sh0;
+        ia.rst->r = rk - before;
+        ia.rst->count = h[j];
+      }
+      before += h[j];
+    }
+    for (int i = threadIdx.x; i < 2048; i += kBlock) ia.hist[i] = 0u;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     DevInit r;
     r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = 0; r.x0 = (double)x[0];
     r.cnt_min = tot.cnt_min; r.cnt_max = tot.cnt_max; r.nonfinite = tot.nonfinite;
@@ -3224,8 +3389,9 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned* hist, const LaunchShape& s, cudaStream_t st, double* vout,
                                 unsigned long long* done, unsigned long long seq, const SegEntry* tab, int side,
-                                unsigned* ticket, const ChainState* chain) {
-  // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10
+                                unsigned* ticket, const ChainState* chain, int first_round) {
+  // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10 (first_round > 0: the earlier rounds
+  // were taken by the init pass, RadixState holds their prefix and rank)
   static const int plan32[] = {21, 11, 10, 11, 0, 10};
   static const int plan64[] = {53, 11, 42, 11, 31, 11, 20, 11, 10, 10, 0, 10};
   const int rounds = dtype == kF32 ? 3 : 6;
@@ -3233,7 +3399,7 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   RadixArgs a{};
   a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
   a.r = r; a.vout = vout; a.done = done; a.seq = seq; a.chain = chain;
-  for (int i = 0; i < rounds; ++i) {
+  for (int i = first_round; i < rounds; ++i) {
     a.shift = plan[2 * i]; a.bits = plan[2 * i + 1];
     a.first = i == 0; a.last = i == rounds - 1;
     const int grid = tab ? s.grid_seg[dtype]
