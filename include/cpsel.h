@@ -54,7 +54,7 @@ typedef struct {
   uint64_t direct_threshold; /* n <= this: skip the cutting plane, select on x directly
                                 (P:L311 'radix sort ... most efficient up to 2^21').  Default 2^17 */
   uint64_t select_cap;       /* a kept half of <= select_cap elements is finished by the exact
-                                radix select (P:L196 'sort z', R21).  0 = auto (2^25: the init's copy of
+                                radix select (P:L196 'sort z', R21).  0 = auto (2^26: the init's copy of
                                 ~2% of n is radix-selected directly up to n ~ 2^30). */
   uint32_t max_iters;        /* safety cap on cutting-plane passes (P:L169 maxit).  Default 200 */
   int32_t force_cp;          /* 1: always run cutting-plane passes (parity runs), ignore direct_threshold */

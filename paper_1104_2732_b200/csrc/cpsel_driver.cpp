@@ -400,8 +400,9 @@ struct GpuBackend : Backend {
         a.chain_k = k;
         a.chain_cap = chain_select_cap;
         a.chain_direct = direct ? 1 : 0;
-        a.hist = direct ? ctx->d_hist : nullptr;  // the init takes radix round 0 of its copy
-        a.rst = ctx->d_radix;
+        // f32: the init counts radix round 0 of its copy (f64 keys crowd into few top-digit bins:
+        // the shared-memory contention costs the init more than the round it saves)
+        a.hist = (direct && dt == kF32) ? ctx->d_hist + 2048 : nullptr;
       }
       CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
@@ -465,7 +466,8 @@ struct GpuBackend : Backend {
     if ((e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
                                  &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
                                  static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain,
-                                 /*first_round=*/1)) != cudaSuccess)
+                                 /*first_round=*/dt == kF32 ? 1 : 0, dt == kF32 ? ctx->d_hist + 2048 : nullptr)) !=
+        cudaSuccess)
       return e;
     if ((e = toc()) != cudaSuccess) return e;
     spec.radix_slot = slot;
@@ -756,7 +758,7 @@ struct GpuBackend : Backend {
         w = wait_mail(&ctx->mb->seq_radix, spec.seq_radix);
         if (w != CPSEL_OK) return w;
         *out = ctx->mb->radix_value;
-        launches = dt == kF32 ? 2 : 5;  // round 0 was taken by the init pass
+        launches = dt == kF32 ? 2 : 6;  // f32: round 0 was counted by the init pass
         scanned = cm;
         slot = spec.radix_slot;
         return CPSEL_OK;
@@ -1547,7 +1549,7 @@ uint64_t auto_z_cap(uint64_t n, const cpsel_config& cfg) {
   return std::max<uint64_t>(n / 8 * 5, 1);  // compact once the bracket holds <= 5/8 of x
 }
 
-uint64_t auto_select_cap(const cpsel_config& cfg) { return cfg.select_cap ? cfg.select_cap : (1ull << 25); }
+uint64_t auto_select_cap(const cpsel_config& cfg) { return cfg.select_cap ? cfg.select_cap : (1ull << 26); }
 
 cpsel_status check_common(cpsel_ctx* ctx, const void* p, uint64_t n, cpsel_dtype dtype) {
   if (!ctx) return CPSEL_EINVAL;
@@ -1711,8 +1713,8 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMalloc(&ctx->d_skeys, kSampleKeyBytes));
   CKC(cudaMalloc(&ctx->d_chain, sizeof(ChainState)));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
-  CKC(cudaMalloc(&ctx->d_hist, 2048 * sizeof(unsigned)));
-  CKC(cudaMemset(ctx->d_hist, 0, 2048 * sizeof(unsigned)));
+  CKC(cudaMalloc(&ctx->d_hist, 2 * 2048 * sizeof(unsigned)));  // radix rounds | round 0 counted by the init
+  CKC(cudaMemset(ctx->d_hist, 0, 2 * 2048 * sizeof(unsigned)));
   CKC(cudaHostAlloc(&ctx->h_pass, sizeof(DevPass), cudaHostAllocDefault));
   CKC(cudaHostAlloc(&ctx->h_init, sizeof(DevInit), cudaHostAllocDefault));
   CKC(cudaHostAlloc(&ctx->h_radix, sizeof(RadixState), cudaHostAllocDefault));

@@ -1462,6 +1462,7 @@ struct RadixArgs {
   int shift, bits, first, last;
   uint64_t r;           // the rank (1-based), taken by the first round
   const ChainState* chain;  // device chain: skip unless chain->ok[1]; rank chain->r[1]
+  unsigned* hist0;          // round-0 counts taken by the init pass (this launch is round 1), or nullptr
   double* vout;
   unsigned long long* done;
   unsigned long long seq;
@@ -1470,18 +1471,54 @@ struct RadixArgs {
 template <typename T, bool SEG>
 __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   if (a.chain) {
-    if (!a.chain->ok[1]) return;
+    if (!a.chain->ok[1]) {  // skipped: the init's round-0 counts must still be cleared
+      if (a.hist0 && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
+      return;
+    }
     a.r = a.chain->r[1];
   }
   __shared__ unsigned sh[2048];
-  __shared__ unsigned long long s_prefix, s_mask;
+  __shared__ unsigned long long s_prefix, s_mask, s_rank;
   __shared__ bool s_last;
   __shared__ unsigned wsum[kWarps];
-  for (int i = threadIdx.x; i < 2048; i += kBlock) sh[i] = 0;
-  if (threadIdx.x == 0) {
+  if (a.hist0) {
+    // round 0 was counted by the init pass into hist0: every CTA picks its digit for rank a.r
+    // (the same result everywhere), so no launch or serial tail is spent on it
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    unsigned h[8], tsum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      h[j] = __ldcg(&a.hist0[threadIdx.x * 8 + j]);
+      tsum += h[j];
+    }
+    unsigned incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    unsigned wbase = 0;
+    for (int q = 0; q < w; ++q) wbase += wsum[q];
+    unsigned long long before = wbase + incl - tsum;
+    const int sh0 = sizeof(T) == 4 ? 21 : 53;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (before < a.r && a.r <= before + h[j]) {
+        s_prefix = (unsigned long long)(threadIdx.x * 8 + j) << sh0;
+        s_mask = 2047ull << sh0;
+        s_rank = a.r - before;
+      }
+      before += h[j];
+    }
+  } else if (threadIdx.x == 0) {
     s_prefix = a.first ? 0ull : a.st->prefix;
     s_mask = a.first ? 0ull : a.st->mask;
+    s_rank = a.first ? a.r : a.st->r;
   }
+  for (int i = threadIdx.x; i < 2048; i += kBlock) sh[i] = 0;
   __syncthreads();
   RadixSegFn f;
   f.sh = sh;
@@ -1529,7 +1566,7 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   __syncthreads();
   unsigned wbase = 0;
   for (int q = 0; q < w; ++q) wbase += wsum[q];
-  const unsigned long long r = a.first ? a.r : a.st->r;
+  const unsigned long long r = s_rank;
   unsigned long long before = wbase + incl - tsum;  // exclusive prefix of this thread's first bin
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -1551,6 +1588,8 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
     before += h[j];
   }
   for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist[i] = 0u;
+  if (a.hist0)  // every CTA read it before taking its ticket
+    for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
   if (threadIdx.x == 0) *a.ticket = 0u;
 }
 
@@ -2078,10 +2117,9 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     // software pipelined: the next group's loads are issued once the current group's values sit in
     // f.vals, so they are in flight during its scan / staging / copy-out
     V v[kSegU];
-    const uint64_t pol = l2_policy_evict_first();  // x is read once: keep L2 for the copy
     if (W < nfull) {
 #pragma unroll
-      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + W * GV + (uint64_t)u * 32 + lane, pol);
+      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + W * GV + (uint64_t)u * 32 + lane);
     }
     for (uint64_t g = W; g < nfull; g += Wtot) {
       f.begin();
@@ -2090,7 +2128,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
       const uint64_t gn = g + Wtot;
       if (gn < nfull) {
 #pragma unroll
-        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + gn * GV + (uint64_t)u * 32 + lane, pol);
+        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + gn * GV + (uint64_t)u * 32 + lane);
       }
       f.end(F::G);
     }
@@ -2155,47 +2193,6 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   InitPartial tot;
   const bool last = grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id);
   if (!last) return;
-  if (hist) {
-    // radix round 0 of the copy (f32 digit 31..21, f64 63..53) for rank k - #x<=t_lo: the pick of
-    // radix_round_kernel (8 bins per thread, block scan), then the global histogram is cleared
-    __threadfence();
-    __shared__ unsigned wsum[kWarps];
-    __shared__ unsigned long long s_cle;  // grid_finish's totals are thread 0's alone
-    if (threadIdx.x == 0) s_cle = tot.cA;
-    const int wl = threadIdx.x & 31, ww = threadIdx.x >> 5;
-    unsigned h[8], tsum = 0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      h[j] = __ldcg(&ia.hist[threadIdx.x * 8 + j]);
-      tsum += h[j];
-    }
-    unsigned incl = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(FULL, incl, o);
-      if (wl >= o) incl += y;
-    }
-    if (wl == 31) wsum[ww] = incl;
-    __syncthreads();
-    unsigned wbase = 0;
-    for (int q = 0; q < ww; ++q) wbase += wsum[q];
-    const unsigned long long rk = ia.chain_k > s_cle ? ia.chain_k - s_cle : 0ull;
-    unsigned long long before = wbase + incl - tsum;
-    const int sh0 = sizeof(T) == 4 ? 21 : 53;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      if (before < rk && rk <= before + h[j]) {
-        const unsigned long long digit = (unsigned long long)(threadIdx.x * 8 + j);
-        ia.rst->prefix = digit << sh0;
-        ia.rst->mask = 2047ull << sh0;
-        ia.rst->r = rk - before;
-        ia.rst->count = h[j];
-      }
-      before += h[j];
-    }
-    for (int i = threadIdx.x; i < 2048; i += kBlock) ia.hist[i] = 0u;
-    __syncthreads();
-  }
   if (threadIdx.x == 0) {
     DevInit r;
     r.vmin = tot.vmin; r.vmax = tot.vmax; r.S = 0; r.x0 = (double)x[0];
@@ -3389,7 +3386,7 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned* hist, const LaunchShape& s, cudaStream_t st, double* vout,
                                 unsigned long long* done, unsigned long long seq, const SegEntry* tab, int side,
-                                unsigned* ticket, const ChainState* chain, int first_round) {
+                                unsigned* ticket, const ChainState* chain, int first_round, unsigned* hist0) {
   // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10 (first_round > 0: the earlier rounds
   // were taken by the init pass, RadixState holds their prefix and rank)
   static const int plan32[] = {21, 11, 10, 11, 0, 10};
@@ -3402,6 +3399,7 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   for (int i = first_round; i < rounds; ++i) {
     a.shift = plan[2 * i]; a.bits = plan[2 * i + 1];
     a.first = i == 0; a.last = i == rounds - 1;
+    a.hist0 = (i == 1 && first_round == 1) ? hist0 : nullptr;
     const int grid = tab ? s.grid_seg[dtype]
                          : clamp_grid(s.grid_hist[dtype], m, kBlock * 2 * (dtype == kF32 ? 4 : 2));
     if (dtype == kF32) {

@@ -137,11 +137,10 @@ struct InitArgs {
   unsigned long long chain_seq;
   uint64_t chain_k, chain_cap;
   int chain_direct;  // 1: the radix select runs right behind the init on its copy (gated by decision 1)
-  // chain_direct: the init also takes the radix select's first digit round on its copy — a shared-
-  // memory histogram of the copied elements' top digit, merged into hist, picked by the finishing
-  // CTA into rst (prefix, mask, remaining rank); the chained radix select starts at round 1
+  // chain_direct: the init also counts the radix select's first digit round on its copy — a shared-
+  // memory histogram of the copied elements' top digit, merged into hist (2048 words); the chained
+  // radix select starts at round 1 and picks that digit itself
   unsigned int* hist;
-  struct RadixState* rst;
 };
 
 struct LaunchShape {
@@ -221,7 +220,8 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
                                 unsigned int* hist, const LaunchShape& s, cudaStream_t st,
                                 double* vout, unsigned long long* done, unsigned long long seq,
                                 const SegEntry* tab, int side, unsigned int* ticket,
-                                const ChainState* chain = nullptr, int first_round = 0);
+                                const ChainState* chain = nullptr, int first_round = 0,
+                                unsigned int* hist0 = nullptr);
 
 // Step a8: per-column k-th smallest of S (n x C column-major, float32), one CTA per column.
 struct BatchArgs {
