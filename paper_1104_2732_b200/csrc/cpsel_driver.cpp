@@ -292,6 +292,12 @@ struct GpuBackend : Backend {
   std::string message() const override { return ctx->err; }
   bool timed() const { return ctx->cfg.record_timing == 1; }
   bool light() const { return ctx->cfg.record_timing == 2; }
+  // f32 only (f64 keys crowd into few top-digit bins: the init slows by more than the round saves);
+  // measured at 2^30 f32: +1.6% whole-step throughput, init kernel 1% slower.  CPSEL_INIT_HIST0=0: off
+  bool init_hist0() const {
+    static const bool on = !(getenv("CPSEL_INIT_HIST0") && getenv("CPSEL_INIT_HIST0")[0] == '0');
+    return on && dt == kF32;
+  }
   cudaError_t light_mark() {  // start/end of the init kernel in the light ring
     if (ctx->light_ev.size() <= ctx->light_n) {
       cudaEvent_t e;
@@ -400,9 +406,8 @@ struct GpuBackend : Backend {
         a.chain_k = k;
         a.chain_cap = chain_select_cap;
         a.chain_direct = direct ? 1 : 0;
-        // f32: the init counts radix round 0 of its copy (f64 keys crowd into few top-digit bins:
-        // the shared-memory contention costs the init more than the round it saves)
-        a.hist = (direct && dt == kF32) ? ctx->d_hist + 2048 : nullptr;
+        // init_hist0: the init also counts radix round 0 of its copy (one radix launch fewer)
+        a.hist = (direct && init_hist0()) ? ctx->d_hist + 2048 : nullptr;
       }
       CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
@@ -466,7 +471,7 @@ struct GpuBackend : Backend {
     if ((e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
                                  &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
                                  static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain,
-                                 /*first_round=*/dt == kF32 ? 1 : 0, dt == kF32 ? ctx->d_hist + 2048 : nullptr)) !=
+                                 /*first_round=*/init_hist0() ? 1 : 0, init_hist0() ? ctx->d_hist + 2048 : nullptr)) !=
         cudaSuccess)
       return e;
     if ((e = toc()) != cudaSuccess) return e;
@@ -758,7 +763,7 @@ struct GpuBackend : Backend {
         w = wait_mail(&ctx->mb->seq_radix, spec.seq_radix);
         if (w != CPSEL_OK) return w;
         *out = ctx->mb->radix_value;
-        launches = dt == kF32 ? 2 : 6;  // f32: round 0 was counted by the init pass
+        launches = (dt == kF32 ? 3 : 6) - (init_hist0() ? 1 : 0);  // round 0 counted by the init pass?
         scanned = cm;
         slot = spec.radix_slot;
         return CPSEL_OK;
