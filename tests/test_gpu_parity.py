@@ -428,3 +428,24 @@ def test_sharded_world1_nccl(cp):
             assert any(r["kind"] == 3 for r in cp.get_trace())
     finally:
         cp.set_config(select_cap=0)
+
+
+def test_direct_chain_declined_then_reused(cp):
+    """Direct device chain (n >= 2^27): when the init's sample cuts miss the target (here: x is huge
+    exactly at the 32768 strided sample positions, so both cuts lie far above the median) the
+    chained radix rounds must stand down — clearing the round-0 digit counts the init pass took —
+    and the host continues with Kelley passes; the next selection through the chain is exact."""
+    n = 1 << 27
+    xd = datagen.make("normal", n, "f32", device="cuda")
+    pos = np.arange(32768, dtype=np.int64) * (n // 32768) + (n // 32768) // 2
+    import torch
+    xd[torch.from_numpy(pos).cuda()] = 1e30
+    k = O.median_rank(n)
+    v, info = cp.select_kth(xd, k, return_info=True)
+    x = host(xd)
+    assert canon(v) == float(O.order_statistic(x, k)), info
+    assert info["passes"] > 1                                   # not the chained finish
+    y = datagen.make("uniform", n, "f32", device="cuda")
+    for kk in (k, n // 10):
+        v2, info2 = cp.select_kth(y, kk, return_info=True)
+        assert canon(v2) == float(O.order_statistic(host(y), kk)), info2
