@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       }
       if (MODE == kFuseStore && col_ok) slot = a.slot[j];
       if (MODE == kFuseLts && col_ok) mj = a.m[j];
-      uint32_t le = 0;
+      uint32_t le = 0, le2 = 0;
       double lsum = 0.0;
       uint32_t ta = base_sa;  // next free staging slot
       for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
@@ -440,7 +440,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         mbar_wait_sleep(&yfull[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * FN + rq * kFRows;
-        const ulonglong2* ys = reinterpret_cast<const ulonglong2*>(ybuf + s * FN + rq * kFRows);
+        const uint32_t ys_sa = smem_u32(ybuf + s * FN + rq * kFRows);
 #pragma unroll 1
         for (uint32_t c0 = 0; c0 < kFRows; c0 += 32) {
           uint32_t r[32];
@@ -448,7 +448,10 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
           const uint64_t rowc = row0 + c0;
           ulonglong2 yv[8];
 #pragma unroll
-          for (int v = 0; v < 8; ++v) yv[v] = ys[c0 / 4 + v];
+          for (int v = 0; v < 8; ++v) {  // shared-memory broadcast (LDS.128)
+            const uint32_t ya = ys_sa + (c0 / 4 + v) * 16;
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(yv[v].x), "=l"(yv[v].y) : "r"(ya));
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           const int nvalid = rowc + 32 <= a.n ? 32 : (rowc >= a.n ? 0 : (int)(a.n - rowc));
           if (MODE == kFuseCuts) {
@@ -462,7 +465,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
                   float s0, s1;
                   resid2(r[i], r[i + 1], y01, s0, s1);
                   cut_elem(s0, lo1, wcut, le, ta);
-                  cut_elem(s1, lo1, wcut, le, ta);
+                  cut_elem(s1, lo1, wcut, le2, ta);  // two counters: half the dependent chain
                 }
               } else {  // the ragged end of x: padded rows enter as +Inf
 #pragma unroll
@@ -555,7 +558,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         const uint32_t cnt = (ta - base_sa) / kSlot;
         unsigned long long pos = 0;
         if (col_ok) {
-          atomicAdd(a.le + j, (unsigned long long)le);
+          atomicAdd(a.le + j, (unsigned long long)le + le2);
           if (cnt) pos = atomicAdd(a.cursor + j, (unsigned long long)cnt);
         }
         unsigned fm = __ballot_sync(0xffffffffu, cnt > 0);
