@@ -1579,17 +1579,20 @@ void store_value(double v, cpsel_dtype dt, void* h_out) {
 cpsel_status run_direct(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype dtype, uint64_t k, void* h_out,
                         cpsel_info* info) {
   const auto t0 = std::chrono::steady_clock::now();
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  struct Ev {  // destroyed on every return path
+    cudaEvent_t e = nullptr;
+    ~Ev() { if (e) cudaEventDestroy(e); }
+  } e0, e1;
   const bool timed = ctx->cfg.record_timing == 1;
   if (timed) {
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
-    CK(cudaEventRecord(e0, ctx->stream));
+    CK(cudaEventCreate(&e0.e));
+    CK(cudaEventCreate(&e1.e));
+    CK(cudaEventRecord(e0.e, ctx->stream));
   }
   const unsigned long long seq = ++ctx->seq;
   CK(launch_exact_cluster((int)dtype, d_x, n, k, &ctx->mb_dev->direct_value, &ctx->mb_dev->direct_bad,
                           &ctx->mb_dev->seq_direct, seq, ctx->stream));
-  if (timed) CK(cudaEventRecord(e1, ctx->stream));
+  if (timed) CK(cudaEventRecord(e1.e, ctx->stream));
   const volatile unsigned long long* f = &ctx->mb->seq_direct;
   for (uint32_t i = 1; *f != seq; ++i) {
     if ((i & 255u) == 0u) {
@@ -1606,10 +1609,8 @@ cpsel_status run_direct(cpsel_ctx* ctx, const void* d_x, uint64_t n, cpsel_dtype
   const unsigned long long bad = ctx->mb->direct_bad;
   float kms = 0.f;
   if (timed) {
-    CK(cudaEventSynchronize(e1));
-    cudaEventElapsedTime(&kms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    CK(cudaEventSynchronize(e1.e));
+    cudaEventElapsedTime(&kms, e0.e, e1.e);
   }
   ctx->trace.clear();
   if (bad) return fail(ctx, CPSEL_ENONFINITE, "input holds NaN or Inf");

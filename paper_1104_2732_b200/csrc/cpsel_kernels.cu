@@ -49,25 +49,8 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
-// the same with an L2 eviction policy (createpolicy): the init pass streams x with evict_first
-// so that its ~2% copy, stored with evict_last, stays in L2 for the radix rounds that read it next
-__device__ __forceinline__ float4 ld_stream(const float4* p, uint64_t pol) {
-  float4 r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ double2 ld_stream(const double2* p, uint64_t pol) {
-  double2 r;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.f64 {%0,%1}, [%2], %3;"
-      : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
-  return r;
-}
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
+// L2 eviction policy (createpolicy) for the init pass's copy: stored evict_last, it stays in L2 for
+// the radix rounds that read it next
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -84,11 +67,6 @@ __device__ __forceinline__ float lane_of(const float4& v, int j) {
 }
 __device__ __forceinline__ double lane_of(const double2& v, int j) { return j == 0 ? v.x : v.y; }
 
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
 
 template <typename T> __device__ __forceinline__ T tmax(T a, T b);
 template <> __device__ __forceinline__ float tmax(float a, float b) { return fmaxf(a, b); }
@@ -1131,8 +1109,6 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(PassArgs a) {
 
 // ------------------------------------------------------------------------------------------
 // Step a5: radix select on order-preserving keys.
-constexpr int kRadixBits = 11;
-constexpr int kBins = 1 << kRadixBits;
 
 template <typename T> struct HistFn {
   unsigned* sh;
@@ -1457,7 +1433,7 @@ struct RadixArgs {
   const SegEntry* tab;  // nullptr: contiguous
   int side;
   RadixState* st;
-  unsigned* hist;       // kBins global counters, zero between rounds
+  unsigned* hist;       // 2048 global digit counters, zero between rounds
   unsigned* ticket;
   int shift, bits, first, last;
   uint64_t r;           // the rank (1-based), taken by the first round

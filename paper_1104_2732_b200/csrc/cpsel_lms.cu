@@ -28,6 +28,24 @@
 namespace cpsel {
 namespace {
 
+// a start/end CUDA-event pair, destroyed on every return path
+struct EventPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EventPair() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~EventPair() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  float ms() const {
+    float v = 0.f;
+    cudaEventElapsedTime(&v, a, b);
+    return v;
+  }
+};
+
 constexpr int TM = 128;              // rows per tile (TMEM lanes)
 constexpr int TN = 256;              // candidates per tile (TMEM columns per accumulator)
 constexpr int KP = 16;               // padded K
@@ -721,21 +739,16 @@ static cudaError_t run_batched(LmsWorkspace& w, BatchArgs a, LmsReport* rep, uin
   if (a.f_le) a.fail_count = reinterpret_cast<unsigned*>(base + scratch + 96);
   cudaError_t e = cudaMemsetAsync(base + scratch, 0, 256, st);
   if (e != cudaSuccess) return e;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0, st);
+  EventPair ev;
+  cudaEventRecord(ev.a, st);
   e = launch_batched_select(a, grid, st);
   if (e != cudaSuccess) return e;
-  cudaEventRecord(e1, st);
+  cudaEventRecord(ev.b, st);
   e = cudaMemcpyAsync(w.host, base + scratch + 64, 40, cudaMemcpyDeviceToHost, st);
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  const float ms = ev.ms();
   const unsigned long long* h = static_cast<const unsigned long long*>(w.host);
   if (rep) {
     rep->passes += (uint32_t)h[0];
@@ -1030,27 +1043,21 @@ cudaError_t lms_fused_select(LmsWorkspace& w, const float* X, const float* y, ui
     return e;
   if ((e = cudaMemsetAsync(c.le, 0, (size_t)C * 16, st)) != cudaSuccess) return e;  // le + cursor
   iota_kernel<<<1, 256, 0, st>>>(c.ct_list, g.n_ct);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaEventRecord(e0, st);
+  EventPair ev;
+  cudaEventRecord(ev.a, st);
   if ((e = fused_sample_cuts(w, g, X, y, n, p, C, k, c, st)) != cudaSuccess) return e;
   FusedArgs a{};
   a.n = n; a.C = C; a.ct_list = c.ct_list;
   a.cuts = c.cuts; a.le = c.le; a.cursor = c.cursor; a.z = w.fz; a.zcap = zcap;
   if ((e = fused_launch<kFuseCuts>(g, a, g.n_ct, st)) != cudaSuccess) return e;
-  cudaEventRecord(e1, st);
+  cudaEventRecord(ev.b, st);
   // continuation on the per-column copies
   BatchArgs b{nullptr, n, C, k, out, nullptr, 0, nullptr, nullptr, max_iters};
   b.f_cuts = c.cuts; b.f_le = c.le; b.f_cursor = c.cursor; b.f_z = w.fz; b.f_zcap = zcap;
   b.fail_list = c.fail_list;
   uint32_t nfail = 0;
   e = run_batched(w, b, rep, &nfail, st);
-  float fms = 0.f;
-  cudaEventElapsedTime(&fms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (rep) { rep->ms_fused = fms; rep->fallback = nfail; }
+  if (rep) { rep->ms_fused = ev.ms(); rep->fallback = nfail; }
   if (e != cudaSuccess) return e;
   if (nfail == 0) return cudaSuccess;
   // fallback: store S for the failed columns only (same kernel, same arithmetic), select from it
