@@ -3087,6 +3087,7 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
         const int t = warp;
         const unsigned long long rk = sh.rank[t];
         const unsigned cs = sh.csum[t][lane];
+        __syncwarp();  // every lane has read rank before lane 0 rewrites it below
         unsigned incl = cs;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -3237,6 +3238,7 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
       if (warp == 0) {
         const unsigned long long rk = sh.rank;
         const unsigned cs = sh.csum[lane];
+        __syncwarp();  // every lane has read rank before lane 0 rewrites it below
         unsigned incl = cs;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {

@@ -502,6 +502,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
               const bool need = ta - base_sa >= kFlush * kSlot;
               unsigned fm = __ballot_sync(0xffffffffu, need);
               if (fm) {
+                __syncwarp();  // every lane's staged stores visible to the warp before the reads
                 unsigned long long pos = 0;
                 if (need) pos = atomicAdd(a.cursor + j, (unsigned long long)kFlush);
                 while (fm) {  // two threads per round: half-warp h serves owner h
@@ -568,6 +569,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
+        fence_proxy_async_smem();  // ybuf[s] reads ordered before the bulk copy that refills it
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
       }
@@ -580,6 +582,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
           if (cnt) pos = atomicAdd(a.cursor + j, (unsigned long long)cnt);
         }
         unsigned fm = __ballot_sync(0xffffffffu, cnt > 0);
+        __syncwarp();  // every lane's staged stores visible to the warp before the reads
         while (fm) {  // cooperative write-out of every thread's remaining staged elements
           const int L = __ffs(fm) - 1;
           fm &= fm - 1;

@@ -37,4 +37,22 @@ uid = cp.nccl_unique_id()
 cp.comm_init(uid, 0, 1, 0)
 x = datagen.make("mix1", n, "f32")
 assert cp.select_kth_sharded(torch.from_numpy(x).cuda(), 12345) == float(O.order_statistic(x, 12345))
+# round-1 additions: the direct device chain (init-counted radix round 0, n >= 2^27), the one-launch
+# small-array path, the fused LMS / LTS tensor-core passes and their stored-S fallback
+for dtype in ("f32", "f64"):
+    xb = datagen.make("normal", (1 << 27) + 5, dtype, device="cuda")
+    kb = O.median_rank(xb.numel())
+    vb = cp.select_kth(xb, kb)
+    assert (0.0 if vb == 0 else vb) == float(torch.kthvalue(xb.cpu(), kb).values), dtype
+    del xb
+for dtype, m in (("f32", 100_000), ("f64", 5_000)):
+    xs = datagen.make("cauchy", m, dtype)
+    assert cp.median(torch.from_numpy(xs).cuda()) == float(O.median(xs))
+X, y, th, _ = datagen.lms_problem(n=20_011, p=10, C=140)
+Xd, yd, thd = (torch.from_numpy(a).cuda() for a in (X, y, th))
+got = cp.lms_objective(Xd, yd, thd).cpu().numpy()
+S = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
+assert all(got[j] == O.order_statistic(S[j], O.median_rank(X.shape[0])) for j in range(140))
+F, mth = cp.lts_objective(Xd, yd, thd, (X.shape[0] + 10) // 2)
+torch.cuda.synchronize()
 print("sanitize workload ok")
