@@ -153,6 +153,28 @@ __device__ __forceinline__ void stream_array(const T* __restrict__ x, uint64_t n
 }
 
 // ------------------------------------------------------------------------------------------
+// Programmatic dependent launch: a kernel launched with pdl_launch() may be scheduled while the
+// kernel before it in the stream is still running (that one calls pdl_trigger()); it calls
+// pdl_wait() before touching anything the previous kernel writes.  Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
+// ------------------------------------------------------------------------------------------
 // Result mailbox: after the finishing thread wrote the result (possibly into mapped host memory),
 // make it visible system-wide, then set the flag the host spins on.
 __device__ __forceinline__ void publish_done(unsigned long long* done, unsigned long long seq) {
@@ -1446,6 +1468,8 @@ struct RadixArgs {
 
 template <typename T, bool SEG>
 __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
+  pdl_wait();     // the previous round's digit / the init's copy and chain decision
+  pdl_trigger();  // the next round may be scheduled (it waits for this grid to finish)
   if (a.chain) {
     if (!a.chain->ok[1]) {  // skipped: the init's round-0 counts must still be cleared
       if (a.hist0 && blockIdx.x == 0)
@@ -2062,6 +2086,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   using F = InitSeg<T, SUMS>;
   using V = typename VecOf<T>::V;
   constexpr int VE = VecOf<T>::N;
+  pdl_wait();  // the sample kernel's cuts
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
   const uint64_t Wtot = (uint64_t)gridDim.x * kWarps;
@@ -2149,6 +2174,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     o.cnt[1] = 0;
     a.seg_out[W] = o;
   }
+  pdl_trigger();  // the chained radix round may be scheduled now (it waits for this grid to finish)
   if (hist) {  // this CTA's round-0 histogram into the global one (before the grid finish's fence)
     __syncthreads();
     for (int i = threadIdx.x; i < 2048; i += kBlock)
@@ -2887,11 +2913,11 @@ cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, con
   // the same grid as seg_pass_kernel: its warp regions / run table are what later passes read
   const int g = s.grid_seg[dtype];
   if (dtype == kF32) {
-    if (sums) init_seg_kernel<float, true><<<g, kBlock, 0, st>>>(ia, a);
-    else init_seg_kernel<float, false><<<g, kBlock, 0, st>>>(ia, a);
+    if (sums) return pdl_launch(init_seg_kernel<float, true>, dim3(g), dim3(kBlock), 0, st, ia, a);
+    return pdl_launch(init_seg_kernel<float, false>, dim3(g), dim3(kBlock), 0, st, ia, a);
   } else {
-    if (sums) init_seg_kernel<double, true><<<g, kBlock, 0, st>>>(ia, a);
-    else init_seg_kernel<double, false><<<g, kBlock, 0, st>>>(ia, a);
+    if (sums) return pdl_launch(init_seg_kernel<double, true>, dim3(g), dim3(kBlock), 0, st, ia, a);
+    return pdl_launch(init_seg_kernel<double, false>, dim3(g), dim3(kBlock), 0, st, ia, a);
   }
   return cudaGetLastError();
 }
@@ -2937,6 +2963,8 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
   cg::cluster_group cl = cg::this_cluster();
   using SK = SampleKey<T>;
   using K = typename SK::K;
+  pdl_wait();
+  pdl_trigger();  // the init pass may be scheduled (it waits for the cuts)
   extern __shared__ __align__(16) unsigned char csm[];
   ClusterSel& sh = *reinterpret_cast<ClusterSel*>(csm);
   unsigned long long* pre = reinterpret_cast<unsigned long long*>(csm + sizeof(ClusterSel));  // run-table prefix
@@ -3381,11 +3409,11 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
     const int grid = tab ? s.grid_seg[dtype]
                          : clamp_grid(s.grid_hist[dtype], m, kBlock * 2 * (dtype == kF32 ? 4 : 2));
     if (dtype == kF32) {
-      if (tab) radix_round_kernel<float, true><<<grid, kBlock, 0, st>>>(a);
-      else radix_round_kernel<float, false><<<grid, kBlock, 0, st>>>(a);
+      if (tab) pdl_launch(radix_round_kernel<float, true>, dim3(grid), dim3(kBlock), 0, st, a);
+      else pdl_launch(radix_round_kernel<float, false>, dim3(grid), dim3(kBlock), 0, st, a);
     } else {
-      if (tab) radix_round_kernel<double, true><<<grid, kBlock, 0, st>>>(a);
-      else radix_round_kernel<double, false><<<grid, kBlock, 0, st>>>(a);
+      if (tab) pdl_launch(radix_round_kernel<double, true>, dim3(grid), dim3(kBlock), 0, st, a);
+      else pdl_launch(radix_round_kernel<double, false>, dim3(grid), dim3(kBlock), 0, st, a);
     }
   }
   return cudaGetLastError();
