@@ -49,19 +49,6 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
-// L2 eviction policy (createpolicy) for the init pass's copy: stored evict_last, it stays in L2 for
-// the radix rounds that read it next
-__device__ __forceinline__ uint64_t l2_policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ void st_keep(float* p, float v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void st_keep(double* p, double v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
-}
 __device__ __forceinline__ float lane_of(const float4& v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
 }
@@ -2067,10 +2054,9 @@ template <typename T, bool SUMS> struct InitSeg {
     __syncwarp();
     T* dst = out + reg_lo + n_in;
     if (hist0) {  // radix round 0 of the copy (direct chain): top digit of each copied element
-      const uint64_t keep = l2_policy_evict_last();  // the radix rounds read the copy next
-      for (unsigned i = lane; i < tot; i += 32) {
-        const T v = stage[i];
-        st_keep(dst + i, v, keep);
+      for (unsigned i = lane; i < tot; i += 32) {  // (an L2 evict-last store hint here measured
+        const T v = stage[i];                        //  1% slower overall: plain stores)
+        dst[i] = v;
         atomicAdd(&hist0[(unsigned)(okey(v) >> (sizeof(T) == 4 ? 21 : 53)) & 2047u], 1u);
       }
     } else {
