@@ -17,6 +17,9 @@
 //             128 B, pointer-stepped by n), then arrive on the TMEM-empty barrier.
 // The stage is HBM-write bound (4 bytes of S per 2p flops); the tensor cores keep the contraction
 // off the FP32 pipes so the epilogue can stream S at full bandwidth.
+//
+// The default LMS/LTS path never stores S: fused_tc_kernel (below) runs the same product transposed
+// and takes the selection's first pass in its epilogue.
 #include <cstdint>
 #include <cstring>
 #include <vector>
@@ -454,6 +457,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
         const uint32_t s = it & 1, ph = (it >> 1) & 1;
         const uint64_t row0 = (uint64_t)rt * FN + rq * kFRows;
+        const bool tile_full = row0 + kFRows <= a.n;
         mbar_wait_sleep(&tfull[s], ph);
         mbar_wait_sleep(&yfull[s], ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
@@ -471,7 +475,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
             asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(yv[v].x), "=l"(yv[v].y) : "r"(ya));
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          const int nvalid = rowc + 32 <= a.n ? 32 : (rowc >= a.n ? 0 : (int)(a.n - rowc));
+          int nvalid = 32;  // only the last row tile is ragged
+          if (!tile_full) nvalid = rowc + 32 <= a.n ? 32 : (rowc >= a.n ? 0 : (int)(a.n - rowc));
           if (MODE == kFuseCuts) {
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
