@@ -274,6 +274,7 @@ constexpr int kFuseCuts = 0, kFuseStore = 1, kFuseLts = 2;
 constexpr int FN = 256;                    // rows per tile (TMEM columns per accumulator)
 constexpr int kFEpiWarps = 16;             // 4 per TMEM lane quarter, each on 64 of the 256 rows
 constexpr int kFYWarp = 2 + kFEpiWarps;    // the warp that stages y for each accumulator stage
+constexpr int kFStages = 3;                // operand (Theta + X tile) stages in shared memory
 constexpr int kFThreads = 32 * (3 + kFEpiWarps);
 constexpr int kFRows = FN / 4;             // rows per epilogue warp per tile
 constexpr int kRing = 32;                  // staging slots per epilogue thread
@@ -335,23 +336,25 @@ template <int MODE>
 __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  unsigned char* stage[2] = {smem, smem + STAGE};
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + 2;
-  uint64_t* tfull = bars + 4;
-  uint64_t* tempty = bars + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
-  uint64_t* yfull = bars + 10;     // [2]: y of the tile in accumulator stage s has landed in ybuf[s]
-  float* ybuf = reinterpret_cast<float*>(smem + 2 * STAGE + 128);  // [2][FN]
-  const uint32_t ring_sa = smem_u32(smem + 2 * STAGE + 128 + 2 * FN * 4);  // 512 threads x kLaneStage B
+  // kFStages operand stages (the loads run up to kFStages-1 tiles ahead), 2 TMEM accumulators
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFStages * STAGE);
+  uint64_t* full = bars;                    // [kFStages]
+  uint64_t* empty = bars + kFStages;        // [kFStages]
+  uint64_t* tfull = bars + 2 * kFStages;    // [2]
+  uint64_t* tempty = tfull + 2;             // [2]
+  uint64_t* yfull = tempty + 2;             // [2]: y of the tile in accumulator stage s is in ybuf[s]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yfull + 2);
+  float* ybuf = reinterpret_cast<float*>(smem + kFStages * STAGE + 128);  // [2][FN]
+  const uint32_t ring_sa = smem_u32(smem + kFStages * STAGE + 128 + 2 * FN * 4);  // 512 threads x kLaneStage B
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t units = a.n_ct_list * a.n_chunks;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kFStages; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kFEpiWarps);
       mbar_init(&yfull[i], 1);
@@ -392,11 +395,11 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
         const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
         for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
-          const uint32_t s = it & 1, ph = (it >> 1) & 1;
+          const uint32_t s = it % kFStages, ph = (it / kFStages) & 1;
           mbar_wait_sleep(&empty[s], ph ^ 1);
           mbar_expect_tx(&full[s], STAGE);
-          bulk_g2s(stage[s], a.a_img + (size_t)ct * A_IMG, A_IMG, &full[s]);
-          bulk_g2s(stage[s] + A_IMG, a.b_img + ((size_t)ct * a.b_ct_stride + rt) * B_IMG, B_IMG, &full[s]);
+          bulk_g2s(smem + s * STAGE, a.a_img + (size_t)ct * A_IMG, A_IMG, &full[s]);
+          bulk_g2s(smem + s * STAGE + A_IMG, a.b_img + ((size_t)ct * a.b_ct_stride + rt) * B_IMG, B_IMG, &full[s]);
         }
       }
     }
@@ -407,14 +410,15 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       const uint32_t ch = u / a.n_ct_list;
       const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
       for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
-        const uint32_t s = it & 1, ph = (it >> 1) & 1;
+        const uint32_t s = it & 1, ph = (it >> 1) & 1;                       // TMEM stage
+        const uint32_t ss = it % kFStages, sph = (it / kFStages) & 1;       // operand stage
         mbar_wait_sleep(&tempty[s], ph ^ 1);
-        mbar_wait_sleep(&full[s], ph);
+        mbar_wait_sleep(&full[ss], sph);
         asm volatile("tcgen05.fence::after_thread_sync;");
         if (lane == 0) {
           const uint32_t d = tmem_base + s * FN;
-          const unsigned char* A = stage[s];
-          const unsigned char* B = stage[s] + A_IMG;
+          const unsigned char* A = smem + ss * STAGE;
+          const unsigned char* B = smem + ss * STAGE + A_IMG;
           for (int ks = 0; ks < 2; ++ks) {
             const uint64_t ahi = sdesc(A + ks * 256), alo = sdesc(A + A_HALF + ks * 256);
             const uint64_t bhi = sdesc(B + ks * 256), blo = sdesc(B + B_HALF + ks * 256);
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
             mma_tf32(d, alo, bhi, 1u);                // x_hi * theta_lo
             mma_tf32(d, ahi, bhi, 1u);
           }
-          mma_commit(&empty[s]);
+          mma_commit(&empty[ss]);
           mma_commit(&tfull[s]);
         }
         __syncwarp();
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   }
 }
 
-constexpr size_t kFusedSmem = 2 * STAGE + 1024 + 128 + 2 * FN * 4 + (size_t)kFEpiWarps * 32 * kLaneStage;  // ring, barriers, y, staging
+constexpr size_t kFusedSmem = kFStages * STAGE + 1024 + 128 + 2 * FN * 4 + (size_t)kFEpiWarps * 32 * kLaneStage;  // ring, barriers, y, staging
 
 __global__ void pad_copy_kernel(const float* __restrict__ src, uint64_t n, float* __restrict__ dst, uint64_t n_pad) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (uint64_t)gridDim.x * blockDim.x)
