@@ -449,3 +449,16 @@ def test_direct_chain_declined_then_reused(cp):
     for kk in (k, n // 10):
         v2, info2 = cp.select_kth(y, kk, return_info=True)
         assert canon(v2) == float(O.order_statistic(host(y), kk)), info2
+
+
+@pytest.mark.parametrize("dist", ["uniform", "dup256"])
+def test_direct_chain_extreme_ranks(cp, dist):
+    """n = 2^27 + 3 takes the direct device chain; the extreme ranks (the cuts sit at the ends of the
+    sample, or the chain stands down) and a ragged n stay bit-exact."""
+    n = (1 << 27) + 3
+    xd = datagen.make(dist, n, "f32", device="cuda")
+    x = host(xd)
+    xs = np.sort(x)
+    for k in (1, 2, 1000, n - 1, n):
+        v, info = cp.select_kth(xd, k, return_info=True)
+        assert canon(v) == float(xs[k - 1]), (dist, k, info)
