@@ -3346,13 +3346,14 @@ cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const Seg
                                  const ChainState* chain, int which) {
   if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
   (void)keys;
-  // one cluster launch: 8 CTAs x 1024 threads x KPT samples (131072 / 8192 for f32, 16384 / 8192 f64;
-  // f32 at 131072: the init's copy ~1% of n — measured +1.1% whole-step vs 32768)
+  // one cluster launch: 8 CTAs x 1024 threads x KPT samples (131072 / 8192 for f32, 65536 / 8192 f64;
+  // f32 at 131072: the init's copy ~1% of n — measured +1.1% whole-step vs 32768; f64 at 65536:
+  // 2^28 median 0.555 -> 0.545 ms vs 16384)
   if (dtype == kF32)
     return small ? sample_cluster_t<float, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which)
                  : sample_cluster_t<float, 16>(x, m, tab, side, Wtot, r, t0, st, chain, which);
   return small ? sample_cluster_t<double, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which)
-               : sample_cluster_t<double, 2>(x, m, tab, side, Wtot, r, t0, st, chain, which);
+               : sample_cluster_t<double, 8>(x, m, tab, side, Wtot, r, t0, st, chain, which);
 }
 
 
