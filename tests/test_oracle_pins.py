@@ -282,6 +282,87 @@ def test_pass_stats_identities():
     assert s["pred"] == x[(x > yL) & (x < t)].max() and s["succ"] == x[(x > t) & (x < yR)].min()
 
 
+def _grid_samples(rng, count):
+    """Small integer-valued samples with heavy duplication: every sum below is exact in float64,
+    and data values (kinks of F) are plentiful so brackets and queries land ON the grid."""
+    for _ in range(count):
+        n = rng.randint(2, 14)
+        yield [float(rng.randint(-4, 4)) for _ in range(n)]
+
+
+def test_F_from_PN_matches_eq2_and_exact_rationals():
+    """oracle.F_from_PN / eval_at()['F'] against two independent forms of Eq. 2:
+    the exact-rational F_k (frac_F, itself pinned to the rank definition by
+    test_eq2_minimizer_is_kth_smallest_with_mapped_k) and oracle.f_os (the penalty u exactly as
+    printed, with paper-k = n-k+1).  Queries on and off the data grid, every k: the weights
+    (k-1/2) on P and (n-k+1/2) on N are not symmetric for k != (n+1)/2, so swapping them fails."""
+    rng = random.Random(11)
+    for xs in _grid_samples(rng, 150):
+        x = np.array(xs)
+        n = x.size
+        grid = sorted(set(xs))
+        ys = grid + [grid[0] - 0.75, grid[-1] + 1.25] + [(a + b) / 2 for a, b in zip(grid, grid[1:])]
+        for y in ys:
+            for k in range(1, n + 1):
+                e = O.eval_at(x, k, y, -math.inf, math.inf)
+                exact = frac_F(xs, y, k)
+                assert Fraction(float(e["F"])) == exact, (xs, y, k)
+                assert float(O.F_from_PN(n, k, e["P"], e["N"])) == float(exact)
+                assert float(O.f_os(x, y, k)) == float(exact)
+
+
+def test_F_from_PN_minimizer_is_kth_smallest():
+    """Brute force: over the data values, the F assembled by eval_at (F_from_PN of the pass's P and
+    N) is minimised exactly at x_(k) (rank definition), and nowhere else (the 1/2 offsets make the
+    minimiser unique, reading R6)."""
+    rng = random.Random(12)
+    for xs in _grid_samples(rng, 150):
+        x = np.array(xs)
+        for k in range(1, x.size + 1):
+            vals = {v: float(O.eval_at(x, k, v, -math.inf, math.inf)["F"]) for v in set(xs)}
+            best = min(vals.values())
+            assert {v for v, f in vals.items() if f == best} == {brute_kth(xs, k)}
+
+
+def test_pass_stats_strict_bracket_on_grid():
+    """pass_stats' bracket is OPEN at both ends (P:L196 'y_L < x_i < y_R'), checked with y_L, t,
+    y_R ON data values that carry duplicates, against properties fixed by the mathematics:
+      c_lo = #{x<t} - #{x<=y_L},  c_hi = #{x<y_R} - #{x<=t}          (counts, brute force)
+      N(t) = N(y_L) + #{x<=y_L}(t-y_L) + L_lo                        (App. A, exact here)
+      P(t) = P(y_R) + #{x>=y_R}(y_R-t) + L_hi
+      pred = x_(#{x<t}) if any element lies in ]y_L,t[ else -inf     (order statistics of
+      succ = x_(#{x<=t}+1) if any element lies in ]t,y_R[ else +inf   a sorted copy)
+    An inclusive end double-counts the elements equal to y_L / y_R in c_lo / L_lo (resp. c_hi /
+    L_hi) and reports pred = y_L on an empty ]y_L, t[."""
+    rng = random.Random(13)
+    cases = 0
+    for xs in _grid_samples(rng, 400):
+        grid = sorted(set(xs))
+        if len(grid) < 3:
+            continue
+        x = np.array(xs)
+        srt = sorted(xs)
+        for i in range(len(grid)):
+            for j in range(i + 1, len(grid)):
+                for q in range(i + 1, j):
+                    yL, t, yR = grid[i], grid[q], grid[j]
+                    s = O.pass_stats(x, t, yL, yR)
+                    lt_t = sum(a < t for a in xs)
+                    le_t = sum(a <= t for a in xs)
+                    le_L = sum(a <= yL for a in xs)
+                    lt_R = sum(a < yR for a in xs)
+                    ge_R = len(xs) - lt_R
+                    assert s["c_lo"] == lt_t - le_L and s["c_hi"] == lt_R - le_t
+                    NL = sum(yL - a for a in xs if a < yL)
+                    PR = sum(a - yR for a in xs if a > yR)
+                    assert float(s["N"]) == NL + le_L * (t - yL) + float(s["L_lo"])
+                    assert float(s["P"]) == PR + ge_R * (yR - t) + float(s["L_hi"])
+                    assert s["pred"] == (srt[lt_t - 1] if lt_t > le_L else -math.inf)
+                    assert s["succ"] == (srt[le_t] if le_t < lt_R else math.inf)
+                    cases += 1
+    assert cases > 1000
+
+
 # ----------------------------------------------------------------------------- Algorithm 1
 def test_appendix_A_kelley_step_is_interior_mean_exact_rationals():
     """with the tightest cuts, step 1.1 equals the arithmetic mean of
