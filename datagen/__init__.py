@@ -175,3 +175,65 @@ def lms_problem(n: int = 1_000_000, p: int = 10, C: int = 4096, seed: int = SEED
     thetas = theta_star[None, :] + sig[:, None] * rng.standard_normal((C, p))
     return (np.ascontiguousarray(X.astype(np.float32)), y.astype(np.float32),
             np.ascontiguousarray(thetas.astype(np.float32)), theta_star)
+
+
+# ----------------------------------------------------------------------------- shard-invariant
+# "generated on device; shard-invariant" — element i of the global array is a pure
+# function of (seed, distribution, i), so rank g of G can draw exactly its block [lo, hi) and the
+# concatenation over ranks is the same array for every G (the strong-scaling runs of configs[3]
+# select from identical data at G = 1, 2, 4, 8).  Counter-based: splitmix64 of the global index,
+# in int64 torch ops (wrapping multiply; logical shifts by masking), on any torch device.
+_M64 = (1 << 64) - 1
+
+
+def _s64(c: int) -> int:
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+_SM_GAMMA, _SM_M1, _SM_M2 = _s64(0x9E3779B97F4A7C15), _s64(0xBF58476D1CE4E5B9), _s64(0x94D049BB133111EB)
+
+
+def _shr(z, s: int):
+    """logical right shift of int64 (torch's >> is arithmetic)"""
+    return (z >> s) & ((1 << (64 - s)) - 1)
+
+
+def _splitmix(idx, key: int):
+    z = idx * _SM_GAMMA + _s64((key * 0xD1B54A32D192ED03) & _M64)
+    z = (z ^ _shr(z, 30)) * _SM_M1
+    z = (z ^ _shr(z, 27)) * _SM_M2
+    return z ^ _shr(z, 31)
+
+
+GLOBAL_DISTS = ["uniform", "normal"]  # configs[3]
+
+
+def make_global(dist: str, n_global: int, lo: int, hi: int, dtype: str = "f32", seed: int = SEED,
+                device="cpu", chunk: int = 1 << 26):
+    """Elements [lo, hi) of the shard-invariant global array of n_global values of `dist`
+    (uniform: 24 (f32) / 53 (f64) random bits; normal: Box-Muller of two such uniforms, in f64).
+    Returns a torch tensor on `device`."""
+    import torch
+    if not (0 <= lo <= hi <= n_global):
+        raise ValueError("need 0 <= lo <= hi <= n_global")
+    if dist not in GLOBAL_DISTS:
+        raise ValueError(f"make_global supports {GLOBAL_DISTS}")
+    tdt = {"f32": torch.float32, "f64": torch.float64}[dtype]
+    out = torch.empty(hi - lo, dtype=tdt, device=device)
+    key = (seed * 64 + _STREAM[dist]) & _M64
+    for a in range(lo, hi, chunk):
+        b = min(a + chunk, hi)
+        idx = torch.arange(a, b, dtype=torch.int64, device=device)
+        if dist == "uniform":
+            z = _splitmix(idx, key)
+            if dtype == "f32":
+                v = _shr(z, 40).to(torch.float32) * (2.0 ** -24)
+            else:
+                v = _shr(z, 11).to(torch.float64) * (2.0 ** -53)
+        else:
+            u1 = (_shr(_splitmix(idx, key), 11).to(torch.float64) + 1.0) * (2.0 ** -53)   # (0, 1]
+            u2 = _shr(_splitmix(idx, key ^ 0x5DEECE66D), 11).to(torch.float64) * (2.0 ** -53)
+            v = torch.sqrt(-2.0 * torch.log(u1)) * torch.cos((2.0 * np.pi) * u2)
+        out[a - lo:b - lo] = v.to(tdt)
+        del idx
+    return out

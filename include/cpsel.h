@@ -50,7 +50,7 @@ typedef struct {
   uint64_t z_cap;            /* compaction threshold on the bracket interior count m: the first
                                 pass whose interior m <= z_cap also copies the two halves of the
                                 bracket (split at t) out (P:L196 copy_if, R8); later passes run on
-                                the kept half only and compact again.  0 = auto (n/2). */
+                                the kept half only and compact again.  0 = auto (5/8 n). */
   uint64_t direct_threshold; /* n <= this: skip the cutting plane, select on x directly
                                 (P:L311 'radix sort ... most efficient up to 2^21').  Default 2^17 */
   uint64_t select_cap;       /* a kept half of <= select_cap elements is finished by the exact
@@ -224,10 +224,27 @@ cpsel_status cpsel_get_trace(const cpsel_ctx* ctx, cpsel_trace_row* rows, uint32
 cpsel_status cpsel_nccl_unique_id(void* id_out128);
 /* Collective: every rank calls with the same id, its rank and the world size. */
 cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int world);
+/* Loopback transport (SURVEY §4 "G virtual shards on one GPU"): `world` virtual ranks inside ONE
+ * process, each a host thread with its own ctx (and stream) on the same device.  The sharded driver
+ * runs unchanged; its all-gathers become device-to-device copies ordered by CUDA events between
+ * two host barriers.  create: *out <- a group handle owned by the caller (destroy it after every
+ * ctx attached to it has been destroyed or re-initialised; the ctxs keep the group alive until
+ * then).  comm_init_loopback: attach ctx as `rank` (each rank exactly once).  A rank that does not
+ * reach a collective within 120 s breaks the group: every rank's call then fails with ENCCL.
+ * Errors: EINVAL (null pointers, rank outside [0, world)), ENCCL (rank already attached). */
+typedef struct cpsel_loopback cpsel_loopback;
+cpsel_status cpsel_loopback_create(int world, cpsel_loopback** out);
+void cpsel_loopback_destroy(cpsel_loopback* group);
+cpsel_status cpsel_comm_init_loopback(cpsel_ctx* ctx, cpsel_loopback* group, int rank);
 /* Collective: x is the concatenation over ranks (in rank order) of the shards d_shard
  * (n_local elements each, may differ per rank, may be 0).  k is the global rank.  Every
- * rank receives the same *h_out.  Per iteration one 64-byte-per-rank NCCL all-gather of
- * the pass tuples; at the end an NCCL all-gather-v of the bracket contents (north_star). */
+ * rank receives the same *h_out.  Init: the pooled sample (R28: each rank's share of 131072
+ * (f32) / 65536 (f64) evenly strided values, proportional to its shard, all-gathered; every rank
+ * picks the same two cuts with the same cluster select), the fused init pass per rank, and an
+ * all-gather of the 128-byte init records.  Per iteration one 96-byte-per-rank all-gather of the
+ * pass tuples, combined in rank order; at the end an all-gather-v of the bracket contents
+ * (north_star; <= 2^22 elements in all unless select_cap says otherwise) and the same radix select
+ * on every rank. */
 cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint64_t n_local,
                                       cpsel_dtype dtype, uint64_t k, void* h_out, cpsel_info* info);
 

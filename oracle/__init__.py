@@ -343,3 +343,51 @@ def lts_objective(rsq, h: int):
     b = int(np.count_nonzero(r == m))
     a = h - bL
     return float(np.sum(r[r < m].astype(LD)) + LD(a) / LD(b) * np.sum(r[r == m].astype(LD)))
+
+
+# ============================================================================ C++ baselines
+_CLIB = None
+
+
+def _clib():
+    """oracle/liboracle_c.so (built by __graft_entry__.build() from oracle/cselect.cpp)."""
+    global _CLIB
+    if _CLIB is None:
+        import ctypes
+        import os
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "liboracle_c.so")
+        if not os.path.exists(p):
+            build_c()
+        lib = ctypes.CDLL(p)
+        for name, ct in (("f32", ctypes.c_float), ("f64", ctypes.c_double)):
+            for fn in ("oracle_nth_element_", "oracle_sort_select_"):
+                f = getattr(lib, fn + name)
+                f.restype = ctypes.c_double
+                f.argtypes = [ctypes.POINTER(ct), ctypes.c_uint64, ctypes.c_uint64]
+        _CLIB = lib
+    return _CLIB
+
+
+def build_c() -> str:
+    """Compile oracle/cselect.cpp (g++ -O2, single thread) into oracle/liboracle_c.so."""
+    import os
+    import subprocess
+    d = os.path.dirname(os.path.abspath(__file__))
+    out = os.path.join(d, "liboracle_c.so")
+    subprocess.run(["g++", "-O2", "-std=c++17", "-shared", "-fPIC", "-o", out + ".tmp",
+                    os.path.join(d, "cselect.cpp")], check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
+def order_statistic_c(x, k: int, method: str = "nth_element"):
+    """x_(k) (P:L32) by the C++ std::nth_element (the paper's CPU quickselect row, P:L339) or
+    std::sort on a copy — the single-core CPU baselines of SURVEY §8(d)."""
+    import ctypes
+    x = np.ascontiguousarray(_as_array(x))
+    n = check_input(x, k)
+    name = ("oracle_nth_element_" if method == "nth_element" else "oracle_sort_select_") + \
+        ("f32" if x.dtype == np.float32 else "f64")
+    ct = ctypes.c_float if x.dtype == np.float32 else ctypes.c_double
+    v = getattr(_clib(), name)(x.ctypes.data_as(ctypes.POINTER(ct)), n, k)
+    return canonical(x.dtype.type(v))

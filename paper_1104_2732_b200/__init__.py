@@ -17,6 +17,7 @@ __all__ = [
     "select_kth", "median", "select_kth_host", "lms_objective", "lms_residuals", "select_kth_batched",
     "eval", "init_stats", "small_select", "get_trace", "set_config", "get_config", "nccl_unique_id",
     "comm_init", "select_kth_sharded", "drive_host", "library_path", "load", "CpselError",
+    "LoopbackGroup", "comm_init_loopback",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -110,7 +111,7 @@ SYMBOLS = [
     "cpsel_select_kth_host", "cpsel_lms_objective", "cpsel_lms_residuals", "cpsel_select_kth_batched",
     "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_init_timings", "cpsel_nccl_unique_id",
     "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host", "cpsel_pooled_cuts",
-    "cpsel_lts_objective",
+    "cpsel_lts_objective", "cpsel_loopback_create", "cpsel_loopback_destroy", "cpsel_comm_init_loopback",
 ]
 
 _lib = None
@@ -160,6 +161,9 @@ def load():
                                      C.POINTER(Info), C.POINTER(TraceRow), U32, C.POINTER(U32)]),
             "cpsel_pooled_cuts": (I, [P, P, U32, U64, I, C.POINTER(D)]),
             "cpsel_lts_objective": (I, [P, P, P, U64, U32, P, U32, U64, P, P, C.POINTER(Info)]),
+            "cpsel_loopback_create": (I, [I, C.POINTER(P)]),
+            "cpsel_loopback_destroy": (None, [P]),
+            "cpsel_comm_init_loopback": (I, [P, P, I]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -195,7 +199,16 @@ class _Ctx:
             pass
 
 
-_ctxs: dict[int, _Ctx] = {}
+# One ctx per (thread, device): a ctx is not thread-safe (include/cpsel.h) and ctypes releases the
+# GIL during every call, so threads never share one.  A thread's ctxs are destroyed when it ends.
+_tls = threading.local()
+
+
+def _ctxs() -> dict:
+    d = getattr(_tls, "ctxs", None)
+    if d is None:
+        d = _tls.ctxs = {}
+    return d
 
 
 def _current_stream(dev: int) -> int:
@@ -204,23 +217,19 @@ def _current_stream(dev: int) -> int:
     return raw(dev) if raw is not None else torch.cuda.current_stream(dev).cuda_stream
 
 
+def _ctx_device(dev: int) -> _Ctx:
+    d = _ctxs()
+    c = d.get(dev)
+    if c is None:
+        c = d[dev] = _Ctx(dev)
+    c.bind_stream(_current_stream(dev))
+    return c
+
+
 def _ctx_for(t) -> _Ctx:
     if not getattr(t, "is_cuda", False):
         raise ValueError("expected a CUDA tensor (no CPU fallback)")
-    dev = t.get_device()
-    c = _ctxs.get(dev)
-    if c is None:
-        c = _ctxs[dev] = _Ctx(dev)
-    c.bind_stream(_current_stream(dev))
-    return c
-
-
-def _ctx_device(dev: int) -> _Ctx:
-    c = _ctxs.get(dev)
-    if c is None:
-        c = _ctxs[dev] = _Ctx(dev)
-    c.bind_stream(_current_stream(dev))
-    return c
+    return _ctx_device(t.get_device())
 
 
 def _check(ctx: _Ctx, st: int):
@@ -335,7 +344,7 @@ def init_timings(device: int = 0, reset: bool = True) -> list:
 
 
 def get_trace(device: int = 0) -> list:
-    c = _ctxs.get(device)
+    c = _ctxs().get(device)
     if c is None:
         return []
     n = C.c_uint32()
@@ -450,6 +459,32 @@ def comm_init(uid: bytes, rank: int, world: int, device: int) -> None:
     c = _ctx_device(device)
     buf = C.create_string_buffer(uid, 128)
     _check(c, load().cpsel_comm_init(c.handle, buf, int(rank), int(world)))
+
+
+class LoopbackGroup:
+    """`world` virtual ranks on one device inside this process: each rank is a thread
+    that calls comm_init_loopback(group, rank, device) and then select_kth_sharded on its shard —
+    the real sharded driver, its all-gathers as device-to-device copies."""
+
+    def __init__(self, world: int):
+        self.world = int(world)
+        self.handle = C.c_void_p()
+        st = load().cpsel_loopback_create(self.world, C.byref(self.handle))
+        if st != OK:
+            raise CpselError(st, "cpsel_loopback_create failed")
+
+    def __del__(self):
+        try:
+            if self.handle and _lib is not None:
+                _lib.cpsel_loopback_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def comm_init_loopback(group: LoopbackGroup, rank: int, device: int = 0) -> None:
+    """Attach the calling thread's ctx on `device` to the loopback group as `rank`."""
+    c = _ctx_device(device)
+    _check(c, load().cpsel_comm_init_loopback(c.handle, group.handle, int(rank)))
 
 
 def select_kth_sharded(shard, k: int, return_info: bool = False):

@@ -20,6 +20,7 @@
 #include "../../include/cpsel.h"
 #include "cpsel_kernels.h"
 #include "cpsel_lms.h"
+#include "cpsel_comm.h"
 #include "cpsel_nccl.h"
 
 using namespace cpsel;
@@ -62,17 +63,14 @@ struct cpsel_ctx {
   RadixState* h_radix = nullptr;
   DevPass* h_gather = nullptr;
   DevInit* h_gather_init = nullptr;
-  // sharded sample cuts (R28): this rank's 1024 sorted sample keys, all ranks' (G x 1024), shard sizes
-  unsigned long long* d_keys = nullptr;
-  unsigned long long* d_keys_all = nullptr;
-  unsigned long long* h_keys_all = nullptr;
+  // sharded sample cuts (R28): the pooled sample (every rank's share of evenly strided values), shard sizes
+  void* d_pool = nullptr;
   unsigned long long* d_sizes = nullptr;     // [0] this rank's, [1..G] all ranks'
   unsigned long long* h_sizes = nullptr;
   // LMS workspace
   LmsWorkspace lms;
   // multi-GPU
-  ncclComm_t comm = nullptr;
-  int rank = 0, world = 1;
+  Comm comm;  // NCCL communicator or loopback group (cpsel_comm.h)
   // last trace
   std::vector<cpsel_trace_row> trace;
   // kernel timing (record_timing): a pool of (start, end) event pairs, one pair per step of a
@@ -298,7 +296,17 @@ struct GpuBackend : Backend {
     static const bool on = !(getenv("CPSEL_INIT_HIST0") && getenv("CPSEL_INIT_HIST0")[0] == '0');
     return on && dt == kF32;
   }
-  cudaError_t light_mark() {  // start/end of the init kernel in the light ring
+  // start/end of the init kernel in the light ring: at most kLightPairs pairs are kept until the
+  // caller reads them (further selections go untimed); a start whose end was never recorded (an
+  // error in between) is overwritten by the next start, so pairs stay aligned
+  static constexpr uint32_t kLightPairs = 4096;
+  cudaError_t light_mark(bool start) {
+    if (start) {
+      ctx->light_n &= ~1u;
+      if (ctx->light_n >= 2 * kLightPairs) return cudaSuccess;
+    } else if ((ctx->light_n & 1u) == 0) {
+      return cudaSuccess;  // its start was not recorded
+    }
     if (ctx->light_ev.size() <= ctx->light_n) {
       cudaEvent_t e;
       cudaError_t err = cudaEventCreate(&e);
@@ -384,7 +392,7 @@ struct GpuBackend : Backend {
       sample_slot = slot;
       CK(tic());
     }
-    if (light()) CK(light_mark());
+    if (light()) CK(light_mark(true));
     // the device chain (§8f-3) when its continuation is likely: the init's copy (~1-4% of n) will
     // exceed the exact-selection cap
     spec = Spec{};
@@ -414,7 +422,7 @@ struct GpuBackend : Backend {
       CK(launch_init(dt, a, ctx->shape, ctx->stream, false));
     }
     CK(toc());
-    if (light()) CK(light_mark());
+    if (light()) CK(light_mark(false));
     const int init_slot_ = slot;
     if (chain) CK(direct ? launch_chain_direct() : launch_chain(k));
     slot = init_slot_;
@@ -424,9 +432,13 @@ struct GpuBackend : Backend {
       cpsel_status w = wait_mail(&ctx->mb->seq_init, a.seq);
       if (w != CPSEL_OK) return w;
       *ctx->h_init = ctx->mb->init;
-    } else {
+    } else if (sync_result) {
       CK(cudaMemcpyAsync(ctx->h_init, ctx->d_init, sizeof(DevInit), cudaMemcpyDeviceToHost, ctx->stream));
       CK(cudaStreamSynchronize(ctx->stream));
+    } else {
+      // the caller reads the record from d_init itself (sharded: all-gathered, checked after it)
+      init_seg_done = fuse;
+      return CPSEL_OK;
     }
     const DevInit& r = *ctx->h_init;
     // fast form: no non-finite count; NaN/Inf surface as a non-finite sum/extreme or, with the
@@ -835,15 +847,40 @@ struct ShardedBackend : GpuBackend {
   ShardedBackend(cpsel_ctx* c, const void* x_, uint64_t n_local, int dt_) : GpuBackend(c, x_, n_local, dt_) {
     use_mail = false;  // the per-rank tuples are all-gathered from device memory
   }
-  // the final all-gather-v sends each rank's kept part as one contiguous block
-  bool kept_dense() const override { return last_dense; }
+  Comm& comm() const { return ctx->comm; }
+  int G() const { return ctx->comm.world; }
+  // every kept part is selectable: select() packs a segmented one before the all-gather-v
+  bool kept_dense() const override { return true; }
+
+#define CM(expr)                                                                 \
+  do {                                                                           \
+    const char* m_ = (expr);                                                     \
+    if (m_) return fail(ctx, CPSEL_ENCCL, "%s: %s", #expr, m_);                  \
+  } while (0)
+
+  // all-gather `bytes` per rank from d_src into d_all and bring the G records to h_all
+  cpsel_status gather_records(const void* d_src, void* d_all, void* h_all, size_t bytes) {
+    CM(comm().allgather(d_src, d_all, bytes, ctx->stream));
+    CK(cudaMemcpyAsync(h_all, d_all, (size_t)G() * bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return CPSEL_OK;
+  }
+
+  // the fast init's record needs the checked form (same test as the one-GPU path)
+  static bool suspicious(const DevInit& r, bool cut, int dt) {
+    const bool f32 = dt == kF32;
+    const double out_lo = f32 ? (double)std::nextafterf((float)r.vmin, -INFINITY) : std::nextafter(r.vmin, -INFINITY);
+    const double out_hi = f32 ? (double)std::nextafterf((float)r.vmax, INFINITY) : std::nextafter(r.vmax, INFINITY);
+    return cut ? (!std::isfinite(r.N_lo) || !std::isfinite(r.P_hi) || !std::isfinite(r.I_in) || !std::isfinite(r.t_est) ||
+                  ((r.has_cut & 8) && !(std::isfinite(out_lo) && std::isfinite(out_hi))) || !std::isfinite(r.vmin) ||
+                  !std::isfinite(r.vmax) || r.nonfinite != 0)
+               : (!std::isfinite(r.S) || !std::isfinite(r.vmin) || !std::isfinite(r.vmax));
+  }
 
   // All-gather the per-rank init records and combine them in rank order (R17).
   cpsel_status gather_init() {
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
     if (n > 0) {
-      cpsel_status st = run_init(false, 0, false);  // leaves the (checked) record in d_init
+      cpsel_status st = run_init(true, 0, false);  // leaves the (checked) record in d_init
       if (st != CPSEL_OK) return st;
     } else {
       launches = 0;
@@ -855,19 +892,18 @@ struct ShardedBackend : GpuBackend {
     // carry the shard size in the pad word
     *reinterpret_cast<uint64_t*>(&ctx->h_init[0].pad) = n;
     CK(cudaMemcpyAsync(&ctx->d_init->pad, &ctx->h_init[0].pad, sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream));
-    NK(nc.AllGather(ctx->d_init, ctx->d_gather_init, sizeof(DevInit), ncclUint8, ctx->comm, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_gather_init, ctx->d_gather_init, G * sizeof(DevInit), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    cpsel_status st = gather_records(ctx->d_init, ctx->d_gather_init, ctx->h_gather_init, sizeof(DevInit));
+    if (st != CPSEL_OK) return st;
     if (n == 0) slot = -1;
     scanned = n;
-    n_rank.assign(G, 0);
+    const int Gn = G();
+    n_rank.assign(Gn, 0);
     combined = cpsel_init_stats{};
     combined.vmin = INFINITY; combined.vmax = -INFINITY;
     n_global = 0;
     bool have_x0 = false;
     double S = 0.0;
-    for (int q = 0; q < G; ++q) {
+    for (int q = 0; q < Gn; ++q) {
       const DevInit& r = ctx->h_gather_init[q];
       n_rank[q] = r.pad;
       n_global += r.pad;
@@ -886,44 +922,59 @@ struct ShardedBackend : GpuBackend {
   }
   // every rank's shard size (one tiny all-gather), before the buffers are sized
   cpsel_status exchange_sizes() {
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
+    const int Gn = G();
     ctx->h_sizes[0] = n;
     CK(cudaMemcpyAsync(ctx->d_sizes, ctx->h_sizes, sizeof(unsigned long long), cudaMemcpyHostToDevice, ctx->stream));
-    NK(nc.AllGather(ctx->d_sizes, ctx->d_sizes + 1, 1, ncclUint64, ctx->comm, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_sizes + 1, ctx->d_sizes + 1, G * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    n_rank.assign(ctx->h_sizes + 1, ctx->h_sizes + 1 + G);
+    cpsel_status st = gather_records(ctx->d_sizes, ctx->d_sizes + 1, ctx->h_sizes + 1, sizeof(unsigned long long));
+    if (st != CPSEL_OK) return st;
+    n_rank.assign(ctx->h_sizes + 1, ctx->h_sizes + 1 + Gn);
     n_global = 0;
     for (uint64_t v : n_rank) n_global += v;
     return CPSEL_OK;
   }
-  // R28: cuts around pooled rank r of the ranks' current arrays (m_rank elements each; the raw x
-  // when `on_x`) into d_t0 on every rank, identical everywhere; t[0..2] = t_a, t_b, estimate
-  cpsel_status pooled_t0(bool on_x, const std::vector<uint64_t>& m_rank, uint64_t r, double t[3]) {
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
-    if (on_x || !cur_seg)
-      CK(launch_sample_cut(dt, on_x ? x : cur, on_x ? n : n_cur, 1, ctx->d_t0, ctx->stream, 1024, ctx->d_keys));
-    else
-      CK(launch_sample_seg(dt, cur, cur_tab, cur_side, seg_total_warps(dt, ctx->shape), n_cur, 1, ctx->d_t0,
-                           ctx->stream, 1024, ctx->d_keys));
-    NK(nc.AllGather(ctx->d_keys, ctx->d_keys_all, 1024, ncclUint64, ctx->comm, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_keys_all, ctx->d_keys_all, (size_t)G * 1024 * sizeof(unsigned long long),
-                       cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    if (!pooled_pick(ctx->h_keys_all, m_rank, r, dt, t)) return fail(ctx, CPSEL_EINTERNAL, "no samples");
-    unsigned char buf[24];
-    for (int j = 0; j < 3; ++j) {
-      if (dt == kF32) {
-        const float f = (float)t[j];
-        memcpy(buf + 4 * j, &f, 4);
-      } else {
-        memcpy(buf + 8 * j, &t[j], 8);
+  // R28: the pooled sample.  The S samples of the one-GPU cut kernel (R29) are apportioned to the
+  // ranks in proportion to their current arrays (largest remainders, ties to the lower rank: the
+  // same numbers on every rank), each rank gathers its share of evenly strided values into its
+  // block of the pooled array, the blocks are all-gathered, and every rank runs the same cluster
+  // select on the same bytes -> identical cuts t0 = {t_a, t_b, estimate} around global rank r.
+  cpsel_status pooled_t0(bool on_x, const std::vector<uint64_t>& m_rank, uint64_t r) {
+    const int Gn = G();
+    const size_t es = elem_size(dt);
+    uint64_t M = 0;
+    for (uint64_t v : m_rank) M += v;
+    const bool small = M <= (1ull << 26) && !on_x;
+    const uint64_t S = pool_sample_size(dt, small);
+    std::vector<uint64_t> s(Gn, 0);
+    if (M <= S) {
+      s = m_rank;
+    } else {
+      uint64_t tot = 0;
+      std::vector<std::pair<unsigned long long, int>> rem;
+      for (int q = 0; q < Gn; ++q) {
+        const unsigned __int128 a = (unsigned __int128)S * m_rank[q];
+        s[q] = (uint64_t)(a / M);
+        tot += s[q];
+        rem.emplace_back((unsigned long long)(a % M), q);
       }
+      std::sort(rem.begin(), rem.end(), [](const auto& u, const auto& v) {
+        return u.first != v.first ? u.first > v.first : u.second < v.second;
+      });
+      for (size_t i = 0; tot < S && i < rem.size(); ++i, ++tot) s[rem[i].second] += 1;
     }
-    CK(cudaMemcpyAsync(ctx->d_t0, buf, dt == kF32 ? 12 : 24, cudaMemcpyHostToDevice, ctx->stream));
+    std::vector<size_t> bytes(Gn);
+    uint64_t off = 0, total = 0;
+    for (int q = 0; q < Gn; ++q) {
+      bytes[q] = (size_t)s[q] * es;
+      if (q < comm().rank) off += s[q];
+      total += s[q];
+    }
+    char* mine = static_cast<char*>(ctx->d_pool) + off * es;
+    const int W = seg_total_warps(dt, ctx->shape);
+    const bool seg = !on_x && cur_seg;
+    CK(launch_pool_gather(dt, on_x ? x : cur, on_x ? n : n_cur, seg ? cur_tab : nullptr, cur_side, W, s[comm().rank],
+                          mine, ctx->stream));
+    CM(comm().allgatherv(mine, ctx->d_pool, bytes.data(), ctx->stream));
+    CK(launch_pool_pick(dt, ctx->d_pool, total, M, r, ctx->d_t0, ctx->stream, small));
     return CPSEL_OK;
   }
   // the init pass: with cuts (R23/R28) every rank runs the fused init at the pooled cuts and the
@@ -940,14 +991,15 @@ struct ShardedBackend : GpuBackend {
       *o = combined;
       return CPSEL_OK;
     }
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
-    double tc[3];
-    cpsel_status st = pooled_t0(true, n_rank, k, tc);
+    const int Gn = G();
+    cpsel_status st = pooled_t0(true, n_rank, k);
     if (st != CPSEL_OK) return st;
     if (n > 0) {
-      st = run_init(false, k, true, /*presampled=*/true);  // launches: the sample kernel + the init
+      // launches: the pooled sample (gather + cluster select) and the init; the record is checked
+      // after the all-gather (every rank takes the same fallback decision)
+      st = run_init(false, k, true, /*presampled=*/true);
       if (st != CPSEL_OK) return st;
+      launches = 3;
     } else {
       launches = 1;
       slot = -1;
@@ -961,38 +1013,42 @@ struct ShardedBackend : GpuBackend {
       init_seg_done = true;
       init_n_in = 0;
     }
-    NK(nc.AllGather(ctx->d_init, ctx->d_gather_init, sizeof(DevInit), ncclUint8, ctx->comm, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_gather_init, ctx->d_gather_init, G * sizeof(DevInit), cudaMemcpyDeviceToHost,
-                       ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    st = gather_records(ctx->d_init, ctx->d_gather_init, ctx->h_gather_init, sizeof(DevInit));
+    if (st != CPSEL_OK) return st;
     scanned = n;
     cpsel_init_stats c{};
     c.vmin = INFINITY; c.vmax = -INFINITY;
     c.has_cut = 11;  // two cuts, the interior compacted, no sums, no #min/#max (R27)
-    c.t_lo = tc[0]; c.t_hi = tc[1]; c.t_est = tc[2];
-    init_rank.assign(G, 0);
+    init_rank.assign(Gn, 0);
     init_total = 0;
-    bool all_fused = true;
-    for (int q = 0; q < G; ++q) {
+    bool all_fused = true, have_cuts = false;
+    for (int q = 0; q < Gn; ++q) {
       const DevInit& r = ctx->h_gather_init[q];
       if (n_rank[q] == 0) continue;
+      if (!have_cuts) {  // the cuts: identical on every rank (same pooled bytes, same select)
+        c.t_lo = r.t_lo; c.t_hi = r.t_hi; c.t_est = r.t_est;
+        have_cuts = true;
+      }
       c.vmin = std::min(c.vmin, r.vmin);
       c.vmax = std::max(c.vmax, r.vmax);
       c.nonfinite += r.nonfinite;
       c.c_le_lo += r.c_le_lo;
       c.c_lt_hi += r.c_lt_hi;
-      if ((r.has_cut & 11) != 11) all_fused = false;  // a rank fell back to the checked init
+      if ((r.has_cut & 11) != 11 || suspicious(r, true, dt)) all_fused = false;
       init_rank[q] = r.pad;
       init_total += r.pad;
     }
     if (!all_fused || !std::isfinite(c.vmin) || !std::isfinite(c.vmax)) {
       // a rank saw NaN/Inf (or could not bracket from the extremes' neighbours): the plain path
+      init_seg_done = false;
       cpsel_status s2 = gather_init();
       if (s2 != CPSEL_OK) return s2;
       *o = combined;
       return CPSEL_OK;
     }
     sharded_fused = true;
+    init_seg_done = true;
+    init_n_in = init_rank[comm().rank];
     cur_rank = n_rank;
     *o = c;
     return CPSEL_OK;
@@ -1006,60 +1062,54 @@ struct ShardedBackend : GpuBackend {
   }
   // R26 + R28: the cut pass with cuts pooled across ranks; tuples all-gathered, combined in rank order
   bool has_cut_pass() const override { return R > 0; }
-  cpsel_status cut_pass(uint64_t r, bool dense, CutResult* o) override {
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
-    double tc[3];
-    cpsel_status st = pooled_t0(false, cur_rank, r, tc);
+  cpsel_status cut_pass(uint64_t r, bool /*dense*/, CutResult* o) override {
+    const int Gn = G();
+    CK(tic());
+    cpsel_status st = pooled_t0(false, cur_rank, r);
     if (st != CPSEL_OK) return st;
+    CK(toc());
+    sample_slot = slot;
     SegArgs a{};
     a.x = cur; a.n = n_cur;
     a.seg_in = cur_seg ? cur_tab : nullptr;
     a.side_in = cur_side;
     a.cuts = ctx->d_t0;
-    a.dense_out = dense ? 1 : 0;
-    if (dense) {
-      tgt = (cur_dbuf == 0) ? 1 : 0;
-      a.out = ctx->d_zb[tgt];
-      a.z_cap = cap;
-    } else {
-      tgt = (cur_sbuf == 0) ? 1 : 0;
-      a.out = ctx->d_sb[tgt];
-      a.R = R;
-      a.seg_out = static_cast<SegEntry*>(ctx->d_st[tgt]);
-    }
+    a.dense_out = 0;  // segmented (warp-private) copy; select() packs it
+    tgt = (cur_sbuf == 0) ? 1 : 0;
+    a.out = ctx->d_sb[tgt];
+    a.R = R;
+    a.seg_out = static_cast<SegEntry*>(ctx->d_st[tgt]);
     a.cursors = ctx->d_cursors;
     a.partials = ctx->d_partials; a.ticket = ctx->d_ticket;
     a.out_tuple = ctx->d_pass;
     CK(tic());
     CK(launch_cut_pass(dt, a, ctx->shape, ctx->stream));  // also for an empty array: run tables
     CK(toc());
-    launches = 2;
+    launches = 3;
     scanned = n_cur;
-    NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    o->ta = tc[0]; o->tb = tc[1]; o->t_est = tc[2];
+    st = gather_records(ctx->d_pass, ctx->d_gather, ctx->h_gather, sizeof(DevPass));
+    if (st != CPSEL_OK) return st;
+    const DevPass& me = ctx->h_gather[comm().rank];
+    o->ta = me.pred; o->tb = me.succ; o->t_est = me.L_lo;  // the cuts (identical on every rank)
     o->le_a = 0; o->inner = 0;
     o->overflow = false;
-    zlo_rank.assign(G, 0);
-    zhi_rank.assign(G, 0);
-    for (int q = 0; q < G; ++q) {
+    zlo_rank.assign(Gn, 0);
+    zhi_rank.assign(Gn, 0);
+    for (int q = 0; q < Gn; ++q) {
       const DevPass& rr = ctx->h_gather[q];
       o->le_a += rr.c_lt;
       o->inner += rr.z_lo;
       o->overflow |= rr.c_eq != 0;
       zlo_rank[q] = rr.z_lo;
     }
-    last_dense = dense;
-    zlo = ctx->h_gather[ctx->rank].z_lo;
+    last_dense = false;
+    zlo = me.z_lo;
     zhi = 0;
     return CPSEL_OK;
   }
   cpsel_status pass(double t, double yL, double yR, bool compact, bool dense, cpsel_pass_stats* o, uint64_t* z_lo,
                     uint64_t* z_hi) override {
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
+    const int Gn = G();
     if (n_cur > 0 || (compact && cur_seg)) {
       // (a segmented current array is processed even when empty so every warp writes its run table)
       cpsel_status st = launch_local_pass(t, yL, yR, compact, dense);
@@ -1078,18 +1128,17 @@ struct ShardedBackend : GpuBackend {
       *ctx->h_pass = e;
       CK(cudaMemcpyAsync(ctx->d_pass, ctx->h_pass, sizeof(DevPass), cudaMemcpyHostToDevice, ctx->stream));
     }
-    NK(nc.AllGather(ctx->d_pass, ctx->d_gather, sizeof(DevPass), ncclUint8, ctx->comm, ctx->stream));
-    CK(cudaMemcpyAsync(ctx->h_gather, ctx->d_gather, G * sizeof(DevPass), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    cpsel_status st = gather_records(ctx->d_pass, ctx->d_gather, ctx->h_gather, sizeof(DevPass));
+    if (st != CPSEL_OK) return st;
     // fixed rank-order combine: identical bytes on every rank (R17)
     cpsel_pass_stats s{};
     s.pred = -INFINITY; s.succ = INFINITY;
     uint64_t tlo = 0, thi = 0;
     if (compact) {
-      zlo_rank.assign(G, 0);
-      zhi_rank.assign(G, 0);
+      zlo_rank.assign(Gn, 0);
+      zhi_rank.assign(Gn, 0);
     }
-    for (int q = 0; q < G; ++q) {
+    for (int q = 0; q < Gn; ++q) {
       const DevPass& r = ctx->h_gather[q];
       s.c_lt += r.c_lt; s.c_eq += r.c_eq; s.c_lo += r.c_lo; s.c_hi += r.c_hi;
       s.L_lo += r.L_lo; s.L_hi += r.L_hi; s.P += r.P; s.N += r.N;
@@ -1099,8 +1148,8 @@ struct ShardedBackend : GpuBackend {
     }
     *o = s;
     if (compact) {
-      zlo = ctx->h_gather[ctx->rank].z_lo;
-      zhi = ctx->h_gather[ctx->rank].z_hi;
+      zlo = ctx->h_gather[comm().rank].z_lo;
+      zhi = ctx->h_gather[comm().rank].z_hi;
     }
     *z_lo = tlo; *z_hi = thi;
     return CPSEL_OK;
@@ -1109,29 +1158,41 @@ struct ShardedBackend : GpuBackend {
     cur_rank = side == 0 ? zlo_rank : zhi_rank;
     return GpuBackend::adopt(side);
   }
-  // all-gather-v of per-rank segments (grouped broadcasts), then the same select on every rank
+  // the exact finish (north_star "the final bracket contents are allgathered"): every
+  // rank's kept part (packed contiguously if it is segmented) all-gathered in rank order (an
+  // all-gather-v), then the same radix select on every rank.  One rank: the all-gather is the
+  // identity, the one-GPU select reads the kept part where it is.
   cpsel_status select(int side, uint64_t r, double* out) override {
-    const NcclApi& nc = nccl_api();
-    const int G = ctx->world;
+    if (G() == 1) return GpuBackend::select(side, r, out);
+    const int Gn = G();
     const size_t es = elem_size(dt);
     const std::vector<uint64_t>& cnt = side == 2 ? cur_rank : side == 0 ? zlo_rank : zhi_rank;
-    const void* mine = side == 2 ? cur : half_ptr(side);
-    uint64_t total = 0;
-    for (int q = 0; q < G; ++q) total += cnt[q];
+    uint64_t total = 0, off = 0;
+    std::vector<size_t> bytes(Gn);
+    for (int q = 0; q < Gn; ++q) {
+      if (q < comm().rank) off += cnt[q];
+      total += cnt[q];
+      bytes[q] = (size_t)cnt[q] * es;
+    }
     cpsel_status st = ensure(ctx, &ctx->d_zall, &ctx->zall_bytes, (size_t)total * es);
     if (st != CPSEL_OK) return st;
-    NK(nc.GroupStart());
-    uint64_t off = 0;
-    for (int q = 0; q < G; ++q) {
-      if (cnt[q]) {
-        NK(nc.Broadcast(q == ctx->rank ? mine : nullptr, static_cast<char*>(ctx->d_zall) + off * es,
-                        (size_t)cnt[q] * es, ncclUint8, q, ctx->comm, ctx->stream));
-      }
-      off += cnt[q];
+    char* mine = static_cast<char*>(ctx->d_zall) + off * es;
+    const void* send = mine;
+    const uint64_t cm = cnt[comm().rank];
+    const int W = seg_total_warps(dt, ctx->shape);
+    if (side == 2 ? cur_seg : !last_dense) {  // segmented: pack into this rank's block
+      const void* base = side == 2 ? cur : ctx->d_sb[tgt];
+      const SegEntry* tab = side == 2 ? cur_tab : static_cast<const SegEntry*>(ctx->d_st[tgt]);
+      if (cm) CK(launch_seg_pack(dt, base, tab, side == 2 ? cur_side : side, W, mine, ctx->stream));
+    } else {
+      send = side == 2 ? cur : half_ptr(side);
     }
-    NK(nc.GroupEnd());
-    return select_on(ctx->d_zall, total, r, out);
+    CM(comm().allgatherv(send, ctx->d_zall, bytes.data(), ctx->stream));
+    st = select_on(ctx->d_zall, total, r, out);
+    launches += 1;
+    return st;
   }
+#undef CM
 };
 
 // ------------------------------------------------------------------------ host callbacks
@@ -1738,16 +1799,16 @@ void cpsel_destroy(cpsel_ctx* ctx) {
   {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
-    if (ctx->comm && nccl_api().ok) nccl_api().CommDestroy(ctx->comm);
+    ctx->comm.release();
     void* dev[] = {ctx->d_t0, ctx->d_skeys, ctx->d_chain, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
-                   ctx->d_keys, ctx->d_keys_all, ctx->d_sizes,
+                   ctx->d_pool, ctx->d_sizes,
                    ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};
     for (void* p : dev)
       if (p) cudaFree(p);
     lms_free(ctx->lms);
     void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init, ctx->mb,
-                    ctx->h_keys_all, ctx->h_sizes};
+                    ctx->h_sizes};
     for (void* p : host)
       if (p) cudaFreeHost(p);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
@@ -1894,45 +1955,64 @@ cpsel_status cpsel_nccl_unique_id(void* id_out128) {
   return CPSEL_OK;
 }
 
-cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int world) {
-  if (!ctx || !id128 || world < 1 || rank < 0 || rank >= world) return CPSEL_EINVAL;
-  const NcclApi& nc = nccl_api();
-  if (!nc.ok) return fail(ctx, CPSEL_ENCCL, "NCCL unavailable: %s", nc.load_error);
-  DeviceGuard g(ctx->device);
-  if (ctx->comm) {
-    nc.CommDestroy(ctx->comm);
-    ctx->comm = nullptr;
-  }
-  ncclUniqueId id;
-  memcpy(&id, id128, 128);
-  NK(nc.CommInitRank(&ctx->comm, world, id, rank));
-  ctx->rank = rank;
-  ctx->world = world;
+// per-world buffers of the sharded path (tuples, records, sizes, the pooled sample)
+static cpsel_status comm_buffers(cpsel_ctx* ctx, int world) {
   if (ctx->d_gather) cudaFree(ctx->d_gather);
   if (ctx->d_gather_init) cudaFree(ctx->d_gather_init);
   if (ctx->h_gather) cudaFreeHost(ctx->h_gather);
   if (ctx->h_gather_init) cudaFreeHost(ctx->h_gather_init);
-  if (ctx->d_keys) cudaFree(ctx->d_keys);
-  if (ctx->d_keys_all) cudaFree(ctx->d_keys_all);
-  if (ctx->h_keys_all) cudaFreeHost(ctx->h_keys_all);
+  if (ctx->d_pool) cudaFree(ctx->d_pool);
   if (ctx->d_sizes) cudaFree(ctx->d_sizes);
   if (ctx->h_sizes) cudaFreeHost(ctx->h_sizes);
+  ctx->d_gather = nullptr; ctx->d_gather_init = nullptr; ctx->h_gather = nullptr; ctx->h_gather_init = nullptr;
+  ctx->d_pool = nullptr; ctx->d_sizes = nullptr; ctx->h_sizes = nullptr;
   CK(cudaMalloc(&ctx->d_gather, world * sizeof(DevPass)));
   CK(cudaMalloc(&ctx->d_gather_init, world * sizeof(DevInit)));
   CK(cudaHostAlloc(&ctx->h_gather, world * sizeof(DevPass), cudaHostAllocDefault));
   CK(cudaHostAlloc(&ctx->h_gather_init, world * sizeof(DevInit), cudaHostAllocDefault));
-  CK(cudaMalloc(&ctx->d_keys, 1024 * sizeof(unsigned long long)));
-  CK(cudaMalloc(&ctx->d_keys_all, (size_t)world * 1024 * sizeof(unsigned long long)));
-  CK(cudaHostAlloc(&ctx->h_keys_all, (size_t)world * 1024 * sizeof(unsigned long long), cudaHostAllocDefault));
+  CK(cudaMalloc(&ctx->d_pool, std::max(pool_sample_size(kF32, false) * 4, pool_sample_size(kF64, false) * 8)));
   CK(cudaMalloc(&ctx->d_sizes, (size_t)(world + 1) * sizeof(unsigned long long)));
   CK(cudaHostAlloc(&ctx->h_sizes, (size_t)(world + 1) * sizeof(unsigned long long), cudaHostAllocDefault));
   return CPSEL_OK;
 }
 
+cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int world) {
+  if (!ctx || !id128 || world < 1 || rank < 0 || rank >= world) return CPSEL_EINVAL;
+  const NcclApi& nc = nccl_api();
+  if (!nc.ok) return fail(ctx, CPSEL_ENCCL, "NCCL unavailable: %s", nc.load_error);
+  DeviceGuard g(ctx->device);
+  ctx->comm.release();
+  ncclUniqueId id;
+  memcpy(&id, id128, 128);
+  NK(nc.CommInitRank(&ctx->comm.nccl, world, id, rank));
+  ctx->comm.rank = rank;
+  ctx->comm.world = world;
+  return comm_buffers(ctx, world);
+}
+
+struct cpsel_loopback {
+  std::shared_ptr<LoopGroup> g;
+};
+
+cpsel_status cpsel_loopback_create(int world, cpsel_loopback** out) {
+  if (!out || world < 1) return CPSEL_EINVAL;
+  *out = new cpsel_loopback{std::make_shared<LoopGroup>(world)};
+  return CPSEL_OK;
+}
+
+void cpsel_loopback_destroy(cpsel_loopback* g) { delete g; }
+
+cpsel_status cpsel_comm_init_loopback(cpsel_ctx* ctx, cpsel_loopback* group, int rank) {
+  if (!ctx || !group || rank < 0 || rank >= group->g->world) return CPSEL_EINVAL;
+  DeviceGuard g(ctx->device);
+  if (const char* m = ctx->comm.attach_loop(group->g, rank)) return fail(ctx, CPSEL_ENCCL, "loopback: %s", m);
+  return comm_buffers(ctx, group->g->world);
+}
+
 cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint64_t n_local, cpsel_dtype dtype,
                                       uint64_t k, void* h_out, cpsel_info* info) {
   if (!ctx) return CPSEL_EINVAL;
-  if (!ctx->comm) return fail(ctx, CPSEL_ENCCL, "cpsel_comm_init has not been called");
+  if (!ctx->comm.active()) return fail(ctx, CPSEL_ENCCL, "cpsel_comm_init has not been called");
   if (n_local > 0 && !d_shard) return fail(ctx, CPSEL_EINVAL, "null shard pointer");
   if (dtype != CPSEL_F32 && dtype != CPSEL_F64) return fail(ctx, CPSEL_EINVAL, "bad dtype");
   if (!h_out) return fail(ctx, CPSEL_EINVAL, "null h_out");
@@ -1951,8 +2031,10 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
   if (s != CPSEL_OK) return s;
   double v = 0;
   // sharded: the kept bracket is all-gathered to every rank before its exact selection, so one more
-  // cut pass (a ~4% tuple exchange) beats gathering a 2^26 copy — the cap stays at 2^20
-  const uint64_t scap = ctx->cfg.select_cap ? ctx->cfg.select_cap : (1ull << 20);
+  // cut pass (a few-% tuple exchange) beats gathering a large copy — the cap is 2^22 elements
+  // (16 MB of f32 gathered); one rank gathers nothing and keeps the one-GPU cap
+  const uint64_t scap = ctx->cfg.select_cap ? ctx->cfg.select_cap
+                                            : (ctx->comm.world == 1 ? auto_select_cap(ctx->cfg) : (1ull << 22));
   s = drive(be, n, (int)dtype, k, ctx->cfg, zc, scap, &v, info, &ctx->trace);
   if (s == CPSEL_ENONFINITE) return fail(ctx, s, "input holds NaN or Inf");
   if (s == CPSEL_EINTERNAL) return fail(ctx, s, "cutting-plane safeguard tripped");

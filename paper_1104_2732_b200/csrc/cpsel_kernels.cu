@@ -1247,7 +1247,81 @@ template <typename T, bool INSIDE> struct WarpSeg {
     for (int u = 0; u < kSegU; ++u) glo[u] = ghi[u] = T(0);
     lo_bits = hi_bits = 0u;
   }
-  // close a group: sums to fp64, warp scan of the counts, stage, coalesced write-out
+  // close a group: sums to fp64, warp scan of the counts, stage, write-out.  Each half is staged at
+  // the 16-byte phase of its destination, so its aligned middle leaves shared memory as 16-byte
+  // vectors (LDS.128 -> STG.128, one instruction pair per 4 f32 / 2 f64 written) and only the
+  // < 16-byte head and tail as scalars.  (A cp.async.bulk store of the middle measured slower: one
+  // ~1 KB bulk copy per half-group per warp queues on the SM's TMA unit.)
+  static constexpr unsigned VA = 16 / sizeof(T);  // elements per 16 bytes
+  static constexpr int GWP = GW + VA;               // staging of one half, phase padding included
+  // dst[i] <- staged element i (shared-window address sa of element 0); dst and sa have the same
+  // 16-byte phase
+  __device__ __forceinline__ void flush(T* dst, unsigned sa, unsigned cnt) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned ph = (unsigned)(reinterpret_cast<uintptr_t>(dst) / sizeof(T)) & (VA - 1u);
+    unsigned head = (VA - ph) & (VA - 1u);
+    if (head > cnt) head = cnt;
+    const unsigned nv = (cnt - head) / VA, tail = cnt - head - nv * VA;
+    if (lane < head) dst[lane] = ld_sh(sa + lane * (unsigned)sizeof(T));
+    const unsigned t0 = head + nv * VA;
+    if (lane < tail) dst[t0 + lane] = ld_sh(sa + (t0 + lane) * (unsigned)sizeof(T));
+    char* dv = reinterpret_cast<char*>(dst + head);
+    const unsigned sv = sa + head * (unsigned)sizeof(T);
+    for (unsigned i = lane; i < nv; i += 32) {
+      unsigned r0, r1, r2, r3;
+      asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(sv + 16 * i));
+      asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(dv + 16 * (size_t)i), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+                   : "memory");
+    }
+  }
+  __device__ __forceinline__ static T ld_sh(unsigned a) {
+    if constexpr (sizeof(T) == 4) {
+      unsigned v;
+      asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+      return __uint_as_float(v);
+    } else {
+      unsigned long long v;
+      asm volatile("ld.shared.b64 %0, [%1];" : "=l"(v) : "r"(a));
+      return __longlong_as_double(v);
+    }
+  }
+  // staging of element j: to the lo half (bit j of lo_bits), the hi half, or nowhere — predicated
+  // shared stores with post-incremented addresses (no branches)
+  template <int J> __device__ __forceinline__ void stage_elem(unsigned& alo, unsigned& ahi) {
+    if constexpr (sizeof(T) == 4) {
+      asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+                   "and.b32 t, %2, %4;\n\t"
+                   "setp.ne.u32 p, t, 0;\n\t"
+                   "and.b32 t, %3, %4;\n\t"
+                   "setp.ne.u32 q, t, 0;\n\t"
+                   "@p st.shared.b32 [%0], %5;\n\t"
+                   "@p add.u32 %0, %0, 4;\n\t"
+                   "@q st.shared.b32 [%1], %5;\n\t"
+                   "@q add.u32 %1, %1, 4;\n\t}"
+                   : "+r"(alo), "+r"(ahi)
+                   : "r"(lo_bits), "r"(hi_bits), "n"(1u << J), "r"(__float_as_uint((float)vals[J]))
+                   : "memory");
+    } else {
+      asm volatile("{\n\t.reg .pred p, q;\n\t.reg .b32 t;\n\t"
+                   "and.b32 t, %2, %4;\n\t"
+                   "setp.ne.u32 p, t, 0;\n\t"
+                   "and.b32 t, %3, %4;\n\t"
+                   "setp.ne.u32 q, t, 0;\n\t"
+                   "@p st.shared.b64 [%0], %5;\n\t"
+                   "@p add.u32 %0, %0, 8;\n\t"
+                   "@q st.shared.b64 [%1], %5;\n\t"
+                   "@q add.u32 %1, %1, 8;\n\t}"
+                   : "+r"(alo), "+r"(ahi)
+                   : "r"(lo_bits), "r"(hi_bits), "n"(1u << J), "l"(__double_as_longlong((double)vals[J]))
+                   : "memory");
+    }
+  }
+  template <int J> __device__ __forceinline__ void stage_all(unsigned& alo, unsigned& ahi) {
+    if constexpr (J < G) {
+      stage_elem<J>(alo, ahi);
+      stage_all<J + 1>(alo, ahi);
+    }
+  }
   __device__ __forceinline__ void end() {
     L_lo += (double)((glo[0] + glo[1]) + (glo[2] + glo[3]));
     L_hi += (double)((ghi[0] + ghi[1]) + (ghi[2] + ghi[3]));
@@ -1261,16 +1335,6 @@ template <typename T, bool INSIDE> struct WarpSeg {
     }
     const unsigned tot = __shfl_sync(FULL, incl, 31);
     if (tot == 0u) return;
-    const unsigned pre = incl - packed;
-    unsigned plo = pre & 0xffffu, phi = pre >> 16;
-    T* slo = stage;
-    T* shi = stage + GW;
-#pragma unroll
-    for (int j = 0; j < G; ++j) {
-      if ((lo_bits >> j) & 1u) slo[plo++] = vals[j];
-      if ((hi_bits >> j) & 1u) shi[phi++] = vals[j];
-    }
-    __syncwarp();
     const unsigned nlo = tot & 0xffffu, nhi = tot >> 16;
     T* dlo;
     T* dhi;
@@ -1288,11 +1352,19 @@ template <typename T, bool INSIDE> struct WarpSeg {
       dlo = out + reg_lo + n_lo;
       dhi = out + (reg_end - n_hi - nhi);
     }
-    for (unsigned i = lane; i < nlo; i += 32) dlo[i] = slo[i];
-    for (unsigned i = lane; i < nhi; i += 32) dhi[i] = shi[i];
+    const unsigned phlo = (unsigned)(reinterpret_cast<uintptr_t>(dlo) / sizeof(T)) & (VA - 1u);
+    const unsigned phhi = (unsigned)(reinterpret_cast<uintptr_t>(dhi) / sizeof(T)) & (VA - 1u);
+    const unsigned slo = smem_u32(stage) + phlo * (unsigned)sizeof(T);
+    const unsigned shi = smem_u32(stage) + (GWP + phhi) * (unsigned)sizeof(T);
+    const unsigned pre = incl - packed;
+    unsigned alo = slo + (pre & 0xffffu) * (unsigned)sizeof(T), ahi = shi + (pre >> 16) * (unsigned)sizeof(T);
+    stage_all<0>(alo, ahi);
+    __syncwarp();
+    if (nlo) flush(dlo, slo, nlo);
+    if (nhi) flush(dhi, shi, nhi);
+    __syncwarp();  // the staging buffer is free for the next group
     n_lo += nlo;
     n_hi += nhi;
-    __syncwarp();
   }
 };
 
@@ -1581,9 +1653,9 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
 }
 
 template <typename T, bool INSIDE>
-__global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) seg_pass_kernel(SegArgs a) {
   using F = WarpSeg<T, INSIDE>;
-  __shared__ __align__(16) T stage_all[kWarps * 2 * F::GW];
+  __shared__ __align__(16) T stage_all[kWarps * 2 * F::GWP];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
   const uint64_t Wtot = (uint64_t)gridDim.x * kWarps;
@@ -1591,7 +1663,7 @@ __global__ void __launch_bounds__(kBlock) seg_pass_kernel(SegArgs a) {
   f.t = (T)a.t; f.yL = (T)a.y_lo; f.yR = (T)a.y_hi;
   f.L_lo = f.L_hi = 0.0;
   f.n_lo = f.n_hi = 0;
-  f.stage = stage_all + (size_t)w * 2 * F::GW;
+  f.stage = stage_all + (size_t)w * 2 * F::GWP;
   f.dense = a.dense_out;
   f.out = static_cast<T*>(a.out);
   f.reg_lo = W * a.R;
@@ -1795,7 +1867,7 @@ template <typename T> struct WarpCut {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kBlock) cut_pass_kernel(SegArgs a) {
+__global__ void __launch_bounds__(kBlock, 4) cut_pass_kernel(SegArgs a) {
   using F = WarpCut<T>;
   if (a.chain && !a.chain->ok[0]) return;  // a device-chain step whose chain did not hold
   __shared__ __align__(16) T stage_all[kWarps * F::GW];
@@ -2944,7 +3016,7 @@ struct ClusterSel {
 template <typename T, int KPT>
 __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     sample_cluster_kernel(const T* __restrict__ x, uint64_t m, const SegEntry* __restrict__ tab, int side, int Wtot,
-                          uint64_t r, T* t0, const ChainState* chain, int which) {
+                          uint64_t r, T* t0, const ChainState* chain, int which, uint64_t m_rank) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   using SK = SampleKey<T>;
@@ -3033,8 +3105,10 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     }
   }
   if (crank == 0 && i == 0) {
+    // m_rank: the population the sample stands for (the pooled sample of G ranks, R28: m samples
+    // of m_rank elements in all); 0 = m
     const double md = (double)ms;
-    const double q = ((double)r - 0.5) / (double)m * md;
+    const double q = ((double)r - 0.5) / (double)(m_rank ? m_rank : m) * md;
     const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
     const double qq[3] = {floor(q - w), ceil(q + w), floor(q)};
 #pragma unroll
@@ -3317,7 +3391,7 @@ cudaError_t launch_exact_cluster(int dtype, const void* x, uint64_t m, uint64_t 
 
 template <typename T, int KPT>
 cudaError_t sample_cluster_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
-                             cudaStream_t st, const ChainState* chain, int which) {
+                             cudaStream_t st, const ChainState* chain, int which, uint64_t m_rank = 0) {
   const size_t smem = sizeof(ClusterSel) + (tab ? (size_t)Wtot * 8 : 0);
   static bool attr = false;
   if (!attr) {
@@ -3327,7 +3401,7 @@ cudaError_t sample_cluster_t(const void* x, uint64_t m, const SegEntry* tab, int
     attr = true;
   }
   sample_cluster_kernel<T, KPT><<<kSampleCluster, 1024, smem, st>>>(static_cast<const T*>(x), m, tab, side, Wtot, r,
-                                                                   static_cast<T*>(t0), chain, which);
+                                                                   static_cast<T*>(t0), chain, which, m_rank);
   return cudaGetLastError();
 }
 
@@ -3357,6 +3431,127 @@ cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const Seg
 }
 
 
+
+// ---------------------------------------------------------------------------- sharded helpers (R28)
+// Inclusive prefix of the run lengths cnt[side] of tab[0..Wtot) into pre[] (shared), by the whole
+// CTA of kGatherThreads threads (per-thread chunks, warp and block scans).
+__device__ __forceinline__ void scan_runs(const SegEntry* __restrict__ tab, int side, int Wtot, unsigned long long* pre,
+                                          unsigned long long* wsum) {
+  const int i = threadIdx.x, lane = i & 31, warp = i >> 5;
+  constexpr int NW = kGatherThreads / 32;
+  const int per = (Wtot + kGatherThreads - 1) / kGatherThreads;
+  const int w0 = i * per, w1 = min(w0 + per, Wtot);
+  unsigned long long c = 0;
+  for (int w = w0; w < w1; ++w) {
+    c += tab[w].cnt[side];
+    pre[w] = c;
+  }
+  unsigned long long incl = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long v = lane < NW ? wsum[lane] : 0ull, inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += y;
+    }
+    if (lane < NW) wsum[lane] = inc - v;
+  }
+  __syncthreads();
+  const unsigned long long base = wsum[warp] + incl - c;
+  for (int w = w0; w < w1; ++w) pre[w] += base;
+  __syncthreads();
+}
+
+// This rank's share of the pooled sample (R28): ms evenly strided VALUES of its m-element current
+// array (contiguous x, or the runs `side` of tab[0..Wtot) based at x) into out[0..ms), ms <= m.
+// Sample s is element floor(s*m/ms) + (m/ms)/2, as in the one-GPU gather.
+template <typename T>
+__global__ void __launch_bounds__(kGatherThreads) pool_gather_kernel(const T* __restrict__ x, uint64_t m,
+                                                                     const SegEntry* __restrict__ tab, int side,
+                                                                     int Wtot, uint64_t ms, T* __restrict__ out) {
+  __shared__ unsigned long long pre[kGatherMaxWarps];
+  __shared__ unsigned long long wsum[32];
+  if (tab) scan_runs(tab, side, Wtot, pre, wsum);
+  const uint64_t smp = (uint64_t)blockIdx.x * kGatherThreads + threadIdx.x;
+  if (smp >= ms) return;
+  uint64_t g = (m == ms) ? smp : (smp * m) / ms + (m / ms) / 2;
+  if (!tab) {
+    out[smp] = x[g];
+    return;
+  }
+  int lo = 0, hi = Wtot - 1;  // first run whose inclusive prefix exceeds g
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (pre[mid] > g) hi = mid; else lo = mid + 1;
+  }
+  g -= lo ? pre[lo - 1] : 0ull;
+  out[smp] = x[tab[lo].off[side] + g];
+}
+
+// The runs `side` of the segmented array (base, tab[0..Wtot)) packed contiguously into out, in run
+// order (the sharded exact finish all-gathers one contiguous block per rank, a6).
+template <typename T>
+__global__ void __launch_bounds__(kGatherThreads) seg_pack_kernel(const T* __restrict__ base,
+                                                                  const SegEntry* __restrict__ tab, int side, int Wtot,
+                                                                  T* __restrict__ out) {
+  __shared__ unsigned long long pre[kGatherMaxWarps];
+  __shared__ unsigned long long wsum[32];
+  scan_runs(tab, side, Wtot, pre, wsum);
+  constexpr int NW = kGatherThreads / 32;
+  const int lane = threadIdx.x & 31;
+  for (int w = blockIdx.x * NW + (threadIdx.x >> 5); w < Wtot; w += gridDim.x * NW) {
+    const unsigned long long c = tab[w].cnt[side], o = tab[w].off[side], dst = pre[w] - c;
+    for (unsigned long long j = lane; j < c; j += 32) out[dst + j] = base[o + j];
+  }
+}
+
+cudaError_t launch_pool_gather(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
+                               uint64_t ms, void* out, cudaStream_t st) {
+  if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
+  if (ms == 0) return cudaSuccess;
+  const unsigned grid = (unsigned)((ms + kGatherThreads - 1) / kGatherThreads);
+  if (dtype == kF32)
+    pool_gather_kernel<float><<<grid, kGatherThreads, 0, st>>>(static_cast<const float*>(x), m, tab, side, Wtot, ms,
+                                                               static_cast<float*>(out));
+  else
+    pool_gather_kernel<double><<<grid, kGatherThreads, 0, st>>>(static_cast<const double*>(x), m, tab, side, Wtot, ms,
+                                                                static_cast<double*>(out));
+  return cudaGetLastError();
+}
+
+uint64_t pool_sample_size(int dtype, bool small) {
+  return (uint64_t)kSampleCluster * 1024 * (small ? 1 : (dtype == kF32 ? 16 : 8));
+}
+
+cudaError_t launch_pool_pick(int dtype, const void* pooled, uint64_t ms, uint64_t m_rank, uint64_t r, void* t0,
+                             cudaStream_t st, bool small) {
+  if (ms > pool_sample_size(dtype, small)) return cudaErrorInvalidValue;
+  if (dtype == kF32)
+    return small ? sample_cluster_t<float, 1>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank)
+                 : sample_cluster_t<float, 16>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank);
+  return small ? sample_cluster_t<double, 1>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank)
+               : sample_cluster_t<double, 8>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank);
+}
+
+cudaError_t launch_seg_pack(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, void* out,
+                            cudaStream_t st) {
+  if (Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
+  const int grid = 32;
+  if (dtype == kF32)
+    seg_pack_kernel<float><<<grid, kGatherThreads, 0, st>>>(static_cast<const float*>(base), tab, side, Wtot,
+                                                            static_cast<float*>(out));
+  else
+    seg_pack_kernel<double><<<grid, kGatherThreads, 0, st>>>(static_cast<const double*>(base), tab, side, Wtot,
+                                                             static_cast<double*>(out));
+  return cudaGetLastError();
+}
 
 cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, uint64_t m,
                               uint64_t r, void* t0, cudaStream_t st, uint32_t smax, unsigned long long* keys_out) {

@@ -195,6 +195,20 @@ cudaError_t launch_sample_seg(int dtype, const void* base, const SegEntry* tab, 
 // pred = t_a, succ = t_b, c_eq = 1 if a dense copy would not fit z_cap (then it is not kept).
 cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, cudaStream_t st);
 
+// Sharded sample cuts (R28): each rank gathers ms <= m evenly strided VALUES of its current array
+// (contiguous x, or runs `side` of tab[0..Wtot)) into out[0..ms); the ranks' shares are all-gathered
+// into one pooled array of <= pool_sample_size() values, and launch_pool_pick finds, on every rank
+// from the same bytes, t0[0..2] = the cuts around rank r of the m_rank-element global array and the
+// estimate (the one-GPU cluster select, with the rank scaled by m_rank instead of the sample size).
+// launch_seg_pack: the runs `side` of a segmented array packed contiguously into out (run order).
+uint64_t pool_sample_size(int dtype, bool small);
+cudaError_t launch_pool_gather(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
+                               uint64_t ms, void* out, cudaStream_t st);
+cudaError_t launch_pool_pick(int dtype, const void* pooled, uint64_t ms, uint64_t m_rank, uint64_t r, void* t0,
+                             cudaStream_t st, bool small);
+cudaError_t launch_seg_pack(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, void* out,
+                            cudaStream_t st);
+
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
 // t0[0], t0[1] <- the sample quantiles bracketing rank k (1024 strided samples of x, one CTA)
 cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, void* t0, cudaStream_t st,

@@ -522,3 +522,25 @@ def test_lts_identity_h_smallest():
         h = rng.randint(1, n)
         expect = sum(sorted(rsq)[:h])
         assert O.lts_objective(np.array(rsq), h) == pytest.approx(expect, rel=4 * 2.2e-16, abs=1e-300)
+
+
+# ----------------------------------------------------------------------------- C++ baselines
+def test_order_statistic_c_matches_definition():
+    """oracle.order_statistic_c (std::nth_element / std::sort on a copy, SURVEY §8(c)) pinned to the
+    definition written out: every k of small random arrays with ties, +-0 and huge magnitudes
+    against sorted(list) in Python, for both dtypes; the input is left untouched."""
+    rng = np.random.default_rng(7)
+    for dtype in (np.float32, np.float64):
+        for n in (1, 2, 3, 7, 64, 257):
+            x = rng.integers(-5, 6, n).astype(dtype) * rng.choice([1.0, 1e9, 1e-30], n).astype(dtype)
+            x[rng.random(n) < 0.2] = -0.0
+            before = x.copy()
+            s = sorted(float(v) for v in x)
+            for k in range(1, n + 1):
+                want = s[k - 1] + 0.0
+                for method in ("nth_element", "sort"):
+                    got = float(O.order_statistic_c(x, k, method))
+                    assert got == want and (got != 0 or math.copysign(1, got) == 1), (n, k, method)
+            assert np.array_equal(before, x, equal_nan=True)
+    with pytest.raises(ValueError):
+        O.order_statistic_c(np.ones(3, np.float32), 4)
