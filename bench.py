@@ -1,18 +1,28 @@
 #!/usr/bin/env python
-"""Benchmark: exact median (k-th order statistic) of n = 2^30 float32 per GPU by the cutting-plane
-path (BASELINE.json metric: "elements/s and HBM-roofline fraction for k-th select at n=2^30,
-1/2/4/8 B200").
+"""Benchmark: exact k-th order statistic by the cutting-plane path (BASELINE.json metric:
+"elements/s and HBM-roofline fraction for k-th select at n=2^30, 1/2/4/8 B200").
 
-One step = one median selection over each of the four resident synthetic arrays (uniform, normal,
-Cauchy, many-duplicate; BASELINE.json configs[1] distributions at the metric size), i.e.
-4 x 2^30 elements per GPU per step.  At N>1 each rank holds its own 2^30-element shard of every
-array and the step is one sharded selection over N x 2^30 elements (weak scaling; one NCCL
-all-gather of the 96-byte pass tuple per iteration, an all-gather-v of the bracket at the end).
+N = 1 (the headline, BASELINE's metric configuration): one step = one median selection over each
+of four resident synthetic arrays of 2^30 float32 (uniform, normal, Cauchy, many-duplicate;
+configs[1]'s distributions at the metric size) = 4 x 2^30 elements.  The default path: the init
+pass evaluates two cuts at sample quantiles of the target rank (R23/R29) and the exact radix
+select finishes on the ~1% between them; Kelley passes run only when the cuts miss.  Side blocks
+(rank 0, N = 1): "kelley" — the paper's method as published (Kelley passes from [x_(1), x_(n)],
+init_cut=0 pass_cuts=0 objective=1) at the same size with its per-pass rooflines;
+"configs" — BASELINE configs[0] (1e5), [1] (2^24 x 4 dists x 4 ranks), [2] (2^28 float64),
+[3] (2^32 float32 on one GPU: the scaling base) and [4] (LMS); "cpu_baseline" — the oracle on the
+host cores (np.partition, C++ nth_element / sort, the literal double-precision cutting plane).
+
+N > 1 (torchrun, one process per GPU): configs[3] — the median of ONE global array of 2^32 float32
+(uniform and normal, the shard-invariant generator: identical data for every N) sharded in
+contiguous blocks over the N GPUs (strong scaling), one sharded selection per array per step: per
+pass one NCCL all-gather of the 96-byte tuple, an all-gather-v of the bracket at the end.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 Prints ONE JSON line (rank 0).  Timing: CUDA events on the launching stream bracketed by a barrier
-and torch.cuda.synchronize(), max over ranks; inputs (4 GiB each) are larger than L2.
+and torch.cuda.synchronize(), max over ranks; inputs are larger than L2 (4 GiB per array; the
+configs[0]/[1] side blocks flush L2 between calls).
 """
 from __future__ import annotations
 
@@ -41,11 +51,13 @@ def parse():
     ap.add_argument("--log2n", type=int, default=30)
     ap.add_argument("--dists", default="uniform,normal,cauchy,dup256")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=24.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--z-cap", type=int, default=0)
     ap.add_argument("--no-lms", action="store_true", help="skip the configs[4] LMS side measurement")
+    ap.add_argument("--no-side", action="store_true", help="skip the kelley / configs side blocks")
+    ap.add_argument("--global-log2n", type=int, default=32, help="N>1: log2 of the global array (configs[3])")
     return ap.parse_args()
 
 
@@ -176,6 +188,204 @@ def lms_side(cp, torch, datagen, dev, reps=5):
                                                   "sample-cut kernels"}}
 
 
+# ------------------------------------------------------------------------------ side blocks (N=1)
+def _ev(torch):
+    return torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+
+def trace_classes(rows, n, es, peak):
+    """per-pass roofline classes of a traced selection: algorithmic bytes = es x (elements read +
+    elements written) per launch, over that launch's CUDA-event time"""
+    cls = {}
+    for r in rows:
+        if r["kind"] == 2:          # the init's cut rows (evaluated inside the init pass)
+            continue
+        key = ("full_pass" if r["scanned"] == n else "bracket_pass") + ("_compacting" if r["compacted"] else "_hot")
+        c = cls.setdefault(key, {"launches": 0, "bytes": 0, "ms": 0.0})
+        c["launches"] += 1
+        c["bytes"] += es * (r["scanned"] + r["written"])
+        c["ms"] += r["kernel_ms"]
+    for c in cls.values():
+        c["GBps"] = c["bytes"] / (c["ms"] / 1e3) / 1e9 if c["ms"] > 0 else None
+        c["frac"] = c["GBps"] / peak if c["GBps"] else None
+    return cls
+
+
+def kelley_side(cp, torch, datagen, dev, dists, log2n, peak, reps=3):
+    """The paper's method as published (Algorithm 1 from the bracket [x_(1), x_(n)], one cut per
+    pass, the interior-mean iterate = step 1.1 with the tightest cuts (App. A), F_k at every iterate,
+    P:L155-198): init_cut=0, pass_cuts=0, objective=1.  Per distribution: ms per selection (CUDA
+    events over `reps` calls), passes (the paper: 7 iterations at 2^25), the F trace, and
+    the per-pass roofline of the traced call."""
+    n = 1 << log2n
+    k = (n + 1) // 2
+    out = {"workload": f"median of n=2^{log2n} float32, Kelley passes from [x_(1), x_(n)] "
+                       f"(init_cut=0, pass_cuts=0, objective=1)", "per_dist": {}}
+    cfg = dict(init_cut=0, pass_cuts=0, objective=1)
+    tot_ms, tot_bytes, all_rows = 0.0, 0, []
+    for d in dists:
+        x = datagen.make(d, n, "f32", device=dev)
+        cp.set_config(dev.index, record_timing=0, **cfg)
+        for _ in range(2):
+            cp.select_kth(x, k)
+        e0, e1 = _ev(torch)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            v, info = cp.select_kth(x, k, return_info=True)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        cp.set_config(dev.index, record_timing=1, **cfg)
+        v2, info2 = cp.select_kth(x, k, return_info=True)
+        rows = cp.get_trace(dev.index)
+        all_rows += rows
+        tot_ms += ms
+        tot_bytes += info["bytes_moved"]
+        out["per_dist"][d] = {
+            "ms": ms, "elements_per_s": n / (ms / 1e3), "passes": info["passes"], "cp_iters": info["cp_iters"],
+            "exit": info["exit"], "same_value_traced": v == v2,
+            "F_trace": [r["F"] for r in rows], "interior_trace": [r["interior"] for r in rows],
+            "whole_call_frac": info["bytes_moved"] / (ms / 1e3) / 1e9 / peak,
+            "kernel_ms": {"init": info2["kernel_ms_init"], "passes": info2["kernel_ms_passes"],
+                          "select": info2["kernel_ms_select"]},
+            "classes": trace_classes(rows, n, 4, peak)}
+        del x
+    cp.set_config(dev.index, record_timing=0, init_cut=1, pass_cuts=1, objective=0)
+    torch.cuda.empty_cache()
+    out["elements_per_s"] = len(dists) * n / (tot_ms / 1e3)
+    out["ms_per_selection"] = tot_ms / len(dists)
+    out["whole_call_frac"] = tot_bytes / (tot_ms / 1e3) / 1e9 / peak
+    out["classes"] = trace_classes(all_rows, n, 4, peak)
+    out["paper_reference"] = "P:L198: 7 iterations at n=2^25 leave < 2^19 elements (then copy_if + sort)"
+    return out
+
+
+def _flush_l2(torch, buf):
+    buf.add_(1.0)  # 256 MiB > 126 MB L2
+
+
+def configs_side(cp, torch, datagen, dev, peak, reps=5):
+    """BASELINE configs[0..3] at their stated sizes on one GPU (the metric config is the headline;
+    configs[4] is the "lms" block).  Each call is timed alone with CUDA events after an L2 flush."""
+    import numpy as np
+    out = {}
+    flush = torch.empty(1 << 26, device=dev, dtype=torch.float32)
+
+    def timed(x, k, reps_=reps):
+        cp.select_kth(x, k)
+        ts = []
+        for _ in range(reps_):
+            _flush_l2(torch, flush)
+            e0, e1 = _ev(torch)
+            e0.record()
+            v, info = cp.select_kth(x, k, return_info=True)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return v, info, statistics.median(ts)
+
+    # configs[0]: median of 1e5 float32 uniform (the one-launch cluster select)
+    x = datagen.make("uniform", 100_000, "f32", device=dev)
+    v, info, ms = timed(x, 50_000, 50)
+    out["configs0"] = {"workload": "median of n=1e5 float32 uniform", "us_per_call": ms * 1e3,
+                       "elements_per_s": 1e5 / (ms / 1e3), "launches": info["launches"], "exit": info["exit"],
+                       "bound": "latency (one 8-CTA cluster launch, L2-resident)"}
+    # configs[1]: 2^24 float32 x 4 dists x k in {1, n/10, median, n-1}
+    n = 1 << 24
+    cells, tot_ms = {}, 0.0
+    for d in ("uniform", "normal", "cauchy", "dup256"):
+        x = datagen.make(d, n, "f32", device=dev)
+        for kk, name in ((1, "1"), (n // 10, "n/10"), ((n + 1) // 2, "median"), (n - 1, "n-1")):
+            v, info, ms = timed(x, kk)
+            cells[f"{d}/{name}"] = {"ms": ms, "passes": info["passes"], "exit": info["exit"]}
+            tot_ms += ms
+    out["configs1"] = {"workload": "k in {1, n/10, median, n-1} of n=2^24 float32 x {uniform, normal, cauchy, dup256}",
+                       "elements_per_s": 16 * n / (tot_ms / 1e3), "ms_per_selection": tot_ms / 16,
+                       "roofline_frac_one_read": (n * 4) / (tot_ms / 16 / 1e3) / 1e9 / peak,
+                       "note": "64 MiB input: L2 flushed before each call; latency-dominated (~4 launches)",
+                       "cells": cells}
+    del x
+    # configs[2]: 2^28 float64, k in {median, 1, n/10, n-1}
+    n = 1 << 28
+    per, tot_ms, tot_b = {}, 0.0, 0
+    for d in ("uniform", "normal"):
+        x = datagen.make(d, n, "f64", device=dev)
+        for kk, name in (((n + 1) // 2, "median"), (1, "1"), (n // 10, "n/10"), (n - 1, "n-1")):
+            v, info, ms = timed(x, kk)
+            per[f"{d}/{name}"] = {"ms": ms, "passes": info["passes"], "exit": info["exit"]}
+            tot_ms += ms
+            tot_b += info["bytes_moved"]
+        del x
+    out["configs2"] = {"workload": "k in {median, 1, n/10, n-1} of n=2^28 float64 x {uniform, normal}",
+                       "elements_per_s": 8 * n / (tot_ms / 1e3), "ms_per_selection": tot_ms / 8,
+                       "whole_call_frac": tot_b / (tot_ms / 1e3) / 1e9 / peak, "cells": per}
+    torch.cuda.empty_cache()
+    # configs[3] at G = 1: the median of 2^32 float32 on one B200 (the scaling base of the sharded runs)
+    n = 1 << 32
+    per, tot_ms, tot_b = {}, 0.0, 0
+    for d in datagen.GLOBAL_DISTS:
+        x = datagen.make_global(d, n, 0, n, "f32", device=dev)
+        v, info, ms = timed(x, (n + 1) // 2, 3)
+        per[d] = {"ms": ms, "passes": info["passes"], "exit": info["exit"], "value": v}
+        tot_ms += ms
+        tot_b += info["bytes_moved"]
+        del x
+        torch.cuda.empty_cache()
+    out["configs3_g1"] = {"workload": "median of n=2^32 float32 (uniform, normal; shard-invariant generator) on ONE B200",
+                          "elements_per_s": 2 * n / (tot_ms / 1e3), "ms_per_selection": tot_ms / 2,
+                          "whole_call_frac": tot_b / (tot_ms / 1e3) / 1e9 / peak, "cells": per}
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_side(xs_host, dists, seconds):
+    """The oracle as it stands on the host cores (rank 0, N = 1), on bounded samples of the workload:
+    np.partition (oracle.order_statistic), C++ std::nth_element and std::sort (oracle.order_statistic_c,
+    single thread; the paper's CPU quickselect row) on 2^24-element prefixes, and the
+    literal double-precision cutting plane (oracle.cutting_plane, Algorithm 1) on 2^22-element prefixes."""
+    import platform
+
+    import oracle
+    model = platform.processor() or "?"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    rows = {}
+
+    def run(name, fn, samples, budget):
+        done, t0 = 0, time.perf_counter()
+        while True:
+            for smp in samples:
+                fn(smp)
+                done += smp.size
+            if time.perf_counter() - t0 > budget:
+                break
+        dt = time.perf_counter() - t0
+        rows[name] = {"value": done / dt, "unit": UNIT, "cores": 1, "elements": done, "seconds": dt}
+
+    s24 = [x[:1 << 24] for x in xs_host]
+    k24 = oracle.median_rank(1 << 24)
+    run("np.partition", lambda z: oracle.order_statistic(z, k24), s24, seconds / 4)
+    run("nth_element", lambda z: oracle.order_statistic_c(z, k24, "nth_element"), s24, seconds / 4)
+    run("sort", lambda z: oracle.order_statistic_c(z, k24, "sort"), s24[:1], seconds / 4)
+    s22 = [x[:1 << 22] for x in xs_host]
+    k22 = oracle.median_rank(1 << 22)
+    run("cutting_plane", lambda z: oracle.cutting_plane(z, k22, z_cap=1 << 16), s22[:2], seconds / 4)
+    best = rows["nth_element"]
+    return {"value": best["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle.order_statistic_c (C++ std::nth_element, 1 thread) medians of the first 2^24 "
+                      f"elements of {dists}; other rows: np.partition, std::sort (2^24), the literal "
+                      f"long-double cutting plane (2^22)",
+            "cpu_model": model, "nproc": os.cpu_count(), "rows": rows}
+
+
 # ------------------------------------------------------------------------------ our arm
 def main():
     a = parse()
@@ -197,11 +407,21 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     cp.load()
-    dists = a.dists.split(",")
-    n = 1 << a.log2n
-    xs = [datagen.make(d, n, "f32", seed=datagen.SEED + 7919 * rank, device=dev) for d in dists]
+    if world == 1:
+        # the metric configuration: 2^30 float32 per array, the four distributions of configs[1]
+        dists = a.dists.split(",")
+        n = 1 << a.log2n
+        xs = [datagen.make(d, n, "f32", device=dev) for d in dists]
+        n_global = n
+    else:
+        # configs[3]: ONE global array of 2^32 float32 per distribution, rank r holding the contiguous
+        # block [r*N/G, (r+1)*N/G) drawn by the shard-invariant generator (same data for every G)
+        dists = list(datagen.GLOBAL_DISTS)
+        n_global = 1 << a.global_log2n
+        lo, hi = n_global * rank // world, n_global * (rank + 1) // world
+        xs = [datagen.make_global(d, n_global, lo, hi, "f32", device=dev) for d in dists]
+        n = hi - lo
     torch.cuda.synchronize()
-    n_global = n * world
     k = (n_global + 1) // 2
     cp.set_config(local, z_cap=a.z_cap)
     if world > 1:
@@ -303,6 +523,11 @@ def main():
     step_kernel_ms = sum(init_ms) / a.steps + sum(i["kernel_ms_passes"] + i["kernel_ms_select"] + i["kernel_ms_sample"]
                                                   for i in tinfos)
     launches = sum(i["launches"] for i in infos)
+    # whole-call fraction: all algorithmic bytes of the timed selections (every pass's
+    # reads + writes, the exact stage's reads of the copy) over the step time
+    bytes_step = sum(i["bytes_moved"] for i in infos) / a.steps
+    whole_call = {"bytes_per_step": bytes_step, "GBps": bytes_step / (ms / 1e3) / 1e9,
+                  "frac": bytes_step / (ms / 1e3) / 1e9 / peak}
     cp.set_config(local, z_cap=a.z_cap, record_timing=0)
 
     # end to end through the C ABI with HOST buffers (H2D inside the timed region)
@@ -344,32 +569,38 @@ def main():
         except Exception as ex:  # the headline line must not depend on the side measurement
             lms = {"error": f"{type(ex).__name__}: {ex}"}
 
-    # CPU baseline: the oracle as it stands, on a bounded host sample (rank 0, N=1 only)
+    # side blocks (rank 0, N=1): the paper's method as published, BASELINE configs[0..3]
+    kelley = side = None
+    if rank == 0 and world == 1 and not a.no_side:
+        try:
+            kelley = kelley_side(cp, torch, datagen, dev, dists, a.log2n, peak)
+        except Exception as ex:
+            kelley = {"error": f"{type(ex).__name__}: {ex}"}
+        try:
+            side = configs_side(cp, torch, datagen, dev, peak)
+        except Exception as ex:
+            side = {"error": f"{type(ex).__name__}: {ex}"}
+
+    # CPU baseline: the oracle as it stands, on bounded host samples (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
-        import oracle
-        m = 1 << 24
-        samples = [x[:m].cpu().numpy() for x in xs]
-        km = oracle.median_rank(m)
-        done, t0 = 0, time.perf_counter()
-        while time.perf_counter() - t0 < a.cpu_seconds:
-            for smp in samples:
-                oracle.order_statistic(smp, km)
-                done += m
-        dt = time.perf_counter() - t0
-        cpu = {"value": done / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"oracle.order_statistic (np.partition, single thread) median of the first 2^24 "
-                         f"elements of each of {dists}, repeated for {a.cpu_seconds:.0f} s"}
+        cpu = cpu_side([x[:1 << 24].cpu().numpy() for x in xs], dists, a.cpu_seconds)
 
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": f"median of n=2^{a.log2n} float32 per GPU x {dists} (4 selections per step)",
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if world == 1 else "strong",
+            "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded; torch.Generator at N=1, the shard-invariant counter generator at N>1)",
+            "config": {"workload": (f"median of n=2^{a.log2n} float32 x {dists} (4 selections per step; "
+                                    f"path: sample-cut init pass + exact radix finish, Kelley passes if the "
+                                    f"cuts miss)") if world == 1 else
+                                   (f"configs[3]: median of ONE n=2^{a.global_log2n} float32 array per "
+                                    f"distribution {dists}, contiguous shards of 2^{a.global_log2n}/{world} "
+                                    f"per GPU ({len(dists)} sharded selections per step)"),
                        "n_per_gpu": n, "n_global": n_global, "k": "lower median (n+1)//2",
                        "parallelism": "single GPU" if world == 1 else f"sharded x{world} (NCCL tuple all-gather)",
-                       "l2": "inputs larger than L2 (4 GiB per array vs 126 MB L2); no flush needed",
+                       "l2": "inputs larger than L2 (>= 2 GiB per array per GPU vs 126 MB L2); no flush needed",
                        "z_cap": a.z_cap or "auto"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -379,6 +610,7 @@ def main():
                          "classes_note": "init_pass from the timed region; pass classes from one traced step after it",
                          "classes": {"init_pass": init_cls, "hot_full_pass": hot_x, "compacting_full_pass": comp_x,
                                      "bracket_passes": z_pass, "all_cp_passes": all_pass}},
+            "whole_call_roofline": whole_call,
             "cp_iters": {"mean": statistics.fmean(iters), "min": min(iters), "max": max(iters)},
             "kernel_ms_per_step": {"init": sum(init_ms) / a.steps, "passes": sum(i["kernel_ms_passes"] for i in tinfos),
                                    "select": sum(sel_ms), "sample": sum(i["kernel_ms_sample"] for i in tinfos),
@@ -389,6 +621,8 @@ def main():
             "clocks": clk,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "kelley": kelley,
+            "configs": side,
             "lms": lms,
         }
         print(json.dumps(out), flush=True)
