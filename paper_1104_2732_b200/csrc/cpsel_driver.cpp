@@ -387,7 +387,7 @@ struct GpuBackend : Backend {
     sample_slot = -1;
     if (cut && !presampled) {
       CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream,
-                              /*small=*/n <= (1ull << 26)));
+                              /*small=*/n <= (1ull << 26), nullptr, 0, /*allow_open=*/!ctx->cfg.objective));
       CK(toc());
       sample_slot = slot;
       CK(tic());
@@ -399,7 +399,7 @@ struct GpuBackend : Backend {
     // the init's copy holds ~2% of n: radix-select it right behind the init when it will fit the
     // select cap (direct), else chain the R26 cut pass first
     const bool chain_ok = fuse && use_mail && !presampled && chain_select_cap > 0 && !ctx->cfg.objective;
-    const bool direct = chain_ok && n / 25 <= chain_select_cap && n / 100 > (1ull << 20);
+    const bool direct = chain_ok && n / 25 <= chain_select_cap && n > (1ull << 22);
     const bool chain = chain_ok && (direct || (ctx->cfg.pass_cuts && n / 100 > chain_select_cap));
     if (fuse) {
       SegArgs sa{};
@@ -483,7 +483,8 @@ struct GpuBackend : Backend {
     if ((e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
                                  &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
                                  static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain,
-                                 /*first_round=*/init_hist0() ? 1 : 0, init_hist0() ? ctx->d_hist + 2048 : nullptr)) !=
+                                 /*first_round=*/init_hist0() ? 1 : 0, init_hist0() ? ctx->d_hist + 2048 : nullptr,
+                                 /*m_hint: the expected copy*/ n / (n <= (1ull << 26) ? 25 : 100))) !=
         cudaSuccess)
       return e;
     if ((e = toc()) != cudaSuccess) return e;
@@ -528,7 +529,8 @@ struct GpuBackend : Backend {
     if ((e = tic()) != cudaSuccess) return e;
     if ((e = launch_radix_select(dt, ctx->d_sb[1], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
                                  &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
-                                 static_cast<const SegEntry*>(ctx->d_st[1]), 0, ctx->d_ticket, ctx->d_chain)) != cudaSuccess)
+                                 static_cast<const SegEntry*>(ctx->d_st[1]), 0, ctx->d_ticket, ctx->d_chain, 0, nullptr,
+                                 /*m_hint: ~4% of the init's ~1% copy*/ n / 2500)) != cudaSuccess)
       return e;
     if ((e = toc()) != cudaSuccess) return e;
     spec.radix_slot = slot;
@@ -974,7 +976,7 @@ struct ShardedBackend : GpuBackend {
     CK(launch_pool_gather(dt, on_x ? x : cur, on_x ? n : n_cur, seg ? cur_tab : nullptr, cur_side, W, s[comm().rank],
                           mine, ctx->stream));
     CM(comm().allgatherv(mine, ctx->d_pool, bytes.data(), ctx->stream));
-    CK(launch_pool_pick(dt, ctx->d_pool, total, M, r, ctx->d_t0, ctx->stream, small));
+    CK(launch_pool_pick(dt, ctx->d_pool, total, M, r, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
     return CPSEL_OK;
   }
   // the init pass: with cuts (R23/R28) every rank runs the fused init at the pooled cuts and the
@@ -1395,8 +1397,12 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     if (!sums) t = (rec.t_est > yL && rec.t_est < yR) ? rec.t_est : (double)NAN;
     free_step = !sums;
     if (!std::isfinite(t)) t = 0.5 * yL + 0.5 * yR;
-    // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
-    if (be.init_compacted() && yL == rec.t_lo && yR == rec.t_hi) {
+    // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it (a cut
+    // outside the bracket with no element between it and the bracket end — the open cut of an
+    // extreme rank — copies the same set)
+    const bool lo_ok = yL == rec.t_lo || (rec.t_lo < yL && rec.c_le_lo == c_le_L);
+    const bool hi_ok = yR == rec.t_hi || (rec.t_hi > yR && rec.c_lt_hi == c_lt_R);
+    if (be.init_compacted() && lo_ok && hi_ok) {
       if (m != be.init_written()) {
         if (info) *info = inf;
         return CPSEL_EINTERNAL;

@@ -1513,6 +1513,7 @@ struct RadixArgs {
   uint64_t m;
   const SegEntry* tab;  // nullptr: contiguous
   int side;
+  int Wtot;             // segmented: runs in tab
   RadixState* st;
   unsigned* hist;       // 2048 global digit counters, zero between rounds
   unsigned* ticket;
@@ -1587,9 +1588,12 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   f.shift = a.shift;
   f.dmask = (1u << a.bits) - 1u;
   if (SEG) {
-    const uint64_t W = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-    const SegEntry e = a.tab[W];
-    seg_run_pipe<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
+    // a warp per run; a grid smaller than the segmented one (a small copy) loops over the runs
+    for (uint64_t W = (uint64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); W < (uint64_t)a.Wtot;
+         W += (uint64_t)gridDim.x * kWarps) {
+      const SegEntry e = a.tab[W];
+      seg_run_pipe<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
+    }
   } else {
     HistFn<T> hf;
     hf.sh = sh; hf.prefix = s_prefix; hf.mask = s_mask; hf.shift = a.shift; hf.dmask = f.dmask;
@@ -1753,8 +1757,10 @@ __device__ void chain_decide0(const DevInit& r, uint64_t k, uint64_t cap, ChainS
                               unsigned long long seq, int direct) {
   const double lo_out = (double)nextafter_t<T>((T)r.vmin, false), hi_out = (double)nextafter_t<T>((T)r.vmax, true);
   const uint64_t written = r.pad;
+  // (a cut at or beyond an extreme's outer neighbour — the open cut of an extreme rank — has nothing
+  // between it and that neighbour: the copy is still exactly the bracket interior)
   const bool base = (r.has_cut & 1) && r.nonfinite == 0 && isfinite(r.vmin) && isfinite(r.vmax) && isfinite(lo_out) &&
-                    isfinite(hi_out) && isfinite(r.t_est) && r.t_lo > lo_out && r.t_hi < hi_out && r.t_lo < r.t_hi &&
+                    isfinite(hi_out) && isfinite(r.t_est) && r.t_lo < r.t_hi &&
                     r.c_le_lo < k && r.c_lt_hi >= k && written == r.c_lt_hi - r.c_le_lo;
   if (direct) {  // the radix select of the init's copy itself is next: decision 1 gates it
     cs->ok[0] = 0;
@@ -2912,6 +2918,7 @@ size_t partial_bytes_needed(const LaunchShape& s) {
   return (size_t)g * per;
 }
 
+constexpr int kRadixPerCta = 16384;  // elements per CTA of a radix round
 static int clamp_grid(int grid, uint64_t n, int per_cta) {
   const uint64_t need = (n + per_cta - 1) / per_cta;
   if (need < (uint64_t)grid) grid = (int)(need > 0 ? need : 1);
@@ -3012,11 +3019,12 @@ struct ClusterSel {
   unsigned csum[3][32];
   unsigned long long prefix[3], mask[3], rank[3];
   unsigned long long wsum[32];
+  int open_lo, open_hi;    // the cut's sample rank fell off the sample: no cut on that side
 };
 template <typename T, int KPT>
 __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     sample_cluster_kernel(const T* __restrict__ x, uint64_t m, const SegEntry* __restrict__ tab, int side, int Wtot,
-                          uint64_t r, T* t0, const ChainState* chain, int which, uint64_t m_rank) {
+                          uint64_t r, T* t0, const ChainState* chain, int which, uint64_t m_rank, int allow_open) {
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   using SK = SampleKey<T>;
@@ -3117,6 +3125,12 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
       sh.prefix[t] = 0;
       sh.mask[t] = 0;
     }
+    // an extreme target rank (k near 1 or n): the sample's own extreme would be a cut the target
+    // may well lie beyond — take the outermost float instead (the cut then keeps everything on
+    // that side; exactness does not depend on where the cuts are)
+    // (not when the init pass also sums (x - t_lo)^+ etc. for F, R25: those sums would overflow)
+    sh.open_lo = allow_open && qq[0] < 0;
+    sh.open_hi = allow_open && qq[1] >= md - 1;
   }
   unsigned* glob0 = cl.map_shared_rank(&sh.glob[0][0], 0);
   ClusterSel* sh0 = cl.map_shared_rank(&sh, 0);
@@ -3217,6 +3231,8 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     K kk = (K)sh.prefix[i];
     if (i == 1) kk |= (K)~(K)sh.mask[1];
     kk = kk < SK::KLO ? SK::KLO : (kk > SK::KHI ? SK::KHI : kk);
+    if (i == 0 && sh.open_lo) kk = SK::KLO;
+    if (i == 1 && sh.open_hi) kk = SK::KHI;
     t0[i] = SK::val(kk);
   }
 }
@@ -3391,7 +3407,8 @@ cudaError_t launch_exact_cluster(int dtype, const void* x, uint64_t m, uint64_t 
 
 template <typename T, int KPT>
 cudaError_t sample_cluster_t(const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot, uint64_t r, void* t0,
-                             cudaStream_t st, const ChainState* chain, int which, uint64_t m_rank = 0) {
+                             cudaStream_t st, const ChainState* chain, int which, uint64_t m_rank = 0,
+                             int allow_open = 1) {
   const size_t smem = sizeof(ClusterSel) + (tab ? (size_t)Wtot * 8 : 0);
   static bool attr = false;
   if (!attr) {
@@ -3401,7 +3418,8 @@ cudaError_t sample_cluster_t(const void* x, uint64_t m, const SegEntry* tab, int
     attr = true;
   }
   sample_cluster_kernel<T, KPT><<<kSampleCluster, 1024, smem, st>>>(static_cast<const T*>(x), m, tab, side, Wtot, r,
-                                                                   static_cast<T*>(t0), chain, which, m_rank);
+                                                                   static_cast<T*>(t0), chain, which, m_rank,
+                                                                   allow_open);
   return cudaGetLastError();
 }
 
@@ -3417,17 +3435,18 @@ cudaError_t sample_select_t(const void* x, uint64_t m, const SegEntry* tab, int 
 
 cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
                                  uint64_t r, void* t0, void* keys, cudaStream_t st, bool small,
-                                 const ChainState* chain, int which) {
+                                 const ChainState* chain, int which, bool allow_open) {
   if (tab && Wtot > kGatherMaxWarps) return cudaErrorInvalidValue;
   (void)keys;
   // one cluster launch: 8 CTAs x 1024 threads x KPT samples (131072 / 8192 for f32, 65536 / 8192 f64;
   // f32 at 131072: the init's copy ~1% of n — measured +1.1% whole-step vs 32768; f64 at 65536:
   // 2^28 median 0.555 -> 0.545 ms vs 16384)
+  const int op = allow_open ? 1 : 0;
   if (dtype == kF32)
-    return small ? sample_cluster_t<float, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which)
-                 : sample_cluster_t<float, 16>(x, m, tab, side, Wtot, r, t0, st, chain, which);
-  return small ? sample_cluster_t<double, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which)
-               : sample_cluster_t<double, 8>(x, m, tab, side, Wtot, r, t0, st, chain, which);
+    return small ? sample_cluster_t<float, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which, 0, op)
+                 : sample_cluster_t<float, 16>(x, m, tab, side, Wtot, r, t0, st, chain, which, 0, op);
+  return small ? sample_cluster_t<double, 1>(x, m, tab, side, Wtot, r, t0, st, chain, which, 0, op)
+               : sample_cluster_t<double, 8>(x, m, tab, side, Wtot, r, t0, st, chain, which, 0, op);
 }
 
 
@@ -3531,13 +3550,14 @@ uint64_t pool_sample_size(int dtype, bool small) {
 }
 
 cudaError_t launch_pool_pick(int dtype, const void* pooled, uint64_t ms, uint64_t m_rank, uint64_t r, void* t0,
-                             cudaStream_t st, bool small) {
+                             cudaStream_t st, bool small, bool allow_open) {
   if (ms > pool_sample_size(dtype, small)) return cudaErrorInvalidValue;
+  const int op = allow_open ? 1 : 0;
   if (dtype == kF32)
-    return small ? sample_cluster_t<float, 1>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank)
-                 : sample_cluster_t<float, 16>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank);
-  return small ? sample_cluster_t<double, 1>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank)
-               : sample_cluster_t<double, 8>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank);
+    return small ? sample_cluster_t<float, 1>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank, op)
+                 : sample_cluster_t<float, 16>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank, op);
+  return small ? sample_cluster_t<double, 1>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank, op)
+               : sample_cluster_t<double, 8>(pooled, ms, nullptr, 0, 0, r, t0, st, nullptr, 0, m_rank, op);
 }
 
 cudaError_t launch_seg_pack(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, void* out,
@@ -3575,7 +3595,8 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned* hist, const LaunchShape& s, cudaStream_t st, double* vout,
                                 unsigned long long* done, unsigned long long seq, const SegEntry* tab, int side,
-                                unsigned* ticket, const ChainState* chain, int first_round, unsigned* hist0) {
+                                unsigned* ticket, const ChainState* chain, int first_round, unsigned* hist0,
+                                uint64_t m_hint) {
   // digit plan, MSB first: f32 11+11+10, f64 11+11+11+11+10+10 (first_round > 0: the earlier rounds
   // were taken by the init pass, RadixState holds their prefix and rank)
   static const int plan32[] = {21, 11, 10, 11, 0, 10};
@@ -3585,12 +3606,16 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   RadixArgs a{};
   a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
   a.r = r; a.vout = vout; a.done = done; a.seq = seq; a.chain = chain;
+  a.Wtot = s.grid_seg[dtype] * kWarps;
+  // dense input: one CTA per kRadixPerCta elements (each CTA merges up to 2048 bins into the global
+  // histogram and the last one scans them, so a small copy is not spread over the whole grid)
+  (void)m_hint;
   for (int i = first_round; i < rounds; ++i) {
     a.shift = plan[2 * i]; a.bits = plan[2 * i + 1];
     a.first = i == 0; a.last = i == rounds - 1;
     a.hist0 = (i == 1 && first_round == 1) ? hist0 : nullptr;
-    const int grid = tab ? s.grid_seg[dtype]
-                         : clamp_grid(s.grid_hist[dtype], m, kBlock * 2 * (dtype == kF32 ? 4 : 2));
+    const int grid = tab ? s.grid_seg[dtype]  // a warp per run: the runs are short, latency-bound
+                         : clamp_grid(s.grid_hist[dtype], m, kRadixPerCta);
     if (dtype == kF32) {
       if (tab) pdl_launch(radix_round_kernel<float, true>, dim3(grid), dim3(kBlock), 0, st, a);
       else pdl_launch(radix_round_kernel<float, false>, dim3(grid), dim3(kBlock), 0, st, a);

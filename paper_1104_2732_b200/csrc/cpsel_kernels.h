@@ -179,9 +179,11 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 // the sample keys and a one-CTA radix select of the three sample order statistics.
 constexpr size_t kSampleKeyBytes = 32768 * 4 > 16384 * 8 ? 32768 * 4 : 16384 * 8;
 // small: 8192 (f32) / 4096 (f64) samples instead (the cut passes over an already small bracket).
+// allow_open: a cut whose sample rank falls off the sample (extreme k) becomes -/+FLT_MAX (DBL_MAX),
+// so the target cannot lie beyond it; off when the init pass sums (x - t_lo)^+ etc. for F (R25).
 cudaError_t launch_sample_select(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
                                  uint64_t r, void* t0, void* keys, cudaStream_t st, bool small = false,
-                                 const ChainState* chain = nullptr, int which = 0);
+                                 const ChainState* chain = nullptr, int which = 0, bool allow_open = true);
 
 // smax (<= 1024): samples drawn; keys_out != nullptr: write the sorted sample keys (order-preserving
 // 64-bit keys, padding ~0) there instead of picking cuts (pooled across ranks, R28).
@@ -205,7 +207,7 @@ uint64_t pool_sample_size(int dtype, bool small);
 cudaError_t launch_pool_gather(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
                                uint64_t ms, void* out, cudaStream_t st);
 cudaError_t launch_pool_pick(int dtype, const void* pooled, uint64_t ms, uint64_t m_rank, uint64_t r, void* t0,
-                             cudaStream_t st, bool small);
+                             cudaStream_t st, bool small, bool allow_open = true);
 cudaError_t launch_seg_pack(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, void* out,
                             cudaStream_t st);
 
@@ -235,7 +237,7 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
                                 double* vout, unsigned long long* done, unsigned long long seq,
                                 const SegEntry* tab, int side, unsigned int* ticket,
                                 const ChainState* chain = nullptr, int first_round = 0,
-                                unsigned int* hist0 = nullptr);
+                                unsigned int* hist0 = nullptr, uint64_t m_hint = 0);
 
 // Step a8: per-column k-th smallest of S (n x C column-major, float32), one CTA per column.
 struct BatchArgs {

@@ -468,3 +468,18 @@ def test_direct_chain_extreme_ranks(cp, dist):
     for k in (1, 2, 1000, n - 1, n):
         v, info = cp.select_kth(xd, k, return_info=True)
         assert canon(v) == float(xs[k - 1]), (dist, k, info)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_extreme_ranks_open_cuts(cp, dtype):
+    """Extreme ranks (k = 1, 2, n-1, n): the sample rank of the outer cut falls off the sample, the
+    cut opens to -/+ the largest float and the init pass's copy holds the target — one pass, exact."""
+    import torch
+    n = (1 << 23) + 5
+    x = datagen.make("normal", n, dtype)
+    xd = torch.from_numpy(x).cuda()
+    srt = np.sort(x)
+    for k in (1, 2, 3, n - 2, n - 1, n):
+        v, info = cp.select_kth(xd, k, return_info=True)
+        assert v == canon(float(srt[k - 1])), (k, v)
+        assert info["passes"] == 1, (k, info)
