@@ -78,6 +78,14 @@ typedef struct {
                                 statistics, counts at two sample cuts per candidate and copies
                                 what lies between them (§8f-2); columns the copy cannot finish
                                 are stored and selected from S.  Used for n >= 16384.  Default 1 */
+  int32_t device_loop;       /* 1: once only Kelley passes remain (pass_cuts=0 or objective=1, or the
+                                sample cuts missed), the rest of the selection runs as ONE CUDA graph
+                                launch — a WHILE node over {Kelley step kernel, IF pass kernels} and
+                                the exact select behind it — with no host round trip per pass (§8f-3).
+                                0: the host drives every pass through the mapped mailbox.  Default 0:
+                                measured on B200, a WHILE iteration costs ~9.7 us of device-side
+                                relaunch, more than the mailbox round trip (+35 us per selection at
+                                2^20..2^27, +2% at 2^30) */
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */

@@ -95,6 +95,13 @@ struct cpsel_ctx {
   Mailbox* mb = nullptr;      // host view
   Mailbox* mb_dev = nullptr;  // device view of the same memory
   unsigned long long seq = 0;
+  // device-resident Kelley loop (§8f-3): its state (device), the host staging of it (pinned), the
+  // report it writes (mapped) and one instantiated graph per dtype
+  KelleyState* d_ks = nullptr;
+  KelleyState* h_ks = nullptr;
+  KelleyReport* h_rep = nullptr;
+  KelleyReport* d_rep = nullptr;
+  cudaGraphExec_t kgraph[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -247,6 +254,22 @@ struct Backend {
   uint64_t scanned = 0;
   // CUDA-event milliseconds of a step's timing slot (waits for it); 0 if none
   virtual double slot_ms(int) { return 0.0; }
+  // §8f-3: the rest of the Kelley iterations (no cut passes) and the exact finish on the device
+  struct LoopIn {
+    double yL, yR, t, N_L, P_R;
+    uint64_t c_le_L, c_lt_R, m, D_lo, it, k, n, z_cap, select_cap, dense_cap, max_iters;
+    int on_z, exact, bisect, slow, free_step, record;
+    double wP, wN;
+  };
+  struct LoopOut {
+    double value = 0.0, loop_ms = 0.0;
+    uint32_t exit_reason = 0, passes = 0, cp_iters = 0, fallback = 0, launches = 0;
+    int error = 0;
+    uint64_t bytes_moved = 0, z_count = 0;
+    std::vector<cpsel_trace_row> rows;
+  };
+  virtual bool has_device_loop() const { return false; }
+  virtual cpsel_status device_loop(const LoopIn&, LoopOut*) { return CPSEL_EINTERNAL; }
 };
 
 // ------------------------------------------------------------------------ one GPU
@@ -764,6 +787,81 @@ struct GpuBackend : Backend {
     scanned = m;
     return CPSEL_OK;
   }
+  // §8f-3: hand the remaining Kelley passes and the exact finish to the device (one graph launch)
+  bool has_device_loop() const override { return use_mail; }
+  cpsel_status device_loop(const LoopIn& li, LoopOut* lo) override {
+    static_assert(sizeof(KRow) == sizeof(cpsel_trace_row), "trace row layout");
+    if (!ctx->d_ks) {
+      CK(cudaMalloc(&ctx->d_ks, sizeof(KelleyState)));
+      CK(cudaHostAlloc(&ctx->h_ks, sizeof(KelleyState), cudaHostAllocDefault));
+      CK(cudaHostAlloc(&ctx->h_rep, sizeof(KelleyReport), cudaHostAllocMapped));
+      CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_rep), ctx->h_rep, 0));
+    }
+    if (!ctx->kgraph[dt])
+      CK(kelley_graph_build(dt, ctx->shape, ctx->d_ks, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_radix,
+                            ctx->d_hist, &ctx->kgraph[dt]));
+    KelleyState& h = *ctx->h_ks;
+    memset(&h, 0, sizeof h);
+    h.n = li.n; h.k = li.k; h.z_cap = li.z_cap; h.select_cap = li.select_cap; h.dense_cap = li.dense_cap;
+    h.max_iters = li.max_iters;
+    h.seq = ++ctx->seq;
+    h.wP = li.wP; h.wN = li.wN;
+    h.x = x;
+    for (int i = 0; i < 2; ++i) {
+      h.sb[i] = ctx->d_sb[i];
+      h.st[i] = static_cast<SegEntry*>(ctx->d_st[i]);
+      h.zb[i] = ctx->d_zb[i];
+    }
+    h.cap = cap; h.R = R;
+    h.dt = dt; h.record = li.record;
+    h.vout = &ctx->mb_dev->radix_value;
+    h.done_flag = &ctx->mb_dev->seq_radix;
+    h.rep = ctx->d_rep;
+    h.yL = li.yL; h.yR = li.yR; h.t = li.t; h.N_L = li.N_L; h.P_R = li.P_R;
+    h.c_le_L = li.c_le_L; h.c_lt_R = li.c_lt_R; h.m = li.m; h.D_lo = li.D_lo; h.it = li.it;
+    h.on_z = li.on_z; h.exact = li.exact && cur_exact; h.bisect = li.bisect; h.slow = li.slow;
+    h.free_step = li.free_step;
+    h.cur = cur; h.n_cur = n_cur; h.cur_tab = cur_seg ? cur_tab : nullptr;
+    h.cur_seg = cur_seg; h.cur_side = cur_side; h.cur_sbuf = cur_sbuf; h.cur_dbuf = cur_dbuf;
+    h.tgt = tgt; h.last_dense = last_dense;
+    CK(cudaMemcpyAsync(ctx->d_ks, &h, sizeof h, cudaMemcpyHostToDevice, ctx->stream));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timed()) {
+      CK(cudaEventCreate(&e0));
+      CK(cudaEventCreate(&e1));
+      CK(cudaEventRecord(e0, ctx->stream));
+    }
+    const cudaError_t le = cudaGraphLaunch(ctx->kgraph[dt], ctx->stream);
+    if (le != cudaSuccess) {
+      if (e0) cudaEventDestroy(e0);
+      if (e1) cudaEventDestroy(e1);
+      return fail(ctx, CPSEL_ECUDA, "cudaGraphLaunch: %s", cudaGetErrorString(le));
+    }
+    if (e1) cudaEventRecord(e1, ctx->stream);
+    cpsel_status w = wait_mail(&ctx->mb->seq_radix, h.seq);
+    if (w == CPSEL_OK && e1) {
+      float ms = 0.f;
+      if (cudaEventSynchronize(e1) == cudaSuccess && cudaEventElapsedTime(&ms, e0, e1) == cudaSuccess) lo->loop_ms = ms;
+    }
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    if (w != CPSEL_OK) return w;
+    const KelleyReport& r = *ctx->h_rep;
+    lo->value = ctx->mb->radix_value;
+    lo->error = r.error;
+    lo->exit_reason = r.exit_reason;
+    lo->passes = r.passes; lo->cp_iters = r.cp_iters; lo->fallback = r.fallback; lo->launches = r.launches;
+    lo->bytes_moved = r.bytes_moved; lo->z_count = r.z_count;
+    lo->rows.clear();
+    const unsigned nr = std::min<unsigned>(r.n_rows, (unsigned)kKelleyMaxRows);
+    for (unsigned i = 0; li.record && i < nr; ++i) {
+      cpsel_trace_row row;
+      memcpy(&row, &r.rows[i], sizeof row);
+      lo->rows.push_back(row);
+    }
+    launches = 1;
+    return CPSEL_OK;
+  }
   // the radix select reads dense and segmented arrays alike
   bool kept_dense() const override { return true; }
   cpsel_status select(int side, uint64_t r, double* out) override {
@@ -851,6 +949,7 @@ struct ShardedBackend : GpuBackend {
   }
   Comm& comm() const { return ctx->comm; }
   int G() const { return ctx->comm.world; }
+  bool has_device_loop() const override { return false; }  // every pass ends in a collective
   // every kept part is selectable: select() packs a segmented one before the all-gather-v
   bool kept_dense() const override { return true; }
 
@@ -1426,6 +1525,42 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       if (info) *info = inf;
       return CPSEL_EINTERNAL;
     }
+    // §8f-3: once no R26 cut pass can follow (pass_cuts off, objective on, or the cuts stalled), the
+    // remaining Kelley passes and the exact finish run on the device as one graph launch; the step
+    // kernel there is this loop's Kelley step (same iterates, same decisions, same trace rows)
+    if (cfg.device_loop && be.has_device_loop() &&
+        (!cfg.pass_cuts || cfg.objective || !be.has_cut_pass() || cuts_stalled)) {
+      Backend::LoopIn li{};
+      li.yL = yL; li.yR = yR; li.t = t; li.N_L = (double)N_L; li.P_R = (double)P_R;
+      li.c_le_L = c_le_L; li.c_lt_R = c_lt_R; li.m = m; li.D_lo = D_lo; li.it = it - 1;
+      li.k = k; li.n = n; li.z_cap = z_cap; li.select_cap = select_cap; li.dense_cap = dense_cap;
+      li.max_iters = cfg.max_iters;
+      li.on_z = on_z; li.exact = exact; li.bisect = bisect; li.slow = slow; li.free_step = free_step;
+      li.record = (trace && cfg.record_trace) ? 1 : 0;
+      li.wP = (double)wP; li.wN = (double)wN;
+      Backend::LoopOut lo;
+      st = be.device_loop(li, &lo);
+      if (st != CPSEL_OK) return st;
+      inf.passes += lo.passes;
+      inf.cp_iters += lo.cp_iters;
+      inf.fallback_steps += lo.fallback;
+      inf.launches += lo.launches;
+      inf.bytes_moved += lo.bytes_moved;
+      if (lo.exit_reason == 5) inf.z_count = lo.z_count;
+      double rows_ms = 0.0;
+      for (const auto& r : lo.rows) rows_ms += r.kernel_ms;
+      if (trace && cfg.record_trace) trace->insert(trace->end(), lo.rows.begin(), lo.rows.end());
+      if (lo.error) {
+        if (info) *info = inf;
+        return CPSEL_EINTERNAL;
+      }
+      done(lo.value, lo.exit_reason);
+      if (cfg.record_timing == 1 && info) {  // the loop's passes (device timestamps) and the rest of it
+        info->kernel_ms_passes += rows_ms;
+        info->kernel_ms_select += std::max(0.0, lo.loop_ms - rows_ms);
+      }
+      return CPSEL_OK;
+    }
     // R26 (multi-point step): a compacted current array that is exactly the bracket
     // interior and too large for the exact selection is cut at two sample quantiles of its own
     // around the local target rank; the copy keeps only ]t_a, t_b[ (~10% of the array) instead of
@@ -1748,6 +1883,7 @@ void cpsel_config_default(cpsel_config* c) {
   c->init_cut = 1;
   c->pass_cuts = 1;
   c->lms_fused = 1;
+  c->device_loop = 0;  // measured slower than the mailbox loop (cpsel.h)
 }
 
 cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
@@ -1817,6 +1953,11 @@ void cpsel_destroy(cpsel_ctx* ctx) {
                     ctx->h_sizes};
     for (void* p : host)
       if (p) cudaFreeHost(p);
+    for (cudaGraphExec_t g : ctx->kgraph)
+      if (g) cudaGraphExecDestroy(g);
+    if (ctx->d_ks) cudaFree(ctx->d_ks);
+    if (ctx->h_ks) cudaFreeHost(ctx->h_ks);
+    if (ctx->h_rep) cudaFreeHost(ctx->h_rep);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->light_ev) cudaEventDestroy(e);
     if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -1072,6 +1072,12 @@ __global__ void __launch_bounds__(kBlock) pass_kernel(PassArgs a) {
   using Fn = PassFn<T, MODE, UNROLL>;
   __shared__ CompactShared cs;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
+  if (a.ks) {  // device loop: this pass's array and bracket from the loop state
+    const KelleyState* ks = a.ks;
+    if (ks->done || ks->compact) return;
+    a.x = ks->cur; a.n = ks->n_cur; a.t = ks->tq; a.y_lo = ks->yL; a.y_hi = ks->yR;
+    a.out = const_cast<DevPass*>(&ks->tuple);
+  }
   Fn f;
   f.t = (T)a.t; f.yL = (T)a.y_lo; f.yR = (T)a.y_hi;
   f.c_lt = f.c_eq = f.c_lo = f.c_hi = 0;
@@ -1509,6 +1515,7 @@ struct RadixSegFn {
 };
 
 struct RadixArgs {
+  const KelleyState* ks;  // device loop: the exact finish's input, rank and mailbox seq from *ks
   const void* z;
   uint64_t m;
   const SegEntry* tab;  // nullptr: contiguous
@@ -1530,6 +1537,11 @@ template <typename T, bool SEG>
 __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   pdl_wait();     // the previous round's digit / the init's copy and chain decision
   pdl_trigger();  // the next round may be scheduled (it waits for this grid to finish)
+  if (a.ks) {
+    a.z = a.ks->sel_base; a.m = a.ks->sel_m; a.tab = a.ks->sel_tab; a.side = a.ks->sel_side;
+    a.r = a.ks->sel_r; a.seq = a.ks->seq;
+    a.vout = a.ks->vout; a.done = a.ks->done_flag;
+  }
   if (a.chain) {
     if (!a.chain->ok[1]) {  // skipped: the init's round-0 counts must still be cleared
       if (a.hist0 && blockIdx.x == 0)
@@ -1659,6 +1671,20 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
 template <typename T, bool INSIDE>
 __global__ void __launch_bounds__(kBlock, 4) seg_pass_kernel(SegArgs a) {
   using F = WarpSeg<T, INSIDE>;
+  if (a.ks) {  // device loop: input, bracket and output from the loop state
+    KelleyState* ks = a.ks;
+    if (ks->done || !ks->compact || (ks->inside != 0) != INSIDE) return;
+    a.x = ks->cur; a.n = ks->n_cur;
+    a.seg_in = ks->cur_seg ? ks->cur_tab : nullptr;
+    a.side_in = ks->cur_side;
+    a.t = ks->tq; a.y_lo = ks->yL; a.y_hi = ks->yR;
+    a.dense_out = ks->dense;
+    a.out = ks->dense ? ks->zb[ks->tgt] : ks->sb[ks->tgt];
+    a.R = ks->R;
+    a.seg_out = ks->st[ks->tgt];
+    a.z_cap = ks->cap;
+    a.out_tuple = &ks->tuple;
+  }
   __shared__ __align__(16) T stage_all[kWarps * 2 * F::GWP];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t W = (uint64_t)blockIdx.x * kWarps + w;
@@ -2879,6 +2905,235 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
   }
 }
 
+
+// ------------------------------------------------------------------------------------------
+// §8f-3 device-resident Kelley loop: the step kernel (one thread) = drive()'s Kelley step.  It
+// consumes the pass that just ran (if any), then schedules the next one through the graph's
+// conditional handles: hw (the WHILE), hh (hot pass), hs0 / hs1 (compacting pass with bracket
+// tests / all inside), hrs / hrd (after the loop: radix rounds over a segmented / dense kept half).
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+template <typename T> __device__ double ks_snap(double t, double yL, double yR);
+template <> __device__ double ks_snap<float>(double t, double yL, double yR) {
+  const float fl = (float)yL, fr = (float)yR;
+  float f = isfinite(t) ? (float)t : (float)(0.5 * yL + 0.5 * yR);
+  if (!(f > fl)) f = nextafterf(fl, INFINITY);
+  if (!(f < fr)) f = nextafterf(fr, -INFINITY);
+  return f;
+}
+template <> __device__ double ks_snap<double>(double t, double yL, double yR) {
+  double f = isfinite(t) ? t : 0.5 * yL + 0.5 * yR;
+  if (!(f > yL)) f = ::nextafter(yL, (double)INFINITY);
+  if (!(f < yR)) f = ::nextafter(yR, -(double)INFINITY);
+  return f;
+}
+template <typename T> __device__ double ks_key_mid(double yL, double yR) {
+  const unsigned long long a = okey((T)yL), b = okey((T)yR);
+  const unsigned long long c = a + (b - a) / 2;
+  return sizeof(T) == 4 ? from_key_f32(c) : from_key_f64(c);
+}
+struct KHandles {
+  cudaGraphConditionalHandle hw, hh, hs0, hs1, hrs, hrd;
+};
+__device__ void ks_set(const KHandles& h, unsigned w, unsigned hot, unsigned s0, unsigned s1, unsigned rs, unsigned rd) {
+  cudaGraphSetConditional(h.hw, w);
+  cudaGraphSetConditional(h.hh, hot);
+  cudaGraphSetConditional(h.hs0, s0);
+  cudaGraphSetConditional(h.hs1, s1);
+  cudaGraphSetConditional(h.hrs, rs);
+  cudaGraphSetConditional(h.hrd, rd);
+}
+// the counters into the mapped report (before the value is published)
+__device__ void ks_report(KelleyState& s) {
+  KelleyReport* r = s.rep;
+  r->error = s.error;
+  r->exit_reason = s.exit_reason;
+  r->passes = s.passes;
+  r->cp_iters = s.cp_iters;
+  r->fallback = s.fallback;
+  r->launches = s.launches;
+  r->n_rows = s.n_rows;
+  r->bytes_moved = s.bytes_moved;
+  r->z_count = s.z_count;
+  __threadfence_system();
+}
+// the loop ends with a value (hit / adjacency) or an error: publish it, run nothing more
+__device__ void ks_finish(KelleyState& s, const KHandles& h, double v, unsigned reason, int error) {
+  s.done = 1;
+  s.error = error;
+  s.value = v;
+  s.exit_reason = reason;
+  ks_set(h, 0, 0, 0, 0, 0, 0);
+  ks_report(s);
+  if (s.vout) *s.vout = v;
+  publish_done(s.done_flag, s.seq);
+}
+__device__ void ks_row(KelleyState& s, const KRow& r) {
+  if (s.record && s.n_rows < (unsigned)kKelleyMaxRows) s.rep->rows[s.n_rows] = r;
+  s.n_rows++;
+}
+template <typename T>
+__global__ void kelley_step_kernel(KelleyState* sp, KHandles h) {
+  if (threadIdx.x != 0) return;
+  KelleyState& s = *sp;
+  constexpr unsigned long long es = sizeof(T);
+  if (s.done) {  // (defensive: the WHILE already stopped)
+    ks_set(h, 0, 0, 0, 0, 0, 0);
+    return;
+  }
+  if (s.pending) {
+    // ---- the pass at tq just ran: its tuple -> counts, F, the rank test, the bracket update
+    s.pending = 0;
+    const DevPass r = s.tuple;
+    const bool compact = s.compact != 0;
+    const unsigned long long now = gtimer_ns();
+    s.passes++;
+    s.cp_iters++;
+    s.launches += 1;
+    const unsigned long long zl = r.z_lo, zh = r.z_hi;
+    s.bytes_moved += s.n_cur * es + (compact ? (zl + zh) * es : 0ull);
+    const unsigned long long c_lt = compact ? s.c_le_L + zl : s.D_lo + r.c_lt;
+    const unsigned long long c_le = compact ? c_lt + (s.m - zl - zh) : c_lt + r.c_eq;
+    // F_k(tq) from positive terms only (App. A identities; Eq. 2 with paper-k = n-k+1, R2)
+    const double tq = s.tq;
+    const double N_t = s.N_L + (double)s.c_le_L * (tq - s.yL) + r.L_lo;
+    const double P_t = s.P_R + (double)(s.n - s.c_lt_R) * (s.yR - tq) + r.L_hi;
+    KRow row;
+    row.t = tq;
+    row.F = s.wP * P_t + s.wN * N_t;
+    row.c_lt = c_lt;
+    row.c_eq = c_le - c_lt;
+    row.interior = 0;
+    row.scanned = s.n_cur;
+    row.written = compact ? zl + zh : 0ull;
+    row.kind = (unsigned)s.kind;
+    row.compacted = compact ? 1u : 0u;
+    row.kernel_ms = 1e-6 * (double)(now - s.t_start_ns);  // this pass, graph-node overheads included
+    const unsigned long long k = s.k;
+    // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
+    if (c_lt < k && k <= c_le) {
+      ks_row(s, row);
+      ks_finish(s, h, tq, 2u, 0);
+      return;
+    }
+    const unsigned long long m_old = s.m;
+    int side;
+    if (c_le < k) {  // dF(t) < 0: y_L <- t (sign per R1)
+      const unsigned long long c_hi = s.c_lt_R - c_le;
+      if (c_le + 1 == k && isfinite(r.succ)) {  // x_(k) = successor of t (P:L192 footnote, mirrored)
+        ks_row(s, row);
+        ks_finish(s, h, r.succ, 4u, 0);
+        return;
+      }
+      if (compact && zh != c_hi) {
+        ks_finish(s, h, 0.0, 0u, 1);
+        return;
+      }
+      s.yL = tq; s.N_L = N_t; s.c_le_L = c_le; s.m = c_hi;
+      s.t = tq + r.L_hi / (double)c_hi;  // mean of ]t, yR[ (App. A)
+      side = 1;
+    } else {  // c_lt >= k: y_R <- t
+      const unsigned long long c_lo = c_lt - s.c_le_L;
+      if (c_lt == k && isfinite(r.pred)) {  // x_(k) = largest x < t (P:L192 footnote)
+        ks_row(s, row);
+        ks_finish(s, h, r.pred, 3u, 0);
+        return;
+      }
+      if (compact && zl != c_lo) {
+        ks_finish(s, h, 0.0, 0u, 1);
+        return;
+      }
+      s.yR = tq; s.P_R = P_t; s.c_lt_R = c_lt; s.m = c_lo;
+      s.t = tq - r.L_lo / (double)c_lo;  // mean of ]yL, t[ (App. A)
+      side = 0;
+    }
+    row.interior = s.m;
+    ks_row(s, row);
+    if (compact) {
+      const unsigned long long hn = side == 0 ? zl : zh;
+      if (s.m <= s.select_cap) {
+        // hybrid finish: the exact select in the kept half, by the radix rounds after the loop
+        s.sel_r = k - s.c_le_L;
+        s.sel_m = hn;
+        s.z_count = hn;
+        if (s.dense) {
+          s.sel_base = static_cast<const char*>(s.zb[s.tgt]) + (side == 0 ? 0ull : (s.cap - zh)) * es;
+          s.sel_tab = nullptr;
+          s.sel_side = 0;
+          s.sel_seg = 0;
+        } else {
+          s.sel_base = s.sb[s.tgt];
+          s.sel_tab = s.st[s.tgt];
+          s.sel_side = side;
+          s.sel_seg = 1;
+        }
+        s.bytes_moved += (unsigned long long)(sizeof(T) == 4 ? 3 : 6) * hn * es;
+        s.launches += sizeof(T) == 4 ? 3u : 6u;
+        s.exit_reason = 5u;
+        s.done = 1;
+        ks_set(h, 0, 0, 0, 0, s.sel_seg ? 1u : 0u, s.sel_seg ? 0u : 1u);
+        ks_report(s);  // the last radix round publishes the value
+        return;
+      }
+      // continue the cutting plane on the kept half only (multi-level compaction, §8f-1)
+      if (s.dense) {
+        s.cur_seg = 0;
+        s.cur = static_cast<const char*>(s.zb[s.tgt]) + (side == 0 ? 0ull : (s.cap - zh)) * es;
+        s.cur_dbuf = s.tgt;
+      } else {
+        s.cur_seg = 1;
+        s.cur = s.sb[s.tgt];
+        s.cur_tab = s.st[s.tgt];
+        s.cur_side = side;
+        s.cur_sbuf = s.tgt;
+      }
+      s.n_cur = hn;
+      s.D_lo = s.c_le_L;
+      s.on_z = 1;
+      s.exact = 1;
+    }
+    // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
+    // ordered-key bisection until progress resumes
+    if (s.free_step) {
+      s.free_step = 0;
+    } else if (s.m > m_old - m_old / 8) {
+      if (++s.slow >= 2) s.bisect = 1;
+    } else {
+      s.slow = 0;
+      s.bisect = 0;
+    }
+  }
+  // ---- schedule the next pass
+  if (++s.it > s.max_iters || s.m == 0) {
+    ks_finish(s, h, 0.0, 0u, 1);
+    return;
+  }
+  s.kind = 0;
+  if (s.bisect) {
+    s.t = ks_key_mid<T>(s.yL, s.yR);
+    s.kind = 1;
+    s.fallback++;
+  }
+  const double tq = ks_snap<T>(s.t, s.yL, s.yR);
+  if (!(tq > s.yL && tq < s.yR)) {
+    ks_finish(s, h, 0.0, 0u, 1);
+    return;
+  }
+  s.tq = tq;
+  s.compact = (s.on_z || s.m <= s.z_cap) ? 1 : 0;
+  s.dense = s.m <= s.dense_cap ? 1 : 0;
+  if (s.compact) {
+    s.tgt = s.dense ? (s.cur_dbuf == 0 ? 1 : 0) : (s.cur_sbuf == 0 ? 1 : 0);
+    s.inside = (s.cur != s.x && s.exact) ? 1 : 0;
+    s.last_dense = s.dense;
+  }
+  s.pending = 1;
+  s.t_start_ns = gtimer_ns();
+  ks_set(h, 1, s.compact ? 0u : 1u, (s.compact && !s.inside) ? 1u : 0u, (s.compact && s.inside) ? 1u : 0u, 0, 0);
+}
 }  // namespace
 
 // ==========================================================================================
@@ -2969,6 +3224,122 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
     case kCompact: return launch_pass_t<double, kCompact>(a, grid, st);
     default: return launch_pass_t<double, kDirect>(a, grid, st);
   }
+}
+
+
+// ---- §8f-3: the device-resident Kelley loop as one CUDA graph -------------------------------
+static cudaError_t add_kernel(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* deps, size_t ndeps,
+                              const void* fn, dim3 grid, dim3 block, size_t smem, void** args) {
+  cudaKernelNodeParams kp = {};
+  kp.func = const_cast<void*>(fn);
+  kp.gridDim = grid;
+  kp.blockDim = block;
+  kp.sharedMemBytes = (unsigned)smem;
+  kp.kernelParams = args;
+  return cudaGraphAddKernelNode(node, g, deps, ndeps, &kp);
+}
+static cudaError_t add_cond(cudaGraph_t g, cudaGraphNode_t* node, const cudaGraphNode_t* deps, size_t ndeps,
+                            cudaGraphConditionalHandle h, cudaGraphConditionalNodeType type, cudaGraph_t* body) {
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = h;
+  p.conditional.type = type;
+  p.conditional.size = 1;
+  cudaError_t e = cudaGraphAddNode(node, g, deps, ndeps, &p);
+  if (e == cudaSuccess) *body = p.conditional.phGraph_out[0];
+  return e;
+}
+
+template <typename T>
+static cudaError_t kelley_graph_t(const LaunchShape& s, KelleyState* ks, void* partials, unsigned* ticket,
+                                  unsigned long long* cursors, RadixState* rstate, unsigned* hist,
+                                  cudaGraphExec_t* out) {
+  const int dt = sizeof(T) == 4 ? kF32 : kF64;
+  cudaGraph_t g = nullptr;
+  cudaError_t e;
+#define GK(x)                        \
+  do {                               \
+    if ((e = (x)) != cudaSuccess) {  \
+      if (g) cudaGraphDestroy(g);    \
+      return e;                      \
+    }                                \
+  } while (0)
+  GK(cudaGraphCreate(&g, 0));
+  KHandles h{};
+  GK(cudaGraphConditionalHandleCreate(&h.hw, g, 1, cudaGraphCondAssignDefault));
+  GK(cudaGraphConditionalHandleCreate(&h.hrs, g, 0, cudaGraphCondAssignDefault));
+  GK(cudaGraphConditionalHandleCreate(&h.hrd, g, 0, cudaGraphCondAssignDefault));
+  cudaGraphNode_t nw, nrs, nrd;
+  cudaGraph_t body, brs, brd;
+  GK(add_cond(g, &nw, nullptr, 0, h.hw, cudaGraphCondTypeWhile, &body));
+  GK(cudaGraphConditionalHandleCreate(&h.hh, body, 0, cudaGraphCondAssignDefault));
+  GK(cudaGraphConditionalHandleCreate(&h.hs0, body, 0, cudaGraphCondAssignDefault));
+  GK(cudaGraphConditionalHandleCreate(&h.hs1, body, 0, cudaGraphCondAssignDefault));
+  // body: step -> IF hot -> IF compacting (bracket tests) -> IF compacting (all inside)
+  KHandles hs_arg = h;  // (kernel-node parameters are copied when the node is created)
+  KelleyState* ks_arg = ks;
+  void* step_args[] = {&ks_arg, &hs_arg};
+  cudaGraphNode_t nstep, nh, ns0, ns1;
+  GK(add_kernel(body, &nstep, nullptr, 0, (const void*)kelley_step_kernel<T>, dim3(1), dim3(32), 0, step_args));
+  cudaGraph_t bh, bs0, bs1;
+  GK(add_cond(body, &nh, &nstep, 1, h.hh, cudaGraphCondTypeIf, &bh));
+  GK(add_cond(body, &ns0, &nh, 1, h.hs0, cudaGraphCondTypeIf, &bs0));
+  GK(add_cond(body, &ns1, &ns0, 1, h.hs1, cudaGraphCondTypeIf, &bs1));
+  PassArgs pa{};
+  pa.ks = ks;
+  pa.mode = kHot;
+  pa.cursors = cursors;
+  pa.partials = partials;
+  pa.ticket = ticket;
+  void* pa_args[] = {&pa};
+  cudaGraphNode_t tmp;
+  GK(add_kernel(bh, &tmp, nullptr, 0, (const void*)pass_kernel<T, kHot, 4>, dim3(s.grid_pass[dt][kHot]), dim3(kBlock),
+                pass_smem<T, kHot>(), pa_args));
+  SegArgs sa{};
+  sa.ks = ks;
+  sa.cursors = cursors;
+  sa.partials = partials;
+  sa.ticket = ticket;
+  void* sa_args[] = {&sa};
+  GK(add_kernel(bs0, &tmp, nullptr, 0, (const void*)seg_pass_kernel<T, false>, dim3(s.grid_seg[dt]), dim3(kBlock), 0,
+                sa_args));
+  GK(add_kernel(bs1, &tmp, nullptr, 0, (const void*)seg_pass_kernel<T, true>, dim3(s.grid_seg[dt]), dim3(kBlock), 0,
+                sa_args));
+  // after the loop: the radix rounds of the exact finish (segmented / dense kept half)
+  GK(add_cond(g, &nrs, &nw, 1, h.hrs, cudaGraphCondTypeIf, &brs));
+  GK(add_cond(g, &nrd, &nrs, 1, h.hrd, cudaGraphCondTypeIf, &brd));
+  static const int plan32[] = {21, 11, 10, 11, 0, 10};
+  static const int plan64[] = {53, 11, 42, 11, 31, 11, 20, 11, 10, 10, 0, 10};
+  const int rounds = dt == kF32 ? 3 : 6;
+  const int* plan = dt == kF32 ? plan32 : plan64;
+  for (int segv = 0; segv < 2; ++segv) {
+    cudaGraph_t bg = segv ? brs : brd;
+    cudaGraphNode_t prev = nullptr;
+    for (int i = 0; i < rounds; ++i) {
+      RadixArgs ra{};
+      ra.ks = ks;
+      ra.st = rstate; ra.hist = hist; ra.ticket = ticket;
+      ra.Wtot = s.grid_seg[dt] * kWarps;
+      ra.shift = plan[2 * i]; ra.bits = plan[2 * i + 1];
+      ra.first = i == 0; ra.last = i == rounds - 1;
+      void* ra_args[] = {&ra};
+      const void* fn = segv ? (const void*)radix_round_kernel<T, true> : (const void*)radix_round_kernel<T, false>;
+      const int grid = segv ? s.grid_seg[dt] : s.grid_hist[dt];
+      cudaGraphNode_t nn;
+      GK(add_kernel(bg, &nn, prev ? &prev : nullptr, prev ? 1 : 0, fn, dim3(grid), dim3(kBlock), 0, ra_args));
+      prev = nn;
+    }
+  }
+  GK(cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  return cudaSuccess;
+#undef GK
+}
+
+cudaError_t kelley_graph_build(int dtype, const LaunchShape& s, KelleyState* ks, void* partials, unsigned* ticket,
+                               unsigned long long* cursors, RadixState* rstate, unsigned* hist, cudaGraphExec_t* out) {
+  if (dtype == kF32) return kelley_graph_t<float>(s, ks, partials, ticket, cursors, rstate, hist, out);
+  return kelley_graph_t<double>(s, ks, partials, ticket, cursors, rstate, hist, out);
 }
 
 int seg_total_warps(int dtype, const LaunchShape& s) { return s.grid_seg[dtype] * kWarps; }

@@ -54,7 +54,10 @@ struct RadixState {
 
 enum PassMode : int { kHot = 0, kCompact = 1, kDirect = 2 };
 
+struct KelleyState;
+
 struct PassArgs {
+  const struct KelleyState* ks;      // device loop (§8f-3): x, n, t, y_lo, y_hi, out taken from *ks
   const void* x;
   uint64_t n;
   double t, y_lo, y_hi;              // representable in the dtype
@@ -79,6 +82,7 @@ struct SegEntry {
   unsigned long long cnt[2];  // lengths
 };
 struct SegArgs {
+  struct KelleyState* ks;      // device loop (§8f-3): input, bracket, output taken from *ks
   // input: contiguous (seg_in == nullptr: x[0..n), warp-strided groups) or segmented
   const void* x;
   uint64_t n;                  // contiguous: elements; segmented: total (diagnostic)
@@ -150,6 +154,67 @@ struct LaunchShape {
   int grid_hist[2];
   int grid_seg[2];
 };
+
+// ---- device-resident Kelley loop (NEXT row §8f-3) ---------------------------------------------
+// The Kelley iterations of Algorithm 1 without a host round trip: ONE CUDA graph per
+// (ctx, dtype) whose WHILE node runs {step kernel; IF hot: pass_kernel; IF compacting:
+// seg_pass_kernel (bracket tests / all inside)} until the step kernel ends the loop, followed by
+// the radix rounds of the exact finish (segmented or dense input) under IF nodes.  Every kernel
+// reads its array, bracket and output from this state; the step kernel (one thread) is drive()'s
+// Kelley step: exact rank test, tightest cuts, interior-mean iterate, snap to the dtype, ordered-key
+// safeguard, compaction / adoption of the kept half, the hand-off to the exact select.
+struct KRow {  // == cpsel_trace_row
+  double t, F;
+  unsigned long long c_lt, c_eq, interior, scanned, written;
+  unsigned kind, compacted;
+  double kernel_ms;
+};
+constexpr int kKelleyMaxRows = 256;
+// what the host reads when the loop is over (mapped pinned memory, written by the step kernel)
+struct KelleyReport {
+  int error;
+  unsigned exit_reason, passes, cp_iters, fallback, launches, n_rows, pad;
+  unsigned long long bytes_moved, z_count;
+  KRow rows[kKelleyMaxRows];
+};
+struct KelleyState {
+  // configuration (host-written)
+  unsigned long long n, k, z_cap, select_cap, dense_cap, max_iters, seq;
+  double wP, wN;
+  const void* x;
+  void* sb[2];
+  SegEntry* st[2];
+  void* zb[2];
+  unsigned long long cap, R;
+  int dt, record;
+  double* vout;                   // mapped mailbox: the value, then `seq` into *done_flag
+  unsigned long long* done_flag;
+  KelleyReport* rep;              // mapped: the trace rows and counters
+  // driver state (host-written at the hand-off, then the step kernel's)
+  double yL, yR, t, N_L, P_R, tq;
+  unsigned long long c_le_L, c_lt_R, m, D_lo, it;
+  int on_z, exact, bisect, slow, free_step, kind;
+  // current array / the pass being run
+  const void* cur;
+  unsigned long long n_cur;
+  const SegEntry* cur_tab;
+  int cur_seg, cur_side, cur_sbuf, cur_dbuf, tgt, last_dense, compact, dense, inside, pending;
+  DevPass tuple;                  // the pass's result (grid finish)
+  // outcome
+  int done, error;
+  unsigned exit_reason, passes, cp_iters, fallback, launches, n_rows;
+  double value;
+  unsigned long long bytes_moved, t_start_ns, z_count;
+  // the exact finish handed to the radix rounds
+  const void* sel_base;
+  const SegEntry* sel_tab;
+  int sel_side, sel_seg;
+  unsigned long long sel_m, sel_r;
+};
+// Build the graph for dtype on ctx scratch (partials, ticket, cursors, radix state / histogram).
+cudaError_t kelley_graph_build(int dtype, const struct LaunchShape& s, KelleyState* ks, void* partials,
+                               unsigned* ticket, unsigned long long* cursors, RadixState* rstate, unsigned* hist,
+                               cudaGraphExec_t* out);
 
 // Query occupancy and fill the persistent grid sizes (multiples of the SM count).
 cudaError_t query_shapes(int device, LaunchShape* shape);

@@ -1,7 +1,7 @@
 """The paper's method as a measured configuration: Kelley passes from [x_(1), x_(n)] (init_cut=0,
 pass_cuts=0, objective=1 — P:L155-198), per-pass CUDA-event time and bytes from the trace.
 
-python scripts/time_kelley.py [log2n] [dists] [--f64] [--zcap N] [--reps R]
+python scripts/time_kelley.py [log2n] [dists] [--f64] [--zcap N] [--reps R] [--device-loop]
 Prints one line per distribution (ms per selection, passes, achieved GB/s per pass class) and the
 trace of the last call.
 """
@@ -37,7 +37,8 @@ for d in dists:
     x = datagen.make(d, n, dtype, device="cuda")
     torch.cuda.synchronize()
     k = (n + 1) // 2
-    cfg = dict(init_cut=0, pass_cuts=0, objective=1, z_cap=zcap)
+    cfg = dict(init_cut=0, pass_cuts=0, objective=1, z_cap=zcap,
+               device_loop=1 if "--device-loop" in sys.argv else 0)
     cp.set_config(dev, record_timing=0, **cfg)
     for _ in range(2):
         cp.select_kth(x, k)
@@ -74,4 +75,4 @@ for d in dists:
                   f"interior {r['interior']:>11} compacted {r['compacted']} kernel_ms {r['kernel_ms']:.4f}", flush=True)
     del x
     torch.cuda.empty_cache()
-cp.set_config(dev, record_timing=0, init_cut=1, pass_cuts=1, objective=0, z_cap=0)
+cp.set_config(dev, record_timing=0, init_cut=1, pass_cuts=1, objective=0, z_cap=0, device_loop=0)

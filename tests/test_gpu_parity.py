@@ -483,3 +483,34 @@ def test_extreme_ranks_open_cuts(cp, dtype):
         v, info = cp.select_kth(xd, k, return_info=True)
         assert v == canon(float(srt[k - 1])), (k, v)
         assert info["passes"] == 1, (k, info)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+@pytest.mark.parametrize("dist", ["uniform", "cauchy", "mix1", "dup256"])
+def test_device_loop_matches_host_loop(cp, dtype, dist):
+    """§8f-3: the device-resident Kelley loop (one CUDA graph: WHILE {step kernel; pass kernel} + the
+    exact select) takes exactly the host driver's steps — the same iterates, counts and interior
+    sizes at every pass, the same element — and the element is the oracle's."""
+    import torch
+    n = 3_000_007
+    x = datagen.make(dist, n, dtype)
+    xd = torch.from_numpy(x).cuda()
+    srt = np.sort(x)
+    for cfg in (dict(init_cut=0, pass_cuts=0, objective=1), dict(init_cut=0, pass_cuts=0, objective=0, z_cap=1 << 20)):
+        for k in (2, n // 10, O.median_rank(n), n - 1):
+            out = {}
+            for dl in (0, 1):
+                cp.set_config(device_loop=dl, **cfg)
+                v, info = cp.select_kth(xd, k, return_info=True)
+                out[dl] = (v, info, cp.get_trace())
+            cp.set_config(device_loop=0, init_cut=1, pass_cuts=1, objective=0, z_cap=0)
+            (v0, i0, t0), (v1, i1, t1) = out[0], out[1]
+            assert v0 == v1 == canon(float(srt[k - 1])), (k, v0, v1)
+            assert i0["passes"] == i1["passes"] and i0["exit"] == i1["exit"], (i0, i1)
+            assert len(t0) == len(t1)
+            for a, b in zip(t0, t1):
+                assert (a["t"], a["c_lt"], a["c_eq"], a["interior"], a["compacted"], a["kind"]) == \
+                       (b["t"], b["c_lt"], b["c_eq"], b["interior"], b["compacted"], b["kind"])
+                if cfg["objective"]:
+                    assert b["F"] == pytest.approx(a["F"], rel=1e-12)
+            assert i1["launches"] < i0["launches"] + 4      # one graph launch for the whole loop
