@@ -261,6 +261,33 @@ def kelley_side(cp, torch, datagen, dev, dists, log2n, peak, reps=3):
     return out
 
 
+def knn_side(cp, torch, dev, peak, reps=3):
+    """kNN regression via d_(k) (§8f-4): n=1e6 reference points in p=10, nq=1024
+    queries, k=32 — distances (float32, written once), the batched k-th select per query and the
+    rho/a,b reduction.  Bound: HBM (the nq x n distance matrix: written, then read by the select's
+    passes and the reduction)."""
+    import numpy as np
+    n, p, nq, k = 1_000_000, 10, 1024, 32
+    rng = np.random.default_rng(11042732)
+    X = rng.standard_normal((n, p)).astype(np.float32)
+    f = (np.sin(X[:, 0]) + 0.1 * rng.standard_normal(n)).astype(np.float32)
+    Q = rng.standard_normal((nq, p)).astype(np.float32)
+    Xd, fd, Qd = (torch.from_numpy(v).to(dev) for v in (X, f, Q))
+    cp.knn_regress(Xd, fd, Qd, k)
+    torch.cuda.synchronize()
+    e0, e1 = _ev(torch)
+    e0.record()
+    for _ in range(reps):
+        out, info = cp.knn_regress(Xd, fd, Qd, k, return_info=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    return {"workload": "kNN regression n=1e6 p=10 nq=1024 k=32 (uniform weights)", "ms": ms,
+            "queries_per_s": nq / (ms / 1e3), "distances_per_s": n * nq / (ms / 1e3),
+            "bytes_moved": info["bytes_moved"], "GBps": info["bytes_moved"] / (ms / 1e3) / 1e9,
+            "frac": info["bytes_moved"] / (ms / 1e3) / 1e9 / peak, "select_passes_per_query": info["passes"] / nq}
+
+
 def _flush_l2(torch, buf):
     buf.add_(1.0)  # 256 MiB > 126 MB L2
 
@@ -580,6 +607,10 @@ def main():
             side = configs_side(cp, torch, datagen, dev, peak)
         except Exception as ex:
             side = {"error": f"{type(ex).__name__}: {ex}"}
+        try:
+            side["knn"] = knn_side(cp, torch, dev, peak)
+        except Exception as ex:
+            side["knn"] = {"error": f"{type(ex).__name__}: {ex}"}
 
     # CPU baseline: the oracle as it stands, on bounded host samples (rank 0, N=1 only)
     cpu = None

@@ -265,6 +265,24 @@ cpsel_status cpsel_select_kth_sharded(cpsel_ctx* ctx, const void* d_shard, uint6
 cpsel_status cpsel_pooled_cuts(const uint64_t* keys, const uint64_t* m, uint32_t G, uint64_t r, cpsel_dtype dtype,
                                double* out3);
 
+/* ---- kNN regression via d_(k) (NEXT row §8f-4) --------------------------------- */
+/* For every query q_j (row j of Q, nq x p float32 row-major) and the n reference points x_i (rows of
+ * X, n x p float32 row-major) with ordinates f_i (float32[n]), all device pointers:
+ *   d2_ij = sum_l (q_jl - x_il)^2            float32, round-to-nearest in the order l = 0..p-1
+ *   d2_(k)j = the k-th smallest of row j     (the batched cutting-plane selection, step a8)
+ *   out[j] = sum_i rho_ij w_ij f_i / sum_i rho_ij w_ij,  rho = 1 if d2 < d2_(k), a/b if d2 = d2_(k),
+ *            0 otherwise, a = k - #{d2 < d2_(k)}, b = #{d2 = d2_(k)}  (the paper's indicator rho,
+ *            P:L469-476 at rank k: exactly k neighbours' worth of weight, ties shared);
+ *            w = 1 (weighting 0) or 1/(d2 + 1e-12) (weighting 1, decreasing in the distance);
+ *            fp64 accumulation, written as float32.
+ * d_dk (nullable, float32[nq]) receives d2_(k) per query.  1 <= p <= 32.  The call owns an
+ * nq x n float32 scratch matrix (grown lazily, freed with the ctx) and returns after completion.
+ * Errors: EINVAL (null pointers, n/nq/p == 0, p > 32, nq > 1048560, weighting not 0/1), ERANK (k outside [1, n]),
+ * ENONFINITE (NaN/Inf in X, Q or f), ENOMEM, ECUDA. */
+cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_f, uint64_t n, uint32_t p,
+                               const float* d_Q, uint32_t nq, uint64_t k, int32_t weighting, float* d_out,
+                               float* d_dk, cpsel_info* info);
+
 /* ---- host-only driver (no GPU needed) ------------------------------------------------------ */
 /* The same cutting-plane driver, with the three device steps supplied as callbacks.  Used by
  * the CPU tests (world-size-2 gloo tests of the sharded combine) to exercise the exact host

@@ -391,3 +391,46 @@ def order_statistic_c(x, k: int, method: str = "nth_element"):
     ct = ctypes.c_float if x.dtype == np.float32 else ctypes.c_double
     v = getattr(_clib(), name)(x.ctypes.data_as(ctypes.POINTER(ct)), n, k)
     return canonical(x.dtype.type(v))
+
+
+# ============================================================================ kNN via d_(k)
+def knn_distances_sq(X, Q):
+    """Squared Euclidean distances D[j, i] = sum_l (Q[j,l] - X[i,l])^2 (P:L483 'the array of
+    distances d'), in float32 with every operation rounded (numpy float32 arithmetic), l in order
+    0..p-1 — the definition written out in the precision the path computes in (north_star: the
+    decision d < d_(k) is taken in the same precision on both sides)."""
+    X = np.asarray(X, dtype=np.float32)
+    Q = np.asarray(Q, dtype=np.float32)
+    acc = np.zeros((Q.shape[0], X.shape[0]), dtype=np.float32)
+    for l in range(X.shape[1]):
+        e = Q[:, l:l + 1] - X[None, :, l]          # float32 - float32 -> float32 (rounded)
+        acc = acc + e * e                           # float32 product, float32 sum (each rounded)
+    return acc
+
+
+def knn_weights(d2, weighting: int):
+    """w_i: 1 (plain mean of the k nearest) or 1/(d2 + 1e-12), a decreasing function of the
+    distance (P:L483 'w_i are the weights that are decreasing functions of the distances')."""
+    d2 = np.asarray(d2, dtype=LD)
+    return np.ones_like(d2) if weighting == 0 else LD(1) / (d2 + LD(1e-12))
+
+
+def knn_regress(X, f, Q, k: int, weighting: int = 0):
+    """kNN regression by the k-th order statistic: d_(k) = the k-th smallest distance,
+    then the indicator rho (P:L469-476 with h = k): rho = 1 for d < d_(k), a/b for d = d_(k) (a =
+    k - #{d < d_(k)}, b = #{d = d_(k)}), 0 otherwise, and f(q) = sum rho w f / sum rho w by
+    reduction (long double).  Returns (predictions float64[nq], d2_(k) float32[nq])."""
+    D = knn_distances_sq(X, Q)
+    f = np.asarray(f, dtype=np.float32).astype(LD)
+    out = np.empty(D.shape[0], dtype=np.float64)
+    dk = np.empty(D.shape[0], dtype=np.float32)
+    for j in range(D.shape[0]):
+        row = D[j]
+        t = order_statistic(row, k)
+        lt, eq = row < t, row == t
+        a, b = k - int(np.count_nonzero(lt)), int(np.count_nonzero(eq))
+        rho = lt.astype(LD) + eq.astype(LD) * (LD(a) / LD(b))
+        w = knn_weights(row, weighting) * rho
+        out[j] = float(np.sum(w * f) / np.sum(w))
+        dk[j] = t
+    return out, dk

@@ -17,7 +17,7 @@ __all__ = [
     "select_kth", "median", "select_kth_host", "lms_objective", "lms_residuals", "select_kth_batched",
     "eval", "init_stats", "small_select", "get_trace", "set_config", "get_config", "nccl_unique_id",
     "comm_init", "select_kth_sharded", "drive_host", "library_path", "load", "CpselError",
-    "LoopbackGroup", "comm_init_loopback",
+    "LoopbackGroup", "comm_init_loopback", "knn_regress",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -112,6 +112,7 @@ SYMBOLS = [
     "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_init_timings", "cpsel_nccl_unique_id",
     "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host", "cpsel_pooled_cuts",
     "cpsel_lts_objective", "cpsel_loopback_create", "cpsel_loopback_destroy", "cpsel_comm_init_loopback",
+    "cpsel_knn_regress",
 ]
 
 _lib = None
@@ -164,6 +165,7 @@ def load():
             "cpsel_loopback_create": (I, [I, C.POINTER(P)]),
             "cpsel_loopback_destroy": (None, [P]),
             "cpsel_comm_init_loopback": (I, [P, P, I]),
+            "cpsel_knn_regress": (I, [P, P, P, U64, U32, P, U32, U64, C.c_int32, P, P, C.POINTER(Info)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -444,6 +446,32 @@ def select_kth_batched(S, k: int, return_info: bool = False):
     _check(ctx, load().cpsel_select_kth_batched(ctx.handle, C.c_void_p(S.data_ptr()), n, Cn, int(k),
                                                 C.c_void_p(out.data_ptr()), C.byref(info)))
     return (out, info.as_dict()) if return_info else out
+
+
+# ------------------------------------------------------------------------------------------ kNN
+def knn_regress(X, f, Q, k: int, weighting: int = 0, return_dk: bool = False, return_info: bool = False):
+    """kNN regression via d_(k): for each query row of Q (nq, p), the rho-weighted mean
+    of f over the k nearest rows of X (n, p) — see cpsel_knn_regress.  Returns a float32 (nq,)
+    tensor (and d2_(k) per query, and the report, if asked)."""
+    import torch
+    for t in (X, f, Q):
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("X, f, Q must be contiguous float32 CUDA tensors")
+    if X.dim() != 2 or Q.dim() != 2 or Q.shape[1] != X.shape[1] or f.numel() != X.shape[0]:
+        raise ValueError("X (n, p), f (n,), Q (nq, p)")
+    n, p = X.shape
+    nq = Q.shape[0]
+    ctx = _ctx_for(X)
+    out = torch.empty(nq, device=X.device, dtype=torch.float32)
+    dk = torch.empty(nq, device=X.device, dtype=torch.float32)
+    info = Info()
+    _check(ctx, load().cpsel_knn_regress(ctx.handle, C.c_void_p(X.data_ptr()), C.c_void_p(f.data_ptr()), n, p,
+                                         C.c_void_p(Q.data_ptr()), nq, int(k), int(weighting),
+                                         C.c_void_p(out.data_ptr()), C.c_void_p(dk.data_ptr()), C.byref(info)))
+    res = (out, dk) if return_dk else (out,)
+    if return_info:
+        res = res + (info.as_dict(),)
+    return res if len(res) > 1 else res[0]
 
 
 # ------------------------------------------------------------------------------------------ multi-GPU

@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
          "--expt-relaxed-constexpr"]
-SOURCES = ["cpsel_kernels.cu", "cpsel_lms.cu", "cpsel_driver.cpp", "cpsel_nccl.cpp", "cpsel_comm.cpp"]
+SOURCES = ["cpsel_kernels.cu", "cpsel_lms.cu", "cpsel_driver.cpp", "cpsel_nccl.cpp", "cpsel_comm.cpp", "cpsel_knn.cu"]
 
 
 def _deps_newer(target: str) -> bool:

@@ -21,6 +21,7 @@
 #include "cpsel_kernels.h"
 #include "cpsel_lms.h"
 #include "cpsel_comm.h"
+#include "cpsel_knn.h"
 #include "cpsel_nccl.h"
 
 using namespace cpsel;
@@ -102,6 +103,9 @@ struct cpsel_ctx {
   KelleyReport* h_rep = nullptr;
   KelleyReport* d_rep = nullptr;
   cudaGraphExec_t kgraph[2] = {nullptr, nullptr};
+  // kNN (§8f-4): the distance matrix, the d2_(k) per query, the non-finite counter
+  void* d_knn = nullptr;
+  size_t knn_bytes = 0;
 };
 
 namespace {
@@ -1956,6 +1960,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     for (cudaGraphExec_t g : ctx->kgraph)
       if (g) cudaGraphExecDestroy(g);
     if (ctx->d_ks) cudaFree(ctx->d_ks);
+    if (ctx->d_knn) cudaFree(ctx->d_knn);
     if (ctx->h_ks) cudaFreeHost(ctx->h_ks);
     if (ctx->h_rep) cudaFreeHost(ctx->h_rep);
     for (cudaEvent_t e : ctx->evpool) cudaEventDestroy(e);
@@ -2332,6 +2337,51 @@ cpsel_status cpsel_lts_objective(cpsel_ctx* ctx, const float* d_X, const float* 
   else CK(lts_reduce(ctx->lms.S, n, C, h, d_m, d_out, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (info) info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return CPSEL_OK;
+}
+
+// ------------------------------------------------------------------------ kNN (§8f-4)
+cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_f, uint64_t n, uint32_t p,
+                               const float* d_Q, uint32_t nq, uint64_t k, int32_t weighting, float* d_out,
+                               float* d_dk, cpsel_info* info) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!d_X || !d_f || !d_Q || !d_out) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || nq == 0 || p == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (p > (uint32_t)kKnnMaxP) return fail(ctx, CPSEL_EINVAL, "p > %d", kKnnMaxP);
+  if (nq > 65535u * 16u) return fail(ctx, CPSEL_EINVAL, "nq > 1048560");
+  if (weighting != 0 && weighting != 1) return fail(ctx, CPSEL_EINVAL, "weighting must be 0 or 1");
+  if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
+  DeviceGuard g(ctx->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  const size_t dbytes = (size_t)n * nq * sizeof(float), off_dk = (dbytes + 255) / 256 * 256;
+  const size_t off_bad = off_dk + ((size_t)nq * sizeof(float) + 255) / 256 * 256;
+  cpsel_status s = ensure(ctx, &ctx->d_knn, &ctx->knn_bytes, off_bad + 256);
+  if (s != CPSEL_OK) return s;
+  char* base = static_cast<char*>(ctx->d_knn);
+  float* D = reinterpret_cast<float*>(base);
+  float* dk = d_dk ? d_dk : reinterpret_cast<float*>(base + off_dk);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(base + off_bad);
+  CK(cudaMemsetAsync(bad, 0, 2 * sizeof *bad, ctx->stream));
+  CK(knn_distances(d_X, d_Q, n, p, nq, D, bad, ctx->stream));            // 1. distances
+  unsigned long long hbad[2] = {0, 0};
+  CK(cudaMemcpyAsync(hbad, bad, sizeof hbad[0], cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hbad[0]) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf (or a distance overflows)");
+  LmsReport rep{};
+  cudaError_t e = batched_select(ctx->lms, D, n, nq, k, dk, ctx->cfg.max_iters, &rep, ctx->stream);  // 2. d2_(k)
+  if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a query");
+  CK(e);
+  if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf");
+  CK(knn_reduce(D, d_f, n, nq, k, dk, weighting, d_out, bad + 1, ctx->stream));  // 3. the rho reduction
+  CK(cudaMemcpyAsync(hbad + 1, bad + 1, sizeof hbad[1], cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hbad[1]) return fail(ctx, CPSEL_ENONFINITE, "f holds NaN or Inf");
+  lms_info(info, rep, false);
+  if (info) {
+    info->launches += 2;
+    info->bytes_moved += 2 * dbytes;  // D written once, read once more by the reduction
+    info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
   return CPSEL_OK;
 }
 

@@ -1,0 +1,19 @@
+// kNN regression via d_(k) (internal; NEXT row §8f-4).  See cpsel_knn.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cpsel {
+
+constexpr int kKnnMaxP = 32;        // dimensions of a point
+constexpr double kKnnEps = 1e-12;   // inverse-distance weight 1/(d^2 + eps)
+
+// D (nq x n row-major): squared Euclidean distances, float32, explicit rn ops in order l = 0..p-1;
+// *bad += #non-finite distances
+cudaError_t knn_distances(const float* X, const float* Q, uint64_t n, uint32_t p, uint32_t nq, float* D,
+                          unsigned long long* bad, cudaStream_t st);
+// out[j] = sum rho_i w_i f_i / sum rho_i w_i, rho = 1 below dk[j], a/b at it; *bad += #non-finite f
+cudaError_t knn_reduce(const float* D, const float* f, uint64_t n, uint32_t nq, uint64_t k, const float* dk,
+                       int weighting, float* out, unsigned long long* bad, cudaStream_t st);
+
+}  // namespace cpsel

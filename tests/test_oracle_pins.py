@@ -544,3 +544,52 @@ def test_order_statistic_c_matches_definition():
             assert np.array_equal(before, x, equal_nan=True)
     with pytest.raises(ValueError):
         O.order_statistic_c(np.ones(3, np.float32), 4)
+
+
+# ----------------------------------------------------------------------------- kNN via d_(k)
+def test_knn_distances_exact_on_integer_grid():
+    """float32 squared distances of small-integer points are exact: equal to the integer formula."""
+    rng = np.random.default_rng(3)
+    X = rng.integers(-20, 21, (50, 4)).astype(np.float32)
+    Q = rng.integers(-20, 21, (7, 4)).astype(np.float32)
+    D = O.knn_distances_sq(X, Q)
+    for j in range(7):
+        for i in range(50):
+            assert D[j, i] == sum(int(Q[j, l] - X[i, l]) ** 2 for l in range(4))
+
+
+def test_knn_without_ties_is_mean_of_k_nearest():
+    """No ties at d_(k): the rho/a,b reduction = the mean of f over the k nearest points found by a
+    full sort (the 'usual approach' of P:L485), uniform and inverse-distance weights."""
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((300, 3)).astype(np.float32)
+    f = rng.standard_normal(300).astype(np.float32)
+    Q = rng.standard_normal((5, 3)).astype(np.float32)
+    for k in (1, 2, 17, 300):
+        got, dk = O.knn_regress(X, f, Q, k)
+        gw, _ = O.knn_regress(X, f, Q, k, weighting=1)
+        for j in range(5):
+            d = [float(sum((float(Q[j, l]) - float(X[i, l])) ** 2 for l in range(3))) for i in range(300)]
+            idx = sorted(range(300), key=lambda i: d[i])[:k]
+            assert got[j] == pytest.approx(sum(float(f[i]) for i in idx) / k, rel=1e-12)
+            D = O.knn_distances_sq(X, Q)[j]
+            w = [1.0 / (float(D[i]) + 1e-12) for i in idx]
+            assert gw[j] == pytest.approx(sum(w[q] * float(f[i]) for q, i in enumerate(idx)) / sum(w), rel=1e-9)
+            assert dk[j] == np.sort(D)[k - 1]
+
+
+def test_knn_ties_share_weight_as_the_average_over_tie_choices():
+    """Ties at d_(k): rho = a/b is exactly the average, over every way of picking the a missing
+    neighbours among the b tied points, of the plain k-nearest mean (exact rationals)."""
+    X = np.array([[0.0], [1.0], [-1.0], [2.0], [-2.0], [2.0], [3.0]], np.float32)  # distances 0,1,1,4,4,4,9
+    f = np.array([10, 20, 30, 40, 50, 60, 70], np.float32)
+    Q = np.zeros((1, 1), np.float32)
+    for k in range(1, 8):
+        got, _ = O.knn_regress(X, f, Q, k)
+        d = [int(x[0]) ** 2 for x in X]
+        dk = sorted(d)[k - 1]
+        below = [i for i in range(7) if d[i] < dk]
+        tied = [i for i in range(7) if d[i] == dk]
+        a = k - len(below)
+        means = [Fraction(sum(int(f[i]) for i in below + list(c)), k) for c in itertools.combinations(tied, a)]
+        assert got[0] == pytest.approx(float(sum(means) / len(means)), rel=1e-15)
