@@ -43,6 +43,7 @@ struct cpsel_ctx {
   DevInit* d_init = nullptr;
   void* d_t0 = nullptr;              // the two extra cuts of the init pass (R23)
   void* d_skeys = nullptr;           // gathered sample keys (R29)
+  void* d_pool1 = nullptr;           // the one-GPU gathered sample values (R29, two-kernel form)
   ChainState* d_chain = nullptr;     // device chain state (§8f-3)
   RadixState* d_radix = nullptr;
   unsigned int* d_hist = nullptr;
@@ -413,8 +414,18 @@ struct GpuBackend : Backend {
     CK(tic());
     sample_slot = -1;
     if (cut && !presampled) {
-      CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream,
-                              /*small=*/n <= (1ull << 26), nullptr, 0, /*allow_open=*/!ctx->cfg.objective));
+      const bool small = n <= (1ull << 26);
+      const uint64_t S = pool_sample_size(dt, small);
+      if (n > 4 * S) {
+        // R29: the strided sample gathered by a many-CTA kernel (every SM's load slots, not just the
+        // cluster's 8: the gather was latency-bound there), then the cluster select reads it
+        // contiguously from L2 — the same sample and the same cuts as the one-launch form
+        CK(launch_pool_gather(dt, x, n, nullptr, 0, 0, S, ctx->d_pool1, ctx->stream));
+        CK(launch_pool_pick(dt, ctx->d_pool1, S, n, k, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
+      } else {
+        CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream, small, nullptr, 0,
+                                /*allow_open=*/!ctx->cfg.objective));
+      }
       CK(toc());
       sample_slot = slot;
       CK(tic());
@@ -1924,6 +1935,7 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMalloc(&ctx->d_init, sizeof(DevInit)));
   CKC(cudaMalloc(&ctx->d_t0, 32));  // t_lo, t_hi, the sample estimate
   CKC(cudaMalloc(&ctx->d_skeys, kSampleKeyBytes));
+  CKC(cudaMalloc(&ctx->d_pool1, std::max(pool_sample_size(kF32, false) * 4, pool_sample_size(kF64, false) * 8)));
   CKC(cudaMalloc(&ctx->d_chain, sizeof(ChainState)));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
   CKC(cudaMalloc(&ctx->d_hist, 2 * 2048 * sizeof(unsigned)));  // radix rounds | round 0 counted by the init
@@ -1946,7 +1958,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
     DeviceGuard g(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     ctx->comm.release();
-    void* dev[] = {ctx->d_t0, ctx->d_skeys, ctx->d_chain, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
+    void* dev[] = {ctx->d_t0, ctx->d_skeys, ctx->d_pool1, ctx->d_chain, ctx->d_partials, ctx->d_ticket, ctx->d_cursors, ctx->d_pass, ctx->d_init, ctx->d_radix,
                    ctx->d_hist, ctx->d_gather, ctx->d_gather_init, ctx->d_zb[0], ctx->d_zb[1], ctx->d_zall,
                    ctx->d_pool, ctx->d_sizes,
                    ctx->d_stage, ctx->d_sb[0], ctx->d_sb[1], ctx->d_st[0], ctx->d_st[1]};
