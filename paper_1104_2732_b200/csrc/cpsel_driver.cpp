@@ -1938,8 +1938,9 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMalloc(&ctx->d_pool1, std::max(pool_sample_size(kF32, false) * 4, pool_sample_size(kF64, false) * 8)));
   CKC(cudaMalloc(&ctx->d_chain, sizeof(ChainState)));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
-  CKC(cudaMalloc(&ctx->d_hist, 2 * 2048 * sizeof(unsigned)));  // radix rounds | round 0 counted by the init
-  CKC(cudaMemset(ctx->d_hist, 0, 2 * 2048 * sizeof(unsigned)));
+  // radix rounds | round 0 counted by the init | the cooperative rounds' histograms and barrier
+  CKC(cudaMalloc(&ctx->d_hist, kRadixHistWords * sizeof(unsigned)));
+  CKC(cudaMemset(ctx->d_hist, 0, kRadixHistWords * sizeof(unsigned)));
   CKC(cudaHostAlloc(&ctx->h_pass, sizeof(DevPass), cudaHostAllocDefault));
   CKC(cudaHostAlloc(&ctx->h_init, sizeof(DevInit), cudaHostAllocDefault));
   CKC(cudaHostAlloc(&ctx->h_radix, sizeof(RadixState), cudaHostAllocDefault));

@@ -1166,6 +1166,7 @@ template <typename T, int MODE> cudaError_t occ_pass(int* blocks) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, pass_kernel<T, MODE, 4>, kBlock, pass_smem<T, MODE>());
 }
 
+
 // ------------------------------------------------------------------------------------------
 // Step a2+a4, segmented form: warp-private compaction (no atomics for regions, no block barriers).
 constexpr int kSegU = 4;  // vectors per lane per group
@@ -1666,6 +1667,160 @@ __global__ void __launch_bounds__(kBlock) radix_round_kernel(RadixArgs a) {
   if (a.hist0)  // every CTA read it before taking its ticket
     for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
   if (threadIdx.x == 0) *a.ticket = 0u;
+}
+
+// ------------------------------------------------------------------------------------------
+// Step a5, all digit rounds in ONE cooperative launch (the grid is co-resident): per round every CTA
+// counts its share into shared memory and merges the nonzero bins into a global histogram (one of
+// three, rotating), a grid barrier, then EVERY CTA picks the digit from that histogram itself (the
+// same bytes, the same pick) and the next round starts — no launch, no last-CTA tail per round.
+// The first round's buffer of the next round is cleared before the barrier (nobody adds to it until
+// after), the one two rounds back is free by then; the last CTA out clears all three and hist0.
+struct RadixPlan {
+  int n;
+  int shift[6], bits[6];
+};
+struct CoopArgs {
+  RadixArgs a;
+  RadixPlan plan;
+  int first_round;
+  unsigned* g3;   // 3 x 2048 global digit counters (zero on entry, left zero)
+  unsigned* bar;  // [0] arrivals, [1] generation, [2] exit ticket (zero on entry, left zero)
+};
+__device__ __forceinline__ void coop_barrier(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+template <typename T, bool SEG>
+__global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_constant__ CoopArgs c) {
+  const RadixArgs& a = c.a;
+  pdl_wait();  // the init's copy, its round-0 counts and the chain decision
+  uint64_t rank0 = a.r;
+  if (a.chain) {
+    if (!a.chain->ok[1]) {  // skipped (uniformly): the init's round-0 counts must still be cleared
+      if (a.hist0 && blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
+      return;
+    }
+    rank0 = a.chain->r[1];
+  }
+  __shared__ unsigned sh[2048];
+  __shared__ unsigned long long s_prefix, s_mask, s_rank;
+  __shared__ unsigned wsum[kWarps];
+  __shared__ bool s_last;
+  __shared__ int s_shift[6], s_bits[6];
+  if (threadIdx.x < 6) {
+    s_shift[threadIdx.x] = c.plan.shift[threadIdx.x];
+    s_bits[threadIdx.x] = c.plan.bits[threadIdx.x];
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  // the digit holding rank r in a 2048-bin histogram h (global, read with ld.cg), as one block:
+  // 8 bins per thread, block scan of the thread totals; the finder updates the shared prefix
+  auto pick = [&](const unsigned* h, int shift, int bits, bool last) {
+    const int nb = 1 << bits;
+    unsigned hv[8], tsum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int b = threadIdx.x * 8 + j;
+      hv[j] = b < nb ? __ldcg(&h[b]) : 0u;
+      tsum += hv[j];
+    }
+    unsigned incl = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[w] = incl;
+    const unsigned long long r = s_rank, pf = s_prefix, mk = s_mask;
+    __syncthreads();
+    unsigned wbase = 0;
+    for (int q = 0; q < w; ++q) wbase += wsum[q];
+    unsigned long long before = wbase + incl - tsum;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (before < r && r <= before + hv[j]) {
+        const int digit = threadIdx.x * 8 + j;
+        const unsigned long long prefix = pf | ((unsigned long long)digit << shift);
+        s_prefix = prefix;
+        s_mask = mk | ((unsigned long long)(nb - 1) << shift);
+        s_rank = r - before;
+        if (last && blockIdx.x == 0) {
+          a.st->prefix = prefix;
+          a.st->mask = s_mask;
+          a.st->r = r - before;
+          a.st->count = hv[j];
+          a.st->key = prefix;
+          a.st->value = (sizeof(T) == 4) ? from_key_f32(prefix) : from_key_f64(prefix);
+          if (a.vout) *a.vout = a.st->value;
+          publish_done(a.done, a.seq);
+        }
+      }
+      before += hv[j];
+    }
+    __syncthreads();
+  };
+  if (threadIdx.x == 0) {
+    s_prefix = 0ull;
+    s_mask = 0ull;
+    s_rank = rank0;
+  }
+  __syncthreads();
+  if (a.hist0) pick(a.hist0, s_shift[0], s_bits[0], false);  // round 0 counted by the init pass
+  for (int ri = c.first_round; ri < c.plan.n; ++ri) {
+    const int shift = s_shift[ri], bits = s_bits[ri];
+    unsigned* G = c.g3 + 2048 * (ri % 3);
+    for (int i = threadIdx.x; i < 2048; i += kBlock) sh[i] = 0;
+    __syncthreads();
+    if (SEG) {
+      RadixSegFn f;
+      f.sh = sh;
+      f.sh_sa = (unsigned)__cvta_generic_to_shared(sh);
+      f.prefix = s_prefix;
+      f.mask = s_mask;
+      f.shift = shift;
+      f.dmask = (1u << bits) - 1u;
+      for (uint64_t W = (uint64_t)blockIdx.x * kWarps + w; W < (uint64_t)a.Wtot; W += (uint64_t)gridDim.x * kWarps) {
+        const SegEntry e = a.tab[W];
+        seg_run_pipe<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
+      }
+    } else {
+      HistFn<T> hf;
+      hf.sh = sh; hf.prefix = s_prefix; hf.mask = s_mask; hf.shift = shift; hf.dmask = (1u << bits) - 1u;
+      stream_array<T, 2>(static_cast<const T*>(a.z), a.m, hf, blockIdx.x, gridDim.x);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += kBlock)
+      if (sh[i]) atomicAdd(&G[i], sh[i]);
+    if (blockIdx.x == 0)  // next round's buffer: last read two barriers ago, added to only after this one
+      for (int i = threadIdx.x; i < 2048; i += kBlock) c.g3[2048 * ((ri + 1) % 3) + i] = 0u;
+    coop_barrier(c.bar, gridDim.x);
+    pick(G, shift, bits, ri == c.plan.n - 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(c.bar + 2, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  for (int i = threadIdx.x; i < 3 * 2048; i += kBlock) c.g3[i] = 0u;
+  if (a.hist0)
+    for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
+  if (threadIdx.x == 0) c.bar[2] = 0u;
 }
 
 template <typename T, bool INSIDE>
@@ -3147,6 +3302,16 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
   OCC(kF32, float, kHot) OCC(kF32, float, kCompact) OCC(kF32, float, kDirect)
   OCC(kF64, double, kHot) OCC(kF64, double, kCompact) OCC(kF64, double, kDirect)
 #undef OCC
+  {
+    int cb = 0;
+#define COOP(DT, T, SEGV)                                                                                  \
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cb, radix_coop_kernel<T, SEGV>, kBlock, 0)) != \
+      cudaSuccess)                                                                                        \
+    return e;                                                                                             \
+  s->coop_max[DT][SEGV ? 1 : 0] = s->num_sms * cb;
+    COOP(kF32, float, false) COOP(kF32, float, true) COOP(kF64, double, false) COOP(kF64, double, true)
+#undef COOP
+  }
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<float, false>, kBlock, 0)) != cudaSuccess) return e;
   s->grid_seg[kF32] = s->num_sms * (b > 0 ? b : 1);
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<double, false>, kBlock, 0)) != cudaSuccess) return e;
@@ -3966,6 +4131,45 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   static const int plan64[] = {53, 11, 42, 11, 31, 11, 20, 11, 10, 10, 0, 10};
   const int rounds = dtype == kF32 ? 3 : 6;
   const int* plan = dtype == kF32 ? plan32 : plan64;
+  {  // all rounds in one cooperative launch, if the grid fits co-resident
+    static const bool coop_on = !(getenv("CPSEL_RADIX_COOP") && getenv("CPSEL_RADIX_COOP")[0] == '0');
+    const int grid = tab ? s.grid_seg[dtype] : clamp_grid(s.grid_hist[dtype], m, kRadixPerCta);
+    if (coop_on && grid <= s.coop_max[dtype][tab ? 1 : 0]) {
+      CoopArgs c{};
+      RadixArgs& a = c.a;
+      a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
+      a.r = r; a.vout = vout; a.done = done; a.seq = seq; a.chain = chain;
+      a.Wtot = s.grid_seg[dtype] * kWarps;
+      a.hist0 = first_round == 1 ? hist0 : nullptr;
+      c.plan.n = rounds;
+      for (int i = 0; i < rounds; ++i) {
+        c.plan.shift[i] = plan[2 * i];
+        c.plan.bits[i] = plan[2 * i + 1];
+      }
+      c.first_round = first_round;
+      c.g3 = hist + 4096;
+      c.bar = hist + 4096 + 3 * 2048;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kBlock);
+      cfg.stream = st;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[1].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 2;
+      cudaError_t e;
+      if (dtype == kF32)
+        e = tab ? cudaLaunchKernelEx(&cfg, radix_coop_kernel<float, true>, c)
+                : cudaLaunchKernelEx(&cfg, radix_coop_kernel<float, false>, c);
+      else
+        e = tab ? cudaLaunchKernelEx(&cfg, radix_coop_kernel<double, true>, c)
+                : cudaLaunchKernelEx(&cfg, radix_coop_kernel<double, false>, c);
+      return e;
+    }
+  }
   RadixArgs a{};
   a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
   a.r = r; a.vout = vout; a.done = done; a.seq = seq; a.chain = chain;

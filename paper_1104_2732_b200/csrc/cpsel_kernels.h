@@ -153,6 +153,7 @@ struct LaunchShape {
   int grid_init[2];
   int grid_hist[2];
   int grid_seg[2];
+  int coop_max[2][2];    // [dtype][segmented]: co-resident CTAs of the cooperative radix select
 };
 
 // ---- device-resident Kelley loop (NEXT row §8f-3) ---------------------------------------------
@@ -283,7 +284,11 @@ cudaError_t launch_sample_cut(int dtype, const void* x, uint64_t n, uint64_t k, 
 cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cudaStream_t st);
 
 // Radix select of the r-th smallest (1-based) of z[0..m) (any element alignment).
-// hist: >= 2048 unsigned ints, zero on entry, left zeroed.  state: device RadixState.
+// hist: >= kRadixHistWords unsigned ints, zero on entry, left zeroed ([0, 2048): the per-launch
+// rounds; [2048, 4096): hist0, the round-0 counts of the init pass; [4096, ...): the cooperative
+// form's three rotating histograms and its grid barrier).  state: device RadixState.
+// All rounds run in ONE cooperative launch when the grid fits co-resident (CPSEL_RADIX_COOP=0: one
+// launch per round).
 // On completion state->value holds the element (as double).
 // vout/done/seq (optional): the last round also writes the value to *vout (mapped host memory)
 // and then sets *done = seq.
@@ -293,6 +298,7 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 // §8f-3 small arrays: x_(r) of x[0..m) (m <= exact_cluster_cap) by ONE 8-CTA cluster launch (exact
 // radix select in registers + DSMEM histograms); *vout = value (canonical +0), *bad_out = #NaN/Inf,
 // then `seq` published to *done.
+constexpr int kRadixHistWords = 4096 + 3 * 2048 + 64;
 uint64_t exact_cluster_cap(int dtype);
 cudaError_t launch_exact_cluster(int dtype, const void* x, uint64_t m, uint64_t r, double* vout,
                                  unsigned long long* bad_out, unsigned long long* done, unsigned long long seq,
