@@ -28,7 +28,7 @@ def short(n):
 inits = [i for i, ((_, n), _) in enumerate(items) if short(n).startswith(("init_seg_kernel", "init_kernel"))]
 # a selection starts at the sample kernels launched just before its init kernel
 first = inits[-nsel]
-while first > 0 and short(items[first - 1][0][1]).startswith("sample"):
+while first > 0 and short(items[first - 1][0][1]).startswith(("sample", "pool_gather")):
     first -= 1
 sel = items[first:]
 tot = sum(m["gpu__time_duration.sum"] for _, m in sel)
@@ -41,7 +41,7 @@ for (_, name), m in sel:
     a[2] += m.get("dram__bytes_read.sum", 0.0)
     a[3] += m.get("dram__bytes_write.sum", 0.0)
     a[4] = min(a[4], m["gpu__time_duration.sum"])
-print(f"| kernel | launches | total us | mean us | min us | DRAM read MB | DRAM write MB | share |")
+print("| kernel | launches | total us | mean us | min us | DRAM read MB | DRAM write MB | share |")
 print("|---|---|---|---|---|---|---|---|")
 for k, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     print(f"| `{k}` | {a[0]} | {a[1] * 1e6:.1f} | {a[1] / a[0] * 1e6:.1f} | {a[4] * 1e6:.1f} | {a[2] / 1e6:.1f} | "
