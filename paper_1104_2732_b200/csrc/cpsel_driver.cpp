@@ -2375,9 +2375,10 @@ cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_
   float* dk = d_dk ? d_dk : reinterpret_cast<float*>(base + off_dk);
   unsigned long long* bad = reinterpret_cast<unsigned long long*>(base + off_bad);
   CK(cudaMemsetAsync(bad, 0, 2 * sizeof *bad, ctx->stream));
+  CK(knn_check_f(d_f, n, bad + 1, ctx->stream));                         // NaN/Inf in f
   CK(knn_distances(d_X, d_Q, n, p, nq, D, bad, ctx->stream));            // 1. distances
   unsigned long long hbad[2] = {0, 0};
-  CK(cudaMemcpyAsync(hbad, bad, sizeof hbad[0], cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   if (hbad[0]) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf (or a distance overflows)");
   LmsReport rep{};
@@ -2385,10 +2386,9 @@ cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_
   if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a query");
   CK(e);
   if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf");
-  CK(knn_reduce(D, d_f, n, nq, k, dk, weighting, d_out, bad + 1, ctx->stream));  // 3. the rho reduction
-  CK(cudaMemcpyAsync(hbad + 1, bad + 1, sizeof hbad[1], cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
   if (hbad[1]) return fail(ctx, CPSEL_ENONFINITE, "f holds NaN or Inf");
+  CK(knn_reduce(D, d_f, n, nq, k, dk, weighting, d_out, ctx->stream));  // 3. the rho reduction
+  CK(cudaStreamSynchronize(ctx->stream));
   lms_info(info, rep, false);
   if (info) {
     info->launches += 2;

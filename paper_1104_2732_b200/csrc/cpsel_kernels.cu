@@ -2621,8 +2621,9 @@ __device__ void batch_sample_cuts(BatchState& st, unsigned* hist, const float* z
   unsigned out[3];
   block_radix_select<PER, 3>(key, hist, rk, out);
   if (threadIdx.x == 0) {
-    st.cut_lo = (float)from_key_f32(out[0]);
-    st.cut_hi = (float)from_key_f32(out[1]);
+    // R31: a cut whose sample rank falls off the sample opens to the largest finite float
+    st.cut_lo = ql < 0 ? -FLT_MAX : (float)from_key_f32(out[0]);
+    st.cut_hi = qh >= md - 1 ? FLT_MAX : (float)from_key_f32(out[1]);
     st.cut_mid = (float)from_key_f32(out[2]);
   }
   __syncthreads();
@@ -2868,6 +2869,8 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
             // midpoint
             const double tl = st.cut_lo, th = st.cut_hi;
             bool settled = false, mean_ok = false;
+            // (an open cut of an extreme rank, R31, lies outside the bracket with nothing between)
+            const bool lo_open = tl <= (double)st.yL && p.cA == 0;
             if (tl > (double)st.yL && tl < (double)st.yR) {
               const unsigned long long c_le = p.cA;
               if (c_le < k) {
@@ -2881,7 +2884,7 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
               const unsigned long long c_lt = p.cC;
               if (c_lt >= k) {
                 st.yR = (float)th; st.c_lt_R = c_lt; st.m = c_lt - st.c_le_L;
-                if ((double)st.yL == tl && st.cut_mid > st.yL && st.cut_mid < st.yR) {
+                if (((double)st.yL == tl || lo_open) && st.cut_mid > st.yL && st.cut_mid < st.yR) {
                   st.t = st.cut_mid;  // the sample's estimate of the target (R25)
                   mean_ok = true;
                 }
@@ -2892,7 +2895,9 @@ __global__ void __launch_bounds__(kBlock, 4) batched_select_kernel(BatchArgs a) 
             if (!mean_ok) st.t = 0.5 * (double)st.yL + 0.5 * (double)st.yR;
             if (!isfinite(st.t)) st.t = 0.5 * p.vmin + 0.5 * p.vmax;
             // the init pass already copied out ]t_lo, t_hi[: if that is the bracket, continue on it
-            if (st.phase == 0 && (double)st.yL == tl && (double)st.yR == th && st.m == p.pad2 && p.pad2 <= a.cap) {
+            const bool hi_open = th >= (double)st.yR && p.cC == n;
+            if (st.phase == 0 && ((double)st.yL == tl || lo_open) && ((double)st.yR == th || hi_open) &&
+                st.m == p.pad2 && p.pad2 <= a.cap) {
               st.cur = my0; st.n_cur = p.pad2; st.cur_buf = 0;
               st.D_lo = st.c_le_L; st.on_z = 1;
               if (st.m <= (unsigned long long)kBatchFinish) { st.k_r = k - st.c_le_L; st.phase = 2; }

@@ -12,8 +12,10 @@ constexpr double kKnnEps = 1e-12;   // inverse-distance weight 1/(d^2 + eps)
 // *bad += #non-finite distances
 cudaError_t knn_distances(const float* X, const float* Q, uint64_t n, uint32_t p, uint32_t nq, float* D,
                           unsigned long long* bad, cudaStream_t st);
-// out[j] = sum rho_i w_i f_i / sum rho_i w_i, rho = 1 below dk[j], a/b at it; *bad += #non-finite f
+// out[j] = sum rho_i w_i f_i / sum rho_i w_i, rho = 1 below dk[j], a/b at it
 cudaError_t knn_reduce(const float* D, const float* f, uint64_t n, uint32_t nq, uint64_t k, const float* dk,
-                       int weighting, float* out, unsigned long long* bad, cudaStream_t st);
+                       int weighting, float* out, cudaStream_t st);
+// *bad += #non-finite f_i
+cudaError_t knn_check_f(const float* f, uint64_t n, unsigned long long* bad, cudaStream_t st);
 
 }  // namespace cpsel
