@@ -65,6 +65,12 @@ struct cpsel_ctx {
   RadixState* h_radix = nullptr;
   DevPass* h_gather = nullptr;
   DevInit* h_gather_init = nullptr;
+  // sharded records published to mapped memory (gather_records): host view, device view, the flag
+  unsigned char* h_rec = nullptr;
+  unsigned char* d_rec = nullptr;
+  size_t rec_bytes = 0;
+  unsigned long long* h_rec_flag = nullptr;
+  unsigned long long* d_rec_flag = nullptr;
   // sharded sample cuts (R28): the pooled sample (every rank's share of evenly strided values), shard sizes
   void* d_pool = nullptr;
   unsigned long long* d_sizes = nullptr;     // [0] this rank's, [1..G] all ranks'
@@ -782,22 +788,15 @@ struct GpuBackend : Backend {
   cpsel_status select_on(const void* base, uint64_t m, uint64_t r, double* out, const SegEntry* tab = nullptr,
                          int side = 0) {
     CK(tic());
-    if (use_mail) {
-      const unsigned long long seq = ++ctx->seq;
-      CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
-                             &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, seq, tab, side, ctx->d_ticket));
-      CK(toc());
-      cpsel_status w = wait_mail(&ctx->mb->seq_radix, seq);
-      if (w != CPSEL_OK) return w;
-      *out = ctx->mb->radix_value;
-    } else {
-      CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream, nullptr, nullptr, 0,
-                             tab, side, ctx->d_ticket));
-      CK(toc());
-      CK(cudaMemcpyAsync(ctx->h_radix, ctx->d_radix, sizeof(RadixState), cudaMemcpyDeviceToHost, ctx->stream));
-      CK(cudaStreamSynchronize(ctx->stream));
-      *out = ctx->h_radix->value;
-    }
+    // the value comes back through the ctx's mapped mailbox (also on the sharded path: every rank's
+    // own select)
+    const unsigned long long seq = ++ctx->seq;
+    CK(launch_radix_select(dt, base, m, r, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
+                           &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, seq, tab, side, ctx->d_ticket));
+    CK(toc());
+    cpsel_status w = wait_mail(&ctx->mb->seq_radix, seq);
+    if (w != CPSEL_OK) return w;
+    *out = ctx->mb->radix_value;
     launches = dt == kF32 ? 3 : 6;
     scanned = m;
     return CPSEL_OK;
@@ -974,11 +973,18 @@ struct ShardedBackend : GpuBackend {
     if (m_) return fail(ctx, CPSEL_ENCCL, "%s: %s", #expr, m_);                  \
   } while (0)
 
-  // all-gather `bytes` per rank from d_src into d_all and bring the G records to h_all
+  // all-gather `bytes` per rank from d_src into d_all and bring the G records to h_all: published
+  // into mapped memory by a one-CTA kernel behind the collective, the host spins on its flag (no
+  // stream synchronisation per exchange)
   cpsel_status gather_records(const void* d_src, void* d_all, void* h_all, size_t bytes) {
     CM(comm().allgather(d_src, d_all, bytes, ctx->stream));
-    CK(cudaMemcpyAsync(h_all, d_all, (size_t)G() * bytes, cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
+    const size_t tot = (size_t)G() * bytes;
+    if (tot > ctx->rec_bytes) return fail(ctx, CPSEL_EINTERNAL, "record mailbox too small");
+    const unsigned long long seq = ++ctx->seq;
+    CK(launch_publish(d_all, ctx->d_rec, tot, ctx->d_rec_flag, seq, ctx->stream));
+    cpsel_status w = wait_mail(ctx->h_rec_flag, seq);
+    if (w != CPSEL_OK) return w;
+    memcpy(h_all, ctx->h_rec, tot);
     return CPSEL_OK;
   }
 
@@ -1967,7 +1973,7 @@ void cpsel_destroy(cpsel_ctx* ctx) {
       if (p) cudaFree(p);
     lms_free(ctx->lms);
     void* host[] = {ctx->h_pass, ctx->h_init, ctx->h_radix, ctx->h_gather, ctx->h_gather_init, ctx->mb,
-                    ctx->h_sizes};
+                    ctx->h_sizes, ctx->h_rec};
     for (void* p : host)
       if (p) cudaFreeHost(p);
     for (cudaGraphExec_t g : ctx->kgraph)
@@ -2129,6 +2135,9 @@ static cpsel_status comm_buffers(cpsel_ctx* ctx, int world) {
   if (ctx->d_pool) cudaFree(ctx->d_pool);
   if (ctx->d_sizes) cudaFree(ctx->d_sizes);
   if (ctx->h_sizes) cudaFreeHost(ctx->h_sizes);
+  if (ctx->h_rec) cudaFreeHost(ctx->h_rec);
+  ctx->h_rec = ctx->d_rec = nullptr;
+  ctx->h_rec_flag = ctx->d_rec_flag = nullptr;
   ctx->d_gather = nullptr; ctx->d_gather_init = nullptr; ctx->h_gather = nullptr; ctx->h_gather_init = nullptr;
   ctx->d_pool = nullptr; ctx->d_sizes = nullptr; ctx->h_sizes = nullptr;
   CK(cudaMalloc(&ctx->d_gather, world * sizeof(DevPass)));
@@ -2138,6 +2147,12 @@ static cpsel_status comm_buffers(cpsel_ctx* ctx, int world) {
   CK(cudaMalloc(&ctx->d_pool, std::max(pool_sample_size(kF32, false) * 4, pool_sample_size(kF64, false) * 8)));
   CK(cudaMalloc(&ctx->d_sizes, (size_t)(world + 1) * sizeof(unsigned long long)));
   CK(cudaHostAlloc(&ctx->h_sizes, (size_t)(world + 1) * sizeof(unsigned long long), cudaHostAllocDefault));
+  ctx->rec_bytes = (size_t)world * std::max(sizeof(DevPass), sizeof(DevInit));
+  CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_rec), ctx->rec_bytes + 64, cudaHostAllocMapped));
+  memset(ctx->h_rec, 0, ctx->rec_bytes + 64);
+  CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->d_rec), ctx->h_rec, 0));
+  ctx->h_rec_flag = reinterpret_cast<unsigned long long*>(ctx->h_rec + ctx->rec_bytes);
+  ctx->d_rec_flag = reinterpret_cast<unsigned long long*>(ctx->d_rec + ctx->rec_bytes);
   return CPSEL_OK;
 }
 

@@ -3512,6 +3512,22 @@ cudaError_t kelley_graph_build(int dtype, const LaunchShape& s, KelleyState* ks,
   return kelley_graph_t<double>(s, ks, partials, ticket, cursors, rstate, hist, out);
 }
 
+// A device buffer published to mapped host memory, then `seq` to *flag (the host spins on it instead
+// of a stream synchronisation): the sharded path's all-gathered records.
+__global__ void publish_kernel(const unsigned long long* __restrict__ src, unsigned long long* dst, uint32_t words,
+                               unsigned long long* flag, unsigned long long seq) {
+  for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) publish_done(flag, seq);
+}
+cudaError_t launch_publish(const void* src, void* dst_mapped, size_t bytes, unsigned long long* flag,
+                           unsigned long long seq, cudaStream_t st) {
+  publish_kernel<<<1, 256, 0, st>>>(static_cast<const unsigned long long*>(src),
+                                    static_cast<unsigned long long*>(dst_mapped), (uint32_t)(bytes / 8), flag, seq);
+  return cudaGetLastError();
+}
+
 int seg_total_warps(int dtype, const LaunchShape& s) { return s.grid_seg[dtype] * kWarps; }
 
 cudaError_t launch_init_seg(int dtype, const InitArgs& ia, const SegArgs& a, const LaunchShape& s, cudaStream_t st,

@@ -276,6 +276,10 @@ cudaError_t launch_pool_pick(int dtype, const void* pooled, uint64_t ms, uint64_
                              cudaStream_t st, bool small, bool allow_open = true);
 cudaError_t launch_seg_pack(int dtype, const void* base, const SegEntry* tab, int side, int Wtot, void* out,
                             cudaStream_t st);
+// bytes (a multiple of 8) of device src copied to mapped host memory (device view dst_mapped), then
+// seq published to *flag (mapped): the host spins on the flag instead of synchronising the stream
+cudaError_t launch_publish(const void* src, void* dst_mapped, size_t bytes, unsigned long long* flag,
+                           unsigned long long seq, cudaStream_t st);
 
 cudaError_t launch_init(int dtype, const InitArgs& a, const LaunchShape& s, cudaStream_t st, bool checked);
 // t0[0], t0[1] <- the sample quantiles bracketing rank k (1024 strided samples of x, one CTA)
