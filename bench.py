@@ -251,7 +251,25 @@ def kelley_side(cp, torch, datagen, dev, dists, log2n, peak, reps=3):
                           "select": info2["kernel_ms_select"]},
             "classes": trace_classes(rows, n, 4, peak)}
         del x
-    cp.set_config(dev.index, record_timing=0, init_cut=1, pass_cuts=1, objective=0)
+    # the paper's outlier claim (P:L413 vs P:L416, Fig. 4): 100 values of 1e3 / 1e9 among uniform
+    # data, the cutting plane against the bisection comparison driver (driver=1)
+    import datagen as dg
+    x = dg.make("uniform", n, "f32", device=dev)
+    pos = torch.randperm(n, generator=torch.Generator().manual_seed(dg.SEED))[:100].to(dev)
+    out["outliers"] = {}
+    for mag in (1e3, 1e9):
+        x[pos] = mag
+        for name, drv in (("kelley", 0), ("bisection", 1)):
+            cp.set_config(dev.index, record_timing=0, driver=drv, **cfg)
+            cp.select_kth(x, k)
+            e0, e1 = _ev(torch)
+            e0.record()
+            v, info = cp.select_kth(x, k, return_info=True)
+            e1.record()
+            torch.cuda.synchronize()
+            out["outliers"][f"{name}/{mag:g}"] = {"passes": info["passes"], "ms": e0.elapsed_time(e1)}
+    del x
+    cp.set_config(dev.index, record_timing=0, init_cut=1, pass_cuts=1, objective=0, driver=0)
     torch.cuda.empty_cache()
     out["elements_per_s"] = len(dists) * n / (tot_ms / 1e3)
     out["ms_per_selection"] = tot_ms / len(dists)

@@ -86,6 +86,11 @@ typedef struct {
                                 measured on B200, a WHILE iteration costs ~9.7 us of device-side
                                 relaunch, more than the mailbox round trip (+35 us per selection at
                                 2^20..2^27, +2% at 2^30) */
+  int32_t driver;            /* 0: Kelley's cutting plane (Algorithm 1, the method).  1: bisection, the
+                                paper's comparison: t = (y_L + y_R)/2 in value, the
+                                same passes, exact rank test and finish; no R26 cut passes, no
+                                ordered-key safeguard (its pass count grows with log2 of the data
+                                range, P:L413 — the outlier-sensitivity demonstration).  Default 0 */
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -144,7 +149,8 @@ typedef struct {
   uint64_t scanned;       /* elements this pass read (x, or the compacted bracket) */
   uint64_t written;       /* elements this pass wrote (compaction of both bracket halves) */
   uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard,
-                             2 the init pass's extra cut (R23) */
+                             2 the init pass's extra cut (R23), 3 a two-cut pass (R26), 4 a step of
+                             the bisection driver (driver = 1) */
   uint32_t compacted;     /* 1 if this pass also wrote z */
   double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
 } cpsel_trace_row;

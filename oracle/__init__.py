@@ -303,6 +303,42 @@ def cutting_plane(x, k: int, maxit: int = 64, z_cap: int = 0, tol_f: float | Non
             "trace": trace, "y_L": yL, "y_R": yR, "z_count": z_count, "exit": exit_reason}
 
 
+def bisection(x, k: int, maxit: int = 400, z_cap: int = 0):
+    """The paper's bisection comparison ("we adapted the classical bisection method", P:L204:
+    "methods based on solving 0 in g(y)"): from [y_L, y_R] = [x_(1), x_(n)], t = (y_L + y_R)/2 in
+    double, rounded to the data's dtype; 0 in dF_k(t) (c_lt < k <= c_le) -> t; dF_k(t) < 0 (c_le < k)
+    -> y_L <- t, else y_R <- t; until the bracket interior holds <= z_cap elements, then the hybrid
+    finish.  Its iteration count grows like log2 of the data range.
+    Returns dict(value, iterations, trace=[(t, c_lt, c_eq, interior)])."""
+    x = _as_array(x)
+    n = check_input(x, k)
+    rec = init_record(x)
+    if k <= rec["cnt_min"]:
+        return {"value": rec["min"], "iterations": 0, "trace": []}
+    if k > n - rec["cnt_max"]:
+        return {"value": rec["max"], "iterations": 0, "trace": []}
+    yL, yR = float(rec["min"]), float(rec["max"])
+    c_le_L, c_lt_R = rec["cnt_min"], n - rec["cnt_max"]
+    trace = []
+    for it in range(1, maxit + 1):
+        t = float(x.dtype.type(0.5 * yL + 0.5 * yR))
+        if not (yL < t < yR):  # adjacent floats: nothing strictly inside, the finish decides
+            break
+        c_lt, c_eq = rank_counts(x, t)
+        if c_lt < k <= c_lt + c_eq:
+            trace.append((t, c_lt, c_eq, 0))
+            return {"value": canonical(x.dtype.type(t)), "iterations": it, "trace": trace}
+        if c_lt + c_eq < k:
+            yL, c_le_L = t, c_lt + c_eq
+        else:
+            yR, c_lt_R = t, c_lt
+        trace.append((t, c_lt, c_eq, c_lt_R - c_le_L))
+        if c_lt_R - c_le_L <= z_cap:
+            break
+    value, _ = hybrid_finish(x, k, yL, yR)
+    return {"value": value, "iterations": it, "trace": trace}
+
+
 def eval_at(x, k: int, t, y_lo, y_hi):
     """Replay hook: one pass at t (pass_stats) plus F_k(t) and dF_k(t) — compared against the
     GPU's cpsel_eval / trace at identical t."""

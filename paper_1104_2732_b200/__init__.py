@@ -39,7 +39,8 @@ class Config(C.Structure):
                 ("max_iters", C.c_uint32),
                 ("force_cp", C.c_int32), ("record_trace", C.c_int32), ("record_timing", C.c_int32),
                 ("init_cut", C.c_int32), ("objective", C.c_int32),
-                ("pass_cuts", C.c_int32), ("lms_fused", C.c_int32), ("device_loop", C.c_int32)]
+                ("pass_cuts", C.c_int32), ("lms_fused", C.c_int32), ("device_loop", C.c_int32),
+                ("driver", C.c_int32)]
 
 
 class Info(C.Structure):

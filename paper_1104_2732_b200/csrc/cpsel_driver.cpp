@@ -1549,7 +1549,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     // §8f-3: once no R26 cut pass can follow (pass_cuts off, objective on, or the cuts stalled), the
     // remaining Kelley passes and the exact finish run on the device as one graph launch; the step
     // kernel there is this loop's Kelley step (same iterates, same decisions, same trace rows)
-    if (cfg.device_loop && be.has_device_loop() &&
+    if (cfg.device_loop && cfg.driver == 0 && be.has_device_loop() &&
         (!cfg.pass_cuts || cfg.objective || !be.has_cut_pass() || cuts_stalled)) {
       Backend::LoopIn li{};
       li.yL = yL; li.yR = yR; li.t = t; li.N_L = (double)N_L; li.P_R = (double)P_R;
@@ -1587,8 +1587,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     // around the local target rank; the copy keeps only ]t_a, t_b[ (~10% of the array) instead of
     // both halves of a Kelley split.  Not with objective=1 (F at the sample cuts would need two
     // more sums per element).
-    if (cfg.pass_cuts && !cfg.objective && on_z && exact && !bisect && !cuts_stalled && m > select_cap &&
-        be.has_cut_pass()) {
+    if (cfg.pass_cuts && !cfg.objective && cfg.driver == 0 && on_z && exact && !bisect && !cuts_stalled &&
+        m > select_cap && be.has_cut_pass()) {
       const uint64_t m_before = m;
       Backend::CutResult cr{};
       // dense output (selectable right away) when the expected copy (~2-4% of m) surely fits; a
@@ -1669,7 +1669,10 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       continue;
     }
     uint32_t kind = 0;
-    if (bisect) {
+    if (cfg.driver == 1) {  // the bisection comparison driver: the bracket's value midpoint
+      t = 0.5 * yL + 0.5 * yR;
+      kind = 4;
+    } else if (bisect) {
       t = key_mid(yL, yR, dt);
       kind = 1;
       inf.fallback_steps++;
@@ -1760,8 +1763,11 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       exact = true;
     }
     // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
-    // ordered-key bisection until progress resumes (bounds the pass count on any input)
-    if (free_step) {
+    // ordered-key bisection until progress resumes (bounds the pass count on any input); not for
+    // the bisection driver, whose slow progress on wide data is what it demonstrates
+    if (cfg.driver == 1) {
+      free_step = false;
+    } else if (free_step) {
       free_step = false;
     } else if (m > m_old - m_old / 8) {
       if (++slow >= 2) bisect = true;
@@ -1994,6 +2000,7 @@ const char* cpsel_last_error(const cpsel_ctx* ctx) { return ctx ? ctx->err.c_str
 cpsel_status cpsel_set_config(cpsel_ctx* ctx, const cpsel_config* cfg) {
   if (!ctx || !cfg) return CPSEL_EINVAL;
   if (cfg->max_iters == 0) return fail(ctx, CPSEL_EINVAL, "max_iters must be >= 1");
+  if (cfg->driver != 0 && cfg->driver != 1) return fail(ctx, CPSEL_EINVAL, "driver must be 0 or 1");
   ctx->cfg = *cfg;
   return CPSEL_OK;
 }

@@ -514,3 +514,33 @@ def test_device_loop_matches_host_loop(cp, dtype, dist):
                 if cfg["objective"]:
                     assert b["F"] == pytest.approx(a["F"], rel=1e-12)
             assert i1["launches"] < i0["launches"] + 4      # one graph launch for the whole loop
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_bisection_driver_matches_oracle(cp, dtype):
+    """driver=1 (the paper's bisection comparison): the same element as the oracle, its
+    iterates are exactly the oracle's bisection iterates (value midpoints rounded to the dtype) with
+    the same counts; and the paper's outlier claim (P:L413 vs P:L416): with 1e9 outliers bisection
+    needs >= 15 more passes than with 1e3, the cutting plane at most 2 more."""
+    import torch
+    n = 1_000_003
+    base = datagen.make("uniform", n, dtype)
+    passes = {}
+    for mag in (1e3, 1e9):
+        x = datagen.inject_outliers(base.copy(), 100, mag)
+        xd = tdev(x)
+        k = O.median_rank(n)
+        ref = O.bisection(x, k, z_cap=0)
+        for drv in (1, 0):
+            cp.set_config(driver=drv, init_cut=0, pass_cuts=0)
+            v, info = cp.select_kth(xd, k, return_info=True)
+            tr = cp.get_trace()
+            cp.set_config(driver=0, init_cut=1, pass_cuts=1)
+            assert v == canon(float(np.sort(x)[k - 1])), (mag, drv)
+            passes[(mag, drv)] = info["passes"]
+            if drv == 1:
+                assert len(tr) <= len(ref["trace"]) and all(r["kind"] == 4 for r in tr)
+                for r, (t, c_lt, c_eq, interior) in zip(tr, ref["trace"]):
+                    assert r["t"] == t and (r["c_lt"], r["c_eq"]) == (c_lt, c_eq), (r, t, c_lt, c_eq)
+    assert passes[(1e9, 1)] - passes[(1e3, 1)] >= 15, passes
+    assert passes[(1e9, 0)] - passes[(1e3, 0)] <= 2, passes

@@ -593,3 +593,22 @@ def test_knn_ties_share_weight_as_the_average_over_tie_choices():
         a = k - len(below)
         means = [Fraction(sum(int(f[i]) for i in below + list(c)), k) for c in itertools.combinations(tied, a)]
         assert got[0] == pytest.approx(float(sum(means) / len(means)), rel=1e-15)
+
+
+def test_bisection_result_and_outlier_sensitivity():
+    """oracle.bisection (the paper's comparison driver): the exact element by the definition, and the
+    paper's claim P:L413 — its iteration count grows with log2 of the data range (outliers 1e3 ->
+    1e9 add ~log2(1e6) ~ 20 iterations) while Kelley's stays within 2 (Fig. 4)."""
+    rng = np.random.default_rng(12)
+    x = rng.random(20001)
+    for k in (1, 7, 10001, 20000, 20001):
+        assert O.bisection(x, k, z_cap=0)["value"] == np.sort(x)[k - 1]
+    its, cps = [], []
+    for mag in (1e3, 1e9):
+        y = x.copy()
+        y[rng.choice(y.size, 20, replace=False)] = mag
+        its.append(O.bisection(y, O.median_rank(y.size), z_cap=64)["iterations"])
+        cps.append(O.cutting_plane(y, O.median_rank(y.size), z_cap=64)["iterations"])
+        assert O.bisection(y, O.median_rank(y.size), z_cap=64)["value"] == np.sort(y)[O.median_rank(y.size) - 1]
+    assert its[1] - its[0] >= 15, its
+    assert abs(cps[1] - cps[0]) <= 2, cps
