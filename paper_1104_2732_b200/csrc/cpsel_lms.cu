@@ -274,11 +274,11 @@ constexpr int kFuseCuts = 0, kFuseStore = 1, kFuseLts = 2;
 constexpr int FN = 256;                    // rows per tile (TMEM columns per accumulator)
 constexpr int kFEpiWarps = 16;             // 4 per TMEM lane quarter, each on 64 of the 256 rows
 constexpr int kFYWarp = 2 + kFEpiWarps;    // the warp that stages y for each accumulator stage
-constexpr int kFStages = 3;                // operand (Theta + X tile) stages in shared memory
+constexpr int kFStages = 2;                // operand (Theta + X tile) stages in shared memory
 constexpr int kFThreads = 32 * (3 + kFEpiWarps);
 constexpr int kFRows = FN / 4;             // rows per epilogue warp per tile
-constexpr int kRing = 32;                  // staging slots per epilogue thread
-constexpr int kFlush = 16;                 // elements per flush
+constexpr int kRing = 48;                  // staging slots per epilogue thread (32 + up to 15 pending + 1 half)
+constexpr int kFlush = 32;                 // elements per flush (one 128-byte store of the warp)
 constexpr uint32_t kSlot = 4;              // a thread's slots are consecutive words ...
 constexpr uint32_t kLaneStage = 4 * (kRing + 1);  // ... skewed by one word per thread (no bank conflicts)
 
@@ -506,37 +506,28 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
                 }
               }
               // warp-cooperative flush of every thread holding >= kFlush staged elements (at most
-              // 15 + 16 < kRing pending): each writes 16 to its column's copy as one coalesced
-              // 64-byte store of 16 lanes, and moves the rest to the front of its slots
+              // 31 + 16 < kRing pending): each owner's 32 go to its column's copy as ONE coalesced
+              // 128-byte store of the warp, the rest moves to the front of its slots.  (Two operand
+              // stages instead of three buy the larger ring: half as many flush events as with 16.)
               const bool need = ta - base_sa >= kFlush * kSlot;
               unsigned fm = __ballot_sync(0xffffffffu, need);
               if (fm) {
                 __syncwarp();  // every lane's staged stores visible to the warp before the reads
                 unsigned long long pos = 0;
                 if (need) pos = atomicAdd(a.cursor + j, (unsigned long long)kFlush);
-                while (fm) {  // two threads per round: half-warp h serves owner h
-                  const int A = __ffs(fm) - 1;
+                while (fm) {
+                  const int src = __ffs(fm) - 1;
                   fm &= fm - 1;
-                  int Bo = -1;
-                  if (fm) {
-                    Bo = __ffs(fm) - 1;
-                    fm &= fm - 1;
-                  }
-                  const int l16 = lane & 15;
-                  const int owner = (lane < 16) ? A : Bo;
-                  const int src = owner < 0 ? A : owner;
                   const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, src);
                   const uint32_t cnt = (__shfl_sync(0xffffffffu, ta, src) - lb) / kSlot;
                   const unsigned long long pl = __shfl_sync(0xffffffffu, pos, src);
-                  float v = 0.f, v2 = 0.f;
-                  const bool mv = owner >= 0 && (uint32_t)(kFlush + l16) < cnt;
-                  if (owner >= 0) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + l16 * kSlot));
-                  if (mv) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v2) : "r"(lb + (kFlush + l16) * kSlot));
+                  float v, v2 = 0.f;
+                  const bool mv = (uint32_t)(kFlush + lane) < cnt;
+                  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + lane * kSlot));
+                  if (mv) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v2) : "r"(lb + (kFlush + lane) * kSlot));
                   __syncwarp();
-                  if (owner >= 0) {
-                    if (pl + l16 < a.zcap) a.z[(size_t)(j - lane + src) * a.zcap + pl + l16] = v;
-                    if (mv) asm volatile("st.shared.f32 [%0], %1;" ::"r"(lb + l16 * kSlot), "f"(v2));
-                  }
+                  if (pl + lane < a.zcap) a.z[(size_t)(j - lane + src) * a.zcap + pl + lane] = v;
+                  if (mv) asm volatile("st.shared.f32 [%0], %1;" ::"r"(lb + lane * kSlot), "f"(v2));
                   __syncwarp();
                 }
                 if (need) ta -= kFlush * kSlot;
@@ -598,10 +589,10 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
           const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, L);
           const uint32_t cl = __shfl_sync(0xffffffffu, cnt, L);
           const unsigned long long pl = __shfl_sync(0xffffffffu, pos, L);
-          if ((uint32_t)lane < cl) {
+          for (uint32_t o = lane; o < cl; o += 32) {  // (up to kRing - 1 pending)
             float v;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + lane * kSlot));
-            if (pl + lane < a.zcap) a.z[(size_t)(j - lane + L) * a.zcap + pl + lane] = v;
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + o * kSlot));
+            if (pl + o < a.zcap) a.z[(size_t)(j - lane + L) * a.zcap + pl + o] = v;
           }
         }
         __syncwarp();
