@@ -55,4 +55,37 @@ S = cp.lms_residuals(Xd, yd, thd).cpu().numpy()
 assert all(got[j] == O.order_statistic(S[j], O.median_rank(X.shape[0])) for j in range(140))
 F, mth = cp.lts_objective(Xd, yd, thd, (X.shape[0] + 10) // 2)
 torch.cuda.synchronize()
+# round-2 additions: the cooperative radix select (every path above), the device-resident Kelley
+# loop (CUDA graph), the bisection driver, kNN, and the loopback-sharded path at G = 2
+x = datagen.make("mix2", n, "f32")
+xd = torch.from_numpy(x).cuda()
+for cfg in (dict(init_cut=0, pass_cuts=0, objective=1, device_loop=1), dict(init_cut=0, pass_cuts=0, driver=1)):
+    cp.set_config(**cfg)
+    assert cp.select_kth(xd, 777) == float(O.order_statistic(x, 777)), cfg
+    cp.set_config(init_cut=1, pass_cuts=1, objective=0, device_loop=0, driver=0)
+rng = np.random.default_rng(1)
+Xk = rng.standard_normal((5000, 3)).astype(np.float32)
+fk = rng.standard_normal(5000).astype(np.float32)
+Qk = rng.standard_normal((20, 3)).astype(np.float32)
+out, dk = cp.knn_regress(*(torch.from_numpy(a).cuda() for a in (Xk, fk, Qk)), 9, return_dk=True)
+assert np.array_equal(dk.cpu().numpy(), O.knn_regress(Xk, fk, Qk, 9)[1])
+import threading
+grp = cp.LoopbackGroup(2)
+res = [None, None]
+xs = datagen.make("uniform", 9_000_001, "f32")
+xsd = torch.from_numpy(xs).cuda()
+torch.cuda.synchronize()
+
+
+def rank(g):
+    with torch.cuda.stream(torch.cuda.Stream()):
+        cp.comm_init_loopback(grp, g, 0)
+        res[g] = cp.select_kth_sharded(xsd[g * 4_000_000:(g + 1) * 4_000_000] if g == 0 else xsd[4_000_000:], 4_500_001)
+
+
+th_ = [threading.Thread(target=rank, args=(g,)) for g in range(2)]
+[t.start() for t in th_]
+[t.join() for t in th_]
+assert res[0] == res[1] == float(O.order_statistic(xs, 4_500_001)), res
+torch.cuda.synchronize()
 print("sanitize workload ok")
