@@ -373,18 +373,25 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
 
   if (warp == kFYWarp) {
     // ---------------- y stager: the tile's 256 y values into ybuf[s] once the epilogue released
-    //                  accumulator stage s (the epilogue reads them as shared-memory broadcasts)
-    if (lane == 0) {
-      uint32_t it = 0;
-      for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
-        const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
-        for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
-          const uint32_t s = it & 1, ph = (it >> 1) & 1;
-          mbar_wait_sleep(&tempty[s], ph ^ 1);
-          mbar_expect_tx(&yfull[s], FN * 4);
-          bulk_g2s(ybuf + s * FN, a.y + ((size_t)ct * a.b_ct_stride + rt) * FN, FN * 4, &yfull[s]);
-        }
+    //                  accumulator stage s (the epilogue reads them as shared-memory broadcasts).
+    //                  A plain warp copy (1 KB per tile; 2 x 16 B per lane), released to the
+    //                  epilogue by an mbarrier arrive: ordinary generic-proxy accesses ordered by
+    //                  the stage barriers (a bulk copy here was an async-proxy write racecheck
+    //                  cannot see ordered behind the epilogue's reads)
+    uint32_t it = 0;
+    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
+      const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
+      for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
+        const uint32_t s = it & 1, ph = (it >> 1) & 1;
+        const float4* src = reinterpret_cast<const float4*>(a.y + ((size_t)ct * a.b_ct_stride + rt) * FN);
+        const float4 y0 = __ldg(src + lane), y1 = __ldg(src + 32 + lane);  // loads ahead of the wait
+        mbar_wait_sleep(&tempty[s], ph ^ 1);
+        float4* dst = reinterpret_cast<float4*>(ybuf + s * FN);
+        dst[lane] = y0;
+        dst[32 + lane] = y1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&yfull[s]);
       }
     }
   } else if (warp == 0) {
@@ -569,7 +576,6 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
           }
         }
         asm volatile("tcgen05.fence::before_thread_sync;");
-        fence_proxy_async_smem();  // ybuf[s] reads ordered before the bulk copy that refills it
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[s]);
       }
