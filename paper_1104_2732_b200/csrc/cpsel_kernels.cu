@@ -1704,22 +1704,25 @@ __device__ __forceinline__ void coop_barrier(unsigned* bar, unsigned nblocks) {
   }
   __syncthreads();
 }
-template <typename T, bool SEG>
-__global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_constant__ CoopArgs c) {
+// NT threads per CTA: 256 (4 CTAs per SM, the segmented grid's shape) or 1024 (one CTA per SM: a
+// quarter of the CTAs to merge histograms and to cross the grid barrier, every warp still on one run)
+template <typename T, bool SEG, int NT>
+__global__ void __launch_bounds__(NT, 1024 / NT) radix_coop_kernel(const __grid_constant__ CoopArgs c) {
+  constexpr int NW = NT / 32, BPT = 2048 / NT;  // warps, bins per thread of the pick
   const RadixArgs& a = c.a;
   pdl_wait();  // the init's copy, its round-0 counts and the chain decision
   uint64_t rank0 = a.r;
   if (a.chain) {
     if (!a.chain->ok[1]) {  // skipped (uniformly): the init's round-0 counts must still be cleared
       if (a.hist0 && blockIdx.x == 0)
-        for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
+        for (int i = threadIdx.x; i < 2048; i += NT) a.hist0[i] = 0u;
       return;
     }
     rank0 = a.chain->r[1];
   }
   __shared__ unsigned sh[2048];
   __shared__ unsigned long long s_prefix, s_mask, s_rank;
-  __shared__ unsigned wsum[kWarps];
+  __shared__ unsigned wsum[NW];
   __shared__ bool s_last;
   __shared__ int s_shift[6], s_bits[6];
   if (threadIdx.x < 6) {
@@ -1731,10 +1734,10 @@ __global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_cons
   // 8 bins per thread, block scan of the thread totals; the finder updates the shared prefix
   auto pick = [&](const unsigned* h, int shift, int bits, bool last) {
     const int nb = 1 << bits;
-    unsigned hv[8], tsum = 0;
+    unsigned hv[BPT], tsum = 0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int b = threadIdx.x * 8 + j;
+    for (int j = 0; j < BPT; ++j) {
+      const int b = threadIdx.x * BPT + j;
       hv[j] = b < nb ? __ldcg(&h[b]) : 0u;
       tsum += hv[j];
     }
@@ -1751,9 +1754,9 @@ __global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_cons
     for (int q = 0; q < w; ++q) wbase += wsum[q];
     unsigned long long before = wbase + incl - tsum;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < BPT; ++j) {
       if (before < r && r <= before + hv[j]) {
-        const int digit = threadIdx.x * 8 + j;
+        const int digit = threadIdx.x * BPT + j;
         const unsigned long long prefix = pf | ((unsigned long long)digit << shift);
         s_prefix = prefix;
         s_mask = mk | ((unsigned long long)(nb - 1) << shift);
@@ -1783,7 +1786,7 @@ __global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_cons
   for (int ri = c.first_round; ri < c.plan.n; ++ri) {
     const int shift = s_shift[ri], bits = s_bits[ri];
     unsigned* G = c.g3 + 2048 * (ri % 3);
-    for (int i = threadIdx.x; i < 2048; i += kBlock) sh[i] = 0;
+    for (int i = threadIdx.x; i < 2048; i += NT) sh[i] = 0;
     __syncthreads();
     if (SEG) {
       RadixSegFn f;
@@ -1793,7 +1796,7 @@ __global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_cons
       f.mask = s_mask;
       f.shift = shift;
       f.dmask = (1u << bits) - 1u;
-      for (uint64_t W = (uint64_t)blockIdx.x * kWarps + w; W < (uint64_t)a.Wtot; W += (uint64_t)gridDim.x * kWarps) {
+      for (uint64_t W = (uint64_t)blockIdx.x * NW + w; W < (uint64_t)a.Wtot; W += (uint64_t)gridDim.x * NW) {
         const SegEntry e = a.tab[W];
         seg_run_pipe<T>(f, static_cast<const T*>(a.z) + e.off[a.side], e.cnt[a.side]);
       }
@@ -1803,10 +1806,10 @@ __global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_cons
       stream_array<T, 2>(static_cast<const T*>(a.z), a.m, hf, blockIdx.x, gridDim.x);
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 2048; i += kBlock)
+    for (int i = threadIdx.x; i < 2048; i += NT)
       if (sh[i]) atomicAdd(&G[i], sh[i]);
     if (blockIdx.x == 0)  // next round's buffer: last read two barriers ago, added to only after this one
-      for (int i = threadIdx.x; i < 2048; i += kBlock) c.g3[2048 * ((ri + 1) % 3) + i] = 0u;
+      for (int i = threadIdx.x; i < 2048; i += NT) c.g3[2048 * ((ri + 1) % 3) + i] = 0u;
     coop_barrier(c.bar, gridDim.x);
     pick(G, shift, bits, ri == c.plan.n - 1);
   }
@@ -1817,9 +1820,9 @@ __global__ void __launch_bounds__(kBlock, 4) radix_coop_kernel(const __grid_cons
   }
   __syncthreads();
   if (!s_last) return;
-  for (int i = threadIdx.x; i < 3 * 2048; i += kBlock) c.g3[i] = 0u;
+  for (int i = threadIdx.x; i < 3 * 2048; i += NT) c.g3[i] = 0u;
   if (a.hist0)
-    for (int i = threadIdx.x; i < 2048; i += kBlock) a.hist0[i] = 0u;
+    for (int i = threadIdx.x; i < 2048; i += NT) a.hist0[i] = 0u;
   if (threadIdx.x == 0) c.bar[2] = 0u;
 }
 
@@ -3309,12 +3312,14 @@ cudaError_t query_shapes(int device, LaunchShape* s) {
 #undef OCC
   {
     int cb = 0;
-#define COOP(DT, T, SEGV)                                                                                  \
-  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cb, radix_coop_kernel<T, SEGV>, kBlock, 0)) != \
-      cudaSuccess)                                                                                        \
-    return e;                                                                                             \
-  s->coop_max[DT][SEGV ? 1 : 0] = s->num_sms * cb;
-    COOP(kF32, float, false) COOP(kF32, float, true) COOP(kF64, double, false) COOP(kF64, double, true)
+#define COOP(DT, T, SEGV, NTV)                                                                                      \
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cb, radix_coop_kernel<T, SEGV, NTV>, NTV, 0)) !=       \
+      cudaSuccess)                                                                                                 \
+    return e;                                                                                                      \
+  s->coop_max[DT][SEGV ? 1 : 0][NTV == 1024 ? 1 : 0] = s->num_sms * cb;
+    COOP(kF32, float, false, 256) COOP(kF32, float, true, 256) COOP(kF64, double, false, 256)
+    COOP(kF64, double, true, 256) COOP(kF32, float, false, 1024) COOP(kF32, float, true, 1024)
+    COOP(kF64, double, false, 1024) COOP(kF64, double, true, 1024)
 #undef COOP
   }
   if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, seg_pass_kernel<float, false>, kBlock, 0)) != cudaSuccess) return e;
@@ -4154,8 +4159,14 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
   const int* plan = dtype == kF32 ? plan32 : plan64;
   {  // all rounds in one cooperative launch, if the grid fits co-resident
     static const bool coop_on = !(getenv("CPSEL_RADIX_COOP") && getenv("CPSEL_RADIX_COOP")[0] == '0');
-    const int grid = tab ? s.grid_seg[dtype] : clamp_grid(s.grid_hist[dtype], m, kRadixPerCta);
-    if (coop_on && grid <= s.coop_max[dtype][tab ? 1 : 0]) {
+    // 1024-thread CTAs, one per SM (CPSEL_RADIX_NT=256: four 256-thread CTAs per SM)
+    // (dense input: stream_array's lane arithmetic assumes kBlock threads, so always 256)
+    static const int nt_seg = (getenv("CPSEL_RADIX_NT") && atoi(getenv("CPSEL_RADIX_NT")) == 256) ? 256 : 1024;
+    const int nt = tab ? nt_seg : kBlock;
+    const int per_cta = nt / kBlock;  // 256-thread CTAs' worth of warps per CTA
+    const int seg_grid = (s.grid_seg[dtype] + per_cta - 1) / per_cta;
+    const int grid = tab ? seg_grid : clamp_grid(s.grid_hist[dtype] / per_cta, m, kRadixPerCta * per_cta);
+    if (coop_on && grid <= s.coop_max[dtype][tab ? 1 : 0][nt == 1024 ? 1 : 0]) {
       CoopArgs c{};
       RadixArgs& a = c.a;
       a.z = z; a.m = m; a.tab = tab; a.side = side; a.st = state; a.hist = hist; a.ticket = ticket;
@@ -4172,7 +4183,7 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
       c.bar = hist + 4096 + 3 * 2048;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(kBlock);
+      cfg.blockDim = dim3(nt);
       cfg.stream = st;
       cudaLaunchAttribute attr[2];
       attr[0].id = cudaLaunchAttributeCooperative;
@@ -4182,12 +4193,13 @@ cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r
       cfg.attrs = attr;
       cfg.numAttrs = 2;
       cudaError_t e;
+#define COOPL(T, SEGV) (nt == 1024 ? cudaLaunchKernelEx(&cfg, radix_coop_kernel<T, SEGV, 1024>, c) \
+                                   : cudaLaunchKernelEx(&cfg, radix_coop_kernel<T, SEGV, 256>, c))
       if (dtype == kF32)
-        e = tab ? cudaLaunchKernelEx(&cfg, radix_coop_kernel<float, true>, c)
-                : cudaLaunchKernelEx(&cfg, radix_coop_kernel<float, false>, c);
+        e = tab ? COOPL(float, true) : COOPL(float, false);
       else
-        e = tab ? cudaLaunchKernelEx(&cfg, radix_coop_kernel<double, true>, c)
-                : cudaLaunchKernelEx(&cfg, radix_coop_kernel<double, false>, c);
+        e = tab ? COOPL(double, true) : COOPL(double, false);
+#undef COOPL
       return e;
     }
   }

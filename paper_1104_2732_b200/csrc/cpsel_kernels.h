@@ -153,7 +153,7 @@ struct LaunchShape {
   int grid_init[2];
   int grid_hist[2];
   int grid_seg[2];
-  int coop_max[2][2];    // [dtype][segmented]: co-resident CTAs of the cooperative radix select
+  int coop_max[2][2][2];  // [dtype][segmented][1024-thread]: co-resident CTAs of the cooperative radix select
 };
 
 // ---- device-resident Kelley loop (NEXT row §8f-3) ---------------------------------------------
