@@ -3639,6 +3639,25 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     __syncthreads();
   }
   K keys[KPT];
+  constexpr int VEK = 16 / sizeof(T);
+  bool vec_done = false;
+  if constexpr (KPT % VEK == 0 && KPT >= VEK) {
+    if (!tab && m == ms && ms == S && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+      // the whole (pooled, contiguous) sample: thread (crank, i) takes KPT consecutive values with
+      // 16-byte loads (which thread holds which sample does not matter to the histograms)
+      using V = typename VecOf<T>::V;
+      const V* xv = reinterpret_cast<const V*>(x + ((uint64_t)crank * 1024 + i) * KPT);
+      V vv[KPT / VEK];
+#pragma unroll
+      for (int u = 0; u < KPT / VEK; ++u) vv[u] = __ldg(xv + u);
+#pragma unroll
+      for (int u = 0; u < KPT / VEK; ++u)
+#pragma unroll
+        for (int q = 0; q < VEK; ++q) keys[u * VEK + q] = SK::key(lane_of(vv[u], q));
+      vec_done = true;
+    }
+  }
+  if (!vec_done)
 #pragma unroll
   for (int j = 0; j < KPT; ++j) {
     const uint64_t smp = ((uint64_t)j * kSampleCluster + crank) * 1024 + i;
@@ -3689,6 +3708,9 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     cl.sync();  // CTA 0's prefixes and zeroed histograms visible to every CTA
     const K p0 = (K)sh0->prefix[0], p1 = (K)sh0->prefix[1], p2 = (K)sh0->prefix[2];
     const K m0 = (K)sh0->mask[0], m1 = (K)sh0->mask[1], m2 = (K)sh0->mask[2];
+    // targets whose prefix class equals an earlier target's share its histogram (the usual case:
+    // the three ranks lie in one class of the first digit)
+    const bool same1 = p1 == p0 && m1 == m0, same2 = p2 == p0 && m2 == m0;
     const int ntg = rd == 0 ? 1 : 3;
     // one predicated shared reduction per key and target: keys of one digit that meet in a warp
     // instruction are aggregated by the hardware (no per-thread sort, no run detection — the sort
@@ -3696,6 +3718,7 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       if (t >= ntg) break;
+      if ((t == 1 && same1) || (t == 2 && same2)) continue;  // copied from target 0 at the merge
       const K pt = t == 0 ? p0 : (t == 1 ? p1 : p2), mt = t == 0 ? m0 : (t == 1 ? m1 : m2);
       const unsigned base = (unsigned)__cvta_generic_to_shared(&sh.loc[t][0]);
 #pragma unroll
@@ -3719,9 +3742,11 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
 #pragma unroll
       for (int q = 0; q < kSampleCluster; ++q) locq[q] = cl.map_shared_rank(&sh.loc[0][0], q);
       for (int b = (int)crank * slice + i; b < ((int)crank + 1) * slice; b += 1024) {
+        const int t = b >> 11;
+        const int src = (t == 1 && same1) || (t == 2 && same2) ? (b & 2047) : b;  // shared histogram
         unsigned v = 0;
 #pragma unroll
-        for (int q = 0; q < kSampleCluster; ++q) v += locq[q][b];
+        for (int q = 0; q < kSampleCluster; ++q) v += locq[q][src];
         glob0[b] = v;
       }
     }
