@@ -259,7 +259,7 @@ def kelley_side(cp, torch, datagen, dev, dists, log2n, peak, reps=3):
     out["outliers"] = {}
     for mag in (1e3, 1e9):
         x[pos] = mag
-        for name, drv in (("kelley", 0), ("bisection", 1)):
+        for name, drv in (("kelley", 0), ("bisection", 1), ("brent_root", 2)):
             cp.set_config(dev.index, record_timing=0, driver=drv, **cfg)
             cp.select_kth(x, k)
             e0, e1 = _ev(torch)

@@ -90,7 +90,10 @@ typedef struct {
                                 paper's comparison: t = (y_L + y_R)/2 in value, the
                                 same passes, exact rank test and finish; no R26 cut passes, no
                                 ordered-key safeguard (its pass count grows with log2 of the data
-                                range, P:L413 — the outlier-sensitivity demonstration).  Default 0 */
+                                range, P:L413 — the outlier-sensitivity demonstration).  2: Brent's
+                                root finder (Numerical Recipes' zbrent) on
+                                f(t) = c_lt(t) + c_le(t) - 2k + 1 proposing the points instead, the
+                                same passes and exact bracket.  Default 0 */
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -150,7 +153,7 @@ typedef struct {
   uint64_t written;       /* elements this pass wrote (compaction of both bracket halves) */
   uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard,
                              2 the init pass's extra cut (R23), 3 a two-cut pass (R26), 4 a step of
-                             the bisection driver (driver = 1) */
+                             the bisection driver (driver = 1), 5 of Brent's root finder (driver 2) */
   uint32_t compacted;     /* 1 if this pass also wrote z */
   double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
 } cpsel_trace_row;

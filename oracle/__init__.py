@@ -339,6 +339,91 @@ def bisection(x, k: int, maxit: int = 400, z_cap: int = 0):
     return {"value": value, "iterations": it, "trace": trace}
 
 
+def _snap(t: float, yL: float, yR: float, dt):
+    """t rounded to the dtype and nudged strictly inside ]yL, yR[ (reading R9)."""
+    f = dt(t) if math.isfinite(t) else dt(0.5 * yL + 0.5 * yR)
+    if not f > dt(yL):
+        f = np.nextafter(dt(yL), dt(math.inf))
+    if not f < dt(yR):
+        f = np.nextafter(dt(yR), dt(-math.inf))
+    return float(f)
+
+
+def brent_root(x, k: int, maxit: int = 400, z_cap: int = 0):
+    """The paper's Brent root-finding comparison ("the method of parabolas combined with golden
+    section, which is also known as Brent algorithm [NR]", "solving 0 in g(y)"): Numerical
+    Recipes' zbrent, literally, on f(t) = c_lt(t) + c_le(t) - 2k + 1 (an integer: < 0 below x_(k),
+    > 0 above, so its sign change is the target), each proposed point rounded into the open
+    bracket (R9); 0 in dF_k(t) -> t; the exact bracket [y_L, y_R] from the counts as in
+    `bisection`; stop when the interior holds <= z_cap elements, then the hybrid finish.
+    Returns dict(value, iterations, trace=[(t, c_lt, c_eq, interior)])."""
+    x = _as_array(x)
+    n = check_input(x, k)
+    dt = x.dtype.type
+    rec = init_record(x)
+    if k <= rec["cnt_min"]:
+        return {"value": rec["min"], "iterations": 0, "trace": []}
+    if k > n - rec["cnt_max"]:
+        return {"value": rec["max"], "iterations": 0, "trace": []}
+    yL, yR = float(rec["min"]), float(rec["max"])
+    c_le_L, c_lt_R = rec["cnt_min"], n - rec["cnt_max"]
+    eps = 2.220446049250313e-16
+    a, fa = yL, 2.0 * c_le_L - 2.0 * k + 1.0
+    b, fb = yR, 2.0 * c_lt_R - 2.0 * k + 1.0
+    c, fc = b, fb
+    d = e = b - a
+    trace = []
+    it = 0
+    for it in range(1, maxit + 1):
+        if (fb > 0 and fc > 0) or (fb < 0 and fc < 0):
+            c, fc = a, fa
+            e = d = b - a
+        if abs(fc) < abs(fb):
+            a, b, c = b, c, b
+            fa, fb, fc = fb, fc, fb
+        tol1 = 2.0 * eps * abs(b)
+        xm = 0.5 * (c - b)
+        if abs(e) >= tol1 and abs(fa) > abs(fb):
+            s_ = fb / fa
+            if a == c:
+                p_ = 2.0 * xm * s_
+                q_ = 1.0 - s_
+            else:
+                qq, r_ = fa / fc, fb / fc
+                p_ = s_ * (2.0 * xm * qq * (qq - r_) - (b - a) * (r_ - 1.0))
+                q_ = (qq - 1.0) * (r_ - 1.0) * (s_ - 1.0)
+            if p_ > 0:
+                q_ = -q_
+            p_ = abs(p_)
+            if 2.0 * p_ < min(3.0 * xm * q_ - abs(tol1 * q_), abs(e * q_)):
+                e = d
+                d = p_ / q_
+            else:
+                d = xm
+                e = d
+        else:
+            d = xm
+            e = d
+        t = _snap(b + (d if abs(d) > tol1 else (tol1 if xm >= 0 else -tol1)), yL, yR, dt)
+        if not (yL < t < yR):
+            break
+        c_lt, c_eq = rank_counts(x, t)
+        a, fa = b, fb
+        b, fb = t, float(c_lt + c_lt + c_eq) - 2.0 * k + 1.0
+        if c_lt < k <= c_lt + c_eq:
+            trace.append((t, c_lt, c_eq, 0))
+            return {"value": canonical(dt(t)), "iterations": it, "trace": trace}
+        if c_lt + c_eq < k:
+            yL, c_le_L = t, c_lt + c_eq
+        else:
+            yR, c_lt_R = t, c_lt
+        trace.append((t, c_lt, c_eq, c_lt_R - c_le_L))
+        if c_lt_R - c_le_L <= z_cap:
+            break
+    value, _ = hybrid_finish(x, k, yL, yR)
+    return {"value": value, "iterations": it, "trace": trace}
+
+
 def eval_at(x, k: int, t, y_lo, y_hi):
     """Replay hook: one pass at t (pass_stats) plus F_k(t) and dF_k(t) — compared against the
     GPU's cpsel_eval / trace at identical t."""

@@ -210,6 +210,60 @@ double snap(double t, double yL, double yR, int dt) {
   return f;
 }
 
+// Brent's root finder (Numerical Recipes' zbrent, the paper's [NR]: P:L136), the comparison
+// driver 2: its interpolation proposes the next point on f(t) = c_lt(t) + c_le(t) - 2k + 1 (negative
+// below x_(k), positive above, an integer), the passes and the exact bracket stay the cutting
+// plane's.  Step by step the same as oracle.brent_root (same operations in double).
+struct BrentRoot {
+  double a = 0, b = 0, c = 0, fa = 0, fb = 0, fc = 0, d = 0, e = 0;
+  void init(double yl, double fl, double yr, double fr) {
+    a = yl; fa = fl; b = yr; fb = fr; c = b; fc = fb;
+    d = e = b - a;
+  }
+  double propose() {
+    if ((fb > 0.0 && fc > 0.0) || (fb < 0.0 && fc < 0.0)) {
+      c = a; fc = fa;
+      e = d = b - a;
+    }
+    if (std::fabs(fc) < std::fabs(fb)) {
+      a = b; b = c; c = a;
+      fa = fb; fb = fc; fc = fa;
+    }
+    const double tol1 = 2.0 * 2.220446049250313e-16 * std::fabs(b);
+    const double xm = 0.5 * (c - b);
+    if (std::fabs(e) >= tol1 && std::fabs(fa) > std::fabs(fb)) {
+      const double s = fb / fa;
+      double p, q;
+      if (a == c) {
+        p = 2.0 * xm * s;
+        q = 1.0 - s;
+      } else {
+        const double qq = fa / fc, r = fb / fc;
+        p = s * (2.0 * xm * qq * (qq - r) - (b - a) * (r - 1.0));
+        q = (qq - 1.0) * (r - 1.0) * (s - 1.0);
+      }
+      if (p > 0.0) q = -q;
+      p = std::fabs(p);
+      const double min1 = 3.0 * xm * q - std::fabs(tol1 * q), min2 = std::fabs(e * q);
+      if (2.0 * p < (min1 < min2 ? min1 : min2)) {
+        e = d;
+        d = p / q;
+      } else {
+        d = xm;
+        e = d;
+      }
+    } else {
+      d = xm;
+      e = d;
+    }
+    return b + (std::fabs(d) > tol1 ? d : (xm >= 0.0 ? tol1 : -tol1));
+  }
+  void accept(double t, double ft) {
+    a = b; fa = fb;
+    b = t; fb = ft;
+  }
+};
+
 // Ordered-key bisection point of ]yL, yR[ (safeguard, R7).
 double key_mid(double yL, double yR, int dt) {
   const uint64_t a = key_of(yL, dt), b = key_of(yR, dt);
@@ -1446,6 +1500,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
                           (double)m;
   int slow = 0;
   bool bisect = false;
+  BrentRoot brent;  // driver 2
+  bool brent_on = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
   constexpr uint64_t kUnknown = ~0ull;
   bool exact = true;  // the current (compacted) array holds exactly the bracket interior
@@ -1672,6 +1728,13 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     if (cfg.driver == 1) {  // the bisection comparison driver: the bracket's value midpoint
       t = 0.5 * yL + 0.5 * yR;
       kind = 4;
+    } else if (cfg.driver == 2) {  // Brent's root finder: its interpolation's next point
+      if (!brent_on) {
+        brent.init(yL, 2.0 * (double)c_le_L - 2.0 * (double)k + 1.0, yR, 2.0 * (double)c_lt_R - 2.0 * (double)k + 1.0);
+        brent_on = true;
+      }
+      t = brent.propose();
+      kind = 5;
     } else if (bisect) {
       t = key_mid(yL, yR, dt);
       kind = 1;
@@ -1711,6 +1774,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     row.kernel_ms = 0.0;  // filled from the timing slot when the selection ends
     row.scanned = be.scanned;
     row.written = compact ? zl + zh : 0;
+    if (cfg.driver == 2) brent.accept(tq, (double)c_lt + (double)c_le - 2.0 * (double)k + 1.0);
     // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
     if (c_lt < k && k <= c_le) {
       if (trace && cfg.record_trace) trace->push_back(row);
@@ -1765,7 +1829,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     // progress safeguard (R7): two consecutive steps keeping > 7/8 of the interior switch to
     // ordered-key bisection until progress resumes (bounds the pass count on any input); not for
     // the bisection driver, whose slow progress on wide data is what it demonstrates
-    if (cfg.driver == 1) {
+    if (cfg.driver != 0) {
       free_step = false;
     } else if (free_step) {
       free_step = false;
@@ -2000,7 +2064,7 @@ const char* cpsel_last_error(const cpsel_ctx* ctx) { return ctx ? ctx->err.c_str
 cpsel_status cpsel_set_config(cpsel_ctx* ctx, const cpsel_config* cfg) {
   if (!ctx || !cfg) return CPSEL_EINVAL;
   if (cfg->max_iters == 0) return fail(ctx, CPSEL_EINVAL, "max_iters must be >= 1");
-  if (cfg->driver != 0 && cfg->driver != 1) return fail(ctx, CPSEL_EINVAL, "driver must be 0 or 1");
+  if (cfg->driver < 0 || cfg->driver > 2) return fail(ctx, CPSEL_EINVAL, "driver must be 0, 1 or 2");
   ctx->cfg = *cfg;
   return CPSEL_OK;
 }

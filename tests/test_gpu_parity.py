@@ -518,10 +518,11 @@ def test_device_loop_matches_host_loop(cp, dtype, dist):
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_bisection_driver_matches_oracle(cp, dtype):
-    """driver=1 (the paper's bisection comparison): the same element as the oracle, its
-    iterates are exactly the oracle's bisection iterates (value midpoints rounded to the dtype) with
-    the same counts; and the paper's outlier claim (P:L413 vs P:L416): with 1e9 outliers bisection
-    needs >= 15 more passes than with 1e3, the cutting plane at most 2 more."""
+    """driver=1 (bisection) and driver=2 (Brent's root finder), the paper's comparisons (P:L135-136,
+    P:L204): the same element as the oracle, their iterates exactly the oracle's (value midpoints /
+    zbrent's points, rounded into the bracket) with the same counts; and the paper's outlier claim
+    (P:L313, P:L413 vs P:L416): with 1e9 outliers both need many more passes than with 1e3, the
+    cutting plane at most 2 more."""
     import torch
     n = 1_000_003
     base = datagen.make("uniform", n, dtype)
@@ -530,17 +531,19 @@ def test_bisection_driver_matches_oracle(cp, dtype):
         x = datagen.inject_outliers(base.copy(), 100, mag)
         xd = tdev(x)
         k = O.median_rank(n)
-        ref = O.bisection(x, k, z_cap=0)
-        for drv in (1, 0):
+        refs = {1: O.bisection(x, k, z_cap=0), 2: O.brent_root(x, k, z_cap=0)}
+        for drv in (1, 2, 0):
             cp.set_config(driver=drv, init_cut=0, pass_cuts=0)
             v, info = cp.select_kth(xd, k, return_info=True)
             tr = cp.get_trace()
             cp.set_config(driver=0, init_cut=1, pass_cuts=1)
             assert v == canon(float(np.sort(x)[k - 1])), (mag, drv)
             passes[(mag, drv)] = info["passes"]
-            if drv == 1:
-                assert len(tr) <= len(ref["trace"]) and all(r["kind"] == 4 for r in tr)
+            if drv in refs:
+                ref = refs[drv]
+                assert len(tr) <= len(ref["trace"]) and all(r["kind"] == 3 + drv for r in tr)
                 for r, (t, c_lt, c_eq, interior) in zip(tr, ref["trace"]):
                     assert r["t"] == t and (r["c_lt"], r["c_eq"]) == (c_lt, c_eq), (r, t, c_lt, c_eq)
     assert passes[(1e9, 1)] - passes[(1e3, 1)] >= 15, passes
+    assert passes[(1e9, 2)] - passes[(1e3, 2)] >= 10, passes
     assert passes[(1e9, 0)] - passes[(1e3, 0)] <= 2, passes

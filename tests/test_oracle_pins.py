@@ -612,3 +612,25 @@ def test_bisection_result_and_outlier_sensitivity():
         assert O.bisection(y, O.median_rank(y.size), z_cap=64)["value"] == np.sort(y)[O.median_rank(y.size) - 1]
     assert its[1] - its[0] >= 15, its
     assert abs(cps[1] - cps[0]) <= 2, cps
+
+
+def test_brent_root_result_and_outlier_sensitivity():
+    """oracle.brent_root (zbrent on the count function): the exact element by the definition for
+    every kind of rank, and the paper's claim (Brent's root finder 'degraded when data
+    contained very large outliers', reverting to bisection steps): 1e9 outliers cost >= 10 more
+    iterations than 1e3, the cutting plane none."""
+    rng = np.random.default_rng(5)
+    x = rng.random(20001)
+    for k in (1, 2, 7, 10001, 19999, 20001):
+        assert O.brent_root(x, k)["value"] == np.sort(x)[k - 1]
+    xd = np.floor(256 * rng.random(5001)).astype(np.float32)   # many duplicates
+    for k in (1, 100, 2501, 5001):
+        assert O.brent_root(xd, k)["value"] == np.sort(xd)[k - 1]
+    its, cps = [], []
+    for mag in (1e3, 1e9):
+        y = x.copy()
+        y[rng.choice(y.size, 20, replace=False)] = mag
+        its.append(O.brent_root(y, 10001, z_cap=64)["iterations"])
+        cps.append(O.cutting_plane(y, 10001, z_cap=64)["iterations"])
+    assert its[1] - its[0] >= 10, its
+    assert abs(cps[1] - cps[0]) <= 2, cps
