@@ -292,6 +292,18 @@ cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_
                                const float* d_Q, uint32_t nq, uint64_t k, int32_t weighting, float* d_out,
                                float* d_dk, cpsel_info* info);
 
+/* kNN classification ("the majority vote (among the k nearest neighbours) is applied"): the
+ * same distances and d2_(k) as cpsel_knn_regress; per query the votes
+ *   V_c = sum_i rho_ij w_ij [labels_i = c]   (rho as above: exactly k neighbours' worth, ties shared)
+ * and d_out[j] = the class with the largest vote (the smallest index among equal votes).
+ * d_labels: int32[n] in [0, n_classes), 1 <= n_classes <= 64; d_votes (nullable): f64 nq x n_classes
+ * row-major (fp64 shared-memory atomics: with weighting 1 the summation order, and so the last bits
+ * of a vote, may vary run to run).  Errors as cpsel_knn_regress, plus EINVAL for n_classes outside
+ * [1, 64] or a voting neighbour's label outside [0, n_classes). */
+cpsel_status cpsel_knn_classify(cpsel_ctx* ctx, const float* d_X, const int32_t* d_labels, uint64_t n, uint32_t p,
+                                const float* d_Q, uint32_t nq, uint64_t k, uint32_t n_classes, int32_t weighting,
+                                int32_t* d_out, double* d_votes, cpsel_info* info);
+
 /* ---- host-only driver (no GPU needed) ------------------------------------------------------ */
 /* The same cutting-plane driver, with the three device steps supplied as callbacks.  Used by
  * the CPU tests (world-size-2 gloo tests of the sharded combine) to exercise the exact host

@@ -555,3 +555,25 @@ def knn_regress(X, f, Q, k: int, weighting: int = 0):
         out[j] = float(np.sum(w * f) / np.sum(w))
         dk[j] = t
     return out, dk
+
+
+def knn_classify(X, labels, Q, k: int, n_classes: int, weighting: int = 0):
+    """kNN classification ("the majority vote (among the k nearest neighbors) is applied"):
+    the votes V_c = sum_i rho_i w_i [label_i = c] with the indicator rho of `knn_regress` (R33) and
+    the winner = argmax V_c, the smallest class among equal votes.  Returns (classes int32[nq],
+    votes float64[nq, n_classes])."""
+    D = knn_distances_sq(X, Q)
+    labels = np.asarray(labels)
+    out = np.empty(D.shape[0], dtype=np.int32)
+    votes = np.zeros((D.shape[0], n_classes), dtype=np.float64)
+    for j in range(D.shape[0]):
+        row = D[j]
+        t = order_statistic(row, k)
+        lt, eq = row < t, row == t
+        a, b = k - int(np.count_nonzero(lt)), int(np.count_nonzero(eq))
+        rho = lt.astype(LD) + eq.astype(LD) * (LD(a) / LD(b))
+        w = knn_weights(row, weighting) * rho
+        for c in range(n_classes):
+            votes[j, c] = float(np.sum(w[labels == c]))
+        out[j] = int(np.argmax(votes[j]))   # first maximum = smallest class among equal votes
+    return out, votes

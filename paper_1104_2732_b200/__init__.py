@@ -17,7 +17,7 @@ __all__ = [
     "select_kth", "median", "select_kth_host", "lms_objective", "lms_residuals", "select_kth_batched",
     "eval", "init_stats", "small_select", "get_trace", "set_config", "get_config", "nccl_unique_id",
     "comm_init", "select_kth_sharded", "drive_host", "library_path", "load", "CpselError",
-    "LoopbackGroup", "comm_init_loopback", "knn_regress",
+    "LoopbackGroup", "comm_init_loopback", "knn_regress", "knn_classify",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -113,7 +113,7 @@ SYMBOLS = [
     "cpsel_eval", "cpsel_init", "cpsel_small_select", "cpsel_get_trace", "cpsel_init_timings", "cpsel_nccl_unique_id",
     "cpsel_comm_init", "cpsel_select_kth_sharded", "cpsel_drive_host", "cpsel_pooled_cuts",
     "cpsel_lts_objective", "cpsel_loopback_create", "cpsel_loopback_destroy", "cpsel_comm_init_loopback",
-    "cpsel_knn_regress",
+    "cpsel_knn_regress", "cpsel_knn_classify",
 ]
 
 _lib = None
@@ -167,6 +167,7 @@ def load():
             "cpsel_loopback_destroy": (None, [P]),
             "cpsel_comm_init_loopback": (I, [P, P, I]),
             "cpsel_knn_regress": (I, [P, P, P, U64, U32, P, U32, U64, C.c_int32, P, P, C.POINTER(Info)]),
+            "cpsel_knn_classify": (I, [P, P, P, U64, U32, P, U32, U64, U32, C.c_int32, P, P, C.POINTER(Info)]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(lib, name)
@@ -473,6 +474,32 @@ def knn_regress(X, f, Q, k: int, weighting: int = 0, return_dk: bool = False, re
     if return_info:
         res = res + (info.as_dict(),)
     return res if len(res) > 1 else res[0]
+
+
+def knn_classify(X, labels, Q, k: int, n_classes: int, weighting: int = 0, return_votes: bool = False):
+    """kNN classification via d_(k): the rho-weighted majority vote of the k nearest rows of
+    X for every query row of Q; labels: int32 (n,) in [0, n_classes).  Returns int32 (nq,) classes
+    (and the (nq, n_classes) float64 votes if asked)."""
+    import torch
+    for t in (X, Q):
+        if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("X, Q must be contiguous float32 CUDA tensors")
+    if labels.dtype != torch.int32 or not labels.is_cuda or not labels.is_contiguous():
+        raise ValueError("labels must be a contiguous int32 CUDA tensor")
+    if X.dim() != 2 or Q.dim() != 2 or Q.shape[1] != X.shape[1] or labels.numel() != X.shape[0]:
+        raise ValueError("X (n, p), labels (n,), Q (nq, p)")
+    n, p = X.shape
+    nq = Q.shape[0]
+    ctx = _ctx_for(X)
+    out = torch.empty(nq, device=X.device, dtype=torch.int32)
+    votes = torch.empty((nq, n_classes), device=X.device, dtype=torch.float64) if return_votes else None
+    info = Info()
+    _check(ctx, load().cpsel_knn_classify(ctx.handle, C.c_void_p(X.data_ptr()), C.c_void_p(labels.data_ptr()), n, p,
+                                          C.c_void_p(Q.data_ptr()), nq, int(k), int(n_classes), int(weighting),
+                                          C.c_void_p(out.data_ptr()),
+                                          C.c_void_p(votes.data_ptr()) if votes is not None else None,
+                                          C.byref(info)))
+    return (out, votes) if return_votes else out
 
 
 # ------------------------------------------------------------------------------------------ multi-GPU

@@ -2440,6 +2440,65 @@ cpsel_status cpsel_lts_objective(cpsel_ctx* ctx, const float* d_X, const float* 
 }
 
 // ------------------------------------------------------------------------ kNN (§8f-4)
+// steps 1-2 of kNN (distances, d2_(k) per query) shared by regression and classification; on
+// success D and dk hold them and *bad points at two zeroed/used counters
+static cpsel_status knn_select(cpsel_ctx* ctx, const float* d_X, uint64_t n, uint32_t p, const float* d_Q,
+                               uint32_t nq, uint64_t k, float* d_dk, float** D_out, float** dk_out,
+                               unsigned long long** bad_out, LmsReport* rep) {
+  const size_t dbytes = (size_t)n * nq * sizeof(float), off_dk = (dbytes + 255) / 256 * 256;
+  const size_t off_bad = off_dk + ((size_t)nq * sizeof(float) + 255) / 256 * 256;
+  cpsel_status s = ensure(ctx, &ctx->d_knn, &ctx->knn_bytes, off_bad + 256);
+  if (s != CPSEL_OK) return s;
+  char* base = static_cast<char*>(ctx->d_knn);
+  float* D = reinterpret_cast<float*>(base);
+  float* dk = d_dk ? d_dk : reinterpret_cast<float*>(base + off_dk);
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(base + off_bad);
+  CK(cudaMemsetAsync(bad, 0, 2 * sizeof *bad, ctx->stream));
+  CK(knn_distances(d_X, d_Q, n, p, nq, D, bad, ctx->stream));            // 1. distances
+  unsigned long long hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hbad) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf (or a distance overflows)");
+  cudaError_t e = batched_select(ctx->lms, D, n, nq, k, dk, ctx->cfg.max_iters, rep, ctx->stream);  // 2. d2_(k)
+  if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a query");
+  CK(e);
+  if (rep->nonfinite) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf");
+  *D_out = D; *dk_out = dk; *bad_out = bad;
+  return CPSEL_OK;
+}
+
+cpsel_status cpsel_knn_classify(cpsel_ctx* ctx, const float* d_X, const int32_t* d_labels, uint64_t n, uint32_t p,
+                                const float* d_Q, uint32_t nq, uint64_t k, uint32_t n_classes, int32_t weighting,
+                                int32_t* d_out, double* d_votes, cpsel_info* info) {
+  if (!ctx) return CPSEL_EINVAL;
+  if (!d_X || !d_labels || !d_Q || !d_out) return fail(ctx, CPSEL_EINVAL, "null pointer");
+  if (n == 0 || nq == 0 || p == 0) return fail(ctx, CPSEL_EINVAL, "empty problem");
+  if (p > (uint32_t)kKnnMaxP) return fail(ctx, CPSEL_EINVAL, "p > %d", kKnnMaxP);
+  if (nq > 65535u * 16u) return fail(ctx, CPSEL_EINVAL, "nq > 1048560");
+  if (n_classes == 0 || n_classes > 64) return fail(ctx, CPSEL_EINVAL, "n_classes must be in [1, 64]");
+  if (weighting != 0 && weighting != 1) return fail(ctx, CPSEL_EINVAL, "weighting must be 0 or 1");
+  if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
+  DeviceGuard g(ctx->device);
+  const auto t0 = std::chrono::steady_clock::now();
+  float *D, *dk;
+  unsigned long long* bad;
+  LmsReport rep{};
+  cpsel_status s = knn_select(ctx, d_X, n, p, d_Q, nq, k, nullptr, &D, &dk, &bad, &rep);
+  if (s != CPSEL_OK) return s;
+  CK(knn_vote(D, d_labels, n, nq, k, n_classes, dk, weighting, d_out, d_votes, bad + 1, ctx->stream));  // 3. votes
+  unsigned long long hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad + 1, sizeof hbad, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hbad) return fail(ctx, CPSEL_EINVAL, "a label of a voting neighbour is outside [0, n_classes)");
+  lms_info(info, rep, false);
+  if (info) {
+    info->launches += 2;
+    info->bytes_moved += 2 * (uint64_t)n * nq * sizeof(float);
+    info->ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  }
+  return CPSEL_OK;
+}
+
 cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_f, uint64_t n, uint32_t p,
                                const float* d_Q, uint32_t nq, uint64_t k, int32_t weighting, float* d_out,
                                float* d_dk, cpsel_info* info) {
@@ -2452,27 +2511,17 @@ cpsel_status cpsel_knn_regress(cpsel_ctx* ctx, const float* d_X, const float* d_
   if (k < 1 || k > n) return fail(ctx, CPSEL_ERANK, "k outside [1,n]");
   DeviceGuard g(ctx->device);
   const auto t0 = std::chrono::steady_clock::now();
-  const size_t dbytes = (size_t)n * nq * sizeof(float), off_dk = (dbytes + 255) / 256 * 256;
-  const size_t off_bad = off_dk + ((size_t)nq * sizeof(float) + 255) / 256 * 256;
-  cpsel_status s = ensure(ctx, &ctx->d_knn, &ctx->knn_bytes, off_bad + 256);
-  if (s != CPSEL_OK) return s;
-  char* base = static_cast<char*>(ctx->d_knn);
-  float* D = reinterpret_cast<float*>(base);
-  float* dk = d_dk ? d_dk : reinterpret_cast<float*>(base + off_dk);
-  unsigned long long* bad = reinterpret_cast<unsigned long long*>(base + off_bad);
-  CK(cudaMemsetAsync(bad, 0, 2 * sizeof *bad, ctx->stream));
-  CK(knn_check_f(d_f, n, bad + 1, ctx->stream));                         // NaN/Inf in f
-  CK(knn_distances(d_X, d_Q, n, p, nq, D, bad, ctx->stream));            // 1. distances
-  unsigned long long hbad[2] = {0, 0};
-  CK(cudaMemcpyAsync(hbad, bad, sizeof hbad, cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));
-  if (hbad[0]) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf (or a distance overflows)");
+  const size_t dbytes = (size_t)n * nq * sizeof(float);
+  float *D, *dk;
+  unsigned long long* bad;
   LmsReport rep{};
-  cudaError_t e = batched_select(ctx->lms, D, n, nq, k, dk, ctx->cfg.max_iters, &rep, ctx->stream);  // 2. d2_(k)
-  if (e == cudaErrorNotSupported) return fail(ctx, CPSEL_EINTERNAL, "batched select: safeguard tripped on a query");
-  CK(e);
-  if (rep.nonfinite) return fail(ctx, CPSEL_ENONFINITE, "X or Q hold NaN or Inf");
-  if (hbad[1]) return fail(ctx, CPSEL_ENONFINITE, "f holds NaN or Inf");
+  cpsel_status s = knn_select(ctx, d_X, n, p, d_Q, nq, k, d_dk, &D, &dk, &bad, &rep);
+  if (s != CPSEL_OK) return s;
+  CK(knn_check_f(d_f, n, bad + 1, ctx->stream));                         // NaN/Inf in f
+  unsigned long long hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad + 1, sizeof hbad, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (hbad) return fail(ctx, CPSEL_ENONFINITE, "f holds NaN or Inf");
   CK(knn_reduce(D, d_f, n, nq, k, dk, weighting, d_out, ctx->stream));  // 3. the rho reduction
   CK(cudaStreamSynchronize(ctx->stream));
   lms_info(info, rep, false);

@@ -168,6 +168,63 @@ __global__ void __launch_bounds__(256) knn_check_kernel(const float* __restrict_
   if (c) atomicAdd(bad, (unsigned long long)c);
 }
 
+
+// kNN classification ("the majority vote (among the k nearest neighbours)"): per query the
+// rho-weighted votes of the classes, rho as in the regression (1 below d_(k), a/b at it), the
+// winner = the largest vote, the smallest class index among equal votes.  Votes in fp64 shared
+// memory (per-CTA; only the d <= d_(k) elements vote).
+constexpr int kKnnMaxClasses = 64;
+__global__ void __launch_bounds__(256) knn_vote_kernel(const float* __restrict__ D, const int* __restrict__ labels,
+                                                       uint64_t n, uint32_t nq, uint64_t k, uint32_t nclass,
+                                                       const float* __restrict__ dk, int weighting,
+                                                       int* __restrict__ out, double* __restrict__ votes_out,
+                                                       unsigned long long* bad) {
+  __shared__ double v_lt[kKnnMaxClasses], v_eq[kKnnMaxClasses];
+  __shared__ unsigned long long s_c[2];
+  for (uint32_t j = blockIdx.x; j < nq; j += gridDim.x) {
+    for (int c = threadIdx.x; c < kKnnMaxClasses; c += blockDim.x) v_lt[c] = v_eq[c] = 0.0;
+    if (threadIdx.x < 2) s_c[threadIdx.x] = 0ull;
+    __syncthreads();
+    const float t = dk[j];
+    const float* row = D + (size_t)j * n;
+    unsigned long long c_lt = 0, c_eq = 0;
+    for (uint64_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const float d = __ldcs(row + i);
+      if (d <= t) {
+        const int lab = labels[i];
+        if (lab < 0 || (uint32_t)lab >= nclass) {
+          atomicAdd(bad, 1ull);
+          continue;
+        }
+        const double wi = knn_w(d, weighting);
+        if (d < t) {
+          atomicAdd(&v_lt[lab], wi);
+          ++c_lt;
+        } else {
+          atomicAdd(&v_eq[lab], wi);
+          ++c_eq;
+        }
+      }
+    }
+    atomicAdd(&s_c[0], c_lt);
+    atomicAdd(&s_c[1], c_eq);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const double a = (double)(k - s_c[0]), b = (double)s_c[1];
+      const double r = b > 0 ? a / b : 0.0;
+      int best = 0;
+      double bv = -1.0;
+      for (uint32_t c = 0; c < nclass; ++c) {
+        const double v = v_lt[c] + r * v_eq[c];
+        if (votes_out) votes_out[(size_t)j * nclass + c] = v;
+        if (v > bv) { bv = v; best = (int)c; }
+      }
+      out[j] = best;
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 cudaError_t knn_distances(const float* X, const float* Q, uint64_t n, uint32_t p, uint32_t nq, float* D,
@@ -199,6 +256,18 @@ cudaError_t knn_reduce(const float* D, const float* f, uint64_t n, uint32_t nq, 
   int grid = sms * 8;
   if ((uint32_t)grid > nq) grid = (int)nq;
   knn_reduce_kernel<<<grid, 256, 0, st>>>(D, f, n, nq, k, dk, weighting, out);
+  return cudaGetLastError();
+}
+
+cudaError_t knn_vote(const float* D, const int* labels, uint64_t n, uint32_t nq, uint64_t k, uint32_t nclass,
+                     const float* dk, int weighting, int* out, double* votes, unsigned long long* bad, cudaStream_t st) {
+  if (nclass == 0 || nclass > (uint32_t)kKnnMaxClasses) return cudaErrorInvalidValue;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int grid = sms * 8;
+  if ((uint32_t)grid > nq) grid = (int)nq;
+  knn_vote_kernel<<<grid, 256, 0, st>>>(D, labels, n, nq, k, nclass, dk, weighting, out, votes, bad);
   return cudaGetLastError();
 }
 

@@ -60,3 +60,22 @@ def test_knn_errors(cp):
     Qb[1, 1] = float("inf")
     with pytest.raises(ValueError):
         cp.knn_regress(Xd, fd, Qb, 3)
+
+
+@pytest.mark.parametrize("ties", [False, True])
+@pytest.mark.parametrize("weighting", [0, 1])
+def test_knn_classify_matches_oracle(cp, ties, weighting):
+    import torch
+    n, p, nq, C = 100_003, 4, 29, 7
+    X, _, Q = problem(n, p, nq, 5 + int(ties), ties)
+    lab = np.random.default_rng(9).integers(0, C, n).astype(np.int32)
+    Xd, ld, Qd = torch.from_numpy(X).cuda(), torch.from_numpy(lab).cuda(), torch.from_numpy(Q).cuda()
+    for k in (1, 9, 200):
+        got, votes = cp.knn_classify(Xd, ld, Qd, k, C, weighting, return_votes=True)
+        ref, rvotes = O.knn_classify(X, lab, Q, k, C, weighting)
+        np.testing.assert_allclose(votes.cpu().numpy(), rvotes, rtol=1e-12, atol=1e-12 * k)
+        gap = np.sort(rvotes, axis=1)[:, -1] - np.sort(rvotes, axis=1)[:, -2]
+        sure = gap > 1e-9 * np.max(rvotes, axis=1)   # the winner is decided beyond rounding
+        assert np.array_equal(got.cpu().numpy()[sure], ref[sure]), k
+    with pytest.raises(ValueError):
+        cp.knn_classify(Xd, torch.full_like(ld, C), Qd, 3, C)

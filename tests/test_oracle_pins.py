@@ -634,3 +634,23 @@ def test_brent_root_result_and_outlier_sensitivity():
         cps.append(O.cutting_plane(y, 10001, z_cap=64)["iterations"])
     assert its[1] - its[0] >= 10, its
     assert abs(cps[1] - cps[0]) <= 2, cps
+
+
+def test_knn_classify_is_the_majority_of_the_k_nearest():
+    """No ties at d_(k): the vote equals the class counts among the k nearest by a full sort, the
+    winner their majority (smallest class on a tie); with ties the votes sum to k exactly."""
+    rng = np.random.default_rng(8)
+    X = rng.standard_normal((400, 2)).astype(np.float32)
+    lab = rng.integers(0, 5, 400).astype(np.int32)
+    Q = rng.standard_normal((6, 2)).astype(np.float32)
+    for k in (1, 5, 40):
+        cls, votes = O.knn_classify(X, lab, Q, k, 5)
+        D = O.knn_distances_sq(X, Q)
+        for j in range(6):
+            idx = np.argsort(D[j], kind="stable")[:k]
+            cnt = np.bincount(lab[idx], minlength=5)
+            assert np.array_equal(votes[j], cnt.astype(np.float64))
+            assert cls[j] == int(np.argmax(cnt))
+    Xg = np.array([[0.0], [1.0], [-1.0], [2.0], [-2.0]], np.float32)          # ties at distance 1, 4
+    cls, votes = O.knn_classify(Xg, np.array([0, 1, 2, 1, 2], np.int32), np.zeros((1, 1), np.float32), 2, 3)
+    assert votes[0].tolist() == [1.0, 0.5, 0.5] and cls[0] == 0
