@@ -463,6 +463,7 @@ struct GpuBackend : Backend {
   // presampled: d_t0 already holds the cuts (sharded: pooled across ranks, R28)
   cpsel_status run_init(bool sync_result, uint64_t k, bool cut, bool presampled = false) {
     InitArgs a{x, n, ctx->d_partials, ctx->d_ticket, ctx->d_init, cut ? ctx->d_t0 : nullptr};
+    a.acc = reinterpret_cast<unsigned long long*>(ctx->d_ticket) + 8;  // words 8..15 of the ticket block
     if (use_mail) {
       a.out = &ctx->mb_dev->init;
       a.done = &ctx->mb_dev->seq_init;

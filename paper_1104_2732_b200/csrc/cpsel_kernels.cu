@@ -2441,7 +2441,40 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
   id.cnt_min = id.cnt_max = id.nonfinite = id.pad2 = 0;
   id.N0 = id.P0 = id.I0 = 0; id.cA = id.cB = id.cC = id.cD = id.cE = 0;
   InitPartial tot;
-  const bool last = grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id);
+  bool last;
+  if (!SUMS && ia.acc) {
+    // no fp sums in this form: every field is an extreme or a count, so the grid's totals are exact
+    // and order-free through atomics (min as the max of the complemented order-preserving key) —
+    // the last CTA reads five words instead of folding every CTA's partial (a ~10 us serial tail)
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+      unsigned long long* g = ia.acc;
+      atomicMax(&g[0], ~okey((T)p.vmin));
+      atomicMax(&g[1], okey((T)p.vmax));
+      if (p.nonfinite) atomicAdd(&g[2], p.nonfinite);
+      if (p.pad2) atomicAdd(&g[3], p.pad2);
+      if (p.cA) atomicAdd(&g[4], p.cA);
+      __threadfence();
+      s_last = atomicAdd(ia.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    last = s_last;
+    if (last && threadIdx.x == 0) {
+      __threadfence();
+      unsigned long long* g = ia.acc;
+      const unsigned long long kmin = ~__ldcg(&g[0]), kmax = __ldcg(&g[1]);
+      tot = id;
+      tot.vmin = sizeof(T) == 4 ? from_key_f32(kmin) : from_key_f64(kmin);
+      tot.vmax = sizeof(T) == 4 ? from_key_f32(kmax) : from_key_f64(kmax);
+      tot.nonfinite = __ldcg(&g[2]);
+      tot.pad2 = __ldcg(&g[3]);
+      tot.cA = __ldcg(&g[4]);
+      for (int q = 0; q < 5; ++q) g[q] = 0ull;  // self-reset for the next launch
+      *ia.ticket = 0u;
+    }
+  } else {
+    last = grid_finish(p, static_cast<InitPartial*>(ia.partials), ia.ticket, &tot, id);
+  }
   if (!last) return;
   if (threadIdx.x == 0) {
     DevInit r;

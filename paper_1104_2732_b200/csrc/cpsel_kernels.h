@@ -145,6 +145,9 @@ struct InitArgs {
   // memory histogram of the copied elements' top digit, merged into hist (2048 words); the chained
   // radix select starts at round 1 and picks that digit itself
   unsigned int* hist;
+  // init_seg_kernel without the fp sums: the grid's totals accumulated by atomics here (8 words,
+  // zero on entry, left zero) instead of a last-CTA fold of every CTA's partial; nullptr: the fold
+  unsigned long long* acc;
 };
 
 struct LaunchShape {
