@@ -423,11 +423,12 @@ def cpu_side(xs_host, dists, seconds):
     s22 = [x[:1 << 22] for x in xs_host]
     k22 = oracle.median_rank(1 << 22)
     run("cutting_plane", lambda z: oracle.cutting_plane(z, k22, z_cap=1 << 16), s22[:2], seconds / 4)
-    best = rows["nth_element"]
-    return {"value": best["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle.order_statistic_c (C++ std::nth_element, 1 thread) medians of the first 2^24 "
-                      f"elements of {dists}; other rows: np.partition, std::sort (2^24), the literal "
-                      f"long-double cutting plane (2^22)",
+    best_name = max(rows, key=lambda r: rows[r]["value"])
+    return {"value": rows[best_name]["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"the fastest oracle row ({best_name}, 1 thread) on medians of the first 2^24 elements "
+                      f"of {dists}; rows: np.partition (oracle.order_statistic), C++ std::nth_element and "
+                      f"std::sort (oracle.order_statistic_c, 2^24), the literal long-double cutting plane "
+                      f"(oracle.cutting_plane, 2^22)",
             "cpu_model": model, "nproc": os.cpu_count(), "rows": rows}
 
 

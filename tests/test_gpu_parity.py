@@ -268,10 +268,15 @@ def test_select_bench_size_2pow30_f32(cp):
     is checked by the rank invariant #{x<v} <= k-1 < #{x<=v} computed by the oracle on the host copy."""
     import torch
     n = 1 << 30
-    for dist in ("uniform", "dup256"):
+    for dist in datagen.BENCH_DISTS:   # the four arrays bench.py times
         xd = datagen.make(dist, n, "f32", device="cuda")
         k = O.median_rank(n)
         v, info = cp.median(xd, return_info=True)
+        # the same element from the paper's method as published (Kelley passes from [x_(1), x_(n)])
+        cp.set_config(init_cut=0, pass_cuts=0, objective=1)
+        v2 = cp.median(xd)
+        cp.set_config(init_cut=1, pass_cuts=1, objective=0)
+        assert v2 == v, (dist, v, v2)
         x = host(xd)
         del xd
         torch.cuda.empty_cache()
