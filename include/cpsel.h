@@ -36,7 +36,10 @@ typedef enum {
   CPSEL_ERANK = 2,      /* k < 1 or k > n */
   CPSEL_ENONFINITE = 3, /* the input holds NaN or +-Inf */
   CPSEL_ECUDA = 4,      /* a CUDA runtime error (message in cpsel_last_error) */
-  CPSEL_ENCCL = 5,      /* an NCCL error, or NCCL not loadable / comm not initialised */
+  CPSEL_ENCCL = 5,      /* an NCCL error, or NCCL not loadable / comm not initialised; also a sharded
+                           call whose collectives reported an asynchronous error or made no progress
+                           for CPSEL_COMM_TIMEOUT_S seconds (default 120): the communicator is then
+                           aborted and must be re-initialised */
   CPSEL_ENOMEM = 6,     /* device or pinned allocation failed */
   CPSEL_EINTERNAL = 7   /* a safeguard tripped (iteration cap); never expected */
 } cpsel_status;
@@ -45,7 +48,9 @@ typedef enum { CPSEL_F32 = 0, CPSEL_F64 = 1 } cpsel_dtype;
 
 typedef struct cpsel_ctx cpsel_ctx;
 
-/* Tunables.  cpsel_config_default() fills the defaults noted here. */
+/* Tunables.  cpsel_config_default() fills the defaults noted here, then applies the operator
+ * overrides CPSEL_ZCAP (z_cap) and CPSEL_MAXIT (max_iters, 1..100000) from the environment when
+ * they are set to an unsigned integer (malformed values are ignored). */
 typedef struct {
   uint64_t z_cap;            /* compaction threshold on the bracket interior count m: the first
                                 pass whose interior m <= z_cap also copies the two halves of the
@@ -239,7 +244,10 @@ cpsel_status cpsel_get_trace(const cpsel_ctx* ctx, cpsel_trace_row* rows, uint32
  * e.g. torch.distributed.broadcast_object_list).  NCCL is resolved at run time from the
  * libnccl.so.2 already loaded in the process (torch's), else from the system. */
 cpsel_status cpsel_nccl_unique_id(void* id_out128);
-/* Collective: every rank calls with the same id, its rank and the world size. */
+/* Collective: every rank calls with the same id, its rank and the world size.  Failure detection:
+ * while a sharded call waits on its collectives it polls ncclCommGetAsyncError and a deadline of
+ * CPSEL_COMM_TIMEOUT_S seconds (read here; default 120); either aborts the communicator
+ * (ncclCommAbort) and fails the call with ENCCL, after which this function must be called again. */
 cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int world);
 /* Loopback transport (SURVEY §4 "G virtual shards on one GPU"): `world` virtual ranks inside ONE
  * process, each a host thread with its own ctx (and stream) on the same device.  The sharded driver
@@ -247,7 +255,7 @@ cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int wo
  * two host barriers.  create: *out <- a group handle owned by the caller (destroy it after every
  * ctx attached to it has been destroyed or re-initialised; the ctxs keep the group alive until
  * then).  comm_init_loopback: attach ctx as `rank` (each rank exactly once).  A rank that does not
- * reach a collective within 120 s breaks the group: every rank's call then fails with ENCCL.
+ * reach a collective within CPSEL_COMM_TIMEOUT_S seconds (read at attach; default 120) breaks the group: every rank's call then fails with ENCCL.
  * Errors: EINVAL (null pointers, rank outside [0, world)), ENCCL (rank already attached). */
 typedef struct cpsel_loopback cpsel_loopback;
 cpsel_status cpsel_loopback_create(int world, cpsel_loopback** out);

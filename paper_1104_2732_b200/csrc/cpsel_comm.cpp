@@ -1,6 +1,7 @@
 #include "cpsel_comm.h"
 
 #include <chrono>
+#include <cstdlib>
 
 namespace cpsel {
 
@@ -100,6 +101,43 @@ const char* Comm::attach_loop(std::shared_ptr<LoopGroup> g, int r) {
   rank = r;
   world = loop->world;
   return nullptr;
+}
+
+const char* Comm::health() const {
+  if (nccl) {
+    const NcclApi& nc = nccl_api();
+    if (!nc.CommGetAsyncError) return nullptr;
+    ncclResult_t a = ncclSuccess;
+    const ncclResult_t r = nc.CommGetAsyncError(nccl, &a);
+    if (r != ncclSuccess) return nc.GetErrorString(r);
+    if (a != ncclSuccess && a != ncclInProgress) return nc.GetErrorString(a);
+    return nullptr;
+  }
+  if (loop) {
+    std::lock_guard<std::mutex> l(loop->mu);
+    if (loop->broken) return "loopback group broken (a peer rank timed out)";
+  }
+  return nullptr;
+}
+
+void Comm::abort() {
+  if (nccl && nccl_api().ok) {
+    if (nccl_api().CommAbort) nccl_api().CommAbort(nccl);
+    nccl = nullptr;  // never CommDestroy an aborted communicator
+  }
+  if (loop) {
+    std::lock_guard<std::mutex> l(loop->mu);
+    loop->broken = true;  // the peers' next (or current) barrier fails instead of hanging
+    loop->cv.notify_all();
+  }
+  release();
+}
+
+double comm_timeout_from_env(double dflt) {
+  const char* e = getenv("CPSEL_COMM_TIMEOUT_S");
+  if (!e) return dflt;
+  const double v = atof(e);
+  return v > 0 ? v : dflt;
 }
 
 void Comm::release() {

@@ -41,7 +41,8 @@ struct Comm {
   std::shared_ptr<LoopGroup> loop;
   int rank = 0, world = 1;
   cudaEvent_t ev_ready = nullptr, ev_done = nullptr;  // loopback: this rank's events
-  double timeout_s = 120.0;
+  double timeout_s = 120.0;  // a collective that has not completed after this long fails the call
+
 
   bool active() const { return nccl != nullptr || loop != nullptr; }
   // out <- the concatenation over ranks q of (q's send, bytes[q]) (bytes[] the same on every rank;
@@ -52,6 +53,15 @@ struct Comm {
   // attach to a loopback group as `rank` (creates the events); nullptr or an error message
   const char* attach_loop(std::shared_ptr<LoopGroup> g, int rank);
   void release();  // destroy the communicator / detach from the group
+  // failure detection while a host waits on a collective: nullptr while healthy, else a message
+  // (an NCCL asynchronous error, e.g. a peer process that died; a broken loopback group)
+  const char* health() const;
+  // tear the communicator down without waiting for peers (after health() or a timeout failed);
+  // the ctx must be re-initialised with cpsel_comm_init* before the next sharded call
+  void abort();
 };
+
+// CPSEL_COMM_TIMEOUT_S (seconds, > 0) overrides Comm::timeout_s at comm init
+double comm_timeout_from_env(double dflt);
 
 }  // namespace cpsel

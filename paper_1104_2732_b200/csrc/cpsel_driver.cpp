@@ -430,8 +430,13 @@ struct GpuBackend : Backend {
   }
   // spin until the kernel published `seq` into the mailbox flag (a failed launch or a kernel that
   // ended without publishing is detected through the stream)
+  // With a communicator attached (sharded calls) the wait also watches the collectives: an NCCL
+  // asynchronous error (a peer process died, a network fault) or no progress for comm.timeout_s
+  // aborts the communicator and fails the call with CPSEL_ENCCL instead of spinning forever.
   cpsel_status wait_mail(const unsigned long long* flag, unsigned long long seq) {
     const volatile unsigned long long* f = flag;
+    const bool watch = ctx->comm.active();
+    const auto t0 = watch ? std::chrono::steady_clock::now() : std::chrono::steady_clock::time_point();
     for (uint32_t i = 1;; ++i) {
       if (*f == seq) {
         std::atomic_thread_fence(std::memory_order_acquire);
@@ -447,6 +452,15 @@ struct GpuBackend : Backend {
           return fail(ctx, CPSEL_EINTERNAL, "kernel finished without publishing its result");
         }
         if (e != cudaErrorNotReady) return fail(ctx, CPSEL_ECUDA, "%s", cudaGetErrorString(e));
+        if (watch && (i & 4095u) == 0u) {
+          const char* bad = ctx->comm.health();
+          const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+          if (bad || waited > ctx->comm.timeout_s) {
+            ctx->comm.abort();
+            return fail(ctx, CPSEL_ENCCL, "sharded collective failed: %s (communicator aborted; re-run comm init)",
+                        bad ? bad : "no progress within the timeout (CPSEL_COMM_TIMEOUT_S)");
+          }
+        }
       }
 #if defined(__x86_64__)
       __builtin_ia32_pause();
@@ -1976,6 +1990,20 @@ void cpsel_config_default(cpsel_config* c) {
   c->pass_cuts = 1;
   c->lms_fused = 1;
   c->device_loop = 0;  // measured slower than the mailbox loop (cpsel.h)
+  // operator overrides: CPSEL_ZCAP, CPSEL_MAXIT (unsigned integers)
+  auto env_u64 = [](const char* name, uint64_t* dst) {
+    const char* e = getenv(name);
+    if (!e || !*e) return;
+    char* end = nullptr;
+    const unsigned long long v = strtoull(e, &end, 0);
+    if (end && *end == '\0') *dst = v;
+  };
+  uint64_t v = c->z_cap;
+  env_u64("CPSEL_ZCAP", &v);
+  c->z_cap = v;
+  v = c->max_iters;
+  env_u64("CPSEL_MAXIT", &v);
+  if (v >= 1 && v <= 100000) c->max_iters = static_cast<uint32_t>(v);
 }
 
 cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
@@ -2239,6 +2267,7 @@ cpsel_status cpsel_comm_init(cpsel_ctx* ctx, const void* id128, int rank, int wo
   NK(nc.CommInitRank(&ctx->comm.nccl, world, id, rank));
   ctx->comm.rank = rank;
   ctx->comm.world = world;
+  ctx->comm.timeout_s = comm_timeout_from_env(120.0);
   return comm_buffers(ctx, world);
 }
 
@@ -2258,6 +2287,7 @@ cpsel_status cpsel_comm_init_loopback(cpsel_ctx* ctx, cpsel_loopback* group, int
   if (!ctx || !group || rank < 0 || rank >= group->g->world) return CPSEL_EINVAL;
   DeviceGuard g(ctx->device);
   if (const char* m = ctx->comm.attach_loop(group->g, rank)) return fail(ctx, CPSEL_ENCCL, "loopback: %s", m);
+  ctx->comm.timeout_s = comm_timeout_from_env(120.0);
   return comm_buffers(ctx, group->g->world);
 }
 

@@ -32,6 +32,8 @@ static void load() {
     g_api.load_error = "libnccl.so.2 lacks a required symbol";
     return;
   }
+  sym(h, "ncclCommGetAsyncError", g_api.CommGetAsyncError);
+  sym(h, "ncclCommAbort", g_api.CommAbort);
   g_api.ok = true;
 }
 

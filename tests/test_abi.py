@@ -49,3 +49,19 @@ def test_host_only_entry_points_without_gpu(lib):
     assert lib.cpsel_status_string(cp.ERANK) == b"rank out of range"
     assert lib.cpsel_select_kth(None, None, 0, 0, 1, None, None) == cp.EINVAL
     assert lib.cpsel_drive_host(None, 1, 0, 1, None, None, None, None, 0, None) == cp.EINVAL
+
+
+def test_config_env_overrides(lib, monkeypatch):
+    """CPSEL_ZCAP / CPSEL_MAXIT override the defaults; malformed values are ignored."""
+    import paper_1104_2732_b200 as cp
+    base = cp.default_config()
+    monkeypatch.setenv("CPSEL_ZCAP", "4096")
+    monkeypatch.setenv("CPSEL_MAXIT", "37")
+    c = cp.default_config()
+    assert c["z_cap"] == 4096 and c["max_iters"] == 37
+    assert {k: v for k, v in c.items() if k not in ("z_cap", "max_iters")} == \
+        {k: v for k, v in base.items() if k not in ("z_cap", "max_iters")}
+    monkeypatch.setenv("CPSEL_ZCAP", "12x")
+    monkeypatch.setenv("CPSEL_MAXIT", "0")
+    c = cp.default_config()
+    assert c["z_cap"] == base["z_cap"] and c["max_iters"] == base["max_iters"]

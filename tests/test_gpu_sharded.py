@@ -197,3 +197,34 @@ def test_sharded_2pow32_on_one_gpu(cp):
         assert v == (float(xd.min()) if kk == 1 else float(xd.max()))
     del xd
     torch.cuda.empty_cache()
+
+
+def test_loopback_missing_peer_fails_instead_of_hanging(cp, monkeypatch):
+    """Failure detection: a rank whose peer never reaches the collective gets ENCCL after
+    CPSEL_COMM_TIMEOUT_S, not a hang; a later, complete group on fresh threads still works."""
+    import time
+    import torch
+    monkeypatch.setenv("CPSEL_COMM_TIMEOUT_S", "2")
+    x = datagen.make("normal", 1 << 20, "f32")
+    xd = torch.from_numpy(x).cuda()
+    grp = cp.LoopbackGroup(2)
+    res = {}
+
+    def lone_rank():
+        with torch.cuda.stream(torch.cuda.Stream()):
+            cp.comm_init_loopback(grp, 0, 0)
+            try:
+                res["value"] = cp.select_kth_sharded(xd, 1000)
+            except Exception as e:  # expected
+                res["err"] = str(e)
+
+    t0 = time.time()
+    t = threading.Thread(target=lone_rank)
+    t.start()
+    t.join(120)
+    assert not t.is_alive(), "the lone rank hung"
+    assert "err" in res and "did not arrive" in res["err"], res
+    assert time.time() - t0 < 60
+    monkeypatch.delenv("CPSEL_COMM_TIMEOUT_S")
+    out = run_virtual(cp, xd, [0, 400_000, 1 << 20], [1000])
+    assert out[0][0][0] == out[1][0][0] == float(O.order_statistic(x, 1000))
