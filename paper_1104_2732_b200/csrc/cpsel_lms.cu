@@ -99,12 +99,13 @@ constexpr uint32_t kIdesc = (1u << 4)              // D: f32
                             | ((uint32_t)(TN >> 3) << 17)
                             | ((uint32_t)(TM >> 4) << 24);
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate,
+                                         uint32_t idesc = kIdesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -258,29 +259,41 @@ constexpr size_t kResidualSmem = 2 * STAGE + 1024 + 128 + 40 * 1024;  // ring + 
 // ------------------------------------------------------------------------------------------
 // Fused residual pass (§8f-2 "fused GEMM-epilogue recompute"): the same 3xTF32 tcgen05 product,
 // transposed — candidates on the TMEM lanes (A = Theta image, 128 candidates per tile), rows on
-// the TMEM columns (B = X image, 256 rows per tile) — so each epilogue thread owns ONE candidate
-// column j and walks 32 consecutive rows per tcgen05.ld.  Nothing of S is stored: per element
-// s = (acc - y_i)^2 is counted against the column's two sample cuts (R23: #s <= t_lo), the
-// ones strictly between them are appended to the column's own buffer z_j (thread-private ring in
-// shared memory, flushed 16 at a time behind one atomicAdd on the column cursor), and the running
-// max (max.NaN: NaN/Inf detection and the upper end of the bracket) is kept.  Work is cut into
-// units (candidate tile, chunk of row tiles) so the per-column counters stay in registers for a
-// whole unit and are flushed once per unit.
+// the TMEM columns (B = X image, 256 rows per operand tile, issued as FS-row sub-tiles into
+// kTStages TMEM accumulators) — so each epilogue thread owns ONE candidate column j and walks 32
+// consecutive rows per tcgen05.ld.  An epilogue warp releases a sub-tile's accumulator (and its y)
+// as soon as both are in registers, before the element work, so the MMA refills it while the
+// warps compute.  Nothing of S is stored: per element s = (acc - y_i)^2 is counted against the
+// column's two sample cuts (R23: #s <= t_lo), and the ones strictly between them are appended to
+// the column's own buffer z_j (thread-private slots in shared memory; a thread holding kFlush
+// writes them out itself behind one atomicAdd on the column cursor).  Work is cut into units
+// (candidate tile, chunk of row tiles) so the per-column counters stay in registers for a whole
+// unit and are flushed once per unit.  (NaN/Inf: the inputs are checked instead, lms_fused_check.)
 //   MODE kFuseCuts : the statistics above (the init pass a1 + R23 cuts + a4 copy of every column)
 //   MODE kFuseStore: s stored to S[slot[j]*n + row] for the columns with slot[j] >= 0 (fallback
 //                    columns, and the parity hook: the S the fused statistics were taken on)
 //   MODE kFuseLts  : sum_{s < m_j} s (fp64) and #{s < m_j} per column (LTS)
 constexpr int kFuseCuts = 0, kFuseStore = 1, kFuseLts = 2;
-constexpr int FN = 256;                    // rows per tile (TMEM columns per accumulator)
-constexpr int kFEpiWarps = 16;             // 4 per TMEM lane quarter, each on 64 of the 256 rows
+constexpr int FN = 256;                    // rows per operand tile (the X image's 256-row tiles)
+#ifndef CPSEL_LMS_FS
+#define CPSEL_LMS_FS 128
+#endif
+constexpr int FS = CPSEL_LMS_FS;           // rows per sub-tile = TMEM columns per accumulator (128 or 256)
+constexpr int kTStages = 512 / FS;         // TMEM accumulator stages (all 512 columns)
+constexpr int kSubs = FN / FS;             // sub-tiles per operand tile
+constexpr int kWR = FS / 4;                // rows per epilogue warp per sub-tile
+constexpr int kChunks = kWR / 32;          // 32-row chunks (one tcgen05.ld each) per warp per sub-tile
+constexpr int kFEpiWarps = 16;             // 4 per TMEM lane quarter, each on 32 of a sub-tile's 128 rows
 constexpr int kFYWarp = 2 + kFEpiWarps;    // the warp that stages y for each accumulator stage
 constexpr int kFStages = 2;                // operand (Theta + X tile) stages in shared memory
 constexpr int kFThreads = 32 * (3 + kFEpiWarps);
-constexpr int kFRows = FN / 4;             // rows per epilogue warp per tile
-constexpr int kRing = 48;                  // staging slots per epilogue thread (32 + up to 15 pending + 1 half)
-constexpr int kFlush = 32;                 // elements per flush (one 128-byte store of the warp)
+constexpr int kRing = 48;                  // staging slots per epilogue thread (kFlush - 1 pending + 16 of a half chunk)
+constexpr int kFlush = 32;                 // elements per flush (one thread's 128 bytes)
 constexpr uint32_t kSlot = 4;              // a thread's slots are consecutive words ...
-constexpr uint32_t kLaneStage = 4 * (kRing + 1);  // ... skewed by one word per thread (no bank conflicts)
+constexpr uint32_t kLaneStage = 4 * (kRing + 4);  // ... 16-byte aligned per thread (conflict-free LDS.128 quarter-warps)
+constexpr int kFBarBytes = 256;            // mbarriers + the TMEM address slot
+// M = 128 candidates, N = FS rows
+constexpr uint32_t kIdescSub = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(FS >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
 
 struct FusedArgs {
   const unsigned char* a_img;   // Theta: n_ct x 16 KB (128 candidates per tile)
@@ -332,20 +345,90 @@ __device__ __forceinline__ void cut_elem(float s, uint32_t lo1, uint32_t w, uint
       : "memory");
 }
 
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
+// Write `cnt` staged elements of this thread (its slots from base_sa on) to zc[0..cnt) within room.
+__device__ __forceinline__ void stage_out(uint32_t base_sa, uint32_t cnt, float* zc, uint64_t room) {
+  for (uint32_t o = 0; o < cnt; o += 4) {
+    const float4 q = lds128(base_sa + o * kSlot);
+    const float qv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (o + i < cnt && o + i < room) zc[o + i] = qv[i];
+  }
+}
+
+// The 16 elements r[h*16 .. h*16+15] of a chunk (rows beyond nvalid enter as +Inf), then the flush
+// of every thread holding >= kFlush staged elements (at most kFlush - 1 + 16 < kRing pending): all
+// such threads at once, each writing ITS first kFlush to its column's copy (16-byte shared loads of
+// its own slots, no cross-lane traffic: one pass of the warp however many lanes flush) and moving
+// the rest to the front of its slots.
+template <bool FULL>
+__device__ __forceinline__ void cut_half(const uint32_t* r, int h, const ulonglong2* yv, int nvalid, uint32_t lo1,
+                                         uint32_t wcut, uint32_t& le, uint32_t& le2, uint32_t& ta,
+                                         uint32_t base_sa, const FusedArgs& a, uint32_t j, float* zcol) {
+#pragma unroll
+  for (int jj = 0; jj < 16; jj += 2) {
+    const int i = h * 16 + jj;
+    const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+    float s0, s1;
+    resid2(r[i], r[i + 1], y01, s0, s1);
+    if (FULL) {
+      cut_elem(s0, lo1, wcut, le, ta);
+      cut_elem(s1, lo1, wcut, le2, ta);  // two counters: half the dependent chain
+    } else {
+      cut_elem(i < nvalid ? s0 : __int_as_float(0x7f800000), lo1, wcut, le, ta);
+      cut_elem(i + 1 < nvalid ? s1 : __int_as_float(0x7f800000), lo1, wcut, le, ta);
+    }
+  }
+  const uint32_t cnt = (ta - base_sa) / kSlot;
+  if (__any_sync(0xffffffffu, cnt >= kFlush)) {
+    if (cnt >= kFlush) {
+      const unsigned long long pos = atomicAdd(a.cursor + j, (unsigned long long)kFlush);
+      float* dst = zcol + pos;
+      if (pos + kFlush <= a.zcap) {
+#pragma unroll
+        for (int v = 0; v < kFlush / 4; ++v) {
+          const float4 q = lds128(base_sa + v * 16);
+          dst[4 * v] = q.x;
+          dst[4 * v + 1] = q.y;
+          dst[4 * v + 2] = q.z;
+          dst[4 * v + 3] = q.w;
+        }
+      } else {
+        stage_out(base_sa, kFlush, dst, pos < a.zcap ? a.zcap - pos : 0);
+      }
+#pragma unroll
+      for (int v = 0; v < (kRing - kFlush) / 4; ++v)  // the rest (<= 15) to the front
+        if ((uint32_t)(kFlush + 4 * v) < cnt) sts128(base_sa + v * 16, lds128(base_sa + kFlush * kSlot + v * 16));
+      ta -= kFlush * kSlot;
+    }
+  }
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // kFStages operand stages (the loads run up to kFStages-1 tiles ahead), 2 TMEM accumulators
+  // kFStages operand stages (the loads run up to kFStages-1 tiles ahead); kTStages TMEM
+  // accumulators of one 128-row sub-tile each (the epilogue warps may drift up to kTStages-1
+  // sub-tiles apart before the MMA has to wait for the slowest)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kFStages * STAGE);
   uint64_t* full = bars;                    // [kFStages]
   uint64_t* empty = bars + kFStages;        // [kFStages]
-  uint64_t* tfull = bars + 2 * kFStages;    // [2]
-  uint64_t* tempty = tfull + 2;             // [2]
-  uint64_t* yfull = tempty + 2;             // [2]: y of the tile in accumulator stage s is in ybuf[s]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yfull + 2);
-  float* ybuf = reinterpret_cast<float*>(smem + kFStages * STAGE + 128);  // [2][FN]
-  const uint32_t ring_sa = smem_u32(smem + kFStages * STAGE + 128 + 2 * FN * 4);  // 512 threads x kLaneStage B
+  uint64_t* tfull = bars + 2 * kFStages;    // [kTStages]
+  uint64_t* tempty = tfull + kTStages;      // [kTStages]
+  uint64_t* yfull = tempty + kTStages;      // [kTStages]: y of the sub-tile in accumulator stage s is in ybuf[s]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(yfull + kTStages);
+  float* ybuf = reinterpret_cast<float*>(smem + kFStages * STAGE + kFBarBytes);  // [kTStages][FS]
+  const uint32_t ring_sa = smem_u32(smem + kFStages * STAGE + kFBarBytes + kTStages * FS * 4);  // 512 threads x kLaneStage B
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t units = a.n_ct_list * a.n_chunks;
 
@@ -354,7 +437,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kTStages; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], kFEpiWarps);
       mbar_init(&yfull[i], 1);
@@ -372,9 +455,9 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == kFYWarp) {
-    // ---------------- y stager: the tile's 256 y values into ybuf[s] once the epilogue released
+    // ---------------- y stager: the sub-tile's 128 y values into ybuf[s] once the epilogue released
     //                  accumulator stage s (the epilogue reads them as shared-memory broadcasts).
-    //                  A plain warp copy (1 KB per tile; 2 x 16 B per lane), released to the
+    //                  A plain warp copy (512 B per sub-tile; 16 B per lane), released to the
     //                  epilogue by an mbarrier arrive: ordinary generic-proxy accesses ordered by
     //                  the stage barriers (a bulk copy here was an async-proxy write racecheck
     //                  cannot see ordered behind the epilogue's reads)
@@ -382,16 +465,18 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
     for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
       const uint32_t ct = a.ct_list[u % a.n_ct_list], ch = u / a.n_ct_list;
       const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
-      for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
-        const uint32_t s = it & 1, ph = (it >> 1) & 1;
+      for (uint32_t rt = r0; rt < r1; ++rt) {
         const float4* src = reinterpret_cast<const float4*>(a.y + ((size_t)ct * a.b_ct_stride + rt) * FN);
-        const float4 y0 = __ldg(src + lane), y1 = __ldg(src + 32 + lane);  // loads ahead of the wait
-        mbar_wait_sleep(&tempty[s], ph ^ 1);
-        float4* dst = reinterpret_cast<float4*>(ybuf + s * FN);
-        dst[lane] = y0;
-        dst[32 + lane] = y1;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&yfull[s]);
+        const float4 yh[2] = {__ldg(src + lane), __ldg(src + 32 + lane)};  // loads ahead of the waits
+#pragma unroll
+        for (int h = 0; h < kSubs; ++h, ++it) {
+          const uint32_t s = it % kTStages, ph = (it / kTStages) & 1;
+          mbar_wait_sleep(&tempty[s], ph ^ 1);
+#pragma unroll
+          for (int c = 0; c < FS / 128; ++c) reinterpret_cast<float4*>(ybuf + s * FS)[c * 32 + lane] = yh[h * (FS / 128) + c];
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&yfull[s]);
+        }
       }
     }
   } else if (warp == 0) {
@@ -411,37 +496,44 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer: D[j][i] = theta_j . x_i, the residual kernel's three products
-    uint32_t it = 0;
+    // ---------------- MMA issuer: D[j][i] = theta_j . x_i, the residual kernel's three products, per
+    //                  128-row half of the operand tile (rows 128h.. of the hi / lo images start
+    //                  8 KB in: 16 core-matrix row groups of 512 B)
+    uint32_t it = 0, ot = 0;
     for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
       const uint32_t ch = u / a.n_ct_list;
       const uint32_t r0 = ch * a.rt_per_unit, r1 = min(a.n_rt, r0 + a.rt_per_unit);
-      for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
-        const uint32_t s = it & 1, ph = (it >> 1) & 1;                       // TMEM stage
-        const uint32_t ss = it % kFStages, sph = (it / kFStages) & 1;       // operand stage
-        mbar_wait_sleep(&tempty[s], ph ^ 1);
+      for (uint32_t rt = r0; rt < r1; ++rt, ++ot) {
+        const uint32_t ss = ot % kFStages, sph = (ot / kFStages) & 1;  // operand stage
         mbar_wait_sleep(&full[ss], sph);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        if (lane == 0) {
-          const uint32_t d = tmem_base + s * FN;
-          const unsigned char* A = smem + ss * STAGE;
-          const unsigned char* B = smem + ss * STAGE + A_IMG;
-          for (int ks = 0; ks < 2; ++ks) {
-            const uint64_t ahi = sdesc(A + ks * 256), alo = sdesc(A + A_HALF + ks * 256);
-            const uint64_t bhi = sdesc(B + ks * 256), blo = sdesc(B + B_HALF + ks * 256);
-            mma_tf32(d, ahi, blo, ks > 0 ? 1u : 0u);  // x_lo * theta_hi (small terms first)
-            mma_tf32(d, alo, bhi, 1u);                // x_hi * theta_lo
-            mma_tf32(d, ahi, bhi, 1u);
+        const unsigned char* A = smem + ss * STAGE;
+        const unsigned char* B = smem + ss * STAGE + A_IMG;
+#pragma unroll
+        for (int h = 0; h < kSubs; ++h, ++it) {
+          const uint32_t s = it % kTStages, ph = (it / kTStages) & 1;  // TMEM stage
+          mbar_wait_sleep(&tempty[s], ph ^ 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            const uint32_t d = tmem_base + s * FS;
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint64_t ahi = sdesc(A + ks * 256), alo = sdesc(A + A_HALF + ks * 256);
+              const uint64_t bhi = sdesc(B + h * (FS * 64) + ks * 256);
+              const uint64_t blo = sdesc(B + B_HALF + h * (FS * 64) + ks * 256);
+              mma_tf32(d, ahi, blo, ks > 0 ? 1u : 0u, kIdescSub);  // x_lo * theta_hi (small terms first)
+              mma_tf32(d, alo, bhi, 1u, kIdescSub);                // x_hi * theta_lo
+              mma_tf32(d, ahi, bhi, 1u, kIdescSub);
+            }
+            mma_commit(&tfull[s]);
           }
-          mma_commit(&empty[ss]);
-          mma_commit(&tfull[s]);
+          __syncwarp();
         }
+        if (lane == 0) mma_commit(&empty[ss]);
         __syncwarp();
       }
     }
   } else if (warp >= 2) {
     // ---------------- epilogue: warps 2..17 -> TMEM lane quarter (warp % 4) = 32 candidates,
-    //                  row quarter rq: rows [rq*64, rq*64+64) of the tile
+    //                  row quarter rq: rows [rq*32, rq*32+32) of each 128-row sub-tile
     const int q = warp & 3;
     const int rq = (warp - 2) >> 2;
     const int e = threadIdx.x - 64;  // 0..511: this thread's staging slots
@@ -465,143 +557,91 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
       uint32_t le = 0, le2 = 0;
       double lsum = 0.0;
       uint32_t ta = base_sa;  // next free staging slot
-      for (uint32_t rt = r0; rt < r1; ++rt, ++it) {
-        const uint32_t s = it & 1, ph = (it >> 1) & 1;
-        const uint64_t row0 = (uint64_t)rt * FN + rq * kFRows;
-        const bool tile_full = row0 + kFRows <= a.n;
-        mbar_wait_sleep(&tfull[s], ph);
-        mbar_wait_sleep(&yfull[s], ph);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * FN + rq * kFRows;
-        const uint32_t ys_sa = smem_u32(ybuf + s * FN + rq * kFRows);
-#pragma unroll 1
-        for (uint32_t c0 = 0; c0 < kFRows; c0 += 32) {
-          uint32_t r[32];
-          TMEM_LD32(taddr + c0, r);
-          const uint64_t rowc = row0 + c0;
-          ulonglong2 yv[8];
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {  // shared-memory broadcast (LDS.128)
-            const uint32_t ya = ys_sa + (c0 / 4 + v) * 16;
-            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(yv[v].x), "=l"(yv[v].y) : "r"(ya));
-          }
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          int nvalid = 32;  // only the last row tile is ragged
-          if (!tile_full) nvalid = rowc + 32 <= a.n ? 32 : (rowc >= a.n ? 0 : (int)(a.n - rowc));
-          if (MODE == kFuseCuts) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              if (nvalid == 32) {
-#pragma unroll
-                for (int jj = 0; jj < 16; jj += 2) {
-                  const int i = h * 16 + jj;
-                  const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
-                  float s0, s1;
-                  resid2(r[i], r[i + 1], y01, s0, s1);
-                  cut_elem(s0, lo1, wcut, le, ta);
-                  cut_elem(s1, lo1, wcut, le2, ta);  // two counters: half the dependent chain
-                }
-              } else {  // the ragged end of x: padded rows enter as +Inf
-#pragma unroll
-                for (int jj = 0; jj < 16; jj += 2) {
-                  const int i = h * 16 + jj;
-                  const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
-                  float s0, s1;
-                  resid2(r[i], r[i + 1], y01, s0, s1);
-                  cut_elem(i < nvalid ? s0 : __int_as_float(0x7f800000), lo1, wcut, le, ta);
-                  cut_elem(i + 1 < nvalid ? s1 : __int_as_float(0x7f800000), lo1, wcut, le, ta);
-                }
-              }
-              // warp-cooperative flush of every thread holding >= kFlush staged elements (at most
-              // 31 + 16 < kRing pending): each owner's 32 go to its column's copy as ONE coalesced
-              // 128-byte store of the warp, the rest moves to the front of its slots.  (Two operand
-              // stages instead of three buy the larger ring: half as many flush events as with 16.)
-              const bool need = ta - base_sa >= kFlush * kSlot;
-              unsigned fm = __ballot_sync(0xffffffffu, need);
-              if (fm) {
-                __syncwarp();  // every lane's staged stores visible to the warp before the reads
-                unsigned long long pos = 0;
-                if (need) pos = atomicAdd(a.cursor + j, (unsigned long long)kFlush);
-                while (fm) {
-                  const int src = __ffs(fm) - 1;
-                  fm &= fm - 1;
-                  const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, src);
-                  const uint32_t cnt = (__shfl_sync(0xffffffffu, ta, src) - lb) / kSlot;
-                  const unsigned long long pl = __shfl_sync(0xffffffffu, pos, src);
-                  float v, v2 = 0.f;
-                  const bool mv = (uint32_t)(kFlush + lane) < cnt;
-                  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + lane * kSlot));
-                  if (mv) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v2) : "r"(lb + (kFlush + lane) * kSlot));
-                  __syncwarp();
-                  if (pl + lane < a.zcap) a.z[(size_t)(j - lane + src) * a.zcap + pl + lane] = v;
-                  if (mv) asm volatile("st.shared.f32 [%0], %1;" ::"r"(lb + lane * kSlot), "f"(v2));
-                  __syncwarp();
-                }
-                if (need) ta -= kFlush * kSlot;
-              }
-            }
-          } else if (MODE == kFuseStore) {
-            if (slot >= 0) {
-              float* dst = a.S + (size_t)slot * a.n + rowc;
-              if (nvalid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // 8 x 16-byte stores
-#pragma unroll
-                for (int i = 0; i < 32; i += 4) {
-                  float s0, s1, s2, s3;
-                  resid2(r[i], r[i + 1], yv[i >> 2].x, s0, s1);
-                  resid2(r[i + 2], r[i + 3], yv[i >> 2].y, s2, s3);
-                  __stcs(reinterpret_cast<float4*>(dst + i), make_float4(s0, s1, s2, s3));
-                }
-              } else {
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                  const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
-                  float s0, s1;
-                  resid2(r[i], r[i + 1], y01, s0, s1);
-                  if (i < nvalid) __stcs(dst + i, s0);
-                  if (i + 1 < nvalid) __stcs(dst + i + 1, s1);
-                }
-              }
-            }
-          } else {
-            unsigned c = 0;
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
-              float s0, s1;
-              resid2(r[i], r[i + 1], y01, s0, s1);
-              if (i < nvalid && s0 < mj) { lsum += (double)s0; ++c; }
-              if (i + 1 < nvalid && s1 < mj) { lsum += (double)s1; ++c; }
-            }
-            le += c;
-          }
+      float* zcol = a.z + (size_t)(col_ok ? j : 0) * a.zcap;
+      // rows left in x from this unit's first row of this warp (only the last row tile is ragged)
+      const uint64_t urow = (uint64_t)r0 * FN + rq * kWR;
+      const uint64_t ur_left = a.n > urow ? a.n - urow : 0;
+      for (uint32_t cc = 0; cc < kSubs * kChunks * (r1 - r0); ++cc) {
+        const uint32_t c = cc % kChunks;  // chunk of this warp's rows in the sub-tile
+        const uint32_t s = it % kTStages, ph = (it / kTStages) & 1;
+        const uint64_t roff = (uint64_t)(cc / kChunks) * FS + c * 32;  // this chunk starts at urow + roff
+        const int nvalid = ur_left >= roff + 32 ? 32 : (ur_left > roff ? (int)(ur_left - roff) : 0);
+        if (c == 0) {
+          mbar_wait_sleep(&tfull[s], ph);
+          mbar_wait_sleep(&yfull[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
         }
-        asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[s]);
+        const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * FS + rq * kWR + c * 32;
+        const uint32_t ys_sa = smem_u32(ybuf + s * FS + rq * kWR + c * 32);
+        uint32_t r[32];
+        TMEM_LD32(taddr, r);
+        ulonglong2 yv[8];
+#pragma unroll
+        for (int v = 0; v < 8; ++v)  // shared-memory broadcast (LDS.128)
+          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(yv[v].x), "=l"(yv[v].y) : "r"(ys_sa + v * 16));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c == kChunks - 1) {
+          // the sub-tile's last accumulator columns and y are in registers: release the stage
+          // before the element work
+          asm volatile("tcgen05.fence::before_thread_sync;");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[s]);
+          ++it;
+        }
+        if (MODE == kFuseCuts) {
+          if (nvalid == 32) {
+            cut_half<true>(r, 0, yv, 32, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+            cut_half<true>(r, 1, yv, 32, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+          } else {  // the ragged end of x: padded rows enter as +Inf
+            cut_half<false>(r, 0, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+            cut_half<false>(r, 1, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+          }
+        } else if (MODE == kFuseStore) {
+          if (slot >= 0) {
+            const uint64_t rowc = urow + roff;
+            float* dst = a.S + (size_t)slot * a.n + rowc;
+            if (nvalid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // 8 x 16-byte stores
+#pragma unroll
+              for (int i = 0; i < 32; i += 4) {
+                float s0, s1, s2, s3;
+                resid2(r[i], r[i + 1], yv[i >> 2].x, s0, s1);
+                resid2(r[i + 2], r[i + 3], yv[i >> 2].y, s2, s3);
+                __stcs(reinterpret_cast<float4*>(dst + i), make_float4(s0, s1, s2, s3));
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) {
+                const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+                float s0, s1;
+                resid2(r[i], r[i + 1], y01, s0, s1);
+                if (i < nvalid) __stcs(dst + i, s0);
+                if (i + 1 < nvalid) __stcs(dst + i + 1, s1);
+              }
+            }
+          }
+        } else {
+          unsigned c = 0;
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+            float s0, s1;
+            resid2(r[i], r[i + 1], y01, s0, s1);
+            if (i < nvalid && s0 < mj) { lsum += (double)s0; ++c; }
+            if (i + 1 < nvalid && s1 < mj) { lsum += (double)s1; ++c; }
+          }
+          le += c;
+        }
       }
       // end of unit: flush this column's counters and the rest of its staging slots
       if (MODE == kFuseCuts) {
         const uint32_t cnt = (ta - base_sa) / kSlot;
-        unsigned long long pos = 0;
         if (col_ok) {
           atomicAdd(a.le + j, (unsigned long long)le + le2);
-          if (cnt) pos = atomicAdd(a.cursor + j, (unsigned long long)cnt);
-        }
-        unsigned fm = __ballot_sync(0xffffffffu, cnt > 0);
-        __syncwarp();  // every lane's staged stores visible to the warp before the reads
-        while (fm) {  // cooperative write-out of every thread's remaining staged elements
-          const int L = __ffs(fm) - 1;
-          fm &= fm - 1;
-          const uint32_t lb = __shfl_sync(0xffffffffu, base_sa, L);
-          const uint32_t cl = __shfl_sync(0xffffffffu, cnt, L);
-          const unsigned long long pl = __shfl_sync(0xffffffffu, pos, L);
-          for (uint32_t o = lane; o < cl; o += 32) {  // (up to kRing - 1 pending)
-            float v;
-            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(lb + o * kSlot));
-            if (pl + o < a.zcap) a.z[(size_t)(j - lane + L) * a.zcap + pl + o] = v;
+          if (cnt) {
+            const unsigned long long pos = atomicAdd(a.cursor + j, (unsigned long long)cnt);
+            stage_out(base_sa, cnt, zcol + pos, pos < a.zcap ? a.zcap - pos : 0);
           }
         }
-        __syncwarp();
       } else if (MODE == kFuseLts && col_ok) {
         atomicAdd(a.le + j, (unsigned long long)le);
         a.sum[((size_t)ch * 4 + rq) * a.C + j] = lsum;  // fixed-order reduction afterwards
@@ -615,7 +655,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   }
 }
 
-constexpr size_t kFusedSmem = kFStages * STAGE + 1024 + 128 + 2 * FN * 4 + (size_t)kFEpiWarps * 32 * kLaneStage;  // ring, barriers, y, staging
+constexpr size_t kFusedSmem = kFStages * STAGE + 1024 + kFBarBytes + kTStages * FS * 4 + (size_t)kFEpiWarps * 32 * kLaneStage;  // ring, barriers, y, staging
 
 __global__ void pad_copy_kernel(const float* __restrict__ src, uint64_t n, float* __restrict__ dst, uint64_t n_pad) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += (uint64_t)gridDim.x * blockDim.x)
