@@ -2669,21 +2669,37 @@ __device__ void batch_sample_cuts(BatchState& st, unsigned* hist, const float* z
 // rows (computed by the fused tensor-core kernel in store mode: exactly elements of S).  Per column,
 // the bin edges around the sample order statistics of ranks q -/+ (3.5 sd + 2) and q (q the target
 // rank k scaled to the sample, as batch_sample_cuts) -> cuts[4j .. 4j+2] = t_lo, t_hi, t_mid.  Two
-// digit rounds on the order-preserving keys below their top bit (set for every s >= +0): an 11-bit
-// histogram of all keys (exponent + 3 mantissa bits), then 11-bit histograms of the
-// keys in each target's bin; t_lo is the lower edge of the lo target's final bin (<= that sample
-// order statistic), t_hi the upper edge of the hi target's (>=): cuts at most 2^9 key units (2^-14
-// relative) wider than the exact sample quantiles, which is all a cut needs — the
-// fused pass counts exactly at whatever values they are.  One CTA of 1024 threads per column.
+// digit rounds on the order-preserving keys RELATIVE to the column's smallest sample key kmin:
+// round 0 bins d = key - kmin by its top 11 significant bits (bin width 2^sh, sh from the column's
+// key span, so the 2048 bins cover the sample evenly in key space — the squared residuals of one
+// candidate share few exponents, and top-bits bins would pile most of them into a handful of
+// contended shared-memory counters), round 1 the next 11 bits of d within each target's bin; t_lo
+// is the lower edge of the lo target's final bin (<= that sample order statistic), t_hi the upper
+// edge of the hi target's (>=): cuts at most 2^max(0, sh-11) key units wider than the exact sample
+// quantiles, which is all a cut needs — the fused pass counts exactly at whatever values they are.
+// One CTA of 1024 threads per column.
+// Each CTA walks its columns with the next column's samples prefetched into shared memory by one
+// bulk copy (double-buffered) while the current one is histogrammed; the counters take predicated
+// shared reductions (no divergent branches).
 constexpr int kCutThreads = 1024;
 constexpr int kCutMaxPer = 16;   // <= 16384 samples
+constexpr size_t kCutSmem = 2 * (size_t)kCutThreads * kCutMaxPer * 4 + 64;  // two column buffers + 2 mbarriers
+__device__ __forceinline__ void red_shared_add1(uint32_t addr, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], 1;\n\t}" ::"r"(addr), "r"((int)p)
+               : "memory");
+}
 __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* __restrict__ Ss, uint32_t ms,
                                                                   uint64_t n, uint32_t C, uint64_t k,
                                                                   float* __restrict__ cuts) {
   __shared__ unsigned hist[3][2048];
   __shared__ unsigned wsum[3][32];
   __shared__ unsigned sel[3][2];
+  __shared__ unsigned wmin[32], wmax[32];
+  extern __shared__ __align__(16) unsigned char cut_smem[];
+  float* buf = reinterpret_cast<float*>(cut_smem);  // [2][kCutThreads * kCutMaxPer]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cut_smem + 2 * (size_t)kCutThreads * kCutMaxPer * 4);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t col_bytes = ms * 4u;  // a multiple of 16 (ms is a multiple of 256)
   unsigned rank[3];
   {
     const double md = (double)ms;
@@ -2694,29 +2710,76 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
     rank[1] = qh >= md ? ms - 1 : (unsigned)qh;
     rank[2] = qm < 0 ? 0u : (qm >= md ? ms - 1 : (unsigned)qm);
   }
-  for (uint32_t j = blockIdx.x; j < C; j += gridDim.x) {
-    const float* col = Ss + (size_t)j * ms;
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < C) {
+    mbar_expect_tx(&bar[0], col_bytes);
+    bulk_g2s(buf, Ss + (size_t)blockIdx.x * ms, col_bytes, &bar[0]);
+  }
+  uint32_t it = 0;
+  for (uint32_t j = blockIdx.x; j < C; j += gridDim.x, ++it) {
+    const uint32_t b = it & 1;
+    mbar_wait(&bar[b], (it >> 1) & 1);
+    const float4* cb = reinterpret_cast<const float4*>(buf + (size_t)b * kCutThreads * kCutMaxPer);
     unsigned key[kCutMaxPer];
+    unsigned kmn = 0xffffffffu, kmx = 0u;
 #pragma unroll
-    for (int u = 0; u < kCutMaxPer; ++u) {
-      const uint32_t i = tid + u * kCutThreads;
-      key[u] = i < ms ? (unsigned)okey(__ldcs(col + i)) : 0xffffffffu;  // padding sorts last
+    for (int v = 0; v < kCutMaxPer / 4; ++v) {  // element (v * kCutThreads + tid) * 4 + c: order is irrelevant
+      const uint32_t e4 = v * kCutThreads + tid;
+      const float4 q = cb[e4];
+      const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const bool ok = e4 * 4 + c < ms;
+        key[4 * v + c] = (unsigned)okey(qq[c]);
+        if (ok) {
+          kmn = min(kmn, key[4 * v + c]);
+          kmx = max(kmx, key[4 * v + c]);
+        }
+      }
     }
+    kmn = __reduce_min_sync(0xffffffffu, kmn);
+    kmx = __reduce_max_sync(0xffffffffu, kmx);
+    if (lane == 0) { wmin[wid] = kmn; wmax[wid] = kmx; }
+    for (int i = tid; i < 3 * 2048; i += kCutThreads) (&hist[0][0])[i] = 0u;
+    __syncthreads();  // every thread has its keys: buffer b is free for the column after next
+    if (tid == 0 && j + gridDim.x < C) {
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bar[b ^ 1], col_bytes);
+      bulk_g2s(buf + (size_t)(b ^ 1) * kCutThreads * kCutMaxPer, Ss + (size_t)(j + gridDim.x) * ms, col_bytes,
+               &bar[b ^ 1]);
+    }
+    kmn = __reduce_min_sync(0xffffffffu, wmin[lane]);
+    kmx = __reduce_max_sync(0xffffffffu, wmax[lane]);
+    // d = key - kmin < 2^span_bits; round 0 takes d >> sh0 (11 bits), round 1 the bits below
+    const unsigned span = kmx - kmn;
+    const int span_bits = span ? 32 - __clz(span) : 0;
+    const int sh0 = span_bits > 11 ? span_bits - 11 : 0;
+    const int sh1 = sh0 > 11 ? sh0 - 11 : 0;
+    const unsigned m1 = (1u << (sh0 - sh1)) - 1u;  // round-1 digit: the bits of d below the round-0 bin
+    const uint32_t h0 = smem_u32(&hist[0][0]), h1 = smem_u32(&hist[1][0]), h2 = smem_u32(&hist[2][0]);
     unsigned bin[3] = {0u, 0u, 0u}, rk[3] = {rank[0], rank[1], rank[2]};
 #pragma unroll 1
     for (int round = 0; round < 2; ++round) {
-      const int nh = round == 0 ? 1 : 3;
-      for (int b = tid; b < nh * 2048; b += kCutThreads) (&hist[0][0])[b] = 0u;
-      __syncthreads();
+      if (round == 1) {
+        for (int i = tid; i < 2048; i += kCutThreads) hist[0][i] = 0u;  // (1, 2 still zero)
+        __syncthreads();
+      }
 #pragma unroll
       for (int u = 0; u < kCutMaxPer; ++u) {
+        const bool ok = ((u >> 2) * kCutThreads + tid) * 4 + (u & 3) < ms;
+        const unsigned d = key[u] - kmn;
         if (round == 0) {
-          atomicAdd(&hist[0][(key[u] >> 20) & 2047u], 1u);
+          red_shared_add1(h0 + 4u * (d >> sh0), ok);
         } else {
-          const unsigned top = (key[u] >> 20) & 2047u, d = (key[u] >> 9) & 2047u;
-#pragma unroll
-          for (int t = 0; t < 3; ++t)
-            if (top == bin[t]) atomicAdd(&hist[t][d], 1u);
+          const unsigned top = d >> sh0, dd = 4u * ((d >> sh1) & m1);
+          red_shared_add1(h0 + dd, ok && top == bin[0]);
+          red_shared_add1(h1 + dd, ok && top == bin[1]);
+          red_shared_add1(h2 + dd, ok && top == bin[2]);
         }
       }
       __syncthreads();
@@ -2763,15 +2826,16 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
-        bin[t] = round == 0 ? sel[t][0] : ((bin[t] << 11) | sel[t][0]);
+        bin[t] = round == 0 ? sel[t][0] : ((bin[t] << (sh0 - sh1)) | sel[t][0]);
         rk[t] -= sel[t][1];
       }
       __syncthreads();
     }
-    if (tid == 0) {  // bin[t] = key bits 30..9 of the target (bit 31 is set: every s >= +0)
-      cuts[4 * (size_t)j] = (float)from_key_f32(0x80000000u | (bin[0] << 9));
-      cuts[4 * (size_t)j + 1] = (float)from_key_f32(0x80000000u | (bin[1] << 9) | 511u);
-      cuts[4 * (size_t)j + 2] = (float)from_key_f32(0x80000000u | (bin[2] << 9) | 256u);
+    if (tid == 0) {  // bin[t] = d >> sh1 of the target: its key lies in kmin + [bin << sh1, (bin + 1) << sh1)
+      const unsigned w1 = (1u << sh1) - 1u;
+      cuts[4 * (size_t)j] = (float)from_key_f32(kmn + (bin[0] << sh1));
+      cuts[4 * (size_t)j + 1] = (float)from_key_f32(kmn + (bin[1] << sh1) + w1);
+      cuts[4 * (size_t)j + 2] = (float)from_key_f32(kmn + (bin[2] << sh1) + (w1 >> 1));
       cuts[4 * (size_t)j + 3] = 0.f;
     }
   }
@@ -4301,10 +4365,13 @@ cudaError_t launch_lms_cuts(const float* Ss, uint32_t ms, uint64_t n, uint32_t C
   int dev = 0, sms = 148, b = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lms_cuts_kernel, kCutThreads, 0);
+  if (ms % 256) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(lms_cuts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCutSmem);
+  if (e != cudaSuccess) return e;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, lms_cuts_kernel, kCutThreads, kCutSmem);
   uint32_t grid = (uint32_t)(sms * (b > 0 ? b : 1));
   if (grid > C) grid = C;
-  lms_cuts_kernel<<<grid, kCutThreads, 0, st>>>(Ss, ms, n, C, k, cuts);
+  lms_cuts_kernel<<<grid, kCutThreads, kCutSmem, st>>>(Ss, ms, n, C, k, cuts);
   return cudaGetLastError();
 }
 
