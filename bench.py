@@ -251,15 +251,16 @@ def kelley_side(cp, torch, datagen, dev, dists, log2n, peak, reps=3):
                           "select": info2["kernel_ms_select"]},
             "classes": trace_classes(rows, n, 4, peak)}
         del x
-    # the paper's outlier claim (P:L413 vs P:L416, Fig. 4): 100 values of 1e3 / 1e9 among uniform
-    # data, the cutting plane against the bisection comparison driver (driver=1)
+    # the paper's outlier claim (P:L413-414 vs P:L416, Fig. 4): 100 values of 1e3 / 1e9 among uniform
+    # data, the cutting plane against the comparison drivers: bisection (driver=1), Brent's
+    # root finder (2) and Brent's minimisation (3)
     import datagen as dg
     x = dg.make("uniform", n, "f32", device=dev)
     pos = torch.randperm(n, generator=torch.Generator().manual_seed(dg.SEED))[:100].to(dev)
     out["outliers"] = {}
     for mag in (1e3, 1e9):
         x[pos] = mag
-        for name, drv in (("kelley", 0), ("bisection", 1), ("brent_root", 2)):
+        for name, drv in (("kelley", 0), ("bisection", 1), ("brent_root", 2), ("brent_min", 3)):
             cp.set_config(dev.index, record_timing=0, driver=drv, **cfg)
             cp.select_kth(x, k)
             e0, e1 = _ev(torch)

@@ -98,7 +98,11 @@ typedef struct {
                                 range, P:L413 — the outlier-sensitivity demonstration).  2: Brent's
                                 root finder (Numerical Recipes' zbrent) on
                                 f(t) = c_lt(t) + c_le(t) - 2k + 1 proposing the points instead, the
-                                same passes and exact bracket.  Default 0 */
+                                same passes and exact bracket.  3: Brent's minimisation (Numerical
+                                Recipes' brent on F_k: parabolic steps, golden section
+                                when they fail; its own bracket intersected with the exact one, R37)
+                                proposing the points; needs F at every pass (init_cut = 0, or
+                                objective = 1), else the call fails with CPSEL_EINVAL.  Default 0 */
 } cpsel_config;
 
 /* Per-call report (SPEC 'SelectionResult': iterations, reductions). */
@@ -158,7 +162,8 @@ typedef struct {
   uint64_t written;       /* elements this pass wrote (compaction of both bracket halves) */
   uint32_t kind;          /* 0 Kelley step (interior mean, R4), 1 ordered-key bisection safeguard,
                              2 the init pass's extra cut (R23), 3 a two-cut pass (R26), 4 a step of
-                             the bisection driver (driver = 1), 5 of Brent's root finder (driver 2) */
+                             the bisection driver (driver = 1), 5 of Brent's root finder (driver 2),
+                             6 of Brent's minimisation (driver 3) */
   uint32_t compacted;     /* 1 if this pass also wrote z */
   double kernel_ms;       /* record_timing: CUDA-event duration of this pass's kernel */
 } cpsel_trace_row;

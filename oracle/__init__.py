@@ -424,6 +424,146 @@ def brent_root(x, k: int, maxit: int = 400, z_cap: int = 0):
     return {"value": value, "iterations": it, "trace": trace}
 
 
+class BrentMinStep:
+    """Numerical Recipes' `brent` (parabolic interpolation, golden section when the parabola is
+    rejected), the paper's 'Brent's method of optimization' (P:L113, P:L136, P:L204, P:L226,
+    P:L229), literally, one evaluation at a time so that a run can be driven by any F values
+    (the oracle's own in `brent_min`, a GPU trace's in `brent_min_replay`).  Reading R37: Brent's
+    own bracket [a, b] is kept as NR keeps it and then intersected with the exact bracket
+    [y_L, y_R] that the counts give (convexity of F makes both valid; the counts are exact);
+    the first point is NR's golden-section point of [y_L, y_R]."""
+    CGOLD = 0.3819660
+    TOL = 1.4901161193847656e-08   # sqrt(DBL_EPSILON) (NR: ~ the square root of the precision)
+    ZEPS = 1.0e-10
+
+    def __init__(self, yL: float, yR: float):
+        self.a, self.b = yL, yR
+        self.x = self.w = self.v = yL + self.CGOLD * (yR - yL)
+        self.fx = self.fw = self.fv = math.nan
+        self.d = self.e = 0.0
+        self.started = False
+
+    def propose(self):
+        """The next point, or None once NR's convergence test holds (then the hybrid finish)."""
+        if not self.started:
+            return self.x
+        a, b, x, w, v = self.a, self.b, self.x, self.w, self.v
+        fx, fw, fv = self.fx, self.fw, self.fv
+        xm = 0.5 * (a + b)
+        tol1 = self.TOL * abs(x) + self.ZEPS
+        tol2 = 2.0 * tol1
+        if abs(x - xm) <= tol2 - 0.5 * (b - a):  # NR's convergence test: brent returns x
+            return None
+        if abs(self.e) > tol1:
+            r = (x - w) * (fx - fv)
+            q = (x - v) * (fx - fw)
+            p = (x - v) * q - (x - w) * r
+            q = 2.0 * (q - r)
+            if q > 0.0:
+                p = -p
+            q = abs(q)
+            etemp = self.e
+            self.e = self.d
+            if abs(p) >= abs(0.5 * q * etemp) or p <= q * (a - x) or p >= q * (b - x):
+                self.e = (a - x) if x >= xm else (b - x)
+                self.d = self.CGOLD * self.e
+            else:
+                self.d = p / q
+                u = x + self.d
+                if u - a < tol2 or b - u < tol2:
+                    self.d = abs(tol1) if xm - x >= 0.0 else -abs(tol1)
+        else:
+            self.e = (a - x) if x >= xm else (b - x)
+            self.d = self.CGOLD * self.e
+        return x + self.d if abs(self.d) >= tol1 else x + (abs(tol1) if self.d >= 0.0 else -abs(tol1))
+
+    def accept(self, u: float, fu: float, yL: float, yR: float):
+        """F(u) = fu; [yL, yR] is the exact bracket after u's counts."""
+        if not self.started:  # the first evaluation: x = w = v = u
+            self.x = self.w = self.v = u
+            self.fx = self.fw = self.fv = fu
+            self.started = True
+        elif fu <= self.fx:
+            if u >= self.x:
+                self.a = self.x
+            else:
+                self.b = self.x
+            self.v, self.w, self.x = self.w, self.x, u
+            self.fv, self.fw, self.fx = self.fw, self.fx, fu
+        else:
+            if u < self.x:
+                self.a = u
+            else:
+                self.b = u
+            if fu <= self.fw or self.w == self.x:
+                self.v, self.w = self.w, u
+                self.fv, self.fw = self.fw, fu
+            elif fu <= self.fv or self.v == self.x or self.v == self.w:
+                self.v, self.fv = u, fu
+        self.a = max(self.a, yL)
+        self.b = min(self.b, yR)
+
+
+def _brent_min_run(x, k: int, maxit: int, z_cap: int, F_of):
+    """Shared loop of brent_min / brent_min_replay: F_of(it, t) gives F_k(t) for iteration it."""
+    x = _as_array(x)
+    n = check_input(x, k)
+    dt = x.dtype.type
+    rec = init_record(x)
+    if k <= rec["cnt_min"]:
+        return {"value": rec["min"], "iterations": 0, "trace": []}
+    if k > n - rec["cnt_max"]:
+        return {"value": rec["max"], "iterations": 0, "trace": []}
+    yL, yR = float(rec["min"]), float(rec["max"])
+    c_le_L, c_lt_R = rec["cnt_min"], n - rec["cnt_max"]
+    br = BrentMinStep(yL, yR)
+    trace = []
+    it = 0
+    for it in range(1, maxit + 1):
+        u = br.propose()
+        if u is None:
+            break
+        t = _snap(u, yL, yR, dt)
+        if not (yL < t < yR):
+            break
+        c_lt, c_eq = rank_counts(x, t)
+        F = F_of(it, t)
+        if c_lt < k <= c_lt + c_eq:
+            trace.append((t, F, c_lt, c_eq, 0))
+            return {"value": canonical(dt(t)), "iterations": it, "trace": trace}
+        if c_lt + c_eq < k:
+            yL, c_le_L = t, c_lt + c_eq
+        else:
+            yR, c_lt_R = t, c_lt
+        br.accept(t, F, yL, yR)
+        trace.append((t, F, c_lt, c_eq, c_lt_R - c_le_L))
+        if c_lt_R - c_le_L <= z_cap:
+            break
+    value, _ = hybrid_finish(x, k, yL, yR)
+    return {"value": value, "iterations": it, "trace": trace}
+
+
+def brent_min(x, k: int, maxit: int = 400, z_cap: int = 0):
+    """The paper's 'Brent's method of optimization' comparison: NR
+    `brent` minimising F_k (Eq. 2, R2) with F from long-double direct sums (f_os), each proposed
+    point rounded into the exact open bracket (R9); 0 in dF_k(t) -> t; the exact bracket
+    [y_L, y_R] from the counts as in `bisection` (R37); stop when the interior holds <= z_cap
+    elements or NR's convergence test holds, then the hybrid finish.  The paper (Fig. 4): with very large
+    outliers F is linear over most of the range, the parabolic fits fail and Brent reverts to
+    golden section — its iteration count grows with the range.
+    Returns dict(value, iterations, trace=[(t, F, c_lt, c_eq, interior)])."""
+    xa = _as_array(x)
+    return _brent_min_run(xa, k, maxit, z_cap, lambda it, t: float(f_os(xa, t, k)))
+
+
+def brent_min_replay(x, k: int, F_values, maxit: int = 400, z_cap: int = 0):
+    """brent_min driven by given F values (F_values[i] = F at iteration i+1, e.g. a GPU trace's):
+    the points it proposes are exactly what a correct implementation of the same steps proposes
+    from those F values; the counts are the oracle's own."""
+    xa = _as_array(x)
+    return _brent_min_run(xa, k, min(maxit, len(F_values)), z_cap, lambda it, t: float(F_values[it - 1]))
+
+
 def eval_at(x, k: int, t, y_lo, y_hi):
     """Replay hook: one pass at t (pass_stats) plus F_k(t) and dF_k(t) — compared against the
     GPU's cpsel_eval / trace at identical t."""

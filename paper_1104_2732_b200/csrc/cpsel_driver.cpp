@@ -264,6 +264,79 @@ struct BrentRoot {
   }
 };
 
+// Brent's minimisation (Numerical Recipes' brent: parabolic interpolation, golden section when the
+// parabola is rejected; the paper's "Brent's method of optimization", P:L113, P:L136, P:L204,
+// P:L229), the comparison driver 3, on F_k from the passes' sums.  Reading R37: Brent's own bracket
+// [a, b] is kept as NR keeps it and intersected with the exact bracket the counts give; the first
+// point is NR's golden-section point.  Step by step the same as oracle.BrentMinStep (the same
+// operations in double), so a trace replays exactly from its F values.
+struct BrentMin {
+  static constexpr double kCgold = 0.3819660, kTol = 1.4901161193847656e-08, kZeps = 1.0e-10;
+  double a = 0, b = 0, x = 0, w = 0, v = 0, fx = 0, fw = 0, fv = 0, d = 0, e = 0;
+  bool started = false;
+  void init(double yl, double yr) {
+    a = yl; b = yr;
+    x = w = v = yl + kCgold * (yr - yl);
+    d = e = 0.0;
+    started = false;
+  }
+  // false once NR's convergence test holds (brent would return x)
+  bool propose(double* u) {
+    if (!started) {
+      *u = x;
+      return true;
+    }
+    const double xm = 0.5 * (a + b);
+    const double tol1 = kTol * std::fabs(x) + kZeps, tol2 = 2.0 * tol1;
+    if (std::fabs(x - xm) <= tol2 - 0.5 * (b - a)) return false;
+    if (std::fabs(e) > tol1) {
+      const double r = (x - w) * (fx - fv);
+      double q = (x - v) * (fx - fw);
+      double p = (x - v) * q - (x - w) * r;
+      q = 2.0 * (q - r);
+      if (q > 0.0) p = -p;
+      q = std::fabs(q);
+      const double etemp = e;
+      e = d;
+      if (std::fabs(p) >= std::fabs(0.5 * q * etemp) || p <= q * (a - x) || p >= q * (b - x)) {
+        e = (x >= xm) ? a - x : b - x;
+        d = kCgold * e;
+      } else {
+        d = p / q;
+        const double uu = x + d;
+        if (uu - a < tol2 || b - uu < tol2) d = (xm - x >= 0.0) ? std::fabs(tol1) : -std::fabs(tol1);
+      }
+    } else {
+      e = (x >= xm) ? a - x : b - x;
+      d = kCgold * e;
+    }
+    *u = std::fabs(d) >= tol1 ? x + d : x + (d >= 0.0 ? std::fabs(tol1) : -std::fabs(tol1));
+    return true;
+  }
+  // F(u) = fu; [yl, yr]: the exact bracket after u's counts
+  void accept(double u, double fu, double yl, double yr) {
+    if (!started) {
+      x = w = v = u;
+      fx = fw = fv = fu;
+      started = true;
+    } else if (fu <= fx) {
+      if (u >= x) a = x; else b = x;
+      v = w; w = x; x = u;
+      fv = fw; fw = fx; fx = fu;
+    } else {
+      if (u < x) a = u; else b = u;
+      if (fu <= fw || w == x) {
+        v = w; w = u;
+        fv = fw; fw = fu;
+      } else if (fu <= fv || v == x || v == w) {
+        v = u; fv = fu;
+      }
+    }
+    a = std::max(a, yl);
+    b = std::min(b, yr);
+  }
+};
+
 // Ordered-key bisection point of ]yL, yR[ (safeguard, R7).
 double key_mid(double yL, double yR, int dt) {
   const uint64_t a = key_of(yL, dt), b = key_of(yR, dt);
@@ -1517,6 +1590,8 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
   bool bisect = false;
   BrentRoot brent;  // driver 2
   bool brent_on = false;
+  BrentMin bmin;    // driver 3
+  bool bmin_on = false;
   const long double wP = (long double)k - 0.5L, wN = (long double)n - (long double)k + 0.5L;
   constexpr uint64_t kUnknown = ~0ull;
   bool exact = true;  // the current (compacted) array holds exactly the bracket interior
@@ -1750,6 +1825,21 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
       }
       t = brent.propose();
       kind = 5;
+    } else if (cfg.driver == 3 && !bisect) {  // Brent's minimisation: its next point
+      if (!bmin_on) {
+        bmin.init(yL, yR);
+        bmin_on = true;
+      }
+      double u;
+      if (bmin.propose(&u)) {
+        t = u;
+        kind = 6;
+      } else {  // NR's convergence test: ordered-key bisection of the exact bracket finishes it
+        bisect = true;
+        t = key_mid(yL, yR, dt);
+        kind = 1;
+        inf.fallback_steps++;
+      }
     } else if (bisect) {
       t = key_mid(yL, yR, dt);
       kind = 1;
@@ -1790,6 +1880,10 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     row.scanned = be.scanned;
     row.written = compact ? zl + zh : 0;
     if (cfg.driver == 2) brent.accept(tq, (double)c_lt + (double)c_le - 2.0 * (double)k + 1.0);
+    if (cfg.driver == 3 && !std::isfinite(row.F)) {  // F untracked (init cuts without their sums, R25)
+      if (info) *info = inf;
+      return CPSEL_EINVAL;
+    }
     // step 1.3: 0 in dF(t) <=> c_lt < k <= c_le -> t = x_(k)
     if (c_lt < k && k <= c_le) {
       if (trace && cfg.record_trace) trace->push_back(row);
@@ -1828,6 +1922,7 @@ cpsel_status drive(Backend& be, uint64_t n, int dt, uint64_t k, const cpsel_conf
     }
     row.interior = m;
     if (trace && cfg.record_trace) trace->push_back(row);
+    if (cfg.driver == 3 && kind == 6) bmin.accept(tq, row.F, yL, yR);
     if (compact) {
       if (m <= select_cap && be.kept_dense()) {  // hybrid finish: exact selection in the kept half
         double v;
@@ -2093,7 +2188,7 @@ const char* cpsel_last_error(const cpsel_ctx* ctx) { return ctx ? ctx->err.c_str
 cpsel_status cpsel_set_config(cpsel_ctx* ctx, const cpsel_config* cfg) {
   if (!ctx || !cfg) return CPSEL_EINVAL;
   if (cfg->max_iters == 0) return fail(ctx, CPSEL_EINVAL, "max_iters must be >= 1");
-  if (cfg->driver < 0 || cfg->driver > 2) return fail(ctx, CPSEL_EINVAL, "driver must be 0, 1 or 2");
+  if (cfg->driver < 0 || cfg->driver > 3) return fail(ctx, CPSEL_EINVAL, "driver must be 0, 1, 2 or 3");
   ctx->cfg = *cfg;
   return CPSEL_OK;
 }

@@ -523,11 +523,13 @@ def test_device_loop_matches_host_loop(cp, dtype, dist):
 
 @pytest.mark.parametrize("dtype", ["f32", "f64"])
 def test_bisection_driver_matches_oracle(cp, dtype):
-    """driver=1 (bisection) and driver=2 (Brent's root finder), the paper's comparisons (P:L135-136,
-    P:L204): the same element as the oracle, their iterates exactly the oracle's (value midpoints /
-    zbrent's points, rounded into the bracket) with the same counts; and the paper's outlier claim
-    (P:L313, P:L413 vs P:L416): with 1e9 outliers both need many more passes than with 1e3, the
-    cutting plane at most 2 more."""
+    """driver=1 (bisection), driver=2 (Brent's root finder) and driver=3 (Brent's minimisation), the
+    paper's comparisons: the same element as the oracle, their iterates
+    exactly the oracle's (value midpoints / zbrent's points, rounded into the bracket; Brent's
+    minimisation: the points oracle.BrentMinStep proposes from the trace's F values, which match the
+    oracle's direct F within rel 1e-6 / 1e-12) with the same counts; and the paper's outlier claim
+    (P:L313, P:L413-414 vs P:L416): with 1e9 outliers all three need many more passes than with 1e3,
+    the cutting plane at most 2 more."""
     import torch
     n = 1_000_003
     base = datagen.make("uniform", n, dtype)
@@ -537,7 +539,7 @@ def test_bisection_driver_matches_oracle(cp, dtype):
         xd = tdev(x)
         k = O.median_rank(n)
         refs = {1: O.bisection(x, k, z_cap=0), 2: O.brent_root(x, k, z_cap=0)}
-        for drv in (1, 2, 0):
+        for drv in (1, 2, 3, 0):
             cp.set_config(driver=drv, init_cut=0, pass_cuts=0)
             v, info = cp.select_kth(xd, k, return_info=True)
             tr = cp.get_trace()
@@ -549,6 +551,16 @@ def test_bisection_driver_matches_oracle(cp, dtype):
                 assert len(tr) <= len(ref["trace"]) and all(r["kind"] == 3 + drv for r in tr)
                 for r, (t, c_lt, c_eq, interior) in zip(tr, ref["trace"]):
                     assert r["t"] == t and (r["c_lt"], r["c_eq"]) == (c_lt, c_eq), (r, t, c_lt, c_eq)
+            elif drv == 3:
+                rows = [r for r in tr if r["kind"] == 6]
+                assert rows and rows == tr[:len(rows)]
+                ref = O.brent_min_replay(x, k, [r["F"] for r in rows])
+                assert len(ref["trace"]) >= len(rows) - 1
+                for r, (t, F, c_lt, c_eq, _) in zip(rows, ref["trace"]):
+                    assert r["t"] == t and (r["c_lt"], r["c_eq"]) == (c_lt, c_eq), (r, t, c_lt, c_eq)
+                for r in rows[:6]:
+                    assert r["F"] == pytest.approx(float(O.f_os(x, r["t"], k)), rel=1e-6 if dtype == "f32" else 1e-12)
     assert passes[(1e9, 1)] - passes[(1e3, 1)] >= 15, passes
     assert passes[(1e9, 2)] - passes[(1e3, 2)] >= 10, passes
+    assert passes[(1e9, 3)] - passes[(1e3, 3)] >= 10, passes
     assert passes[(1e9, 0)] - passes[(1e3, 0)] <= 2, passes

@@ -214,3 +214,24 @@ def test_sharded_host_logic_gloo_world2():
             assert got[0][j][1:] == got[1][j][1:]             # identical driver decisions
     # the pooled cuts ran (kind-2 init cuts and kind-3 cut passes) in the median case
     assert any(row[3] == 2 for row in got[0][1][2]) and any(row[3] == 3 for row in got[0][1][2])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_driver_brent_min_replays_the_oracle(dtype):
+    """driver=3 (Brent's minimisation): the exact element, and every point it
+    proposed is the point oracle.BrentMinStep proposes from the same F values (the trace's, which
+    match the oracle's direct long-double F within the north_star tolerance); the counts exact."""
+    tol = 1e-6 if dtype == "f32" else 1e-12
+    for dist in ("uniform", "normal", "cauchy", "dup256"):
+        x = datagen.make(dist, 20_011, dtype)
+        n = x.size
+        for k in (2, n // 10, O.median_rank(n), n - 1):
+            v, info, trace = drive(x, k, dtype, config={"driver": 3, "force_cp": 1, "z_cap": n, "select_cap": 8})
+            assert canon(v) == float(O.order_statistic(x, k)), (dist, k, info)
+            rows = [r for r in trace if r["kind"] == 6]
+            assert rows == trace[:len(rows)] and (rows or info["exit"] in ("init_min", "init_max"))
+            ref = O.brent_min_replay(x, k, [r["F"] for r in rows])
+            assert len(ref["trace"]) >= len(rows) - 1
+            for r, (t, F, c_lt, c_eq, _) in zip(rows, ref["trace"]):
+                assert r["t"] == t and (r["c_lt"], r["c_eq"]) == (c_lt, c_eq), (dist, k, r, t)
+                assert r["F"] == pytest.approx(float(O.f_os(x, t, k)), rel=tol)

@@ -654,3 +654,68 @@ def test_knn_classify_is_the_majority_of_the_k_nearest():
     Xg = np.array([[0.0], [1.0], [-1.0], [2.0], [-2.0]], np.float32)          # ties at distance 1, 4
     cls, votes = O.knn_classify(Xg, np.array([0, 1, 2, 1, 2], np.int32), np.zeros((1, 1), np.float32), 2, 3)
     assert votes[0].tolist() == [1.0, 0.5, 0.5] and cls[0] == 0
+
+
+def test_brent_min_step_tracks_an_independent_brent():
+    """oracle.BrentMinStep (NR `brent`, the paper's 'Brent's method of optimization', P:L136,
+    P:L229) against scipy's fminbound — an independent implementation of Brent's method from the
+    same golden-section starting point: the evaluation points agree through the golden and the
+    parabolic phases (up to NR's 7-digit golden constant) until the steps reach the tolerance.
+    A wrong sign or operand in the parabola, or a wrong bracket update, leaves that path."""
+    from scipy.optimize import fminbound
+    for f, a, b in ((lambda u: math.exp(u) - 2.0 * u + 0.1 * math.sin(5.0 * u), 0.0, 3.0),
+                    (lambda u: abs(u - 0.3) ** 1.5 + 0.2 * u * u, -2.0, 1.0),
+                    (lambda u: (u - 7.25) ** 2 * (1.0 + 0.01 * u), 0.0, 100.0)):
+        pts = []
+
+        def g(u):
+            pts.append(float(u))
+            return f(float(u))
+
+        fminbound(g, a, b, xtol=1e-12, maxfun=60)
+        br = O.BrentMinStep(a, b)
+        mine = []
+        for _ in range(8):
+            u = br.propose()
+            mine.append(u)
+            br.accept(u, f(u), a, b)
+        assert np.allclose(mine, pts[:8], rtol=0, atol=1e-6 * (b - a)), (mine, pts[:8])
+    # a linear function: every parabola is rejected (collinear points) -> pure golden-section steps
+    br = O.BrentMinStep(0.0, 1.0)
+    pts = []
+    for _ in range(6):
+        u = br.propose()
+        pts.append(u)
+        br.accept(u, u, 0.0, 1.0)
+    # golden section toward the minimum at 0: 0.381966, then the larger segment's golden point
+    # 0.618034 (worse: b <- it), then x shrinks by 1 - CGOLD = 0.618034 per step
+    assert pts[0] == pytest.approx(0.381966, abs=1e-12) and pts[1] == pytest.approx(0.618034, abs=1e-6)
+    assert all(pts[i + 1] / pts[i] == pytest.approx(0.618034, abs=1e-6) for i in range(2, 5))
+
+
+def test_brent_min_result_and_outlier_sensitivity():
+    """oracle.brent_min: the exact element by the definition for every kind of rank (the hybrid
+    finish after NR's convergence), and the paper's claim (Fig. 4 caption P:L514: with very
+    large outliers F is linear over most of the range, the parabolic fits fail and Brent's method
+    reverts to golden section): 1e9 outliers cost >= 10 more iterations than 1e3, the cutting plane
+    none.  brent_min_replay driven by brent_min's own F values retraces it exactly."""
+    rng = np.random.default_rng(5)
+    x = rng.random(20001)
+    for k in (1, 2, 7, 10001, 19999, 20001):
+        r = O.brent_min(x, k)
+        assert r["value"] == np.sort(x)[k - 1]
+        assert r["iterations"] < 60
+    xd = np.floor(256 * rng.random(5001)).astype(np.float32)   # many duplicates
+    for k in (1, 100, 2501, 5001):
+        assert O.brent_min(xd, k)["value"] == np.sort(xd)[k - 1]
+    its, cps = [], []
+    for mag in (1e3, 1e9):
+        y = x.copy()
+        y[rng.choice(y.size, 20, replace=False)] = mag
+        its.append(O.brent_min(y, 10001, z_cap=64)["iterations"])
+        cps.append(O.cutting_plane(y, 10001, z_cap=64)["iterations"])
+    assert its[1] - its[0] >= 10, its
+    assert abs(cps[1] - cps[0]) <= 2, cps
+    r = O.brent_min(x, 10001)
+    rp = O.brent_min_replay(x, 10001, [row[1] for row in r["trace"]])
+    assert rp["trace"] == r["trace"] and rp["value"] == r["value"]
