@@ -96,6 +96,7 @@ struct cpsel_ctx {
     DevInit init;
     double radix_value;
     unsigned long long seq_pass, seq_init, seq_radix;
+    unsigned long long radix_fallback;          // the value-binned finish left it to the radix select
     double direct_value;                        // exact_cluster_kernel (small arrays, §8f-3)
     unsigned long long direct_bad, seq_direct;
     ChainMail chain;  // the device chain's step decisions (§8f-3)
@@ -441,7 +442,7 @@ struct GpuBackend : Backend {
   // copy, the radix select of its copy) is launched right behind the init; the driver's requests
   // take those results when they ask for exactly those steps
   struct Spec {
-    bool active = false, cut_used = false, small = false, direct = false;
+    bool active = false, cut_used = false, small = false, direct = false, vbin = false;
     unsigned long long seq_c0 = 0, seq_cut = 0, seq_c1 = 0, seq_radix = 0;
     int sample_slot = -1, cut_slot = -1, radix_slot = -1;
   } spec;
@@ -456,6 +457,13 @@ struct GpuBackend : Backend {
   bool init_hist0() const {
     static const bool on = !(getenv("CPSEL_INIT_HIST0") && getenv("CPSEL_INIT_HIST0")[0] == '0');
     return on && dt == kF32;
+  }
+  // the direct chain's finish by value bins (launch_vbin_finish: the init counts its copy per value
+  // bin of ]t_lo, t_hi[, one pass over the copy and a shared-memory select of the target bin), both
+  // dtypes; CPSEL_VBIN=0: the key-digit radix select (init_hist0 for f32)
+  bool vbin_on() const {
+    static const bool on = !(getenv("CPSEL_VBIN") && getenv("CPSEL_VBIN")[0] == '0');
+    return on;
   }
   // start/end of the init kernel in the light ring: at most kLightPairs pairs are kept until the
   // caller reads them (further selections go untimed); a start whose end was never recorded (an
@@ -600,8 +608,10 @@ struct GpuBackend : Backend {
         a.chain_k = k;
         a.chain_cap = chain_select_cap;
         a.chain_direct = direct ? 1 : 0;
-        // init_hist0: the init also counts radix round 0 of its copy (one radix launch fewer)
-        a.hist = (direct && init_hist0()) ? ctx->d_hist + 2048 : nullptr;
+        // vbin: the init counts its copy per value bin for the value-binned finish; else (init_hist0)
+        // radix round 0 of its copy (one radix round fewer)
+        a.vbin = (direct && vbin_on()) ? 1 : 0;
+        a.hist = (direct && (vbin_on() || init_hist0())) ? ctx->d_hist + 2048 : nullptr;
       }
       CK(launch_init_seg(dt, a, sa, ctx->shape, ctx->stream, ctx->cfg.objective != 0));
     } else {
@@ -665,14 +675,20 @@ struct GpuBackend : Backend {
     spec.active = true;
     spec.direct = true;
     spec.seq_radix = ++ctx->seq;
+    spec.vbin = vbin_on();
     if ((e = tic()) != cudaSuccess) return e;
-    if ((e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
-                                 &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
-                                 static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain,
-                                 /*first_round=*/init_hist0() ? 1 : 0, init_hist0() ? ctx->d_hist + 2048 : nullptr,
-                                 /*m_hint: the expected copy*/ n / (n <= (1ull << 26) ? 25 : 100))) !=
-        cudaSuccess)
-      return e;
+    if (spec.vbin) {
+      e = launch_vbin_finish(dt, ctx->d_sb[0], static_cast<const SegEntry*>(ctx->d_st[0]), ctx->d_t0, ctx->d_hist,
+                             ctx->shape, ctx->stream, ctx->d_chain, &ctx->mb_dev->radix_value,
+                             &ctx->mb_dev->radix_fallback, &ctx->mb_dev->seq_radix, spec.seq_radix);
+    } else {
+      e = launch_radix_select(dt, ctx->d_sb[0], 0, 0, ctx->d_radix, ctx->d_hist, ctx->shape, ctx->stream,
+                              &ctx->mb_dev->radix_value, &ctx->mb_dev->seq_radix, spec.seq_radix,
+                              static_cast<const SegEntry*>(ctx->d_st[0]), 0, ctx->d_ticket, ctx->d_chain,
+                              /*first_round=*/init_hist0() ? 1 : 0, init_hist0() ? ctx->d_hist + 2048 : nullptr,
+                              /*m_hint: the expected copy*/ n / (n <= (1ull << 26) ? 25 : 100));
+    }
+    if (e != cudaSuccess) return e;
     if ((e = toc()) != cudaSuccess) return e;
     spec.radix_slot = slot;
     return cudaSuccess;
@@ -1030,11 +1046,14 @@ struct GpuBackend : Backend {
       if (ok && cr == r && cm == n_cur) {  // the chain ran this select right behind the init
         w = wait_mail(&ctx->mb->seq_radix, spec.seq_radix);
         if (w != CPSEL_OK) return w;
-        *out = ctx->mb->radix_value;
-        launches = (dt == kF32 ? 3 : 6) - (init_hist0() ? 1 : 0);  // round 0 counted by the init pass?
-        scanned = cm;
-        slot = spec.radix_slot;
-        return CPSEL_OK;
+        if (!(spec.vbin && ctx->mb->radix_fallback)) {
+          *out = ctx->mb->radix_value;
+          launches = spec.vbin ? 1 : (dt == kF32 ? 3 : 6) - (init_hist0() ? 1 : 0);  // round 0 by the init?
+          scanned = cm;
+          slot = spec.radix_slot;
+          return CPSEL_OK;
+        }
+        // a large target bin of several values: the key-digit radix select below (it left everything clean)
       }
     }
     if (spec.active && spec.cut_used && side == 0 && !last_dense && tgt == 1) {

@@ -49,6 +49,20 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   asm("ld.global.nc.L1::no_allocate.L2::256B.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
   return r;
 }
+// the same with an L2 evict-first policy (createpolicy): the init pass's one read of x, so that its
+// streaming does not push the copy it writes (read again by the exact finish) out of L2
+__device__ __forceinline__ float4 ld_stream_ef(const float4* p, uint64_t pol) {
+  float4 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ double2 ld_stream_ef(const double2* p, uint64_t pol) {
+  double2 r;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.L2::256B.v2.f64 {%0,%1}, [%2], %3;" : "=d"(r.x), "=d"(r.y)
+      : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ float lane_of(const float4& v, int j) {
   return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
 }
@@ -83,6 +97,29 @@ __device__ __forceinline__ double from_key_f32(unsigned long long k) {
 __device__ __forceinline__ double from_key_f64(unsigned long long k) {
   const unsigned long long u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
   return __longlong_as_double((long long)u);
+}
+
+// Value-linear bins of ]t_lo, t_hi[ (the direct chain's first digit, vbin): bin = trunc((v - t_lo) *
+// 2048 / (t_hi - t_lo)) clamped to 2047, with the two roundings done explicitly (no contraction) so
+// the init pass and the finish compute the same bin for every value; v <= v' => bin(v) <= bin(v')
+// (each step is monotone).  vbin_scale = 0: the span is not finite (an open cut, R31) -> key digits.
+__device__ __forceinline__ float vbin_scale(float tl, float th) {
+  const float span = __fsub_rn(th, tl);
+  return (th > tl && span < __int_as_float(0x7f800000)) ? __fdiv_rn(2048.f, span) : 0.f;
+}
+__device__ __forceinline__ double vbin_scale(double tl, double th) {
+  const double span = __dsub_rn(th, tl);
+  return (th > tl && span < __longlong_as_double(0x7ff0000000000000ll)) ? __ddiv_rn(2048.0, span) : 0.0;
+}
+__device__ __forceinline__ unsigned vbin_of(float v, float tl, float sc) {
+  return (unsigned)fminf(fmaxf(__fmul_rn(__fsub_rn(v, tl), sc), 0.f), 2047.f);
+}
+__device__ __forceinline__ unsigned vbin_of(double v, double tl, double sc) {
+  return (unsigned)fmin(fmax(__dmul_rn(__dsub_rn(v, tl), sc), 0.0), 2047.0);
+}
+// the first digit of a copied element: its value bin, or (sc == 0) the top 11 bits of its key
+template <typename T> __device__ __forceinline__ unsigned vbin_digit(T v, T tl, T sc) {
+  return sc > T(0) ? vbin_of(v, tl, sc) : (unsigned)(okey(v) >> (sizeof(T) == 4 ? 21 : 53)) & 2047u;
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1826,6 +1863,202 @@ __global__ void __launch_bounds__(NT, 1024 / NT) radix_coop_kernel(const __grid_
   if (threadIdx.x == 0) c.bar[2] = 0u;
 }
 
+// ------------------------------------------------------------------------------------------
+// Step a5 behind the vbin init (launch_vbin_finish): the init counted its copy per VALUE bin of
+// ]t_lo, t_hi[ (2048 equal widths: for any smooth density near the target each bin holds ~1/2048 of
+// the copy, where the top key digits put most of it in one or two bins), so after the bin pick only a
+// few thousand elements remain: one pass over the copy takes their key range (and copies them if
+// they fit), the last CTA selects among them in shared memory.  No grid barrier, no second pass.
+struct VbArgs {
+  const void* z;
+  const SegEntry* tab;
+  int Wtot;
+  const void* cuts;          // t_lo, t_hi (the init's)
+  unsigned* hist0;           // the init's 2048 first-digit counts (cleared here)
+  unsigned long long* st;    // [0] ticket, [1] copied count, [2] ~min key, [3] max key (left zero)
+  void* zb;                  // kVbCap elements: the target bin's copy
+  const ChainState* chain;
+  double* vout;
+  unsigned long long* fallback;
+  unsigned long long* done;
+  unsigned long long seq;
+};
+template <typename T> struct VbFn {
+  T tl, sc;
+  unsigned b;
+  bool comp;
+  unsigned long long kmin = ~0ull, kmax = 0ull;
+  unsigned long long* cnt;
+  T* zb;
+  __device__ __forceinline__ void elem(T v, int, int) {
+    if (vbin_digit(v, tl, sc) == b) {
+      const unsigned long long k = okey(v);
+      kmin = k < kmin ? k : kmin;
+      kmax = k > kmax ? k : kmax;
+      if (comp) {
+        const unsigned long long i = atomicAdd(cnt, 1ull);
+        if (i < (unsigned long long)kVbCap) zb[i] = v;
+      }
+    }
+  }
+  __device__ __forceinline__ void begin() {}
+  __device__ __forceinline__ void end() {}
+};
+// the digit of a 2048-bin block histogram h (nb bins) holding rank r (1-based): 1024 threads, two
+// bins each; returns (in shared memory) the digit and the count before it
+__device__ __forceinline__ void pick1024(const unsigned* h, int nb, unsigned long long r, unsigned* wsum,
+                                         unsigned* s_d, unsigned long long* s_before, unsigned* s_cnt,
+                                         bool global) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int b0 = 2 * threadIdx.x;
+  const unsigned h0 = b0 < nb ? (global ? __ldcg(&h[b0]) : h[b0]) : 0u;
+  const unsigned h1 = b0 + 1 < nb ? (global ? __ldcg(&h[b0 + 1]) : h[b0 + 1]) : 0u;
+  const unsigned tsum = h0 + h1;
+  unsigned incl = tsum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(FULL, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  unsigned long long before = 0;
+  for (int q = 0; q < w; ++q) before += wsum[q];
+  before += incl - tsum;
+  if (before < r && r <= before + h0) {
+    *s_d = (unsigned)b0; *s_before = before; *s_cnt = h0;
+  } else if (before + h0 < r && r <= before + tsum) {
+    *s_d = (unsigned)b0 + 1u; *s_before = before + h0; *s_cnt = h1;
+  }
+  __syncthreads();
+}
+template <typename T>
+__global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_constant__ VbArgs a) {
+  constexpr int NW = 32;
+  pdl_wait();  // the init's copy, its bin counts and the chain decision
+  if (a.chain && !a.chain->ok[1]) {  // skipped (uniformly): the init's counts must still be cleared
+    if (blockIdx.x == 0)
+      for (int i = threadIdx.x; i < 2048; i += 1024) a.hist0[i] = 0u;
+    return;
+  }
+  const unsigned long long r = a.chain->r[1];
+  __shared__ unsigned wsum[NW];
+  __shared__ unsigned s_b, s_cb, s_d, s_dc;
+  __shared__ unsigned long long s_base, s_bef, s_kmin[NW], s_kmax[NW];
+  __shared__ bool s_last;
+  pick1024(a.hist0, 2048, r, wsum, &s_b, &s_base, &s_cb, true);
+  const T* cuts = static_cast<const T*>(a.cuts);
+  VbFn<T> f;
+  f.tl = cuts[0];
+  f.sc = vbin_scale(cuts[0], cuts[1]);
+  f.b = s_b;
+  f.comp = s_cb <= (unsigned)kVbCap;
+  f.cnt = &a.st[1];
+  f.zb = static_cast<T*>(a.zb);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // one warp per run, 8 vectors per lane in flight (a run of the ~1% copy is a few thousand
+  // elements: ~3 dependent L2 round trips instead of one per 4-vector group)
+  using V = typename VecOf<T>::V;
+  constexpr int VE = VecOf<T>::N, U = 8;
+  for (uint64_t W = (uint64_t)blockIdx.x * NW + w; W < (uint64_t)a.Wtot; W += (uint64_t)gridDim.x * NW) {
+    const SegEntry e = a.tab[W];
+    const T* p = static_cast<const T*>(a.z) + e.off[0];
+    const uint64_t c = e.cnt[0];
+    const uint64_t mis = (reinterpret_cast<uintptr_t>(p) / sizeof(T)) & (VE - 1);
+    const uint64_t head = mis ? ((VE - mis) < c ? (VE - mis) : c) : 0;
+    const uint64_t nvec = (c - head) / VE, tail0 = head + nvec * VE;
+    if ((uint64_t)lane < head) f.elem(p[lane], 0, 0);
+    if ((uint64_t)lane < c - tail0) f.elem(p[tail0 + lane], 0, 0);
+    const V* xv = reinterpret_cast<const V*>(p + head);
+    for (uint64_t v0 = 0; v0 < nvec; v0 += 32 * U) {
+      V buf[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = v0 + (uint64_t)u * 32 + lane;
+        if (i < nvec) buf[u] = ld_stream(xv + i);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = v0 + (uint64_t)u * 32 + lane;
+        if (i < nvec) {
+#pragma unroll
+          for (int j = 0; j < VE; ++j) f.elem(lane_of(buf[u], j), 0, 0);
+        }
+      }
+    }
+  }
+  unsigned long long kmn = f.kmin, kmx = f.kmax;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const unsigned long long p = __shfl_xor_sync(FULL, kmn, o), q = __shfl_xor_sync(FULL, kmx, o);
+    kmn = p < kmn ? p : kmn;
+    kmx = q > kmx ? q : kmx;
+  }
+  if (lane == 0) { s_kmin[w] = kmn; s_kmax[w] = kmx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 1; q < NW; ++q) {
+      kmn = s_kmin[q] < kmn ? s_kmin[q] : kmn;
+      kmx = s_kmax[q] > kmx ? s_kmax[q] : kmx;
+    }
+    if (kmx >= kmn) {  // this CTA saw elements of the bin
+      atomicMax(&a.st[2], ~kmn);
+      atomicMax(&a.st[3], kmx);
+    }
+    __threadfence();
+    s_last = atomicAdd(reinterpret_cast<unsigned*>(&a.st[0]), 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const unsigned long long gmin = ~__ldcg(&a.st[2]), gmax = __ldcg(&a.st[3]);
+  const unsigned c = s_cb;
+  unsigned long long key = gmin;
+  bool fb = false;
+  if (gmin != gmax) {
+    if (c <= (unsigned)kVbCap) {
+      // radix select of rank r - base among the bin's c keys, in shared memory, from the highest
+      // bit in which the bin's smallest and largest key differ
+      extern __shared__ __align__(16) unsigned long long vb_keys[];
+      __shared__ unsigned hist[2048];
+      const T* zb = static_cast<const T*>(a.zb);
+      for (unsigned i = threadIdx.x; i < c; i += 1024) vb_keys[i] = okey(__ldcg(&zb[i]));
+      const int hb = 63 - __clzll(gmin ^ gmax);
+      unsigned long long mask = hb >= 63 ? 0ull : ~((2ull << hb) - 1ull);
+      unsigned long long prefix = gmin & mask;
+      unsigned long long rk = r - s_base;
+      int lo = hb + 1;
+      while (lo > 0) {
+        const int bits = lo < 11 ? lo : 11, shift = lo - bits;
+        const unsigned dm = (1u << bits) - 1u;
+        for (int i = threadIdx.x; i < 2048; i += 1024) hist[i] = 0u;
+        __syncthreads();
+        for (unsigned i = threadIdx.x; i < c; i += 1024) {
+          const unsigned long long k = vb_keys[i];
+          if ((k & mask) == prefix) atomicAdd(&hist[(unsigned)(k >> shift) & dm], 1u);
+        }
+        __syncthreads();
+        pick1024(hist, 1 << bits, rk, wsum, &s_d, &s_bef, &s_dc, false);
+        prefix |= (unsigned long long)s_d << shift;
+        mask |= (unsigned long long)dm << shift;
+        rk -= s_bef;
+        lo = shift;
+        __syncthreads();
+      }
+      key = prefix;
+    } else {
+      fb = true;  // a large bin of several values: the host runs the key-digit radix select
+    }
+  }
+  if (threadIdx.x == 0) {
+    *a.fallback = fb ? 1ull : 0ull;
+    if (!fb) *a.vout = sizeof(T) == 4 ? from_key_f32(key) : from_key_f64(key);
+    publish_done(a.done, a.seq);
+  }
+  for (int i = threadIdx.x; i < 2048; i += 1024) a.hist0[i] = 0u;  // every CTA read it before its ticket
+  if (threadIdx.x < 4) a.st[threadIdx.x] = 0ull;
+}
+
 template <typename T, bool INSIDE>
 __global__ void __launch_bounds__(kBlock, 4) seg_pass_kernel(SegArgs a) {
   using F = WarpSeg<T, INSIDE>;
@@ -2160,7 +2393,8 @@ template <typename T, bool SUMS> struct InitSeg {
   T* out;
   uint64_t reg_lo;
   T* stage;                       // this warp's GW-element staging buffer (shared memory)
-  unsigned* hist0 = nullptr;      // direct chain: shared-memory histogram of the copy's top digit
+  unsigned* hist0 = nullptr;      // direct chain: shared-memory histogram of the copy's first digit
+  T vtl = T(0), vsc = T(0);       // vbin: t_lo and the bin scale (0: top key digit)
 
   // one element, SUMS: 3 compares, 2 subs, 1 counter, 3 sums, 1 interior bit (10 issue slots):
   //   fL = #x<=t_lo, N += (t_lo-x) on x<=t_lo, P += (x-t_hi) on x>t_hi, I += (x-t_lo) and the
@@ -2315,9 +2549,15 @@ template <typename T, bool SUMS> struct InitSeg {
       if (bits & (1u << j)) *sp++ = vals[j];
     __syncwarp();
     T* dst = out + reg_lo + n_in;
-    if (hist0) {  // radix round 0 of the copy (direct chain): top digit of each copied element
-      for (unsigned i = lane; i < tot; i += 32) {  // (an L2 evict-last store hint here measured
-        const T v = stage[i];                        //  1% slower overall: plain stores)
+    if (hist0 && vsc > T(0)) {  // the copy's first digit (direct chain): its value bin (vbin) ...
+      for (unsigned i = lane; i < tot; i += 32) {
+        const T v = stage[i];
+        dst[i] = v;
+        atomicAdd(&hist0[vbin_of(v, vtl, vsc)], 1u);
+      }
+    } else if (hist0) {  // ... or its top key digit  (an L2 evict-last store hint here measured 1%
+      for (unsigned i = lane; i < tot; i += 32) {  //  slower overall: plain stores)
+        const T v = stage[i];
         dst[i] = v;
         atomicAdd(&hist0[(unsigned)(okey(v) >> (sizeof(T) == 4 ? 21 : 53)) & 2047u], 1u);
       }
@@ -2352,6 +2592,10 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     for (int i = threadIdx.x; i < 2048; i += kBlock) h0[i] = 0u;
     __syncthreads();
     f.hist0 = h0;
+    if (ia.vbin) {
+      f.vtl = f.tl;
+      f.vsc = vbin_scale(f.tl, f.th);
+    }
   }
   const uint64_t mis = (reinterpret_cast<uintptr_t>(x) / sizeof(T)) & (VE - 1);
   uint64_t head = mis ? (VE - mis) : 0;
@@ -2366,9 +2610,10 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
     // software pipelined: the next group's loads are issued once the current group's values sit in
     // f.vals, so they are in flight during its scan / staging / copy-out
     V v[kSegU];
+    const uint64_t pol = policy_evict_first();
     if (W < nfull) {
 #pragma unroll
-      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + W * GV + (uint64_t)u * 32 + lane);
+      for (int u = 0; u < kSegU; ++u) v[u] = ld_stream_ef(xv + W * GV + (uint64_t)u * 32 + lane, pol);
     }
     for (uint64_t g = W; g < nfull; g += Wtot) {
       f.begin();
@@ -2377,7 +2622,7 @@ __global__ void __launch_bounds__(kBlock, 4) init_seg_kernel(InitArgs ia, SegArg
       const uint64_t gn = g + Wtot;
       if (gn < nfull) {
 #pragma unroll
-        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream(xv + gn * GV + (uint64_t)u * 32 + lane);
+        for (int u = 0; u < kSegU; ++u) v[u] = ld_stream_ef(xv + gn * GV + (uint64_t)u * 32 + lane, pol);
       }
       f.end(F::G);
     }
@@ -4266,6 +4511,42 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
   if (dtype == kF32) cut_pass_kernel<float><<<g, kBlock, 0, st>>>(a);
   else cut_pass_kernel<double><<<g, kBlock, 0, st>>>(a);
   return cudaGetLastError();
+}
+
+cudaError_t launch_vbin_finish(int dtype, const void* z, const SegEntry* tab, const void* cuts, unsigned* hist,
+                               const LaunchShape& s, cudaStream_t st, const ChainState* chain, double* vout,
+                               unsigned long long* fallback, unsigned long long* done, unsigned long long seq) {
+  VbArgs a{};
+  a.z = z; a.tab = tab; a.cuts = cuts; a.chain = chain; a.vout = vout; a.fallback = fallback; a.done = done;
+  a.seq = seq;
+  a.Wtot = s.grid_seg[dtype] * kWarps;
+  a.hist0 = hist + 2048;
+  a.st = reinterpret_cast<unsigned long long*>(hist + kVbState);
+  a.zb = hist + kVbBuf;
+  const size_t smem = (size_t)kVbCap * 8;  // the last CTA's keys
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((a.Wtot + 31) / 32);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (dtype == kF32) {
+    static const cudaError_t a0 = cudaFuncSetAttribute(vbin_finish_kernel<float>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a0 != cudaSuccess) return a0;
+    e = cudaLaunchKernelEx(&cfg, vbin_finish_kernel<float>, a);
+  } else {
+    static const cudaError_t a1 = cudaFuncSetAttribute(vbin_finish_kernel<double>,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (a1 != cudaSuccess) return a1;
+    e = cudaLaunchKernelEx(&cfg, vbin_finish_kernel<double>, a);
+  }
+  return e;
 }
 
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,

@@ -145,6 +145,10 @@ struct InitArgs {
   // memory histogram of the copied elements' top digit, merged into hist (2048 words); the chained
   // radix select starts at round 1 and picks that digit itself
   unsigned int* hist;
+  // vbin: the copy's first digit is its VALUE-LINEAR bin in ]t_lo, t_hi[ (2048 equal-width bins,
+  // monotone in the value) instead of the top 11 key bits, whenever t_hi - t_lo is finite (an open
+  // cut, R31, falls back to the key digit); the chained finish is vbin_finish_kernel
+  int vbin;
   // init_seg_kernel without the fp sums: the grid's totals accumulated by atomics here (8 words,
   // zero on entry, left zero) instead of a last-CTA fold of every CTA's partial; nullptr: the fold
   unsigned long long* acc;
@@ -305,11 +309,26 @@ cudaError_t launch_pass(int dtype, const PassArgs& a, const LaunchShape& s, cuda
 // §8f-3 small arrays: x_(r) of x[0..m) (m <= exact_cluster_cap) by ONE 8-CTA cluster launch (exact
 // radix select in registers + DSMEM histograms); *vout = value (canonical +0), *bad_out = #NaN/Inf,
 // then `seq` published to *done.
-constexpr int kRadixHistWords = 4096 + 3 * 2048 + 64;
+// + the value-binned finish (launch_vbin_finish): 16 state words at kVbState, then kVbCap elements
+// (8 bytes each) of the target bin's copy at kVbBuf
+constexpr int kVbState = 4096 + 3 * 2048 + 64;
+constexpr int kVbCap = 16384;
+constexpr int kVbBuf = kVbState + 16;
+constexpr int kRadixHistWords = kVbBuf + 2 * kVbCap;
 uint64_t exact_cluster_cap(int dtype);
 cudaError_t launch_exact_cluster(int dtype, const void* x, uint64_t m, uint64_t r, double* vout,
                                  unsigned long long* bad_out, unsigned long long* done, unsigned long long seq,
                                  cudaStream_t st);
+// The direct chain's exact finish behind an init pass with vbin = 1 (§8f-3, a5): every CTA picks the
+// bin holding the rank from the init's 2048 counts (value-linear bins, or top key digits after an
+// open cut), ONE pass over the init's segmented copy takes the bin's key range and, when the bin holds
+// <= kVbCap elements, copies them; the last CTA finishes: a bin of one value is the answer, a small
+// bin is radix-selected in shared memory from the common prefix of its key range on; a larger bin of
+// several values sets *fallback (the host then runs launch_radix_select on the copy).  hist: the
+// context's kRadixHistWords block (hist0 at +2048 is cleared, the state left zero).
+cudaError_t launch_vbin_finish(int dtype, const void* z, const SegEntry* tab, const void* cuts, unsigned* hist,
+                               const LaunchShape& s, cudaStream_t st, const ChainState* chain, double* vout,
+                               unsigned long long* fallback, unsigned long long* done, unsigned long long seq);
 cudaError_t launch_radix_select(int dtype, const void* z, uint64_t m, uint64_t r, RadixState* state,
                                 unsigned int* hist, const LaunchShape& s, cudaStream_t st,
                                 double* vout, unsigned long long* done, unsigned long long seq,

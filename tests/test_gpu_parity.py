@@ -564,3 +564,36 @@ def test_bisection_driver_matches_oracle(cp, dtype):
     assert passes[(1e9, 2)] - passes[(1e3, 2)] >= 10, passes
     assert passes[(1e9, 3)] - passes[(1e3, 3)] >= 10, passes
     assert passes[(1e9, 0)] - passes[(1e3, 0)] <= 2, passes
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_value_binned_finish_paths(cp, dtype):
+    """The direct chain's value-binned finish (vbin_finish_kernel, §8f-3/a5): the init counts its copy
+    per value bin of ]t_lo, t_hi[, the finish selects inside the target bin.  All three of its exits
+    stay exact: a small bin (shared-memory select: every rank of smooth data), a bin of ONE value
+    (many duplicates at the target: no select at all), and a bin holding more than its capacity of
+    distinct values (a dense cluster at the target: the fallback to the key-digit radix select)."""
+    import torch
+    n = (1 << 23) + 11
+    rng = np.random.default_rng(23)
+    base = rng.random(n).astype(np.float64)
+    cases = {"smooth": base.copy()}
+    d = base.copy()
+    d[rng.choice(n, 300_000, replace=False)] = 0.5          # one value at the median
+    cases["one_value"] = d
+    c = base.copy()
+    idx = rng.choice(n, 400_000, replace=False)
+    c[idx] = 0.5 + rng.random(idx.size) * 2e-6               # 400k distinct values in one bin width
+    cases["dense_cluster"] = c
+    launches = {}
+    for name, xv in cases.items():
+        x = xv.astype(np.float32 if dtype == "f32" else np.float64)
+        xd = torch.from_numpy(x).cuda()
+        xs = np.sort(x)
+        for k in (O.median_rank(n), n // 2 + 777, n // 3):
+            v, info = cp.select_kth(xd, k, return_info=True)
+            assert v == canon(float(xs[k - 1])), (name, k, v, info)
+            launches[(name, k)] = info["launches"]
+    km = O.median_rank(n)
+    # the cluster's bin overflows: the key-digit radix select runs after the finish (more launches)
+    assert launches[("dense_cluster", km)] > launches[("smooth", km)] == launches[("one_value", km)], launches
