@@ -577,13 +577,14 @@ def test_value_binned_finish_paths(cp, dtype):
     n = (1 << 23) + 11
     rng = np.random.default_rng(23)
     base = rng.random(n).astype(np.float64)
+    # the init's sample cuts (8192 samples at this n) keep about +-2% of the ranks around the target:
+    # a value bin is ~2e-5 wide here
     cases = {"smooth": base.copy()}
-    d = base.copy()
-    d[rng.choice(n, 300_000, replace=False)] = 0.5          # one value at the median
-    cases["one_value"] = d
+    cases["one_value"] = np.floor(base * 500.0) / 500.0      # 500 levels ~2e-3 apart: a bin holds one
     c = base.copy()
-    idx = rng.choice(n, 400_000, replace=False)
-    c[idx] = 0.5 + rng.random(idx.size) * 2e-6               # 400k distinct values in one bin width
+    idx = rng.choice(n, 40_000, replace=False)              # 0.5% of the ranks, inside the cuts:
+    ulp = float(np.spacing(np.float32(0.5)))                 # 40k elements on 10 values ~6e-7 apart,
+    c[idx] = 0.5 + ulp * rng.integers(0, 10, idx.size)       # one bin over its 16384-element capacity
     cases["dense_cluster"] = c
     launches = {}
     for name, xv in cases.items():
