@@ -59,7 +59,8 @@ torch.cuda.synchronize()
 # loop (CUDA graph), the bisection driver, kNN, and the loopback-sharded path at G = 2
 x = datagen.make("mix2", n, "f32")
 xd = torch.from_numpy(x).cuda()
-for cfg in (dict(init_cut=0, pass_cuts=0, objective=1, device_loop=1), dict(init_cut=0, pass_cuts=0, driver=1)):
+for cfg in (dict(init_cut=0, pass_cuts=0, objective=1, device_loop=1), dict(init_cut=0, pass_cuts=0, driver=1),
+            dict(init_cut=0, pass_cuts=0, driver=3)):
     cp.set_config(**cfg)
     assert cp.select_kth(xd, 777) == float(O.order_statistic(x, 777)), cfg
     cp.set_config(init_cut=1, pass_cuts=1, objective=0, device_loop=0, driver=0)
@@ -87,5 +88,17 @@ th_ = [threading.Thread(target=rank, args=(g,)) for g in range(2)]
 [t.start() for t in th_]
 [t.join() for t in th_]
 assert res[0] == res[1] == float(O.order_statistic(xs, 4_500_001)), res
+torch.cuda.synchronize()
+print("sanitize workload ok")
+# round-2 (late) additions: the value-binned finish's overflow fallback (a dense cluster at the
+# target), f64 through the value bins, Brent's minimisation driver (above)
+nb = (1 << 23) + 11
+rng = np.random.default_rng(23)
+xc = rng.random(nb).astype(np.float32)
+idc = rng.choice(nb, 40_000, replace=False)
+xc[idc] = np.float32(0.5) + np.float32(np.spacing(np.float32(0.5))) * rng.integers(0, 10, idc.size).astype(np.float32)
+assert cp.median(torch.from_numpy(xc).cuda()) == float(O.median(xc))
+xf = rng.random(nb)
+assert cp.median(torch.from_numpy(xf).cuda()) == float(O.median(xf))
 torch.cuda.synchronize()
 print("sanitize workload ok")
