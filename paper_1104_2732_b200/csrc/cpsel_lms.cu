@@ -71,8 +71,11 @@ __device__ __forceinline__ uint32_t tf32_rna(float x) {
   return r;
 }
 
+// extra (fold): column p carries extra_v[row] (X: y_i) or extra_c (Theta: -1), so the product is
+// x_i . theta_j - y_i — the residual itself comes out of the tensor core (p <= 15)
 __global__ void pack_rows_kernel(const float* __restrict__ src, uint64_t rows, uint32_t p, int tile_rows,
-                                 unsigned char* __restrict__ img) {
+                                 unsigned char* __restrict__ img, int extra = 0, const float* extra_v = nullptr,
+                                 float extra_c = 0.f) {
   const uint64_t tile = blockIdx.x;
   const int r = threadIdx.x;
   const uint64_t row = tile * tile_rows + r;
@@ -80,7 +83,8 @@ __global__ void pack_rows_kernel(const float* __restrict__ src, uint64_t rows, u
   unsigned char* base = img + tile * (uint64_t)(2 * half);
 #pragma unroll
   for (int k = 0; k < KP; ++k) {
-    const float v = (row < rows && k < (int)p) ? src[row * p + k] : 0.f;
+    float v = (row < rows && k < (int)p) ? src[row * p + k] : 0.f;
+    if (extra && k == (int)p && row < rows) v = extra_v ? extra_v[row] : extra_c;
     const uint32_t hi = tf32_rna(v);
     const uint32_t lo = tf32_rna(v - __uint_as_float(hi));
     *reinterpret_cast<uint32_t*>(base + core_off(r, k)) = hi;
@@ -326,6 +330,20 @@ __device__ __forceinline__ void resid2(uint32_t a0, uint32_t a1, unsigned long l
   s1 = __uint_as_float((uint32_t)(sq >> 32));
 }
 
+// FOLD (y folded into the product, p <= 15): the accumulator already holds the residuals r — only
+// the squares remain (one FMUL2 per two rows, the same IEEE round-to-nearest as FMUL)
+template <bool FOLD>
+__device__ __forceinline__ void resid2x(uint32_t a0, uint32_t a1, unsigned long long y01, float& s0, float& s1) {
+  if (FOLD) {
+    unsigned long long acc = ((unsigned long long)a1 << 32) | a0, sq;
+    asm("mul.rn.f32x2 %0, %1, %1;" : "=l"(sq) : "l"(acc));
+    s0 = __uint_as_float((uint32_t)sq);
+    s1 = __uint_as_float((uint32_t)(sq >> 32));
+  } else {
+    resid2(a0, a1, y01, s0, s1);
+  }
+}
+
 // The per-element step of the fused cut pass (a1 + R23 + a4 on one residual).  Every s is >= 0 (or
 // +Inf for a padded row), so float order is unsigned order of the bits: with d = bits(s) - lo1,
 // lo1 = bits(t_lo) + 1, s <= t_lo iff d wraps (its top bit is set: #s <= t_lo += d >> 31) and
@@ -370,7 +388,7 @@ __device__ __forceinline__ void stage_out(uint32_t base_sa, uint32_t cnt, float*
 // such threads at once, each writing ITS first kFlush to its column's copy (16-byte shared loads of
 // its own slots, no cross-lane traffic: one pass of the warp however many lanes flush) and moving
 // the rest to the front of its slots.
-template <bool FULL>
+template <bool FULL, bool FOLD>
 __device__ __forceinline__ void cut_half(const uint32_t* r, int h, const ulonglong2* yv, int nvalid, uint32_t lo1,
                                          uint32_t wcut, uint32_t& le, uint32_t& le2, uint32_t& ta,
                                          uint32_t base_sa, const FusedArgs& a, uint32_t j, float* zcol) {
@@ -379,7 +397,7 @@ __device__ __forceinline__ void cut_half(const uint32_t* r, int h, const ulonglo
     const int i = h * 16 + jj;
     const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
     float s0, s1;
-    resid2(r[i], r[i + 1], y01, s0, s1);
+    resid2x<FOLD>(r[i], r[i + 1], y01, s0, s1);
     if (FULL) {
       cut_elem(s0, lo1, wcut, le, ta);
       cut_elem(s1, lo1, wcut, le2, ta);  // two counters: half the dependent chain
@@ -413,7 +431,7 @@ __device__ __forceinline__ void cut_half(const uint32_t* r, int h, const ulonglo
   }
 }
 
-template <int MODE>
+template <int MODE, bool FOLD>
 __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -454,7 +472,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == kFYWarp) {
+  if (!FOLD && warp == kFYWarp) {
     // ---------------- y stager: the sub-tile's 128 y values into ybuf[s] once the epilogue released
     //                  accumulator stage s (the epilogue reads them as shared-memory broadcasts).
     //                  A plain warp copy (512 B per sub-tile; 16 B per lane), released to the
@@ -531,7 +549,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         __syncwarp();
       }
     }
-  } else if (warp >= 2) {
+  } else if (warp >= 2 && warp < 2 + kFEpiWarps) {
     // ---------------- epilogue: warps 2..17 -> TMEM lane quarter (warp % 4) = 32 candidates,
     //                  row quarter rq: rows [rq*32, rq*32+32) of each 128-row sub-tile
     const int q = warp & 3;
@@ -568,7 +586,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         const int nvalid = ur_left >= roff + 32 ? 32 : (ur_left > roff ? (int)(ur_left - roff) : 0);
         if (c == 0) {
           mbar_wait_sleep(&tfull[s], ph);
-          mbar_wait_sleep(&yfull[s], ph);
+          if (!FOLD) mbar_wait_sleep(&yfull[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;");
         }
         const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + s * FS + rq * kWR + c * 32;
@@ -576,9 +594,14 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         uint32_t r[32];
         TMEM_LD32(taddr, r);
         ulonglong2 yv[8];
+        if (!FOLD) {
 #pragma unroll
-        for (int v = 0; v < 8; ++v)  // shared-memory broadcast (LDS.128)
-          asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(yv[v].x), "=l"(yv[v].y) : "r"(ys_sa + v * 16));
+          for (int v = 0; v < 8; ++v)  // shared-memory broadcast (LDS.128)
+            asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(yv[v].x), "=l"(yv[v].y) : "r"(ys_sa + v * 16));
+        } else {
+#pragma unroll
+          for (int v = 0; v < 8; ++v) yv[v].x = yv[v].y = 0ull;  // unused
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c == kChunks - 1) {
           // the sub-tile's last accumulator columns and y are in registers: release the stage
@@ -590,11 +613,11 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
         }
         if (MODE == kFuseCuts) {
           if (nvalid == 32) {
-            cut_half<true>(r, 0, yv, 32, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
-            cut_half<true>(r, 1, yv, 32, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+            cut_half<true, FOLD>(r, 0, yv, 32, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+            cut_half<true, FOLD>(r, 1, yv, 32, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
           } else {  // the ragged end of x: padded rows enter as +Inf
-            cut_half<false>(r, 0, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
-            cut_half<false>(r, 1, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+            cut_half<false, FOLD>(r, 0, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
+            cut_half<false, FOLD>(r, 1, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
           }
         } else if (MODE == kFuseStore) {
           if (slot >= 0) {
@@ -604,8 +627,8 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
 #pragma unroll
               for (int i = 0; i < 32; i += 4) {
                 float s0, s1, s2, s3;
-                resid2(r[i], r[i + 1], yv[i >> 2].x, s0, s1);
-                resid2(r[i + 2], r[i + 3], yv[i >> 2].y, s2, s3);
+                resid2x<FOLD>(r[i], r[i + 1], yv[i >> 2].x, s0, s1);
+                resid2x<FOLD>(r[i + 2], r[i + 3], yv[i >> 2].y, s2, s3);
                 __stcs(reinterpret_cast<float4*>(dst + i), make_float4(s0, s1, s2, s3));
               }
             } else {
@@ -613,7 +636,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
               for (int i = 0; i < 32; i += 2) {
                 const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
                 float s0, s1;
-                resid2(r[i], r[i + 1], y01, s0, s1);
+                resid2x<FOLD>(r[i], r[i + 1], y01, s0, s1);
                 if (i < nvalid) __stcs(dst + i, s0);
                 if (i + 1 < nvalid) __stcs(dst + i + 1, s1);
               }
@@ -625,7 +648,7 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
           for (int i = 0; i < 32; i += 2) {
             const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
             float s0, s1;
-            resid2(r[i], r[i + 1], y01, s0, s1);
+            resid2x<FOLD>(r[i], r[i + 1], y01, s0, s1);
             if (i < nvalid && s0 < mj) { lsum += (double)s0; ++c; }
             if (i + 1 < nvalid && s1 < mj) { lsum += (double)s1; ++c; }
           }
@@ -828,6 +851,7 @@ struct FusedGeom {
   uint32_t n_ct, n_rt, n_chunks, rt_per_unit = kRtPerUnit, b_ct_stride = 0;
   unsigned char *a_img, *b_img;
   float* y_pad;
+  bool fold = false;  // y folded into the images (column p): the product is the residual (p < 16)
 };
 
 __global__ void slot_map_kernel(int* slot, uint32_t C, const unsigned* list, uint32_t nlist) {
@@ -866,14 +890,20 @@ cudaError_t fused_prepare(LmsWorkspace& w, const float* X, const float* y, uint6
   g.a_img = static_cast<unsigned char*>(w.fimg);
   g.b_img = g.a_img + (size_t)g.n_ct * A_IMG;
   g.y_pad = reinterpret_cast<float*>(g.b_img + (size_t)g.n_rt * B_IMG);
-  pack_rows_kernel<<<g.n_ct, TM, 0, st>>>(thetas, C, p, TM, g.a_img);
-  pack_rows_kernel<<<g.n_rt, FN, 0, st>>>(X, n, p, FN, g.b_img);
-  pad_copy_kernel<<<512, 256, 0, st>>>(y, n, g.y_pad, (uint64_t)g.n_rt * FN);
+  g.fold = p < (uint32_t)KP;
+  if (g.fold) {  // r = [x_i, y_i] . [theta_j, -1]: the residual comes out of the tensor core
+    pack_rows_kernel<<<g.n_ct, TM, 0, st>>>(thetas, C, p, TM, g.a_img, 1, nullptr, -1.f);
+    pack_rows_kernel<<<g.n_rt, FN, 0, st>>>(X, n, p, FN, g.b_img, 1, y, 0.f);
+  } else {
+    pack_rows_kernel<<<g.n_ct, TM, 0, st>>>(thetas, C, p, TM, g.a_img);
+    pack_rows_kernel<<<g.n_rt, FN, 0, st>>>(X, n, p, FN, g.b_img);
+    pad_copy_kernel<<<512, 256, 0, st>>>(y, n, g.y_pad, (uint64_t)g.n_rt * FN);
+  }
   return cudaGetLastError();
 }
 
-template <int MODE>
-cudaError_t fused_launch(const FusedGeom& g, FusedArgs a, uint32_t n_ct_list, cudaStream_t st) {
+template <int MODE, bool FOLD>
+cudaError_t fused_launch_t(const FusedGeom& g, FusedArgs a, uint32_t n_ct_list, cudaStream_t st) {
   a.a_img = g.a_img;
   a.b_img = g.b_img;
   a.y = g.y_pad;
@@ -882,7 +912,7 @@ cudaError_t fused_launch(const FusedGeom& g, FusedArgs a, uint32_t n_ct_list, cu
   a.n_chunks = g.n_chunks;
   a.b_ct_stride = g.b_ct_stride;
   a.n_ct_list = n_ct_list;
-  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<MODE, FOLD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)kFusedSmem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 148;
@@ -890,8 +920,12 @@ cudaError_t fused_launch(const FusedGeom& g, FusedArgs a, uint32_t n_ct_list, cu
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const uint32_t units = n_ct_list * g.n_chunks;
   const int grid = (int)(units < (uint32_t)sms ? units : (uint32_t)sms);
-  fused_tc_kernel<MODE><<<grid, kFThreads, kFusedSmem, st>>>(a);
+  fused_tc_kernel<MODE, FOLD><<<grid, kFThreads, kFusedSmem, st>>>(a);
   return cudaGetLastError();
+}
+template <int MODE>
+cudaError_t fused_launch(const FusedGeom& g, FusedArgs a, uint32_t n_ct_list, cudaStream_t st) {
+  return g.fold ? fused_launch_t<MODE, true>(g, a, n_ct_list, st) : fused_launch_t<MODE, false>(g, a, n_ct_list, st);
 }
 
 // per-column arrays in w.fcol
@@ -966,8 +1000,10 @@ cudaError_t fused_sample_cuts(LmsWorkspace& w, const FusedGeom& g, const float* 
   float* Xs = ys + (size_t)gs.n_ct * ms;
   gs.y_pad = ys;  // ms is a multiple of the row tile: no padding
   gs.a_img = g.a_img;
+  gs.fold = g.fold;
   gather_sample_kernel<<<dim3(ms / 256, gs.n_ct), 256, 0, st>>>(X, y, n, p, ms, Xs, ys);
-  pack_rows_kernel<<<gs.n_ct * gs.n_rt, FN, 0, st>>>(Xs, (uint64_t)gs.n_ct * ms, p, FN, gs.b_img);
+  pack_rows_kernel<<<gs.n_ct * gs.n_rt, FN, 0, st>>>(Xs, (uint64_t)gs.n_ct * ms, p, FN, gs.b_img, gs.fold ? 1 : 0,
+                                                     ys, 0.f);
   slot_map_kernel<<<1, 1024, 0, st>>>(c.slot, C, nullptr, C);
   FusedArgs a{};
   a.n = ms; a.C = C; a.ct_list = c.ct_list; a.slot = c.slot; a.S = Ss;
