@@ -175,7 +175,7 @@ def lms_side(cp, torch, datagen, dev, reps=5):
     fused_ms = info["kernel_ms_init"]          # sample cuts + the fused tensor-core pass
     sm_mhz = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
-    peak_el = 148 * 4 * sm_mhz * 1e6 * 32 / 6.0  # residual-steps/s at full issue, 6 instr each
+    peak_el = 148 * 4 * sm_mhz * 1e6 * 32 / 5.5  # residual-steps/s at full issue, 5.5 instr each
     return {"workload": "LMS objective n=1e6 p=10 C=4096 (BASELINE configs[4]), fused path",
             "ms": ms, "candidates_per_s": C / (ms / 1e3), "residuals_per_s": n * C / (ms / 1e3),
             "fused_stage_ms": fused_ms, "continuation_ms": info["kernel_ms_passes"],
@@ -183,9 +183,10 @@ def lms_side(cp, torch, datagen, dev, reps=5):
             "roofline_fused_stage": {"bound": "alu", "unit": "residuals/s", "achieved": n * C / (fused_ms / 1e3),
                                      "peak": peak_el, "frac": n * C / (fused_ms / 1e3) / peak_el,
                                      "peak_note": "issue rate 148x4x1 warp-instr/clk at sm_max_mhz, "
-                                                  "6 thread-instructions per residual (FADD2/FMUL2 + the "
-                                                  "5-instruction cut step); the stage also includes the "
-                                                  "sample-cut kernels"}}
+                                                  "5.5 thread-instructions per residual (one FMUL2 per two "
+                                                  "residuals — y is folded into the tensor-core product, "
+                                                  "R39 — + the 5-instruction cut step); the stage also "
+                                                  "includes the sample-cut kernels"}}
 
 
 # ------------------------------------------------------------------------------ side blocks (N=1)
