@@ -620,27 +620,29 @@ __global__ void __launch_bounds__(kFThreads, 1) fused_tc_kernel(FusedArgs a) {
             cut_half<false, FOLD>(r, 1, yv, nvalid, lo1, wcut, le, le2, ta, base_sa, a, j, zcol);
           }
         } else if (MODE == kFuseStore) {
-          if (slot >= 0) {
-            const uint64_t rowc = urow + roff;
-            float* dst = a.S + (size_t)slot * a.n + rowc;
-            if (nvalid == 32 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {  // 8 x 16-byte stores
+          // the warp's 32 columns x 32 rows transposed through its staging slots (row stride 33
+          // words: conflict-free both ways), so every store writes 32 consecutive rows (128 bytes)
+          // of one column instead of 16 bytes of 32 columns
+          if (__any_sync(0xffffffffu, slot >= 0)) {
+            const uint32_t tb = ring_sa + kLaneStage * 32u * (uint32_t)(warp - 2);
 #pragma unroll
-              for (int i = 0; i < 32; i += 4) {
-                float s0, s1, s2, s3;
-                resid2x<FOLD>(r[i], r[i + 1], yv[i >> 2].x, s0, s1);
-                resid2x<FOLD>(r[i + 2], r[i + 3], yv[i >> 2].y, s2, s3);
-                __stcs(reinterpret_cast<float4*>(dst + i), make_float4(s0, s1, s2, s3));
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; i += 2) {
-                const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
-                float s0, s1;
-                resid2x<FOLD>(r[i], r[i + 1], y01, s0, s1);
-                if (i < nvalid) __stcs(dst + i, s0);
-                if (i + 1 < nvalid) __stcs(dst + i + 1, s1);
-              }
+            for (int i = 0; i < 32; i += 2) {
+              const unsigned long long y01 = (i & 2) ? yv[i >> 2].y : yv[i >> 2].x;
+              float s0, s1;
+              resid2x<FOLD>(r[i], r[i + 1], y01, s0, s1);
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(tb + (uint32_t)(i * 33 + lane) * 4u), "f"(s0) : "memory");
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(tb + (uint32_t)((i + 1) * 33 + lane) * 4u), "f"(s1) : "memory");
             }
+            __syncwarp();
+            const uint64_t rowc = urow + roff;
+#pragma unroll 4
+            for (int cc2 = 0; cc2 < 32; ++cc2) {
+              const int sl = __shfl_sync(0xffffffffu, slot, cc2);
+              float v;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(tb + (uint32_t)(lane * 33 + cc2) * 4u));
+              if (sl >= 0 && lane < nvalid) __stcs(a.S + (size_t)sl * a.n + rowc + lane, v);
+            }
+            __syncwarp();  // the slots are rewritten by the next chunk
           }
         } else {
           unsigned c = 0;
