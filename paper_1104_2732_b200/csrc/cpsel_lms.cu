@@ -981,6 +981,31 @@ __global__ void gather_sample_kernel(const float* __restrict__ X, const float* _
   }
 }
 
+// The same rows packed straight into the fold image (X with y as column p), no gathered copy: tile t
+// of candidate tile ct = t / (ms / FN) holds sample rows (i * n) / ms + phase(ct) of X.
+__global__ void pack_sample_fold_kernel(const float* __restrict__ X, const float* __restrict__ y, uint64_t n,
+                                        uint32_t p, uint32_t ms, unsigned char* __restrict__ img) {
+  const uint32_t tiles_per_ct = ms / FN;
+  const uint64_t tile = blockIdx.x;
+  const uint32_t ct = (uint32_t)(tile / tiles_per_ct);
+  const uint32_t i = (uint32_t)(tile % tiles_per_ct) * FN + threadIdx.x;  // sample index within ct
+  const uint64_t stride = n / ms;
+  const uint64_t phase = ((uint64_t)ct * 2654435761ull) % stride;
+  const uint64_t row = ((uint64_t)i * n) / ms + phase;  // < n (as gather_sample_kernel)
+  const int half = FN * KP * 4;
+  unsigned char* base = img + tile * (uint64_t)(2 * half);
+  const int r = threadIdx.x;
+#pragma unroll
+  for (int k = 0; k < KP; ++k) {
+    float v = k < (int)p ? X[row * p + k] : 0.f;
+    if (k == (int)p) v = y[row];
+    const uint32_t hi = tf32_rna(v);
+    const uint32_t lo = tf32_rna(v - __uint_as_float(hi));
+    *reinterpret_cast<uint32_t*>(base + core_off(r, k)) = hi;
+    *reinterpret_cast<uint32_t*>(base + half + core_off(r, k)) = lo;
+  }
+}
+
 cudaError_t fused_sample_cuts(LmsWorkspace& w, const FusedGeom& g, const float* X, const float* y, uint64_t n,
                               uint32_t p, uint32_t C, uint64_t k, const FusedCols& c, cudaStream_t st) {
   const uint32_t ms = kLmsSamples;
@@ -1003,9 +1028,12 @@ cudaError_t fused_sample_cuts(LmsWorkspace& w, const FusedGeom& g, const float* 
   gs.y_pad = ys;  // ms is a multiple of the row tile: no padding
   gs.a_img = g.a_img;
   gs.fold = g.fold;
-  gather_sample_kernel<<<dim3(ms / 256, gs.n_ct), 256, 0, st>>>(X, y, n, p, ms, Xs, ys);
-  pack_rows_kernel<<<gs.n_ct * gs.n_rt, FN, 0, st>>>(Xs, (uint64_t)gs.n_ct * ms, p, FN, gs.b_img, gs.fold ? 1 : 0,
-                                                     ys, 0.f);
+  if (gs.fold) {  // y is column p of the image: the strided rows packed directly
+    pack_sample_fold_kernel<<<gs.n_ct * gs.n_rt, FN, 0, st>>>(X, y, n, p, ms, gs.b_img);
+  } else {
+    gather_sample_kernel<<<dim3(ms / 256, gs.n_ct), 256, 0, st>>>(X, y, n, p, ms, Xs, ys);
+    pack_rows_kernel<<<gs.n_ct * gs.n_rt, FN, 0, st>>>(Xs, (uint64_t)gs.n_ct * ms, p, FN, gs.b_img);
+  }
   slot_map_kernel<<<1, 1024, 0, st>>>(c.slot, C, nullptr, C);
   FusedArgs a{};
   a.n = ms; a.C = C; a.ct_list = c.ct_list; a.slot = c.slot; a.S = Ss;
