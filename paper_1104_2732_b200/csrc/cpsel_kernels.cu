@@ -2923,26 +2923,30 @@ __device__ void batch_sample_cuts(BatchState& st, unsigned* hist, const float* z
 // edge of the hi target's (>=): cuts at most 2^max(0, sh-11) key units wider than the exact sample
 // quantiles, which is all a cut needs — the fused pass counts exactly at whatever values they are.
 // One CTA of 1024 threads per column.
-// Each CTA walks its columns with the next column's samples prefetched into shared memory by one
-// bulk copy (double-buffered) while the current one is histogrammed; the counters take predicated
-// shared reductions (no divergent branches).
-constexpr int kCutThreads = 1024;
-constexpr int kCutMaxPer = 16;   // <= 16384 samples
-constexpr size_t kCutSmem = 2 * (size_t)kCutThreads * kCutMaxPer * 4 + 64;  // two column buffers + 2 mbarriers
+// Each CTA (512 threads, two per SM, so one CTA's copy and histogram rounds overlap the other's)
+// walks its columns: the column's samples are bulk-copied into the CTA's shared buffer and every
+// round reads its keys from there (32 per thread would not fit the registers of two CTAs per SM).
+// The counters take predicated shared reductions (no divergent branches).
+constexpr int kCutThreads = 512;
+constexpr int kCutMaxPer = 32;   // <= 16384 samples
+constexpr int kCutBPT = 2048 / kCutThreads;  // histogram bins per thread in the scans (one uint4)
+static_assert(kCutBPT == 4, "the scans read one uint4 of bins per thread");
+constexpr size_t kCutSmem = (size_t)kCutThreads * kCutMaxPer * 4 + 64;  // one column buffer + an mbarrier
 __device__ __forceinline__ void red_shared_add1(uint32_t addr, bool p) {
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %1, 0;\n\t@q red.shared.add.u32 [%0], 1;\n\t}" ::"r"(addr), "r"((int)p)
                : "memory");
 }
-__global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* __restrict__ Ss, uint32_t ms,
+__global__ void __launch_bounds__(kCutThreads, 2) lms_cuts_kernel(const float* __restrict__ Ss, uint32_t ms,
                                                                   uint64_t n, uint32_t C, uint64_t k,
                                                                   float* __restrict__ cuts) {
-  __shared__ unsigned hist[3][2048];
-  __shared__ unsigned wsum[3][32];
+  constexpr int NW = kCutThreads / 32;
+  __shared__ __align__(16) unsigned hist[3][2048];
+  __shared__ unsigned wsum[3][NW];
   __shared__ unsigned sel[3][2];
-  __shared__ unsigned wmin[32], wmax[32];
+  __shared__ unsigned wmin[NW], wmax[NW];
   extern __shared__ __align__(16) unsigned char cut_smem[];
-  float* buf = reinterpret_cast<float*>(cut_smem);  // [2][kCutThreads * kCutMaxPer]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(cut_smem + 2 * (size_t)kCutThreads * kCutMaxPer * 4);
+  float* buf = reinterpret_cast<float*>(cut_smem);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(cut_smem + (size_t)kCutThreads * kCutMaxPer * 4);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t col_bytes = ms * 4u;  // a multiple of 16 (ms is a multiple of 256)
   unsigned rank[3];
@@ -2957,20 +2961,18 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
   }
   if (tid == 0) {
     mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0 && blockIdx.x < C) {
-    mbar_expect_tx(&bar[0], col_bytes);
-    bulk_g2s(buf, Ss + (size_t)blockIdx.x * ms, col_bytes, &bar[0]);
-  }
   uint32_t it = 0;
+  const float4* cb = reinterpret_cast<const float4*>(buf);
   for (uint32_t j = blockIdx.x; j < C; j += gridDim.x, ++it) {
-    const uint32_t b = it & 1;
-    mbar_wait(&bar[b], (it >> 1) & 1);
-    const float4* cb = reinterpret_cast<const float4*>(buf + (size_t)b * kCutThreads * kCutMaxPer);
-    unsigned key[kCutMaxPer];
+    if (tid == 0) {  // (every thread's reads of the previous column ended at the last barrier)
+      fence_proxy_async_smem();
+      mbar_expect_tx(&bar[0], col_bytes);
+      bulk_g2s(buf, Ss + (size_t)j * ms, col_bytes, &bar[0]);
+    }
+    mbar_wait(&bar[0], it & 1);
     unsigned kmn = 0xffffffffu, kmx = 0u;
 #pragma unroll
     for (int v = 0; v < kCutMaxPer / 4; ++v) {  // element (v * kCutThreads + tid) * 4 + c: order is irrelevant
@@ -2979,11 +2981,10 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
       const float qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        const bool ok = e4 * 4 + c < ms;
-        key[4 * v + c] = (unsigned)okey(qq[c]);
-        if (ok) {
-          kmn = min(kmn, key[4 * v + c]);
-          kmx = max(kmx, key[4 * v + c]);
+        if (e4 * 4 + c < ms) {
+          const unsigned kk = (unsigned)okey(qq[c]);
+          kmn = min(kmn, kk);
+          kmx = max(kmx, kk);
         }
       }
     }
@@ -2991,15 +2992,9 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
     kmx = __reduce_max_sync(0xffffffffu, kmx);
     if (lane == 0) { wmin[wid] = kmn; wmax[wid] = kmx; }
     for (int i = tid; i < 3 * 2048; i += kCutThreads) (&hist[0][0])[i] = 0u;
-    __syncthreads();  // every thread has its keys: buffer b is free for the column after next
-    if (tid == 0 && j + gridDim.x < C) {
-      fence_proxy_async_smem();
-      mbar_expect_tx(&bar[b ^ 1], col_bytes);
-      bulk_g2s(buf + (size_t)(b ^ 1) * kCutThreads * kCutMaxPer, Ss + (size_t)(j + gridDim.x) * ms, col_bytes,
-               &bar[b ^ 1]);
-    }
-    kmn = __reduce_min_sync(0xffffffffu, wmin[lane]);
-    kmx = __reduce_max_sync(0xffffffffu, wmax[lane]);
+    __syncthreads();
+    kmn = __reduce_min_sync(0xffffffffu, lane < NW ? wmin[lane] : 0xffffffffu);
+    kmx = __reduce_max_sync(0xffffffffu, lane < NW ? wmax[lane] : 0u);
     // d = key - kmin < 2^span_bits; round 0 takes d >> sh0 (11 bits), round 1 the bits below
     const unsigned span = kmx - kmn;
     const int span_bits = span ? 32 - __clz(span) : 0;
@@ -3014,27 +3009,33 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
         for (int i = tid; i < 2048; i += kCutThreads) hist[0][i] = 0u;  // (1, 2 still zero)
         __syncthreads();
       }
+#pragma unroll 2
+      for (int v = 0; v < kCutMaxPer / 4; ++v) {  // 16-byte reads of the column (conflict-free)
+        const uint32_t e4 = v * kCutThreads + tid;
+        const float4 q = cb[e4];
+        const float qq[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-      for (int u = 0; u < kCutMaxPer; ++u) {
-        const bool ok = ((u >> 2) * kCutThreads + tid) * 4 + (u & 3) < ms;
-        const unsigned d = key[u] - kmn;
-        if (round == 0) {
-          red_shared_add1(h0 + 4u * (d >> sh0), ok);
-        } else {
-          const unsigned top = d >> sh0, dd = 4u * ((d >> sh1) & m1);
-          red_shared_add1(h0 + dd, ok && top == bin[0]);
-          red_shared_add1(h1 + dd, ok && top == bin[1]);
-          red_shared_add1(h2 + dd, ok && top == bin[2]);
+        for (int c = 0; c < 4; ++c) {
+          const bool ok = e4 * 4 + c < ms;
+          const unsigned d = (unsigned)okey(qq[c]) - kmn;
+          if (round == 0) {
+            red_shared_add1(h0 + 4u * (d >> sh0), ok);
+          } else {
+            const unsigned top = d >> sh0, dd = 4u * ((d >> sh1) & m1);
+            red_shared_add1(h0 + dd, ok && top == bin[0]);
+            red_shared_add1(h1 + dd, ok && top == bin[1]);
+            red_shared_add1(h2 + dd, ok && top == bin[2]);
+          }
         }
       }
       __syncthreads();
-      unsigned c0[3], c1[3], incl[3];
+      unsigned incl[3], tsum[3];
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         const int hsrc = round == 0 ? 0 : t;
-        c0[t] = hist[hsrc][2 * tid];
-        c1[t] = hist[hsrc][2 * tid + 1];
-        unsigned v = c0[t] + c1[t];
+        const uint4 hv = reinterpret_cast<const uint4*>(&hist[hsrc][0])[tid];  // kCutBPT == 4 bins
+        tsum[t] = hv.x + hv.y + hv.z + hv.w;
+        unsigned v = tsum[t];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const unsigned w = __shfl_up_sync(0xffffffffu, v, o);
@@ -3047,25 +3048,30 @@ __global__ void __launch_bounds__(kCutThreads, 1) lms_cuts_kernel(const float* _
       if (wid == 0) {
 #pragma unroll
         for (int t = 0; t < 3; ++t) {
-          unsigned v = wsum[t][lane];
+          unsigned v = lane < NW ? wsum[t][lane] : 0u;
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
             const unsigned w = __shfl_up_sync(0xffffffffu, v, o);
             if (lane >= o) v += w;
           }
-          wsum[t][lane] = v;
+          if (lane < NW) wsum[t][lane] = v;
         }
       }
       __syncthreads();
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
-        const unsigned before = (wid ? wsum[t][wid - 1] : 0u) + incl[t] - c0[t] - c1[t];
-        if (before <= rk[t] && rk[t] < before + c0[t]) {
-          sel[t][0] = 2u * tid;
-          sel[t][1] = before;
-        } else if (before + c0[t] <= rk[t] && rk[t] < before + c0[t] + c1[t]) {
-          sel[t][0] = 2u * tid + 1u;
-          sel[t][1] = before + c0[t];
+        unsigned before = (wid ? wsum[t][wid - 1] : 0u) + incl[t] - tsum[t];
+        if (before <= rk[t] && rk[t] < before + tsum[t]) {  // this thread's 4 bins hold the rank
+          const uint4 hv = reinterpret_cast<const uint4*>(&hist[round == 0 ? 0 : t][0])[tid];
+          const unsigned cv[4] = {hv.x, hv.y, hv.z, hv.w};
+#pragma unroll
+          for (int q = 0; q < kCutBPT; ++q) {
+            if (before <= rk[t] && rk[t] < before + cv[q]) {
+              sel[t][0] = (unsigned)(kCutBPT * tid + q);
+              sel[t][1] = before;
+            }
+            before += cv[q];
+          }
         }
       }
       __syncthreads();
