@@ -1044,58 +1044,59 @@ cudaError_t fused_sample_cuts(LmsWorkspace& w, const FusedGeom& g, const float* 
 
 // Input check of the fused path: the fused pass does not test its residuals for NaN/Inf, so the
 // inputs are checked instead — every s = (x.theta - y)^2 is finite when X, y, Theta are finite and
-// B = sum_l max_i|X_il| max_j|theta_lj| + max_i|y_i| < 2^60 (|r| <= B(1 + 2^-20) with the 3xTF32
-// split and fp32 accumulation, so s < 2^121 < FLT_MAX).  out: [0] non-finite count, [1..p] max|X_l|,
-// [p+1..2p] max|theta_l|, [2p+1] max|y| (float bits; all values >= 0 so unsigned order = float order).
+// B = p max|X| max|theta| + max|y| < 2^60 (|r| <= sum_l |x_l||theta_l| + |y| <= B, times (1 + 2^-20)
+// for the 3xTF32 split and fp32 accumulation, so s < 2^121 < FLT_MAX).  One flat, 16-byte-load pass
+// over each array (the per-coordinate maxima of round 1 cost a strided walk: 48 us at configs[4]).
+// out: [0] non-finite count, [1] max|X|, [2] max|theta|, [3] max|y| (float bits; all values >= 0,
+// so unsigned order = float order).
+__device__ __forceinline__ void check_span(const float* __restrict__ a, uint64_t m, unsigned& bad, float& mx) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x, t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t mis = (reinterpret_cast<uintptr_t>(a) / 4) & 3;
+  uint64_t head = mis ? 4 - mis : 0;
+  if (head > m) head = m;
+  const float4* a4 = reinterpret_cast<const float4*>(a + head);
+  const uint64_t nv = (m - head) / 4;
+  for (uint64_t i = t; i < nv; i += stride) {
+    const float4 q = __ldg(a4 + i);  // (cached: the pack reads X right after)
+    const float v[4] = {fabsf(q.x), fabsf(q.y), fabsf(q.z), fabsf(q.w)};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      bad += !(v[c] <= 3.4028235e38f);
+      mx = fmaxf(mx, v[c]);
+    }
+  }
+  const uint64_t tail0 = head + nv * 4;
+  if (t < head) {
+    const float v = fabsf(a[t]);
+    bad += !(v <= 3.4028235e38f);
+    mx = fmaxf(mx, v);
+  }
+  if (t < m - tail0) {
+    const float v = fabsf(a[tail0 + t]);
+    bad += !(v <= 3.4028235e38f);
+    mx = fmaxf(mx, v);
+  }
+}
 __global__ void lms_check_kernel(const float* __restrict__ X, const float* __restrict__ y,
                                  const float* __restrict__ th, uint64_t n, uint32_t p, uint32_t C,
                                  unsigned* __restrict__ out) {
-  float mx[kLmsMaxP];
-#pragma unroll
-  for (int l = 0; l < kLmsMaxP; ++l) mx[l] = 0.f;
-  float my = 0.f, mt[kLmsMaxP];
-#pragma unroll
-  for (int l = 0; l < kLmsMaxP; ++l) mt[l] = 0.f;
   unsigned bad = 0;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-#pragma unroll
-    for (int l = 0; l < kLmsMaxP; ++l)
-      if (l < (int)p) {
-        const float v = fabsf(X[i * p + l]);
-        bad += !(v <= 3.4028235e38f);
-        mx[l] = fmaxf(mx[l], v);
-      }
-    const float v = fabsf(y[i]);
-    bad += !(v <= 3.4028235e38f);
-    my = fmaxf(my, v);
-  }
-  for (uint64_t jj = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; jj < C; jj += stride) {
-#pragma unroll
-    for (int l = 0; l < kLmsMaxP; ++l)
-      if (l < (int)p) {
-        const float v = fabsf(th[jj * p + l]);
-        bad += !(v <= 3.4028235e38f);
-        mt[l] = fmaxf(mt[l], v);
-      }
-  }
+  float mX = 0.f, mT = 0.f, mY = 0.f;
+  check_span(X, n * p, bad, mX);
+  check_span(th, (uint64_t)C * p, bad, mT);
+  check_span(y, n, bad, mY);
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     bad += __shfl_xor_sync(0xffffffffu, bad, o);
-    my = fmaxf(my, __shfl_xor_sync(0xffffffffu, my, o));
-#pragma unroll
-    for (int l = 0; l < kLmsMaxP; ++l) {
-      mx[l] = fmaxf(mx[l], __shfl_xor_sync(0xffffffffu, mx[l], o));
-      mt[l] = fmaxf(mt[l], __shfl_xor_sync(0xffffffffu, mt[l], o));
-    }
+    mX = fmaxf(mX, __shfl_xor_sync(0xffffffffu, mX, o));
+    mT = fmaxf(mT, __shfl_xor_sync(0xffffffffu, mT, o));
+    mY = fmaxf(mY, __shfl_xor_sync(0xffffffffu, mY, o));
   }
   if ((threadIdx.x & 31) == 0) {
     if (bad) atomicAdd(out, bad);
-    for (uint32_t l = 0; l < p; ++l) {
-      atomicMax(out + 1 + l, __float_as_uint(mx[l]));
-      atomicMax(out + 1 + p + l, __float_as_uint(mt[l]));
-    }
-    atomicMax(out + 1 + 2 * p, __float_as_uint(my));
+    atomicMax(out + 1, __float_as_uint(mX));
+    atomicMax(out + 2, __float_as_uint(mT));
+    atomicMax(out + 3, __float_as_uint(mY));
   }
 }
 
@@ -1110,21 +1111,16 @@ int lms_fused_check(LmsWorkspace& w, const float* X, const float* y, uint64_t n,
   }
   unsigned* d = static_cast<unsigned*>(w.fcol);
   if ((*err = cudaMemsetAsync(d, 0, 256, st)) != cudaSuccess) return -1;
-  lms_check_kernel<<<296, 256, 0, st>>>(X, y, thetas, n, p, C, d);
-  if ((*err = cudaMemcpyAsync(w.host, d, (2 * p + 2) * 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return -1;
+  lms_check_kernel<<<296 * 4, 256, 0, st>>>(X, y, thetas, n, p, C, d);
+  if ((*err = cudaMemcpyAsync(w.host, d, 16, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return -1;
   if ((*err = cudaStreamSynchronize(st)) != cudaSuccess) return -1;
   const unsigned* h = static_cast<const unsigned*>(w.host);
   if (h[0]) return 1;
-  double B = 0.0;
-  for (uint32_t l = 0; l < p; ++l) {
-    float a, b;
-    memcpy(&a, h + 1 + l, 4);
-    memcpy(&b, h + 1 + p + l, 4);
-    B += (double)a * (double)b;
-  }
-  float my;
-  memcpy(&my, h + 1 + 2 * p, 4);
-  B += (double)my;
+  float mX, mT, mY;
+  memcpy(&mX, h + 1, 4);
+  memcpy(&mT, h + 2, 4);
+  memcpy(&mY, h + 3, 4);
+  const double B = (double)p * (double)mX * (double)mT + (double)mY;
   return B < 1152921504606846976.0 /* 2^60 */ ? 0 : 2;
 }
 
