@@ -81,14 +81,20 @@ __global__ void pack_rows_kernel(const float* __restrict__ src, uint64_t rows, u
   const uint64_t row = tile * tile_rows + r;
   const int half = tile_rows * KP * 4;
   unsigned char* base = img + tile * (uint64_t)(2 * half);
+  // four consecutive k of one row are one 16-byte chunk of the core-matrix image: 16-byte stores
 #pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    float v = (row < rows && k < (int)p) ? src[row * p + k] : 0.f;
-    if (extra && k == (int)p && row < rows) v = extra_v ? extra_v[row] : extra_c;
-    const uint32_t hi = tf32_rna(v);
-    const uint32_t lo = tf32_rna(v - __uint_as_float(hi));
-    *reinterpret_cast<uint32_t*>(base + core_off(r, k)) = hi;
-    *reinterpret_cast<uint32_t*>(base + half + core_off(r, k)) = lo;
+  for (int kq = 0; kq < KP; kq += 4) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = kq + c;
+      float v = (row < rows && k < (int)p) ? src[row * p + k] : 0.f;
+      if (extra && k == (int)p && row < rows) v = extra_v ? extra_v[row] : extra_c;
+      hi[c] = tf32_rna(v);
+      lo[c] = tf32_rna(v - __uint_as_float(hi[c]));
+    }
+    *reinterpret_cast<uint4*>(base + core_off(r, kq)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(base + half + core_off(r, kq)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
 }
 
@@ -996,13 +1002,18 @@ __global__ void pack_sample_fold_kernel(const float* __restrict__ X, const float
   unsigned char* base = img + tile * (uint64_t)(2 * half);
   const int r = threadIdx.x;
 #pragma unroll
-  for (int k = 0; k < KP; ++k) {
-    float v = k < (int)p ? X[row * p + k] : 0.f;
-    if (k == (int)p) v = y[row];
-    const uint32_t hi = tf32_rna(v);
-    const uint32_t lo = tf32_rna(v - __uint_as_float(hi));
-    *reinterpret_cast<uint32_t*>(base + core_off(r, k)) = hi;
-    *reinterpret_cast<uint32_t*>(base + half + core_off(r, k)) = lo;
+  for (int kq = 0; kq < KP; kq += 4) {
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int k = kq + c;
+      float v = k < (int)p ? X[row * p + k] : 0.f;
+      if (k == (int)p) v = y[row];
+      hi[c] = tf32_rna(v);
+      lo[c] = tf32_rna(v - __uint_as_float(hi[c]));
+    }
+    *reinterpret_cast<uint4*>(base + core_off(r, kq)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    *reinterpret_cast<uint4*>(base + half + core_off(r, kq)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
   }
 }
 
