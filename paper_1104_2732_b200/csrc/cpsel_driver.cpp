@@ -461,6 +461,10 @@ struct GpuBackend : Backend {
   // the direct chain's finish by value bins (launch_vbin_finish: the init counts its copy per value
   // bin of ]t_lo, t_hi[, one pass over the copy and a shared-memory select of the target bin), both
   // dtypes; CPSEL_VBIN=0: the key-digit radix select (init_hist0 for f32)
+  bool sample_grid_on() const {  // R40; CPSEL_SAMPLE_GRID=0: pool_gather + the cluster select
+    static const bool on = !(getenv("CPSEL_SAMPLE_GRID") && getenv("CPSEL_SAMPLE_GRID")[0] == '0');
+    return on;
+  }
   bool vbin_on() const {
     static const bool on = !(getenv("CPSEL_VBIN") && getenv("CPSEL_VBIN")[0] == '0');
     return on;
@@ -576,8 +580,14 @@ struct GpuBackend : Backend {
         // R29: the strided sample gathered by a many-CTA kernel (every SM's load slots, not just the
         // cluster's 8: the gather was latency-bound there), then the cluster select reads it
         // contiguously from L2 — the same sample and the same cuts as the one-launch form
-        CK(launch_pool_gather(dt, x, n, nullptr, 0, 0, S, ctx->d_pool1, ctx->stream));
-        CK(launch_pool_pick(dt, ctx->d_pool1, S, n, k, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
+        if (sample_grid_on()) {
+          // R40: the same sample and cuts in one cooperative launch (d_pool1 as its zeroed scratch)
+          CK(launch_sample_grid(dt, x, n, S, n, k, ctx->d_t0, static_cast<unsigned*>(ctx->d_pool1), ctx->stream,
+                                !ctx->cfg.objective));
+        } else {
+          CK(launch_pool_gather(dt, x, n, nullptr, 0, 0, S, ctx->d_pool1, ctx->stream));
+          CK(launch_pool_pick(dt, ctx->d_pool1, S, n, k, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
+        }
       } else {
         CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream, small, nullptr, 0,
                                 /*allow_open=*/!ctx->cfg.objective));
@@ -2155,6 +2165,8 @@ cpsel_status cpsel_create(int device, void* cuda_stream, cpsel_ctx** out) {
   CKC(cudaMalloc(&ctx->d_t0, 32));  // t_lo, t_hi, the sample estimate
   CKC(cudaMalloc(&ctx->d_skeys, kSampleKeyBytes));
   CKC(cudaMalloc(&ctx->d_pool1, std::max(pool_sample_size(kF32, false) * 4, pool_sample_size(kF64, false) * 8)));
+  // R40's scratch (zero between uses; the two-kernel form, CPSEL_SAMPLE_GRID=0, never runs in the same process)
+  CKC(cudaMemset(ctx->d_pool1, 0, sample_grid_words() * sizeof(unsigned)));
   CKC(cudaMalloc(&ctx->d_chain, sizeof(ChainState)));
   CKC(cudaMalloc(&ctx->d_radix, sizeof(RadixState)));
   // radix rounds | round 0 counted by the init | the cooperative rounds' histograms and barrier

@@ -1,3 +1,6 @@
+#ifdef CPSEL_VB_PROF
+#include <cstdio>
+#endif
 // sm_100a kernels of the cutting-plane selection path (Beliakov, arXiv:1104.2732).
 //
 //   init_kernel   step a1: one streaming pass -> (min, #min, max, #max, sum(x-x0), #nonfinite)
@@ -81,13 +84,14 @@ template <> __device__ __forceinline__ float tinf() { return __int_as_float(0x7f
 template <> __device__ __forceinline__ double tinf() { return __longlong_as_double(0x7ff0000000000000ll); }
 
 // Order-preserving integer keys of floats (radix select, sample cut, ordered-key bisection).
+// (negative: all bits flipped, else the sign bit set — one arithmetic shift and one xor)
 __device__ __forceinline__ unsigned long long okey(float v) {
   const unsigned u = __float_as_uint(v);
-  return (unsigned long long)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
+  return (unsigned long long)(u ^ ((unsigned)(__float_as_int(v) >> 31) | 0x80000000u));
 }
 __device__ __forceinline__ unsigned long long okey(double v) {
-  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
-  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+  const long long s = __double_as_longlong(v);
+  return (unsigned long long)s ^ ((unsigned long long)(s >> 63) | 0x8000000000000000ull);
 }
 __device__ __forceinline__ double from_key_f32(unsigned long long k) {
   const unsigned kk = (unsigned)k;
@@ -1884,14 +1888,25 @@ struct VbArgs {
   unsigned long long seq;
 };
 template <typename T> struct VbFn {
-  T tl, sc;
+  T lo, hi;     // a value interval holding bin b (a superset: vb_bounds), tested first
+  T tl, sc;     // the exact bin test on the few values inside it
   unsigned b;
   bool comp;
   unsigned long long kmin = ~0ull, kmax = 0ull;
   unsigned long long* cnt;
   T* zb;
+  // one vector of VE values: two compares per value, one rarely taken branch per vector
+  template <int VE> __device__ __forceinline__ void vec(const T (&v)[VE]) {
+    bool any = false;
+#pragma unroll
+    for (int j = 0; j < VE; ++j) any |= v[j] >= lo && v[j] <= hi;
+    if (any) {
+#pragma unroll
+      for (int j = 0; j < VE; ++j) elem(v[j], 0, 0);
+    }
+  }
   __device__ __forceinline__ void elem(T v, int, int) {
-    if (vbin_digit(v, tl, sc) == b) {
+    if (v >= lo && v <= hi && vbin_digit(v, tl, sc) == b) {
       const unsigned long long k = okey(v);
       kmin = k < kmin ? k : kmin;
       kmax = k > kmax ? k : kmax;
@@ -1901,9 +1916,37 @@ template <typename T> struct VbFn {
       }
     }
   }
-  __device__ __forceinline__ void begin() {}
-  __device__ __forceinline__ void end() {}
 };
+// A value interval [lo, hi] containing every v of ]tl, th[ whose vbin_digit is b (more is harmless:
+// the exact digit test follows).  Value bins: the digit's two roundings move (v - tl) * sc by less
+// than 2^-p * 2048 * 2 bins (p = 24 / 53), so bin b lies in tl + [b - 1/2, b + 3/2] / sc, evaluated
+// in double (f32: |tl| * sc < 2048 * 2^23, error < 10^-6 bins; f64: within 0.02 bins while
+// |tl| * sc, |th| * sc < 10^14, else the whole span) and rounded outward to T.  Key digits (sc = 0):
+// the values of the key class [b << S, (b + 1) << S).
+template <typename T> __device__ __forceinline__ void vb_bounds(T tl, T th, T sc, unsigned b, T& lo, T& hi) {
+  if (sc > T(0)) {
+    const double dtl = (double)tl, dsc = (double)sc;
+    if (sizeof(T) == 8 && !(fabs(dtl) * dsc < 1e14 && fabs((double)th) * dsc < 1e14)) {
+      lo = tl; hi = th;
+      return;
+    }
+    const double l = dtl + ((double)b - 0.5) / dsc, h = b >= 2047u ? (double)th : dtl + ((double)b + 1.5) / dsc;
+    if (sizeof(T) == 4) {
+      lo = (T)__double2float_rd(l);
+      hi = (T)__double2float_ru(h);
+    } else {
+      lo = (T)l; hi = (T)h;
+    }
+  } else {
+    constexpr int S = sizeof(T) == 4 ? 21 : 53;
+    using K = typename SampleKey<T>::K;
+    lo = SampleKey<T>::val((K)b << S);
+    hi = SampleKey<T>::val((((K)b + 1) << S) - 1);  // b = 2047: the key of the largest NaN, harmless
+    if (b == 2047u) hi = th;
+    if (!(lo == lo)) lo = -tinf<T>();  // a class of NaN keys below -inf / above +inf
+    if (!(hi == hi)) hi = tinf<T>();
+  }
+}
 // the digit of a 2048-bin block histogram h (nb bins) holding rank r (1-based): 1024 threads, two
 // bins each; returns (in shared memory) the digit and the count before it
 __device__ __forceinline__ void pick1024(const unsigned* h, int nb, unsigned long long r, unsigned* wsum,
@@ -1922,8 +1965,14 @@ __device__ __forceinline__ void pick1024(const unsigned* h, int nb, unsigned lon
   }
   if (lane == 31) wsum[w] = incl;
   __syncthreads();
-  unsigned long long before = 0;
-  for (int q = 0; q < w; ++q) before += wsum[q];
+  const unsigned long long ws = wsum[lane];  // the 32 warp totals, scanned by every warp
+  unsigned long long wi = ws;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, wi, o);
+    if (lane >= o) wi += y;
+  }
+  unsigned long long before = __shfl_sync(FULL, wi - ws, w);
   before += incl - tsum;
   if (before < r && r <= before + h0) {
     *s_d = (unsigned)b0; *s_before = before; *s_cnt = h0;
@@ -1932,10 +1981,23 @@ __device__ __forceinline__ void pick1024(const unsigned* h, int nb, unsigned lon
   }
   __syncthreads();
 }
+#ifdef CPSEL_VB_PROF
+__device__ unsigned long long g_vbprof[16];
+#define VBT(i)                                                                  \
+  if (threadIdx.x == 0) {                                                       \
+    unsigned long long t_;                                                      \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+    atomicMin(&g_vbprof[2 * (i)], t_ | 0ull);                                   \
+    atomicMax(&g_vbprof[2 * (i) + 1], t_);                                      \
+  }
+#else
+#define VBT(i)
+#endif
 template <typename T>
 __global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_constant__ VbArgs a) {
   constexpr int NW = 32;
   pdl_wait();  // the init's copy, its bin counts and the chain decision
+  VBT(0);
   if (a.chain && !a.chain->ok[1]) {  // skipped (uniformly): the init's counts must still be cleared
     if (blockIdx.x == 0)
       for (int i = threadIdx.x; i < 2048; i += 1024) a.hist0[i] = 0u;
@@ -1948,14 +2010,16 @@ __global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_const
   __shared__ bool s_last;
   pick1024(a.hist0, 2048, r, wsum, &s_b, &s_base, &s_cb, true);
   const T* cuts = static_cast<const T*>(a.cuts);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  VBT(1);
   VbFn<T> f;
   f.tl = cuts[0];
   f.sc = vbin_scale(cuts[0], cuts[1]);
   f.b = s_b;
+  vb_bounds<T>(f.tl, cuts[1], f.sc, s_b, f.lo, f.hi);
   f.comp = s_cb <= (unsigned)kVbCap;
   f.cnt = &a.st[1];
   f.zb = static_cast<T*>(a.zb);
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // one warp per run, 8 vectors per lane in flight (a run of the ~1% copy is a few thousand
   // elements: ~3 dependent L2 round trips instead of one per 4-vector group)
   using V = typename VecOf<T>::V;
@@ -1970,23 +2034,28 @@ __global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_const
     if ((uint64_t)lane < head) f.elem(p[lane], 0, 0);
     if ((uint64_t)lane < c - tail0) f.elem(p[tail0 + lane], 0, 0);
     const V* xv = reinterpret_cast<const V*>(p + head);
-    for (uint64_t v0 = 0; v0 < nvec; v0 += 32 * U) {
+    const uint64_t nfull = nvec / (32 * U) * (32 * U);
+    for (uint64_t v0 = 0; v0 < nfull; v0 += 32 * U) {  // full batches: no bounds tests
       V buf[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const uint64_t i = v0 + (uint64_t)u * 32 + lane;
-        if (i < nvec) buf[u] = ld_stream(xv + i);
-      }
+      for (int u = 0; u < U; ++u) buf[u] = ld_stream(xv + v0 + (uint64_t)u * 32 + lane);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const uint64_t i = v0 + (uint64_t)u * 32 + lane;
-        if (i < nvec) {
+        T vv[VE];
 #pragma unroll
-          for (int j = 0; j < VE; ++j) f.elem(lane_of(buf[u], j), 0, 0);
-        }
+        for (int j = 0; j < VE; ++j) vv[j] = lane_of(buf[u], j);
+        f.vec(vv);
       }
     }
+    for (uint64_t i = nfull + lane; i < nvec; i += 32) {
+      const V b = ld_stream(xv + i);
+      T vv[VE];
+#pragma unroll
+      for (int j = 0; j < VE; ++j) vv[j] = lane_of(b, j);
+      f.vec(vv);
+    }
   }
+  VBT(2);
   unsigned long long kmn = f.kmin, kmx = f.kmax;
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -2010,6 +2079,7 @@ __global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_const
   }
   __syncthreads();
   if (!s_last) return;
+  VBT(3);
   __threadfence();
   const unsigned long long gmin = ~__ldcg(&a.st[2]), gmax = __ldcg(&a.st[3]);
   const unsigned c = s_cb;
@@ -2023,6 +2093,10 @@ __global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_const
       __shared__ unsigned hist[2048];
       const T* zb = static_cast<const T*>(a.zb);
       for (unsigned i = threadIdx.x; i < c; i += 1024) vb_keys[i] = okey(__ldcg(&zb[i]));
+#ifdef CPSEL_VB_PROF
+      __syncthreads();
+      VBT(5);
+#endif
       const int hb = 63 - __clzll(gmin ^ gmax);
       unsigned long long mask = hb >= 63 ? 0ull : ~((2ull << hb) - 1ull);
       unsigned long long prefix = gmin & mask;
@@ -2050,6 +2124,18 @@ __global__ void __launch_bounds__(1024, 1) vbin_finish_kernel(const __grid_const
       fb = true;  // a large bin of several values: the host runs the key-digit radix select
     }
   }
+#ifdef CPSEL_VB_PROF
+  __syncthreads();
+  VBT(4);
+  if (threadIdx.x == 0) {
+    __threadfence();
+    printf("vbprof c=%u start 0..%llu  bounds %llu..%llu  scanned %llu..%llu  last %llu  loaded %llu  end %llu (ns)\n", c,
+           g_vbprof[1] - g_vbprof[0], g_vbprof[2] - g_vbprof[0], g_vbprof[3] - g_vbprof[0],
+           g_vbprof[4] - g_vbprof[0], g_vbprof[5] - g_vbprof[0], g_vbprof[7] - g_vbprof[0], g_vbprof[11] - g_vbprof[0],
+           g_vbprof[9] - g_vbprof[0]);
+    for (int q = 0; q < 16; q += 2) { g_vbprof[q] = ~0ull; g_vbprof[q + 1] = 0ull; }
+  }
+#endif
   if (threadIdx.x == 0) {
     *a.fallback = fb ? 1ull : 0ull;
     if (!fb) *a.vout = sizeof(T) == 4 ? from_key_f32(key) : from_key_f64(key);
@@ -3922,6 +4008,18 @@ cudaError_t launch_seg_pass(int dtype, const SegArgs& a, bool inside, const Laun
 // them into CTA 0's through DSMEM atomics; CTA 0 picks the digits and the others read the new
 // prefixes back from it.  Replaces the global round trip of the keys and one launch, and spreads
 // the sorting / histogram work over 8 SMs.
+#ifdef CPSEL_VB_PROF
+__device__ unsigned long long g_scprof[16];
+#define SCT(i)                                                                  \
+  if (threadIdx.x == 0) {                                                       \
+    unsigned long long t_;                                                      \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                     \
+    atomicMin(&g_scprof[2 * (i)], t_ | 0ull);                                   \
+    atomicMax(&g_scprof[2 * (i) + 1], t_);                                      \
+  }
+#else
+#define SCT(i)
+#endif
 constexpr int kSampleCluster = 8;
 struct ClusterSel {
   unsigned loc[3][2048];   // this CTA's histograms
@@ -3941,6 +4039,7 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
   using K = typename SK::K;
   pdl_wait();
   pdl_trigger();  // the init pass may be scheduled (it waits for the cuts)
+  SCT(0);
   extern __shared__ __align__(16) unsigned char csm[];
   ClusterSel& sh = *reinterpret_cast<ClusterSel*>(csm);
   unsigned long long* pre = reinterpret_cast<unsigned long long*>(csm + sizeof(ClusterSel));  // run-table prefix
@@ -4025,6 +4124,7 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
       }
     }
   }
+  SCT(1);
   if (crank == 0 && i == 0) {
     // m_rank: the population the sample stands for (the pooled sample of G ranks, R28: m samples
     // of m_rank elements in all); 0 = m
@@ -4152,8 +4252,10 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
       }
     }
     __syncthreads();  // CTA 0: the digit search is done before the next round clears its histograms
+    SCT(2 + rd);
   }
   cl.sync();
+  SCT(7);
   if (crank == 0 && i < 3) {
     K kk = (K)sh.prefix[i];
     if (i == 1) kk |= (K)~(K)sh.mask[1];
@@ -4162,6 +4264,14 @@ __global__ void __cluster_dims__(kSampleCluster, 1, 1) __launch_bounds__(1024)
     if (i == 1 && sh.open_hi) kk = SK::KHI;
     t0[i] = SK::val(kk);
   }
+#ifdef CPSEL_VB_PROF
+  if (crank == 0 && i == 0) {
+    printf("scprof start 0..%llu keys %llu..%llu r0 %llu..%llu r1 %llu..%llu end %llu..%llu\n", g_scprof[1] - g_scprof[0],
+           g_scprof[2] - g_scprof[0], g_scprof[3] - g_scprof[0], g_scprof[4] - g_scprof[0], g_scprof[5] - g_scprof[0],
+           g_scprof[6] - g_scprof[0], g_scprof[7] - g_scprof[0], g_scprof[14] - g_scprof[0], g_scprof[15] - g_scprof[0]);
+    for (int q = 0; q < 16; q += 2) { g_scprof[q] = ~0ull; g_scprof[q + 1] = 0ull; }
+  }
+#endif
 }
 
 // §8f-3 for small arrays (BASELINE configs[0], n = 1e5): the WHOLE selection as one launch.  The
@@ -4470,6 +4580,202 @@ cudaError_t launch_pool_gather(int dtype, const void* x, uint64_t m, const SegEn
     pool_gather_kernel<double><<<grid, kGatherThreads, 0, st>>>(static_cast<const double*>(x), m, tab, side, Wtot, ms,
                                                                 static_cast<double*>(out));
   return cudaGetLastError();
+}
+
+// R40: the one-GPU sample cuts as ONE cooperative grid kernel (replacing pool_gather + the 8-CTA
+// cluster select of the same sample): S / 1024 CTAs of 1024 threads, one strided sample per thread
+// (the gather's positions), so each CTA histograms ~1024 keys per round (not 16384 as in the
+// cluster, where the shared-memory atomics of the first round dominated); the per-CTA histograms
+// are added into a global one (scratch, zero on entry and left zero), one grid barrier per digit
+// round, and every CTA then picks the next digits of the three sample ranks from the global counts
+// itself (the same deterministic scan everywhere: no broadcast).  Same ranks, digits and cut
+// values as sample_cluster_kernel (R23, R29).
+constexpr int kSgMaxRounds = 4;
+constexpr size_t kSgHalf = (size_t)kSgMaxRounds * 3 * 2048 + 32;  // counts + [the barrier counter]
+constexpr size_t kSampleGridWords = 2 * kSgHalf + 32;                 // two halves + [the phase]
+template <typename T>
+__global__ void __launch_bounds__(1024, 1)
+    sample_grid_kernel(const T* __restrict__ x, uint64_t m, uint64_t ms, uint64_t m_rank, uint64_t r, T* t0,
+                       unsigned* __restrict__ scratch, int allow_open) {
+  using SK = SampleKey<T>;
+  using K = typename SK::K;
+  __shared__ unsigned loc[3][2048];
+  __shared__ unsigned wsum3[3][32];
+  __shared__ unsigned s_d3[3];
+  __shared__ unsigned long long s_b3[3];
+  __shared__ unsigned long long prefix[3], mask[3], rank[3];
+  __shared__ int open_lo, open_hi;
+  // two halves used alternately: this launch counts in half ph and clears the other (the previous
+  // launch's, complete in stream order) for the next, so nothing waits for a last CTA to clean up
+  const unsigned ph = __ldcg(scratch + 2 * kSgHalf) & 1u;
+  unsigned* const H = scratch + ph * kSgHalf;
+  unsigned* const bar = H + (size_t)kSgMaxRounds * 3 * 2048;
+  pdl_trigger();  // the init pass may be scheduled (it waits for the cuts)
+  SCT(0);
+  const int i = threadIdx.x;
+  {
+    unsigned* const O = scratch + (ph ^ 1u) * kSgHalf;
+    for (size_t b = (size_t)blockIdx.x * 1024 + i; b < kSgHalf; b += (size_t)gridDim.x * 1024) O[b] = 0u;
+  }
+  const uint64_t smp = (uint64_t)blockIdx.x * 1024 + i;
+  bool have = smp < ms;
+  K key = 0;
+  if (have) {
+    const uint64_t g = (m == ms) ? smp : (smp * m) / ms + (m / ms) / 2;
+    key = SK::key(x[g]);
+  }
+  if (i == 0) {
+    const double md = (double)ms;
+    const double q = ((double)r - 0.5) / (double)(m_rank ? m_rank : m) * md;
+    const double w = 3.5 * sqrt(fmax(q * (md - q) / md, 0.0)) + 2.0;
+    const double qq[3] = {floor(q - w), ceil(q + w), floor(q)};
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      rank[t] = qq[t] < 0 ? 0 : (qq[t] >= md ? ms - 1 : (uint64_t)qq[t]);
+      prefix[t] = 0;
+      mask[t] = 0;
+    }
+    open_lo = allow_open && qq[0] < 0;
+    open_hi = allow_open && qq[1] >= md - 1;
+  }
+  for (int b = i; b < 3 * 2048; b += 1024) (&loc[0][0])[b] = 0u;
+  __syncthreads();
+  SCT(1);
+  for (int rd = 0; rd < SK::ROUNDS; ++rd) {
+    const int shift = SK::shift(rd), nb = 1 << SK::bits(rd);
+    // the distinct classes of the three targets: src[t] = the first target with t's class
+    int src[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      src[t] = t;
+      for (int u = t - 1; u >= 0; --u)
+        if (prefix[u] == prefix[t] && mask[u] == mask[t]) src[t] = u;
+    }
+    unsigned* G = H + (size_t)rd * 3 * 2048;
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (src[t] != t) continue;
+      if (have && (key & (K)mask[t]) == (K)prefix[t]) atomicAdd(&loc[t][(unsigned)(key >> shift) & (unsigned)(nb - 1)], 1u);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (src[t] != t) continue;
+      for (int b = i; b < nb; b += 1024) {
+        const unsigned v = loc[t][b];
+        if (v) {
+          atomicAdd(&G[t * 2048 + b], v);
+          loc[t][b] = 0u;
+        }
+      }
+    }
+    SCT(2 + 2 * (rd & 1));
+    // grid barrier rd + 1 on a counter that only grows within the launch (one release-add per CTA,
+    // acquire polls until every CTA has arrived; the last CTA out resets it)
+    __syncthreads();
+    if (i == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+      const unsigned target = (unsigned)(rd + 1) * gridDim.x;
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      } while (v < target);
+    }
+    __syncthreads();
+    SCT(3 + 2 * (rd & 1));
+    // the digit of every target: each thread loads two bins of every distinct class at once (one
+    // L2 round trip, not three), one block scan per class, then each target's range test
+    const int lane = i & 31, w = i >> 5, bi = 2 * i;
+    unsigned h0[3], h1[3], incl[3];
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      h0[t] = h1[t] = 0u;
+      if (src[t] == t && bi < nb) {
+        h0[t] = __ldcg(&G[t * 2048 + bi]);
+        h1[t] = __ldcg(&G[t * 2048 + bi + 1]);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      incl[t] = h0[t] + h1[t];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, incl[t], o);
+        if (lane >= o) incl[t] += y;
+      }
+      if (lane == 31) wsum3[t][w] = incl[t];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      const int c = src[t];  // the class whose counts target t reads (c <= t)
+      unsigned long long ws = wsum3[c][lane], wi = ws;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long y = __shfl_up_sync(FULL, wi, o);
+        if (lane >= o) wi += y;
+      }
+      const unsigned a0 = c == 0 ? h0[0] : (c == 1 ? h0[1] : h0[2]);
+      const unsigned a1 = c == 0 ? h1[0] : (c == 1 ? h1[1] : h1[2]);
+      const unsigned ic = c == 0 ? incl[0] : (c == 1 ? incl[1] : incl[2]);
+      const unsigned long long before = __shfl_sync(FULL, wi - ws, w) + ic - (a0 + a1);
+      const unsigned long long rk = rank[t] + 1;  // 1-based
+      if (before < rk && rk <= before + a0) {
+        s_d3[t] = (unsigned)bi;
+        s_b3[t] = before;
+      } else if (before + a0 < rk && rk <= before + a0 + a1) {
+        s_d3[t] = (unsigned)bi + 1u;
+        s_b3[t] = before + a0;
+      }
+    }
+    __syncthreads();
+    if (i < 3) {
+      prefix[i] |= (unsigned long long)s_d3[i] << shift;
+      mask[i] |= (unsigned long long)(nb - 1) << shift;
+      rank[i] -= s_b3[i];
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && i < 3) {
+    K kk = (K)prefix[i];
+    if (i == 1) kk |= (K)~(K)mask[1];
+    kk = kk < SK::KLO ? SK::KLO : (kk > SK::KHI ? SK::KHI : kk);
+    if (i == 0 && open_lo) kk = SK::KLO;
+    if (i == 1 && open_hi) kk = SK::KHI;
+    t0[i] = SK::val(kk);
+  }
+#ifdef CPSEL_VB_PROF
+  SCT(6);
+  if (blockIdx.x == 0 && i == 0) {
+    printf("sgprof start 0..%llu keys %llu..%llu r0 %llu..%llu bar0 %llu..%llu r1 %llu..%llu bar1 %llu..%llu end0 %llu\n",
+           g_scprof[1] - g_scprof[0], g_scprof[2] - g_scprof[0], g_scprof[3] - g_scprof[0], g_scprof[4] - g_scprof[0],
+           g_scprof[5] - g_scprof[0], g_scprof[6] - g_scprof[0], g_scprof[7] - g_scprof[0], g_scprof[8] - g_scprof[0],
+           g_scprof[9] - g_scprof[0], g_scprof[10] - g_scprof[0], g_scprof[11] - g_scprof[0], g_scprof[13] - g_scprof[0]);
+    for (int q = 0; q < 16; q += 2) { g_scprof[q] = ~0ull; g_scprof[q + 1] = 0ull; }
+  }
+#endif
+  // every CTA read the phase before the first barrier, and CTA 0 is past the last one
+  if (blockIdx.x == 0 && i == 0) scratch[2 * kSgHalf] = ph ^ 1u;
+}
+size_t sample_grid_words() { return kSampleGridWords; }
+cudaError_t launch_sample_grid(int dtype, const void* x, uint64_t m, uint64_t ms, uint64_t m_rank, uint64_t r,
+                               void* t0, unsigned* scratch, cudaStream_t st, bool allow_open) {
+  if (ms == 0 || ms > m || ms % 1024 || ms / 1024 > 148) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(ms / 1024));
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int op = allow_open ? 1 : 0;
+  if (dtype == kF32)
+    return cudaLaunchKernelEx(&cfg, sample_grid_kernel<float>, static_cast<const float*>(x), m, ms, m_rank, r,
+                              static_cast<float*>(t0), scratch, op);
+  return cudaLaunchKernelEx(&cfg, sample_grid_kernel<double>, static_cast<const double*>(x), m, ms, m_rank, r,
+                            static_cast<double*>(t0), scratch, op);
 }
 
 uint64_t pool_sample_size(int dtype, bool small) {

@@ -277,6 +277,13 @@ cudaError_t launch_cut_pass(int dtype, const SegArgs& a, const LaunchShape& s, c
 // estimate (the one-GPU cluster select, with the rank scaled by m_rank instead of the sample size).
 // launch_seg_pack: the runs `side` of a segmented array packed contiguously into out (run order).
 uint64_t pool_sample_size(int dtype, bool small);
+// R40: the one-GPU sample cuts in one cooperative launch (ms / 1024 <= 148 CTAs; ms % 1024 == 0):
+// the ms strided samples of x[0..m) (launch_pool_gather's positions) and the three sample ranks of
+// launch_pool_pick, written to t0[0..2] — the same values as gather + pick.  scratch:
+// sample_grid_words() words, zero on entry, left zero.
+size_t sample_grid_words();
+cudaError_t launch_sample_grid(int dtype, const void* x, uint64_t m, uint64_t ms, uint64_t m_rank, uint64_t r,
+                               void* t0, unsigned* scratch, cudaStream_t st, bool allow_open);
 cudaError_t launch_pool_gather(int dtype, const void* x, uint64_t m, const SegEntry* tab, int side, int Wtot,
                                uint64_t ms, void* out, cudaStream_t st);
 cudaError_t launch_pool_pick(int dtype, const void* pooled, uint64_t ms, uint64_t m_rank, uint64_t r, void* t0,
