@@ -465,6 +465,15 @@ struct GpuBackend : Backend {
     static const bool on = !(getenv("CPSEL_SAMPLE_GRID") && getenv("CPSEL_SAMPLE_GRID")[0] == '0');
     return on;
   }
+  // R40: the grid kernel's sample, as a multiple of the cluster's (f32 131072, f64 65536 values):
+  // 4 by default — the cuts' rank window narrows by 2 (1/sqrt(S)), so the init copies ~0.5% of x
+  // instead of ~1% and the finish reads half as much; measured at 2^30 f32: 700 -> 672 us per
+  // median (the init 35 us faster, the sample kernel 10 us slower).  CPSEL_SAMPLE_X=1: the
+  // cluster's sample size
+  uint64_t sample_grid_x() const {
+    static const uint64_t x = (getenv("CPSEL_SAMPLE_X") && getenv("CPSEL_SAMPLE_X")[0] == '1') ? 1 : 4;
+    return x;
+  }
   bool vbin_on() const {
     static const bool on = !(getenv("CPSEL_VBIN") && getenv("CPSEL_VBIN")[0] == '0');
     return on;
@@ -573,7 +582,9 @@ struct GpuBackend : Backend {
     init_seg_done = false;
     CK(tic());
     sample_slot = -1;
+    int sample_launches = 0;
     if (cut && !presampled) {
+      sample_launches = 1;
       const bool small = n <= (1ull << 26);
       const uint64_t S = pool_sample_size(dt, small);
       if (n > 4 * S) {
@@ -582,11 +593,13 @@ struct GpuBackend : Backend {
         // contiguously from L2 — the same sample and the same cuts as the one-launch form
         if (sample_grid_on()) {
           // R40: the same sample and cuts in one cooperative launch (d_pool1 as its zeroed scratch)
-          CK(launch_sample_grid(dt, x, n, S, n, k, ctx->d_t0, static_cast<unsigned*>(ctx->d_pool1), ctx->stream,
-                                !ctx->cfg.objective));
+          const uint64_t Sg = small ? S : S * sample_grid_x();
+          CK(launch_sample_grid(dt, x, n, n > 4 * Sg ? Sg : S, n, k, ctx->d_t0, static_cast<unsigned*>(ctx->d_pool1),
+                                ctx->stream, !ctx->cfg.objective));
         } else {
           CK(launch_pool_gather(dt, x, n, nullptr, 0, 0, S, ctx->d_pool1, ctx->stream));
           CK(launch_pool_pick(dt, ctx->d_pool1, S, n, k, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
+          sample_launches = 2;
         }
       } else {
         CK(launch_sample_select(dt, x, n, nullptr, 0, 0, k, ctx->d_t0, ctx->d_skeys, ctx->stream, small, nullptr, 0,
@@ -632,7 +645,7 @@ struct GpuBackend : Backend {
     const int init_slot_ = slot;
     if (chain) CK(direct ? launch_chain_direct() : launch_chain(k));
     slot = init_slot_;
-    launches = cut ? 2 : 1;
+    launches = 1 + sample_launches;  // the init and the sample kernels before it
     scanned = n;
     if (use_mail) {
       cpsel_status w = wait_mail(&ctx->mb->seq_init, a.seq);

@@ -4593,7 +4593,7 @@ cudaError_t launch_pool_gather(int dtype, const void* x, uint64_t m, const SegEn
 constexpr int kSgMaxRounds = 4;
 constexpr size_t kSgHalf = (size_t)kSgMaxRounds * 3 * 2048 + 32;  // counts + [the barrier counter]
 constexpr size_t kSampleGridWords = 2 * kSgHalf + 32;                 // two halves + [the phase]
-template <typename T>
+template <typename T, int KPT>
 __global__ void __launch_bounds__(1024, 1)
     sample_grid_kernel(const T* __restrict__ x, uint64_t m, uint64_t ms, uint64_t m_rank, uint64_t r, T* t0,
                        unsigned* __restrict__ scratch, int allow_open) {
@@ -4617,12 +4617,17 @@ __global__ void __launch_bounds__(1024, 1)
     unsigned* const O = scratch + (ph ^ 1u) * kSgHalf;
     for (size_t b = (size_t)blockIdx.x * 1024 + i; b < kSgHalf; b += (size_t)gridDim.x * 1024) O[b] = 0u;
   }
-  const uint64_t smp = (uint64_t)blockIdx.x * 1024 + i;
-  bool have = smp < ms;
-  K key = 0;
-  if (have) {
-    const uint64_t g = (m == ms) ? smp : (smp * m) / ms + (m / ms) / 2;
-    key = SK::key(x[g]);
+  bool have[KPT];
+  K key[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const uint64_t smp = ((uint64_t)j * gridDim.x + blockIdx.x) * 1024 + i;
+    have[j] = smp < ms;
+    key[j] = 0;
+    if (have[j]) {
+      const uint64_t g = (m == ms) ? smp : (smp * m) / ms + (m / ms) / 2;
+      key[j] = SK::key(x[g]);
+    }
   }
   if (i == 0) {
     const double md = (double)ms;
@@ -4655,7 +4660,10 @@ __global__ void __launch_bounds__(1024, 1)
 #pragma unroll
     for (int t = 0; t < 3; ++t) {
       if (src[t] != t) continue;
-      if (have && (key & (K)mask[t]) == (K)prefix[t]) atomicAdd(&loc[t][(unsigned)(key >> shift) & (unsigned)(nb - 1)], 1u);
+#pragma unroll
+      for (int j = 0; j < KPT; ++j)
+        if (have[j] && (key[j] & (K)mask[t]) == (K)prefix[t])
+          atomicAdd(&loc[t][(unsigned)(key[j] >> shift) & (unsigned)(nb - 1)], 1u);
     }
     __syncthreads();
 #pragma unroll
@@ -4760,9 +4768,11 @@ __global__ void __launch_bounds__(1024, 1)
 size_t sample_grid_words() { return kSampleGridWords; }
 cudaError_t launch_sample_grid(int dtype, const void* x, uint64_t m, uint64_t ms, uint64_t m_rank, uint64_t r,
                                void* t0, unsigned* scratch, cudaStream_t st, bool allow_open) {
-  if (ms == 0 || ms > m || ms % 1024 || ms / 1024 > 148) return cudaErrorInvalidValue;
+  // one key per thread up to 128 CTAs, else 4 (<= 128 x 4096 samples)
+  const int kpt = ms > 128 * 1024 ? 4 : 1;
+  if (ms == 0 || ms > m || ms % (1024 * kpt) || ms / (1024 * kpt) > 128) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(ms / 1024));
+  cfg.gridDim = dim3((unsigned)(ms / (1024 * kpt)));
   cfg.blockDim = dim3(1024);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -4771,11 +4781,16 @@ cudaError_t launch_sample_grid(int dtype, const void* x, uint64_t m, uint64_t ms
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   const int op = allow_open ? 1 : 0;
-  if (dtype == kF32)
-    return cudaLaunchKernelEx(&cfg, sample_grid_kernel<float>, static_cast<const float*>(x), m, ms, m_rank, r,
-                              static_cast<float*>(t0), scratch, op);
-  return cudaLaunchKernelEx(&cfg, sample_grid_kernel<double>, static_cast<const double*>(x), m, ms, m_rank, r,
-                            static_cast<double*>(t0), scratch, op);
+  if (dtype == kF32) {
+    void (*f)(const float*, uint64_t, uint64_t, uint64_t, uint64_t, float*, unsigned*, int) =
+        kpt == 4 ? sample_grid_kernel<float, 4> : sample_grid_kernel<float, 1>;
+    return cudaLaunchKernelEx(&cfg, f, static_cast<const float*>(x), m, ms, m_rank, r, static_cast<float*>(t0), scratch,
+                              op);
+  }
+  void (*f)(const double*, uint64_t, uint64_t, uint64_t, uint64_t, double*, unsigned*, int) =
+      kpt == 4 ? sample_grid_kernel<double, 4> : sample_grid_kernel<double, 1>;
+  return cudaLaunchKernelEx(&cfg, f, static_cast<const double*>(x), m, ms, m_rank, r, static_cast<double*>(t0), scratch,
+                            op);
 }
 
 uint64_t pool_sample_size(int dtype, bool small) {

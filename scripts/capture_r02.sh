@@ -8,7 +8,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
   --csv --log-file $out/r02_launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-lms --no-side \
   > $out/r02_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"init_seg|sample_cluster|pool_gather|radix_coop|vbin" -c 8 \
+  -k regex:"init_seg|sample_grid|sample_cluster|pool_gather|radix_coop|vbin" -c 8 \
   -o $out/r02_full python scripts/prof_kernels.py select > $out/r02_full.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"seg_pass|pass_kernel" -c 4 \
   -o $out/r02_kelley python scripts/time_kelley.py 30 uniform --reps 1 > $out/r02_kelley_ncu.log 2>&1

@@ -442,13 +442,14 @@ def test_sharded_world1_nccl(cp):
 
 def test_direct_chain_declined_then_reused(cp):
     """Direct device chain (n >= 2^27): when the init's sample cuts miss the target (here: x is huge
-    exactly at the 131072 strided sample positions, so both cuts lie far above the median) the
+    exactly at the strided sample positions, so both cuts lie far above the median) the
     chained radix rounds must stand down — clearing the round-0 digit counts the init pass took —
     and the host continues with Kelley passes; the next selection through the chain is exact."""
     n = 1 << 27
     xd = datagen.make("normal", n, "f32", device="cuda")
-    ms = 131072                                     # the f32 init sample (8-CTA cluster x 1024 x 16)
-    pos = np.arange(ms, dtype=np.int64) * (n // ms) + (n // ms) // 2
+    # the f32 init sample: 131072 strided values (the cluster's size, CPSEL_SAMPLE_X=1) or 4x that
+    # (the grid kernel's default, R40) — both sets of positions poisoned
+    pos = np.concatenate([np.arange(ms, dtype=np.int64) * (n // ms) + (n // ms) // 2 for ms in (131072, 524288)])
     import torch
     xd[torch.from_numpy(pos).cuda()] = 1e30
     k = O.median_rank(n)
