@@ -466,13 +466,18 @@ struct GpuBackend : Backend {
     return on;
   }
   // R40: the grid kernel's sample, as a multiple of the cluster's (f32 131072, f64 65536 values):
-  // 4 by default — the cuts' rank window narrows by 2 (1/sqrt(S)), so the init copies ~0.5% of x
-  // instead of ~1% and the finish reads half as much; measured at 2^30 f32: 700 -> 672 us per
-  // median (the init 35 us faster, the sample kernel 10 us slower).  CPSEL_SAMPLE_X=1: the
-  // cluster's sample size
+  // f32 4x (524288) — the cuts' rank window narrows by 2 (1/sqrt(S)), so the init copies ~0.5% of
+  // x instead of ~1% and the finish reads half as much; measured at 2^30 f32: 700 -> 672 us per
+  // median (the init 35 us faster, the sample kernel 10 us slower; 8x and 16x: slower again, the
+  // sample's scattered loads cost more than the smaller copy saves); f64 8x (524288 values too):
+  // 2^28 f64 medians 429 -> 422 us against 4x.  CPSEL_SAMPLE_X=1|4|8|16 overrides both
   uint64_t sample_grid_x() const {
-    static const uint64_t x = (getenv("CPSEL_SAMPLE_X") && getenv("CPSEL_SAMPLE_X")[0] == '1') ? 1 : 4;
-    return x;
+    static const long env = [] {
+      const char* e = getenv("CPSEL_SAMPLE_X");
+      const long v = e ? atol(e) : 0;
+      return v == 1 || v == 4 || v == 8 || v == 16 ? v : 0L;
+    }();
+    return (uint64_t)(env ? env : (dt == kF32 ? 4 : 8));
   }
   bool vbin_on() const {
     static const bool on = !(getenv("CPSEL_VBIN") && getenv("CPSEL_VBIN")[0] == '0');

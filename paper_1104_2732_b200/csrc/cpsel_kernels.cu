@@ -4768,8 +4768,8 @@ __global__ void __launch_bounds__(1024, 1)
 size_t sample_grid_words() { return kSampleGridWords; }
 cudaError_t launch_sample_grid(int dtype, const void* x, uint64_t m, uint64_t ms, uint64_t m_rank, uint64_t r,
                                void* t0, unsigned* scratch, cudaStream_t st, bool allow_open) {
-  // one key per thread up to 128 CTAs, else 4 (<= 128 x 4096 samples)
-  const int kpt = ms > 128 * 1024 ? 4 : 1;
+  // one key per thread up to 128 CTAs, else 4, 8 or 16 (<= 128 x 16384 samples)
+  const int kpt = ms <= 128 * 1024 ? 1 : ms <= 4 * 128 * 1024 ? 4 : ms <= 8 * 128 * 1024 ? 8 : 16;
   if (ms == 0 || ms > m || ms % (1024 * kpt) || ms / (1024 * kpt) > 128) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(ms / (1024 * kpt)));
@@ -4783,12 +4783,16 @@ cudaError_t launch_sample_grid(int dtype, const void* x, uint64_t m, uint64_t ms
   const int op = allow_open ? 1 : 0;
   if (dtype == kF32) {
     void (*f)(const float*, uint64_t, uint64_t, uint64_t, uint64_t, float*, unsigned*, int) =
-        kpt == 4 ? sample_grid_kernel<float, 4> : sample_grid_kernel<float, 1>;
+        kpt == 16 ? sample_grid_kernel<float, 16>
+                  : kpt == 8 ? sample_grid_kernel<float, 8>
+                             : kpt == 4 ? sample_grid_kernel<float, 4> : sample_grid_kernel<float, 1>;
     return cudaLaunchKernelEx(&cfg, f, static_cast<const float*>(x), m, ms, m_rank, r, static_cast<float*>(t0), scratch,
                               op);
   }
   void (*f)(const double*, uint64_t, uint64_t, uint64_t, uint64_t, double*, unsigned*, int) =
-      kpt == 4 ? sample_grid_kernel<double, 4> : sample_grid_kernel<double, 1>;
+      kpt == 16 ? sample_grid_kernel<double, 16>
+                : kpt == 8 ? sample_grid_kernel<double, 8>
+                           : kpt == 4 ? sample_grid_kernel<double, 4> : sample_grid_kernel<double, 1>;
   return cudaLaunchKernelEx(&cfg, f, static_cast<const double*>(x), m, ms, m_rank, r, static_cast<double*>(t0), scratch,
                             op);
 }
