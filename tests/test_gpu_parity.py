@@ -599,3 +599,53 @@ def test_value_binned_finish_paths(cp, dtype):
     km = O.median_rank(n)
     # the cluster's bin overflows: the key-digit radix select runs after the finish (more launches)
     assert launches[("dense_cluster", km)] > launches[("smooth", km)] == launches[("one_value", km)], launches
+
+
+_SAMPLE_PROBE = r"""
+import json, sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import datagen
+import oracle as O
+import paper_1104_2732_b200 as cp
+out = {}
+for dtype, lg in (("f32", 27), ("f64", 27)):
+    x = datagen.make("normal", (1 << lg) + 5, dtype)
+    xd = torch.from_numpy(x).cuda()
+    k = O.median_rank(x.size)
+    v, info = cp.select_kth(xd, k, return_info=True)
+    out[dtype] = {"v": float(v), "want": float(O.order_statistic(x, k)), "written": int(info["init_written"]),
+                  "launches": int(info["launches"]), "exit": info["exit"]}
+print(json.dumps(out))
+"""
+
+
+def _probe(env):
+    import json
+    import os
+    import subprocess
+    import sys
+    e = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, "-c", _SAMPLE_PROBE], env=e, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stderr[-2000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_sample_grid_kernel_cuts():
+    """R40: the one-GPU sample cuts from the cooperative grid kernel.  At the cluster's sample size
+    (CPSEL_SAMPLE_X=1) its cuts are the cluster kernel's (R29: the same strided sample, the same
+    three sample ranks, the same digits), so the init copies exactly as many elements; at the default
+    524288 samples the rank window shrinks by sqrt(S'/S) (3.5 sigma of the larger sample), so the copy
+    does too — and every selection stays exact (each call's value against the oracle)."""
+    old = _probe({"CPSEL_SAMPLE_GRID": "0"})
+    grid1 = _probe({"CPSEL_SAMPLE_GRID": "1", "CPSEL_SAMPLE_X": "1"})
+    dflt = _probe({})
+    for dtype, shrink in (("f32", 2.0), ("f64", 8 ** 0.5)):
+        for r in (old[dtype], grid1[dtype], dflt[dtype]):
+            assert r["v"] == r["want"], r
+        assert grid1[dtype]["written"] == old[dtype]["written"], (old, grid1)
+        assert old[dtype]["launches"] == grid1[dtype]["launches"] + 1, (old, grid1)  # gather + pick -> one
+        ratio = dflt[dtype]["written"] / old[dtype]["written"]
+        assert 0.7 / shrink < ratio < 1.3 / shrink, (dtype, ratio, old, dflt)
