@@ -1254,7 +1254,12 @@ struct ShardedBackend : GpuBackend {
     uint64_t M = 0;
     for (uint64_t v : m_rank) M += v;
     const bool small = M <= (1ull << 26) && !on_x;
-    const uint64_t S = pool_sample_size(dt, small);
+    // R40 for the init's cuts: the grid kernel's larger pooled sample (same apportioning).  Not for
+    // loopback ranks: they share one GPU and run at once, and a cooperative grid per virtual rank
+    // could spin on CTAs that cannot become resident while another rank's grid holds the SMs
+    const bool grid = on_x && !small && sample_grid_on() && !ctx->comm.loop &&
+                      M > 4 * pool_sample_size(dt, false) * sample_grid_x();
+    const uint64_t S = pool_sample_size(dt, small) * (grid ? sample_grid_x() : 1);
     std::vector<uint64_t> s(Gn, 0);
     if (M <= S) {
       s = m_rank;
@@ -1285,7 +1290,11 @@ struct ShardedBackend : GpuBackend {
     CK(launch_pool_gather(dt, on_x ? x : cur, on_x ? n : n_cur, seg ? cur_tab : nullptr, cur_side, W, s[comm().rank],
                           mine, ctx->stream));
     CM(comm().allgatherv(mine, ctx->d_pool, bytes.data(), ctx->stream));
-    CK(launch_pool_pick(dt, ctx->d_pool, total, M, r, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
+    if (grid)  // the pooled array is the sample itself (m = ms: every value, in order)
+      CK(launch_sample_grid(dt, ctx->d_pool, total, total, M, r, ctx->d_t0, static_cast<unsigned*>(ctx->d_pool1),
+                            ctx->stream, !ctx->cfg.objective));
+    else
+      CK(launch_pool_pick(dt, ctx->d_pool, total, M, r, ctx->d_t0, ctx->stream, small, !ctx->cfg.objective));
     return CPSEL_OK;
   }
   // the init pass: with cuts (R23/R28) every rank runs the fused init at the pooled cuts and the
@@ -2388,7 +2397,8 @@ static cpsel_status comm_buffers(cpsel_ctx* ctx, int world) {
   CK(cudaMalloc(&ctx->d_gather_init, world * sizeof(DevInit)));
   CK(cudaHostAlloc(&ctx->h_gather, world * sizeof(DevPass), cudaHostAllocDefault));
   CK(cudaHostAlloc(&ctx->h_gather_init, world * sizeof(DevInit), cudaHostAllocDefault));
-  CK(cudaMalloc(&ctx->d_pool, std::max(pool_sample_size(kF32, false) * 4, pool_sample_size(kF64, false) * 8)));
+  // the pooled sample: up to 16x the cluster's (R40's CPSEL_SAMPLE_X), f64
+  CK(cudaMalloc(&ctx->d_pool, pool_sample_size(kF64, false) * 16 * 8));
   CK(cudaMalloc(&ctx->d_sizes, (size_t)(world + 1) * sizeof(unsigned long long)));
   CK(cudaHostAlloc(&ctx->h_sizes, (size_t)(world + 1) * sizeof(unsigned long long), cudaHostAllocDefault));
   ctx->rec_bytes = (size_t)world * std::max(sizeof(DevPass), sizeof(DevInit));
