@@ -2619,20 +2619,38 @@ template <typename T, bool SUMS> struct InitSeg {
     }
     const int lane = threadIdx.x & 31;
     const unsigned cnt = (unsigned)__popc(bits);
-    unsigned incl = cnt;
+    const unsigned act = __ballot_sync(FULL, cnt != 0u);
+    if (act == 0u) return;
+    unsigned excl, tot;
+    if (__all_sync(FULL, cnt <= 1u)) {  // the usual case: at most one interior element per lane
+      unsigned lt;
+      asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+      excl = (unsigned)__popc(act & lt);
+      tot = (unsigned)__popc(act);
+    } else {
+      unsigned incl = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      excl = incl - cnt;
+      tot = __shfl_sync(FULL, incl, 31);
     }
-    const unsigned tot = __shfl_sync(FULL, incl, 31);
-    if (tot == 0u) return;
-    // predicated shared stores: lane l stages its interior elements at [excl_l, incl_l), then
-    // the warp writes the group's run out coalesced (the order inside a run is free)
-    T* sp = stage + (incl - cnt);
+    // predicated shared stores: lane l stages its interior elements at [excl_l, excl_l + cnt_l),
+    // then the warp writes the group's run out coalesced (the order inside a run is free); a
+    // vector slot no lane has an interior element in is skipped by the whole warp
+    T* sp = stage + excl;
+    constexpr int VU = G / kSegU;
 #pragma unroll
-    for (int j = 0; j < G; ++j)
-      if (bits & (1u << j)) *sp++ = vals[j];
+    for (int u = 0; u < kSegU; ++u) {
+      const unsigned mu = (bits >> (u * VU)) & ((1u << VU) - 1u);
+      if (__any_sync(FULL, mu != 0u)) {
+#pragma unroll
+        for (int q = 0; q < VU; ++q)
+          if (mu & (1u << q)) *sp++ = vals[u * VU + q];
+      }
+    }
     __syncwarp();
     T* dst = out + reg_lo + n_in;
     if (hist0 && vsc > T(0)) {  // the copy's first digit (direct chain): its value bin (vbin) ...
