@@ -650,3 +650,34 @@ def test_sample_grid_kernel_cuts():
         assert old[dtype]["launches"] == grid1[dtype]["launches"] + 1, (old, grid1)  # gather + pick -> one
         ratio = dflt[dtype]["written"] / old[dtype]["written"]
         assert 0.7 / shrink < ratio < 1.3 / shrink, (dtype, ratio, old, dflt)
+
+
+def test_concurrent_threads_own_contexts():
+    """Python threads each get their own ctx and stream (threading.local): four threads running the
+    default one-GPU path at once — the cooperative sample-grid kernel (R40), the fused init and the
+    chained finish of several selections in flight on one device — all return the oracle's values."""
+    import threading
+    import torch
+    import paper_1104_2732_b200 as cpm
+    n = (1 << 27) + 7                    # > 2^26: the 128-CTA sample grid, the direct chain
+    xs = [datagen.make(d, n, "f32") for d in ("uniform", "normal", "cauchy", "dup256")]
+    want = [float(O.median(x)) for x in xs]
+    xds = [tdev(x) for x in xs]
+    torch.cuda.synchronize()
+    got, errs = {}, []
+
+    def worker(i):
+        try:
+            torch.cuda.set_device(0)
+            vs = [cpm.median(xds[i]) for _ in range(6)]
+            got[i] = vs
+        except Exception as e:  # noqa: BLE001
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    [t.start() for t in th]
+    [t.join(120) for t in th]
+    assert not any(t.is_alive() for t in th), "a selection thread did not finish"
+    assert not errs, errs
+    for i in range(4):
+        assert all(canon(v) == want[i] for v in got[i]), (i, got[i], want[i])
