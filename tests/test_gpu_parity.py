@@ -602,6 +602,26 @@ def test_value_binned_finish_paths(cp, dtype):
     assert launches[("dense_cluster", km)] > launches[("smooth", km)] == launches[("one_value", km)], launches
 
 
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_value_binned_finish_infinite_span(cp, dtype):
+    """The value-binned finish when t_hi - t_lo overflows (R38's open span: the copy's first digit
+    is then the top 11 bits of the order-preserving key, and vb_bounds takes the values of that key
+    class, whose ends may be NaN keys).  Two modes of opposite sign near the largest finite value,
+    so the sample cuts around the median straddle the gap; also ranks inside either mode."""
+    import torch
+    n = (1 << 23) + 11
+    rng = np.random.default_rng(29)
+    big = float(np.finfo(np.float32 if dtype == "f32" else np.float64).max)
+    u = rng.random(n)
+    sign = np.where(rng.random(n) < 0.5, -1.0, 1.0)
+    x = (sign * big * (0.75 + 0.25 * u)).astype(np.float32 if dtype == "f32" else np.float64)  # span 1.5 big
+    xd = torch.from_numpy(x).cuda()
+    xs = np.sort(x)
+    for k in (O.median_rank(n), O.median_rank(n) + 5, n // 3, 2 * n // 3, 17, n - 17):
+        v, info = cp.select_kth(xd, k, return_info=True)
+        assert v == canon(float(xs[k - 1])), (k, v, float(xs[k - 1]), info)
+
+
 _SAMPLE_PROBE = r"""
 import json, sys
 import numpy as np
